@@ -1,0 +1,77 @@
+"""Host-side checks of the shared seeded generators (datagen/), -m "not gpu"."""
+import math
+
+import numpy as np
+
+import datagen
+
+
+def test_exp10_accuracy():
+    L = datagen.host_lib()
+    t = np.linspace(-300, 300, 20001)
+    v = np.array([L.gen_exp10_host(x) for x in t])
+    assert np.max(np.abs(v / 10.0 ** t - 1)) < 1e-13
+    assert L.gen_exp10_host(0.0) == 1.0
+
+
+def test_counter_based_fill_equals_sample_and_is_shardable():
+    for name in ("cfg1", "cfg2", "cfg5"):
+        w = datagen.workload(name, count=50_000)
+        full = w.targets.host_fill(0, w.count, w.table)
+        # any shard boundaries give the same stream
+        a = w.targets.host_fill(0, 17_001, w.table)
+        b = w.targets.host_fill(17_001, w.count - 17_001, w.table)
+        assert np.array_equal(np.concatenate([a, b]), full)
+        idx = np.random.default_rng(0).integers(0, w.count, 999)
+        assert np.array_equal(w.targets.host_sample(idx, w.table), full[idx])
+        assert np.array_equal(w.targets.host_fill(0, w.count, w.table), full)  # determinism
+
+
+def test_walk_fill_sample_and_offset():
+    w = datagen.workload("cfg3", count=100_000)
+    full = w.targets.host_fill(0, w.count)
+    assert np.array_equal(w.targets.host_fill(40_000, 60_000), full[40_000:])
+    idx = np.sort(np.random.default_rng(1).integers(0, w.count, 500))
+    assert np.array_equal(w.targets.host_sample(idx), full[idx])
+    lg = np.log10(full)
+    assert lg.min() >= -1e-12 and lg.max() <= 8 + 1e-12
+    step = np.abs(np.diff(lg))
+    # step sd 0.01 decades: median |N(0, s)| = 0.6745 s
+    assert abs(np.median(step) / 0.6745 - 0.01) < 0.001
+
+
+def test_cfg1_recipe_out_of_range_and_copies():
+    """BASELINE.json configs[0]: '~5% out of range' plus '1% exact copies'."""
+    w = datagen.workload("cfg1")
+    X = w.table
+    assert X.size == 64 and np.all(np.diff(X) > 0)
+    assert X[0] == 1e-4 and X[-1] == 1e4          # pinned endpoints
+    y = w.targets.host_fill(0, w.count, X)
+    oor = np.mean((y < X[0]) | (y > X[-1]))
+    assert 0.04 < oor < 0.056
+    assert 0.008 < np.mean(np.isin(y, X)) < 0.012
+    assert y[0] == X[0] and y[1] == X[-1]
+
+
+def test_paper_targets_half_out_of_range():
+    """'Approximately half of the values were outside of the bounds of the data
+    array' -- holds only for the log-uniform reading of P:224."""
+    w = datagen.workload("paper", count=200_000)
+    y = w.targets.host_fill(0, w.count)
+    X = w.table
+    frac_in = np.mean((y >= X[0]) & (y <= X[-1]))
+    assert 0.49 < frac_in < 0.54
+
+
+def test_table_recipes():
+    t2 = datagen.table_cfg2()
+    assert t2.size == 300 and np.all(np.diff(t2) > 0)
+    t3 = datagen.table_cfg3()
+    assert t3.size == 1000 and t3[0] == 1.0 and abs(t3[-1] / 1e8 - 1) < 1e-12
+    t5 = datagen.table_cfg5()
+    assert t5.size == 4096 and np.all(np.diff(t5) > 0)
+    assert abs(np.mean((t5 >= 1) & (t5 < 100)) - 0.70) < 0.01
+    rho, T, P = datagen.grid_cfg4()
+    assert P.shape == (200, 100) and np.all(P > 0)
+    ex = datagen.table_paper_exemplar()
+    assert ex.size == 110 and math.isclose(ex[0], 3e-6) and math.isclose(ex[-1], 5.4e4)

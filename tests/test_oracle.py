@@ -1,0 +1,251 @@
+"""Pins of the CPU oracle against things other than itself (-m "not gpu").
+
+Each test names what fixes the expected value: the paper's definition worked
+by hand (golden files), brute force on tiny inputs, a library routine
+(numpy / bisect / scipy), closed forms, or invariants.
+"""
+import bisect
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from tests._golden import interp_cases, lower_bound_cases
+
+SPECIALS = [0.0, -0.0, math.inf, -math.inf, math.nan, 5e-324, 2.2250738585072014e-308,
+            math.nextafter(2.2250738585072014e-308, 0.0), 1e-300, 1e300, -1.0, 1.0, 2.0, 0.5]
+
+
+def brute_force(X, y):
+    """Linear count straight from P:54: last element <= y, 0 if none."""
+    c = 0
+    for x in X:
+        if x <= y:
+            c += 1
+    return max(c - 1, 0)
+
+
+def probes_for(X):
+    p = list(SPECIALS)
+    for x in X:
+        p += [x, math.nextafter(x, math.inf), math.nextafter(x, -math.inf)]
+        if x > 0:
+            e = math.floor(math.log2(x))
+            p += [2.0 ** e, math.nextafter(2.0 ** e, 0.0), 2.0 ** (e + 1)]
+    for a, b in zip(X[:-1], X[1:]):
+        p.append(0.5 * (a + b))
+    return np.array(p, dtype=np.float64)
+
+
+# ---------------------------------------------------------------- golden ----
+@pytest.mark.parametrize("name", sorted(lower_bound_cases().keys()))
+def test_golden_lower_bound(name):
+    X, cases = lower_bound_cases()[name]
+    ys = np.array([c[0] for c in cases])
+    exp = np.array([c[1] for c in cases], dtype=np.int32)
+    got = oracle.search(X, ys)
+    assert got.tolist() == exp.tolist(), list(zip(ys.tolist(), got.tolist(), exp.tolist()))
+    for y, e in cases:
+        assert oracle.lower_bound(X, y) == e
+
+
+# ------------------------------------------------------------ brute force ---
+def _random_tables(rng, count):
+    for t in range(count):
+        n = int(rng.integers(1, 13))
+        kind = t % 6
+        if kind == 0:      # log-uniform
+            X = 10.0 ** rng.uniform(-8, 8, n)
+        elif kind == 1:    # exact powers of two
+            X = 2.0 ** rng.integers(-20, 20, n).astype(np.float64)
+        elif kind == 2:    # zero head + subnormals
+            X = np.concatenate([[0.0], rng.uniform(0, 1, n) * 1e-310, 10.0 ** rng.uniform(-5, 5, n)])
+        elif kind == 3:    # dense cluster with duplicates
+            X = np.round(rng.uniform(1.0, 1.01, n), 3)
+        elif kind == 4:    # mixed sign with zeros
+            X = np.concatenate([rng.normal(0, 10, n), [0.0, -0.0]])
+        else:              # heavy duplicates
+            X = rng.choice([1.0, 2.0, 3.0], n)
+        yield np.sort(X)
+
+
+def test_brute_force_exhaustive_tiny_tables():
+    rng = np.random.default_rng(12345)
+    total = 0
+    for X in _random_tables(rng, 600):
+        P = probes_for(X)
+        got = oracle.search(X, P, threads=1)
+        exp = [brute_force(X, y) for y in P]
+        assert got.tolist() == exp, X
+        total += P.size
+    assert total > 20000
+
+
+def test_every_probe_of_every_prefix_table():
+    """Exhaustive over all prefixes of a fixed table containing every hazard."""
+    base = [0.0, 5e-324, 1e-310, 2.2250738585072014e-308, 0.25, 0.5, 0.5, 1.0, 1.5, 2.0, 3.0,
+            3.0, 3.0, 8.0, 1e300]
+    for n in range(1, len(base) + 1):
+        X = np.array(base[:n])
+        P = probes_for(X)
+        assert oracle.search(X, P, threads=1).tolist() == [brute_force(X, y) for y in P]
+
+
+# --------------------------------------------------------- library routine --
+def test_numpy_searchsorted_and_bisect_nan_masked():
+    import datagen
+    w = datagen.workload("cfg1")
+    X = w.table
+    Y = w.targets.host_fill(0, w.count, X)
+    Y[::997] = np.nan
+    got = oracle.search(X, Y)
+    ref = np.clip(np.searchsorted(X, Y, side="right") - 1, 0, None)
+    nan = np.isnan(Y)
+    assert np.array_equal(got[~nan], ref[~nan])
+    assert np.all(got[nan] == 0)          # reading R4 (numpy would say n-1)
+    for y in Y[:2000]:
+        if not math.isnan(y):
+            assert oracle.lower_bound(X, y) == max(bisect.bisect_right(list(X), y) - 1, 0)
+
+
+def test_bracketing_invariant_all_outputs():
+    import datagen
+    for name in ("cfg1", "paper"):
+        w = datagen.workload(name, count=200_000)
+        X = w.table
+        Y = w.targets.host_fill(0, w.count, X)
+        idx = oracle.search(X, Y).astype(np.int64)
+        n = X.size
+        inr = Y >= X[0]
+        assert np.all(idx[~inr] == 0)
+        i = idx[inr]
+        y = Y[inr]
+        assert np.all(X[i] <= y)
+        assert np.all((i == n - 1) | (y < X[np.minimum(i + 1, n - 1)]))
+
+
+def test_permutation_invariance():
+    rng = np.random.default_rng(7)
+    X = np.sort(10.0 ** rng.uniform(-6, 3, 300))
+    Y = 10.0 ** rng.uniform(-7, 4, 50_000)
+    perm = rng.permutation(Y.size)
+    assert np.array_equal(oracle.search(X, Y)[perm], oracle.search(X, Y[perm]))
+
+
+def test_threads_do_not_change_result():
+    rng = np.random.default_rng(8)
+    X = np.sort(rng.uniform(0, 1, 1000))
+    Y = rng.uniform(-0.1, 1.1, 300_001)
+    assert np.array_equal(oracle.search(X, Y, threads=1), oracle.search(X, Y, threads=7))
+
+
+# ---------------------------------------------------------- interpolation ---
+def test_golden_interp2d():
+    R, T, G, cases = interp_cases()
+    rho = np.array([c[0] for c in cases])
+    t = np.array([c[1] for c in cases])
+    P, iR, iT = oracle.interp2d(R, T, G, rho, t)
+    for k, (r, tt, p, i, j) in enumerate(cases):
+        assert P[k] == p, (r, tt, P[k], p)
+        assert (iR[k], iT[k]) == (i, j)
+
+
+def _axes(rng, nr=37, nt=23):
+    R = np.sort(10.0 ** rng.uniform(-6, 3, nr))
+    T = np.sort(10.0 ** rng.uniform(0, 8, nt))
+    assert np.all(np.diff(R) > 0) and np.all(np.diff(T) > 0)
+    return R, T
+
+
+def test_interp_reproduces_bilinear_closed_form():
+    rng = np.random.default_rng(1)
+    R, T = _axes(rng)
+    a, b, c, d = 3.0, 0.7, 1.3e-4, 2.1e-7
+    G = a + b * R[:, None] + c * T[None, :] + d * R[:, None] * T[None, :]
+    rho = 10.0 ** rng.uniform(np.log10(R[0]), np.log10(R[-1]), 20000)
+    tt = 10.0 ** rng.uniform(np.log10(T[0]), np.log10(T[-1]), 20000)
+    rho = np.clip(rho, R[0], R[-1])
+    tt = np.clip(tt, T[0], T[-1])
+    P, _, _ = oracle.interp2d(R, T, G, rho, tt)
+    exact = a + b * rho + c * tt + d * rho * tt
+    assert np.max(np.abs(P - exact) / np.abs(exact)) < 1e-12
+
+
+def test_interp_nodes_exact_and_1d_reduction():
+    rng = np.random.default_rng(2)
+    R, T = _axes(rng)
+    G = rng.uniform(1.0, 5.0, (R.size, T.size))
+    rr, tt = np.meshgrid(R, T, indexing="ij")
+    P, iR, iT = oracle.interp2d(R, T, G, rr.ravel(), tt.ravel())
+    assert np.array_equal(P, G.ravel())
+    assert np.array_equal(iR, np.repeat(np.arange(R.size), T.size))
+    # G depending on rho only -> 1-D linear interpolation (np.interp clamps the same way)
+    g1 = rng.uniform(1.0, 5.0, R.size)
+    G1 = np.repeat(g1[:, None], T.size, axis=1)
+    rho = 10.0 ** rng.uniform(-7, 4, 30000)
+    t = 10.0 ** rng.uniform(-1, 9, 30000)
+    P1, _, _ = oracle.interp2d(R, T, G1, rho, t)
+    assert np.max(np.abs(P1 - np.interp(rho, R, g1)) / np.abs(P1)) < 1e-13
+
+
+def test_interp_scipy_and_convex_hull():
+    from scipy.interpolate import RegularGridInterpolator
+    import datagen
+    w = datagen.workload("cfg4", count=100_000)
+    rho = w.rho_targets.host_fill(0, w.count)
+    t = w.T_targets.host_fill(0, w.count)
+    rho = np.clip(rho, w.rho[0], w.rho[-1])
+    t = np.clip(t, w.T[0], w.T[-1])
+    P, iR, iT = oracle.interp2d(w.rho, w.T, w.P, rho, t)
+    ref = RegularGridInterpolator((w.rho, w.T), w.P, method="linear")(np.stack([rho, t], 1))
+    assert np.max(np.abs(P - ref) / np.abs(ref)) < 1e-12
+    ci = np.minimum(iR, w.rho.size - 2)
+    cj = np.minimum(iT, w.T.size - 2)
+    corners = np.stack([w.P[ci, cj], w.P[ci, cj + 1], w.P[ci + 1, cj], w.P[ci + 1, cj + 1]])
+    lo, hi = corners.min(0), corners.max(0)
+    assert np.all(P >= lo * (1 - 1e-15)) and np.all(P <= hi * (1 + 1e-15))
+
+
+def test_interp_nan_propagates_bracket_zero():
+    R, T, G, _ = interp_cases()
+    P, iR, iT = oracle.interp2d(R, T, G, np.array([np.nan, 1.5]), np.array([15.0, np.nan]))
+    assert np.isnan(P).all()
+    assert iR.tolist() == [0, 0] and iT.tolist() == [0, 0]
+
+
+# --------------------------------------------------------------- counters ---
+def _mix64_np(z):
+    z = z.astype(np.uint64)
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def test_counters_match_definitions():
+    rng = np.random.default_rng(3)
+    X = np.sort(10.0 ** rng.uniform(-3, 3, 100))
+    Y = 10.0 ** rng.uniform(-4, 4, 10000)
+    Y[::50] = np.nan
+    Y[1::77] = X[rng.integers(0, X.size, Y[1::77].size)]
+    idx = oracle.search(X, Y)
+    off = 123456789
+    c = oracle.counters(X, Y, idx, off)
+    pos = np.arange(Y.size, dtype=np.uint64) + np.uint64(off)
+    with np.errstate(over="ignore"):
+        c2 = np.sum(_mix64_np((pos << np.uint64(20)) | idx.astype(np.uint64)), dtype=np.uint64)
+    assert c[0] == Y.size
+    assert c[1] == idx.astype(np.uint64).sum()
+    assert c[2] == c2
+    assert c[3] == np.sum(~(Y >= X[0]))
+    assert c[4] == np.sum(Y > X[-1])
+    assert c[5] == np.sum(np.isnan(Y))
+    assert c[6] == np.sum(Y == X[idx])
+    assert c[7] == 0
+    # shard additivity (what the NCCL all_reduce relies on)
+    h = 4321
+    c_a = oracle.counters(X, Y[:h], idx[:h], off)
+    c_b = oracle.counters(X, Y[h:], idx[h:], off + h)
+    with np.errstate(over="ignore"):
+        assert np.array_equal(c_a + c_b, c)
