@@ -1,0 +1,468 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the hot path on B200 (the driver's contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, NCCL)
+
+A step = one pass of the hot path (stage table, stream
+targets, bin lookup, in-bin search, fix-up, store indices) over one batch of
+synthetic input resident in HBM: ONE kernel launch of eos_search (cfg4: of
+eos_interp2d).  Default workload: BASELINE.json configs[1] (cfg2: n=300,
+2^27 fp64 targets per GPU, weak scaling).  cfg5 shards its fixed 8*2^30
+targets over the ranks (strong scaling).
+
+Prints ONE JSON line on rank 0.  `value` = lookups (pairs for cfg4) of all
+ranks / max-over-ranks device time, in G/s.  `e2e` = the same metric through
+the C-ABI host-buffer entry point (eos_search_host: pinned H2D + search + D2H
+inside the timed region).  `roofline` = the kernel's algorithmic bytes / its
+CUDA-event launch time vs the measured HBM peak.  `cpu_baseline` = the CPU
+oracle (oracle/, test infrastructure) timed on this host on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "Glookups/s per GPU and box (1/2/4/8 B200); achieved HBM GB/s vs peak"
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback (6.65 TB/s), used only without MEASURED_PEAKS.json
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "paper"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--k", type=int, default=None, help="override the directory k (default: auto)")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--count", type=int, default=None, help="override targets per GPU (testing)")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------- clocks ---
+class ClockSampler:
+    """NVML samples of SM clock + clock-event reasons during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.ok = False
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _reasons(self):
+        nv = self.nv
+        f = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        return f(self.h)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self._reasons()
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": float(self.max_mhz),
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------- distributed -----
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend="nccl"):
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            import torch
+            self.pg.barrier(device_ids=[torch.cuda.current_device()]) if torch.cuda.is_available() \
+                else self.pg.barrier()
+
+    def allreduce(self, t, op="max"):
+        if self.pg:
+            self.pg.all_reduce(t, op=getattr(self.pg.ReduceOp, op.upper()))
+        return t
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+def shard(total: int, world: int, rank: int):
+    """Contiguous block sharding: rank r takes [r*total/world, (r+1)*total/world)."""
+    lo = total * rank // world
+    hi = total * (rank + 1) // world
+    return lo, hi - lo
+
+
+# ------------------------------------------------------------ our arm ------
+def run_ours(a, d: Dist):
+    import torch
+    import datagen
+    import paper_2112_03229_b200 as eos
+
+    torch.cuda.set_device(d.local)
+    dev = torch.device("cuda", d.local)
+    w = datagen.workload(a.workload)
+    strong = a.workload == "cfg5"
+    per_gpu = a.count or w.count
+    if strong:
+        total = a.count or w.count
+        offset, count = shard(total, d.world, d.rank)
+    else:
+        total = per_gpu * d.world
+        offset, count = per_gpu * d.rank, per_gpu
+    is2d = w.is_2d
+    bytes_per = 32 if is2d else 12
+    stream = torch.cuda.current_stream()
+
+    # inputs resident in HBM, generated in place (rank-invariant counter RNG)
+    if is2d:
+        rho = torch.empty(count, dtype=torch.float64, device=dev)
+        T = torch.empty(count, dtype=torch.float64, device=dev)
+        w.rho_targets.device_fill(rho, offset)
+        w.T_targets.device_fill(T, offset)
+        P = torch.empty(count, dtype=torch.float64, device=dev)
+        iR = torch.empty(count, dtype=torch.int32, device=dev)
+        iT = torch.empty(count, dtype=torch.int32, device=dev)
+        obj = eos.Grid2D(w.rho, w.T, w.P)
+        info = {"rho": obj.rho_info.as_dict(), "T": obj.T_info.as_dict()}
+
+        def step():
+            eos.eos_interp2d(obj.handle, rho.data_ptr(), T.data_ptr(), count, P.data_ptr(),
+                             iR.data_ptr(), iT.data_ptr(), stream.cuda_stream)
+    else:
+        Y = torch.empty(count, dtype=torch.float64, device=dev)
+        w.targets.device_fill(Y, offset, table_dev=torch.from_numpy(w.table).to(dev))
+        out = torch.empty(count, dtype=torch.int32, device=dev)
+        obj = eos.Table(w.table, k=a.k)
+        info = obj.info.as_dict()
+
+        def step():
+            eos.eos_search(obj.handle, Y.data_ptr(), count, out.data_ptr(), stream.cuda_stream)
+    torch.cuda.synchronize()
+
+    for _ in range(max(a.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(a.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = eos.launch_count()
+    d.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(d.local) as clk:
+        t0.record(stream)
+        for i in range(a.steps):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    d.barrier()
+    launches = eos.launch_count() - launches0
+    ms_total = t0.elapsed_time(t1)
+    kern_ms = float(np.mean([s.elapsed_time(e) for s, e in ev]))
+    tm = torch.tensor([ms_total, kern_ms], dtype=torch.float64, device=dev)
+    d.allreduce(tm, "max")
+    ms_total, kern_ms_max = float(tm[0]), float(tm[1])
+    ms_step = ms_total / a.steps
+    value = total / (ms_step * 1e-3) / 1e9  # G units / s, whole job
+
+    # validation counters over this shard (untimed), reduced with one NCCL all_reduce
+    counters = None
+    if not is2d:
+        c = torch.zeros(8, dtype=torch.int64, device=dev)
+        obj.search(Y, out=out, counters=c, global_offset=offset)
+        d.allreduce(c, "sum")
+        counters = [int(x) & 0xFFFFFFFFFFFFFFFF for x in c.cpu().tolist()]
+
+    # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, d, w, obj, offset, count, total, is2d, dev)
+
+    hbm_peak, peak_src = peaks()
+    achieved = bytes_per * count / (kern_ms * 1e-3) / 1e9
+    res = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "Gpairs/s" if is2d else "Glookups/s",
+        "n_gpus": d.world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded counter-based generators, generated in HBM; DESIGN.md input recipe)",
+        "config": {
+            "workload": a.workload,
+            "desc": w.note,
+            "units_per_gpu": count,
+            "units_total": total,
+            "table": info,
+            "bytes_per_unit": bytes_per,
+            "l2": f"inputs larger than L2: {bytes_per * count / 1e9:.2f} GB streamed per step per GPU "
+                  "(126 MB L2), no flush needed" if bytes_per * count > 4 * 126e6 else
+                  "inputs L2-resident (launch-bound parity config)",
+            "parallelism": f"dp{d.world} (target-stream sharding, no data-path collective)",
+        },
+        "gpu_launches": int(launches),
+        "roofline": {
+            "bound": "hbm",
+            "achieved": round(achieved, 1),
+            "peak": hbm_peak,
+            "unit": "GB/s",
+            "frac": round(achieved / hbm_peak, 4),
+            "traffic": ncu_traffic(a.workload),
+            "kernel": "interp2d_kernel" if is2d else "search1d_kernel",
+            "kernel_ms_avg": round(kern_ms, 5),
+            "kernel_ms_avg_max_rank": round(kern_ms_max, 5),
+            "algorithmic_bytes_per_launch": bytes_per * count,
+            "peak_source": peak_src,
+        },
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if counters is not None:
+        res["validation"] = {"counters_u64": counters}
+    if d.world == 1 and d.rank == 0 and not a.no_cpu:
+        res["cpu_baseline"] = cpu_baseline(w, is2d)
+    return res
+
+
+def run_e2e(a, d, w, obj, offset, count, total, is2d, dev):
+    import torch
+    import paper_2112_03229_b200 as eos
+    steps = a.e2e_steps or max(3, min(20, a.steps // 50))
+    stream = torch.cuda.current_stream()
+    # bounded host footprint: at most 2^28 units per rank per e2e step (cfg5 would need 96 GiB pinned)
+    count = min(count, 1 << 28)
+    total = count * d.world
+    if is2d:
+        rh = torch.empty(count, dtype=torch.float64).pin_memory()
+        th = torch.empty(count, dtype=torch.float64).pin_memory()
+        rh.numpy()[:] = w.rho_targets.host_fill(offset, count)
+        th.numpy()[:] = w.T_targets.host_fill(offset, count)
+        Ph = torch.empty(count, dtype=torch.float64).pin_memory()
+        iRh = torch.empty(count, dtype=torch.int32).pin_memory()
+        iTh = torch.empty(count, dtype=torch.int32).pin_memory()
+        h2d, d2h = 16 * count, 16 * count
+
+        def step():
+            eos.eos_interp2d_host(obj.handle, rh.data_ptr(), th.data_ptr(), count, Ph.data_ptr(),
+                                  iRh.data_ptr(), iTh.data_ptr(), stream.cuda_stream)
+    else:
+        Yh = torch.empty(count, dtype=torch.float64).pin_memory()
+        fill_host_parallel(w, offset, count, Yh.numpy())
+        Ih = torch.empty(count, dtype=torch.int32).pin_memory()
+        h2d, d2h = 8 * count, 4 * count
+
+        def step():
+            eos.eos_search_host(obj.handle, Yh.data_ptr(), count, Ih.data_ptr(), stream.cuda_stream)
+    step()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d.barrier()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for _ in range(steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    d.barrier()
+    tm = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+    d.allreduce(tm, "max")
+    ms = float(tm[0]) / steps
+    return {"value": round(total / (ms * 1e-3) / 1e9, 4), "unit": "Gpairs/s" if is2d else "Glookups/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "ms_per_step": round(ms, 3), "api": "eos_interp2d_host" if is2d else "eos_search_host",
+            "units_per_step": total, "host_buffers": "pinned"}
+
+
+def fill_host_parallel(w, offset, count, out, threads=None):
+    from concurrent.futures import ThreadPoolExecutor
+    threads = threads or host_cores()
+    if w.targets.kind == "walk":
+        out[:] = w.targets.host_fill(offset, count)
+        return
+    step = (count + threads - 1) // threads
+
+    def job(s):
+        e = min(count, s + step)
+        out[s:e] = w.targets.host_fill(offset + s, e - s, w.table)
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(job, range(0, count, step)))
+
+
+def ncu_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        v = d.get(workload)
+        if isinstance(v, dict):
+            return v.get("dram_bytes_per_launch")
+    return None
+
+
+# -------------------------------------------------------- CPU oracle -------
+def oracle_run(w, is2d, sample: int, threads: int):
+    """Time the oracle (as it stands) on the first `sample` units of the workload."""
+    import oracle
+    if is2d:
+        rho = w.rho_targets.host_fill(0, sample)
+        T = w.T_targets.host_fill(0, sample)
+        t = time.perf_counter()
+        oracle.interp2d(w.rho, w.T, w.P, rho, T, threads=threads)
+        return time.perf_counter() - t
+    Y = np.empty(sample, dtype=np.float64)
+    fill_host_parallel(w, 0, sample, Y)
+    t = time.perf_counter()
+    oracle.search(w.table, Y, threads=threads)
+    return time.perf_counter() - t
+
+
+def cpu_sample_size(w, is2d):
+    return min(w.count, (1 << 25) if is2d else (1 << 27))
+
+
+def cpu_baseline(w, is2d):
+    threads = host_cores()
+    sample = cpu_sample_size(w, is2d)
+    dt = oracle_run(w, is2d, sample, threads)
+    return {"value": round(sample / dt / 1e9, 5), "unit": "Gpairs/s" if is2d else "Glookups/s",
+            "cores": threads, "kind": "oracle",
+            "sample": f"first {sample} units of {w.name} (host-generated, same recipe), "
+                      f"oracle/eos_oracle.c scalar bisection over {threads} threads; "
+                      f"{dt:.2f} s wall; cpu: {cpu_model()}"}
+
+
+# ------------------------------------------------------ reference arm ------
+def run_reference(a, d: Dist):
+    """The oracle as the reference arm: rank 0 only, bounded sample per step."""
+    import datagen
+    w = datagen.workload(a.workload)
+    is2d = w.is_2d
+    threads = host_cores()
+    sample = min(w.count, (1 << 22) if is2d else (1 << 24))
+    for _ in range(min(a.warmup, 1)):
+        oracle_run(w, is2d, min(sample, 1 << 16), threads)
+    times = [oracle_run(w, is2d, sample, threads) for _ in range(max(1, min(a.steps, 10)))]
+    s = float(np.mean(times))
+    value = sample / s / 1e9
+    unit = "Gpairs/s" if is2d else "Glookups/s"
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": unit,
+        "n_gpus": d.world, "steps": len(times), "warmup": a.warmup, "ms_per_step": round(s * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong" if a.workload == "cfg5" else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": a.workload, "desc": w.note, "sample_units_per_step": sample},
+        "cpu_baseline": {"value": round(value, 5), "unit": unit, "cores": threads, "kind": "oracle",
+                         "sample": f"first {sample} units of {w.name} per step; cpu: {cpu_model()}"},
+        "e2e": {"value": round(value, 5), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference arm = the CPU oracle (no reference implementation exists; PAPER.md only)",
+    }
+
+
+def main():
+    a = parse()
+    d = Dist()
+    if a.impl == "reference":
+        if d.rank == 0:
+            print(json.dumps(run_reference(a, d)), flush=True)
+        return
+    import torch
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    if d.world > 1:
+        torch.cuda.set_device(d.local)
+    d.init("nccl")
+    try:
+        res = run_ours(a, d)
+        if d.rank == 0:
+            print(json.dumps(res), flush=True)
+    finally:
+        d.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,204 @@
+/* eossearch.h -- C ABI of the B200-native batched table lookup.
+ *
+ * The hot path of arXiv 2112.03229 ("vectorized search over small,
+ * logarithmically distributed sorted tables", EOSPAC case study), rebuilt for
+ * sm_100a.  Citations: P:<n> = line n of the paper text; the
+ * readings R<n> are listed in DESIGN.md.
+ *
+ * Conventions for every call:
+ *   - Returns eos_status (EOS_OK = 0) unless noted.  Argument errors are
+ *     detected synchronously, before any device work is queued, and no
+ *     output is written.  Asynchronous kernel faults surface as EOS_ERR_CUDA
+ *     from a later call or at the caller's stream synchronisation.
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *     Device work is queued on it and the call returns without waiting
+ *     (except the *_host entry points, see below).
+ *   - "_dev" pointers are device memory of the device the handle was created
+ *     on (any allocator: cudaMalloc, torch, ...), owned by the caller.
+ *     "_host" pointers are host memory owned by the caller (pinned memory
+ *     gives overlapped copies; pageable memory works, slower).
+ *   - Any alignment is accepted (vectorised interior + scalar peel / tail).
+ *   - count == 0 is an EOS_OK no-op; count must be <= 2^62.
+ *   - Handles are immutable after create: concurrent calls on one handle
+ *     from several host threads / streams are safe.  destroy must not race
+ *     with in-flight work (it synchronises the device before freeing).
+ */
+#ifndef EOSSEARCH_H
+#define EOSSEARCH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define EOS_API __attribute__((visibility("default")))
+#else
+#define EOS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EOS_MAX_TABLE 16384 /* table entries staged in shared memory (fp64) */
+#define EOS_MAX_K 20        /* mantissa bits appended to the exponent hash */
+#define EOS_K_AUTO (-1)     /* let eos_search_create_ex choose k */
+#define EOS_N_COUNTERS 8
+
+typedef enum {
+  EOS_OK = 0,
+  EOS_ERR_NULL = 1,        /* a required pointer / handle is NULL */
+  EOS_ERR_SIZE = 2,        /* n or count out of range */
+  EOS_ERR_NONFINITE = 3,   /* a table / grid value is NaN or +-inf */
+  EOS_ERR_UNSORTED = 4,    /* table not non-decreasing (axes: not strictly increasing) */
+  EOS_ERR_DEVICE = 5,      /* no CUDA device, or current device differs from the handle's */
+  EOS_ERR_CUDA = 6,        /* a CUDA runtime call failed (incl. earlier async faults) */
+  EOS_ERR_NOMEM = 7,       /* host or device allocation failed */
+  EOS_ERR_UNSUPPORTED = 8, /* valid request this build does not support (e.g. k > EOS_MAX_K) */
+  EOS_ERR_ALIAS = 9        /* output overlaps an input */
+} eos_status;
+
+typedef struct eos_table_s* eos_table;
+typedef struct eos_grid2d_s* eos_grid2d;
+
+/* Description of a built table (see eos_plan_table for the meaning). */
+typedef struct {
+  int64_t n;           /* table entries */
+  int32_t key_mode;    /* 0: X[0] >= 0, key = |bits| (sign masked); 1: negatives, order-preserving key */
+  int32_t k;           /* mantissa bits appended to the binary exponent (k = 0: the paper's exponent hash) */
+  int32_t bins;        /* B: number of bins of the directory */
+  int32_t max_occ;     /* largest number of table entries in one bin */
+  int32_t steps;       /* S = ceil(log2(max_occ + 1)): fixed in-bin search steps */
+  int32_t base;        /* key >> (20 - k) of the lowest binned entry */
+  int64_t image_bytes; /* shared-memory image: X fp64[n] (16-B padded) + directory u32[B] */
+  int32_t device;      /* CUDA device of the handle (-1 for eos_plan_table) */
+  int32_t ctas_per_sm; /* resident CTAs per SM of the search kernel (0 for plan) */
+} eos_table_info_t;
+
+/* ---------------------------------------------------------------------------
+ * Host-only planning (no device needed).
+ *
+ * eos_plan_table: validates a table and builds its exponent-hash bin
+ * directory on the host, exactly as eos_search_create does, without touching
+ * a device.  Used by the host-logic tests and for inspection.
+ *   table_host : fp64[n], finite, non-decreasing (duplicates allowed, P:54-56
+ *                "monotonically increasing"; -0.0 is canonicalised to +0.0)
+ *   n          : 1 <= n <= EOS_MAX_TABLE
+ *   k          : EOS_K_AUTO or 0..EOS_MAX_K.  The bin of a value v is
+ *                  b(v) = clamp((key(v) >> (52 - k)) - base, 0, B-1),
+ *                key = the IEEE-754 binary64 bits with the sign masked
+ *                (mode 0); k = 0 is exactly the paper's "Exponent Hash
+ *                Search" (bin by the base-2 exponent field),
+ *                k > 0 appends the top k mantissa bits (a finer, still
+ *                monotone hash; R10/R13).
+ *   dir_out    : optional (may be NULL) u32[cap]; receives the packed count
+ *                directory, entry b = lo_b | (occ_b << 16) with
+ *                lo_b = #{j : b(X_j) < b} and occ_b = #{j : b(X_j) == b}
+ *                (P:150 and Eq. 3 re-formulated as counts, R10/R11).
+ *                EOS_ERR_SIZE if cap < bins.
+ *   info       : required, filled on success.
+ * ------------------------------------------------------------------------- */
+EOS_API eos_status eos_plan_table(const double* table_host, int64_t n, int32_t k, eos_table_info_t* info,
+                          uint32_t* dir_out, int64_t cap);
+
+/* ---------------------------------------------------------------------------
+ * 1-D search ("Each algorithm takes a targets array (Y, of size m), and
+ * a data array (X, of size n).  They perform a lower-bounds search, returning
+ * an array of size m containing the index of the last element of X which is
+ * less than or equal to each element of Y.  If X contains no such lower bound
+ * for a given y in Y, the index 0 is chosen.  In the case that the element is
+ * higher than the highest of X, the index n-1 is chosen.")
+ *
+ * Result per target y: idx = max(0, #{j : X[j] <= y} - 1) with IEEE "<=".
+ * Hence ties -> that entry, duplicates -> the last one, y < X[0] -> 0,
+ * NaN -> 0 (R4), +inf -> n-1, -inf -> 0, -0.0 == +0.0 (R6).
+ * ------------------------------------------------------------------------- */
+
+/* Setup once per table ("the search setup [is] performed only once"):
+ * validates, builds the directory (k chosen by the cost model, EOS_K_AUTO)
+ * and uploads the device image to the CURRENT CUDA device.  The table is
+ * copied; the caller may free table_host on return. */
+EOS_API eos_status eos_search_create(const double* table_host, int64_t n, eos_table* out);
+
+/* Same with an explicit k (EOS_K_AUTO or 0..EOS_MAX_K).  Results do not
+ * depend on k (tested); only speed does. */
+EOS_API eos_status eos_search_create_ex(const double* table_host, int64_t n, int32_t k, eos_table* out);
+
+/* idx_out_dev[i] = lower bound of targets_dev[i], i in [0, count).
+ *   targets_dev : fp64[count] device, read once (streaming)
+ *   idx_out_dev : int32[count] device, written once; must not overlap targets
+ * Asynchronous on `stream`. */
+EOS_API eos_status eos_search(eos_table t, const double* targets_dev, int64_t count, int32_t* idx_out_dev,
+                      void* stream);
+
+/* eos_search plus optional validation counters.
+ *   global_offset : global position of targets_dev[0] in a sharded stream
+ *   counters_dev  : NULL, or device u64[8] that is ACCUMULATED into (+=,
+ *                   modulo 2^64; zero it first):
+ *       c0 #targets            c1 sum idx
+ *       c2 sum mix64((global_position << 20) | idx)   (splitmix64 finalizer)
+ *       c3 #(!(y >= X[0]))     c4 #(y > X[n-1])
+ *       c5 #NaN                c6 #(y == X[idx])      c7 reserved (0)
+ *   With counters_dev == NULL this is exactly eos_search. */
+EOS_API eos_status eos_search_ex(eos_table t, const double* targets_dev, int64_t count,
+                         int32_t* idx_out_dev, int64_t global_offset, uint64_t* counters_dev,
+                         void* stream);
+
+/* End-to-end form with HOST buffers: the targets are copied host->device in
+ * chunks, searched, and the indices copied device->host, with the copies of
+ * one chunk overlapping the search/copies of the next (two internal streams,
+ * stream-ordered device staging allocated on `stream`).  Ordered after prior
+ * work on `stream`; returns once the work is queued -- the indices are valid
+ * after `stream` is synchronised.  Pinned host memory is required for
+ * overlap (pageable memory is accepted). */
+EOS_API eos_status eos_search_host(eos_table t, const double* targets_host, int64_t count,
+                           int32_t* idx_out_host, void* stream);
+
+EOS_API eos_status eos_table_info(eos_table t, eos_table_info_t* out);
+EOS_API eos_status eos_search_destroy(eos_table t);
+
+/* ---------------------------------------------------------------------------
+ * 2-D EOSPAC-style interpolation (EOSPAC "provides interpolation
+ * mechanisms" over a SESAME density x temperature table; the paper gives no
+ * formula -- bilinear reading R14):
+ *   i = lower bound of rho in R, j = lower bound of T in Tax
+ *   ci = min(i, nR-2), cj = min(j, nT-2)
+ *   tx = clamp01((rho - R[ci]) / (R[ci+1] - R[ci])), ty likewise (NaN kept)
+ *   P = (1-tx)((1-ty) G[ci][cj] + ty G[ci][cj+1])
+ *     +    tx ((1-ty) G[ci+1][cj] + ty G[ci+1][cj+1])
+ * ------------------------------------------------------------------------- */
+
+/* rho_host fp64[n_rho], T_host fp64[n_T]: strictly increasing, finite,
+ * 2 <= n <= EOS_MAX_TABLE; P_host fp64[n_rho * n_T] row-major (T fastest),
+ * finite; the grid must fit in shared memory (n_rho*n_T*8 + axes <= ~200 KB,
+ * else EOS_ERR_UNSUPPORTED).  Copied; bound to the current device. */
+EOS_API eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double* T_host,
+                             int64_t n_T, const double* P_host, eos_grid2d* out);
+
+/* P_out_dev[q] = interpolated value at (rho_dev[q], T_dev[q]);
+ * irho_out_dev / iT_out_dev (nullable) receive the brackets i, j.
+ * All device arrays of length count; outputs must not overlap inputs. */
+EOS_API eos_status eos_interp2d(eos_grid2d g, const double* rho_dev, const double* T_dev, int64_t count,
+                        double* P_out_dev, int32_t* irho_out_dev, int32_t* iT_out_dev,
+                        void* stream);
+
+/* End-to-end form with host buffers (see eos_search_host). */
+EOS_API eos_status eos_interp2d_host(eos_grid2d g, const double* rho_host, const double* T_host,
+                             int64_t count, double* P_out_host, int32_t* irho_out_host,
+                             int32_t* iT_out_host, void* stream);
+
+/* info of the two axis tables (either pointer may be NULL) */
+EOS_API eos_status eos_grid2d_info(eos_grid2d g, eos_table_info_t* rho_info, eos_table_info_t* T_info);
+EOS_API eos_status eos_grid2d_destroy(eos_grid2d g);
+
+/* ---------------------------------------------------------------------------
+ * Misc
+ * ------------------------------------------------------------------------- */
+EOS_API const char* eos_status_str(eos_status s); /* static string, never NULL */
+EOS_API int32_t eos_abi_version(void);            /* 1 */
+/* Kernel launches issued by this library since load (all entry points). */
+EOS_API int64_t eos_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EOSSEARCH_H */

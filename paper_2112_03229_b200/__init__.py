@@ -1,0 +1,362 @@
+"""paper_2112_03229_b200 -- B200-native batched lower-bound search + EOS interpolation.
+
+Thin Python binding (argument marshalling only) over the C ABI of
+include/eossearch.h, implemented by lib/libeossearch.so (sm_100a kernels).
+Every step of the hot path runs in that library; there is no Python or CPU
+fallback: if the library is missing or cannot be loaded, importing the
+binding's functions raises.
+
+PyTorch is used only as the device-memory / stream provider: tensors are
+passed as raw pointers with `torch.cuda.current_stream().cuda_stream`.
+
+Paper: arXiv 2112.03229: lower-bound contract P:54, exponent hash
+P:211-213, EOSPAC interpolation P:14/P:41.  Readings R<n>: DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from ._build import LIB as _LIB_PATH
+
+__all__ = [
+    "EosError", "Table", "Grid2D", "TableInfo", "plan_table", "load_library", "launch_count",
+    "eos_search_create", "eos_search_create_ex", "eos_search", "eos_search_ex", "eos_search_host",
+    "eos_search_destroy", "eos_table_info", "eos_plan_table", "eos_grid2d_create", "eos_interp2d",
+    "eos_interp2d_host", "eos_grid2d_destroy", "eos_grid2d_info", "eos_status_str", "EOS_K_AUTO",
+    "EOS_MAX_TABLE", "EOS_MAX_K", "EXPORTED_SYMBOLS",
+]
+
+EOS_MAX_TABLE = 16384
+EOS_MAX_K = 20
+EOS_K_AUTO = -1
+
+STATUS = {
+    0: "EOS_OK", 1: "EOS_ERR_NULL", 2: "EOS_ERR_SIZE", 3: "EOS_ERR_NONFINITE",
+    4: "EOS_ERR_UNSORTED", 5: "EOS_ERR_DEVICE", 6: "EOS_ERR_CUDA", 7: "EOS_ERR_NOMEM",
+    8: "EOS_ERR_UNSUPPORTED", 9: "EOS_ERR_ALIAS",
+}
+
+# every symbol include/eossearch.h declares
+EXPORTED_SYMBOLS = (
+    "eos_plan_table", "eos_search_create", "eos_search_create_ex", "eos_search", "eos_search_ex",
+    "eos_search_host", "eos_table_info", "eos_search_destroy", "eos_grid2d_create",
+    "eos_interp2d", "eos_interp2d_host", "eos_grid2d_info", "eos_grid2d_destroy",
+    "eos_status_str", "eos_abi_version", "eos_launch_count",
+)
+
+
+class EosError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        self.name = STATUS.get(code, f"status {code}")
+        super().__init__(f"{where}: {self.name} ({eos_status_str(code)})")
+
+
+class TableInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("key_mode", ctypes.c_int32), ("k", ctypes.c_int32),
+                ("bins", ctypes.c_int32), ("max_occ", ctypes.c_int32), ("steps", ctypes.c_int32),
+                ("base", ctypes.c_int32), ("image_bytes", ctypes.c_int64),
+                ("device", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_ST = ctypes.c_int
+
+
+def load_library():
+    """Load lib/libeossearch.so (fails loudly: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(python -m paper_2112_03229_b200._build); there is no CPU fallback")
+    L = ctypes.CDLL(_LIB_PATH)
+    sig = {
+        "eos_plan_table": [_P, _I64, _I32, _P, _P, _I64],
+        "eos_search_create": [_P, _I64, _P],
+        "eos_search_create_ex": [_P, _I64, _I32, _P],
+        "eos_search": [_P, _P, _I64, _P, _P],
+        "eos_search_ex": [_P, _P, _I64, _P, _I64, _P, _P],
+        "eos_search_host": [_P, _P, _I64, _P, _P],
+        "eos_table_info": [_P, _P],
+        "eos_search_destroy": [_P],
+        "eos_grid2d_create": [_P, _I64, _P, _I64, _P, _P],
+        "eos_interp2d": [_P, _P, _P, _I64, _P, _P, _P, _P],
+        "eos_interp2d_host": [_P, _P, _P, _I64, _P, _P, _P, _P],
+        "eos_grid2d_info": [_P, _P, _P],
+        "eos_grid2d_destroy": [_P],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = _ST
+    L.eos_status_str.argtypes = [_ST]
+    L.eos_status_str.restype = ctypes.c_char_p
+    L.eos_abi_version.restype = _I32
+    L.eos_launch_count.restype = _I64
+    _lib = L
+    return L
+
+
+def _check(code: int, where: str):
+    if code != 0:
+        raise EosError(code, where)
+
+
+def eos_status_str(code: int) -> str:
+    return load_library().eos_status_str(code).decode()
+
+
+def launch_count() -> int:
+    """Kernel launches issued by libeossearch.so in this process."""
+    return int(load_library().eos_launch_count())
+
+
+def _f64_host(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dev(t, dtype_name: str, what: str):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{what} must be a CUDA tensor")
+    if t.dtype != getattr(torch, dtype_name):
+        raise TypeError(f"{what} must be torch.{dtype_name}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    return t
+
+
+# ----------------------------------------------------------- raw C-ABI -----
+def eos_plan_table(table, k: int = EOS_K_AUTO, with_directory: bool = True):
+    """Host-only plan (no device): (TableInfo, directory u32[bins] | None)."""
+    L = load_library()
+    X = _f64_host(table)
+    info = TableInfo()
+    _check(L.eos_plan_table(X.ctypes.data, X.size, k, ctypes.byref(info), None, 0), "eos_plan_table")
+    d = None
+    if with_directory:
+        d = np.empty(info.bins, dtype=np.uint32)
+        _check(L.eos_plan_table(X.ctypes.data, X.size, k, ctypes.byref(info), d.ctypes.data, d.size),
+               "eos_plan_table")
+    return info, d
+
+
+plan_table = eos_plan_table
+
+
+def eos_search_create(table) -> int:
+    return eos_search_create_ex(table, EOS_K_AUTO)
+
+
+def eos_search_create_ex(table, k: int = EOS_K_AUTO) -> int:
+    L = load_library()
+    X = _f64_host(table)
+    h = ctypes.c_void_p()
+    _check(L.eos_search_create_ex(X.ctypes.data, X.size, k, ctypes.byref(h)), "eos_search_create")
+    return h.value
+
+
+def eos_search(handle: int, targets_ptr: int, count: int, idx_out_ptr: int, stream: int) -> None:
+    _check(load_library().eos_search(handle, targets_ptr, count, idx_out_ptr, stream), "eos_search")
+
+
+def eos_search_ex(handle, targets_ptr, count, idx_out_ptr, global_offset, counters_ptr, stream):
+    _check(load_library().eos_search_ex(handle, targets_ptr, count, idx_out_ptr, global_offset,
+                                        counters_ptr, stream), "eos_search_ex")
+
+
+def eos_search_host(handle, targets_host_ptr, count, idx_out_host_ptr, stream):
+    _check(load_library().eos_search_host(handle, targets_host_ptr, count, idx_out_host_ptr, stream),
+           "eos_search_host")
+
+
+def eos_table_info(handle) -> TableInfo:
+    info = TableInfo()
+    _check(load_library().eos_table_info(handle, ctypes.byref(info)), "eos_table_info")
+    return info
+
+
+def eos_search_destroy(handle) -> None:
+    _check(load_library().eos_search_destroy(handle), "eos_search_destroy")
+
+
+def eos_grid2d_create(rho, T, P) -> int:
+    L = load_library()
+    r, t, p = _f64_host(rho), _f64_host(T), _f64_host(P)
+    if p.size != r.size * t.size:
+        raise ValueError("P must have n_rho * n_T values (row-major, T fastest)")
+    h = ctypes.c_void_p()
+    _check(L.eos_grid2d_create(r.ctypes.data, r.size, t.ctypes.data, t.size, p.ctypes.data,
+                               ctypes.byref(h)), "eos_grid2d_create")
+    return h.value
+
+
+def eos_interp2d(handle, rho_ptr, T_ptr, count, P_ptr, iR_ptr, iT_ptr, stream):
+    _check(load_library().eos_interp2d(handle, rho_ptr, T_ptr, count, P_ptr, iR_ptr, iT_ptr, stream),
+           "eos_interp2d")
+
+
+def eos_interp2d_host(handle, rho_ptr, T_ptr, count, P_ptr, iR_ptr, iT_ptr, stream):
+    _check(load_library().eos_interp2d_host(handle, rho_ptr, T_ptr, count, P_ptr, iR_ptr, iT_ptr,
+                                            stream), "eos_interp2d_host")
+
+
+def eos_grid2d_info(handle):
+    a, b = TableInfo(), TableInfo()
+    _check(load_library().eos_grid2d_info(handle, ctypes.byref(a), ctypes.byref(b)), "eos_grid2d_info")
+    return a, b
+
+
+def eos_grid2d_destroy(handle) -> None:
+    _check(load_library().eos_grid2d_destroy(handle), "eos_grid2d_destroy")
+
+
+# ------------------------------------------------------------ objects ------
+class Table:
+    """A search table bound to the current CUDA device (eos_search_create)."""
+
+    def __init__(self, table, k: int | None = None):
+        self.X = _f64_host(table).copy()
+        self._h = eos_search_create_ex(self.X, EOS_K_AUTO if k is None else k)
+        self.info = eos_table_info(self._h)
+
+    @property
+    def handle(self) -> int:
+        return self._h
+
+    def search(self, targets, out=None, stream=None, counters=None, global_offset: int = 0):
+        """int32 indices of the last table entry <= each target."""
+        import torch
+        _dev(targets, "float64", "targets")
+        if out is None:
+            out = torch.empty(targets.numel(), dtype=torch.int32, device=targets.device)
+        _dev(out, "int32", "out")
+        if out.numel() != targets.numel():
+            raise ValueError("out must have one int32 per target")
+        cptr = None
+        if counters is not None:
+            _dev(counters, "int64", "counters")
+            if counters.numel() < 8:
+                raise ValueError("counters needs 8 entries")
+            cptr = counters.data_ptr()
+        eos_search_ex(self._h, targets.data_ptr(), targets.numel(), out.data_ptr(), global_offset,
+                      cptr, _stream_ptr(stream))
+        return out
+
+    def search_host(self, targets: np.ndarray, out: np.ndarray | None = None, stream=None,
+                    sync: bool = True) -> np.ndarray:
+        """End-to-end from host buffers (eos_search_host); pinned memory recommended."""
+        import torch
+        if isinstance(targets, torch.Tensor):
+            targets = targets.numpy()
+        if targets.dtype != np.float64 or not targets.flags.c_contiguous:
+            raise TypeError("targets must be a contiguous float64 host array")
+        if out is None:
+            out = np.empty(targets.size, dtype=np.int32)
+        if isinstance(out, torch.Tensor):
+            out_ptr = out.data_ptr()
+        else:
+            out_ptr = out.ctypes.data
+        sp = _stream_ptr(stream)
+        eos_search_host(self._h, targets.ctypes.data, targets.size, out_ptr, sp)
+        if sync:
+            torch.cuda.current_stream().synchronize() if stream is None else torch.cuda.synchronize()
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            eos_search_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class Grid2D:
+    """EOSPAC-style 2-D table (density x temperature) for eos_interp2d."""
+
+    def __init__(self, rho, T, P):
+        self.rho, self.T = _f64_host(rho).copy(), _f64_host(T).copy()
+        self.P = _f64_host(P).reshape(self.rho.size, self.T.size).copy()
+        self._h = eos_grid2d_create(self.rho, self.T, self.P)
+        self.rho_info, self.T_info = eos_grid2d_info(self._h)
+
+    @property
+    def handle(self) -> int:
+        return self._h
+
+    def interp(self, rho, T, P_out=None, irho_out=None, iT_out=None, brackets: bool = True,
+               stream=None):
+        import torch
+        _dev(rho, "float64", "rho")
+        _dev(T, "float64", "T")
+        m = rho.numel()
+        if T.numel() != m:
+            raise ValueError("rho and T must have the same length")
+        if P_out is None:
+            P_out = torch.empty(m, dtype=torch.float64, device=rho.device)
+        if brackets and irho_out is None:
+            irho_out = torch.empty(m, dtype=torch.int32, device=rho.device)
+        if brackets and iT_out is None:
+            iT_out = torch.empty(m, dtype=torch.int32, device=rho.device)
+        eos_interp2d(self._h, rho.data_ptr(), T.data_ptr(), m, _dev(P_out, "float64", "P").data_ptr(),
+                     irho_out.data_ptr() if irho_out is not None else None,
+                     iT_out.data_ptr() if iT_out is not None else None, _stream_ptr(stream))
+        return P_out, irho_out, iT_out
+
+    def interp_host(self, rho: np.ndarray, T: np.ndarray, P_out=None, irho_out=None, iT_out=None,
+                    stream=None, sync: bool = True):
+        import torch
+        m = rho.size
+        P_out = np.empty(m, np.float64) if P_out is None else P_out
+        irho_out = np.empty(m, np.int32) if irho_out is None else irho_out
+        iT_out = np.empty(m, np.int32) if iT_out is None else iT_out
+
+        def ptr(a):
+            return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
+
+        eos_interp2d_host(self._h, ptr(rho), ptr(T), m, ptr(P_out), ptr(irho_out), ptr(iT_out),
+                          _stream_ptr(stream))
+        if sync:
+            torch.cuda.synchronize()
+        return P_out, irho_out, iT_out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            eos_grid2d_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,482 @@
+// eossearch.cu -- the C ABI of include/eossearch.h: handle management, device
+// image upload, launch configuration and the end-to-end host-buffer pipelines.
+// Product path (never includes or links oracle/).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <new>
+#include <vector>
+
+#include "eos_internal.h"
+#include "eossearch.h"
+#include "kernels.cuh"
+
+using eos::TablePlan;
+namespace dv = eos::dev;
+
+static std::atomic<int64_t> g_launches{0};
+
+struct eos_table_s {
+  TablePlan plan;
+  int device = -1;
+  int num_sms = 0;
+  void* image_dev = nullptr;
+  dv::AxisParams ax{};
+  // launch configuration per counters on/off
+  const void* fn[2] = {nullptr, nullptr};
+  int grid[2] = {0, 0};
+  int ctas_per_sm = 0;
+};
+
+struct eos_grid2d_s {
+  TablePlan pr, pt;
+  int device = -1;
+  int num_sms = 0;
+  void* image_dev = nullptr;
+  int64_t image_bytes = 0;
+  int32_t g_off = 0;
+  dv::AxisParams ar{}, at{};
+  const void* fn = nullptr;
+  int grid = 0;
+};
+
+namespace {
+
+// ---------------------------------------------------------- kernel table ---
+template <int S, int MODE>
+const void* search_fn(bool cnt) {
+  return cnt ? (const void*)dv::search1d_kernel<S, MODE, true>
+             : (const void*)dv::search1d_kernel<S, MODE, false>;
+}
+
+template <int MODE>
+const void* search_fn_mode(int steps, bool cnt) {
+  switch (steps) {
+    case 1: return search_fn<1, MODE>(cnt);
+    case 2: return search_fn<2, MODE>(cnt);
+    case 3: return search_fn<3, MODE>(cnt);
+    case 4: return search_fn<4, MODE>(cnt);
+    case 5: return search_fn<5, MODE>(cnt);
+    case 6: return search_fn<6, MODE>(cnt);
+    case 7: return search_fn<7, MODE>(cnt);
+    case 8: return search_fn<8, MODE>(cnt);
+    default: return search_fn<0, MODE>(cnt);  // runtime S
+  }
+}
+
+const void* pick_search(int mode, int steps, bool cnt) {
+  return mode == 0 ? search_fn_mode<0>(steps, cnt) : search_fn_mode<1>(steps, cnt);
+}
+
+const void* pick_interp(int steps) {
+  switch (steps) {
+    case 1: return (const void*)dv::interp2d_kernel<1>;
+    case 2: return (const void*)dv::interp2d_kernel<2>;
+    case 3: return (const void*)dv::interp2d_kernel<3>;
+    case 4: return (const void*)dv::interp2d_kernel<4>;
+    default: return (const void*)dv::interp2d_kernel<0>;
+  }
+}
+
+dv::AxisParams axis_params(const TablePlan& p, int32_t x_off) {
+  dv::AxisParams a{};
+  a.n = (int32_t)p.n;
+  a.x_off = x_off;
+  a.d_off = x_off + (int32_t)p.x_bytes;
+  a.shift = p.shift;
+  a.base = p.base;
+  a.top = p.top;
+  a.steps = std::max(p.steps, 1);
+  a.x0 = p.X[0];
+  a.xlast = p.X[p.n - 1];
+  return a;
+}
+
+eos_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return EOS_OK;
+  if (e == cudaErrorMemoryAllocation) return EOS_ERR_NOMEM;
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return EOS_ERR_DEVICE;
+  return EOS_ERR_CUDA;
+}
+
+#define EOS_CUDA(call)                              \
+  do {                                              \
+    cudaError_t e_ = (call);                        \
+    if (e_ != cudaSuccess) return cuda_status(e_);  \
+  } while (0)
+
+eos_status check_device(int device) {
+  int cur = -1;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return cuda_status(e);
+  return cur == device ? EOS_OK : EOS_ERR_DEVICE;
+}
+
+bool overlaps(const void* a, int64_t abytes, const void* b, int64_t bbytes) {
+  uintptr_t a0 = (uintptr_t)a, b0 = (uintptr_t)b;
+  return a0 < b0 + (uintptr_t)bbytes && b0 < a0 + (uintptr_t)abytes;
+}
+
+// Configure a kernel for `smem` bytes of dynamic shared memory and return the
+// persistent grid (#SM x resident CTAs per SM).
+eos_status configure(const void* fn, int threads, int64_t smem, int num_sms, int* grid, int* per_sm) {
+  EOS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  EOS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, (size_t)smem));
+  if (occ < 1) return EOS_ERR_UNSUPPORTED;
+  *grid = occ * num_sms;
+  if (per_sm) *per_sm = occ;
+  return EOS_OK;
+}
+
+eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* out, int64_t gofs,
+                         uint64_t* counters, cudaStream_t st) {
+  const bool cnt = counters != nullptr;
+  dv::SearchArgs a{};
+  a.image = (const uint4*)t->image_dev;
+  a.image_16 = (int32_t)(t->plan.image_bytes / 16);
+  a.ax = t->ax;
+  a.Y = Y;
+  a.out = out;
+  a.count = count;
+  a.gofs = gofs;
+  a.counters = (unsigned long long*)counters;
+  // Vector body needs Y+head 16-B aligned and out+head 8-B aligned.
+  const uintptr_t ya = (uintptr_t)Y, oa = (uintptr_t)out;
+  a.head = (ya & 15) ? 1 : 0;
+  a.vec_ok = ((ya & 7) == 0) && (((oa + 4 * (uintptr_t)a.head) & 7) == 0) && count > a.head;
+  // Do not launch more CTAs than there is work for (small batches).
+  const int64_t per_cta = (int64_t)dv::kThreads * dv::kUnroll * 2;
+  int64_t grid = std::min<int64_t>(t->grid[cnt], (count + per_cta - 1) / per_cta);
+  grid = std::max<int64_t>(grid, 1);
+  void* params[] = {&a};
+  EOS_CUDA(cudaLaunchKernel(t->fn[cnt], dim3((unsigned)grid), dim3(dv::kThreads), params,
+                            (size_t)t->plan.image_bytes, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return EOS_OK;
+}
+
+eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64_t count,
+                         double* P, int32_t* iR, int32_t* iT, cudaStream_t st) {
+  dv::Interp2DArgs a{};
+  a.image = (const uint4*)g->image_dev;
+  a.image_16 = (int32_t)(g->image_bytes / 16);
+  a.g_off = g->g_off;
+  a.r = g->ar;
+  a.t = g->at;
+  a.rho = rho;
+  a.T = T;
+  a.P = P;
+  a.iR = iR;
+  a.iT = iT;
+  a.count = count;
+  const uintptr_t al16 = (uintptr_t)rho | (uintptr_t)T | (uintptr_t)P;
+  const uintptr_t al8 = (uintptr_t)iR | (uintptr_t)iT;
+  a.vec_ok = ((al16 & 15) == 0) && ((al8 & 7) == 0);
+  const int64_t per_cta = (int64_t)dv::kThreads2D * 4;
+  int64_t grid = std::min<int64_t>(g->grid, (count + per_cta - 1) / per_cta);
+  grid = std::max<int64_t>(grid, 1);
+  void* params[] = {&a};
+  EOS_CUDA(cudaLaunchKernel(g->fn, dim3((unsigned)grid), dim3(dv::kThreads2D), params,
+                            (size_t)g->image_bytes, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return EOS_OK;
+}
+
+eos_status upload(const std::vector<uint8_t>& img, void** dev) {
+  EOS_CUDA(cudaMalloc(dev, img.size()));
+  cudaError_t e = cudaMemcpy(*dev, img.data(), img.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(*dev);
+    *dev = nullptr;
+    return cuda_status(e);
+  }
+  return EOS_OK;
+}
+
+// Two-stream chunked pipeline over host buffers: chunk c uses slot c % 2 (its
+// own stream and device staging), so H2D(c+1) overlaps search(c) / D2H(c).
+template <class Body>
+eos_status host_pipeline(cudaStream_t caller, int64_t count, int64_t chunk, int64_t bytes_per_elem,
+                         Body body) {
+  const int64_t nchunk = (count + chunk - 1) / chunk;
+  const int nslot = nchunk > 1 ? 2 : 1;
+  const int64_t slot_elems = (std::min(chunk, count) + 63) & ~int64_t(63);  // keeps 16-B alignment
+  char* stage = nullptr;
+  EOS_CUDA(cudaMallocAsync((void**)&stage, (size_t)(nslot * slot_elems * bytes_per_elem), caller));
+  cudaStream_t s[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr, ev_done[2] = {nullptr, nullptr};
+  eos_status st = EOS_OK;
+  auto fail = [&](cudaError_t e) { if (st == EOS_OK && e != cudaSuccess) st = cuda_status(e); };
+  fail(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  for (int i = 0; i < nslot && st == EOS_OK; ++i) {
+    fail(cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking));
+    fail(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
+  }
+  if (st == EOS_OK) fail(cudaEventRecord(ev_start, caller));
+  for (int i = 0; i < nslot && st == EOS_OK; ++i) fail(cudaStreamWaitEvent(s[i], ev_start, 0));
+  for (int64_t c = 0; c < nchunk && st == EOS_OK; ++c) {
+    const int slot = (int)(c % nslot);
+    const int64_t off = c * chunk;
+    const int64_t len = std::min(chunk, count - off);
+    st = body(s[slot], stage + slot * slot_elems * bytes_per_elem, slot_elems, off, len);
+  }
+  for (int i = 0; i < nslot; ++i) {
+    if (s[i] && ev_done[i]) {
+      cudaEventRecord(ev_done[i], s[i]);
+      cudaStreamWaitEvent(caller, ev_done[i], 0);
+    }
+  }
+  cudaFreeAsync(stage, caller);
+  for (int i = 0; i < nslot; ++i) {
+    if (s[i]) cudaStreamDestroy(s[i]);
+    if (ev_done[i]) cudaEventDestroy(ev_done[i]);
+  }
+  if (ev_start) cudaEventDestroy(ev_start);
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* eos_status_str(eos_status s) {
+  switch (s) {
+    case EOS_OK: return "ok";
+    case EOS_ERR_NULL: return "null pointer or handle";
+    case EOS_ERR_SIZE: return "size out of range";
+    case EOS_ERR_NONFINITE: return "table or grid value is NaN or infinite";
+    case EOS_ERR_UNSORTED: return "table not sorted (axes: not strictly increasing)";
+    case EOS_ERR_DEVICE: return "no CUDA device or wrong current device";
+    case EOS_ERR_CUDA: return "CUDA runtime error";
+    case EOS_ERR_NOMEM: return "out of memory";
+    case EOS_ERR_UNSUPPORTED: return "unsupported request";
+    case EOS_ERR_ALIAS: return "output overlaps an input";
+  }
+  return "unknown status";
+}
+
+int32_t eos_abi_version(void) { return 1; }
+
+int64_t eos_launch_count(void) { return g_launches.load(); }
+
+eos_status eos_plan_table(const double* table_host, int64_t n, int32_t k, eos_table_info_t* info,
+                          uint32_t* dir_out, int64_t cap) {
+  if (!info) return EOS_ERR_NULL;
+  TablePlan p;
+  eos_status st = eos::plan_table(table_host, n, k, false, &p);
+  if (st != EOS_OK) return st;
+  if (dir_out) {
+    if (cap < p.bins) return EOS_ERR_SIZE;
+    memcpy(dir_out, p.dir.data(), 4 * (size_t)p.bins);
+  }
+  eos::fill_info(p, info);
+  return EOS_OK;
+}
+
+eos_status eos_search_create_ex(const double* table_host, int64_t n, int32_t k, eos_table* out) {
+  if (!out) return EOS_ERR_NULL;
+  *out = nullptr;
+  eos_table t = new (std::nothrow) eos_table_s();
+  if (!t) return EOS_ERR_NOMEM;
+  eos_status st = eos::plan_table(table_host, n, k, false, &t->plan);
+  if (st != EOS_OK) { delete t; return st; }
+  cudaError_t e = cudaGetDevice(&t->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, t->device);
+  if (e != cudaSuccess) { delete t; return cuda_status(e); }
+  st = upload(eos::make_image(t->plan), &t->image_dev);
+  if (st != EOS_OK) { delete t; return st; }
+  t->ax = axis_params(t->plan, 0);
+  for (int c = 0; c < 2 && st == EOS_OK; ++c) {
+    t->fn[c] = pick_search(t->plan.key_mode, t->plan.steps, c == 1);
+    st = configure(t->fn[c], dv::kThreads, t->plan.image_bytes, t->num_sms, &t->grid[c],
+                   c == 0 ? &t->ctas_per_sm : nullptr);
+  }
+  if (st != EOS_OK) { cudaFree(t->image_dev); delete t; return st; }
+  *out = t;
+  return EOS_OK;
+}
+
+eos_status eos_search_create(const double* table_host, int64_t n, eos_table* out) {
+  return eos_search_create_ex(table_host, n, EOS_K_AUTO, out);
+}
+
+eos_status eos_search_ex(eos_table t, const double* targets_dev, int64_t count,
+                         int32_t* idx_out_dev, int64_t global_offset, uint64_t* counters_dev,
+                         void* stream) {
+  if (!t) return EOS_ERR_NULL;
+  if (count < 0 || count > (int64_t(1) << 62)) return EOS_ERR_SIZE;
+  if (count == 0) return EOS_OK;
+  if (!targets_dev || !idx_out_dev) return EOS_ERR_NULL;
+  if (overlaps(targets_dev, 8 * count, idx_out_dev, 4 * count)) return EOS_ERR_ALIAS;
+  eos_status st = check_device(t->device);
+  if (st != EOS_OK) return st;
+  return launch_search(t, targets_dev, count, idx_out_dev, global_offset, counters_dev,
+                       (cudaStream_t)stream);
+}
+
+eos_status eos_search(eos_table t, const double* targets_dev, int64_t count, int32_t* idx_out_dev,
+                      void* stream) {
+  return eos_search_ex(t, targets_dev, count, idx_out_dev, 0, nullptr, stream);
+}
+
+eos_status eos_search_host(eos_table t, const double* targets_host, int64_t count,
+                           int32_t* idx_out_host, void* stream) {
+  if (!t) return EOS_ERR_NULL;
+  if (count < 0 || count > (int64_t(1) << 62)) return EOS_ERR_SIZE;
+  if (count == 0) return EOS_OK;
+  if (!targets_host || !idx_out_host) return EOS_ERR_NULL;
+  if (overlaps(targets_host, 8 * count, idx_out_host, 4 * count)) return EOS_ERR_ALIAS;
+  eos_status st = check_device(t->device);
+  if (st != EOS_OK) return st;
+  const int64_t chunk = int64_t(1) << 23;  // 8 Mi targets: 64 MiB in + 32 MiB out per slot
+  return host_pipeline(
+      (cudaStream_t)stream, count, chunk, 12,
+      [&](cudaStream_t s, char* stage, int64_t slot_elems, int64_t off, int64_t len) -> eos_status {
+        double* dY = (double*)stage;
+        int32_t* dI = (int32_t*)(stage + 8 * slot_elems);
+        EOS_CUDA(cudaMemcpyAsync(dY, targets_host + off, 8 * len, cudaMemcpyHostToDevice, s));
+        eos_status r = launch_search(t, dY, len, dI, off, nullptr, s);
+        if (r != EOS_OK) return r;
+        EOS_CUDA(cudaMemcpyAsync(idx_out_host + off, dI, 4 * len, cudaMemcpyDeviceToHost, s));
+        return EOS_OK;
+      });
+}
+
+eos_status eos_table_info(eos_table t, eos_table_info_t* out) {
+  if (!t || !out) return EOS_ERR_NULL;
+  eos::fill_info(t->plan, out);
+  out->device = t->device;
+  out->ctas_per_sm = t->ctas_per_sm;
+  return EOS_OK;
+}
+
+eos_status eos_search_destroy(eos_table t) {
+  if (!t) return EOS_ERR_NULL;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != t->device) cudaSetDevice(t->device);
+  cudaError_t e = cudaFree(t->image_dev);  // synchronises with in-flight work
+  if (cur != t->device && cur >= 0) cudaSetDevice(cur);
+  delete t;
+  return cuda_status(e);
+}
+
+// -------------------------------------------------------------------- 2-D --
+eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double* T_host,
+                             int64_t n_T, const double* P_host, eos_grid2d* out) {
+  if (!out) return EOS_ERR_NULL;
+  *out = nullptr;
+  if (!rho_host || !T_host || !P_host) return EOS_ERR_NULL;
+  eos_grid2d g = new (std::nothrow) eos_grid2d_s();
+  if (!g) return EOS_ERR_NOMEM;
+  eos_status st = eos::plan_table(rho_host, n_rho, EOS_K_AUTO, true, &g->pr);
+  if (st == EOS_OK) st = eos::plan_table(T_host, n_T, EOS_K_AUTO, true, &g->pt);
+  if (st == EOS_OK && (g->pr.key_mode != 0 || g->pt.key_mode != 0)) st = EOS_ERR_UNSUPPORTED;
+  if (st != EOS_OK) { delete g; return st; }
+  const int64_t ncell = n_rho * n_T;
+  for (int64_t q = 0; q < ncell; ++q)
+    if (!isfinite(P_host[q])) { delete g; return EOS_ERR_NONFINITE; }
+  // image: [rho X | rho dir][T X | T dir][G]
+  const int64_t r_bytes = g->pr.image_bytes, t_bytes = g->pt.image_bytes;
+  const int64_t g_bytes = (8 * ncell + 15) & ~int64_t(15);
+  g->image_bytes = r_bytes + t_bytes + g_bytes;
+  if (g->image_bytes > 220 * 1024) { delete g; return EOS_ERR_UNSUPPORTED; }
+  std::vector<uint8_t> img((size_t)g->image_bytes, 0);
+  std::vector<uint8_t> ir = eos::make_image(g->pr), it = eos::make_image(g->pt);
+  memcpy(img.data(), ir.data(), ir.size());
+  memcpy(img.data() + r_bytes, it.data(), it.size());
+  memcpy(img.data() + r_bytes + t_bytes, P_host, 8 * (size_t)ncell);
+  g->g_off = (int32_t)(r_bytes + t_bytes);
+  g->ar = axis_params(g->pr, 0);
+  g->at = axis_params(g->pt, (int32_t)r_bytes);
+  cudaError_t e = cudaGetDevice(&g->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device);
+  if (e != cudaSuccess) { delete g; return cuda_status(e); }
+  st = upload(img, &g->image_dev);
+  if (st != EOS_OK) { delete g; return st; }
+  g->fn = pick_interp(std::max(g->pr.steps, g->pt.steps));
+  st = configure(g->fn, dv::kThreads2D, g->image_bytes, g->num_sms, &g->grid, nullptr);
+  if (st != EOS_OK) { cudaFree(g->image_dev); delete g; return st; }
+  *out = g;
+  return EOS_OK;
+}
+
+eos_status eos_interp2d(eos_grid2d g, const double* rho_dev, const double* T_dev, int64_t count,
+                        double* P_out_dev, int32_t* irho_out_dev, int32_t* iT_out_dev,
+                        void* stream) {
+  if (!g) return EOS_ERR_NULL;
+  if (count < 0 || count > (int64_t(1) << 62)) return EOS_ERR_SIZE;
+  if (count == 0) return EOS_OK;
+  if (!rho_dev || !T_dev || !P_out_dev) return EOS_ERR_NULL;
+  const void* ins[2] = {rho_dev, T_dev};
+  const void* outs[3] = {P_out_dev, irho_out_dev, iT_out_dev};
+  const int64_t ob[3] = {8 * count, 4 * count, 4 * count};
+  for (int o = 0; o < 3; ++o) {
+    if (!outs[o]) continue;
+    for (int i = 0; i < 2; ++i)
+      if (overlaps(ins[i], 8 * count, outs[o], ob[o])) return EOS_ERR_ALIAS;
+    for (int o2 = o + 1; o2 < 3; ++o2)
+      if (outs[o2] && overlaps(outs[o], ob[o], outs[o2], ob[o2])) return EOS_ERR_ALIAS;
+  }
+  eos_status st = check_device(g->device);
+  if (st != EOS_OK) return st;
+  return launch_interp(g, rho_dev, T_dev, count, P_out_dev, irho_out_dev, iT_out_dev,
+                       (cudaStream_t)stream);
+}
+
+eos_status eos_interp2d_host(eos_grid2d g, const double* rho_host, const double* T_host,
+                             int64_t count, double* P_out_host, int32_t* irho_out_host,
+                             int32_t* iT_out_host, void* stream) {
+  if (!g) return EOS_ERR_NULL;
+  if (count < 0 || count > (int64_t(1) << 62)) return EOS_ERR_SIZE;
+  if (count == 0) return EOS_OK;
+  if (!rho_host || !T_host || !P_out_host) return EOS_ERR_NULL;
+  eos_status st = check_device(g->device);
+  if (st != EOS_OK) return st;
+  const int64_t chunk = int64_t(1) << 22;
+  return host_pipeline(
+      (cudaStream_t)stream, count, chunk, 32,
+      [&](cudaStream_t s, char* stage, int64_t se, int64_t off, int64_t len) -> eos_status {
+        double* dR = (double*)stage;
+        double* dT = (double*)(stage + 8 * se);
+        double* dP = (double*)(stage + 16 * se);
+        int32_t* dI = (int32_t*)(stage + 24 * se);
+        int32_t* dJ = (int32_t*)(stage + 28 * se);
+        EOS_CUDA(cudaMemcpyAsync(dR, rho_host + off, 8 * len, cudaMemcpyHostToDevice, s));
+        EOS_CUDA(cudaMemcpyAsync(dT, T_host + off, 8 * len, cudaMemcpyHostToDevice, s));
+        eos_status r = launch_interp(g, dR, dT, len, dP, irho_out_host ? dI : nullptr,
+                                     iT_out_host ? dJ : nullptr, s);
+        if (r != EOS_OK) return r;
+        EOS_CUDA(cudaMemcpyAsync(P_out_host + off, dP, 8 * len, cudaMemcpyDeviceToHost, s));
+        if (irho_out_host)
+          EOS_CUDA(cudaMemcpyAsync(irho_out_host + off, dI, 4 * len, cudaMemcpyDeviceToHost, s));
+        if (iT_out_host)
+          EOS_CUDA(cudaMemcpyAsync(iT_out_host + off, dJ, 4 * len, cudaMemcpyDeviceToHost, s));
+        return EOS_OK;
+      });
+}
+
+eos_status eos_grid2d_info(eos_grid2d g, eos_table_info_t* rho_info, eos_table_info_t* T_info) {
+  if (!g) return EOS_ERR_NULL;
+  if (rho_info) { eos::fill_info(g->pr, rho_info); rho_info->device = g->device; }
+  if (T_info) { eos::fill_info(g->pt, T_info); T_info->device = g->device; }
+  return EOS_OK;
+}
+
+eos_status eos_grid2d_destroy(eos_grid2d g) {
+  if (!g) return EOS_ERR_NULL;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != g->device) cudaSetDevice(g->device);
+  cudaError_t e = cudaFree(g->image_dev);
+  if (cur != g->device && cur >= 0) cudaSetDevice(cur);
+  delete g;
+  return cuda_status(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,44 @@
+#!/bin/bash
+# One gpurun call: build check, GPU tests, bench, ncu launch list + full capture.
+# usage (on the GPU box): bash scripts/gpu_round.sh [stages...]  (default: all)
+set -u
+OUT=gpurun_out
+mkdir -p $OUT
+STAGES="${*:-smi smoke tests bench ncu}"
+has() { [[ " $STAGES " == *" $1 "* ]]; }
+if has smi; then
+  nvidia-smi > $OUT/smi.txt 2>&1
+  nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.limit --format=csv >> $OUT/smi.txt 2>&1
+  nproc >> $OUT/smi.txt; free -g >> $OUT/smi.txt
+fi
+if has build; then
+  timeout 900 python __graft_entry__.py > $OUT/build.log 2>&1; echo "build rc=$?"
+fi
+if has smoke; then
+  timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?"
+  tail -3 $OUT/smoke.log
+fi
+if has tests; then
+  timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $OUT/pytest_gpu.log 2>&1; echo "pytest gpu rc=$?"
+  tail -15 $OUT/pytest_gpu.log
+fi
+if has bench; then
+  timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
+  cat $OUT/bench.json; tail -5 $OUT/bench.err
+fi
+if has benchall; then
+  for wl in cfg1 cfg3 cfg4 cfg5 paper; do
+    timeout 900 python bench.py --workload $wl --steps 100 --warmup 5 --no-cpu > $OUT/bench_$wl.json 2> $OUT/bench_$wl.err; echo "bench $wl rc=$?"
+    cat $OUT/bench_$wl.json; tail -3 $OUT/bench_$wl.err
+  done
+fi
+if has ncu; then
+  CMD="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu"
+  $CMD > $OUT/ncu_plain.log 2>&1 && \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
+      --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
+  $CMD > $OUT/ncu_plain2.log 2>&1 && \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:search1d -s 5 -c 1 \
+      -o $OUT/prof_search1d -f $CMD > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"
+  tail -3 $OUT/ncu_full.log
+fi

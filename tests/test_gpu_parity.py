@@ -1,0 +1,407 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle (-m gpu).
+
+Indices must be bit-identical to the oracle; interpolated values within
+1e-12 relative (BASELINE.json north_star).  Oracle inputs always come from
+the host generators (datagen host side), never from the device; the device
+generators are proven bit-identical to the host ones first.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2112_03229_b200 as eos  # noqa: E402
+from tests._golden import interp_cases, lower_bound_cases  # noqa: E402
+
+DEV = torch.device("cuda:0")
+REL_TOL = 1e-12  # north_star: "within 1e-12 relative for fp64 interpolated values"
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def gpu_search(X, Y, k=None, **kw):
+    t = eos.Table(X, k=k)
+    out = t.search(to_dev(Y), **kw)
+    torch.cuda.synchronize()
+    r = out.cpu().numpy()
+    t.close()
+    return r
+
+
+def assert_same(got, ref, Y=None):
+    bad = np.flatnonzero(got != ref)
+    if bad.size:
+        i = bad[:8]
+        raise AssertionError(f"{bad.size} mismatches; first at {i}: gpu {got[i]} oracle {ref[i]}"
+                             + (f" y {Y[i]}" if Y is not None else ""))
+
+
+def feasible_ks(X, ks):
+    out = []
+    for k in ks:
+        try:
+            eos.plan_table(X, k, with_directory=False)
+            out.append(k)
+        except eos.EosError:
+            pass
+    return out
+
+
+# --------------------------------------------------------------- smoke -----
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()
+
+
+# ----------------------------------------------------------- generators ----
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5", "paper"])
+def test_device_generators_bit_identical_to_host(name):
+    w = datagen.workload(name, count=300_001)
+    for off in (0, 12_345):
+        n = w.count - off
+        d = torch.empty(n, dtype=torch.float64, device=DEV)
+        tab = to_dev(w.table)
+        w.targets.device_fill(d, off, table_dev=tab)
+        h = w.targets.host_fill(off, n, w.table)
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy().view(np.uint64), h.view(np.uint64))
+
+
+def test_device_generators_cfg4():
+    w = datagen.workload("cfg4", count=100_000)
+    for spec in (w.rho_targets, w.T_targets):
+        d = torch.empty(w.count, dtype=torch.float64, device=DEV)
+        spec.device_fill(d, 0)
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy(), spec.host_fill(0, w.count))
+
+
+# ------------------------------------------------------------ 1-D parity ---
+@pytest.mark.parametrize("name", sorted(lower_bound_cases().keys()))
+def test_golden_cases_every_k(name):
+    X, cases = lower_bound_cases()[name]
+    ys = np.array([c[0] for c in cases] * 37)  # repeated: crosses the vector body and tail
+    exp = np.array([c[1] for c in cases] * 37, dtype=np.int32)
+    for k in feasible_ks(X, [None, 0, 1, 2, 4, 8, 12, 20]):
+        assert_same(gpu_search(X, ys, k=k), exp, ys)
+
+
+def _edge_tables(rng, count):
+    for t in range(count):
+        n = int(rng.integers(1, 14))
+        kind = t % 7
+        if kind == 0:
+            X = 10.0 ** rng.uniform(-8, 8, n)
+        elif kind == 1:
+            X = 2.0 ** rng.integers(-20, 20, n).astype(np.float64)
+        elif kind == 2:
+            X = np.concatenate([[0.0], rng.uniform(0, 1, n) * 1e-310, 10.0 ** rng.uniform(-5, 5, n)])
+        elif kind == 3:
+            X = np.round(rng.uniform(1.0, 1.01, n), 3)
+        elif kind == 4:
+            X = np.concatenate([rng.normal(0, 10, n), [0.0, -0.0]])
+        elif kind == 5:
+            X = rng.choice([1.0, 2.0, 3.0], n)
+        else:
+            X = -(10.0 ** rng.uniform(-3, 3, n))
+        yield np.sort(X)
+
+
+def _probes(X):
+    p = [0.0, -0.0, math.inf, -math.inf, math.nan, 5e-324, 2.2250738585072014e-308, 1e-300,
+         1e300, -1.0, 1.0, 2.0, 0.5, -1e-310]
+    for x in X:
+        p += [x, math.nextafter(x, math.inf), math.nextafter(x, -math.inf)]
+        if x != 0:
+            e = math.floor(math.log2(abs(x)))
+            p += [math.copysign(2.0 ** e, x), math.nextafter(math.copysign(2.0 ** e, x), 0.0)]
+    for a, b in zip(X[:-1], X[1:]):
+        p.append(0.5 * (a + b))
+    return np.array(p)
+
+
+def test_edge_tables_exhaustive_probes_every_k():
+    rng = np.random.default_rng(2024)
+    checked = 0
+    for X in _edge_tables(rng, 140):
+        P = _probes(X)
+        P = np.concatenate([P, rng.permutation(np.repeat(P, 5))])
+        ref = oracle.search(X, P)
+        for k in feasible_ks(X, [None, 0, 1, 3, 6, 10]):
+            assert_same(gpu_search(X, P, k=k), ref, P)
+            checked += P.size
+    assert checked > 100_000
+
+
+def test_cfg1_full_every_k():
+    w = datagen.workload("cfg1")
+    Y = w.targets.host_fill(0, w.count, w.table)
+    ref = oracle.search(w.table, Y)
+    for k in feasible_ks(w.table, [None] + list(range(0, 16))):
+        assert_same(gpu_search(w.table, Y, k=k), ref, Y)
+
+
+@pytest.mark.parametrize("count", [0, 1, 2, 3, 5, 511, 2047, 2048, 2049, 4097, 65_537, 1_000_003])
+@pytest.mark.parametrize("y_off,o_off", [(0, 0), (1, 0), (0, 1), (1, 1), (3, 2)])
+def test_ragged_and_misaligned(count, y_off, o_off):
+    w = datagen.workload("cfg2", count=count + 8)
+    Yall = w.targets.host_fill(0, count + 8, w.table)
+    yd = to_dev(Yall)[y_off:y_off + count]
+    od_all = torch.full((count + 8,), -7, dtype=torch.int32, device=DEV)
+    od = od_all[o_off:o_off + count]
+    t = eos.Table(w.table)
+    t.search(yd, out=od)
+    torch.cuda.synchronize()
+    got = od_all.cpu().numpy()
+    assert_same(got[o_off:o_off + count], oracle.search(w.table, Yall[y_off:y_off + count]))
+    assert np.all(got[:o_off] == -7) and np.all(got[o_off + count:] == -7)  # no stray writes
+    t.close()
+
+
+def test_counters_match_oracle():
+    w = datagen.workload("cfg1", count=777_777)
+    Y = w.targets.host_fill(0, w.count, w.table)
+    Y[::1001] = np.nan
+    Y[3::5003] = np.inf
+    off = 5_000_000_000
+    ref_idx = oracle.search(w.table, Y)
+    ref = oracle.counters(w.table, Y, ref_idx, off)
+    t = eos.Table(w.table)
+    c = torch.zeros(8, dtype=torch.int64, device=DEV)
+    idx = t.search(to_dev(Y), counters=c, global_offset=off)
+    torch.cuda.synchronize()
+    assert_same(idx.cpu().numpy(), ref_idx)
+    assert np.array_equal(c.cpu().numpy().view(np.uint64), ref)
+    # accumulation over two shards == whole
+    c2 = torch.zeros(8, dtype=torch.int64, device=DEV)
+    yd = to_dev(Y)
+    h = 300_001
+    t.search(yd[:h], counters=c2, global_offset=off)
+    t.search(yd[h:], counters=c2, global_offset=off + h)
+    torch.cuda.synchronize()
+    assert np.array_equal(c2.cpu().numpy().view(np.uint64), ref)
+    t.close()
+
+
+def test_errors_are_reported():
+    t = eos.Table([1.0, 2.0, 3.0])
+    y = torch.ones(16, dtype=torch.float64, device=DEV)
+    with pytest.raises(eos.EosError) as e:   # output aliasing the input
+        eos.eos_search(t.handle, y.data_ptr(), 16, y.data_ptr() + 8, 0)
+    assert e.value.code == 9
+    with pytest.raises(eos.EosError) as e:
+        eos.eos_search(t.handle, 0, 16, y.data_ptr(), 0)
+    assert e.value.code == 1
+    with pytest.raises(eos.EosError) as e:
+        eos.eos_search(t.handle, y.data_ptr(), -1, y.data_ptr(), 0)
+    assert e.value.code == 2
+    eos.eos_search(t.handle, 0, 0, 0, 0)  # count == 0: no-op
+    with pytest.raises(eos.EosError):
+        eos.Table([2.0, 1.0])
+    n0 = eos.launch_count()
+    t.search(y)
+    assert eos.launch_count() == n0 + 1
+    t.close()
+
+
+# -------------------------------------------------------- full configs -----
+def invariant_on_device(Xd, Yd, Id, chunk=1 << 26):
+    """P:54 bracketing on every output: X[i] <= y < X[i+1] (or i = n-1); y < X[0] / NaN -> 0."""
+    n = Xd.numel()
+    for s in range(0, Yd.numel(), chunk):
+        y = Yd[s:s + chunk]
+        i = Id[s:s + chunk].long()
+        assert int(i.min()) >= 0 and int(i.max()) <= n - 1
+        inr = y >= Xd[0]
+        assert bool((i[~inr] == 0).all())
+        yi, ii = y[inr], i[inr]
+        assert bool((Xd[ii] <= yi).all())
+        assert bool(((ii == n - 1) | (yi < Xd[torch.clamp(ii + 1, max=n - 1)])).all())
+
+
+def test_cfg2_full_bit_exact():
+    w = datagen.workload("cfg2")
+    Yh = w.targets.host_fill(0, w.count, w.table)
+    ref = oracle.search(w.table, Yh)
+    Yd = torch.empty(w.count, dtype=torch.float64, device=DEV)
+    w.targets.device_fill(Yd, 0)
+    t = eos.Table(w.table)
+    out = t.search(Yd)
+    torch.cuda.synchronize()
+    assert_same(out.cpu().numpy(), ref)
+    t.close()
+
+
+def _sampled_check(w, Yd, out, nsample=1 << 20, seed=0):
+    idx = np.sort(np.random.default_rng(seed).integers(0, w.count, nsample))
+    idx[:2] = [0, w.count - 1]
+    idx = np.sort(idx)
+    Ys = w.targets.host_sample(idx, w.table)
+    ref = oracle.search(w.table, Ys)
+    got = out[torch.from_numpy(idx).to(DEV)].cpu().numpy()
+    assert_same(got, ref, Ys)
+    # the device stream really is the host stream at those positions
+    assert np.array_equal(Yd[torch.from_numpy(idx).to(DEV)].cpu().numpy(), Ys)
+
+
+def test_cfg3_full_sampled_and_invariant():
+    w = datagen.workload("cfg3")
+    Yd = torch.empty(w.count, dtype=torch.float64, device=DEV)
+    w.targets.device_fill(Yd, 0)
+    t = eos.Table(w.table)
+    out = t.search(Yd)
+    torch.cuda.synchronize()
+    _sampled_check(w, Yd, out)
+    invariant_on_device(to_dev(w.table), Yd, out)
+    # k-invariance on a 2^27 slice: the paper's pure exponent hash (k=0) gives the same indices
+    t0 = eos.Table(w.table, k=0)
+    s = Yd[:1 << 27]
+    assert torch.equal(t0.search(s), out[:1 << 27])
+    t.close()
+    t0.close()
+
+
+def test_cfg5_full_sampled_invariant_counters():
+    w = datagen.workload("cfg5")
+    Yd = torch.empty(w.count, dtype=torch.float64, device=DEV)
+    w.targets.device_fill(Yd, 0)
+    t = eos.Table(w.table)
+    out = torch.empty(w.count, dtype=torch.int32, device=DEV)
+    t.search(Yd, out=out)
+    torch.cuda.synchronize()
+    _sampled_check(w, Yd, out, nsample=1 << 21, seed=5)
+    Xd = to_dev(w.table)
+    invariant_on_device(Xd, Yd, out)
+    # counters of a validation launch over a 2^26 shard in the middle == oracle counters there
+    off = 5 << 30
+    m = 1 << 26
+    c = torch.zeros(8, dtype=torch.int64, device=DEV)
+    t.search(Yd[off:off + m], out=torch.empty(m, dtype=torch.int32, device=DEV), counters=c,
+             global_offset=off)
+    Yh = w.targets.host_fill(off, m, w.table)
+    ref = oracle.counters(w.table, Yh, oracle.search(w.table, Yh), off)
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy().view(np.uint64), ref)
+    for k in (0, 9):
+        tk = eos.Table(w.table, k=k)
+        assert torch.equal(tk.search(Yd[off:off + m]), out[off:off + m])
+        tk.close()
+    t.close()
+    del Yd, out
+
+
+# ------------------------------------------------------------------ 2-D ----
+def check_interp(Pg, Pr):
+    nan_g, nan_r = np.isnan(Pg), np.isnan(Pr)
+    assert np.array_equal(nan_g, nan_r)
+    ok = ~nan_r
+    err = np.abs(Pg[ok] - Pr[ok])
+    tol = REL_TOL * np.abs(Pr[ok])
+    assert np.all(err <= tol), float(np.max(err / np.maximum(np.abs(Pr[ok]), 1e-300)))
+    return float(np.max(err / np.maximum(np.abs(Pr[ok]), 1e-300))) if ok.any() else 0.0
+
+
+def test_interp_golden():
+    R, T, G, cases = interp_cases()
+    rho = np.array([c[0] for c in cases] * 300)
+    tt = np.array([c[1] for c in cases] * 300)
+    g = eos.Grid2D(R, T, G)
+    P, iR, iT = g.interp(to_dev(rho), to_dev(tt))
+    torch.cuda.synchronize()
+    assert np.array_equal(P.cpu().numpy(), np.array([c[2] for c in cases] * 300))
+    assert np.array_equal(iR.cpu().numpy(), np.array([c[3] for c in cases] * 300))
+    assert np.array_equal(iT.cpu().numpy(), np.array([c[4] for c in cases] * 300))
+    g.close()
+
+
+def test_interp_random_grids_edges():
+    rng = np.random.default_rng(11)
+    for t in range(25):
+        nr, nt = int(rng.integers(2, 60)), int(rng.integers(2, 60))
+        R = np.unique(10.0 ** rng.uniform(-6, 3, nr))
+        T = np.unique(10.0 ** rng.uniform(0, 8, nt))
+        if R.size < 2 or T.size < 2:
+            continue
+        G = rng.uniform(-5, 5, (R.size, T.size)) if t % 2 else rng.uniform(0.5, 5, (R.size, T.size))
+        m = 20_011
+        rho = 10.0 ** rng.uniform(-7, 4, m)
+        tt = 10.0 ** rng.uniform(-1, 9, m)
+        rho[:R.size] = R
+        tt[:T.size] = T
+        rho[-5:] = [np.nan, np.inf, -np.inf, 0.0, -1.0]
+        g = eos.Grid2D(R, T, G)
+        P, iR, iT = g.interp(to_dev(rho), to_dev(tt))
+        torch.cuda.synchronize()
+        Pr, iRr, iTr = oracle.interp2d(R, T, G, rho, tt)
+        assert np.array_equal(iR.cpu().numpy(), iRr) and np.array_equal(iT.cpu().numpy(), iTr)
+        Pg = P.cpu().numpy()
+        if t % 2:   # signed grid: cancellation -> compare against the corner scale
+            ok = ~np.isnan(Pr)
+            assert np.array_equal(np.isnan(Pg), ~ok)
+            assert np.all(np.abs(Pg[ok] - Pr[ok]) <= REL_TOL * np.abs(G).max())
+        else:
+            check_interp(Pg, Pr)
+        g.close()
+
+
+def test_interp_cfg4_sampled_full_and_prefix_exact():
+    w = datagen.workload("cfg4")
+    rd = torch.empty(w.count, dtype=torch.float64, device=DEV)
+    td = torch.empty(w.count, dtype=torch.float64, device=DEV)
+    w.rho_targets.device_fill(rd, 0)
+    w.T_targets.device_fill(td, 0)
+    g = eos.Grid2D(w.rho, w.T, w.P)
+    P, iR, iT = g.interp(rd, td)
+    torch.cuda.synchronize()
+    # full 2^22 prefix against the oracle
+    m = 1 << 22
+    rh = w.rho_targets.host_fill(0, m)
+    th = w.T_targets.host_fill(0, m)
+    Pr, iRr, iTr = oracle.interp2d(w.rho, w.T, w.P, rh, th)
+    assert np.array_equal(iR[:m].cpu().numpy(), iRr) and np.array_equal(iT[:m].cpu().numpy(), iTr)
+    check_interp(P[:m].cpu().numpy(), Pr)
+    # sampled over the whole 2^28 stream
+    idx = np.sort(np.random.default_rng(3).integers(0, w.count, 1 << 20))
+    rs, ts = w.rho_targets.host_sample(idx), w.T_targets.host_sample(idx)
+    Pr, iRr, iTr = oracle.interp2d(w.rho, w.T, w.P, rs, ts)
+    di = torch.from_numpy(idx).to(DEV)
+    assert np.array_equal(iR[di].cpu().numpy(), iRr) and np.array_equal(iT[di].cpu().numpy(), iTr)
+    check_interp(P[di].cpu().numpy(), Pr)
+    g.close()
+
+
+# ------------------------------------------------------- host end-to-end ---
+def test_search_host_pipeline_matches():
+    w = datagen.workload("cfg2", count=(1 << 25) + 12345)
+    Y = torch.from_numpy(w.targets.host_fill(0, w.count, w.table)).pin_memory()
+    out = torch.empty(w.count, dtype=torch.int32).pin_memory()
+    t = eos.Table(w.table)
+    t.search_host(Y.numpy(), out)
+    assert_same(out.numpy(), oracle.search(w.table, Y.numpy()))
+    # pageable buffers work too
+    small = w.targets.host_fill(0, 100_003, w.table)
+    assert_same(t.search_host(small), oracle.search(w.table, small))
+    t.close()
+
+
+def test_interp_host_pipeline_matches():
+    w = datagen.workload("cfg4", count=(1 << 23) + 3)
+    rh = w.rho_targets.host_fill(0, w.count)
+    th = w.T_targets.host_fill(0, w.count)
+    g = eos.Grid2D(w.rho, w.T, w.P)
+    P, iR, iT = g.interp_host(rh, th)
+    Pr, iRr, iTr = oracle.interp2d(w.rho, w.T, w.P, rh, th)
+    assert np.array_equal(iR, iRr) and np.array_equal(iT, iTr)
+    check_interp(P, Pr)
+    g.close()

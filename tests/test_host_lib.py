@@ -1,0 +1,217 @@
+"""Host-side logic of libeossearch.so, no GPU needed (-m "not gpu").
+
+The library must load and export every symbol include/eossearch.h declares,
+and eos_plan_table (validation, bin key, count directory, k choice) is
+checked here against independent derivations (math.frexp exponents, brute
+recounts, the oracle's answers, the paper's printed bin statistics).
+"""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2112_03229_b200 as eos
+from paper_2112_03229_b200 import _build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    _build.build()
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "eossearch.h")).read()
+    return set(re.findall(r"^EOS_API\s+[\w\s\*]+?\b(eos_\w+)\(", src, flags=re.M))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    L = eos.load_library()
+    declared = header_symbols()
+    assert len(declared) >= 16
+    assert declared == set(eos.EXPORTED_SYMBOLS)
+    for s in declared:
+        assert hasattr(L, s), s
+    assert L.eos_abi_version() == 1
+    assert eos.eos_status_str(0) == "ok"
+    assert "sorted" in eos.eos_status_str(4)
+
+
+def test_sm100a_cubin_embedded():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _build.LIB],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+# ---------------------------------------------------------------- plan -----
+def fine_index_frexp(x: float, k: int) -> int:
+    """Independent bin index of a positive normal x: e*2^k + floor((m-1)*2^k), x = m*2^e."""
+    f, E = math.frexp(x)
+    m, e = 2.0 * f, E - 1
+    return e * (1 << k) + int(math.floor((m - 1.0) * (1 << k)))
+
+
+def unpack(d):
+    return (d & 0xFFFF).astype(np.int64), (d >> 16).astype(np.int64)
+
+
+def random_positive_tables(rng, count):
+    for t in range(count):
+        n = int(rng.integers(1, 400))
+        if t % 3 == 0:
+            X = 10.0 ** rng.uniform(-8, 8, n)
+        elif t % 3 == 1:
+            X = 2.0 ** rng.integers(-30, 30, n).astype(np.float64)
+        else:
+            X = np.round(10.0 ** rng.uniform(0, 1, n), 2)
+        yield np.sort(X)
+
+
+def test_directory_invariants_and_recount():
+    rng = np.random.default_rng(0)
+    for X in random_positive_tables(rng, 60):
+        for k in range(0, 11):
+            fi = np.array([fine_index_frexp(x, k) for x in X])
+            try:
+                info, d = eos.plan_table(X, k)
+            except eos.EosError as e:   # directory would not fit in shared memory
+                assert e.code == 8 and 8 * X.size + 4 * (fi[-1] - fi[0] + 1) > 200 * 1024
+                continue
+            lo, occ = unpack(d)
+            assert info.bins == d.size and info.k == k and info.key_mode == 0
+            assert lo[0] == 0 and lo[-1] + occ[-1] == X.size
+            assert np.all(lo[1:] == lo[:-1] + occ[:-1])
+            assert info.max_occ == occ.max()
+            assert info.steps == math.ceil(math.log2(info.max_occ + 1))
+            # recount with the frexp-derived fine index
+            assert info.bins == fi[-1] - fi[0] + 1
+            cnt = np.bincount(fi - fi[0], minlength=info.bins)
+            assert np.array_equal(cnt, occ)
+
+
+def test_k0_is_the_paper_exponent_hash():
+    """k = 0: bins are the binary exponents spanned; bin id = floor(log2 x) - e_min."""
+    X = np.sort(10.0 ** np.random.default_rng(1).uniform(-6, 6, 500))
+    info, d = eos.plan_table(X, 0)
+    e = np.array([math.frexp(x)[1] - 1 for x in X])
+    assert np.array_equal(e, np.floor(np.log2(X)).astype(int))
+    assert info.bins == e.max() - e.min() + 1
+    assert np.array_equal(unpack(d)[1], np.bincount(e - e.min(), minlength=info.bins))
+
+
+def test_paper_exemplar_bin_statistics():
+    """a log-distributed table over 3e-6..5.4e4 spans 'about 34 powers of 2', giving
+    '110/34 = 3.235' entries per bin.  The exponent hash (k=0) gives 35 bins here."""
+    import datagen
+    X = datagen.table_paper_exemplar()
+    info, d = eos.plan_table(X, 0)
+    assert info.bins in (34, 35)
+    assert 3.0 <= X.size / info.bins <= 3.5
+    assert info.bins == 35 and abs(X.size / info.bins - 3.14) < 0.01
+
+
+def _bin_of(y, info, X):
+    """bin of target y under mode 0 (test-side restatement, for the bracketing check)."""
+    hi = (np.array([y]).view(np.uint64)[0] >> np.uint64(32)) & np.uint64(0x7FFFFFFF)
+    kb = int(hi) >> (20 - info.k)
+    xlo = X[X > 0][0] if np.any(X > 0) else X[-1]
+    base = (int(np.array([xlo]).view(np.uint64)[0] >> np.uint64(32)) & 0x7FFFFFFF) >> (20 - info.k)
+    return min(max(kb, base), base + info.bins - 1) - base
+
+
+def test_directory_brackets_the_oracle_answer():
+    """For every in-range target the oracle's count lies inside the target's bin range
+    [lo_b, lo_b + occ_b] (SPEC 'Bracketing' property), at every k."""
+    import datagen
+    for name in ("cfg1", "cfg2", "cfg3", "cfg5"):
+        w = datagen.workload(name, count=3000)
+        X = w.table
+        Y = w.targets.host_fill(0, w.count, X)
+        Y = np.concatenate([Y, X, np.nextafter(X, 0), np.nextafter(X, np.inf)])
+        ref = oracle.search(X, Y)
+        for k in (0, 2, 5, 9):
+            info, d = eos.plan_table(X, k)
+            lo, occ = unpack(d)
+            for y, r in zip(Y, ref):
+                if not (y >= X[0]):
+                    continue
+                b = _bin_of(y, info, X)
+                assert lo[b] <= r + 1 <= lo[b] + occ[b], (name, k, y)
+
+
+def test_auto_k_reaches_short_searches_on_configs():
+    import datagen
+    chosen = {}
+    for name in ("cfg1", "cfg2", "cfg3", "cfg5", "paper"):
+        X = datagen.workload(name, count=1).table
+        info, _ = eos.plan_table(X)
+        chosen[name] = (info.k, info.bins, info.steps, info.image_bytes)
+        assert info.image_bytes <= 100 * 1024 or info.k == 0
+    assert chosen["cfg2"][2] == 1 and chosen["cfg3"][2] == 1
+    assert chosen["cfg5"][2] <= 4
+    rho, T, _ = datagen.grid_cfg4()
+    for ax in (rho, T):
+        assert eos.plan_table(ax)[0].steps == 1
+
+
+def test_validation_status_codes():
+    def code(X, k=eos.EOS_K_AUTO):
+        try:
+            eos.plan_table(np.asarray(X, dtype=np.float64), k)
+            return 0
+        except eos.EosError as e:
+            return e.code
+    assert code([]) == 2
+    assert code(np.arange(eos.EOS_MAX_TABLE + 1, dtype=float)) == 2
+    assert code(np.arange(eos.EOS_MAX_TABLE, dtype=float)) == 0
+    assert code([1.0, np.nan]) == 3
+    assert code([1.0, np.inf]) == 3
+    assert code([2.0, 1.0]) == 4
+    assert code([1.0, 1.0, 1.0]) == 0            # duplicates allowed
+    assert code([1.0, 2.0], k=21) == 8
+    assert code([1.0, 2.0], k=-2) == 8
+    assert code([7.0]) == 0                       # n = 1
+    with pytest.raises(eos.EosError) as ei:
+        L = eos.load_library()
+        X = np.array([1.0, 2.0, 4.0])
+        info = eos.TableInfo()
+        d = np.zeros(1, np.uint32)
+        r = L.eos_plan_table(X.ctypes.data, 3, 0, __import__("ctypes").byref(info), d.ctypes.data, 1)
+        eos._check(r, "cap")
+    assert ei.value.code == 2
+
+
+def test_key_modes_and_degenerate_tables():
+    info, d = eos.plan_table([-2.0, -0.5, 0.0, 0.5])
+    assert info.key_mode == 1
+    info, d = eos.plan_table([-0.0, 1.0, 2.0])     # -0.0 canonicalised -> mode 0
+    assert info.key_mode == 0
+    info, d = eos.plan_table([0.0, 0.0])           # all zeros: one bin
+    assert info.bins == 1 and info.max_occ == 2
+    info, d = eos.plan_table([0.0, 5e-324, 1e-310, 2.2250738585072014e-308, 1.0], 0)
+    lo, occ = unpack(d)
+    assert lo[0] == 0 and occ.sum() == 5
+    # a table of 16384 equal values: one bin holding everything (16-bit occ field)
+    info, d = eos.plan_table(np.full(eos.EOS_MAX_TABLE, 3.0))
+    assert info.max_occ == eos.EOS_MAX_TABLE and info.steps == 15
+
+
+def test_mode1_directory_monotone_over_mixed_signs():
+    rng = np.random.default_rng(5)
+    for _ in range(30):
+        X = np.sort(rng.normal(0, 100, int(rng.integers(2, 300))))
+        for k in (0, 3, 8):
+            try:
+                info, d = eos.plan_table(X, k)
+            except eos.EosError as e:   # a sign-crossing key spans ~2046 exponents per 2^k
+                assert e.code == 8 and k > 0
+                continue
+            lo, occ = unpack(d)
+            assert info.key_mode == 1
+            assert lo[0] == 0 and lo[-1] + occ[-1] == X.size
+            assert np.all(lo[1:] == lo[:-1] + occ[:-1])
