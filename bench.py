@@ -134,41 +134,7 @@ class ClockSampler:
 
 
 # --------------------------------------------------------- distributed -----
-class Dist:
-    def __init__(self):
-        self.world = int(os.environ.get("WORLD_SIZE", "1"))
-        self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.pg = None
-
-    def init(self, backend="nccl"):
-        if self.world > 1:
-            import torch.distributed as dist
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group(backend)
-            self.pg = dist
-
-    def barrier(self):
-        if self.pg:
-            import torch
-            self.pg.barrier(device_ids=[torch.cuda.current_device()]) if torch.cuda.is_available() \
-                else self.pg.barrier()
-
-    def allreduce(self, t, op="max"):
-        if self.pg:
-            self.pg.all_reduce(t, op=getattr(self.pg.ReduceOp, op.upper()))
-        return t
-
-    def close(self):
-        if self.pg:
-            self.pg.destroy_process_group()
-
-
-def shard(total: int, world: int, rank: int):
-    """Contiguous block sharding: rank r takes [r*total/world, (r+1)*total/world)."""
-    lo = total * rank // world
-    hi = total * (rank + 1) // world
-    return lo, hi - lo
+from paper_2112_03229_b200.dist import Dist, counters_to_u64, shard  # noqa: E402
 
 
 # ------------------------------------------------------------ our arm ------
@@ -250,8 +216,8 @@ def run_ours(a, d: Dist):
     if not is2d:
         c = torch.zeros(8, dtype=torch.int64, device=dev)
         obj.search(Y, out=out, counters=c, global_offset=offset)
-        d.allreduce(c, "sum")
-        counters = [int(x) & 0xFFFFFFFFFFFFFFFF for x in c.cpu().tolist()]
+        d.reduce_counters(c)
+        counters = counters_to_u64(c.cpu().tolist())
 
     # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None

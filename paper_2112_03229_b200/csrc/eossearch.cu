@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -29,6 +30,9 @@ struct eos_table_s {
   // launch configuration per counters on/off
   const void* fn[2] = {nullptr, nullptr};
   int grid[2] = {0, 0};
+  int threads[2] = {dv::kThreads, dv::kThreads};
+  int unroll[2] = {dv::kUnroll, dv::kUnroll};
+  bool persistent[2] = {true, true};
   int ctas_per_sm = 0;
 };
 
@@ -47,30 +51,64 @@ struct eos_grid2d_s {
 namespace {
 
 // ---------------------------------------------------------- kernel table ---
-template <int S, int MODE>
+template <int S, int MODE, class SH>
 const void* search_fn(bool cnt) {
-  return cnt ? (const void*)dv::search1d_kernel<S, MODE, true>
-             : (const void*)dv::search1d_kernel<S, MODE, false>;
+  return cnt ? (const void*)dv::search1d_kernel<S, MODE, true, SH>
+             : (const void*)dv::search1d_kernel<S, MODE, false, SH>;
 }
 
-template <int MODE>
+template <int MODE, class SH>
 const void* search_fn_mode(int steps, bool cnt) {
   switch (steps) {
-    case 1: return search_fn<1, MODE>(cnt);
-    case 2: return search_fn<2, MODE>(cnt);
-    case 3: return search_fn<3, MODE>(cnt);
-    case 4: return search_fn<4, MODE>(cnt);
-    case 5: return search_fn<5, MODE>(cnt);
-    case 6: return search_fn<6, MODE>(cnt);
-    case 7: return search_fn<7, MODE>(cnt);
-    case 8: return search_fn<8, MODE>(cnt);
-    default: return search_fn<0, MODE>(cnt);  // runtime S
+    case 1: return search_fn<1, MODE, SH>(cnt);
+    case 2: return search_fn<2, MODE, SH>(cnt);
+    case 3: return search_fn<3, MODE, SH>(cnt);
+    case 4: return search_fn<4, MODE, SH>(cnt);
+    case 5: return search_fn<5, MODE, SH>(cnt);
+    case 6: return search_fn<6, MODE, SH>(cnt);
+    case 7: return search_fn<7, MODE, SH>(cnt);
+    case 8: return search_fn<8, MODE, SH>(cnt);
+    default: return search_fn<0, MODE, SH>(cnt);  // runtime S
   }
 }
 
 const void* pick_search(int mode, int steps, bool cnt) {
-  return mode == 0 ? search_fn_mode<0>(steps, cnt) : search_fn_mode<1>(steps, cnt);
+  return mode == 0 ? search_fn_mode<0, dv::DefaultShape>(steps, cnt)
+                   : search_fn_mode<1, dv::DefaultShape>(steps, cnt);
 }
+
+// Launch-shape variants for tuning experiments (EOS_SEARCH_VARIANT=<name> at
+// create time; mode 0, S <= 4, no counters).  Not part of the C ABI.
+struct Variant {
+  const char* name;
+  int threads, unroll;
+  bool persistent;
+  const void* (*get)(int steps);
+};
+
+template <class SH>
+const void* variant_fn(int steps) {
+  switch (steps) {
+    case 1: return (const void*)dv::search1d_kernel<1, 0, false, SH>;
+    case 2: return (const void*)dv::search1d_kernel<2, 0, false, SH>;
+    case 3: return (const void*)dv::search1d_kernel<3, 0, false, SH>;
+    case 4: return (const void*)dv::search1d_kernel<4, 0, false, SH>;
+    default: return nullptr;
+  }
+}
+
+const Variant kVariants[] = {
+    {"t256u4", 256, 4, true, variant_fn<dv::Shape<256, 4, 4, false>>},
+    {"t256u4np", 256, 4, false, variant_fn<dv::Shape<256, 4, 4, false>>},
+    {"t256u8", 256, 8, true, variant_fn<dv::Shape<256, 8, 4, false>>},
+    {"t256u4pf", 256, 4, true, variant_fn<dv::Shape<256, 4, 4, true>>},
+    {"t256u8pf", 256, 8, true, variant_fn<dv::Shape<256, 8, 3, true>>},
+    {"t512u4", 512, 4, true, variant_fn<dv::Shape<512, 4, 2, false>>},
+    {"t512u2", 512, 2, true, variant_fn<dv::Shape<512, 2, 2, false>>},
+    {"t128u8", 128, 8, true, variant_fn<dv::Shape<128, 8, 8, false>>},
+    {"t256u2", 256, 2, true, variant_fn<dv::Shape<256, 2, 4, false>>},
+    {"t256u8np", 256, 8, false, variant_fn<dv::Shape<256, 8, 4, false>>},
+};
 
 const void* pick_interp(int steps) {
   switch (steps) {
@@ -149,12 +187,13 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
   const uintptr_t ya = (uintptr_t)Y, oa = (uintptr_t)out;
   a.head = (ya & 15) ? 1 : 0;
   a.vec_ok = ((ya & 7) == 0) && (((oa + 4 * (uintptr_t)a.head) & 7) == 0) && count > a.head;
-  // Do not launch more CTAs than there is work for (small batches).
-  const int64_t per_cta = (int64_t)dv::kThreads * dv::kUnroll * 2;
-  int64_t grid = std::min<int64_t>(t->grid[cnt], (count + per_cta - 1) / per_cta);
-  grid = std::max<int64_t>(grid, 1);
+  // Persistent grid, but never more CTAs than there are tiles (small batches).
+  const int64_t per_cta = (int64_t)t->threads[cnt] * t->unroll[cnt] * 2;
+  const int64_t tiles = (count + per_cta - 1) / per_cta;
+  int64_t grid = t->persistent[cnt] ? std::min<int64_t>(t->grid[cnt], tiles) : tiles;
+  grid = std::max<int64_t>(std::min<int64_t>(grid, 0x7FFFFFFF), 1);
   void* params[] = {&a};
-  EOS_CUDA(cudaLaunchKernel(t->fn[cnt], dim3((unsigned)grid), dim3(dv::kThreads), params,
+  EOS_CUDA(cudaLaunchKernel(t->fn[cnt], dim3((unsigned)grid), dim3(t->threads[cnt]), params,
                             (size_t)t->plan.image_bytes, st));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return EOS_OK;
@@ -293,7 +332,19 @@ eos_status eos_search_create_ex(const double* table_host, int64_t n, int32_t k, 
   t->ax = axis_params(t->plan, 0);
   for (int c = 0; c < 2 && st == EOS_OK; ++c) {
     t->fn[c] = pick_search(t->plan.key_mode, t->plan.steps, c == 1);
-    st = configure(t->fn[c], dv::kThreads, t->plan.image_bytes, t->num_sms, &t->grid[c],
+    if (c == 0) {
+      const char* want = getenv("EOS_SEARCH_VARIANT");
+      for (const Variant& v : kVariants) {
+        if (!want || strcmp(want, v.name) != 0 || t->plan.key_mode != 0) continue;
+        const void* f = v.get(t->plan.steps);
+        if (!f) break;
+        t->fn[0] = f;
+        t->threads[0] = v.threads;
+        t->unroll[0] = v.unroll;
+        t->persistent[0] = v.persistent;
+      }
+    }
+    st = configure(t->fn[c], t->threads[c], t->plan.image_bytes, t->num_sms, &t->grid[c],
                    c == 0 ? &t->ctas_per_sm : nullptr);
   }
   if (st != EOS_OK) { cudaFree(t->image_dev); delete t; return st; }

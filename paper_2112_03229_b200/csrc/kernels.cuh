@@ -130,8 +130,24 @@ __device__ __forceinline__ void stage_image(uint4* smem, const uint4* __restrict
   __syncthreads();
 }
 
-template <int S, int MODE, bool CNT>
-__global__ void __launch_bounds__(kThreads, 4) search1d_kernel(const SearchArgs args) {
+// Launch shape of search1d (compile-time): threads per CTA, double2 loads in
+// flight per thread per tile, min resident CTAs per SM (register cap), and
+// whether the next tile's loads are issued before the current tile is
+// searched (software prefetch).
+template <int THREADS, int UNROLL, int MINB, bool PREFETCH>
+struct Shape {
+  static constexpr int kThreads = THREADS;
+  static constexpr int kUnroll = UNROLL;
+  static constexpr int kMinBlocks = MINB;
+  static constexpr bool kPrefetch = PREFETCH;
+  static constexpr int kTilePairs = THREADS * UNROLL;
+};
+using DefaultShape = Shape<kThreads, kUnroll, 4, false>;
+
+template <int S, int MODE, bool CNT, class SH>
+__global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(const SearchArgs args) {
+  constexpr int T = SH::kThreads;
+  constexpr int U = SH::kUnroll;
   extern __shared__ __align__(16) uint4 smem[];
   stage_image(smem, args.image, args.image_16);
   const AxisParams a = args.ax;
@@ -142,8 +158,8 @@ __global__ void __launch_bounds__(kThreads, 4) search1d_kernel(const SearchArgs 
   const double* __restrict__ Y = args.Y;
   int32_t* __restrict__ out = args.out;
   const int64_t count = args.count;
-  const int64_t gtid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  const int64_t gthreads = (int64_t)gridDim.x * kThreads;
+  const int64_t gtid = (int64_t)blockIdx.x * T + threadIdx.x;
+  const int64_t gthreads = (int64_t)gridDim.x * T;
 
   Counters cn;
   if (CNT) cn.zero();
@@ -166,40 +182,56 @@ __global__ void __launch_bounds__(kThreads, 4) search1d_kernel(const SearchArgs 
     const double2* __restrict__ Y2 = reinterpret_cast<const double2*>(Y + head);
     int2* __restrict__ O2 = reinterpret_cast<int2*>(out + head);
     const int64_t npairs = (count - head) >> 1;
-    constexpr int kTilePairs = kThreads * kUnroll;
-    const int64_t ntiles = npairs / kTilePairs;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t p0 = t * kTilePairs + threadIdx.x;
-      double2 v[kUnroll];
+    const int64_t ntiles = npairs / SH::kTilePairs;
+    int64_t t = blockIdx.x;
+    double2 v[U];
+    if (t < ntiles) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) v[u] = __ldcs(Y2 + p0 + u * kThreads);
-      int2 r[kUnroll];
+      for (int u = 0; u < U; ++u) v[u] = __ldcs(Y2 + t * SH::kTilePairs + threadIdx.x + u * T);
+    }
+    while (t < ntiles) {
+      const int64_t p0 = t * SH::kTilePairs + threadIdx.x;
+      const int64_t tn = t + gridDim.x;
+      double2 vn[U];
+      if (SH::kPrefetch && tn < ntiles) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+        for (int u = 0; u < U; ++u) vn[u] = __ldcs(Y2 + tn * SH::kTilePairs + threadIdx.x + u * T);
+      }
+      int2 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
         r[u].x = lookup<S, MODE>(v[u].x, sX, sD, a);
         r[u].y = lookup<S, MODE>(v[u].y, sX, sD, a);
       }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) __stcs(O2 + p0 + u * kThreads, r[u]);
+      for (int u = 0; u < U; ++u) __stcs(O2 + p0 + u * T, r[u]);
       if (CNT) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int64_t g = args.gofs + head + 2 * (p0 + u * kThreads);
+        for (int u = 0; u < U; ++u) {
+          const int64_t g = args.gofs + head + 2 * (p0 + u * T);
           cn.add(v[u].x, r[u].x, g, sX, a);
           cn.add(v[u].y, r[u].y, g + 1, sX, a);
         }
       }
+      if (SH::kPrefetch) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = vn[u];
+      } else if (tn < ntiles) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(Y2 + tn * SH::kTilePairs + threadIdx.x + u * T);
+      }
+      t = tn;
     }
     // remaining pairs (< one tile), then the odd last element
-    for (int64_t p = ntiles * kTilePairs + gtid; p < npairs; p += gthreads) {
-      const double2 v = __ldcs(Y2 + p);
+    for (int64_t p = ntiles * SH::kTilePairs + gtid; p < npairs; p += gthreads) {
+      const double2 w = __ldcs(Y2 + p);
       int2 r;
-      r.x = lookup<S, MODE>(v.x, sX, sD, a);
-      r.y = lookup<S, MODE>(v.y, sX, sD, a);
+      r.x = lookup<S, MODE>(w.x, sX, sD, a);
+      r.y = lookup<S, MODE>(w.y, sX, sD, a);
       __stcs(O2 + p, r);
       if (CNT) {
-        cn.add(v.x, r.x, args.gofs + head + 2 * p, sX, a);
-        cn.add(v.y, r.y, args.gofs + head + 2 * p + 1, sX, a);
+        cn.add(w.x, r.x, args.gofs + head + 2 * p, sX, a);
+        cn.add(w.y, r.y, args.gofs + head + 2 * p + 1, sX, a);
       }
     }
     const int64_t last = head + 2 * npairs;

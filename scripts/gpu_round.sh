@@ -32,6 +32,12 @@ if has benchall; then
     cat $OUT/bench_$wl.json; tail -3 $OUT/bench_$wl.err
   done
 fi
+if has exp; then
+  timeout 900 python scripts/exp_search.py --workload cfg2 --ks 2,3,4,5,6,7,8 > $OUT/exp_cfg2.json 2> $OUT/exp_cfg2.err; echo "exp cfg2 rc=$?"
+  timeout 900 python scripts/exp_search.py --workload cfg3 --steps 50 --ks 3,4,5,6,7,8 > $OUT/exp_cfg3.json 2> $OUT/exp_cfg3.err; echo "exp cfg3 rc=$?"
+  timeout 900 python scripts/exp_search.py --workload cfg5 --count 1073741824 --steps 50 --ks 4,5,6,7,8,9 > $OUT/exp_cfg5.json 2> $OUT/exp_cfg5.err; echo "exp cfg5 rc=$?"
+  tail -2 $OUT/exp_cfg*.err
+fi
 if has ncu; then
   CMD="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu"
   $CMD > $OUT/ncu_plain.log 2>&1 && \

@@ -51,7 +51,7 @@ def feasible_ks(X, ks):
     out = []
     for k in ks:
         try:
-            eos.plan_table(X, k, with_directory=False)
+            eos.plan_table(X, eos.EOS_K_AUTO if k is None else k, with_directory=False)
             out.append(k)
         except eos.EosError:
             pass
