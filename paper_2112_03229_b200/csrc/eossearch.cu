@@ -30,9 +30,9 @@ struct eos_table_s {
   // launch configuration per counters on/off
   const void* fn[2] = {nullptr, nullptr};
   int grid[2] = {0, 0};
-  int threads[2] = {dv::kThreads, dv::kThreads};
-  int unroll[2] = {dv::kUnroll, dv::kUnroll};
-  bool persistent[2] = {true, true};
+  int threads[2] = {256, 256};
+  int unroll[2] = {4, 4};
+  bool clc[2] = {true, true};
   int ctas_per_sm = 0;
 };
 
@@ -72,9 +72,26 @@ const void* search_fn_mode(int steps, bool cnt) {
   }
 }
 
-const void* pick_search(int mode, int steps, bool cnt) {
-  return mode == 0 ? search_fn_mode<0, dv::DefaultShape>(steps, cnt)
-                   : search_fn_mode<1, dv::DefaultShape>(steps, cnt);
+template <class SH>
+const void* search_fn_shape(int mode, int steps, bool cnt) {
+  return mode == 0 ? search_fn_mode<0, SH>(steps, cnt) : search_fn_mode<1, SH>(steps, cnt);
+}
+
+struct LaunchShape {
+  const void* fn;
+  int threads, unroll;
+  bool clc;
+};
+
+// Default launch shape by image size: as many threads per SM as registers
+// allow (~1024 at <= 64 regs) with as few image copies per SM as possible.
+LaunchShape pick_search(int mode, int steps, bool cnt, int64_t image_bytes) {
+  if (cnt) return {search_fn_shape<dv::ShapeCnt>(mode, steps, true), 256, 4, true};
+  if (image_bytes <= 48 * 1024)
+    return {search_fn_shape<dv::ShapeSmall>(mode, steps, false), 256, 4, true};
+  if (image_bytes <= 100 * 1024)
+    return {search_fn_shape<dv::ShapeMid>(mode, steps, false), 512, 4, true};
+  return {search_fn_shape<dv::ShapeBig>(mode, steps, false), 1024, 4, true};
 }
 
 // Launch-shape variants for tuning experiments (EOS_SEARCH_VARIANT=<name> at
@@ -82,7 +99,7 @@ const void* pick_search(int mode, int steps, bool cnt) {
 struct Variant {
   const char* name;
   int threads, unroll;
-  bool persistent;
+  bool clc;
   const void* (*get)(int steps);
 };
 
@@ -98,16 +115,16 @@ const void* variant_fn(int steps) {
 }
 
 const Variant kVariants[] = {
-    {"t256u4", 256, 4, true, variant_fn<dv::Shape<256, 4, 4, false>>},
-    {"t256u4np", 256, 4, false, variant_fn<dv::Shape<256, 4, 4, false>>},
-    {"t256u8", 256, 8, true, variant_fn<dv::Shape<256, 8, 4, false>>},
-    {"t256u4pf", 256, 4, true, variant_fn<dv::Shape<256, 4, 4, true>>},
-    {"t256u8pf", 256, 8, true, variant_fn<dv::Shape<256, 8, 3, true>>},
-    {"t512u4", 512, 4, true, variant_fn<dv::Shape<512, 4, 2, false>>},
-    {"t512u2", 512, 2, true, variant_fn<dv::Shape<512, 2, 2, false>>},
-    {"t128u8", 128, 8, true, variant_fn<dv::Shape<128, 8, 8, false>>},
-    {"t256u2", 256, 2, true, variant_fn<dv::Shape<256, 2, 4, false>>},
-    {"t256u8np", 256, 8, false, variant_fn<dv::Shape<256, 8, 4, false>>},
+    {"static256u4", 256, 4, false, variant_fn<dv::Shape<256, 4, 4, false>>},
+    {"static512u4", 512, 4, false, variant_fn<dv::Shape<512, 4, 2, false>>},
+    {"clc256u4", 256, 4, true, variant_fn<dv::Shape<256, 4, 4, true>>},
+    {"clc256u8", 256, 8, true, variant_fn<dv::Shape<256, 8, 4, true>>},
+    {"clc256u2", 256, 2, true, variant_fn<dv::Shape<256, 2, 4, true>>},
+    {"clc512u4", 512, 4, true, variant_fn<dv::Shape<512, 4, 2, true>>},
+    {"clc512u2", 512, 2, true, variant_fn<dv::Shape<512, 2, 2, true>>},
+    {"clc1024u4", 1024, 4, true, variant_fn<dv::Shape<1024, 4, 1, true>>},
+    {"clc1024u2", 1024, 2, true, variant_fn<dv::Shape<1024, 2, 1, true>>},
+    {"clc128u8", 128, 8, true, variant_fn<dv::Shape<128, 8, 8, true>>},
 };
 
 const void* pick_interp(int steps) {
@@ -187,11 +204,14 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
   const uintptr_t ya = (uintptr_t)Y, oa = (uintptr_t)out;
   a.head = (ya & 15) ? 1 : 0;
   a.vec_ok = ((ya & 7) == 0) && (((oa + 4 * (uintptr_t)a.head) & 7) == 0) && count > a.head;
-  // Persistent grid, but never more CTAs than there are tiles (small batches).
-  const int64_t per_cta = (int64_t)t->threads[cnt] * t->unroll[cnt] * 2;
-  const int64_t tiles = (count + per_cta - 1) / per_cta;
-  int64_t grid = t->persistent[cnt] ? std::min<int64_t>(t->grid[cnt], tiles) : tiles;
-  grid = std::max<int64_t>(std::min<int64_t>(grid, 0x7FFFFFFF), 1);
+  // One CTA per tile (CLC work stealing keeps ~#SM x occupancy of them
+  // resident); the static schedule uses a persistent grid instead.
+  const int64_t per_tile = (int64_t)t->threads[cnt] * t->unroll[cnt] * 2;
+  const int64_t tiles = (count - a.head + per_tile - 1) / per_tile;
+  if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;  // > 2^31 tiles (~4.4e12 targets) per call
+  a.ntiles = tiles;
+  int64_t grid = t->clc[cnt] ? tiles : std::min<int64_t>(t->grid[cnt], tiles);
+  grid = std::max<int64_t>(grid, 1);
   void* params[] = {&a};
   EOS_CUDA(cudaLaunchKernel(t->fn[cnt], dim3((unsigned)grid), dim3(t->threads[cnt]), params,
                             (size_t)t->plan.image_bytes, st));
@@ -331,7 +351,11 @@ eos_status eos_search_create_ex(const double* table_host, int64_t n, int32_t k, 
   if (st != EOS_OK) { delete t; return st; }
   t->ax = axis_params(t->plan, 0);
   for (int c = 0; c < 2 && st == EOS_OK; ++c) {
-    t->fn[c] = pick_search(t->plan.key_mode, t->plan.steps, c == 1);
+    LaunchShape ls = pick_search(t->plan.key_mode, t->plan.steps, c == 1, t->plan.image_bytes);
+    t->fn[c] = ls.fn;
+    t->threads[c] = ls.threads;
+    t->unroll[c] = ls.unroll;
+    t->clc[c] = ls.clc;
     if (c == 0) {
       const char* want = getenv("EOS_SEARCH_VARIANT");
       for (const Variant& v : kVariants) {
@@ -341,7 +365,7 @@ eos_status eos_search_create_ex(const double* table_host, int64_t n, int32_t k, 
         t->fn[0] = f;
         t->threads[0] = v.threads;
         t->unroll[0] = v.unroll;
-        t->persistent[0] = v.persistent;
+        t->clc[0] = v.clc;
       }
     }
     st = configure(t->fn[c], t->threads[c], t->plan.image_bytes, t->num_sms, &t->grid[c],

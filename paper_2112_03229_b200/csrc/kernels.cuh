@@ -5,11 +5,15 @@
 //
 // Design: HBM-bound streams.  The table X (fp64) and
 // its exponent-hash count directory (u32) are staged once per CTA into shared
-// memory; a persistent grid (#SM x resident CTAs) walks the target stream in
-// tiles with 128-bit streaming loads (ld.global.cs) and 64-bit streaming
-// stores; each target does a branchless bin lookup and a fixed-S-step
-// branchless in-bin binary lifting (no warp divergence: S is a template
-// constant of the launch).
+// memory.  The grid has one CTA per tile of the target stream, but resident
+// CTAs keep their staged image and steal the tiles of not-yet-launched CTAs
+// with Blackwell cluster launch control (clusterlaunchcontrol.try_cancel):
+// dynamic load balance at persistent-kernel cost, with no global counters.
+// Tiles move with 128-bit streaming loads (ld.global.cs) and 64-bit
+// streaming stores; the next tile's loads are issued before the current
+// tile's results are stored.  Each target does a branchless bin lookup and a
+// fixed-S-step branchless in-bin binary lifting (no warp divergence: S is a
+// template constant of the launch).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -18,8 +22,6 @@
 namespace eos {
 namespace dev {
 
-constexpr int kThreads = 256;  // threads per CTA of search1d
-constexpr int kUnroll = 4;     // double2 loads in flight per thread per tile
 constexpr int kMaxTemplSteps = 8;  // S above this uses the runtime-S instantiation
 
 struct AxisParams {
@@ -41,6 +43,7 @@ struct SearchArgs {
   int32_t head;         // scalar-peeled leading elements (0/1) before the vector body
   int32_t vec_ok;       // 1: vector body usable (alignment)
   int32_t pad_;
+  int64_t ntiles;       // tiles of the body (elements [head, count))
   AxisParams ax;
   const double* Y;
   int32_t* out;
@@ -130,26 +133,85 @@ __device__ __forceinline__ void stage_image(uint4* smem, const uint4* __restrict
   __syncthreads();
 }
 
+// ---- Blackwell cluster launch control + mbarrier (inline PTX, sm_100a) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// Ask the hardware scheduler to cancel a not-yet-launched CTA of this grid;
+// the 16-byte response lands in `resp` and completes `bar`.
+__device__ __forceinline__ void clc_try_cancel(uint4* resp, uint64_t* bar) {
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];"
+      ::"r"(smem_u32(resp)), "r"(smem_u32(bar))
+      : "memory");
+}
+// Decode the response: returns the canceled CTA's blockIdx.x, or -1.
+__device__ __forceinline__ int64_t clc_query(const uint4* resp) {
+  uint32_t valid = 0, x = 0;
+  asm volatile(
+      "{\n\t.reg .b128 R;\n\t.reg .pred P;\n\t"
+      "ld.shared.b128 R, [%2];\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 P, R;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t"
+      "@P clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, R;\n\t}"
+      : "=r"(valid), "=r"(x)
+      : "r"(smem_u32(resp))
+      : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  return valid ? (int64_t)x : -1;
+}
+
 // Launch shape of search1d (compile-time): threads per CTA, double2 loads in
-// flight per thread per tile, min resident CTAs per SM (register cap), and
-// whether the next tile's loads are issued before the current tile is
-// searched (software prefetch).
-template <int THREADS, int UNROLL, int MINB, bool PREFETCH>
+// flight per thread per tile, min resident CTAs per SM (register cap:
+// 65536 / (THREADS*MINB) per thread), and the tile schedule:
+// CLC = work stealing via cluster launch control over a one-CTA-per-tile
+// grid; otherwise a static grid-stride loop over a persistent grid.
+template <int THREADS, int UNROLL, int MINB, bool CLC>
 struct Shape {
   static constexpr int kThreads = THREADS;
   static constexpr int kUnroll = UNROLL;
   static constexpr int kMinBlocks = MINB;
-  static constexpr bool kPrefetch = PREFETCH;
+  static constexpr bool kClc = CLC;
   static constexpr int kTilePairs = THREADS * UNROLL;
+  static constexpr int kTileElems = 2 * THREADS * UNROLL;
 };
-using DefaultShape = Shape<kThreads, kUnroll, 4, false>;
+using ShapeSmall = Shape<256, 4, 4, true>;    // image <= 48 KB: 4 CTAs x 256 threads per SM
+using ShapeMid = Shape<512, 4, 2, true>;      // image <= 100 KB: 2 CTAs x 512
+using ShapeBig = Shape<1024, 4, 1, true>;     // larger: 1 CTA x 1024 (one image copy per SM)
+using ShapeCnt = Shape<256, 4, 1, true>;      // validation launches (counters on)
 
 template <int S, int MODE, bool CNT, class SH>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(const SearchArgs args) {
   constexpr int T = SH::kThreads;
   constexpr int U = SH::kUnroll;
+  constexpr int TP = SH::kTilePairs;
+  constexpr int TE = SH::kTileElems;
   extern __shared__ __align__(16) uint4 smem[];
-  stage_image(smem, args.image, args.image_16);
+  __shared__ __align__(16) uint4 clc_resp;
+  __shared__ __align__(8) uint64_t clc_bar;
+  if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
+  stage_image(smem, args.image, args.image_16);  // ends with __syncthreads
   const AxisParams a = args.ax;
   const double* __restrict__ sX =
       reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
@@ -158,53 +220,55 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
   const double* __restrict__ Y = args.Y;
   int32_t* __restrict__ out = args.out;
   const int64_t count = args.count;
-  const int64_t gtid = (int64_t)blockIdx.x * T + threadIdx.x;
-  const int64_t gthreads = (int64_t)gridDim.x * T;
+  const int64_t head = args.head;
+  const int64_t body = count - head;
+  const int64_t ntiles = args.ntiles;
+  const bool vec = args.vec_ok != 0;
+  const double2* __restrict__ Y2 = reinterpret_cast<const double2*>(Y + head);
+  int2* __restrict__ O2 = reinterpret_cast<int2*>(out + head);
 
   Counters cn;
   if (CNT) cn.zero();
 
-  if (!args.vec_ok) {
-    for (int64_t i = gtid; i < count; i += gthreads) {
-      const double y = Y[i];
-      const int32_t r = lookup<S, MODE>(y, sX, sD, a);
-      out[i] = r;
-      if (CNT) cn.add(y, r, args.gofs + i, sX, a);
-    }
-  } else {
-    const int64_t head = args.head;
-    if (gtid < head) {
-      const double y = Y[gtid];
-      const int32_t r = lookup<S, MODE>(y, sX, sD, a);
-      out[gtid] = r;
-      if (CNT) cn.add(y, r, args.gofs + gtid, sX, a);
-    }
-    const double2* __restrict__ Y2 = reinterpret_cast<const double2*>(Y + head);
-    int2* __restrict__ O2 = reinterpret_cast<int2*>(out + head);
-    const int64_t npairs = (count - head) >> 1;
-    const int64_t ntiles = npairs / SH::kTilePairs;
-    int64_t t = blockIdx.x;
-    double2 v[U];
-    if (t < ntiles) {
+  // the leading unaligned element (if any) belongs to tile 0
+  if (blockIdx.x == 0 && threadIdx.x == 0 && head) {
+    const double y = Y[0];
+    const int32_t r = lookup<S, MODE>(y, sX, sD, a);
+    out[0] = r;
+    if (CNT) cn.add(y, r, args.gofs, sX, a);
+  }
+
+  uint32_t phase = 0;
+  auto next_tile = [&](int64_t t) -> int64_t {
+    if (!SH::kClc) return t + gridDim.x;
+    mbar_wait(&clc_bar, phase);
+    phase ^= 1u;
+    const int64_t tn = clc_query(&clc_resp);
+    __syncthreads();  // everyone has read the response before it is reused
+    return tn < 0 ? ntiles : tn;
+  };
+  auto full = [&](int64_t t) { return vec && (t + 1) * TE <= body; };
+
+  int64_t t = blockIdx.x;
+  double2 v[U];
+  if (t < ntiles && full(t)) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = __ldcs(Y2 + t * SH::kTilePairs + threadIdx.x + u * T);
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(Y2 + t * TP + threadIdx.x + u * T);
+  }
+  while (t < ntiles) {
+    if (SH::kClc && threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&clc_bar, 16);
+      clc_try_cancel(&clc_resp, &clc_bar);
     }
-    while (t < ntiles) {
-      const int64_t p0 = t * SH::kTilePairs + threadIdx.x;
-      const int64_t tn = t + gridDim.x;
-      double2 vn[U];
-      if (SH::kPrefetch && tn < ntiles) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) vn[u] = __ldcs(Y2 + tn * SH::kTilePairs + threadIdx.x + u * T);
-      }
+    int64_t tn;
+    if (full(t)) {
+      const int64_t p0 = t * TP + threadIdx.x;
       int2 r[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         r[u].x = lookup<S, MODE>(v[u].x, sX, sD, a);
         r[u].y = lookup<S, MODE>(v[u].y, sX, sD, a);
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) __stcs(O2 + p0 + u * T, r[u]);
       if (CNT) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -213,34 +277,30 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
           cn.add(v[u].y, r[u].y, g + 1, sX, a);
         }
       }
-      if (SH::kPrefetch) {
+      tn = next_tile(t);
+      if (tn < ntiles && full(tn)) {  // prefetch the next tile before storing this one
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = vn[u];
-      } else if (tn < ntiles) {
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(Y2 + tn * TP + threadIdx.x + u * T);
+      }
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = __ldcs(Y2 + tn * SH::kTilePairs + threadIdx.x + u * T);
+      for (int u = 0; u < U; ++u) __stcs(O2 + p0 + u * T, r[u]);
+    } else {
+      // ragged / unaligned tile: scalar over its elements
+      const int64_t e0 = head + t * TE;
+      const int64_t e1 = min(count, e0 + TE);
+      for (int64_t i = e0 + threadIdx.x; i < e1; i += T) {
+        const double y = Y[i];
+        const int32_t r = lookup<S, MODE>(y, sX, sD, a);
+        out[i] = r;
+        if (CNT) cn.add(y, r, args.gofs + i, sX, a);
       }
-      t = tn;
-    }
-    // remaining pairs (< one tile), then the odd last element
-    for (int64_t p = ntiles * SH::kTilePairs + gtid; p < npairs; p += gthreads) {
-      const double2 w = __ldcs(Y2 + p);
-      int2 r;
-      r.x = lookup<S, MODE>(w.x, sX, sD, a);
-      r.y = lookup<S, MODE>(w.y, sX, sD, a);
-      __stcs(O2 + p, r);
-      if (CNT) {
-        cn.add(w.x, r.x, args.gofs + head + 2 * p, sX, a);
-        cn.add(w.y, r.y, args.gofs + head + 2 * p + 1, sX, a);
+      tn = next_tile(t);
+      if (tn < ntiles && full(tn)) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(Y2 + tn * TP + threadIdx.x + u * T);
       }
     }
-    const int64_t last = head + 2 * npairs;
-    if (last < count && gtid == 0) {
-      const double y = Y[last];
-      const int32_t r = lookup<S, MODE>(y, sX, sD, a);
-      out[last] = r;
-      if (CNT) cn.add(y, r, args.gofs + last, sX, a);
-    }
+    t = tn;
   }
   if (CNT) cn.flush(args.counters);
 }
