@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--count", type=int, default=None, help="override targets per GPU (testing)")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch each step from Python with per-launch events instead of a CUDA graph")
     return ap.parse_args()
 
 
@@ -170,9 +172,9 @@ def run_ours(a, d: Dist):
         obj = eos.Grid2D(w.rho, w.T, w.P)
         info = {"rho": obj.rho_info.as_dict(), "T": obj.T_info.as_dict()}
 
-        def step():
+        def step(sp=None):
             eos.eos_interp2d(obj.handle, rho.data_ptr(), T.data_ptr(), count, P.data_ptr(),
-                             iR.data_ptr(), iT.data_ptr(), stream.cuda_stream)
+                             iR.data_ptr(), iT.data_ptr(), sp or stream.cuda_stream)
     else:
         Y = torch.empty(count, dtype=torch.float64, device=dev)
         w.targets.device_fill(Y, offset, table_dev=torch.from_numpy(w.table).to(dev))
@@ -180,31 +182,53 @@ def run_ours(a, d: Dist):
         obj = eos.Table(w.table, k=a.k)
         info = obj.info.as_dict()
 
-        def step():
-            eos.eos_search(obj.handle, Y.data_ptr(), count, out.data_ptr(), stream.cuda_stream)
+        def step(sp=None):
+            eos.eos_search(obj.handle, Y.data_ptr(), count, out.data_ptr(), sp or stream.cuda_stream)
     torch.cuda.synchronize()
 
     for _ in range(max(a.warmup, 0)):
         step()
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(a.steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = eos.launch_count()
+    if a.eager:
+        # K launches from Python with an event pair around each (diagnostic mode)
+        ts = stream
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(a.steps)]
+
+        def timed():
+            for i in range(a.steps):
+                ev[i][0].record(ts)
+                step()
+                ev[i][1].record(ts)
+    else:
+        # the K steps captured once into a CUDA graph and replayed (no host launch gaps)
+        ts = torch.cuda.Stream(device=dev)
+        ts.wait_stream(stream)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=ts):
+            for _ in range(a.steps):
+                step(ts.cuda_stream)
+        torch.cuda.synchronize()
+        g.replay()  # one untimed replay (graph upload)
+        torch.cuda.synchronize()
+
+        def timed():
+            g.replay()
+    launches_captured = eos.launch_count() - launches0
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     d.barrier()
     torch.cuda.synchronize()
     with ClockSampler(d.local) as clk:
-        t0.record(stream)
-        for i in range(a.steps):
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
-        t1.record(stream)
+        t0.record(ts)
+        timed()
+        t1.record(ts)
         torch.cuda.synchronize()
     d.barrier()
-    launches = eos.launch_count() - launches0
+    launches = a.steps if not a.eager else eos.launch_count() - launches0
     ms_total = t0.elapsed_time(t1)
-    kern_ms = float(np.mean([s.elapsed_time(e) for s, e in ev]))
+    # one kernel per step: its average launch duration over the timed region
+    kern_ms = float(np.mean([x.elapsed_time(y) for x, y in ev])) if a.eager else ms_total / a.steps
     tm = torch.tensor([ms_total, kern_ms], dtype=torch.float64, device=dev)
     d.allreduce(tm, "max")
     ms_total, kern_ms_max = float(tm[0]), float(tm[1])
@@ -252,6 +276,9 @@ def run_ours(a, d: Dist):
             "parallelism": f"dp{d.world} (target-stream sharding, no data-path collective)",
         },
         "gpu_launches": int(launches),
+        "timing": ("eager: K launches, CUDA events per launch" if a.eager else
+                   f"CUDA graph of the K={a.steps} search launches ({launches_captured} captured), "
+                   "events on the replay stream around one replay"),
         "roofline": {
             "bound": "hbm",
             "achieved": round(achieved, 1),

@@ -87,6 +87,11 @@ struct LaunchShape {
 // allow (~1024 at <= 64 regs) with as few image copies per SM as possible.
 LaunchShape pick_search(int mode, int steps, bool cnt, int64_t image_bytes) {
   if (cnt) return {search_fn_shape<dv::ShapeCnt>(mode, steps, true), 256, 4, true};
+  if (steps >= 3) {
+    if (image_bytes <= 100 * 1024)
+      return {search_fn_shape<dv::ShapeDeepMid>(mode, steps, false), 512, 4, false};
+    return {search_fn_shape<dv::ShapeDeepBig>(mode, steps, false), 1024, 4, false};
+  }
   if (image_bytes <= 48 * 1024)
     return {search_fn_shape<dv::ShapeSmall>(mode, steps, false), 256, 4, true};
   if (image_bytes <= 100 * 1024)

@@ -26,6 +26,10 @@ if has bench; then
   timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
   cat $OUT/bench.json; tail -5 $OUT/bench.err
 fi
+if has bencheager; then
+  timeout 900 python bench.py --eager --no-cpu > $OUT/bench_eager.json 2> $OUT/bench_eager.err; echo "bench eager rc=$?"
+  cat $OUT/bench_eager.json
+fi
 if has benchall; then
   for wl in cfg1 cfg3 cfg4 cfg5 paper; do
     timeout 900 python bench.py --workload $wl --steps 100 --warmup 5 --no-cpu > $OUT/bench_$wl.json 2> $OUT/bench_$wl.err; echo "bench $wl rc=$?"
@@ -36,10 +40,10 @@ if has exp; then
   timeout 900 python scripts/exp_search.py --workload cfg2 --ks 2,3,4,5,6,7,8 > $OUT/exp_cfg2.json 2> $OUT/exp_cfg2.err; echo "exp cfg2 rc=$?"
   timeout 900 python scripts/exp_search.py --workload cfg3 --steps 50 --ks 3,4,5,6,7,8 > $OUT/exp_cfg3.json 2> $OUT/exp_cfg3.err; echo "exp cfg3 rc=$?"
   timeout 900 python scripts/exp_search.py --workload cfg5 --count 1073741824 --steps 50 --ks 4,5,6,7,8,9 > $OUT/exp_cfg5.json 2> $OUT/exp_cfg5.err; echo "exp cfg5 rc=$?"
-  tail -2 $OUT/exp_cfg*.err
+  for f in $OUT/exp_cfg*.err; do tail -n 2 $f; done
 fi
 if has ncu; then
-  CMD="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu"
+  CMD="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --eager"
   $CMD > $OUT/ncu_plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
       --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
