@@ -210,11 +210,13 @@ def run_ours(a, d: Dist):
             for _ in range(a.steps):
                 step(ts.cuda_stream)
         torch.cuda.synchronize()
-        g.replay()  # one untimed replay (graph upload)
+        with torch.cuda.stream(ts):
+            g.replay()  # one untimed replay (graph upload)
         torch.cuda.synchronize()
 
         def timed():
-            g.replay()
+            with torch.cuda.stream(ts):  # CUDAGraph.replay() launches on the current stream
+                g.replay()
     launches_captured = eos.launch_count() - launches0
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     d.barrier()
