@@ -46,6 +46,9 @@ struct eos_grid2d_s {
   dv::AxisParams ar{}, at{};
   const void* fn = nullptr;
   int grid = 0;
+  int threads = 512, unroll = 2;
+  bool clc = true;
+  int32_t wr_off = 0, wt_off = 0;
 };
 
 namespace {
@@ -132,14 +135,43 @@ const Variant kVariants[] = {
     {"clc128u8", 128, 8, true, variant_fn<dv::Shape<128, 8, 8, true>>},
 };
 
-const void* pick_interp(int steps) {
-  switch (steps) {
-    case 1: return (const void*)dv::interp2d_kernel<1>;
-    case 2: return (const void*)dv::interp2d_kernel<2>;
-    case 3: return (const void*)dv::interp2d_kernel<3>;
-    case 4: return (const void*)dv::interp2d_kernel<4>;
-    default: return (const void*)dv::interp2d_kernel<0>;
+template <int S>
+const void* interp_fn_s(int variant) {
+  switch (variant) {
+    case 1: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 1, 1, true>, false>;
+    case 2: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 2, 1, true>, false>;
+    case 3: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 4, 1, true>, false>;
+    case 4: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, false>, false>;
+    case 5: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, true>, true>;
+    case 6: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 1, 1, true>, true>;
+    default: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false>;
   }
+}
+
+struct Interp2DShape {
+  const void* fn;
+  int threads, unroll;
+  bool clc;
+};
+
+// EOS_INTERP_VARIANT (tuning experiments only): 1 clc1024u1, 2 clc1024u2,
+// 3 clc512u4, 4 static512u2, 5 clc512u2+recip, 6 clc1024u1+recip.
+Interp2DShape pick_interp(int steps) {
+  int v = 0;
+  if (const char* e = getenv("EOS_INTERP_VARIANT")) v = atoi(e);
+  static const int thr[7] = {512, 1024, 1024, 512, 512, 512, 1024};
+  static const int unr[7] = {2, 1, 2, 4, 2, 2, 1};
+  static const bool clc[7] = {true, true, true, true, false, true, true};
+  if (v < 0 || v > 6) v = 0;
+  const void* fn;
+  switch (steps) {
+    case 1: fn = interp_fn_s<1>(v); break;
+    case 2: fn = interp_fn_s<2>(v); break;
+    case 3: fn = interp_fn_s<3>(v); break;
+    case 4: fn = interp_fn_s<4>(v); break;
+    default: fn = interp_fn_s<0>(v); break;
+  }
+  return {fn, thr[v], unr[v], clc[v]};
 }
 
 dv::AxisParams axis_params(const TablePlan& p, int32_t x_off) {
@@ -230,6 +262,8 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   a.image = (const uint4*)g->image_dev;
   a.image_16 = (int32_t)(g->image_bytes / 16);
   a.g_off = g->g_off;
+  a.wr_off = g->wr_off;
+  a.wt_off = g->wt_off;
   a.r = g->ar;
   a.t = g->at;
   a.rho = rho;
@@ -241,11 +275,14 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   const uintptr_t al16 = (uintptr_t)rho | (uintptr_t)T | (uintptr_t)P;
   const uintptr_t al8 = (uintptr_t)iR | (uintptr_t)iT;
   a.vec_ok = ((al16 & 15) == 0) && ((al8 & 7) == 0);
-  const int64_t per_cta = (int64_t)dv::kThreads2D * 4;
-  int64_t grid = std::min<int64_t>(g->grid, (count + per_cta - 1) / per_cta);
+  const int64_t per_tile = (int64_t)g->threads * g->unroll * 2;
+  const int64_t tiles = (count + per_tile - 1) / per_tile;
+  if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;
+  a.ntiles = tiles;
+  int64_t grid = g->clc ? tiles : std::min<int64_t>(g->grid, tiles);
   grid = std::max<int64_t>(grid, 1);
   void* params[] = {&a};
-  EOS_CUDA(cudaLaunchKernel(g->fn, dim3((unsigned)grid), dim3(dv::kThreads2D), params,
+  EOS_CUDA(cudaLaunchKernel(g->fn, dim3((unsigned)grid), dim3(g->threads), params,
                             (size_t)g->image_bytes, st));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return EOS_OK;
@@ -461,10 +498,12 @@ eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double
   const int64_t ncell = n_rho * n_T;
   for (int64_t q = 0; q < ncell; ++q)
     if (!isfinite(P_host[q])) { delete g; return EOS_ERR_NONFINITE; }
-  // image: [rho X | rho dir][T X | T dir][G]
+  // image: [rho X | rho dir][T X | T dir][G][1/dR][1/dT]
   const int64_t r_bytes = g->pr.image_bytes, t_bytes = g->pt.image_bytes;
   const int64_t g_bytes = (8 * ncell + 15) & ~int64_t(15);
-  g->image_bytes = r_bytes + t_bytes + g_bytes;
+  const int64_t wr_bytes = (8 * (n_rho - 1) + 15) & ~int64_t(15);
+  const int64_t wt_bytes = (8 * (n_T - 1) + 15) & ~int64_t(15);
+  g->image_bytes = r_bytes + t_bytes + g_bytes + wr_bytes + wt_bytes;
   if (g->image_bytes > 220 * 1024) { delete g; return EOS_ERR_UNSUPPORTED; }
   std::vector<uint8_t> img((size_t)g->image_bytes, 0);
   std::vector<uint8_t> ir = eos::make_image(g->pr), it = eos::make_image(g->pt);
@@ -472,6 +511,16 @@ eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double
   memcpy(img.data() + r_bytes, it.data(), it.size());
   memcpy(img.data() + r_bytes + t_bytes, P_host, 8 * (size_t)ncell);
   g->g_off = (int32_t)(r_bytes + t_bytes);
+  g->wr_off = (int32_t)(g->g_off + g_bytes);
+  g->wt_off = (int32_t)(g->wr_off + wr_bytes);
+  for (int64_t q = 0; q + 1 < n_rho; ++q) {
+    const double w = 1.0 / (g->pr.X[q + 1] - g->pr.X[q]);
+    memcpy(img.data() + g->wr_off + 8 * q, &w, 8);
+  }
+  for (int64_t q = 0; q + 1 < n_T; ++q) {
+    const double w = 1.0 / (g->pt.X[q + 1] - g->pt.X[q]);
+    memcpy(img.data() + g->wt_off + 8 * q, &w, 8);
+  }
   g->ar = axis_params(g->pr, 0);
   g->at = axis_params(g->pt, (int32_t)r_bytes);
   cudaError_t e = cudaGetDevice(&g->device);
@@ -479,8 +528,12 @@ eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double
   if (e != cudaSuccess) { delete g; return cuda_status(e); }
   st = upload(img, &g->image_dev);
   if (st != EOS_OK) { delete g; return st; }
-  g->fn = pick_interp(std::max(g->pr.steps, g->pt.steps));
-  st = configure(g->fn, dv::kThreads2D, g->image_bytes, g->num_sms, &g->grid, nullptr);
+  Interp2DShape sh = pick_interp(std::max(g->pr.steps, g->pt.steps));
+  g->fn = sh.fn;
+  g->threads = sh.threads;
+  g->unroll = sh.unroll;
+  g->clc = sh.clc;
+  st = configure(g->fn, g->threads, g->image_bytes, g->num_sms, &g->grid, nullptr);
   if (st != EOS_OK) { cudaFree(g->image_dev); delete g; return st; }
   *out = g;
   return EOS_OK;

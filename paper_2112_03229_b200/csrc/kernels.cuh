@@ -311,14 +311,15 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
 }
 
 // ------------------------------------------------------------------ 2-D ----
-constexpr int kThreads2D = 512;
-
 struct Interp2DArgs {
   const uint4* image;
   int32_t image_16;
   int32_t g_off;    // byte offset of G fp64[nR*nT] in the image
+  int32_t wr_off;   // byte offset of 1/(R[i+1]-R[i]) fp64[nR-1] (RECIP variant)
+  int32_t wt_off;   // byte offset of 1/(T[j+1]-T[j]) fp64[nT-1] (RECIP variant)
   int32_t vec_ok;
   int32_t pad_;
+  int64_t ntiles;
   AxisParams r;     // density axis
   AxisParams t;     // temperature axis
   const double* rho;
@@ -336,8 +337,10 @@ __device__ __forceinline__ double clamp01(double t) {
 // Bilinear on the bracket cell (R14).  Written with explicit
 // round-to-nearest intrinsics (no FMA contraction), in the order of the
 // formula in eossearch.h, so the value is the correctly-rounded evaluation
-// of that formula.
-template <int S>
+// of that formula (bit-identical to a plain evaluation in that order).
+// RECIP: weights as (x - X[c]) * (1/(X[c+1]-X[c])) with the reciprocal
+// precomputed at create (a few ulp from the divide; within the 1e-12 bar).
+template <int S, bool RECIP>
 __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, int32_t& j,
                                              const char* sm, const Interp2DArgs& A) {
   const double* sR = reinterpret_cast<const double*>(sm + A.r.x_off);
@@ -349,10 +352,18 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   j = lookup<S, 0>(T, sT, dT, A.t);
   const int32_t ci = min(i, A.r.n - 2);
   const int32_t cj = min(j, A.t.n - 2);
-  const double r0 = sR[ci], r1 = sR[ci + 1];
-  const double t0 = sT[cj], t1 = sT[cj + 1];
-  const double tx = clamp01(__ddiv_rn(__dsub_rn(rho, r0), __dsub_rn(r1, r0)));
-  const double ty = clamp01(__ddiv_rn(__dsub_rn(T, t0), __dsub_rn(t1, t0)));
+  double tx, ty;
+  if (RECIP) {
+    const double* wR = reinterpret_cast<const double*>(sm + A.wr_off);
+    const double* wT = reinterpret_cast<const double*>(sm + A.wt_off);
+    tx = clamp01(__dmul_rn(__dsub_rn(rho, sR[ci]), wR[ci]));
+    ty = clamp01(__dmul_rn(__dsub_rn(T, sT[cj]), wT[cj]));
+  } else {
+    const double r0 = sR[ci], r1 = sR[ci + 1];
+    const double t0 = sT[cj], t1 = sT[cj + 1];
+    tx = clamp01(__ddiv_rn(__dsub_rn(rho, r0), __dsub_rn(r1, r0)));
+    ty = clamp01(__ddiv_rn(__dsub_rn(T, t0), __dsub_rn(t1, t0)));
+  }
   const double* g0 = sG + (int64_t)ci * A.t.n + cj;
   const double* g1 = g0 + A.t.n;
   const double g00 = g0[0], g01 = g0[1], g10 = g1[0], g11 = g1[1];
@@ -362,52 +373,99 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   return __dadd_rn(__dmul_rn(__dsub_rn(1.0, tx), a0), __dmul_rn(tx, a1));
 }
 
-template <int S>
-__global__ void __launch_bounds__(kThreads2D, 1) interp2d_kernel(const Interp2DArgs A) {
+using Shape2D = Shape<512, 2, 1, true>;  // default 2-D launch shape (165 KB image: 1 CTA/SM)
+
+template <int S, class SH, bool RECIP>
+__global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {
+  constexpr int T = SH::kThreads;
+  constexpr int U = SH::kUnroll;
+  constexpr int TP = SH::kTilePairs;
+  constexpr int TE = SH::kTileElems;
   extern __shared__ __align__(16) uint4 smem[];
+  __shared__ __align__(16) uint4 clc_resp;
+  __shared__ __align__(8) uint64_t clc_bar;
+  if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
   stage_image(smem, A.image, A.image_16);
   const char* sm = reinterpret_cast<const char*>(smem);
   const int64_t count = A.count;
-  const int64_t gtid = (int64_t)blockIdx.x * kThreads2D + threadIdx.x;
-  const int64_t gthreads = (int64_t)gridDim.x * kThreads2D;
-  int64_t done = 0;
-  if (A.vec_ok) {
-    constexpr int U = 2;
-    constexpr int kTilePairs = kThreads2D * U;  // in double2 units
-    const double2* __restrict__ R2 = reinterpret_cast<const double2*>(A.rho);
-    const double2* __restrict__ T2 = reinterpret_cast<const double2*>(A.T);
-    double2* __restrict__ P2 = reinterpret_cast<double2*>(A.P);
-    int2* __restrict__ IR2 = reinterpret_cast<int2*>(A.iR);
-    int2* __restrict__ IT2 = reinterpret_cast<int2*>(A.iT);
-    const int64_t npairs = count >> 1;
-    const int64_t ntiles = npairs / kTilePairs;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t p0 = t * kTilePairs + threadIdx.x;
-      double2 vr[U], vt[U];
+  const int64_t ntiles = A.ntiles;
+  const bool vec = A.vec_ok != 0;
+  const bool br = A.iR != nullptr, bt = A.iT != nullptr;
+  const double2* __restrict__ R2 = reinterpret_cast<const double2*>(A.rho);
+  const double2* __restrict__ T2 = reinterpret_cast<const double2*>(A.T);
+  double2* __restrict__ P2 = reinterpret_cast<double2*>(A.P);
+  int2* __restrict__ IR2 = reinterpret_cast<int2*>(A.iR);
+  int2* __restrict__ IT2 = reinterpret_cast<int2*>(A.iT);
+
+  uint32_t phase = 0;
+  auto next_tile = [&](int64_t t) -> int64_t {
+    if (!SH::kClc) return t + gridDim.x;
+    mbar_wait(&clc_bar, phase);
+    phase ^= 1u;
+    const int64_t tn = clc_query(&clc_resp);
+    __syncthreads();
+    return tn < 0 ? ntiles : tn;
+  };
+  auto full = [&](int64_t t) { return vec && (t + 1) * TE <= count; };
+
+  int64_t t = blockIdx.x;
+  double2 vr[U], vt[U];
+  if (t < ntiles && full(t)) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      vr[u] = __ldcs(R2 + t * TP + threadIdx.x + u * T);
+      vt[u] = __ldcs(T2 + t * TP + threadIdx.x + u * T);
+    }
+  }
+  while (t < ntiles) {
+    if (SH::kClc && threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&clc_bar, 16);
+      clc_try_cancel(&clc_resp, &clc_bar);
+    }
+    int64_t tn;
+    if (full(t)) {
+      const int64_t p0 = t * TP + threadIdx.x;
+      double2 p[U];
+      int2 ir[U], it[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        vr[u] = __ldcs(R2 + p0 + u * kThreads2D);
-        vt[u] = __ldcs(T2 + p0 + u * kThreads2D);
+        p[u].x = interp_one<S, RECIP>(vr[u].x, vt[u].x, ir[u].x, it[u].x, sm, A);
+        p[u].y = interp_one<S, RECIP>(vr[u].y, vt[u].y, ir[u].y, it[u].y, sm, A);
+      }
+      tn = next_tile(t);
+      if (tn < ntiles && full(tn)) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          vr[u] = __ldcs(R2 + tn * TP + threadIdx.x + u * T);
+          vt[u] = __ldcs(T2 + tn * TP + threadIdx.x + u * T);
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        int2 ir, it;
-        double2 p;
-        p.x = interp_one<S>(vr[u].x, vt[u].x, ir.x, it.x, sm, A);
-        p.y = interp_one<S>(vr[u].y, vt[u].y, ir.y, it.y, sm, A);
-        __stcs(P2 + p0 + u * kThreads2D, p);
-        if (A.iR) __stcs(IR2 + p0 + u * kThreads2D, ir);
-        if (A.iT) __stcs(IT2 + p0 + u * kThreads2D, it);
+        __stcs(P2 + p0 + u * T, p[u]);
+        if (br) __stcs(IR2 + p0 + u * T, ir[u]);
+        if (bt) __stcs(IT2 + p0 + u * T, it[u]);
+      }
+    } else {
+      const int64_t e0 = t * TE;
+      const int64_t e1 = min(count, e0 + TE);
+      for (int64_t q = e0 + threadIdx.x; q < e1; q += T) {
+        int32_t i, j;
+        const double pq = interp_one<S, RECIP>(A.rho[q], A.T[q], i, j, sm, A);
+        A.P[q] = pq;
+        if (br) A.iR[q] = i;
+        if (bt) A.iT[q] = j;
+      }
+      tn = next_tile(t);
+      if (tn < ntiles && full(tn)) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          vr[u] = __ldcs(R2 + tn * TP + threadIdx.x + u * T);
+          vt[u] = __ldcs(T2 + tn * TP + threadIdx.x + u * T);
+        }
       }
     }
-    done = ntiles * kTilePairs * 2;
-  }
-  for (int64_t q = done + gtid; q < count; q += gthreads) {
-    int32_t i, j;
-    const double p = interp_one<S>(A.rho[q], A.T[q], i, j, sm, A);
-    A.P[q] = p;
-    if (A.iR) A.iR[q] = i;
-    if (A.iT) A.iT[q] = j;
+    t = tn;
   }
 }
 

@@ -42,6 +42,9 @@ if has exp; then
   timeout 900 python scripts/exp_search.py --workload cfg5 --count 1073741824 --steps 50 --ks 4,5,6,7,8,9 > $OUT/exp_cfg5.json 2> $OUT/exp_cfg5.err; echo "exp cfg5 rc=$?"
   for f in $OUT/exp_cfg*.err; do tail -n 2 $f; done
 fi
+if has expi; then
+  timeout 900 python scripts/exp_interp.py > $OUT/exp_interp.json 2> $OUT/exp_interp.err; echo "exp interp rc=$?"; tail -n 3 $OUT/exp_interp.err
+fi
 if has ncu; then
   CMD="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --eager"
   $CMD > $OUT/ncu_plain.log 2>&1 && \
