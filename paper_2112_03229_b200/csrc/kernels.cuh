@@ -340,6 +340,42 @@ __device__ __forceinline__ double clamp01(double t) {
 // of that formula (bit-identical to a plain evaluation in that order).
 // RECIP: weights as (x - X[c]) * (1/(X[c+1]-X[c])) with the reciprocal
 // precomputed at create (a few ulp from the divide; within the 1e-12 bar).
+// Bracket + cell endpoints on one axis: i (the P:54 lower bound), the cell
+// ci = min(i, n-2) and its endpoints X[ci], X[ci+1].  With S = 1 (every bin
+// holds at most one entry) the in-bin probe value X[lo] is always one of the
+// two endpoints in the common case, so only one more gather is needed.
+template <int S>
+__device__ __forceinline__ void axis_cell(double y, const double* __restrict__ sX,
+                                          const uint32_t* __restrict__ sD, const AxisParams& a,
+                                          int32_t& i, int32_t& ci, double& xl, double& xr) {
+  if (S == 1) {
+    uint32_t kb = key_hi<0>(y) >> a.shift;
+    kb = min(max(kb, a.base), a.top);
+    const uint32_t d = sD[kb - a.base];
+    const int32_t lo = (int32_t)(d & 0xFFFFu);  // <= n-1: X[n-1] lies in the top bin
+    const int32_t occ = (int32_t)(d >> 16);     // 0 or 1 when S == 1
+    const double pv = sX[lo];
+    const int32_t c = (occ >= 1 && pv <= y) ? 1 : 0;
+    i = (y >= a.x0) ? lo + c - 1 : 0;
+    ci = min(i, a.n - 2);
+    const bool left = (ci == lo), right = (ci + 1 == lo);
+    const double ov = sX[left ? lo + 1 : (right ? lo - 1 : ci)];
+    xl = left ? pv : ov;
+    xr = left ? ov : (right ? pv : sX[ci + 1]);
+  } else {
+    i = lookup<S, 0>(y, sX, sD, a);
+    ci = min(i, a.n - 2);
+    xl = sX[ci];
+    xr = sX[ci + 1];
+  }
+}
+
+// Bilinear on the bracket cell (R14).  Written with explicit
+// round-to-nearest intrinsics (no FMA contraction), in the order of the
+// formula in eossearch.h, so the value is the correctly-rounded evaluation
+// of that formula (bit-identical to a plain evaluation in that order).
+// RECIP: weights as (x - X[c]) * (1/(X[c+1]-X[c])) with the reciprocal
+// precomputed at create (a few ulp from the divide; within the 1e-12 bar).
 template <int S, bool RECIP>
 __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, int32_t& j,
                                              const char* sm, const Interp2DArgs& A) {
@@ -348,19 +384,17 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   const uint32_t* dR = reinterpret_cast<const uint32_t*>(sm + A.r.d_off);
   const uint32_t* dT = reinterpret_cast<const uint32_t*>(sm + A.t.d_off);
   const double* sG = reinterpret_cast<const double*>(sm + A.g_off);
-  i = lookup<S, 0>(rho, sR, dR, A.r);
-  j = lookup<S, 0>(T, sT, dT, A.t);
-  const int32_t ci = min(i, A.r.n - 2);
-  const int32_t cj = min(j, A.t.n - 2);
+  int32_t ci, cj;
+  double r0, r1, t0, t1;
+  axis_cell<S>(rho, sR, dR, A.r, i, ci, r0, r1);
+  axis_cell<S>(T, sT, dT, A.t, j, cj, t0, t1);
   double tx, ty;
   if (RECIP) {
     const double* wR = reinterpret_cast<const double*>(sm + A.wr_off);
     const double* wT = reinterpret_cast<const double*>(sm + A.wt_off);
-    tx = clamp01(__dmul_rn(__dsub_rn(rho, sR[ci]), wR[ci]));
-    ty = clamp01(__dmul_rn(__dsub_rn(T, sT[cj]), wT[cj]));
+    tx = clamp01(__dmul_rn(__dsub_rn(rho, r0), wR[ci]));
+    ty = clamp01(__dmul_rn(__dsub_rn(T, t0), wT[cj]));
   } else {
-    const double r0 = sR[ci], r1 = sR[ci + 1];
-    const double t0 = sT[cj], t1 = sT[cj + 1];
     tx = clamp01(__ddiv_rn(__dsub_rn(rho, r0), __dsub_rn(r1, r0)));
     ty = clamp01(__ddiv_rn(__dsub_rn(T, t0), __dsub_rn(t1, t0)));
   }
@@ -373,7 +407,10 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   return __dadd_rn(__dmul_rn(__dsub_rn(1.0, tx), a0), __dmul_rn(tx, a1));
 }
 
-using Shape2D = Shape<512, 2, 1, true>;  // default 2-D launch shape (165 KB image: 1 CTA/SM)
+// default 2-D launch shape (165 KB image: 1 CTA/SM).  Static schedule: the
+// 2-D body is smem/latency-bound, where the CLC loop's per-tile CTA barrier
+// costs more than the static tail (profiles/r01_exp_interp.json).
+using Shape2D = Shape<512, 2, 1, false>;
 
 template <int S, class SH, bool RECIP>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {

@@ -45,6 +45,14 @@ fi
 if has expi; then
   timeout 900 python scripts/exp_interp.py > $OUT/exp_interp.json 2> $OUT/exp_interp.err; echo "exp interp rc=$?"; tail -n 3 $OUT/exp_interp.err
 fi
+if has ncu2; then
+  for wl in cfg4 cfg5; do
+    CMD="python bench.py --workload $wl --count 268435456 --steps 5 --warmup 2 --no-e2e --no-cpu --eager"
+    $CMD > $OUT/ncu_plain_$wl.log 2>&1 && \
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:'search1d|interp2d' -s 2 -c 1 \
+        -o $OUT/prof_$wl -f $CMD > $OUT/ncu_full_$wl.log 2>&1; echo "ncu $wl rc=$?"
+  done
+fi
 if has ncu; then
   CMD="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --eager"
   $CMD > $OUT/ncu_plain.log 2>&1 && \
