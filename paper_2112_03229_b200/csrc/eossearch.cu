@@ -138,7 +138,7 @@ const Variant kVariants[] = {
 template <int S>
 const void* interp_fn_s(int variant) {
   switch (variant) {
-    case 1: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 1, 1, false>, false>;
+    case 1: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, false>, false>;
     case 2: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 2, 1, false>, false>;
     case 3: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 4, 1, false>, false>;
     case 4: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, true>, false>;
@@ -154,14 +154,14 @@ struct Interp2DShape {
   bool clc;
 };
 
-// EOS_INTERP_VARIANT (tuning experiments only): 0 static512u2 (default),
-// 1 static1024u1, 2 static1024u2, 3 static512u4, 4 clc512u2,
+// EOS_INTERP_VARIANT (tuning experiments only): 0 static1024u1 (default),
+// 1 static512u2, 2 static1024u2, 3 static512u4, 4 clc512u2,
 // 5 static512u2+recip, 6 static1024u1+recip.
 Interp2DShape pick_interp(int steps) {
   int v = 0;
   if (const char* e = getenv("EOS_INTERP_VARIANT")) v = atoi(e);
-  static const int thr[7] = {512, 1024, 1024, 512, 512, 512, 1024};
-  static const int unr[7] = {2, 1, 2, 4, 2, 2, 1};
+  static const int thr[7] = {1024, 512, 1024, 512, 512, 512, 1024};
+  static const int unr[7] = {1, 2, 2, 4, 2, 2, 1};
   static const bool clc[7] = {false, false, false, false, true, false, false};
   if (v < 0 || v > 6) v = 0;
   const void* fn;

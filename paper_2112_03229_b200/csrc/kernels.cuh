@@ -127,11 +127,6 @@ struct Counters {
   }
 };
 
-// Stage the device image (L2-resident after the first CTA) into shared memory.
-__device__ __forceinline__ void stage_image(uint4* smem, const uint4* __restrict__ img, int n16) {
-  for (int i = threadIdx.x; i < n16; i += blockDim.x) smem[i] = __ldg(img + i);
-  __syncthreads();
-}
 
 // ---- Blackwell cluster launch control + mbarrier (inline PTX, sm_100a) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -182,6 +177,32 @@ __device__ __forceinline__ int64_t clc_query(const uint4* resp) {
   return valid ? (int64_t)x : -1;
 }
 
+// TMA 1-D bulk copy global -> this CTA's shared memory, completing on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Stage the device image (L2-resident after the first CTA) into shared
+// memory with TMA bulk copies (one thread issues them; everyone waits on the
+// mbarrier).  SASS: UBLKCP.S.G + SYNCS.  All threads return with the image
+// visible.  `bar` is single-use (phase 0).
+__device__ __forceinline__ void stage_image(uint4* smem, const uint4* __restrict__ img, int n16,
+                                            uint64_t* bar) {
+  const uint32_t bytes = (uint32_t)n16 * 16u;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_arrive_expect_tx(bar, bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768u)
+      bulk_g2s(reinterpret_cast<char*>(smem) + off, reinterpret_cast<const char*>(img) + off,
+               min(32768u, bytes - off), bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+}
+
 // Launch shape of search1d (compile-time): threads per CTA, double2 loads in
 // flight per thread per tile, min resident CTAs per SM (register cap:
 // 65536 / (THREADS*MINB) per thread), and the tile schedule:
@@ -214,9 +235,9 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
   constexpr int TE = SH::kTileElems;
   extern __shared__ __align__(16) uint4 smem[];
   __shared__ __align__(16) uint4 clc_resp;
-  __shared__ __align__(8) uint64_t clc_bar;
+  __shared__ __align__(8) uint64_t clc_bar, stage_bar;
   if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
-  stage_image(smem, args.image, args.image_16);  // ends with __syncthreads
+  stage_image(smem, args.image, args.image_16, &stage_bar);
   const AxisParams a = args.ax;
   const double* __restrict__ sX =
       reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
@@ -410,7 +431,7 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
 // default 2-D launch shape (165 KB image: 1 CTA/SM).  Static schedule: the
 // 2-D body is smem/latency-bound, where the CLC loop's per-tile CTA barrier
 // costs more than the static tail (profiles/r01_exp_interp.json).
-using Shape2D = Shape<512, 2, 1, false>;
+using Shape2D = Shape<1024, 1, 1, false>;
 
 template <int S, class SH, bool RECIP>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {
@@ -420,9 +441,9 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
   constexpr int TE = SH::kTileElems;
   extern __shared__ __align__(16) uint4 smem[];
   __shared__ __align__(16) uint4 clc_resp;
-  __shared__ __align__(8) uint64_t clc_bar;
+  __shared__ __align__(8) uint64_t clc_bar, stage_bar;
   if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
-  stage_image(smem, A.image, A.image_16);
+  stage_image(smem, A.image, A.image_16, &stage_bar);
   const char* sm = reinterpret_cast<const char*>(smem);
   const int64_t count = A.count;
   const int64_t ntiles = A.ntiles;

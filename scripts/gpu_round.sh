@@ -45,6 +45,10 @@ fi
 if has expi; then
   timeout 900 python scripts/exp_interp.py > $OUT/exp_interp.json 2> $OUT/exp_interp.err; echo "exp interp rc=$?"; tail -n 3 $OUT/exp_interp.err
 fi
+if has exps; then
+  timeout 900 python scripts/exp_small.py > $OUT/exp_small_cfg1.json 2> $OUT/exp_small.err; echo "exp small rc=$?"; tail -n 3 $OUT/exp_small.err
+  timeout 900 python scripts/exp_small.py --workload cfg5 --ks auto,5,7,9 > $OUT/exp_small_cfg5.json 2>> $OUT/exp_small.err; echo "exp small5 rc=$?"
+fi
 if has ncu2; then
   for wl in cfg4 cfg5; do
     CMD="python bench.py --workload $wl --count 268435456 --steps 5 --warmup 2 --no-e2e --no-cpu --eager"
