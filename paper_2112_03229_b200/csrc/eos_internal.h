@@ -36,8 +36,11 @@ struct TablePlan {
   int64_t image_bytes = 0; // X region + directory (16-B padded)
 };
 
-// Smem budget used by the automatic k choice (bytes of X + directory).
-constexpr int64_t kAutoImageBudget = 100 * 1024;
+// Smem budget used by the automatic k choice (bytes of X + directory): one
+// image copy per SM at the 1024-thread launch shape.  Measured: a larger
+// image that removes an in-bin step wins (cfg5 k=9/S=3 at 138 KB beats
+// k=7/S=4 at 59 KB by 6%; cfg1 k=9/S=1 beats k=5/S=2 by 3%).
+constexpr int64_t kAutoImageBudget = 200 * 1024;
 
 // Validate + build (eos_plan_table semantics).  k_req: EOS_K_AUTO or 0..EOS_MAX_K.
 // strict: axes of a 2-D grid must be strictly increasing and n >= 2.

@@ -111,7 +111,7 @@ eos_status plan_table(const double* Xin, int64_t n, int k_req, bool strict, Tabl
     return EOS_OK;
   }
 
-  // Automatic k (DESIGN.md "k choice"): the smallest fixed in-bin step count S
+  // Automatic k (DESIGN.md §6.3): the smallest fixed in-bin step count S
   // reachable with an image within kAutoImageBudget; ties -> smallest k
   // (smaller directory).  Bins only grow with k, so stop at the budget.
   TablePlan best;

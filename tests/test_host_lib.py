@@ -151,9 +151,9 @@ def test_auto_k_reaches_short_searches_on_configs():
         X = datagen.workload(name, count=1).table
         info, _ = eos.plan_table(X)
         chosen[name] = (info.k, info.bins, info.steps, info.image_bytes)
-        assert info.image_bytes <= 100 * 1024 or info.k == 0
+        assert info.image_bytes <= 200 * 1024 or info.k == 0
     assert chosen["cfg2"][2] == 1 and chosen["cfg3"][2] == 1
-    assert chosen["cfg5"][2] <= 4
+    assert chosen["cfg5"][2] <= 3
     rho, T, _ = datagen.grid_cfg4()
     for ax in (rho, T):
         assert eos.plan_table(ax)[0].steps == 1
