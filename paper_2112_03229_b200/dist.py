@@ -32,7 +32,8 @@ class Dist:
         self.backend = None
 
     def init(self, backend: str = "nccl"):
-        if self.world > 1:
+        # world > 1, or launched by torchrun (exercises the NCCL path even at N = 1)
+        if self.world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             dist.init_process_group(backend)

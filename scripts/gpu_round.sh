@@ -49,6 +49,17 @@ if has exps; then
   timeout 900 python scripts/exp_small.py > $OUT/exp_small_cfg1.json 2> $OUT/exp_small.err; echo "exp small rc=$?"; tail -n 3 $OUT/exp_small.err
   timeout 900 python scripts/exp_small.py --workload cfg5 --ks auto,5,7,9 > $OUT/exp_small_cfg5.json 2>> $OUT/exp_small.err; echo "exp small5 rc=$?"
 fi
+for tool in memcheck racecheck synccheck initcheck; do
+  if has san_$tool; then
+    python scripts/sanitize_small.py > $OUT/san_plain.log 2>&1 && \
+    timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize_small.py > $OUT/san_$tool.log 2>&1
+    echo "sanitizer $tool rc=$?"; tail -n 5 $OUT/san_$tool.log
+  fi
+done
+if has torchrun1; then
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 200 --warmup 5 --no-cpu > $OUT/bench_torchrun1.json 2> $OUT/bench_torchrun1.err; echo "torchrun1 rc=$?"
+  cat $OUT/bench_torchrun1.json; tail -n 3 $OUT/bench_torchrun1.err
+fi
 if has ncu2; then
   for wl in cfg4 cfg5; do
     CMD="python bench.py --workload $wl --count 268435456 --steps 5 --warmup 2 --no-e2e --no-cpu --eager"
