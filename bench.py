@@ -448,8 +448,7 @@ def main():
     import torch
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
-    if d.world > 1:
-        torch.cuda.set_device(d.local)
+    torch.cuda.set_device(d.local)
     d.init("nccl")
     try:
         res = run_ours(a, d)
