@@ -19,6 +19,7 @@ import os
 
 import numpy as np
 
+from ._build import CHECKED_LIB as _CHECKED_LIB_PATH
 from ._build import LIB as _LIB_PATH
 
 __all__ = [
@@ -77,10 +78,12 @@ def load_library():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_LIB_PATH):
-        raise ImportError(f"{_LIB_PATH} is missing: run __graft_entry__.build() "
+    # EOS_LIBRARY=checked selects the bounds-checked debug build (tests only)
+    path = _CHECKED_LIB_PATH if os.environ.get("EOS_LIBRARY") == "checked" else _LIB_PATH
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run __graft_entry__.build() "
                           "(python -m paper_2112_03229_b200._build); there is no CPU fallback")
-    L = ctypes.CDLL(_LIB_PATH)
+    L = ctypes.CDLL(path)
     sig = {
         "eos_plan_table": [_P, _I64, _I32, _P, _P, _I64],
         "eos_search_create": [_P, _I64, _P],

@@ -19,6 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libeossearch.so")
+CHECKED_LIB = os.path.join(LIBDIR, "libeossearch_checked.so")  # -DEOS_DEVICE_CHECKS debug build
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -32,10 +33,10 @@ def deps() -> list[str]:
         + [os.path.join(INCLUDE, "eossearch.h")]
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(d) > t for d in deps())
 
 
@@ -45,22 +46,24 @@ def nvcc_cmd(out: str = LIB, extra: list[str] | None = None) -> list[str]:
             "-Xptxas", "-v", *(extra or []), "-o", out, *sources()]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or stale():
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    lib = CHECKED_LIB if checked else LIB
+    if force or stale(lib):
         os.makedirs(LIBDIR, exist_ok=True)
-        tmp = LIB + ".tmp"
-        r = subprocess.run(nvcc_cmd(tmp), capture_output=True, text=True)
-        log = os.path.join(LIBDIR, "ptxas.log")
+        tmp = lib + ".tmp"
+        r = subprocess.run(nvcc_cmd(tmp, ["-DEOS_DEVICE_CHECKS"] if checked else None),
+                           capture_output=True, text=True)
+        log = os.path.join(LIBDIR, "ptxas_checked.log" if checked else "ptxas.log")
         with open(log, "w") as f:
             f.write(r.stdout + r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc failed building libeossearch.so")
-        os.replace(tmp, LIB)
+        os.replace(tmp, lib)
         if verbose:
-            print(f"built {LIB}")
-    return LIB
+            print(f"built {lib}")
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv)

@@ -19,6 +19,24 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Debug build (-DEOS_DEVICE_CHECKS, lib/libeossearch_checked.so): bounds checks
+// on every shared/global access of the hot loops; a failure traps the kernel.
+// (compute-sanitizer is not available on this GPU pool.)
+#ifdef EOS_DEVICE_CHECKS
+#include <cstdio>
+#define EOS_DCHECK(c)                                                     \
+  do {                                                                    \
+    if (!(c)) {                                                           \
+      printf("EOS_DCHECK failed: %s (%s:%d)\n", #c, __FILE__, __LINE__); \
+      __trap();                                                           \
+    }                                                                     \
+  } while (0)
+#else
+#define EOS_DCHECK(c) \
+  do {                \
+  } while (0)
+#endif
+
 namespace eos {
 namespace dev {
 
@@ -77,9 +95,11 @@ __device__ __forceinline__ int32_t lookup(double y, const double* __restrict__ s
                                           const uint32_t* __restrict__ sD, const AxisParams& a) {
   uint32_t kb = key_hi<MODE>(y) >> a.shift;
   kb = min(max(kb, a.base), a.top);
+  EOS_DCHECK(kb - a.base <= a.top - a.base);
   const uint32_t d = sD[kb - a.base];
   const int32_t lo = (int32_t)(d & 0xFFFFu);
   const int32_t occ = (int32_t)(d >> 16);
+  EOS_DCHECK(lo + occ <= a.n && occ < (1 << (S > 0 ? S : a.steps)));
   int32_t c = 0;
   if (S > 0) {
 #pragma unroll
@@ -239,6 +259,8 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
   if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
   stage_image(smem, args.image, args.image_16, &stage_bar);
   const AxisParams a = args.ax;
+  EOS_DCHECK(a.d_off + 4 * (int64_t)(a.top - a.base + 1) <= 16 * (int64_t)args.image_16 &&
+             a.x_off + 8 * (int64_t)a.n <= a.d_off);
   const double* __restrict__ sX =
       reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
   const uint32_t* __restrict__ sD =
@@ -314,6 +336,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
       // ragged / unaligned tile: scalar over its elements
       const int64_t e0 = head + t * TE;
       const int64_t e1 = min(count, e0 + TE);
+      EOS_DCHECK(e0 >= 0 && t >= 0);
       for (int64_t i = e0 + threadIdx.x; i < e1; i += T) {
         const double y = Y[i];
         const int32_t r = lookup<S, MODE>(y, sX, sD, a);
@@ -375,6 +398,7 @@ __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ s
     const uint32_t d = sD[kb - a.base];
     const int32_t lo = (int32_t)(d & 0xFFFFu);  // <= n-1: X[n-1] lies in the top bin
     const int32_t occ = (int32_t)(d >> 16);     // 0 or 1 when S == 1
+    EOS_DCHECK(lo < a.n && occ <= 1);
     const double pv = sX[lo];
     const int32_t c = (occ >= 1 && pv <= y) ? 1 : 0;
     i = (y >= a.x0) ? lo + c - 1 : 0;
@@ -383,6 +407,7 @@ __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ s
     const double ov = sX[left ? lo + 1 : (right ? lo - 1 : ci)];
     xl = left ? pv : ov;
     xr = left ? ov : (right ? pv : sX[ci + 1]);
+    EOS_DCHECK(ci >= 0 && ci + 1 < a.n && (left ? lo + 1 : (right ? lo - 1 : ci)) < a.n);
   } else {
     i = lookup<S, 0>(y, sX, sD, a);
     ci = min(i, a.n - 2);
@@ -419,6 +444,7 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
     tx = clamp01(__ddiv_rn(__dsub_rn(rho, r0), __dsub_rn(r1, r0)));
     ty = clamp01(__ddiv_rn(__dsub_rn(T, t0), __dsub_rn(t1, t0)));
   }
+  EOS_DCHECK(ci >= 0 && cj >= 0 && ci + 1 < A.r.n && cj + 1 < A.t.n);
   const double* g0 = sG + (int64_t)ci * A.t.n + cj;
   const double* g1 = g0 + A.t.n;
   const double g00 = g0[0], g01 = g0[1], g10 = g1[0], g11 = g1[1];
@@ -483,6 +509,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
     int64_t tn;
     if (full(t)) {
       const int64_t p0 = t * TP + threadIdx.x;
+      EOS_DCHECK(2 * (p0 + (U - 1) * T) + 1 < count);
       double2 p[U];
       int2 ir[U], it[U];
 #pragma unroll

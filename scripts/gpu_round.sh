@@ -22,6 +22,11 @@ if has tests; then
   timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $OUT/pytest_gpu.log 2>&1; echo "pytest gpu rc=$?"
   tail -15 $OUT/pytest_gpu.log
 fi
+if has checked; then
+  EOS_LIBRARY=checked timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $OUT/pytest_gpu_checked.log 2>&1; echo "pytest gpu (checked build) rc=$?"
+  tail -n 4 $OUT/pytest_gpu_checked.log
+  EOS_LIBRARY=checked timeout 600 python scripts/sanitize_small.py > $OUT/checked_small.log 2>&1; echo "checked small rc=$?"; tail -n 2 $OUT/checked_small.log
+fi
 if has bench; then
   timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
   cat $OUT/bench.json; tail -5 $OUT/bench.err
