@@ -101,7 +101,7 @@ __device__ __forceinline__ int32_t lookup(double y, const double* __restrict__ s
   const int32_t occ = (int32_t)(d >> 16);
   EOS_DCHECK(lo + occ <= a.n && occ < (1 << (S > 0 ? S : a.steps)));
   int32_t c = 0;
-  if (S > 0) {
+  if (S > 0 && S <= 2) {
 #pragma unroll
     for (int s = 1 << (S > 0 ? S - 1 : 0); s > 0; s >>= 1) {
       const int32_t j = c + s;
@@ -109,11 +109,27 @@ __device__ __forceinline__ int32_t lookup(double y, const double* __restrict__ s
         if (sX[lo + j - 1] <= y) c = j;
       }
     }
-  } else {  // runtime S (large bins)
-    for (int s = 1 << (a.steps - 1); s > 0; s >>= 1) {
-      const int32_t j = c + s;
-      if (j <= occ) {
-        if (sX[lo + j - 1] <= y) c = j;
+  } else {
+    // Deep tables: steps with s > max(occ) over the warp change no lane
+    // (j = c + s > occ), so they are skipped warp-uniformly (one REDUX).
+    // Most warps of a clustered table never reach its largest bins.
+    const uint32_t m = __reduce_max_sync(__activemask(), (uint32_t)occ);
+    if (S > 0) {
+#pragma unroll
+      for (int s = 1 << (S > 0 ? S - 1 : 0); s > 0; s >>= 1) {
+        if ((uint32_t)s <= m) {
+          const int32_t j = c + s;
+          if (j <= occ) {
+            if (sX[lo + j - 1] <= y) c = j;
+          }
+        }
+      }
+    } else {  // runtime S: exactly the bits of the warp max
+      for (int s = m ? (1 << (31 - __clz(m))) : 0; s > 0; s >>= 1) {
+        const int32_t j = c + s;
+        if (j <= occ) {
+          if (sX[lo + j - 1] <= y) c = j;
+        }
       }
     }
   }
