@@ -35,6 +35,10 @@ if has bencheager; then
   timeout 900 python bench.py --eager --no-cpu > $OUT/bench_eager.json 2> $OUT/bench_eager.err; echo "bench eager rc=$?"
   cat $OUT/bench_eager.json
 fi
+if has bench5; then
+  timeout 900 python bench.py --workload cfg5 --steps 60 --warmup 5 --no-cpu --no-e2e > $OUT/bench_cfg5.json 2> $OUT/bench_cfg5.err; echo "bench cfg5 rc=$?"
+  cat $OUT/bench_cfg5.json | head -c 600; echo
+fi
 if has benchall; then
   for wl in cfg1 cfg3 cfg4 cfg5 paper; do
     timeout 900 python bench.py --workload $wl --steps 100 --warmup 5 --no-cpu > $OUT/bench_$wl.json 2> $OUT/bench_$wl.err; echo "bench $wl rc=$?"
