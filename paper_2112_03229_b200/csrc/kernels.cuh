@@ -120,53 +120,6 @@ __device__ __forceinline__ int32_t lookup(double y, const double* __restrict__ s
   return (y >= a.x0) ? (lo + c - 1) : 0;
 }
 
-// NB lookups of one thread at once, for full tiles (all 32 lanes active).
-// Deep tables (S >= 3): a step with s > max(occ) over the thread's NB bins and
-// the warp changes no lane (j = c + s > occ), so it is skipped warp-uniformly
-// -- one REDUX per NB lookups; the NB probes of a step stay independent (ILP).
-// In a clustered table most warps never touch its largest bins.
-template <int S, int MODE, int NB>
-__device__ __forceinline__ void lookup_batch(const double (&y)[NB], int32_t (&r)[NB],
-                                             const double* __restrict__ sX,
-                                             const uint32_t* __restrict__ sD,
-                                             const AxisParams& a) {
-  if (S > 0 && S <= 2) {
-#pragma unroll
-    for (int u = 0; u < NB; ++u) r[u] = lookup<S, MODE>(y[u], sX, sD, a);
-    return;
-  }
-  int32_t lo[NB], occ[NB], c[NB];
-  uint32_t m = 0;
-#pragma unroll
-  for (int u = 0; u < NB; ++u) {
-    uint32_t kb = key_hi<MODE>(y[u]) >> a.shift;
-    kb = min(max(kb, a.base), a.top);
-    EOS_DCHECK(kb - a.base <= a.top - a.base);
-    const uint32_t d = sD[kb - a.base];
-    lo[u] = (int32_t)(d & 0xFFFFu);
-    occ[u] = (int32_t)(d >> 16);
-    c[u] = 0;
-    m = max(m, (uint32_t)occ[u]);
-  }
-  m = __reduce_max_sync(0xFFFFFFFFu, m);
-  const int top = m ? (1 << (31 - __clz(m))) : 0;  // highest useful step
-  const int s0 = S > 0 ? (1 << (S - 1)) : top;
-#pragma unroll
-  for (int s = s0; s > 0; s >>= 1) {
-    if (s <= top) {
-#pragma unroll
-      for (int u = 0; u < NB; ++u) {
-        const int32_t j = c[u] + s;
-        if (j <= occ[u]) {
-          if (sX[lo[u] + j - 1] <= y[u]) c[u] = j;
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < NB; ++u) r[u] = (y[u] >= a.x0) ? (lo[u] + c[u] - 1) : 0;
-}
-
 struct Counters {
   uint64_t c[7];
   __device__ __forceinline__ void zero() {
@@ -359,17 +312,10 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
     if (full(t)) {
       const int64_t p0 = t * TP + threadIdx.x;
       int2 r[U];
-      {
-        double yy[2 * U];
-        int32_t rr[2 * U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          yy[2 * u] = v[u].x;
-          yy[2 * u + 1] = v[u].y;
-        }
-        lookup_batch<S, MODE, 2 * U>(yy, rr, sX, sD, a);
-#pragma unroll
-        for (int u = 0; u < U; ++u) r[u] = make_int2(rr[2 * u], rr[2 * u + 1]);
+      for (int u = 0; u < U; ++u) {
+        r[u].x = lookup<S, MODE>(v[u].x, sX, sD, a);
+        r[u].y = lookup<S, MODE>(v[u].y, sX, sD, a);
       }
       if (CNT) {
 #pragma unroll
