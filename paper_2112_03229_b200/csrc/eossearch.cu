@@ -226,6 +226,28 @@ eos_status configure(const void* fn, int threads, int64_t smem, int num_sms, int
   return EOS_OK;
 }
 
+// Launch with programmatic stream serialization (PDL), so a kernel's prologue
+// overlaps the previous kernel in the stream (see pdl_enter in kernels.cuh).
+// EOS_PDL=0 disables it (A/B experiments).
+cudaError_t launch(const void* fn, int64_t grid, int threads, size_t smem, cudaStream_t st,
+                   void** params) {
+  static const bool pdl = [] {
+    const char* e = getenv("EOS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelExC(&cfg, fn, params);
+}
+
 eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* out, int64_t gofs,
                          uint64_t* counters, cudaStream_t st) {
   const bool cnt = counters != nullptr;
@@ -251,8 +273,7 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
   int64_t grid = t->clc[cnt] ? tiles : std::min<int64_t>(t->grid[cnt], tiles);
   grid = std::max<int64_t>(grid, 1);
   void* params[] = {&a};
-  EOS_CUDA(cudaLaunchKernel(t->fn[cnt], dim3((unsigned)grid), dim3(t->threads[cnt]), params,
-                            (size_t)t->plan.image_bytes, st));
+  EOS_CUDA(launch(t->fn[cnt], grid, t->threads[cnt], (size_t)t->plan.image_bytes, st, params));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return EOS_OK;
 }
@@ -283,8 +304,7 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   int64_t grid = g->clc ? tiles : std::min<int64_t>(g->grid, tiles);
   grid = std::max<int64_t>(grid, 1);
   void* params[] = {&a};
-  EOS_CUDA(cudaLaunchKernel(g->fn, dim3((unsigned)grid), dim3(g->threads), params,
-                            (size_t)g->image_bytes, st));
+  EOS_CUDA(launch(g->fn, grid, g->threads, (size_t)g->image_bytes, st, params));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return EOS_OK;
 }

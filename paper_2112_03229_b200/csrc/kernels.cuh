@@ -223,6 +223,16 @@ __device__ __forceinline__ void stage_image(uint4* smem, const uint4* __restrict
   mbar_wait(bar, 0);
 }
 
+// Programmatic dependent launch (PDL): the part of a kernel before this call
+// (CTA launch, barrier init, smem image staging -- none of it touches memory
+// other kernels write) may overlap the tail of the previous kernel in the
+// stream; every access to the caller's buffers comes after it.  Then let the
+// next PDL launch in the stream start its own prologue.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Launch shape of search1d (compile-time): threads per CTA, double2 loads in
 // flight per thread per tile, min resident CTAs per SM (register cap:
 // 65536 / (THREADS*MINB) per thread), and the tile schedule:
@@ -258,6 +268,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
   __shared__ __align__(8) uint64_t clc_bar, stage_bar;
   if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
   stage_image(smem, args.image, args.image_16, &stage_bar);
+  pdl_enter();
   const AxisParams a = args.ax;
   EOS_DCHECK(a.d_off + 4 * (int64_t)(a.top - a.base + 1) <= 16 * (int64_t)args.image_16 &&
              a.x_off + 8 * (int64_t)a.n <= a.d_off);
@@ -470,6 +481,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
   __shared__ __align__(8) uint64_t clc_bar, stage_bar;
   if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
   stage_image(smem, A.image, A.image_16, &stage_bar);
+  pdl_enter();
   const char* sm = reinterpret_cast<const char*>(smem);
   const int64_t count = A.count;
   const int64_t ntiles = A.ntiles;

@@ -39,6 +39,14 @@ if has bench5; then
   timeout 900 python bench.py --workload cfg5 --steps 60 --warmup 5 --no-cpu --no-e2e > $OUT/bench_cfg5.json 2> $OUT/bench_cfg5.err; echo "bench cfg5 rc=$?"
   cat $OUT/bench_cfg5.json | head -c 600; echo
 fi
+if has pdlab; then
+  for wl in cfg2 cfg3 cfg4; do
+    for pdl in 0 1 0 1; do
+      EOS_PDL=$pdl timeout 600 python bench.py --workload $wl --steps 300 --warmup 5 --no-cpu --no-e2e > $OUT/pdl_${wl}_$pdl.json 2>/dev/null
+      python -c "import json;d=json.load(open('$OUT/pdl_${wl}_$pdl.json'));print('$wl pdl=$pdl', d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'])"
+    done
+  done
+fi
 if has benchall; then
   for wl in cfg1 cfg3 cfg4 cfg5 paper; do
     timeout 900 python bench.py --workload $wl --steps 100 --warmup 5 --no-cpu > $OUT/bench_$wl.json 2> $OUT/bench_$wl.err; echo "bench $wl rc=$?"
