@@ -40,8 +40,13 @@ extern "C" {
 #endif
 
 #define EOS_MAX_TABLE 16384 /* table entries staged in shared memory (fp64) */
-#define EOS_MAX_K 20        /* mantissa bits appended to the exponent hash */
-#define EOS_K_AUTO (-1)     /* let eos_search_create_ex choose k */
+#define EOS_MAX_K 19        /* mantissa bits appended to the exponent hash */
+#define EOS_K_AUTO (-1)     /* let eos_search_create_ex choose the hash */
+
+/* Bin hash of the directory (eos_search_create_hash / eos_plan_table_hash). */
+#define EOS_HASH_AUTO 0     /* choose kind and parameter by the cost rule */
+#define EOS_HASH_EXPONENT 1 /* param = k: binary exponent + k mantissa bits */
+#define EOS_HASH_LOG 2      /* param = |H|: logarithm hash with |H| bins (Eqs. 1-3) */
 #define EOS_N_COUNTERS 8
 
 typedef enum {
@@ -64,14 +69,16 @@ typedef struct eos_grid2d_s* eos_grid2d;
 typedef struct {
   int64_t n;           /* table entries */
   int32_t key_mode;    /* 0: X[0] >= 0, key = |bits| (sign masked); 1: negatives, order-preserving key */
-  int32_t k;           /* mantissa bits appended to the binary exponent (k = 0: the paper's exponent hash) */
+  int32_t k;           /* exponent hash: mantissa bits appended (k = 0: the paper's exponent hash); log hash: -1 */
   int32_t bins;        /* B: number of bins of the directory */
   int32_t max_occ;     /* largest number of table entries in one bin */
   int32_t steps;       /* S = ceil(log2(max_occ + 1)): fixed in-bin search steps */
-  int32_t base;        /* key >> (20 - k) of the lowest binned entry */
+  int32_t base;        /* hb: key of the lowest binned entry (aligned for the exponent hash) */
   int64_t image_bytes; /* shared-memory image: X fp64[n] (16-B padded) + directory u32[B] */
   int32_t device;      /* CUDA device of the handle (-1 for eos_plan_table) */
   int32_t ctas_per_sm; /* resident CTAs per SM of the search kernel (0 for plan) */
+  int32_t hash_kind;   /* EOS_HASH_EXPONENT or EOS_HASH_LOG */
+  uint32_t hash_mult;  /* M of the bin function below */
 } eos_table_info_t;
 
 /* ---------------------------------------------------------------------------
@@ -83,13 +90,18 @@ typedef struct {
  *   table_host : fp64[n], finite, non-decreasing (duplicates allowed, P:54-56
  *                "monotonically increasing"; -0.0 is canonicalised to +0.0)
  *   n          : 1 <= n <= EOS_MAX_TABLE
- *   k          : EOS_K_AUTO or 0..EOS_MAX_K.  The bin of a value v is
- *                  b(v) = clamp((key(v) >> (52 - k)) - base, 0, B-1),
- *                key = the IEEE-754 binary64 bits with the sign masked
- *                (mode 0); k = 0 is exactly the paper's "Exponent Hash
- *                Search" (bin by the base-2 exponent field),
- *                k > 0 appends the top k mantissa bits (a finer, still
- *                monotone hash; R10/R13).
+ *   k          : EOS_K_AUTO (any hash, see eos_plan_table_hash) or 0..EOS_MAX_K
+ *                (exponent hash).  The bin of a value v is
+ *                  b(v) = min( (max(key(v), hb) - hb) * M >> 32, B-1 ),
+ *                key = the upper 32 bits of the IEEE-754 binary64 pattern,
+ *                sign masked (mode 0): a fixed-point log2 of v.
+ *                Exponent hash, M = 2^(12+k), hb aligned: b = the binary
+ *                exponent plus the top k mantissa bits; k = 0 is exactly the
+ *                paper's "Exponent Hash Search".  Logarithm hash,
+ *                M = |H| 2^32 / span: |H| bins of equal width in log2 (Eqs.
+ *                1-2, with the fixed-point log2; R22).
+ *                Both are monotone, so every bin is a value interval and the
+ *                answer never depends on the hash (R10/R13).
  *   dir_out    : optional (may be NULL) u32[cap]; receives the packed count
  *                directory, entry b = lo_b | (occ_b << 16) with
  *                lo_b = #{j : b(X_j) < b} and occ_b = #{j : b(X_j) == b}
@@ -99,6 +111,13 @@ typedef struct {
  * ------------------------------------------------------------------------- */
 EOS_API eos_status eos_plan_table(const double* table_host, int64_t n, int32_t k, eos_table_info_t* info,
                           uint32_t* dir_out, int64_t cap);
+
+/* Same with an explicit hash: kind EOS_HASH_AUTO (param ignored),
+ * EOS_HASH_EXPONENT (param = k, 0..EOS_MAX_K) or EOS_HASH_LOG (param = |H|,
+ * 1..2^22, the paper's H_size).  EOS_ERR_UNSUPPORTED if the image would not
+ * fit in shared memory (> 200 KB). */
+EOS_API eos_status eos_plan_table_hash(const double* table_host, int64_t n, int32_t kind, int64_t param,
+                               eos_table_info_t* info, uint32_t* dir_out, int64_t cap);
 
 /* ---------------------------------------------------------------------------
  * 1-D search ("Each algorithm takes a targets array (Y, of size m), and
@@ -122,6 +141,10 @@ EOS_API eos_status eos_search_create(const double* table_host, int64_t n, eos_ta
 /* Same with an explicit k (EOS_K_AUTO or 0..EOS_MAX_K).  Results do not
  * depend on k (tested); only speed does. */
 EOS_API eos_status eos_search_create_ex(const double* table_host, int64_t n, int32_t k, eos_table* out);
+
+/* Same with an explicit hash (kind/param as in eos_plan_table_hash). */
+EOS_API eos_status eos_search_create_hash(const double* table_host, int64_t n, int32_t kind, int64_t param,
+                                  eos_table* out);
 
 /* idx_out_dev[i] = lower bound of targets_dev[i], i in [0, count).
  *   targets_dev : fp64[count] device, read once (streaming)

@@ -27,12 +27,14 @@ __all__ = [
     "eos_search_create", "eos_search_create_ex", "eos_search", "eos_search_ex", "eos_search_host",
     "eos_search_destroy", "eos_table_info", "eos_plan_table", "eos_grid2d_create", "eos_interp2d",
     "eos_interp2d_host", "eos_grid2d_destroy", "eos_grid2d_info", "eos_status_str", "EOS_K_AUTO",
-    "EOS_MAX_TABLE", "EOS_MAX_K", "EXPORTED_SYMBOLS",
+    "EOS_MAX_TABLE", "EOS_MAX_K", "EXPORTED_SYMBOLS", "EOS_HASH_AUTO", "EOS_HASH_EXPONENT",
+    "EOS_HASH_LOG", "eos_plan_table_hash", "eos_search_create_hash",
 ]
 
 EOS_MAX_TABLE = 16384
-EOS_MAX_K = 20
+EOS_MAX_K = 19
 EOS_K_AUTO = -1
+EOS_HASH_AUTO, EOS_HASH_EXPONENT, EOS_HASH_LOG = 0, 1, 2
 
 STATUS = {
     0: "EOS_OK", 1: "EOS_ERR_NULL", 2: "EOS_ERR_SIZE", 3: "EOS_ERR_NONFINITE",
@@ -45,7 +47,8 @@ EXPORTED_SYMBOLS = (
     "eos_plan_table", "eos_search_create", "eos_search_create_ex", "eos_search", "eos_search_ex",
     "eos_search_host", "eos_table_info", "eos_search_destroy", "eos_grid2d_create",
     "eos_interp2d", "eos_interp2d_host", "eos_grid2d_info", "eos_grid2d_destroy",
-    "eos_status_str", "eos_abi_version", "eos_launch_count",
+    "eos_status_str", "eos_abi_version", "eos_launch_count", "eos_plan_table_hash",
+    "eos_search_create_hash",
 )
 
 
@@ -60,7 +63,8 @@ class TableInfo(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("key_mode", ctypes.c_int32), ("k", ctypes.c_int32),
                 ("bins", ctypes.c_int32), ("max_occ", ctypes.c_int32), ("steps", ctypes.c_int32),
                 ("base", ctypes.c_int32), ("image_bytes", ctypes.c_int64),
-                ("device", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
+                ("hash_kind", ctypes.c_int32), ("hash_mult", ctypes.c_uint32)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -86,6 +90,8 @@ def load_library():
     L = ctypes.CDLL(path)
     sig = {
         "eos_plan_table": [_P, _I64, _I32, _P, _P, _I64],
+        "eos_plan_table_hash": [_P, _I64, _I32, _I64, _P, _P, _I64],
+        "eos_search_create_hash": [_P, _I64, _I32, _I64, _P],
         "eos_search_create": [_P, _I64, _P],
         "eos_search_create_ex": [_P, _I64, _I32, _P],
         "eos_search": [_P, _P, _I64, _P, _P],
@@ -150,18 +156,39 @@ def _dev(t, dtype_name: str, what: str):
 
 
 # ----------------------------------------------------------- raw C-ABI -----
-def eos_plan_table(table, k: int = EOS_K_AUTO, with_directory: bool = True):
+def _hash_args(k, log_bins):
+    if log_bins is not None:
+        if k not in (None, EOS_K_AUTO):
+            raise ValueError("give k (exponent hash) or log_bins (logarithm hash), not both")
+        return EOS_HASH_LOG, int(log_bins)
+    if k is None or k == EOS_K_AUTO:
+        return EOS_HASH_AUTO, 0
+    if k < 0:
+        return EOS_HASH_EXPONENT, -1   # rejected by the library (EOS_ERR_UNSUPPORTED)
+    return EOS_HASH_EXPONENT, int(k)
+
+
+def eos_plan_table_hash(table, kind: int, param: int, with_directory: bool = True):
     """Host-only plan (no device): (TableInfo, directory u32[bins] | None)."""
     L = load_library()
     X = _f64_host(table)
     info = TableInfo()
-    _check(L.eos_plan_table(X.ctypes.data, X.size, k, ctypes.byref(info), None, 0), "eos_plan_table")
+    _check(L.eos_plan_table_hash(X.ctypes.data, X.size, kind, param, ctypes.byref(info), None, 0),
+           "eos_plan_table")
     d = None
     if with_directory:
         d = np.empty(info.bins, dtype=np.uint32)
-        _check(L.eos_plan_table(X.ctypes.data, X.size, k, ctypes.byref(info), d.ctypes.data, d.size),
-               "eos_plan_table")
+        _check(L.eos_plan_table_hash(X.ctypes.data, X.size, kind, param, ctypes.byref(info),
+                                     d.ctypes.data, d.size), "eos_plan_table")
     return info, d
+
+
+def eos_plan_table(table, k: int | None = EOS_K_AUTO, with_directory: bool = True,
+                   log_bins: int | None = None):
+    """Host-only plan: k = exponent-hash mantissa bits (None/-1 = automatic choice of
+    any hash), or log_bins = |H| of the logarithm hash."""
+    kind, param = _hash_args(k, log_bins)
+    return eos_plan_table_hash(table, kind, param, with_directory)
 
 
 plan_table = eos_plan_table
@@ -176,6 +203,15 @@ def eos_search_create_ex(table, k: int = EOS_K_AUTO) -> int:
     X = _f64_host(table)
     h = ctypes.c_void_p()
     _check(L.eos_search_create_ex(X.ctypes.data, X.size, k, ctypes.byref(h)), "eos_search_create")
+    return h.value
+
+
+def eos_search_create_hash(table, kind: int, param: int) -> int:
+    L = load_library()
+    X = _f64_host(table)
+    h = ctypes.c_void_p()
+    _check(L.eos_search_create_hash(X.ctypes.data, X.size, kind, param, ctypes.byref(h)),
+           "eos_search_create")
     return h.value
 
 
@@ -238,9 +274,11 @@ def eos_grid2d_destroy(handle) -> None:
 class Table:
     """A search table bound to the current CUDA device (eos_search_create)."""
 
-    def __init__(self, table, k: int | None = None):
+    def __init__(self, table, k: int | None = None, log_bins: int | None = None):
+        """k: exponent hash with k mantissa bits; log_bins: logarithm hash with |H| bins;
+        neither: the automatic choice.  Results never depend on it."""
         self.X = _f64_host(table).copy()
-        self._h = eos_search_create_ex(self.X, EOS_K_AUTO if k is None else k)
+        self._h = eos_search_create_hash(self.X, *_hash_args(k, log_bins))
         self.info = eos_table_info(self._h)
 
     @property

@@ -13,21 +13,34 @@ namespace eos {
 // Bin-key of a binary64 value, host side.  Must equal the device key in
 // kernels.cuh bit for bit (tested through eos_plan_table vs the kernels).
 //   mode 0 (X[0] >= 0): hi = upper 32 bits of |v| (sign masked).  For v >= 0
-//     the upper word is (biased exponent << 20) | top 20 mantissa bits, so
-//     hi >> (20 - k) is the paper's exponent hash refined by k
-//     mantissa bits; it is monotone non-decreasing in v >= 0.
+//     the upper word is (biased exponent << 20) | top 20 mantissa bits: a
+//     fixed-point log2(v) (exact at powers of two, linear in the mantissa in
+//     between), monotone non-decreasing in v >= 0.
 //   mode 1 (negatives present): order-preserving transform of the bits of
 //     (v + 0.0) (canonicalises -0.0), monotone over all non-NaN doubles.
 uint32_t key_hi(double v, int mode);
 
+// The one bin function of both hashes (host copy of kernels.cuh::bin_of):
+//   bin(v) = min( umulhi( max(key_hi(v), hb) - hb, M ), bmax )
+// Exponent hash with k mantissa bits: M = 2^(12+k), hb aligned
+// down to a multiple of 2^(20-k)  =>  bin = (key >> (20-k)) - (hb >> (20-k)).
+// Logarithm hash with |H| bins (Eqs. 1-2): M = |H| 2^32 / span,
+// i.e. floor((log2~(v) - log2~(X_lo)) / log2~(b)) with the fixed-point log2~.
+inline uint32_t bin_of_key(uint32_t key, uint32_t hb, uint32_t M, uint32_t bmax) {
+  const uint32_t h = (key > hb ? key : hb) - hb;
+  const uint32_t b = (uint32_t)(((uint64_t)h * (uint64_t)M) >> 32);
+  return b < bmax ? b : bmax;
+}
+
 struct TablePlan {
   int64_t n = 0;
   int key_mode = 0;
-  int k = 0;
-  int shift = 20;          // 20 - k
-  uint32_t base = 0;       // key_hi(X_lo) >> shift
-  uint32_t top = 0;        // key_hi(X[n-1]) >> shift
-  int bins = 0;            // top - base + 1
+  int hash_kind = 0;       // EOS_HASH_EXPONENT | EOS_HASH_LOG
+  int k = 0;               // exponent hash: mantissa bits; log hash: -1
+  uint32_t hb = 0;         // key of the lowest binned entry (aligned for the exponent hash)
+  uint32_t M = 0;          // bin multiplier
+  uint32_t bmax = 0;       // bins - 1
+  int bins = 0;
   int max_occ = 0;
   int steps = 0;           // ceil(log2(max_occ + 1))
   std::vector<double> X;   // canonicalised table (-0.0 -> +0.0)
@@ -36,15 +49,18 @@ struct TablePlan {
   int64_t image_bytes = 0; // X region + directory (16-B padded)
 };
 
-// Smem budget used by the automatic k choice (bytes of X + directory): one
+// Smem budget used by the automatic hash choice (bytes of X + directory): one
 // image copy per SM at the 1024-thread launch shape.  Measured: a larger
 // image that removes an in-bin step wins (cfg5 k=9/S=3 at 138 KB beats
 // k=7/S=4 at 59 KB by 6%; cfg1 k=9/S=1 beats k=5/S=2 by 3%).
 constexpr int64_t kAutoImageBudget = 200 * 1024;
+constexpr int64_t kMaxImage = 200 * 1024;  // explicit requests beyond this do not fit in smem
 
-// Validate + build (eos_plan_table semantics).  k_req: EOS_K_AUTO or 0..EOS_MAX_K.
-// strict: axes of a 2-D grid must be strictly increasing and n >= 2.
-eos_status plan_table(const double* X, int64_t n, int k_req, bool strict, TablePlan* out);
+// Validate + build (eos_plan_table_hash semantics).  kind/param: see
+// eossearch.h (EOS_HASH_AUTO ignores param).  strict: axes of a 2-D grid must
+// be strictly increasing and n >= 2.
+eos_status plan_table(const double* X, int64_t n, int kind, int64_t param, bool strict,
+                      TablePlan* out);
 
 // Serialise X | dir into a 16-B padded byte image.
 std::vector<uint8_t> make_image(const TablePlan& p);

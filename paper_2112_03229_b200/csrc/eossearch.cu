@@ -180,9 +180,9 @@ dv::AxisParams axis_params(const TablePlan& p, int32_t x_off) {
   a.n = (int32_t)p.n;
   a.x_off = x_off;
   a.d_off = x_off + (int32_t)p.x_bytes;
-  a.shift = p.shift;
-  a.base = p.base;
-  a.top = p.top;
+  a.hb = p.hb;
+  a.M = p.M;
+  a.bmax = p.bmax;
   a.steps = std::max(p.steps, 1);
   a.x0 = p.X[0];
   a.xlast = p.X[p.n - 1];
@@ -386,11 +386,19 @@ int32_t eos_abi_version(void) { return 1; }
 
 int64_t eos_launch_count(void) { return g_launches.load(); }
 
+static int kind_of_k(int32_t k) { return k == EOS_K_AUTO ? EOS_HASH_AUTO : EOS_HASH_EXPONENT; }
+
 eos_status eos_plan_table(const double* table_host, int64_t n, int32_t k, eos_table_info_t* info,
                           uint32_t* dir_out, int64_t cap) {
+  if (k != EOS_K_AUTO && k < 0) return EOS_ERR_UNSUPPORTED;
+  return eos_plan_table_hash(table_host, n, kind_of_k(k), k, info, dir_out, cap);
+}
+
+eos_status eos_plan_table_hash(const double* table_host, int64_t n, int32_t kind, int64_t param,
+                               eos_table_info_t* info, uint32_t* dir_out, int64_t cap) {
   if (!info) return EOS_ERR_NULL;
   TablePlan p;
-  eos_status st = eos::plan_table(table_host, n, k, false, &p);
+  eos_status st = eos::plan_table(table_host, n, kind, param, false, &p);
   if (st != EOS_OK) return st;
   if (dir_out) {
     if (cap < p.bins) return EOS_ERR_SIZE;
@@ -401,11 +409,17 @@ eos_status eos_plan_table(const double* table_host, int64_t n, int32_t k, eos_ta
 }
 
 eos_status eos_search_create_ex(const double* table_host, int64_t n, int32_t k, eos_table* out) {
+  if (k != EOS_K_AUTO && k < 0) return EOS_ERR_UNSUPPORTED;
+  return eos_search_create_hash(table_host, n, kind_of_k(k), k, out);
+}
+
+eos_status eos_search_create_hash(const double* table_host, int64_t n, int32_t kind, int64_t param,
+                                  eos_table* out) {
   if (!out) return EOS_ERR_NULL;
   *out = nullptr;
   eos_table t = new (std::nothrow) eos_table_s();
   if (!t) return EOS_ERR_NOMEM;
-  eos_status st = eos::plan_table(table_host, n, k, false, &t->plan);
+  eos_status st = eos::plan_table(table_host, n, kind, param, false, &t->plan);
   if (st != EOS_OK) { delete t; return st; }
   cudaError_t e = cudaGetDevice(&t->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, t->device);
@@ -512,8 +526,8 @@ eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double
   if (!rho_host || !T_host || !P_host) return EOS_ERR_NULL;
   eos_grid2d g = new (std::nothrow) eos_grid2d_s();
   if (!g) return EOS_ERR_NOMEM;
-  eos_status st = eos::plan_table(rho_host, n_rho, EOS_K_AUTO, true, &g->pr);
-  if (st == EOS_OK) st = eos::plan_table(T_host, n_T, EOS_K_AUTO, true, &g->pt);
+  eos_status st = eos::plan_table(rho_host, n_rho, EOS_HASH_AUTO, 0, true, &g->pr);
+  if (st == EOS_OK) st = eos::plan_table(T_host, n_T, EOS_HASH_AUTO, 0, true, &g->pt);
   if (st == EOS_OK && (g->pr.key_mode != 0 || g->pt.key_mode != 0)) st = EOS_ERR_UNSUPPORTED;
   if (st != EOS_OK) { delete g; return st; }
   const int64_t ncell = n_rho * n_T;

@@ -46,11 +46,10 @@ struct AxisParams {
   int32_t n;        // entries
   int32_t x_off;    // byte offset of X (fp64[n]) in the smem image
   int32_t d_off;    // byte offset of the directory (u32[bins])
-  int32_t shift;    // 20 - k
-  uint32_t base;    // lowest bin key
-  uint32_t top;     // highest bin key
+  uint32_t hb;      // key of the lowest binned entry
+  uint32_t M;       // bin multiplier (exponent hash: 2^(12+k); log hash: |H| 2^32 / span)
+  uint32_t bmax;    // bins - 1
   int32_t steps;    // S (used by the runtime-S path)
-  int32_t pad_;
   double x0;        // X[0]
   double xlast;     // X[n-1]
 };
@@ -85,18 +84,22 @@ __device__ __forceinline__ uint32_t key_hi(double y) {
   return h ^ ((uint32_t)((int32_t)h >> 31) | 0x80000000u);
 }
 
+// The bin function of both hashes (host copy: eos_internal.h::bin_of_key).
+__device__ __forceinline__ uint32_t bin_of(uint32_t key, const AxisParams& a) {
+  return min(__umulhi(max(key, a.hb) - a.hb, a.M), a.bmax);
+}
+
 // The hot per-target body:
-//   bin b = clamp(key >> shift, base, top) - base           (exponent hash + k bits)
+//   bin b = min(umulhi(max(key, hb) - hb, M), B-1)          (exponent / log hash)
 //   lo, occ = directory[b]                                  (count directory)
 //   c = #{j < occ : X[lo + j] <= y}  by S-step binary lifting (branchless)
 //   idx = (y >= X[0]) ? lo + c - 1 : 0                      (P:54 fix-up; NaN -> 0)
 template <int S, int MODE>
 __device__ __forceinline__ int32_t lookup(double y, const double* __restrict__ sX,
                                           const uint32_t* __restrict__ sD, const AxisParams& a) {
-  uint32_t kb = key_hi<MODE>(y) >> a.shift;
-  kb = min(max(kb, a.base), a.top);
-  EOS_DCHECK(kb - a.base <= a.top - a.base);
-  const uint32_t d = sD[kb - a.base];
+  const uint32_t b = bin_of(key_hi<MODE>(y), a);
+  EOS_DCHECK(b <= a.bmax);
+  const uint32_t d = sD[b];
   const int32_t lo = (int32_t)(d & 0xFFFFu);
   const int32_t occ = (int32_t)(d >> 16);
   EOS_DCHECK(lo + occ <= a.n && occ < (1 << (S > 0 ? S : a.steps)));
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
   stage_image(smem, args.image, args.image_16, &stage_bar);
   pdl_enter();
   const AxisParams a = args.ax;
-  EOS_DCHECK(a.d_off + 4 * (int64_t)(a.top - a.base + 1) <= 16 * (int64_t)args.image_16 &&
+  EOS_DCHECK(a.d_off + 4 * ((int64_t)a.bmax + 1) <= 16 * (int64_t)args.image_16 &&
              a.x_off + 8 * (int64_t)a.n <= a.d_off);
   const double* __restrict__ sX =
       reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
@@ -404,9 +407,7 @@ __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ s
                                           const uint32_t* __restrict__ sD, const AxisParams& a,
                                           int32_t& i, int32_t& ci, double& xl, double& xr) {
   if (S == 1) {
-    uint32_t kb = key_hi<0>(y) >> a.shift;
-    kb = min(max(kb, a.base), a.top);
-    const uint32_t d = sD[kb - a.base];
+    const uint32_t d = sD[bin_of(key_hi<0>(y), a)];
     const int32_t lo = (int32_t)(d & 0xFFFFu);  // <= n-1: X[n-1] lies in the top bin
     const int32_t occ = (int32_t)(d >> 16);     // 0 or 1 when S == 1
     EOS_DCHECK(lo < a.n && occ <= 1);

@@ -1,7 +1,7 @@
 // table_build.cpp -- host-side setup of a search table (runs once per table,
 // P:276 "Hashtable generation time is O(n)", "search setup ... performed
 // only once").  Validation, canonicalisation, bin key, count directory and the
-// choice of k.  Product path: shares no code with oracle/.
+// choice of hash.  Product path: shares no code with oracle/.
 #include <math.h>
 #include <string.h>
 
@@ -33,63 +33,122 @@ int ceil_log2_plus1(int occ) {  // S = ceil(log2(occ + 1)), occ >= 0
 
 int64_t pad16(int64_t b) { return (b + 15) & ~int64_t(15); }
 
-// Bin range for a given k (no directory yet).
-void bin_range(const std::vector<double>& X, int mode, int k, uint32_t* base, uint32_t* top) {
-  const int shift = 20 - k;
+// Key of the lowest binned entry.  Mode 0: the first strictly positive entry
+// (a 0.0 head clamps into bin 0; R13); an all-zero table gives a
+// single bin.  Mode 1: X[0].
+uint32_t low_key(const std::vector<double>& X, int mode) {
   const int64_t n = (int64_t)X.size();
-  double lo = X[n - 1];
-  if (mode == 0) {
-    // lowest binned entry: first strictly positive one (a 0.0 head clamps into
-    // bin 0; R13).  All-zero table -> a single bin.
-    for (int64_t j = 0; j < n; ++j)
-      if (X[j] > 0.0) { lo = X[j]; break; }
-  } else {
-    lo = X[0];
-  }
-  *base = key_hi(lo, mode) >> shift;
-  *top = key_hi(X[n - 1], mode) >> shift;
+  if (mode == 1) return key_hi(X[0], 1);
+  for (int64_t j = 0; j < n; ++j)
+    if (X[j] > 0.0) return key_hi(X[j], 0);
+  return key_hi(X[n - 1], 0);
 }
 
-eos_status build_for_k(const std::vector<double>& X, int mode, int k, TablePlan* p) {
-  const int64_t n = (int64_t)X.size();
-  uint32_t base, top;
-  bin_range(X, mode, k, &base, &top);
-  const int64_t bins = (int64_t)top - (int64_t)base + 1;
-  if (bins < 1 || bins > (1 << 22)) return EOS_ERR_UNSUPPORTED;
+// Bin parameters of a hash; returns the number of bins (0 if unusable).
+struct HashParams {
+  int kind, k;
+  uint32_t hb, M, bmax;
+  int64_t bins;
+};
+
+HashParams exponent_params(const std::vector<double>& X, int mode, int k) {
+  HashParams h{EOS_HASH_EXPONENT, k, 0, 0, 0, 0};
   const int shift = 20 - k;
-  std::vector<uint32_t> occ((size_t)bins, 0);
-  for (int64_t j = 0; j < n; ++j) {
-    uint32_t kb = key_hi(X[j], mode) >> shift;
-    kb = std::min(std::max(kb, base), top);
-    occ[kb - base]++;
-  }
-  p->dir.assign((size_t)bins, 0);
+  const uint32_t lo = low_key(X, mode), top = key_hi(X.back(), mode);
+  h.hb = lo & ~((1u << shift) - 1u);
+  h.M = 1u << (12 + k);
+  h.bins = (int64_t)((top - h.hb) >> shift) + 1;
+  h.bmax = (uint32_t)(h.bins - 1);
+  return h;
+}
+
+HashParams log_params(const std::vector<double>& X, int mode, int64_t H) {
+  // Eq. 1: |H| bins of equal width in log2~ over [X_lo, X_max];
+  // M = floor(|H| 2^32 / (span + 1)) keeps every bin index below |H|.
+  HashParams h{EOS_HASH_LOG, -1, 0, 0, 0, 0};
+  const uint32_t lo = low_key(X, mode), top = key_hi(X.back(), mode);
+  h.hb = lo;
+  const uint64_t span = (uint64_t)(top - lo) + 1;
+  uint64_t M = ((uint64_t)H << 32) / span;
+  M = std::max<uint64_t>(1, std::min<uint64_t>(M, 0xFFFFFFFFull));
+  h.M = (uint32_t)M;
+  h.bins = (int64_t)bin_of_key(top, h.hb, h.M, 0xFFFFFFFFu) + 1;
+  h.bmax = (uint32_t)(h.bins - 1);
+  return h;
+}
+
+int64_t image_of(int64_t n, int64_t bins) { return pad16(8 * n) + pad16(4 * bins); }
+
+eos_status build(const std::vector<double>& X, int mode, const HashParams& h, TablePlan* p) {
+  const int64_t n = (int64_t)X.size();
+  if (h.bins < 1 || h.bins > (int64_t(1) << 22)) return EOS_ERR_UNSUPPORTED;
+  std::vector<uint32_t> occ((size_t)h.bins, 0);
+  for (int64_t j = 0; j < n; ++j) occ[bin_of_key(key_hi(X[j], mode), h.hb, h.M, h.bmax)]++;
+  p->dir.assign((size_t)h.bins, 0);
   uint32_t lo = 0, mx = 0;
-  for (int64_t b = 0; b < bins; ++b) {
+  for (int64_t b = 0; b < h.bins; ++b) {
     p->dir[b] = lo | (occ[b] << 16);
     lo += occ[b];
     mx = std::max(mx, occ[b]);
   }
   p->n = n;
   p->key_mode = mode;
-  p->k = k;
-  p->shift = shift;
-  p->base = base;
-  p->top = top;
-  p->bins = (int)bins;
+  p->hash_kind = h.kind;
+  p->k = h.k;
+  p->hb = h.hb;
+  p->M = h.M;
+  p->bmax = h.bmax;
+  p->bins = (int)h.bins;
   p->max_occ = (int)mx;
   p->steps = ceil_log2_plus1((int)mx);
   p->x_bytes = pad16(8 * n);
-  p->image_bytes = p->x_bytes + pad16(4 * bins);
+  p->image_bytes = image_of(n, h.bins);
+  return EOS_OK;
+}
+
+// Automatic choice: the smallest fixed in-bin step count S
+// reachable with an image within kAutoImageBudget; ties -> the smaller image
+// (fewer bins), then the exponent hash.  Candidates: the exponent hash for
+// every k, and the logarithm hash for |H| on a geometric grid (8 per octave).
+eos_status plan_auto(const std::vector<double>& X, int mode, TablePlan* out) {
+  const int64_t n = (int64_t)X.size();
+  TablePlan best;
+  bool have = false;
+  auto consider = [&](const HashParams& h) {
+    if (h.bins < 1) return;
+    if (have && image_of(n, h.bins) > kAutoImageBudget) return;
+    TablePlan p;
+    if (build(X, mode, h, &p) != EOS_OK) return;
+    if (!have || p.steps < best.steps ||
+        (p.steps == best.steps && p.image_bytes < best.image_bytes)) {
+      best = std::move(p);
+      have = true;
+    }
+  };
+  for (int k = 0; k <= EOS_MAX_K; ++k) {
+    HashParams h = exponent_params(X, mode, k);
+    if (k > 0 && image_of(n, h.bins) > kAutoImageBudget) break;
+    consider(h);
+  }
+  const int64_t max_bins = (kAutoImageBudget - pad16(8 * n)) / 4;
+  for (double H = 1.0; H <= (double)max_bins; H *= 1.0905077326652577 /* 2^(1/8) */) {
+    consider(log_params(X, mode, (int64_t)H));
+  }
+  if (!have) return EOS_ERR_UNSUPPORTED;
+  *out = std::move(best);
   return EOS_OK;
 }
 
 }  // namespace
 
-eos_status plan_table(const double* Xin, int64_t n, int k_req, bool strict, TablePlan* out) {
+eos_status plan_table(const double* Xin, int64_t n, int kind, int64_t param, bool strict,
+                      TablePlan* out) {
   if (!Xin || !out) return EOS_ERR_NULL;
   if (n < (strict ? 2 : 1) || n > EOS_MAX_TABLE) return EOS_ERR_SIZE;
-  if (k_req != EOS_K_AUTO && (k_req < 0 || k_req > EOS_MAX_K)) return EOS_ERR_UNSUPPORTED;
+  if (kind == EOS_HASH_EXPONENT && (param < 0 || param > EOS_MAX_K)) return EOS_ERR_UNSUPPORTED;
+  if (kind == EOS_HASH_LOG && (param < 1 || param > (int64_t(1) << 22))) return EOS_ERR_UNSUPPORTED;
+  if (kind != EOS_HASH_AUTO && kind != EOS_HASH_EXPONENT && kind != EOS_HASH_LOG)
+    return EOS_ERR_UNSUPPORTED;
   std::vector<double> X((size_t)n);
   for (int64_t j = 0; j < n; ++j) {
     double v = Xin[j];
@@ -101,38 +160,19 @@ eos_status plan_table(const double* Xin, int64_t n, int k_req, bool strict, Tabl
   }
   const int mode = (X[0] >= 0.0) ? 0 : 1;
 
-  if (k_req != EOS_K_AUTO) {
-    TablePlan p;
-    eos_status st = build_for_k(X, mode, k_req, &p);
-    if (st != EOS_OK) return st;
-    if (p.image_bytes > 200 * 1024) return EOS_ERR_UNSUPPORTED;  // does not fit in smem
-    p.X = std::move(X);
-    *out = std::move(p);
-    return EOS_OK;
+  TablePlan p;
+  eos_status st;
+  if (kind == EOS_HASH_AUTO) {
+    st = plan_auto(X, mode, &p);
+  } else {
+    const HashParams h = kind == EOS_HASH_EXPONENT ? exponent_params(X, mode, (int)param)
+                                                   : log_params(X, mode, param);
+    st = build(X, mode, h, &p);
+    if (st == EOS_OK && p.image_bytes > kMaxImage) st = EOS_ERR_UNSUPPORTED;
   }
-
-  // Automatic k: the smallest fixed in-bin step count S
-  // reachable with an image within kAutoImageBudget; ties -> smallest k
-  // (smaller directory).  Bins only grow with k, so stop at the budget.
-  TablePlan best;
-  bool have = false;
-  for (int k = 0; k <= EOS_MAX_K; ++k) {
-    uint32_t base, top;
-    bin_range(X, mode, k, &base, &top);
-    int64_t bins = (int64_t)top - (int64_t)base + 1;
-    int64_t img = pad16(8 * n) + pad16(4 * bins);
-    if (have && img > kAutoImageBudget) break;
-    TablePlan p;
-    if (build_for_k(X, mode, k, &p) != EOS_OK) break;
-    if (!have || p.steps < best.steps) {
-      best = std::move(p);
-      have = true;
-    }
-    if (best.steps <= 1) break;  // cannot do better than one probe
-  }
-  if (!have) return EOS_ERR_UNSUPPORTED;
-  best.X = std::move(X);
-  *out = std::move(best);
+  if (st != EOS_OK) return st;
+  p.X = std::move(X);
+  *out = std::move(p);
   return EOS_OK;
 }
 
@@ -150,10 +190,12 @@ void fill_info(const TablePlan& p, eos_table_info_t* info) {
   info->bins = p.bins;
   info->max_occ = p.max_occ;
   info->steps = p.steps;
-  info->base = (int32_t)p.base;
+  info->base = (int32_t)p.hb;
   info->image_bytes = p.image_bytes;
   info->device = -1;
   info->ctas_per_sm = 0;
+  info->hash_kind = p.hash_kind;
+  info->hash_mult = p.M;
 }
 
 }  // namespace eos

@@ -30,8 +30,8 @@ def to_dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
 
 
-def gpu_search(X, Y, k=None, **kw):
-    t = eos.Table(X, k=k)
+def gpu_search(X, Y, k=None, log_bins=None, **kw):
+    t = eos.Table(X, k=k, log_bins=log_bins)
     out = t.search(to_dev(Y), **kw)
     torch.cuda.synchronize()
     r = out.cpu().numpy()
@@ -93,8 +93,10 @@ def test_golden_cases_every_k(name):
     X, cases = lower_bound_cases()[name]
     ys = np.array([c[0] for c in cases] * 37)  # repeated: crosses the vector body and tail
     exp = np.array([c[1] for c in cases] * 37, dtype=np.int32)
-    for k in feasible_ks(X, [None, 0, 1, 2, 4, 8, 12, 20]):
+    for k in feasible_ks(X, [None, 0, 1, 2, 4, 8, 12, 19]):
         assert_same(gpu_search(X, ys, k=k), exp, ys)
+    for H in (1, 2, 3, 17, 1000):   # the logarithm hash, any |H|
+        assert_same(gpu_search(X, ys, log_bins=H), exp, ys)
 
 
 def _edge_tables(rng, count):
@@ -141,6 +143,8 @@ def test_edge_tables_exhaustive_probes_every_k():
         for k in feasible_ks(X, [None, 0, 1, 3, 6, 10]):
             assert_same(gpu_search(X, P, k=k), ref, P)
             checked += P.size
+        for H in (1, 5, 300):
+            assert_same(gpu_search(X, P, log_bins=H), ref, P)
     assert checked > 100_000
 
 
@@ -150,6 +154,8 @@ def test_cfg1_full_every_k():
     ref = oracle.search(w.table, Y)
     for k in feasible_ks(w.table, [None] + list(range(0, 16))):
         assert_same(gpu_search(w.table, Y, k=k), ref, Y)
+    for H in (1, 10, 64, 500, 1722, 5000, 40000):
+        assert_same(gpu_search(w.table, Y, log_bins=H), ref, Y)
 
 
 @pytest.mark.parametrize("count", [0, 1, 2, 3, 5, 511, 2047, 2048, 2049, 4097, 65_537, 1_000_003])
@@ -293,8 +299,8 @@ def test_cfg5_full_sampled_invariant_counters():
     ref = oracle.counters(w.table, Yh, oracle.search(w.table, Yh), off)
     torch.cuda.synchronize()
     assert np.array_equal(c.cpu().numpy().view(np.uint64), ref)
-    for k in (0, 9):
-        tk = eos.Table(w.table, k=k)
+    for kw in ({"k": 0}, {"k": 7}, {"k": 9}, {"log_bins": 5000}):
+        tk = eos.Table(w.table, **kw)
         assert torch.equal(tk.search(Yd[off:off + m]), out[off:off + m])
         tk.close()
     t.close()

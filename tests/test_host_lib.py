@@ -215,3 +215,80 @@ def test_mode1_directory_monotone_over_mixed_signs():
             assert info.key_mode == 1
             assert lo[0] == 0 and lo[-1] + occ[-1] == X.size
             assert np.all(lo[1:] == lo[:-1] + occ[:-1])
+
+
+# ------------------------------------------------------ logarithm hash (f1) --
+def _keys(X):
+    return ((np.asarray(X, dtype=np.float64).view(np.uint64) >> np.uint64(32)) &
+            np.uint64(0x7FFFFFFF)).astype(np.int64)
+
+
+@pytest.mark.parametrize("H", [1, 2, 7, 34, 110, 1000, 20000])
+def test_log_hash_directory_and_eq1_range(H):
+    """'any value we search for that is within [Xmin, Xmax] must satisfy
+    0 <= hash(x) < |H|' -- and the directory is the exact count over those bins."""
+    rng = np.random.default_rng(H)
+    for _ in range(20):
+        X = np.sort(10.0 ** rng.uniform(-6, 6, int(rng.integers(1, 500))))
+        info, d = eos.plan_table(X, log_bins=H)
+        lo, occ = unpack(d)
+        assert info.hash_kind == eos.EOS_HASH_LOG and info.k == -1
+        assert 1 <= info.bins <= H
+        assert lo[0] == 0 and lo[-1] + occ[-1] == X.size
+        assert np.all(lo[1:] == lo[:-1] + occ[:-1])
+        # recount: bin = floor((key - key(X0)) * M / 2^32), the fixed-point log2 scaled
+        kx = _keys(X)
+        b = ((kx - kx[0]) * int(info.hash_mult)) >> 32
+        assert b.max() == info.bins - 1 < H
+        assert np.array_equal(np.bincount(b, minlength=info.bins), occ)
+        # monotone in the value, equal-width in log2 up to the bit-pattern approximation
+        assert np.all(np.diff(b) >= 0)
+
+
+def test_log_hash_bins_have_equal_log_width():
+    """Eq. 1: bins of equal width in log_b; with the fixed-point log2 of the
+    IEEE bits the width is constant in key units, and within 0.09 log2 of the true log."""
+    X = datagen_table()
+    info, _ = eos.plan_table(X, log_bins=34)
+    kx = _keys(X)
+    approx_log2 = kx / 2.0 ** 20 - 1023
+    assert np.max(np.abs(approx_log2 - np.log2(X))) < 0.0861
+    width_log2 = 2.0 ** 32 / info.hash_mult / 2 ** 20
+    assert abs(width_log2 * 34 - (approx_log2[-1] - approx_log2[0])) < 2 * width_log2
+
+
+def datagen_table():
+    import datagen
+    return datagen.table_paper_exemplar()
+
+
+def test_log_hash_brackets_oracle_answer():
+    import datagen
+    for name in ("cfg1", "cfg2", "cfg5"):
+        w = datagen.workload(name, count=2000)
+        X = w.table
+        Y = np.concatenate([w.targets.host_fill(0, w.count, X), X, np.nextafter(X, 0)])
+        ref = oracle.search(X, Y)
+        kx = _keys(X)
+        for H in (5, 64, 999):
+            info, d = eos.plan_table(X, log_bins=H)
+            lo, occ = unpack(d)
+            ky = _keys(Y)
+            b = np.minimum(((np.maximum(ky, info.base) - info.base) * int(info.hash_mult)) >> 32,
+                           info.bins - 1)
+            inr = Y >= X[0]
+            assert np.all(lo[b][inr] <= ref[inr] + 1)
+            assert np.all(ref[inr] + 1 <= lo[b][inr] + occ[b][inr])
+
+
+def test_auto_choice_prefers_fewer_steps_then_smaller_image():
+    import datagen
+    X = datagen.table_cfg1()
+    auto, _ = eos.plan_table(X)
+    for k in range(0, 12):
+        try:
+            e, _ = eos.plan_table(X, k)
+        except eos.EosError:
+            continue
+        assert (auto.steps, auto.image_bytes) <= (e.steps, e.image_bytes) or auto.steps < e.steps
+    assert auto.steps == 1 and auto.image_bytes < 16 * 1024
