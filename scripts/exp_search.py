@@ -49,6 +49,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--count", type=int, default=None)
     ap.add_argument("--ks", default="")
+    ap.add_argument("--logbins", default="")
+    ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--variants", default=",".join(VARIANTS))
     a = ap.parse_args()
     dev = torch.device("cuda:0")
@@ -87,17 +89,21 @@ def main():
         res[key] = r
         t.close()
     os.environ.pop("EOS_SEARCH_VARIANT", None)
-    for k in [int(x) for x in a.ks.split(",") if x]:
+    plans = [("k%d" % int(x), {"k": int(x)}) for x in a.ks.split(",") if x]
+    plans += [("H%d" % int(x), {"log_bins": int(x)}) for x in a.logbins.split(",") if x]
+    plans = plans * a.repeat
+    for name, kw in plans:
         try:
-            t = eos.Table(w.table, k=k)
+            t = eos.Table(w.table, **kw)
         except eos.EosError as e:
-            res[f"k{k}"] = str(e)
+            res[name] = str(e)
             continue
+        k = name + ("_2" if name in res else "")
         r = time_fn(lambda: eos.eos_search(t.handle, Y.data_ptr(), n, out.data_ptr(), st), a.steps)
         r["GBps_median"] = algo / r["median_ms"] / 1e6
         r["info"] = t.info.as_dict()
         r["same_as_first"] = bool(torch.equal(out, ref_out)) if ref_out is not None else None
-        res[f"k{k}"] = r
+        res[k] = r
         t.close()
 
     # CUDA graph of 20 launches (default variant)

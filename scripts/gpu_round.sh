@@ -77,6 +77,11 @@ if has torchrun1; then
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 200 --warmup 5 --no-cpu > $OUT/bench_torchrun1.json 2> $OUT/bench_torchrun1.err; echo "torchrun1 rc=$?"
   cat $OUT/bench_torchrun1.json; tail -n 3 $OUT/bench_torchrun1.err
 fi
+if has exph; then
+  timeout 900 python scripts/exp_search.py --workload cfg2 --variants default --ks 4,5,6 --logbins 256,512,957,2000 --repeat 2 > $OUT/exph_cfg2.json 2> $OUT/exph.err; echo "exph cfg2 rc=$?"
+  timeout 900 python scripts/exp_search.py --workload cfg5 --count 1073741824 --steps 40 --variants default --ks 7,9 --logbins 8192,16384,24000 --repeat 2 > $OUT/exph_cfg5.json 2>> $OUT/exph.err; echo "exph cfg5 rc=$?"
+  tail -n 3 $OUT/exph.err
+fi
 if has ncu2; then
   for wl in cfg4 cfg5; do
     CMD="python bench.py --workload $wl --count 268435456 --steps 5 --warmup 2 --no-e2e --no-cpu --eager"
