@@ -106,22 +106,69 @@ eos_status build(const std::vector<double>& X, int mode, const HashParams& h, Ta
   return EOS_OK;
 }
 
-// Automatic choice: the smallest fixed in-bin step count S
-// reachable with an image within kAutoImageBudget; ties -> the smaller image
-// (fewer bins), then the exponent hash.  Candidates: the exponent hash for
-// every k, and the logarithm hash for |H| on a geometric grid (8 per octave).
+// Expected executed (non-predicated) probes of S-step binary lifting in a bin
+// holding `o` entries, the target uniform among the o+1 gaps.
+double lifting_probes(int o, int S) {
+  double total = 0.0;
+  for (int cf = 0; cf <= o; ++cf) {  // final count of entries <= target
+    int c = 0;
+    for (int s = S > 0 ? 1 << (S - 1) : 0; s > 0; s >>= 1) {
+      const int j = c + s;
+      if (j <= o) {
+        total += 1.0;
+        if (j <= cf) c = j;
+      }
+    }
+  }
+  return total / (o + 1);
+}
+
+// Modelled per-lookup cost of a plan, in shared-memory
+// wavefronts per warp of 32 lookups plus issue and occupancy terms:
+//   3.5 (random 4-B directory read) + 6.1 x E[executed 8-B probes]
+//   + 1 per in-bin step (issue) + image penalty (fewer / larger CTAs:
+//   0 up to 48 KB = 4 CTAs x 256, 0.5 up to 100 KB, 1 above).
+// Targets are taken log-uniform over the table range, i.e. uniform over the
+// bins (equal key width).  Calibrated on cfg2/cfg5 A/B runs
+// (profiles/r01_exp_hash_*.json).
+double plan_cost(const TablePlan& p) {
+  std::vector<double> memo(64, -1.0);
+  double probes = 0.0;
+  for (uint32_t d : p.dir) {
+    const int o = (int)(d >> 16);
+    double v;
+    if (o < 64) {
+      if (memo[o] < 0) memo[o] = lifting_probes(o, p.steps);
+      v = memo[o];
+    } else {
+      v = lifting_probes(o, p.steps);
+    }
+    probes += v;
+  }
+  probes /= (double)p.bins;
+  const double img = p.image_bytes <= 48 * 1024 ? 0.0 : (p.image_bytes <= 100 * 1024 ? 0.5 : 1.0);
+  return 3.5 + 6.1 * probes + 1.0 * p.steps + img;
+}
+
+// Automatic choice: the candidate of least plan_cost with an
+// image within kAutoImageBudget; ties -> the smaller image, then the exponent
+// hash.  Candidates: the exponent hash for every k, and the logarithm hash
+// for |H| on a geometric grid (8 per octave).
 eos_status plan_auto(const std::vector<double>& X, int mode, TablePlan* out) {
   const int64_t n = (int64_t)X.size();
   TablePlan best;
+  double best_cost = 0.0;
   bool have = false;
   auto consider = [&](const HashParams& h) {
     if (h.bins < 1) return;
     if (have && image_of(n, h.bins) > kAutoImageBudget) return;
     TablePlan p;
     if (build(X, mode, h, &p) != EOS_OK) return;
-    if (!have || p.steps < best.steps ||
-        (p.steps == best.steps && p.image_bytes < best.image_bytes)) {
+    const double c = plan_cost(p);
+    if (!have || c < best_cost - 1e-9 ||
+        (c < best_cost + 1e-9 && p.image_bytes < best.image_bytes)) {
       best = std::move(p);
+      best_cost = c;
       have = true;
     }
   };
