@@ -49,11 +49,13 @@ struct TablePlan {
   int64_t image_bytes = 0; // X region + directory (16-B padded)
 };
 
-// Smem budget used by the automatic hash choice (bytes of X + directory): one
-// image copy per SM at the 1024-thread launch shape.  Measured: a larger
-// image that removes an in-bin step wins (cfg5 k=9/S=3 at 138 KB beats
-// k=7/S=4 at 59 KB by 6%; cfg1 k=9/S=1 beats k=5/S=2 by 3%).
-constexpr int64_t kAutoImageBudget = 200 * 1024;
+// Smem budget of the automatic hash choice (bytes of X + directory): one image
+// copy per SM at the 1024-thread shape, leaving >= ~80 KB of L1 for in-flight
+// loads.  Measured: a larger image that removes an in-bin step wins (cfg5
+// k=9/S=3 at 138 KB beats k=7/S=4 at 59 KB by 6%), but a 198 KB image loses
+// 18% (L1 starved).
+constexpr int64_t kAutoImageBudget = 144 * 1024;
+constexpr int64_t kAxisImageBudget = 16 * 1024;  // per axis of a 2-D grid (the grid owns smem)
 constexpr int64_t kMaxImage = 200 * 1024;  // explicit requests beyond this do not fit in smem
 
 // Validate + build (eos_plan_table_hash semantics).  kind/param: see

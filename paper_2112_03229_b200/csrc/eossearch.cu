@@ -87,17 +87,18 @@ struct LaunchShape {
 };
 
 // Default launch shape by image size: as many threads per SM as registers
-// allow (~1024 at <= 64 regs) with as few image copies per SM as possible.
+// allow (~1024 at <= 64 regs), with all image copies of an SM <= ~144 KB of
+// smem so L1 keeps room for the in-flight streaming loads.
 LaunchShape pick_search(int mode, int steps, bool cnt, int64_t image_bytes) {
   if (cnt) return {search_fn_shape<dv::ShapeCnt>(mode, steps, true), 256, 4, true};
   if (steps >= 3) {
-    if (image_bytes <= 100 * 1024)
+    if (image_bytes <= 72 * 1024)
       return {search_fn_shape<dv::ShapeDeepMid>(mode, steps, false), 512, 4, false};
     return {search_fn_shape<dv::ShapeDeepBig>(mode, steps, false), 1024, 4, false};
   }
-  if (image_bytes <= 48 * 1024)
+  if (image_bytes <= 32 * 1024)
     return {search_fn_shape<dv::ShapeSmall>(mode, steps, false), 256, 4, true};
-  if (image_bytes <= 100 * 1024)
+  if (image_bytes <= 72 * 1024)
     return {search_fn_shape<dv::ShapeMid>(mode, steps, false), 512, 4, true};
   return {search_fn_shape<dv::ShapeBig>(mode, steps, false), 1024, 4, true};
 }

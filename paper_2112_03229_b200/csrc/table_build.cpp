@@ -126,11 +126,14 @@ double lifting_probes(int o, int S) {
 // Modelled per-lookup cost of a plan, in shared-memory
 // wavefronts per warp of 32 lookups plus issue and occupancy terms:
 //   3.5 (random 4-B directory read) + 6.1 x E[executed 8-B probes]
-//   + 1 per in-bin step (issue) + image penalty (fewer / larger CTAs:
-//   0 up to 48 KB = 4 CTAs x 256, 0.5 up to 100 KB, 1 above).
-// Targets are taken log-uniform over the table range, i.e. uniform over the
-// bins (equal key width).  Calibrated on cfg2/cfg5 A/B runs
-// (profiles/r01_exp_hash_*.json).
+//   + 1 per in-bin step (issue) + a launch-shape penalty.
+// The shape (eossearch.cu::pick_search) keeps the smem of all resident image
+// copies <= ~144 KB per SM, leaving L1 for the in-flight streaming loads:
+// image <= 32 KB: 4 CTAs x 256 threads (penalty 0); <= 72 KB: 2 x 512 (1);
+// <= 144 KB: 1 x 1024 (1.5).  Measured: directories that squeeze L1 below
+// ~80 KB lose 4-18% (profiles/r01_exp_hash_*.json), so the automatic choice
+// stays within 144 KB.  Targets are taken log-uniform over the table range,
+// i.e. uniform over the bins (equal key width).
 double plan_cost(const TablePlan& p) {
   std::vector<double> memo(64, -1.0);
   double probes = 0.0;
@@ -146,25 +149,31 @@ double plan_cost(const TablePlan& p) {
     probes += v;
   }
   probes /= (double)p.bins;
-  const double img = p.image_bytes <= 48 * 1024 ? 0.0 : (p.image_bytes <= 100 * 1024 ? 0.5 : 1.0);
-  return 3.5 + 6.1 * probes + 1.0 * p.steps + img;
+  const double shape =
+      p.image_bytes <= 32 * 1024 ? 0.0 : (p.image_bytes <= 72 * 1024 ? 1.0 : 1.5);
+  return 3.5 + 6.1 * probes + 1.0 * p.steps + shape;
 }
 
 // Automatic choice: the candidate of least plan_cost with an
 // image within kAutoImageBudget; ties -> the smaller image, then the exponent
 // hash.  Candidates: the exponent hash for every k, and the logarithm hash
 // for |H| on a geometric grid (8 per octave).
-eos_status plan_auto(const std::vector<double>& X, int mode, TablePlan* out) {
+// Grid axes (compact = true) use the smallest S, then the smallest image: the
+// 2-D kernel's smem is dominated by the grid and its S = 1 cell lookup reads
+// the probe unconditionally (kernels.cuh::axis_cell), so bigger directories
+// buy nothing there.
+eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, TablePlan* out) {
   const int64_t n = (int64_t)X.size();
+  const int64_t budget = compact ? kAxisImageBudget : kAutoImageBudget;
   TablePlan best;
   double best_cost = 0.0;
   bool have = false;
   auto consider = [&](const HashParams& h) {
     if (h.bins < 1) return;
-    if (have && image_of(n, h.bins) > kAutoImageBudget) return;
+    if (have && image_of(n, h.bins) > budget) return;
     TablePlan p;
     if (build(X, mode, h, &p) != EOS_OK) return;
-    const double c = plan_cost(p);
+    const double c = compact ? (double)p.steps : plan_cost(p);
     if (!have || c < best_cost - 1e-9 ||
         (c < best_cost + 1e-9 && p.image_bytes < best.image_bytes)) {
       best = std::move(p);
@@ -174,10 +183,10 @@ eos_status plan_auto(const std::vector<double>& X, int mode, TablePlan* out) {
   };
   for (int k = 0; k <= EOS_MAX_K; ++k) {
     HashParams h = exponent_params(X, mode, k);
-    if (k > 0 && image_of(n, h.bins) > kAutoImageBudget) break;
+    if (k > 0 && image_of(n, h.bins) > budget) break;
     consider(h);
   }
-  const int64_t max_bins = (kAutoImageBudget - pad16(8 * n)) / 4;
+  const int64_t max_bins = (budget - pad16(8 * n)) / 4;
   for (double H = 1.0; H <= (double)max_bins; H *= 1.0905077326652577 /* 2^(1/8) */) {
     consider(log_params(X, mode, (int64_t)H));
   }
@@ -210,7 +219,7 @@ eos_status plan_table(const double* Xin, int64_t n, int kind, int64_t param, boo
   TablePlan p;
   eos_status st;
   if (kind == EOS_HASH_AUTO) {
-    st = plan_auto(X, mode, &p);
+    st = plan_auto(X, mode, strict, &p);
   } else {
     const HashParams h = kind == EOS_HASH_EXPONENT ? exponent_params(X, mode, (int)param)
                                                    : log_params(X, mode, param);

@@ -78,9 +78,9 @@ if has torchrun1; then
   cat $OUT/bench_torchrun1.json; tail -n 3 $OUT/bench_torchrun1.err
 fi
 if has exph; then
-  timeout 900 python scripts/exp_search.py --workload cfg2 --variants default --ks 5,6 --logbins 2000,5000,11585,20000,40000 --repeat 2 > $OUT/exph_cfg2.json 2> $OUT/exph.err; echo "exph cfg2 rc=$?"
-  timeout 900 python scripts/exp_search.py --workload cfg5 --count 1073741824 --steps 40 --variants default --ks 9 --logbins 16384,24000,32000,42494 --repeat 2 > $OUT/exph_cfg5.json 2>> $OUT/exph.err; echo "exph cfg5 rc=$?"
-  timeout 900 python scripts/exp_search.py --workload cfg3 --steps 40 --variants default --ks 6 --logbins 1448,4000,9741,20000 --repeat 2 > $OUT/exph_cfg3.json 2>> $OUT/exph.err; echo "exph cfg3 rc=$?"
+  timeout 900 python scripts/exp_search.py --workload cfg2 --variants default --ks 5 --logbins 5000 --repeat 2 > $OUT/exph_cfg2.json 2> $OUT/exph.err; echo "exph cfg2 rc=$?"
+  timeout 900 python scripts/exp_search.py --workload cfg5 --count 1073741824 --steps 40 --variants default --ks 9 --logbins 24000 --repeat 2 > $OUT/exph_cfg5.json 2>> $OUT/exph.err; echo "exph cfg5 rc=$?"
+  timeout 900 python scripts/exp_search.py --workload cfg3 --steps 40 --variants default --ks 6 --logbins 4000 --repeat 2 > $OUT/exph_cfg3.json 2>> $OUT/exph.err; echo "exph cfg3 rc=$?"
   tail -n 3 $OUT/exph.err
 fi
 if has ncu2; then
