@@ -91,6 +91,18 @@ if has ncu2; then
         -o $OUT/prof_$wl -f $CMD > $OUT/ncu_full_$wl.log 2>&1; echo "ncu $wl rc=$?"
   done
 fi
+if has ncufinal; then
+  CMD="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu"
+  $CMD > $OUT/ncuf_plain.log 2>&1 && \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
+      --log-file $OUT/launches_final.csv $CMD > $OUT/ncuf_launches.log 2>&1; echo "ncu launches rc=$?"
+  for wl in cfg2 cfg3 cfg5; do
+    CMD="python bench.py --workload $wl --count 134217728 --steps 6 --warmup 2 --no-e2e --no-cpu --eager"
+    $CMD > $OUT/ncuf_plain_$wl.log 2>&1 && \
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:search1d -s 2 -c 1 \
+        -o $OUT/prof_final_$wl -f $CMD > $OUT/ncuf_full_$wl.log 2>&1; echo "ncu full $wl rc=$?"
+  done
+fi
 if has ncu; then
   CMD="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --eager"
   $CMD > $OUT/ncu_plain.log 2>&1 && \
