@@ -101,6 +101,10 @@ if has ncufinal; then
     $CMD > $OUT/ncuf_plain_$wl.log 2>&1 && \
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:search1d -s 2 -c 1 \
         -o $OUT/prof_final_$wl -f $CMD > $OUT/ncuf_full_$wl.log 2>&1; echo "ncu full $wl rc=$?"
+    python scripts/ncu_summary.py $OUT/prof_final_$wl.ncu-rep > $OUT/ncu_summary_$wl.json
+    ncu -i $OUT/prof_final_$wl.ncu-rep --page details --csv > $OUT/ncu_details_$wl.csv 2>/dev/null
+    ncu -i $OUT/prof_final_$wl.ncu-rep --page raw --csv > $OUT/ncu_raw_$wl.csv 2>/dev/null
+    [ "$wl" != "cfg2" ] && rm -f $OUT/prof_final_$wl.ncu-rep
   done
 fi
 if has ncu; then
