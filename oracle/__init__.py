@@ -47,6 +47,7 @@ def lib():
         L.oracle_search.argtypes = [P, I64, P, I64, P]
         L.oracle_interp2d.argtypes = [P, I64, P, I64, P, P, P, I64, P, P, P]
         L.oracle_counters.argtypes = [P, I64, P, P, I64, I64, P]
+        L.oracle_interp2d_deriv.argtypes = [P, I64, P, I64, P, P, P, I64, P, P]
         _lib = L
     return _lib
 
@@ -106,6 +107,27 @@ def interp2d(R, Tax, G, rho, T, threads: int | None = None):
     with ThreadPoolExecutor(threads) as ex:
         list(ex.map(run, _chunks(m, threads)))
     return P, iR, iT
+
+
+def interp2d_deriv(R, Tax, G, rho, T, threads: int | None = None):
+    """(dP/drho, dP/dT) of the bilinear interpolant (eos_oracle.c, reading R23)."""
+    R, Tax, G, rho, T = _f64(R), _f64(Tax), _f64(G), _f64(rho), _f64(T)
+    assert G.shape == (R.size, Tax.size) and rho.size == T.size
+    m = rho.size
+    dr = np.empty(m, dtype=np.float64)
+    dt = np.empty(m, dtype=np.float64)
+    L = lib()
+    threads = threads or default_threads()
+
+    def run(r):
+        s, e = r
+        L.oracle_interp2d_deriv(R.ctypes.data, R.size, Tax.ctypes.data, Tax.size, G.ctypes.data,
+                                rho.ctypes.data + 8 * s, T.ctypes.data + 8 * s, e - s,
+                                dr.ctypes.data + 8 * s, dt.ctypes.data + 8 * s)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(run, _chunks(m, threads)))
+    return dr, dt
 
 
 def counters(X, Y, idx, global_offset: int = 0) -> np.ndarray:

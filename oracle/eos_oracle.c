@@ -79,6 +79,38 @@ void oracle_interp2d(const double* R, int64_t nR, const double* Tax, int64_t nT,
   }
 }
 
+/* Derivatives of the interpolant above (EOSPAC returns F, dF/dx, dF/dy with
+ * every interpolation; P:14, P:41 name the interpolation, the formula is
+ * reading R23 in DESIGN.md): the partial derivatives of the bilinear form on
+ * the bracket cell,
+ *   dP/drho = ((1-ty)(G[ci+1][cj]-G[ci][cj]) + ty(G[ci+1][cj+1]-G[ci][cj+1]))
+ *             / (R[ci+1]-R[ci])
+ *   dP/dT   = ((1-tx)(G[ci][cj+1]-G[ci][cj]) + tx(G[ci+1][cj+1]-G[ci+1][cj]))
+ *             / (T[cj+1]-T[cj])
+ * inside the grid; outside the axis range the clamped interpolant is constant
+ * along that axis, so the derivative is 0; a NaN coordinate gives NaN.
+ * dPdrho / dPdT may be NULL. */
+void oracle_interp2d_deriv(const double* R, int64_t nR, const double* Tax, int64_t nT,
+                           const double* G, const double* rho, const double* T, int64_t m,
+                           double* dPdrho, double* dPdT) {
+  for (int64_t q = 0; q < m; ++q) {
+    int32_t i = oracle_lower_bound(R, nR, rho[q]);
+    int32_t j = oracle_lower_bound(Tax, nT, T[q]);
+    int64_t ci = i < nR - 2 ? i : nR - 2;
+    int64_t cj = j < nT - 2 ? j : nT - 2;
+    double tx = clamp01((rho[q] - R[ci]) / (R[ci + 1] - R[ci]));
+    double ty = clamp01((T[q] - Tax[cj]) / (Tax[cj + 1] - Tax[cj]));
+    double g00 = G[ci * nT + cj], g01 = G[ci * nT + cj + 1];
+    double g10 = G[(ci + 1) * nT + cj], g11 = G[(ci + 1) * nT + cj + 1];
+    double sr = ((1.0 - ty) * (g10 - g00) + ty * (g11 - g01)) / (R[ci + 1] - R[ci]);
+    double st = ((1.0 - tx) * (g01 - g00) + tx * (g11 - g10)) / (Tax[cj + 1] - Tax[cj]);
+    int in_r = rho[q] >= R[0] && rho[q] <= R[nR - 1];
+    int in_t = T[q] >= Tax[0] && T[q] <= Tax[nT - 1];
+    if (dPdrho) dPdrho[q] = (rho[q] != rho[q]) ? rho[q] : (in_r ? sr : 0.0);
+    if (dPdT) dPdT[q] = (T[q] != T[q]) ? T[q] : (in_t ? st : 0.0);
+  }
+}
+
 /* Validation counters over one shard (DESIGN.md
  * "Counters").  Accumulated (+=) into c[8], all sums modulo 2^64:
  *   c0 = number of targets

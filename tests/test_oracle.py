@@ -249,3 +249,48 @@ def test_counters_match_definitions():
     c_b = oracle.counters(X, Y[h:], idx[h:], off + h)
     with np.errstate(over="ignore"):
         assert np.array_equal(c_a + c_b, c)
+
+
+# ----------------------------------------------------- interp derivatives ---
+def test_interp_derivatives_closed_form_and_outside():
+    """For G = a + b*rho + c*T + d*rho*T the bilinear interpolant is exact, so its
+    derivatives are b + d*T and c + d*rho inside the grid; outside an axis range the
+    clamped interpolant is constant along it (derivative 0); NaN propagates (R23)."""
+    rng = np.random.default_rng(4)
+    # well-conditioned axes: a difference quotient loses ~log10(|G| / |dG|) digits
+    R = np.unique(rng.uniform(1.0, 10.0, 37))
+    T = np.unique(rng.uniform(1.0, 10.0, 23))
+    a, b, c, d = 3.0, 0.7, -1.3, 0.21
+    G = a + b * R[:, None] + c * T[None, :] + d * R[:, None] * T[None, :]
+    rho = rng.uniform(R[0], R[-1], 20000)
+    t = rng.uniform(T[0], T[-1], 20000)
+    dr, dt = oracle.interp2d_deriv(R, T, G, rho, t)
+    assert np.max(np.abs(dr - (b + d * t))) < 1e-12
+    assert np.max(np.abs(dt - (c + d * rho))) < 1e-12
+    out = np.array([R[0] / 2, R[-1] * 2, np.nan, R[1]])
+    tt = np.array([T[3], T[3], T[3], T[-1] * 3])
+    dr, dt = oracle.interp2d_deriv(R, T, G, out, tt)
+    assert dr[0] == 0.0 and dr[1] == 0.0 and np.isnan(dr[2]) and dr[3] != 0.0
+    assert dt[3] == 0.0 and dt[0] != 0.0
+
+
+def test_interp_derivatives_match_finite_differences():
+    """Central differences of the oracle's own P inside a cell (the interpolant is
+    bilinear there, so the difference quotient is exact up to rounding)."""
+    rng = np.random.default_rng(5)
+    R, T = _axes(rng)
+    G = rng.uniform(1.0, 5.0, (R.size, T.size))
+    i = rng.integers(0, R.size - 1, 500)
+    j = rng.integers(0, T.size - 1, 500)
+    fr, ft = rng.uniform(0.2, 0.8, 500), rng.uniform(0.2, 0.8, 500)
+    rho = R[i] + fr * (R[i + 1] - R[i])
+    t = T[j] + ft * (T[j + 1] - T[j])
+    hr = 1e-4 * (R[i + 1] - R[i])
+    ht = 1e-4 * (T[j + 1] - T[j])
+    dr, dt = oracle.interp2d_deriv(R, T, G, rho, t)
+    pp, _, _ = oracle.interp2d(R, T, G, rho + hr, t)
+    pm, _, _ = oracle.interp2d(R, T, G, rho - hr, t)
+    assert np.allclose((pp - pm) / (2 * hr), dr, rtol=1e-6, atol=1e-9 * np.abs(dr).max())
+    pp, _, _ = oracle.interp2d(R, T, G, rho, t + ht)
+    pm, _, _ = oracle.interp2d(R, T, G, rho, t - ht)
+    assert np.allclose((pp - pm) / (2 * ht), dt, rtol=1e-6, atol=1e-9 * np.abs(dt).max())
