@@ -191,9 +191,10 @@ EOS_API eos_status eos_search_destroy(eos_table t);
  * ------------------------------------------------------------------------- */
 
 /* rho_host fp64[n_rho], T_host fp64[n_T]: strictly increasing, finite,
- * 2 <= n <= EOS_MAX_TABLE; P_host fp64[n_rho * n_T] row-major (T fastest),
- * finite; the grid must fit in shared memory (n_rho*n_T*8 + axes <= ~200 KB,
- * else EOS_ERR_UNSUPPORTED).  Copied; bound to the current device. */
+ * 2 <= n <= EOS_MAX_TABLE (negative axis values allowed: key mode 1);
+ * P_host fp64[n_rho * n_T] row-major (T fastest), finite; the grid must fit
+ * in shared memory (n_rho*n_T*8 + axes <= ~220 KB, else
+ * EOS_ERR_UNSUPPORTED).  Copied; bound to the current device. */
 EOS_API eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double* T_host,
                              int64_t n_T, const double* P_host, eos_grid2d* out);
 
@@ -203,6 +204,17 @@ EOS_API eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, cons
 EOS_API eos_status eos_interp2d(eos_grid2d g, const double* rho_dev, const double* T_dev, int64_t count,
                         double* P_out_dev, int32_t* irho_out_dev, int32_t* iT_out_dev,
                         void* stream);
+
+/* eos_interp2d plus the partial derivatives of the interpolant (EOSPAC
+ * returns F, dF/dx, dF/dy; reading R23):
+ *   dP/drho = ((1-ty)(G[ci+1][cj]-G[ci][cj]) + ty(G[ci+1][cj+1]-G[ci][cj+1])) / (R[ci+1]-R[ci])
+ *   dP/dT   = ((1-tx)(G[ci][cj+1]-G[ci][cj]) + tx(G[ci+1][cj+1]-G[ci+1][cj])) / (T[cj+1]-T[cj])
+ * inside the axis range; 0 outside it (the clamped interpolant is constant
+ * there); NaN for a NaN coordinate.  dPdrho_out_dev / dPdT_out_dev: device
+ * fp64[count] or NULL (both NULL: exactly eos_interp2d). */
+EOS_API eos_status eos_interp2d_ex(eos_grid2d g, const double* rho_dev, const double* T_dev, int64_t count,
+                           double* P_out_dev, int32_t* irho_out_dev, int32_t* iT_out_dev,
+                           double* dPdrho_out_dev, double* dPdT_out_dev, void* stream);
 
 /* End-to-end form with host buffers (see eos_search_host). */
 EOS_API eos_status eos_interp2d_host(eos_grid2d g, const double* rho_host, const double* T_host,

@@ -28,7 +28,7 @@ __all__ = [
     "eos_search_destroy", "eos_table_info", "eos_plan_table", "eos_grid2d_create", "eos_interp2d",
     "eos_interp2d_host", "eos_grid2d_destroy", "eos_grid2d_info", "eos_status_str", "EOS_K_AUTO",
     "EOS_MAX_TABLE", "EOS_MAX_K", "EXPORTED_SYMBOLS", "EOS_HASH_AUTO", "EOS_HASH_EXPONENT",
-    "EOS_HASH_LOG", "eos_plan_table_hash", "eos_search_create_hash",
+    "EOS_HASH_LOG", "eos_plan_table_hash", "eos_search_create_hash", "eos_interp2d_ex",
 ]
 
 EOS_MAX_TABLE = 16384
@@ -48,7 +48,7 @@ EXPORTED_SYMBOLS = (
     "eos_search_host", "eos_table_info", "eos_search_destroy", "eos_grid2d_create",
     "eos_interp2d", "eos_interp2d_host", "eos_grid2d_info", "eos_grid2d_destroy",
     "eos_status_str", "eos_abi_version", "eos_launch_count", "eos_plan_table_hash",
-    "eos_search_create_hash",
+    "eos_search_create_hash", "eos_interp2d_ex",
 )
 
 
@@ -101,6 +101,7 @@ def load_library():
         "eos_search_destroy": [_P],
         "eos_grid2d_create": [_P, _I64, _P, _I64, _P, _P],
         "eos_interp2d": [_P, _P, _P, _I64, _P, _P, _P, _P],
+        "eos_interp2d_ex": [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P],
         "eos_interp2d_host": [_P, _P, _P, _I64, _P, _P, _P, _P],
         "eos_grid2d_info": [_P, _P, _P],
         "eos_grid2d_destroy": [_P],
@@ -255,6 +256,11 @@ def eos_interp2d(handle, rho_ptr, T_ptr, count, P_ptr, iR_ptr, iT_ptr, stream):
            "eos_interp2d")
 
 
+def eos_interp2d_ex(handle, rho_ptr, T_ptr, count, P_ptr, iR_ptr, iT_ptr, dPr_ptr, dPt_ptr, stream):
+    _check(load_library().eos_interp2d_ex(handle, rho_ptr, T_ptr, count, P_ptr, iR_ptr, iT_ptr,
+                                          dPr_ptr, dPt_ptr, stream), "eos_interp2d_ex")
+
+
 def eos_interp2d_host(handle, rho_ptr, T_ptr, count, P_ptr, iR_ptr, iT_ptr, stream):
     _check(load_library().eos_interp2d_host(handle, rho_ptr, T_ptr, count, P_ptr, iR_ptr, iT_ptr,
                                             stream), "eos_interp2d_host")
@@ -356,7 +362,8 @@ class Grid2D:
         return self._h
 
     def interp(self, rho, T, P_out=None, irho_out=None, iT_out=None, brackets: bool = True,
-               stream=None):
+               stream=None, derivatives: bool = False):
+        """(P, irho, iT) -- or (P, irho, iT, dP/drho, dP/dT) with derivatives=True."""
         import torch
         _dev(rho, "float64", "rho")
         _dev(T, "float64", "T")
@@ -369,9 +376,18 @@ class Grid2D:
             irho_out = torch.empty(m, dtype=torch.int32, device=rho.device)
         if brackets and iT_out is None:
             iT_out = torch.empty(m, dtype=torch.int32, device=rho.device)
-        eos_interp2d(self._h, rho.data_ptr(), T.data_ptr(), m, _dev(P_out, "float64", "P").data_ptr(),
-                     irho_out.data_ptr() if irho_out is not None else None,
-                     iT_out.data_ptr() if iT_out is not None else None, _stream_ptr(stream))
+        dr = dt = None
+        if derivatives:
+            dr = torch.empty(m, dtype=torch.float64, device=rho.device)
+            dt = torch.empty(m, dtype=torch.float64, device=rho.device)
+        eos_interp2d_ex(self._h, rho.data_ptr(), T.data_ptr(), m,
+                        _dev(P_out, "float64", "P").data_ptr(),
+                        irho_out.data_ptr() if irho_out is not None else None,
+                        iT_out.data_ptr() if iT_out is not None else None,
+                        dr.data_ptr() if dr is not None else None,
+                        dt.data_ptr() if dt is not None else None, _stream_ptr(stream))
+        if derivatives:
+            return P_out, irho_out, iT_out, dr, dt
         return P_out, irho_out, iT_out
 
     def interp_host(self, rho: np.ndarray, T: np.ndarray, P_out=None, irho_out=None, iT_out=None,

@@ -45,7 +45,8 @@ struct eos_grid2d_s {
   int32_t g_off = 0;
   dv::AxisParams ar{}, at{};
   const void* fn = nullptr;
-  int grid = 0;
+  const void* fn_deriv = nullptr;
+  int grid = 0, grid_deriv = 0;
   int threads = 512, unroll = 2;
   bool clc = true;
   int32_t wr_off = 0, wt_off = 0;
@@ -139,18 +140,24 @@ const Variant kVariants[] = {
 template <int S>
 const void* interp_fn_s(int variant) {
   switch (variant) {
-    case 1: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, false>, false>;
-    case 2: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 2, 1, false>, false>;
-    case 3: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 4, 1, false>, false>;
-    case 4: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, true>, false>;
-    case 5: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, false>, true>;
-    case 6: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 1, 1, false>, true>;
-    default: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false>;
+    case 1: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, false>, false, false>;
+    case 2: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 2, 1, false>, false, false>;
+    case 3: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 4, 1, false>, false, false>;
+    case 4: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, true>, false, false>;
+    case 5: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, false>, true, false>;
+    case 6: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 1, 1, false>, true, false>;
+    default: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false>;
   }
+}
+
+template <int S>
+const void* interp_deriv_fn_s() {
+  return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, true>;
 }
 
 struct Interp2DShape {
   const void* fn;
+  const void* fn_deriv;  // same shape, with dP/drho and dP/dT outputs
   int threads, unroll;
   bool clc;
 };
@@ -166,14 +173,15 @@ Interp2DShape pick_interp(int steps) {
   static const bool clc[7] = {false, false, false, false, true, false, false};
   if (v < 0 || v > 6) v = 0;
   const void* fn;
+  const void* fd;
   switch (steps) {
-    case 1: fn = interp_fn_s<1>(v); break;
-    case 2: fn = interp_fn_s<2>(v); break;
-    case 3: fn = interp_fn_s<3>(v); break;
-    case 4: fn = interp_fn_s<4>(v); break;
-    default: fn = interp_fn_s<0>(v); break;
+    case 1: fn = interp_fn_s<1>(v); fd = interp_deriv_fn_s<1>(); break;
+    case 2: fn = interp_fn_s<2>(v); fd = interp_deriv_fn_s<2>(); break;
+    case 3: fn = interp_fn_s<3>(v); fd = interp_deriv_fn_s<3>(); break;
+    case 4: fn = interp_fn_s<4>(v); fd = interp_deriv_fn_s<4>(); break;
+    default: fn = interp_fn_s<0>(v); fd = interp_deriv_fn_s<0>(); break;
   }
-  return {fn, thr[v], unr[v], clc[v]};
+  return {fn, fd, thr[v], unr[v], clc[v]};
 }
 
 dv::AxisParams axis_params(const TablePlan& p, int32_t x_off) {
@@ -185,6 +193,7 @@ dv::AxisParams axis_params(const TablePlan& p, int32_t x_off) {
   a.M = p.M;
   a.bmax = p.bmax;
   a.steps = std::max(p.steps, 1);
+  a.mode = p.key_mode;
   a.x0 = p.X[0];
   a.xlast = p.X[p.n - 1];
   return a;
@@ -280,7 +289,9 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
 }
 
 eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64_t count,
-                         double* P, int32_t* iR, int32_t* iT, cudaStream_t st) {
+                         double* P, int32_t* iR, int32_t* iT, double* dPr, double* dPt,
+                         cudaStream_t st) {
+  const bool deriv = dPr != nullptr || dPt != nullptr;
   dv::Interp2DArgs a{};
   a.image = (const uint4*)g->image_dev;
   a.image_16 = (int32_t)(g->image_bytes / 16);
@@ -294,18 +305,22 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   a.P = P;
   a.iR = iR;
   a.iT = iT;
+  a.dPr = dPr;
+  a.dPt = dPt;
   a.count = count;
-  const uintptr_t al16 = (uintptr_t)rho | (uintptr_t)T | (uintptr_t)P;
+  const uintptr_t al16 =
+      (uintptr_t)rho | (uintptr_t)T | (uintptr_t)P | (uintptr_t)dPr | (uintptr_t)dPt;
   const uintptr_t al8 = (uintptr_t)iR | (uintptr_t)iT;
   a.vec_ok = ((al16 & 15) == 0) && ((al8 & 7) == 0);
   const int64_t per_tile = (int64_t)g->threads * g->unroll * 2;
   const int64_t tiles = (count + per_tile - 1) / per_tile;
   if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;
   a.ntiles = tiles;
-  int64_t grid = g->clc ? tiles : std::min<int64_t>(g->grid, tiles);
+  int64_t grid = g->clc ? tiles : std::min<int64_t>(deriv ? g->grid_deriv : g->grid, tiles);
   grid = std::max<int64_t>(grid, 1);
   void* params[] = {&a};
-  EOS_CUDA(launch(g->fn, grid, g->threads, (size_t)g->image_bytes, st, params));
+  EOS_CUDA(launch(deriv ? g->fn_deriv : g->fn, grid, g->threads, (size_t)g->image_bytes, st,
+                  params));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return EOS_OK;
 }
@@ -529,7 +544,6 @@ eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double
   if (!g) return EOS_ERR_NOMEM;
   eos_status st = eos::plan_table(rho_host, n_rho, EOS_HASH_AUTO, 0, true, &g->pr);
   if (st == EOS_OK) st = eos::plan_table(T_host, n_T, EOS_HASH_AUTO, 0, true, &g->pt);
-  if (st == EOS_OK && (g->pr.key_mode != 0 || g->pt.key_mode != 0)) st = EOS_ERR_UNSUPPORTED;
   if (st != EOS_OK) { delete g; return st; }
   const int64_t ncell = n_rho * n_T;
   for (int64_t q = 0; q < ncell; ++q)
@@ -566,36 +580,47 @@ eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double
   if (st != EOS_OK) { delete g; return st; }
   Interp2DShape sh = pick_interp(std::max(g->pr.steps, g->pt.steps));
   g->fn = sh.fn;
+  g->fn_deriv = sh.fn_deriv;
   g->threads = sh.threads;
   g->unroll = sh.unroll;
   g->clc = sh.clc;
   st = configure(g->fn, g->threads, g->image_bytes, g->num_sms, &g->grid, nullptr);
+  if (st == EOS_OK)
+    st = configure(g->fn_deriv, g->threads, g->image_bytes, g->num_sms, &g->grid_deriv, nullptr);
   if (st != EOS_OK) { cudaFree(g->image_dev); delete g; return st; }
   *out = g;
   return EOS_OK;
 }
 
-eos_status eos_interp2d(eos_grid2d g, const double* rho_dev, const double* T_dev, int64_t count,
-                        double* P_out_dev, int32_t* irho_out_dev, int32_t* iT_out_dev,
-                        void* stream) {
+eos_status eos_interp2d_ex(eos_grid2d g, const double* rho_dev, const double* T_dev,
+                           int64_t count, double* P_out_dev, int32_t* irho_out_dev,
+                           int32_t* iT_out_dev, double* dPdrho_out_dev, double* dPdT_out_dev,
+                           void* stream) {
   if (!g) return EOS_ERR_NULL;
   if (count < 0 || count > (int64_t(1) << 62)) return EOS_ERR_SIZE;
   if (count == 0) return EOS_OK;
   if (!rho_dev || !T_dev || !P_out_dev) return EOS_ERR_NULL;
   const void* ins[2] = {rho_dev, T_dev};
-  const void* outs[3] = {P_out_dev, irho_out_dev, iT_out_dev};
-  const int64_t ob[3] = {8 * count, 4 * count, 4 * count};
-  for (int o = 0; o < 3; ++o) {
+  const void* outs[5] = {P_out_dev, irho_out_dev, iT_out_dev, dPdrho_out_dev, dPdT_out_dev};
+  const int64_t ob[5] = {8 * count, 4 * count, 4 * count, 8 * count, 8 * count};
+  for (int o = 0; o < 5; ++o) {
     if (!outs[o]) continue;
     for (int i = 0; i < 2; ++i)
       if (overlaps(ins[i], 8 * count, outs[o], ob[o])) return EOS_ERR_ALIAS;
-    for (int o2 = o + 1; o2 < 3; ++o2)
+    for (int o2 = o + 1; o2 < 5; ++o2)
       if (outs[o2] && overlaps(outs[o], ob[o], outs[o2], ob[o2])) return EOS_ERR_ALIAS;
   }
   eos_status st = check_device(g->device);
   if (st != EOS_OK) return st;
   return launch_interp(g, rho_dev, T_dev, count, P_out_dev, irho_out_dev, iT_out_dev,
-                       (cudaStream_t)stream);
+                       dPdrho_out_dev, dPdT_out_dev, (cudaStream_t)stream);
+}
+
+eos_status eos_interp2d(eos_grid2d g, const double* rho_dev, const double* T_dev, int64_t count,
+                        double* P_out_dev, int32_t* irho_out_dev, int32_t* iT_out_dev,
+                        void* stream) {
+  return eos_interp2d_ex(g, rho_dev, T_dev, count, P_out_dev, irho_out_dev, iT_out_dev, nullptr,
+                         nullptr, stream);
 }
 
 eos_status eos_interp2d_host(eos_grid2d g, const double* rho_host, const double* T_host,
@@ -619,7 +644,7 @@ eos_status eos_interp2d_host(eos_grid2d g, const double* rho_host, const double*
         EOS_CUDA(cudaMemcpyAsync(dR, rho_host + off, 8 * len, cudaMemcpyHostToDevice, s));
         EOS_CUDA(cudaMemcpyAsync(dT, T_host + off, 8 * len, cudaMemcpyHostToDevice, s));
         eos_status r = launch_interp(g, dR, dT, len, dP, irho_out_host ? dI : nullptr,
-                                     iT_out_host ? dJ : nullptr, s);
+                                     iT_out_host ? dJ : nullptr, nullptr, nullptr, s);
         if (r != EOS_OK) return r;
         EOS_CUDA(cudaMemcpyAsync(P_out_host + off, dP, 8 * len, cudaMemcpyDeviceToHost, s));
         if (irho_out_host)

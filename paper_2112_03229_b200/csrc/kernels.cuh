@@ -50,6 +50,7 @@ struct AxisParams {
   uint32_t M;       // bin multiplier (exponent hash: 2^(12+k); log hash: |H| 2^32 / span)
   uint32_t bmax;    // bins - 1
   int32_t steps;    // S (used by the runtime-S path)
+  int32_t mode;     // key mode (0: X[0] >= 0, sign-masked key; 1: order-preserving key)
   double x0;        // X[0]
   double xlast;     // X[n-1]
 };
@@ -385,6 +386,8 @@ struct Interp2DArgs {
   double* P;
   int32_t* iR;      // nullable
   int32_t* iT;      // nullable
+  double* dPr;      // nullable: dP/drho (DERIV kernels)
+  double* dPt;      // nullable: dP/dT (DERIV kernels)
   int64_t count;
 };
 
@@ -407,7 +410,8 @@ __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ s
                                           const uint32_t* __restrict__ sD, const AxisParams& a,
                                           int32_t& i, int32_t& ci, double& xl, double& xr) {
   if (S == 1) {
-    const uint32_t d = sD[bin_of(key_hi<0>(y), a)];
+    const uint32_t key = a.mode ? key_hi<1>(y) : key_hi<0>(y);
+    const uint32_t d = sD[bin_of(key, a)];
     const int32_t lo = (int32_t)(d & 0xFFFFu);  // <= n-1: X[n-1] lies in the top bin
     const int32_t occ = (int32_t)(d >> 16);     // 0 or 1 when S == 1
     EOS_DCHECK(lo < a.n && occ <= 1);
@@ -421,7 +425,7 @@ __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ s
     xr = left ? ov : (right ? pv : sX[ci + 1]);
     EOS_DCHECK(ci >= 0 && ci + 1 < a.n && (left ? lo + 1 : (right ? lo - 1 : ci)) < a.n);
   } else {
-    i = lookup<S, 0>(y, sX, sD, a);
+    i = a.mode ? lookup<S, 1>(y, sX, sD, a) : lookup<S, 0>(y, sX, sD, a);
     ci = min(i, a.n - 2);
     xl = sX[ci];
     xr = sX[ci + 1];
@@ -434,9 +438,10 @@ __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ s
 // of that formula (bit-identical to a plain evaluation in that order).
 // RECIP: weights as (x - X[c]) * (1/(X[c+1]-X[c])) with the reciprocal
 // precomputed at create (a few ulp from the divide; within the 1e-12 bar).
-template <int S, bool RECIP>
+template <int S, bool RECIP, bool DERIV>
 __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, int32_t& j,
-                                             const char* sm, const Interp2DArgs& A) {
+                                             double& dpr, double& dpt, const char* sm,
+                                             const Interp2DArgs& A) {
   const double* sR = reinterpret_cast<const double*>(sm + A.r.x_off);
   const double* sT = reinterpret_cast<const double*>(sm + A.t.x_off);
   const uint32_t* dR = reinterpret_cast<const uint32_t*>(sm + A.r.d_off);
@@ -461,9 +466,24 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   const double* g1 = g0 + A.t.n;
   const double g00 = g0[0], g01 = g0[1], g10 = g1[0], g11 = g1[1];
   const double uy = __dsub_rn(1.0, ty);
+  const double ux = __dsub_rn(1.0, tx);
   const double a0 = __dadd_rn(__dmul_rn(uy, g00), __dmul_rn(ty, g01));
   const double a1 = __dadd_rn(__dmul_rn(uy, g10), __dmul_rn(ty, g11));
-  return __dadd_rn(__dmul_rn(__dsub_rn(1.0, tx), a0), __dmul_rn(tx, a1));
+  if (DERIV) {
+    // Partial derivatives of the bilinear form on the cell (R23); 0 outside an
+    // axis range (the clamped interpolant is constant there); NaN kept.
+    const double sr = __ddiv_rn(__dadd_rn(__dmul_rn(uy, __dsub_rn(g10, g00)),
+                                          __dmul_rn(ty, __dsub_rn(g11, g01))),
+                                __dsub_rn(r1, r0));
+    const double st = __ddiv_rn(__dadd_rn(__dmul_rn(ux, __dsub_rn(g01, g00)),
+                                          __dmul_rn(tx, __dsub_rn(g11, g10))),
+                                __dsub_rn(t1, t0));
+    const bool in_r = rho >= A.r.x0 && rho <= A.r.xlast;
+    const bool in_t = T >= A.t.x0 && T <= A.t.xlast;
+    dpr = (rho != rho) ? rho : (in_r ? sr : 0.0);
+    dpt = (T != T) ? T : (in_t ? st : 0.0);
+  }
+  return __dadd_rn(__dmul_rn(ux, a0), __dmul_rn(tx, a1));
 }
 
 // default 2-D launch shape (165 KB image: 1 CTA/SM).  Static schedule: the
@@ -471,7 +491,7 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
 // costs more than the static tail (profiles/r01_exp_interp.json).
 using Shape2D = Shape<1024, 1, 1, false>;
 
-template <int S, class SH, bool RECIP>
+template <int S, class SH, bool RECIP, bool DERIV>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {
   constexpr int T = SH::kThreads;
   constexpr int U = SH::kUnroll;
@@ -493,6 +513,9 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
   double2* __restrict__ P2 = reinterpret_cast<double2*>(A.P);
   int2* __restrict__ IR2 = reinterpret_cast<int2*>(A.iR);
   int2* __restrict__ IT2 = reinterpret_cast<int2*>(A.iT);
+  double2* __restrict__ DR2 = reinterpret_cast<double2*>(A.dPr);
+  double2* __restrict__ DT2 = reinterpret_cast<double2*>(A.dPt);
+  const bool bdr = DERIV && A.dPr != nullptr, bdt = DERIV && A.dPt != nullptr;
 
   uint32_t phase = 0;
   auto next_tile = [&](int64_t t) -> int64_t {
@@ -523,12 +546,14 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
     if (full(t)) {
       const int64_t p0 = t * TP + threadIdx.x;
       EOS_DCHECK(2 * (p0 + (U - 1) * T) + 1 < count);
-      double2 p[U];
+      double2 p[U], dr[U], dt[U];
       int2 ir[U], it[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        p[u].x = interp_one<S, RECIP>(vr[u].x, vt[u].x, ir[u].x, it[u].x, sm, A);
-        p[u].y = interp_one<S, RECIP>(vr[u].y, vt[u].y, ir[u].y, it[u].y, sm, A);
+        p[u].x = interp_one<S, RECIP, DERIV>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
+                                             sm, A);
+        p[u].y = interp_one<S, RECIP, DERIV>(vr[u].y, vt[u].y, ir[u].y, it[u].y, dr[u].y, dt[u].y,
+                                             sm, A);
       }
       tn = next_tile(t);
       if (tn < ntiles && full(tn)) {
@@ -543,16 +568,21 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
         __stcs(P2 + p0 + u * T, p[u]);
         if (br) __stcs(IR2 + p0 + u * T, ir[u]);
         if (bt) __stcs(IT2 + p0 + u * T, it[u]);
+        if (bdr) __stcs(DR2 + p0 + u * T, dr[u]);
+        if (bdt) __stcs(DT2 + p0 + u * T, dt[u]);
       }
     } else {
       const int64_t e0 = t * TE;
       const int64_t e1 = min(count, e0 + TE);
       for (int64_t q = e0 + threadIdx.x; q < e1; q += T) {
         int32_t i, j;
-        const double pq = interp_one<S, RECIP>(A.rho[q], A.T[q], i, j, sm, A);
+        double dpr, dpt;
+        const double pq = interp_one<S, RECIP, DERIV>(A.rho[q], A.T[q], i, j, dpr, dpt, sm, A);
         A.P[q] = pq;
         if (br) A.iR[q] = i;
         if (bt) A.iT[q] = j;
+        if (bdr) A.dPr[q] = dpr;
+        if (bdt) A.dPt[q] = dpt;
       }
       tn = next_tile(t);
       if (tn < ntiles && full(tn)) {

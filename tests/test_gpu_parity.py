@@ -411,3 +411,61 @@ def test_interp_host_pipeline_matches():
     assert np.array_equal(iR, iRr) and np.array_equal(iT, iTr)
     check_interp(P, Pr)
     g.close()
+
+
+# ------------------------------------------------- f4: derivatives, mode 1 --
+def _check_deriv(got, ref):
+    nan_g, nan_r = np.isnan(got), np.isnan(ref)
+    assert np.array_equal(nan_g, nan_r)
+    ok = ~nan_r
+    scale = max(np.abs(ref[ok]).max(), 1e-300) if ok.any() else 1.0
+    assert np.all(np.abs(got[ok] - ref[ok]) <= REL_TOL * np.maximum(np.abs(ref[ok]), 1e-3 * scale))
+
+
+def test_interp_derivatives_match_oracle():
+    w = datagen.workload("cfg4", count=(1 << 20) + 3)
+    rho = w.rho_targets.host_fill(0, w.count)
+    T = w.T_targets.host_fill(0, w.count)
+    rho[:4] = [np.nan, w.rho[0] / 10, w.rho[-1] * 10, w.rho[5]]
+    T[4:8] = [np.nan, w.T[0] / 10, w.T[-1] * 10, w.T[7]]
+    g = eos.Grid2D(w.rho, w.T, w.P)
+    P, iR, iT, dR, dT = g.interp(to_dev(rho), to_dev(T), derivatives=True)
+    torch.cuda.synchronize()
+    Pr, iRr, iTr = oracle.interp2d(w.rho, w.T, w.P, rho, T)
+    dRr, dTr = oracle.interp2d_deriv(w.rho, w.T, w.P, rho, T)
+    assert np.array_equal(iR.cpu().numpy(), iRr) and np.array_equal(iT.cpu().numpy(), iTr)
+    check_interp(P.cpu().numpy(), Pr)
+    _check_deriv(dR.cpu().numpy(), dRr)
+    _check_deriv(dT.cpu().numpy(), dTr)
+    # without derivatives the values are unchanged
+    P2, _, _ = g.interp(to_dev(rho), to_dev(T))
+    torch.cuda.synchronize()
+    assert torch.equal(P2, P)
+    g.close()
+
+
+def test_interp_negative_axes_mode1_and_odd_sizes():
+    rng = np.random.default_rng(31)
+    for t in range(12):
+        R = np.unique(rng.normal(0, 50, int(rng.integers(2, 80))))
+        T = np.unique(rng.uniform(-5, 5, int(rng.integers(2, 40))))
+        if R.size < 2 or T.size < 2:
+            continue
+        G = rng.uniform(0.5, 5.0, (R.size, T.size))
+        m = 10_007
+        rho = rng.uniform(R[0] - 10, R[-1] + 10, m)
+        tt = rng.uniform(T[0] - 1, T[-1] + 1, m)
+        rho[:R.size] = R
+        tt[-T.size:] = T
+        rho[R.size:R.size + 2] = [-0.0, 0.0]
+        g = eos.Grid2D(R, T, G)
+        assert g.rho_info.key_mode == 1
+        P, iR, iT, dR, dT = g.interp(to_dev(rho), to_dev(tt), derivatives=True)
+        torch.cuda.synchronize()
+        Pr, iRr, iTr = oracle.interp2d(R, T, G, rho, tt)
+        dRr, dTr = oracle.interp2d_deriv(R, T, G, rho, tt)
+        assert np.array_equal(iR.cpu().numpy(), iRr) and np.array_equal(iT.cpu().numpy(), iTr)
+        check_interp(P.cpu().numpy(), Pr)
+        _check_deriv(dR.cpu().numpy(), dRr)
+        _check_deriv(dT.cpu().numpy(), dTr)
+        g.close()
