@@ -176,6 +176,22 @@ EOS_API eos_status eos_search_ex(eos_table t, const double* targets_dev, int64_t
 EOS_API eos_status eos_search_host(eos_table t, const double* targets_host, int64_t count,
                            int32_t* idx_out_host, void* stream);
 
+/* Zero-setup search ("algorithms with zero setup
+ * cost may be a better choice" when tables are not known in advance): no
+ * handle, no host work.  Each CTA stages table_dev into shared memory and
+ * builds a logarithm-hash count directory there (<= 8192 bins) before
+ * streaming the targets.  Same results as eos_search.
+ *   table_dev  : device fp64[n], 1 <= n <= 4096 (EOS_DIRECT_MAX_TABLE); it must
+ *                be finite and non-decreasing -- this is checked on the device:
+ *                if violated, *status_dev (nullable, device int32) receives
+ *                EOS_ERR_NONFINITE / EOS_ERR_UNSORTED and the indices are
+ *                unspecified.  May be written by earlier work on `stream`.
+ *   other arguments as eos_search; asynchronous on `stream`. */
+#define EOS_DIRECT_MAX_TABLE 4096
+EOS_API eos_status eos_search_direct(const double* table_dev, int64_t n, const double* targets_dev,
+                             int64_t count, int32_t* idx_out_dev, int32_t* status_dev,
+                             void* stream);
+
 EOS_API eos_status eos_table_info(eos_table t, eos_table_info_t* out);
 EOS_API eos_status eos_search_destroy(eos_table t);
 

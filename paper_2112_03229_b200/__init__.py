@@ -29,6 +29,7 @@ __all__ = [
     "eos_interp2d_host", "eos_grid2d_destroy", "eos_grid2d_info", "eos_status_str", "EOS_K_AUTO",
     "EOS_MAX_TABLE", "EOS_MAX_K", "EXPORTED_SYMBOLS", "EOS_HASH_AUTO", "EOS_HASH_EXPONENT",
     "EOS_HASH_LOG", "eos_plan_table_hash", "eos_search_create_hash", "eos_interp2d_ex",
+    "eos_search_direct", "search_direct",
 ]
 
 EOS_MAX_TABLE = 16384
@@ -48,7 +49,7 @@ EXPORTED_SYMBOLS = (
     "eos_search_host", "eos_table_info", "eos_search_destroy", "eos_grid2d_create",
     "eos_interp2d", "eos_interp2d_host", "eos_grid2d_info", "eos_grid2d_destroy",
     "eos_status_str", "eos_abi_version", "eos_launch_count", "eos_plan_table_hash",
-    "eos_search_create_hash", "eos_interp2d_ex",
+    "eos_search_create_hash", "eos_interp2d_ex", "eos_search_direct",
 )
 
 
@@ -102,6 +103,7 @@ def load_library():
         "eos_grid2d_create": [_P, _I64, _P, _I64, _P, _P],
         "eos_interp2d": [_P, _P, _P, _I64, _P, _P, _P, _P],
         "eos_interp2d_ex": [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P],
+        "eos_search_direct": [_P, _I64, _P, _I64, _P, _P, _P],
         "eos_interp2d_host": [_P, _P, _P, _I64, _P, _P, _P, _P],
         "eos_grid2d_info": [_P, _P, _P],
         "eos_grid2d_destroy": [_P],
@@ -228,6 +230,29 @@ def eos_search_ex(handle, targets_ptr, count, idx_out_ptr, global_offset, counte
 def eos_search_host(handle, targets_host_ptr, count, idx_out_host_ptr, stream):
     _check(load_library().eos_search_host(handle, targets_host_ptr, count, idx_out_host_ptr, stream),
            "eos_search_host")
+
+
+def eos_search_direct(table_ptr, n, targets_ptr, count, idx_out_ptr, status_ptr, stream):
+    _check(load_library().eos_search_direct(table_ptr, n, targets_ptr, count, idx_out_ptr,
+                                            status_ptr, stream), "eos_search_direct")
+
+
+def search_direct(table, targets, out=None, status=None, stream=None):
+    """Zero-setup search: `table` is a CUDA float64 tensor (n <= 4096, sorted), no handle
+    is created; the directory is built on the device by every CTA (f2)."""
+    import torch
+    _dev(table, "float64", "table")
+    _dev(targets, "float64", "targets")
+    if out is None:
+        out = torch.empty(targets.numel(), dtype=torch.int32, device=targets.device)
+    _dev(out, "int32", "out")
+    sp = None
+    if status is not None:
+        _dev(status, "int32", "status")
+        sp = status.data_ptr()
+    eos_search_direct(table.data_ptr(), table.numel(), targets.data_ptr(), targets.numel(),
+                      out.data_ptr(), sp, _stream_ptr(stream))
+    return out
 
 
 def eos_table_info(handle) -> TableInfo:

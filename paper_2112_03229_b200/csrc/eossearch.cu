@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -513,6 +514,56 @@ eos_status eos_search_host(eos_table t, const double* targets_host, int64_t coun
         EOS_CUDA(cudaMemcpyAsync(idx_out_host + off, dI, 4 * len, cudaMemcpyDeviceToHost, s));
         return EOS_OK;
       });
+}
+
+eos_status eos_search_direct(const double* table_dev, int64_t n, const double* targets_dev,
+                             int64_t count, int32_t* idx_out_dev, int32_t* status_dev,
+                             void* stream) {
+  if (n < 1 || n > dv::kDirectMaxTable) return EOS_ERR_SIZE;
+  if (count < 0 || count > (int64_t(1) << 62)) return EOS_ERR_SIZE;
+  if (!table_dev) return EOS_ERR_NULL;
+  if (count == 0) return EOS_OK;
+  if (!targets_dev || !idx_out_dev) return EOS_ERR_NULL;
+  if (overlaps(targets_dev, 8 * count, idx_out_dev, 4 * count) ||
+      overlaps(table_dev, 8 * n, idx_out_dev, 4 * count))
+    return EOS_ERR_ALIAS;
+  int dev = 0;
+  EOS_CUDA(cudaGetDevice(&dev));
+  using SH = dv::ShapeDirect;
+  const void* fn = (const void*)dv::search1d_direct_kernel<SH>;
+  int32_t bins_max = 1;
+  while (bins_max < 4 * n && bins_max < dv::kDirectMaxBins) bins_max <<= 1;
+  const int64_t smem = ((8 * n + 15) & ~int64_t(15)) + 4 * (int64_t)bins_max;
+  {  // one-time per device: allow the largest dynamic smem this kernel uses
+    static std::mutex mu;
+    static bool done[64] = {false};
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 64 && !done[dev]) {
+      const int64_t mx = ((8 * dv::kDirectMaxTable + 15) & ~int64_t(15)) + 4 * dv::kDirectMaxBins;
+      EOS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+      done[dev] = true;
+    }
+  }
+  dv::DirectArgs a{};
+  a.table = table_dev;
+  a.n = (int32_t)n;
+  a.bins_max = bins_max;
+  a.status = status_dev;
+  a.s.Y = targets_dev;
+  a.s.out = idx_out_dev;
+  a.s.count = count;
+  const uintptr_t ya = (uintptr_t)targets_dev, oa = (uintptr_t)idx_out_dev;
+  a.s.head = (ya & 15) ? 1 : 0;
+  a.s.vec_ok = ((ya & 7) == 0) && (((oa + 4 * (uintptr_t)a.s.head) & 7) == 0) && count > a.s.head;
+  const int64_t per_tile = (int64_t)SH::kTileElems;
+  const int64_t tiles = (count - a.s.head + per_tile - 1) / per_tile;
+  if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;
+  a.s.ntiles = tiles;
+  void* params[] = {&a};
+  EOS_CUDA(launch(fn, std::max<int64_t>(tiles, 1), SH::kThreads, (size_t)smem,
+                  (cudaStream_t)stream, params));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return EOS_OK;
 }
 
 eos_status eos_table_info(eos_table t, eos_table_info_t* out) {

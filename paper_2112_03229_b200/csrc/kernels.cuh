@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "eossearch.h"
+
 // Debug build (-DEOS_DEVICE_CHECKS, lib/libeossearch_checked.so): bounds checks
 // on every shared/global access of the hot loops; a failure traps the kernel.
 // (compute-sanitizer is not available on this GPU pool.)
@@ -261,25 +263,19 @@ using ShapeDeepMid = Shape<512, 4, 2, false>;   // S >= 3, image <= 72 KB
 using ShapeDeepBig = Shape<1024, 4, 1, false>;  // S >= 3, larger
 using ShapeCnt = Shape<256, 4, 1, true>;        // validation launches (counters on)
 
+// The streaming tile loop of search1d (after the image is in smem): CLC or
+// static tile schedule, 128-bit streaming loads, next-tile prefetch.
 template <int S, int MODE, bool CNT, class SH>
-__global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(const SearchArgs args) {
+__device__ __forceinline__ void search_body(const SearchArgs& args, const AxisParams& a,
+                                            const double* __restrict__ sX,
+                                            const uint32_t* __restrict__ sD, uint4* clc_resp_p,
+                                            uint64_t* clc_bar_p) {
   constexpr int T = SH::kThreads;
   constexpr int U = SH::kUnroll;
   constexpr int TP = SH::kTilePairs;
   constexpr int TE = SH::kTileElems;
-  extern __shared__ __align__(16) uint4 smem[];
-  __shared__ __align__(16) uint4 clc_resp;
-  __shared__ __align__(8) uint64_t clc_bar, stage_bar;
-  if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
-  stage_image(smem, args.image, args.image_16, &stage_bar);
-  pdl_enter();
-  const AxisParams a = args.ax;
-  EOS_DCHECK(a.d_off + 4 * ((int64_t)a.bmax + 1) <= 16 * (int64_t)args.image_16 &&
-             a.x_off + 8 * (int64_t)a.n <= a.d_off);
-  const double* __restrict__ sX =
-      reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
-  const uint32_t* __restrict__ sD =
-      reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(smem) + a.d_off);
+  uint4& clc_resp = *clc_resp_p;
+  uint64_t& clc_bar = *clc_bar_p;
   const double* __restrict__ Y = args.Y;
   int32_t* __restrict__ out = args.out;
   const int64_t count = args.count;
@@ -367,6 +363,152 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
     t = tn;
   }
   if (CNT) cn.flush(args.counters);
+}
+
+template <int S, int MODE, bool CNT, class SH>
+__global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(const SearchArgs args) {
+  extern __shared__ __align__(16) uint4 smem[];
+  __shared__ __align__(16) uint4 clc_resp;
+  __shared__ __align__(8) uint64_t clc_bar, stage_bar;
+  if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
+  stage_image(smem, args.image, args.image_16, &stage_bar);
+  pdl_enter();
+  const AxisParams a = args.ax;
+  EOS_DCHECK(a.d_off + 4 * ((int64_t)a.bmax + 1) <= 16 * (int64_t)args.image_16 &&
+             a.x_off + 8 * (int64_t)a.n <= a.d_off);
+  const double* __restrict__ sX =
+      reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
+  const uint32_t* __restrict__ sD =
+      reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(smem) + a.d_off);
+  search_body<S, MODE, CNT, SH>(args, a, sX, sD, &clc_resp, &clc_bar);
+}
+
+// ------------------------------------------------ zero-setup search (f2) ----
+// eos_search_direct: no host setup at all ("algorithms with zero setup
+// cost may be a better choice" when tables are not known in advance).  Each
+// CTA copies the device-resident table into smem, builds the count directory
+// of a logarithm hash there (histogram + block scan, O(n + bins)), then runs
+// the same streaming tile loop with a runtime in-bin step count.
+constexpr int kDirectMaxTable = 4096;
+constexpr int kDirectMaxBins = 8192;
+using ShapeDirect = Shape<512, 4, 2, true>;
+
+struct DirectArgs {
+  SearchArgs s;          // image unused; ax filled in by the kernel
+  const double* table;   // device fp64[n]
+  int32_t n;
+  int32_t bins_max;      // power of two <= kDirectMaxBins
+  int32_t* status;       // nullable: receives EOS_ERR_UNSORTED / EOS_ERR_NONFINITE
+};
+
+template <class SH>
+__global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
+    search1d_direct_kernel(const DirectArgs A) {
+  constexpr int T = SH::kThreads;
+  extern __shared__ __align__(16) uint4 smem[];
+  __shared__ __align__(16) uint4 clc_resp;
+  __shared__ __align__(8) uint64_t clc_bar;
+  __shared__ AxisParams sa;
+  __shared__ uint32_t s_maxocc, s_bad, s_warp[T / 32];
+  if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
+  pdl_enter();  // the table may come from the previous kernel in the stream
+  const int n = A.n;
+  const int32_t x_bytes = (int32_t)((8 * n + 15) & ~15);
+  double* sX = reinterpret_cast<double*>(smem);
+  uint32_t* sD = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(smem) + x_bytes);
+  uint32_t bad = 0;
+  for (int j = threadIdx.x; j < n; j += T) {
+    const double v = __ldg(A.table + j);
+    if (!isfinite(v)) bad = EOS_ERR_NONFINITE;
+    sX[j] = (v == 0.0) ? 0.0 : v;  // canonicalise -0.0 (R6)
+  }
+  if (threadIdx.x == 0) {
+    s_maxocc = 0;
+    s_bad = 0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j + 1 < n; j += T)
+    if (sX[j + 1] < sX[j]) bad = bad ? bad : EOS_ERR_UNSORTED;
+  if (bad) atomicMax(&s_bad, bad);
+  if (threadIdx.x == 0) {
+    // hash over [lowest binned entry, X[n-1]] (R13): mode 0 bins from the
+    // first entry > 0 (binary search), mode 1 from X[0]
+    AxisParams a{};
+    a.n = n;
+    a.x_off = 0;
+    a.d_off = x_bytes;
+    a.mode = sX[0] >= 0.0 ? 0 : 1;
+    int lo = 0;
+    if (a.mode == 0) {
+      int l = 0, h = n;  // first index with X > 0
+      while (l < h) {
+        const int m = (l + h) >> 1;
+        if (sX[m] > 0.0) h = m; else l = m + 1;
+      }
+      lo = l < n ? l : n - 1;
+    }
+    const uint32_t klo = a.mode ? key_hi<1>(sX[lo]) : key_hi<0>(sX[lo]);
+    const uint32_t khi = a.mode ? key_hi<1>(sX[n - 1]) : key_hi<0>(sX[n - 1]);
+    const uint64_t span = (uint64_t)(khi - klo) + 1;
+    uint64_t M = ((uint64_t)A.bins_max << 32) / span;
+    M = M < 1 ? 1 : (M > 0xFFFFFFFFull ? 0xFFFFFFFFull : M);
+    a.hb = klo;
+    a.M = (uint32_t)M;
+    a.bmax = __umulhi(khi - klo, a.M);
+    a.x0 = sX[0];
+    a.xlast = sX[n - 1];
+    sa = a;
+  }
+  __syncthreads();
+  const int bins = (int)sa.bmax + 1;
+  for (int b = threadIdx.x; b < bins; b += T) sD[b] = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += T) {
+    const uint32_t key = sa.mode ? key_hi<1>(sX[j]) : key_hi<0>(sX[j]);
+    atomicAdd(&sD[bin_of(key, sa)], 1u);
+  }
+  __syncthreads();
+  // exclusive scan of the counts -> packed directory lo | occ << 16
+  const int per = (bins + T - 1) / T;
+  const int b0 = min(bins, (int)threadIdx.x * per), b1 = min(bins, b0 + per);
+  uint32_t local = 0;
+  for (int b = b0; b < b1; ++b) local += sD[b];
+  uint32_t incl = local;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int w = 0; w < T / 32; ++w) {
+      const uint32_t v = s_warp[w];
+      s_warp[w] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  uint32_t run = s_warp[warp] + incl - local, mx = 0;
+  for (int b = b0; b < b1; ++b) {
+    const uint32_t o = sD[b];
+    sD[b] = run | (o << 16);
+    run += o;
+    mx = max(mx, o);
+  }
+  atomicMax(&s_maxocc, mx);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_bad && A.status) atomicExch(A.status, (int32_t)s_bad);
+  AxisParams a = sa;
+  int steps = 0;
+  while ((1u << steps) < s_maxocc + 1) ++steps;
+  a.steps = steps > 0 ? steps : 1;
+  if (a.mode)
+    search_body<0, 1, false, SH>(A.s, a, sX, sD, &clc_resp, &clc_bar);
+  else
+    search_body<0, 0, false, SH>(A.s, a, sX, sD, &clc_resp, &clc_bar);
 }
 
 // ------------------------------------------------------------------ 2-D ----

@@ -70,6 +70,38 @@ def main():
                                 "Glookups_s": round(m / us / 1e3, 3), "create_us": round(create_us, 1)})
             del g
         t.close()
+    # zero-setup path (f2): no create at all
+    Xd = torch.from_numpy(w.table).to(dev)
+    for m in counts:
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                eos.eos_search_direct(Xd.data_ptr(), Xd.numel(), Y.data_ptr(), m, out.data_ptr(), None,
+                                      s.cuda_stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(20):
+                eos.eos_search_direct(Xd.data_ptr(), Xd.numel(), Y.data_ptr(), m, out.data_ptr(),
+                                      None, s.cuda_stream)
+        with torch.cuda.stream(s):
+            g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            for _ in range(5):
+                g.replay()
+            e1.record(s)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / 100
+        res["rows"].append({"k": "direct", "m": m, "us_per_launch": round(us, 3),
+                            "Glookups_s": round(m / us / 1e3, 3), "create_us": 0.0})
+        del g
+    # host cost of create (plan + upload + configure), warm
+    t0 = time.perf_counter()
+    for _ in range(20):
+        eos.Table(w.table).close()
+    res["create_us_warm"] = round((time.perf_counter() - t0) / 20 * 1e6, 1)
     print(json.dumps(res))
 
 

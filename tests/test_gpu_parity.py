@@ -469,3 +469,56 @@ def test_interp_negative_axes_mode1_and_odd_sizes():
         _check_deriv(dR.cpu().numpy(), dRr)
         _check_deriv(dT.cpu().numpy(), dTr)
         g.close()
+
+
+# ---------------------------------------------------- f2: zero-setup search --
+def direct(X, Y, **kw):
+    out = eos.search_direct(to_dev(X), to_dev(Y), **kw)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", sorted(lower_bound_cases().keys()))
+def test_direct_golden(name):
+    X, cases = lower_bound_cases()[name]
+    ys = np.array([c[0] for c in cases] * 101)
+    exp = np.array([c[1] for c in cases] * 101, dtype=np.int32)
+    assert_same(direct(X, ys), exp, ys)
+
+
+def test_direct_edge_tables_and_configs():
+    rng = np.random.default_rng(77)
+    for X in _edge_tables(rng, 80):
+        P = _probes(X)
+        P = np.concatenate([P, rng.permutation(np.repeat(P, 3))])
+        assert_same(direct(X, P), oracle.search(X, P), P)
+    for name in ("cfg1", "cfg2", "cfg3", "cfg5", "paper"):
+        w = datagen.workload(name, count=(1 << 21) + 5)
+        Y = w.targets.host_fill(0, w.count, w.table)
+        assert_same(direct(w.table, Y), oracle.search(w.table, Y), Y)
+        yd = to_dev(Y)[1:]   # misaligned view
+        out = eos.search_direct(to_dev(w.table), yd)
+        torch.cuda.synchronize()
+        assert_same(out.cpu().numpy(), oracle.search(w.table, Y[1:]))
+
+
+def test_direct_reports_invalid_tables_and_limits():
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    y = torch.linspace(0, 10, 5000, dtype=torch.float64, device=DEV)
+    eos.search_direct(torch.tensor([1.0, 3.0, 2.0], dtype=torch.float64, device=DEV), y, status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 4          # EOS_ERR_UNSORTED
+    st.zero_()
+    eos.search_direct(torch.tensor([1.0, float("nan"), 2.0], dtype=torch.float64, device=DEV), y,
+                      status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 3          # EOS_ERR_NONFINITE
+    st.zero_()
+    eos.search_direct(torch.tensor([1.0, 2.0, 2.0, 5.0], dtype=torch.float64, device=DEV), y,
+                      status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    with pytest.raises(eos.EosError) as e:
+        eos.search_direct(torch.ones(4097, dtype=torch.float64, device=DEV), y)
+    assert e.value.code == 2
+    assert_same(direct(np.array([7.0]), np.array([1.0, 7.0, 9.0, np.nan])), np.zeros(4, np.int32))
