@@ -227,8 +227,20 @@ bool overlaps(const void* a, int64_t abytes, const void* b, int64_t bbytes) {
 
 // Configure a kernel for `smem` bytes of dynamic shared memory and return the
 // persistent grid (#SM x resident CTAs per SM).
+// The dynamic-smem limit is a per-function attribute shared by every handle
+// that uses the same kernel instantiation, so it is raised to the device's
+// opt-in maximum (never lowered to one table's size: a later, smaller table
+// must not break launches of an earlier, larger one).  Occupancy still
+// follows the actual per-launch size.
 eos_status configure(const void* fn, int threads, int64_t smem, int num_sms, int* grid, int* per_sm) {
-  EOS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, optin = 0;
+  EOS_CUDA(cudaGetDevice(&dev));
+  EOS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa;
+  EOS_CUDA(cudaFuncGetAttributes(&fa, fn));
+  const int64_t limit = (int64_t)optin - (int64_t)fa.sharedSizeBytes;
+  if (smem > limit) return EOS_ERR_UNSUPPORTED;
+  EOS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit));
   int occ = 0;
   EOS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, (size_t)smem));
   if (occ < 1) return EOS_ERR_UNSUPPORTED;

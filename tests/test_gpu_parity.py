@@ -522,3 +522,21 @@ def test_direct_reports_invalid_tables_and_limits():
         eos.search_direct(torch.ones(4097, dtype=torch.float64, device=DEV), y)
     assert e.value.code == 2
     assert_same(direct(np.array([7.0]), np.array([1.0, 7.0, 9.0, np.nan])), np.zeros(4, np.int32))
+
+
+def test_handles_sharing_a_kernel_do_not_interfere():
+    """A big-image table created first, then a small-image one using the same kernel
+    instantiation: the first must still launch (the smem limit is per kernel, not per table)."""
+    rng = np.random.default_rng(3)
+    Xs = np.sort(10.0 ** rng.uniform(-3, 3, 50))
+    Xb = np.sort(10.0 ** rng.uniform(-3, 3, 3000))
+    big = eos.Table(Xb, log_bins=20000)       # S=1..2, ~100 KB image
+    small = eos.Table(Xs, log_bins=16)
+    Y = 10.0 ** rng.uniform(-4, 4, 100_003)
+    yd = to_dev(Y)
+    for t, X in ((big, Xb), (small, Xs), (big, Xb)):
+        out = t.search(yd)
+        torch.cuda.synchronize()
+        assert_same(out.cpu().numpy(), oracle.search(X, Y))
+    big.close()
+    small.close()
