@@ -528,10 +528,12 @@ def test_handles_sharing_a_kernel_do_not_interfere():
     """A big-image table created first, then a small-image one using the same kernel
     instantiation: the first must still launch (the smem limit is per kernel, not per table)."""
     rng = np.random.default_rng(3)
-    Xs = np.sort(10.0 ** rng.uniform(-3, 3, 50))
-    Xb = np.sort(10.0 ** rng.uniform(-3, 3, 3000))
-    big = eos.Table(Xb, log_bins=20000)       # S=1..2, ~100 KB image
-    small = eos.Table(Xs, log_bins=16)
+    Xb = np.logspace(-3, 3, 1000)
+    Xs = np.logspace(-3, 3, 100)
+    big = eos.Table(Xb, log_bins=12000)        # S=1, ~56 KB image: 2 x 512 shape
+    small = eos.Table(Xs, log_bins=8300)       # S=1, ~34 KB image: same kernel instantiation
+    assert big.info.steps == small.info.steps == 1
+    assert 32 * 1024 < small.info.image_bytes < big.info.image_bytes <= 72 * 1024
     Y = 10.0 ** rng.uniform(-4, 4, 100_003)
     yd = to_dev(Y)
     for t, X in ((big, Xb), (small, Xs), (big, Xb)):
