@@ -48,6 +48,7 @@ def lib():
         L.oracle_interp2d.argtypes = [P, I64, P, I64, P, P, P, I64, P, P, P]
         L.oracle_counters.argtypes = [P, I64, P, P, I64, I64, P]
         L.oracle_interp2d_deriv.argtypes = [P, I64, P, I64, P, P, P, I64, P, P]
+        L.oracle_interp2d_loglog.argtypes = [P, I64, P, I64, P, P, P, I64, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -128,6 +129,30 @@ def interp2d_deriv(R, Tax, G, rho, T, threads: int | None = None):
     with ThreadPoolExecutor(threads) as ex:
         list(ex.map(run, _chunks(m, threads)))
     return dr, dt
+
+
+def interp2d_loglog(R, Tax, G, rho, T, threads: int | None = None):
+    """(P, iR, iT, dP/drho, dP/dT): log-log bilinear interpolation (eos_oracle.c, R24)."""
+    R, Tax, G, rho, T = _f64(R), _f64(Tax), _f64(G), _f64(rho), _f64(T)
+    assert G.shape == (R.size, Tax.size) and rho.size == T.size
+    m = rho.size
+    P, dr, dt = (np.empty(m, dtype=np.float64) for _ in range(3))
+    iR = np.empty(m, dtype=np.int32)
+    iT = np.empty(m, dtype=np.int32)
+    L = lib()
+    threads = threads or default_threads()
+
+    def run(r):
+        s, e = r
+        L.oracle_interp2d_loglog(R.ctypes.data, R.size, Tax.ctypes.data, Tax.size, G.ctypes.data,
+                                 rho.ctypes.data + 8 * s, T.ctypes.data + 8 * s, e - s,
+                                 P.ctypes.data + 8 * s, iR.ctypes.data + 4 * s,
+                                 iT.ctypes.data + 4 * s, dr.ctypes.data + 8 * s,
+                                 dt.ctypes.data + 8 * s)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(run, _chunks(m, threads)))
+    return P, iR, iT, dr, dt
 
 
 def counters(X, Y, idx, global_offset: int = 0) -> np.ndarray:

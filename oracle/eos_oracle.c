@@ -111,6 +111,43 @@ void oracle_interp2d_deriv(const double* R, int64_t nR, const double* Tax, int64
   }
 }
 
+/* Log-log bilinear interpolation (EOSPAC-style table variant, SURVEY §8(f)
+ * f4; reading R24 in DESIGN.md): the same brackets and cells as
+ * oracle_interp2d, but the interpolation runs on ln P over (ln rho, ln T):
+ *   tx = clamp01((ln rho - ln R[ci]) / (ln R[ci+1] - ln R[ci])), ty likewise
+ *   P  = exp((1-tx)((1-ty) ln G[ci][cj] + ty ln G[ci][cj+1])
+ *            + tx ((1-ty) ln G[ci+1][cj] + ty ln G[ci+1][cj+1]))
+ * Requires R, T, G > 0.  Exact for power laws G = C rho^a T^b.  Derivatives
+ * (NULL-able): dP/drho = P * s_rho / rho with s_rho the cell slope of ln P in
+ * ln rho, 0 outside the axis range, NaN for NaN; likewise dP/dT. */
+void oracle_interp2d_loglog(const double* R, int64_t nR, const double* Tax, int64_t nT,
+                            const double* G, const double* rho, const double* T, int64_t m,
+                            double* P, int32_t* iR, int32_t* iT, double* dPdrho, double* dPdT) {
+  for (int64_t q = 0; q < m; ++q) {
+    int32_t i = oracle_lower_bound(R, nR, rho[q]);
+    int32_t j = oracle_lower_bound(Tax, nT, T[q]);
+    int64_t ci = i < nR - 2 ? i : nR - 2;
+    int64_t cj = j < nT - 2 ? j : nT - 2;
+    double lr0 = log(R[ci]), lr1 = log(R[ci + 1]);
+    double lt0 = log(Tax[cj]), lt1 = log(Tax[cj + 1]);
+    double tx = clamp01((log(rho[q]) - lr0) / (lr1 - lr0));
+    double ty = clamp01((log(T[q]) - lt0) / (lt1 - lt0));
+    double l00 = log(G[ci * nT + cj]), l01 = log(G[ci * nT + cj + 1]);
+    double l10 = log(G[(ci + 1) * nT + cj]), l11 = log(G[(ci + 1) * nT + cj + 1]);
+    double lp = (1.0 - tx) * ((1.0 - ty) * l00 + ty * l01) + tx * ((1.0 - ty) * l10 + ty * l11);
+    double p = exp(lp);
+    P[q] = p;
+    if (iR) iR[q] = i;
+    if (iT) iT[q] = j;
+    double sr = ((1.0 - ty) * (l10 - l00) + ty * (l11 - l01)) / (lr1 - lr0);
+    double st = ((1.0 - tx) * (l01 - l00) + tx * (l11 - l10)) / (lt1 - lt0);
+    int in_r = rho[q] >= R[0] && rho[q] <= R[nR - 1];
+    int in_t = T[q] >= Tax[0] && T[q] <= Tax[nT - 1];
+    if (dPdrho) dPdrho[q] = (rho[q] != rho[q]) ? rho[q] : (in_r ? p * sr / rho[q] : 0.0);
+    if (dPdT) dPdT[q] = (T[q] != T[q]) ? T[q] : (in_t ? p * st / T[q] : 0.0);
+  }
+}
+
 /* Validation counters over one shard (DESIGN.md
  * "Counters").  Accumulated (+=) into c[8], all sums modulo 2^64:
  *   c0 = number of targets

@@ -294,3 +294,39 @@ def test_interp_derivatives_match_finite_differences():
     pp, _, _ = oracle.interp2d(R, T, G, rho, t + ht)
     pm, _, _ = oracle.interp2d(R, T, G, rho, t - ht)
     assert np.allclose((pp - pm) / (2 * ht), dt, rtol=1e-6, atol=1e-9 * np.abs(dt).max())
+
+
+# ------------------------------------------------------- log-log bilinear ---
+def test_loglog_is_exact_for_power_laws():
+    """R24: interpolating ln P bilinearly in (ln rho, ln T) reproduces G = C rho^a T^b
+    exactly (up to rounding) inside the grid, with dP/drho = a P / rho, dP/dT = b P / T."""
+    rng = np.random.default_rng(9)
+    R, T = _axes(rng)
+    C, a, b = 2.5, 1.0, 1.5
+    G = C * R[:, None] ** a * T[None, :] ** b
+    rho = 10.0 ** rng.uniform(np.log10(R[0]), np.log10(R[-1]), 20000)
+    t = 10.0 ** rng.uniform(np.log10(T[0]), np.log10(T[-1]), 20000)
+    rho = np.clip(rho, R[0], R[-1])
+    t = np.clip(t, T[0], T[-1])
+    P, iR, iT, dr, dt = oracle.interp2d_loglog(R, T, G, rho, t)
+    exact = C * rho ** a * t ** b
+    assert np.max(np.abs(P / exact - 1)) < 1e-12
+    assert np.max(np.abs(dr / (a * exact / rho) - 1)) < 1e-9
+    assert np.max(np.abs(dt / (b * exact / t) - 1)) < 1e-9
+    assert np.array_equal(iR, oracle.search(R, rho)) and np.array_equal(iT, oracle.search(T, t))
+
+
+def test_loglog_nodes_outside_and_nan():
+    rng = np.random.default_rng(10)
+    R, T = _axes(rng)
+    G = rng.uniform(1.0, 50.0, (R.size, T.size))
+    rr, tt = np.meshgrid(R, T, indexing="ij")
+    P, _, _, _, _ = oracle.interp2d_loglog(R, T, G, rr.ravel(), tt.ravel())
+    assert np.max(np.abs(P / G.ravel() - 1)) < 1e-14            # nodes (exp(log g) round trip)
+    rho = np.array([R[0] / 10, R[-1] * 10, np.nan, R[2], -1.0])
+    t = np.array([T[1], T[1], T[1], np.nan, T[1]])
+    P, _, _, dr, dt = oracle.interp2d_loglog(R, T, G, rho, t)
+    assert abs(P[0] / G[0, 1] - 1) < 1e-14 and abs(P[1] / G[-1, 1] - 1) < 1e-14   # clamped
+    assert dr[0] == 0.0 and dr[1] == 0.0
+    assert np.isnan(P[2]) and np.isnan(dr[2]) and np.isnan(P[3]) and np.isnan(dt[3])
+    assert np.isnan(P[4])                                         # ln of a negative density
