@@ -214,6 +214,17 @@ EOS_API eos_status eos_search_destroy(eos_table t);
 EOS_API eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double* T_host,
                              int64_t n_T, const double* P_host, eos_grid2d* out);
 
+/* Interpolation variant of a grid (eos_grid2d_create_ex flags). */
+#define EOS_GRID_LINEAR 0 /* bilinear in (rho, T) on P -- the formula above (R14) */
+#define EOS_GRID_LOGLOG 1 /* bilinear in (ln rho, ln T) on ln P, P = exp(.) (R24):
+                           *   tx = clamp01((ln rho - ln R[ci]) / (ln R[ci+1] - ln R[ci])), ty
+                           *   likewise, P = exp(bilinear of ln G); exact for power laws.
+                           *   Needs R, T, P > 0 (else EOS_ERR_UNSUPPORTED).  Brackets are
+                           *   the same P:54 lower bounds.  Derivatives (eos_interp2d_ex):
+                           *   dP/drho = P (d ln P / d ln rho) / rho on the cell. */
+EOS_API eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const double* T_host,
+                                int64_t n_T, const double* P_host, int32_t flags, eos_grid2d* out);
+
 /* P_out_dev[q] = interpolated value at (rho_dev[q], T_dev[q]);
  * irho_out_dev / iT_out_dev (nullable) receive the brackets i, j.
  * All device arrays of length count; outputs must not overlap inputs. */

@@ -29,13 +29,15 @@ __all__ = [
     "eos_interp2d_host", "eos_grid2d_destroy", "eos_grid2d_info", "eos_status_str", "EOS_K_AUTO",
     "EOS_MAX_TABLE", "EOS_MAX_K", "EXPORTED_SYMBOLS", "EOS_HASH_AUTO", "EOS_HASH_EXPONENT",
     "EOS_HASH_LOG", "eos_plan_table_hash", "eos_search_create_hash", "eos_interp2d_ex",
-    "eos_search_direct", "search_direct",
+    "eos_search_direct", "search_direct", "eos_grid2d_create_ex", "EOS_GRID_LINEAR",
+    "EOS_GRID_LOGLOG",
 ]
 
 EOS_MAX_TABLE = 16384
 EOS_MAX_K = 19
 EOS_K_AUTO = -1
 EOS_HASH_AUTO, EOS_HASH_EXPONENT, EOS_HASH_LOG = 0, 1, 2
+EOS_GRID_LINEAR, EOS_GRID_LOGLOG = 0, 1
 
 STATUS = {
     0: "EOS_OK", 1: "EOS_ERR_NULL", 2: "EOS_ERR_SIZE", 3: "EOS_ERR_NONFINITE",
@@ -49,7 +51,7 @@ EXPORTED_SYMBOLS = (
     "eos_search_host", "eos_table_info", "eos_search_destroy", "eos_grid2d_create",
     "eos_interp2d", "eos_interp2d_host", "eos_grid2d_info", "eos_grid2d_destroy",
     "eos_status_str", "eos_abi_version", "eos_launch_count", "eos_plan_table_hash",
-    "eos_search_create_hash", "eos_interp2d_ex", "eos_search_direct",
+    "eos_search_create_hash", "eos_interp2d_ex", "eos_search_direct", "eos_grid2d_create_ex",
 )
 
 
@@ -101,6 +103,7 @@ def load_library():
         "eos_table_info": [_P, _P],
         "eos_search_destroy": [_P],
         "eos_grid2d_create": [_P, _I64, _P, _I64, _P, _P],
+        "eos_grid2d_create_ex": [_P, _I64, _P, _I64, _P, _I32, _P],
         "eos_interp2d": [_P, _P, _P, _I64, _P, _P, _P, _P],
         "eos_interp2d_ex": [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P],
         "eos_search_direct": [_P, _I64, _P, _I64, _P, _P, _P],
@@ -265,15 +268,18 @@ def eos_search_destroy(handle) -> None:
     _check(load_library().eos_search_destroy(handle), "eos_search_destroy")
 
 
-def eos_grid2d_create(rho, T, P) -> int:
+def eos_grid2d_create(rho, T, P, flags: int = EOS_GRID_LINEAR) -> int:
     L = load_library()
     r, t, p = _f64_host(rho), _f64_host(T), _f64_host(P)
     if p.size != r.size * t.size:
         raise ValueError("P must have n_rho * n_T values (row-major, T fastest)")
     h = ctypes.c_void_p()
-    _check(L.eos_grid2d_create(r.ctypes.data, r.size, t.ctypes.data, t.size, p.ctypes.data,
-                               ctypes.byref(h)), "eos_grid2d_create")
+    _check(L.eos_grid2d_create_ex(r.ctypes.data, r.size, t.ctypes.data, t.size, p.ctypes.data,
+                                  flags, ctypes.byref(h)), "eos_grid2d_create")
     return h.value
+
+
+eos_grid2d_create_ex = eos_grid2d_create
 
 
 def eos_interp2d(handle, rho_ptr, T_ptr, count, P_ptr, iR_ptr, iT_ptr, stream):
@@ -376,10 +382,13 @@ class Table:
 class Grid2D:
     """EOSPAC-style 2-D table (density x temperature) for eos_interp2d."""
 
-    def __init__(self, rho, T, P):
+    def __init__(self, rho, T, P, loglog: bool = False):
+        """loglog=True: interpolate ln P bilinearly in (ln rho, ln T) (EOS_GRID_LOGLOG, R24)."""
         self.rho, self.T = _f64_host(rho).copy(), _f64_host(T).copy()
         self.P = _f64_host(P).reshape(self.rho.size, self.T.size).copy()
-        self._h = eos_grid2d_create(self.rho, self.T, self.P)
+        self.loglog = loglog
+        self._h = eos_grid2d_create(self.rho, self.T, self.P,
+                                    EOS_GRID_LOGLOG if loglog else EOS_GRID_LINEAR)
         self.rho_info, self.T_info = eos_grid2d_info(self._h)
 
     @property

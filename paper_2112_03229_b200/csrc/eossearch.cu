@@ -50,7 +50,8 @@ struct eos_grid2d_s {
   int grid = 0, grid_deriv = 0;
   int threads = 512, unroll = 2;
   bool clc = true;
-  int32_t wr_off = 0, wt_off = 0;
+  int32_t flags = 0;
+  int32_t wr_off = 0, wt_off = 0, lr_off = 0, lt_off = 0;
 };
 
 namespace {
@@ -156,6 +157,12 @@ const void* interp_deriv_fn_s() {
   return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, true>;
 }
 
+template <int S>
+const void* interp_loglog_fn_s(bool deriv) {
+  return deriv ? (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, true, true>
+               : (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, true>;
+}
+
 struct Interp2DShape {
   const void* fn;
   const void* fn_deriv;  // same shape, with dP/drho and dP/dT outputs
@@ -166,7 +173,18 @@ struct Interp2DShape {
 // EOS_INTERP_VARIANT (tuning experiments only): 0 static1024u1 (default),
 // 1 static512u2, 2 static1024u2, 3 static512u4, 4 clc512u2,
 // 5 static512u2+recip, 6 static1024u1+recip.
-Interp2DShape pick_interp(int steps) {
+Interp2DShape pick_interp(int steps, bool loglog) {
+  if (loglog) {
+    const void *fn, *fd;
+    switch (steps) {
+      case 1: fn = interp_loglog_fn_s<1>(false); fd = interp_loglog_fn_s<1>(true); break;
+      case 2: fn = interp_loglog_fn_s<2>(false); fd = interp_loglog_fn_s<2>(true); break;
+      case 3: fn = interp_loglog_fn_s<3>(false); fd = interp_loglog_fn_s<3>(true); break;
+      case 4: fn = interp_loglog_fn_s<4>(false); fd = interp_loglog_fn_s<4>(true); break;
+      default: fn = interp_loglog_fn_s<0>(false); fd = interp_loglog_fn_s<0>(true); break;
+    }
+    return {fn, fd, dv::Shape2D::kThreads, dv::Shape2D::kUnroll, dv::Shape2D::kClc};
+  }
   int v = 0;
   if (const char* e = getenv("EOS_INTERP_VARIANT")) v = atoi(e);
   static const int thr[7] = {1024, 512, 1024, 512, 512, 512, 1024};
@@ -311,6 +329,8 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   a.g_off = g->g_off;
   a.wr_off = g->wr_off;
   a.wt_off = g->wt_off;
+  a.lr_off = g->lr_off;
+  a.lt_off = g->lt_off;
   a.r = g->ar;
   a.t = g->at;
   a.rho = rho;
@@ -600,32 +620,65 @@ eos_status eos_search_destroy(eos_table t) {
 // -------------------------------------------------------------------- 2-D --
 eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double* T_host,
                              int64_t n_T, const double* P_host, eos_grid2d* out) {
+  return eos_grid2d_create_ex(rho_host, n_rho, T_host, n_T, P_host, EOS_GRID_LINEAR, out);
+}
+
+eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const double* T_host,
+                                int64_t n_T, const double* P_host, int32_t flags,
+                                eos_grid2d* out) {
   if (!out) return EOS_ERR_NULL;
   *out = nullptr;
   if (!rho_host || !T_host || !P_host) return EOS_ERR_NULL;
+  if (flags != EOS_GRID_LINEAR && flags != EOS_GRID_LOGLOG) return EOS_ERR_UNSUPPORTED;
+  const bool loglog = flags == EOS_GRID_LOGLOG;
   eos_grid2d g = new (std::nothrow) eos_grid2d_s();
   if (!g) return EOS_ERR_NOMEM;
   eos_status st = eos::plan_table(rho_host, n_rho, EOS_HASH_AUTO, 0, true, &g->pr);
   if (st == EOS_OK) st = eos::plan_table(T_host, n_T, EOS_HASH_AUTO, 0, true, &g->pt);
   if (st != EOS_OK) { delete g; return st; }
+  g->flags = flags;
   const int64_t ncell = n_rho * n_T;
   for (int64_t q = 0; q < ncell; ++q)
     if (!isfinite(P_host[q])) { delete g; return EOS_ERR_NONFINITE; }
+  if (loglog) {  // ln of the axes and the grid must exist (R24)
+    bool ok = g->pr.X[0] > 0.0 && g->pt.X[0] > 0.0;
+    for (int64_t q = 0; q < ncell && ok; ++q) ok = P_host[q] > 0.0;
+    if (!ok) { delete g; return EOS_ERR_UNSUPPORTED; }
+  }
   // image: [rho X | rho dir][T X | T dir][G][1/dR][1/dT]
   const int64_t r_bytes = g->pr.image_bytes, t_bytes = g->pt.image_bytes;
   const int64_t g_bytes = (8 * ncell + 15) & ~int64_t(15);
   const int64_t wr_bytes = (8 * (n_rho - 1) + 15) & ~int64_t(15);
   const int64_t wt_bytes = (8 * (n_T - 1) + 15) & ~int64_t(15);
-  g->image_bytes = r_bytes + t_bytes + g_bytes + wr_bytes + wt_bytes;
+  const int64_t lr_bytes = loglog ? (8 * n_rho + 15) & ~int64_t(15) : 0;
+  const int64_t lt_bytes = loglog ? (8 * n_T + 15) & ~int64_t(15) : 0;
+  g->image_bytes = r_bytes + t_bytes + g_bytes + wr_bytes + wt_bytes + lr_bytes + lt_bytes;
   if (g->image_bytes > 220 * 1024) { delete g; return EOS_ERR_UNSUPPORTED; }
   std::vector<uint8_t> img((size_t)g->image_bytes, 0);
   std::vector<uint8_t> ir = eos::make_image(g->pr), it = eos::make_image(g->pt);
   memcpy(img.data(), ir.data(), ir.size());
   memcpy(img.data() + r_bytes, it.data(), it.size());
-  memcpy(img.data() + r_bytes + t_bytes, P_host, 8 * (size_t)ncell);
   g->g_off = (int32_t)(r_bytes + t_bytes);
   g->wr_off = (int32_t)(g->g_off + g_bytes);
   g->wt_off = (int32_t)(g->wr_off + wr_bytes);
+  g->lr_off = (int32_t)(g->wt_off + wt_bytes);
+  g->lt_off = (int32_t)(g->lr_off + lr_bytes);
+  if (loglog) {  // the grid holds ln G; ln of the axes follow the reciprocal widths
+    for (int64_t q = 0; q < ncell; ++q) {
+      const double v = log(P_host[q]);
+      memcpy(img.data() + g->g_off + 8 * q, &v, 8);
+    }
+    for (int64_t q = 0; q < n_rho; ++q) {
+      const double v = log(g->pr.X[q]);
+      memcpy(img.data() + g->lr_off + 8 * q, &v, 8);
+    }
+    for (int64_t q = 0; q < n_T; ++q) {
+      const double v = log(g->pt.X[q]);
+      memcpy(img.data() + g->lt_off + 8 * q, &v, 8);
+    }
+  } else {
+    memcpy(img.data() + g->g_off, P_host, 8 * (size_t)ncell);
+  }
   for (int64_t q = 0; q + 1 < n_rho; ++q) {
     const double w = 1.0 / (g->pr.X[q + 1] - g->pr.X[q]);
     memcpy(img.data() + g->wr_off + 8 * q, &w, 8);
@@ -641,7 +694,7 @@ eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double
   if (e != cudaSuccess) { delete g; return cuda_status(e); }
   st = upload(img, &g->image_dev);
   if (st != EOS_OK) { delete g; return st; }
-  Interp2DShape sh = pick_interp(std::max(g->pr.steps, g->pt.steps));
+  Interp2DShape sh = pick_interp(std::max(g->pr.steps, g->pt.steps), loglog);
   g->fn = sh.fn;
   g->fn_deriv = sh.fn_deriv;
   g->threads = sh.threads;

@@ -518,6 +518,8 @@ struct Interp2DArgs {
   int32_t g_off;    // byte offset of G fp64[nR*nT] in the image
   int32_t wr_off;   // byte offset of 1/(R[i+1]-R[i]) fp64[nR-1] (RECIP variant)
   int32_t wt_off;   // byte offset of 1/(T[j+1]-T[j]) fp64[nT-1] (RECIP variant)
+  int32_t lr_off;   // byte offset of ln R fp64[nR] (LOGLOG grids)
+  int32_t lt_off;   // byte offset of ln T fp64[nT] (LOGLOG grids)
   int32_t vec_ok;
   int32_t pad_;
   int64_t ntiles;
@@ -580,7 +582,7 @@ __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ s
 // of that formula (bit-identical to a plain evaluation in that order).
 // RECIP: weights as (x - X[c]) * (1/(X[c+1]-X[c])) with the reciprocal
 // precomputed at create (a few ulp from the divide; within the 1e-12 bar).
-template <int S, bool RECIP, bool DERIV>
+template <int S, bool RECIP, bool DERIV, bool LOGLOG>
 __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, int32_t& j,
                                              double& dpr, double& dpt, const char* sm,
                                              const Interp2DArgs& A) {
@@ -588,20 +590,31 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   const double* sT = reinterpret_cast<const double*>(sm + A.t.x_off);
   const uint32_t* dR = reinterpret_cast<const uint32_t*>(sm + A.r.d_off);
   const uint32_t* dT = reinterpret_cast<const uint32_t*>(sm + A.t.d_off);
-  const double* sG = reinterpret_cast<const double*>(sm + A.g_off);
+  const double* sG = reinterpret_cast<const double*>(sm + A.g_off);  // G, or ln G (LOGLOG)
   int32_t ci, cj;
   double r0, r1, t0, t1;
   axis_cell<S>(rho, sR, dR, A.r, i, ci, r0, r1);
   axis_cell<S>(T, sT, dT, A.t, j, cj, t0, t1);
+  double xr = rho, xt = T;  // interpolation coordinates
+  if (LOGLOG) {             // R24: ln P bilinear in (ln rho, ln T)
+    const double* lR = reinterpret_cast<const double*>(sm + A.lr_off);
+    const double* lT = reinterpret_cast<const double*>(sm + A.lt_off);
+    r0 = lR[ci];
+    r1 = lR[ci + 1];
+    t0 = lT[cj];
+    t1 = lT[cj + 1];
+    xr = log(rho);
+    xt = log(T);
+  }
   double tx, ty;
-  if (RECIP) {
+  if (RECIP && !LOGLOG) {
     const double* wR = reinterpret_cast<const double*>(sm + A.wr_off);
     const double* wT = reinterpret_cast<const double*>(sm + A.wt_off);
-    tx = clamp01(__dmul_rn(__dsub_rn(rho, r0), wR[ci]));
-    ty = clamp01(__dmul_rn(__dsub_rn(T, t0), wT[cj]));
+    tx = clamp01(__dmul_rn(__dsub_rn(xr, r0), wR[ci]));
+    ty = clamp01(__dmul_rn(__dsub_rn(xt, t0), wT[cj]));
   } else {
-    tx = clamp01(__ddiv_rn(__dsub_rn(rho, r0), __dsub_rn(r1, r0)));
-    ty = clamp01(__ddiv_rn(__dsub_rn(T, t0), __dsub_rn(t1, t0)));
+    tx = clamp01(__ddiv_rn(__dsub_rn(xr, r0), __dsub_rn(r1, r0)));
+    ty = clamp01(__ddiv_rn(__dsub_rn(xt, t0), __dsub_rn(t1, t0)));
   }
   EOS_DCHECK(ci >= 0 && cj >= 0 && ci + 1 < A.r.n && cj + 1 < A.t.n);
   const double* g0 = sG + (int64_t)ci * A.t.n + cj;
@@ -611,9 +624,12 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   const double ux = __dsub_rn(1.0, tx);
   const double a0 = __dadd_rn(__dmul_rn(uy, g00), __dmul_rn(ty, g01));
   const double a1 = __dadd_rn(__dmul_rn(uy, g10), __dmul_rn(ty, g11));
+  const double v = __dadd_rn(__dmul_rn(ux, a0), __dmul_rn(tx, a1));
+  const double p = LOGLOG ? exp(v) : v;
   if (DERIV) {
-    // Partial derivatives of the bilinear form on the cell (R23); 0 outside an
-    // axis range (the clamped interpolant is constant there); NaN kept.
+    // Partial derivatives of the interpolant on the cell (R23 / R24); 0
+    // outside an axis range (the clamped interpolant is constant there); NaN
+    // kept.  LOGLOG: dP/drho = P * (d ln P / d ln rho) / rho.
     const double sr = __ddiv_rn(__dadd_rn(__dmul_rn(uy, __dsub_rn(g10, g00)),
                                           __dmul_rn(ty, __dsub_rn(g11, g01))),
                                 __dsub_rn(r1, r0));
@@ -622,10 +638,12 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
                                 __dsub_rn(t1, t0));
     const bool in_r = rho >= A.r.x0 && rho <= A.r.xlast;
     const bool in_t = T >= A.t.x0 && T <= A.t.xlast;
-    dpr = (rho != rho) ? rho : (in_r ? sr : 0.0);
-    dpt = (T != T) ? T : (in_t ? st : 0.0);
+    const double dr = LOGLOG ? __ddiv_rn(__dmul_rn(p, sr), rho) : sr;
+    const double dt = LOGLOG ? __ddiv_rn(__dmul_rn(p, st), T) : st;
+    dpr = (rho != rho) ? rho : (in_r ? dr : 0.0);
+    dpt = (T != T) ? T : (in_t ? dt : 0.0);
   }
-  return __dadd_rn(__dmul_rn(ux, a0), __dmul_rn(tx, a1));
+  return p;
 }
 
 // default 2-D launch shape (165 KB image: 1 CTA/SM).  Static schedule: the
@@ -633,7 +651,7 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
 // costs more than the static tail (profiles/r01_exp_interp.json).
 using Shape2D = Shape<1024, 1, 1, false>;
 
-template <int S, class SH, bool RECIP, bool DERIV>
+template <int S, class SH, bool RECIP, bool DERIV, bool LOGLOG = false>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {
   constexpr int T = SH::kThreads;
   constexpr int U = SH::kUnroll;
@@ -692,9 +710,9 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       int2 ir[U], it[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        p[u].x = interp_one<S, RECIP, DERIV>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
+        p[u].x = interp_one<S, RECIP, DERIV, LOGLOG>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
                                              sm, A);
-        p[u].y = interp_one<S, RECIP, DERIV>(vr[u].y, vt[u].y, ir[u].y, it[u].y, dr[u].y, dt[u].y,
+        p[u].y = interp_one<S, RECIP, DERIV, LOGLOG>(vr[u].y, vt[u].y, ir[u].y, it[u].y, dr[u].y, dt[u].y,
                                              sm, A);
       }
       tn = next_tile(t);
@@ -719,7 +737,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       for (int64_t q = e0 + threadIdx.x; q < e1; q += T) {
         int32_t i, j;
         double dpr, dpt;
-        const double pq = interp_one<S, RECIP, DERIV>(A.rho[q], A.T[q], i, j, dpr, dpt, sm, A);
+        const double pq = interp_one<S, RECIP, DERIV, LOGLOG>(A.rho[q], A.T[q], i, j, dpr, dpt, sm, A);
         A.P[q] = pq;
         if (br) A.iR[q] = i;
         if (bt) A.iT[q] = j;

@@ -542,3 +542,41 @@ def test_handles_sharing_a_kernel_do_not_interfere():
         assert_same(out.cpu().numpy(), oracle.search(X, Y))
     big.close()
     small.close()
+
+
+# ------------------------------------------------------ f4: log-log grids ---
+def test_loglog_grid_matches_oracle():
+    w = datagen.workload("cfg4", count=(1 << 20) + 1)
+    rho = w.rho_targets.host_fill(0, w.count)
+    T = w.T_targets.host_fill(0, w.count)
+    rho[:5] = [np.nan, w.rho[0] / 10, w.rho[-1] * 10, w.rho[5], -1.0]
+    T[5:8] = [np.nan, w.T[0] / 10, w.T[-1] * 10]
+    g = eos.Grid2D(w.rho, w.T, w.P, loglog=True)
+    P, iR, iT, dR, dT = g.interp(to_dev(rho), to_dev(T), derivatives=True)
+    P0, _, _ = g.interp(to_dev(rho), to_dev(T))
+    torch.cuda.synchronize()
+    Pr, iRr, iTr, dRr, dTr = oracle.interp2d_loglog(w.rho, w.T, w.P, rho, T)
+    assert np.array_equal(iR.cpu().numpy(), iRr) and np.array_equal(iT.cpu().numpy(), iTr)
+    err = check_interp(P.cpu().numpy(), Pr)
+    assert err < 1e-13   # device vs libm log/exp: a few ulp
+    assert np.array_equal(P0.cpu().numpy(), P.cpu().numpy(), equal_nan=True)
+    _check_deriv(dR.cpu().numpy(), dRr)
+    _check_deriv(dT.cpu().numpy(), dTr)
+    g.close()
+    with pytest.raises(eos.EosError) as e:
+        bad = w.P.copy()
+        bad[3, 4] = -1.0
+        eos.Grid2D(w.rho, w.T, bad, loglog=True)
+    assert e.value.code == 8
+
+
+def test_loglog_host_pipeline():
+    w = datagen.workload("cfg4", count=300_007)
+    rho = w.rho_targets.host_fill(0, w.count)
+    T = w.T_targets.host_fill(0, w.count)
+    g = eos.Grid2D(w.rho, w.T, w.P, loglog=True)
+    P, iR, iT = g.interp_host(rho, T)
+    Pr, iRr, iTr, _, _ = oracle.interp2d_loglog(w.rho, w.T, w.P, rho, T)
+    assert np.array_equal(iR, iRr) and np.array_equal(iT, iTr)
+    check_interp(P, Pr)
+    g.close()
