@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--count", type=int, default=None, help="override targets per GPU (testing)")
+    ap.add_argument("--loglog", action="store_true", help="cfg4: log-log grid (EOS_GRID_LOGLOG)")
+    ap.add_argument("--derivatives", action="store_true", help="cfg4: also write dP/drho, dP/dT")
     ap.add_argument("--eager", action="store_true",
                     help="launch each step from Python with per-launch events instead of a CUDA graph")
     return ap.parse_args()
@@ -169,12 +171,20 @@ def run_ours(a, d: Dist):
         P = torch.empty(count, dtype=torch.float64, device=dev)
         iR = torch.empty(count, dtype=torch.int32, device=dev)
         iT = torch.empty(count, dtype=torch.int32, device=dev)
-        obj = eos.Grid2D(w.rho, w.T, w.P)
-        info = {"rho": obj.rho_info.as_dict(), "T": obj.T_info.as_dict()}
+        obj = eos.Grid2D(w.rho, w.T, w.P, loglog=a.loglog)
+        info = {"rho": obj.rho_info.as_dict(), "T": obj.T_info.as_dict(),
+                "grid": "loglog" if a.loglog else "linear", "derivatives": a.derivatives}
+        dPr = torch.empty(count, dtype=torch.float64, device=dev) if a.derivatives else None
+        dPt = torch.empty(count, dtype=torch.float64, device=dev) if a.derivatives else None
+        if a.derivatives:
+            bytes_per = 48
 
         def step(sp=None):
-            eos.eos_interp2d(obj.handle, rho.data_ptr(), T.data_ptr(), count, P.data_ptr(),
-                             iR.data_ptr(), iT.data_ptr(), sp or stream.cuda_stream)
+            eos.eos_interp2d_ex(obj.handle, rho.data_ptr(), T.data_ptr(), count, P.data_ptr(),
+                                iR.data_ptr(), iT.data_ptr(),
+                                dPr.data_ptr() if dPr is not None else None,
+                                dPt.data_ptr() if dPt is not None else None,
+                                sp or stream.cuda_stream)
     else:
         Y = torch.empty(count, dtype=torch.float64, device=dev)
         w.targets.device_fill(Y, offset, table_dev=torch.from_numpy(w.table).to(dev))

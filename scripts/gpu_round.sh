@@ -47,6 +47,12 @@ if has pdlab; then
     done
   done
 fi
+if has bench4; then
+  for flags in "" "--loglog" "--derivatives" "--loglog --derivatives"; do
+    timeout 600 python bench.py --workload cfg4 $flags --steps 100 --warmup 5 --no-cpu --no-e2e > $OUT/b4.json 2>/dev/null
+    python -c "import json;d=json.load(open('$OUT/b4.json'));print('cfg4 [$flags]', d['value'], d['unit'], d['roofline']['frac'], d['ms_per_step'])"
+  done
+fi
 if has benchall; then
   for wl in cfg1 cfg3 cfg4 cfg5 paper; do
     timeout 900 python bench.py --workload $wl --steps 100 --warmup 5 --no-cpu > $OUT/bench_$wl.json 2> $OUT/bench_$wl.err; echo "bench $wl rc=$?"
