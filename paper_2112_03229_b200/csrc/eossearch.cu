@@ -48,6 +48,7 @@ struct eos_grid2d_s {
   const void* fn = nullptr;
   const void* fn_deriv = nullptr;
   int grid = 0, grid_deriv = 0;
+  int threads_deriv = dv::Shape2DDeriv::kThreads, unroll_deriv = dv::Shape2DDeriv::kUnroll;
   int threads = 512, unroll = 2;
   bool clc = true;
   int32_t flags = 0;
@@ -154,18 +155,18 @@ const void* interp_fn_s(int variant) {
 
 template <int S>
 const void* interp_deriv_fn_s() {
-  return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, true>;
+  return (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true>;
 }
 
 template <int S>
 const void* interp_loglog_fn_s(bool deriv) {
-  return deriv ? (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, true, true>
+  return deriv ? (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, true>
                : (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, true>;
 }
 
 struct Interp2DShape {
   const void* fn;
-  const void* fn_deriv;  // same shape, with dP/drho and dP/dT outputs
+  const void* fn_deriv;  // with dP/drho and dP/dT outputs (Shape2DDeriv, static schedule)
   int threads, unroll;
   bool clc;
 };
@@ -345,14 +346,16 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
       (uintptr_t)rho | (uintptr_t)T | (uintptr_t)P | (uintptr_t)dPr | (uintptr_t)dPt;
   const uintptr_t al8 = (uintptr_t)iR | (uintptr_t)iT;
   a.vec_ok = ((al16 & 15) == 0) && ((al8 & 7) == 0);
-  const int64_t per_tile = (int64_t)g->threads * g->unroll * 2;
+  const int threads = deriv ? g->threads_deriv : g->threads;
+  const int64_t per_tile = (int64_t)threads * (deriv ? g->unroll_deriv : g->unroll) * 2;
   const int64_t tiles = (count + per_tile - 1) / per_tile;
   if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;
   a.ntiles = tiles;
-  int64_t grid = g->clc ? tiles : std::min<int64_t>(deriv ? g->grid_deriv : g->grid, tiles);
+  const bool clc = deriv ? dv::Shape2DDeriv::kClc : g->clc;
+  int64_t grid = clc ? tiles : std::min<int64_t>(deriv ? g->grid_deriv : g->grid, tiles);
   grid = std::max<int64_t>(grid, 1);
   void* params[] = {&a};
-  EOS_CUDA(launch(deriv ? g->fn_deriv : g->fn, grid, g->threads, (size_t)g->image_bytes, st,
+  EOS_CUDA(launch(deriv ? g->fn_deriv : g->fn, grid, threads, (size_t)g->image_bytes, st,
                   params));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return EOS_OK;
@@ -702,7 +705,8 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   g->clc = sh.clc;
   st = configure(g->fn, g->threads, g->image_bytes, g->num_sms, &g->grid, nullptr);
   if (st == EOS_OK)
-    st = configure(g->fn_deriv, g->threads, g->image_bytes, g->num_sms, &g->grid_deriv, nullptr);
+    st = configure(g->fn_deriv, g->threads_deriv, g->image_bytes, g->num_sms, &g->grid_deriv,
+                   nullptr);
   if (st != EOS_OK) { cudaFree(g->image_dev); delete g; return st; }
   *out = g;
   return EOS_OK;

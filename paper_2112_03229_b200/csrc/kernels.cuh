@@ -650,6 +650,7 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
 // 2-D body is smem/latency-bound, where the CLC loop's per-tile CTA barrier
 // costs more than the static tail (profiles/r01_exp_interp.json).
 using Shape2D = Shape<1024, 1, 1, false>;
+using Shape2DDeriv = Shape<512, 1, 1, false>;  // derivative outputs need > 64 registers
 
 template <int S, class SH, bool RECIP, bool DERIV, bool LOGLOG = false>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {
