@@ -41,9 +41,12 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "paper"])
+    ap.add_argument("--workload", default="cfg2",
+                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "paper", "big"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--k", type=int, default=None, help="override the directory k (default: auto)")
+    ap.add_argument("--levels", type=int, default=-1,
+                    help="tiered table depth D (default: auto; `big` needs D >= 3)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -189,7 +192,7 @@ def run_ours(a, d: Dist):
         Y = torch.empty(count, dtype=torch.float64, device=dev)
         w.targets.device_fill(Y, offset, table_dev=torch.from_numpy(w.table).to(dev))
         out = torch.empty(count, dtype=torch.int32, device=dev)
-        obj = eos.Table(w.table, k=a.k)
+        obj = eos.Table(w.table, k=a.k, levels=a.levels)
         info = obj.info.as_dict()
 
         def step(sp=None):
@@ -307,6 +310,18 @@ def run_ours(a, d: Dist):
         "clocks": clk.summary(),
         "e2e": e2e,
     }
+    if not is2d and obj.info.levels > 0:
+        # tiered table: each level reads one 32-B sector from L2; the
+        # L2 (LTS) throughput, not HBM, bounds it.  LTS cap ~6300 B/clk is the guide's
+        # B300 measurement (B300_MICROARCH.md "LTS throughput cap"), scaled by the SM clock.
+        lts_b = 12 + 32 * obj.info.levels
+        mhz = res["clocks"].get("sm_mhz") or 1965.0
+        lts_ach = lts_b * count / (kern_ms * 1e-3) / 1e9
+        lts_cap = 6300.0 * mhz * 1e6 / 1e9
+        res["roofline"]["l2"] = {"bound": "lts", "bytes_per_unit": lts_b, "achieved": round(lts_ach, 1),
+                                 "peak_est": round(lts_cap, 1), "unit": "GB/s",
+                                 "frac": round(lts_ach / lts_cap, 4),
+                                 "peak_source": "6300 B/clk (B300_MICROARCH.md) x median SM clock"}
     if counters is not None:
         res["validation"] = {"counters_u64": counters}
     if d.world == 1 and d.rank == 0 and not a.no_cpu:

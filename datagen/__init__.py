@@ -169,6 +169,14 @@ def table_paper_exemplar() -> np.ndarray:
     return np.logspace(math.log10(3e-6), math.log10(5.4e4), 110)
 
 
+def table_big(seed: int = 6, n: int = 1 << 20) -> np.ndarray:
+    """A table far larger than shared memory (SURVEY §8(f) f4 "tables larger than smem"):
+    n = 2^20 sorted values 10^u, u ~ U[-6, 10] (the cfg5 span, log-distributed like the
+    paper's tables).  Not a BASELINE.json config; the f4 measurement workload."""
+    rng = np.random.default_rng(seed)
+    return np.sort(10.0 ** rng.uniform(-6.0, 10.0, n))
+
+
 # --------------------------------------------------------------------------
 # Target streams
 # --------------------------------------------------------------------------
@@ -312,7 +320,12 @@ def workload(name: str, count: int | None = None) -> Workload:
         return Workload(name, count or 5_000_000, X,
                         TargetSpec("loguniform", 5, a=-10.0, w=20.0),
                         note="paper-shaped: n=110 over [3e-6,5.4e4], 5e6 log-uniform over 1e-10..1e10")
+    if name == "big":
+        X = table_big(6)
+        return Workload(name, count or (1 << 27), X, loguniform_over(X, 6),
+                        note="n=2^20 table (tiered: smem sample + L2-resident 4-ary levels), "
+                             "2^27 log-uniform targets")
     raise KeyError(name)
 
 
-WORKLOADS = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "paper")
+WORKLOADS = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "paper", "big")

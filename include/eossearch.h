@@ -40,6 +40,8 @@ extern "C" {
 #endif
 
 #define EOS_MAX_TABLE 16384 /* table entries staged in shared memory (fp64) */
+#define EOS_MAX_TABLE_TIERED (1 << 30) /* entries of a tiered table (eos_search_create_levels) */
+#define EOS_LEVELS_AUTO (-1)           /* eos_search_create_levels: choose D */
 #define EOS_MAX_K 19        /* mantissa bits appended to the exponent hash */
 #define EOS_K_AUTO (-1)     /* let eos_search_create_ex choose the hash */
 
@@ -79,6 +81,13 @@ typedef struct {
   int32_t ctas_per_sm; /* resident CTAs per SM of the search kernel (0 for plan) */
   int32_t hash_kind;   /* EOS_HASH_EXPONENT or EOS_HASH_LOG */
   uint32_t hash_mult;  /* M of the bin function below */
+  /* tiered tables (eos_search_create_levels); levels == 0: the fields above
+   * describe the whole table.  levels = D >= 1: the fields above (except n)
+   * describe the shared-memory sample table T1 of top_n entries. */
+  int32_t levels;      /* D: 4-ary levels in global memory */
+  int32_t pad_;
+  int64_t top_n;       /* n1 = ceil(n / 4^D) */
+  int64_t level_bytes; /* device bytes of the levels (0 when D == 0) */
 } eos_table_info_t;
 
 /* ---------------------------------------------------------------------------
@@ -89,7 +98,8 @@ typedef struct {
  * a device.  Used by the host-logic tests and for inspection.
  *   table_host : fp64[n], finite, non-decreasing (duplicates allowed, P:54-56
  *                "monotonically increasing"; -0.0 is canonicalised to +0.0)
- *   n          : 1 <= n <= EOS_MAX_TABLE
+ *   n          : 1 <= n <= EOS_MAX_TABLE (single-level tables; tiered ones:
+ *                eos_plan_table_levels)
  *   k          : EOS_K_AUTO (any hash, see eos_plan_table_hash) or 0..EOS_MAX_K
  *                (exponent hash).  The bin of a value v is
  *                  b(v) = min( (max(key(v), hb) - hb) * M >> 32, B-1 ),
@@ -135,7 +145,9 @@ EOS_API eos_status eos_plan_table_hash(const double* table_host, int64_t n, int3
 /* Setup once per table ("the search setup [is] performed only once"):
  * validates, builds the directory (k chosen by the cost model, EOS_K_AUTO)
  * and uploads the device image to the CURRENT CUDA device.  The table is
- * copied; the caller may free table_host on return. */
+ * copied; the caller may free table_host on return.  1 <= n <=
+ * EOS_MAX_TABLE_TIERED: tables above EOS_MAX_TABLE are tiered
+ * (eos_search_create_levels with EOS_LEVELS_AUTO). */
 EOS_API eos_status eos_search_create(const double* table_host, int64_t n, eos_table* out);
 
 /* Same with an explicit k (EOS_K_AUTO or 0..EOS_MAX_K).  Results do not
@@ -145,6 +157,31 @@ EOS_API eos_status eos_search_create_ex(const double* table_host, int64_t n, int
 /* Same with an explicit hash (kind/param as in eos_plan_table_hash). */
 EOS_API eos_status eos_search_create_hash(const double* table_host, int64_t n, int32_t kind, int64_t param,
                                   eos_table* out);
+
+/* Tables of any size ("tables larger than smem"), 1 <= n <=
+ * EOS_MAX_TABLE_TIERED.  Same result for every n; eos_search_create*
+ * call this with levels = EOS_LEVELS_AUTO, so they accept the same n.
+ *   levels = D: 0 = the whole table (and directory) in shared memory
+ *     (n <= EOS_MAX_TABLE); D >= 1 (<= 8) = a two-level structure: the
+ *     sample table T1[j] = X[j 4^D], j < n1 = ceil(n/4^D) <= EOS_MAX_TABLE,
+ *     with its hash directory in shared memory, and D 4-ary levels
+ *     Lv_d[j] = X[j 4^d] (d = D-1..0, NaN-padded to n1 4^(D-d) entries,
+ *     ~1.33 x 8n bytes) in device memory, where each level step reads one
+ *     32-byte sector: c = #{t < 4 : Lv_d[4b+t] <= y}, b = 4b + c - 1.
+ *     EOS_LEVELS_AUTO: D = 0 if n <= EOS_MAX_TABLE, else the smallest D with
+ *     n1 <= EOS_MAX_TABLE (one L2 sector per level is the cost).
+ *   kind/param: the hash of the shared-memory table (T1 when D >= 1), as in
+ *     eos_search_create_hash.
+ * Errors: EOS_ERR_SIZE (n out of range, or n1 > EOS_MAX_TABLE for the given
+ * D), EOS_ERR_UNSUPPORTED (D > 8), EOS_ERR_NOMEM, plus the table errors of
+ * eos_plan_table. */
+EOS_API eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t levels,
+                                            int32_t kind, int64_t param, eos_table* out);
+
+/* Host-only planning of eos_search_create_levels (no device): fills info
+ * (levels, top_n, level_bytes and the plan of the shared-memory table). */
+EOS_API eos_status eos_plan_table_levels(const double* table_host, int64_t n, int32_t levels,
+                                         int32_t kind, int64_t param, eos_table_info_t* info);
 
 /* idx_out_dev[i] = lower bound of targets_dev[i], i in [0, count).
  *   targets_dev : fp64[count] device, read once (streaming)
@@ -256,7 +293,7 @@ EOS_API eos_status eos_grid2d_destroy(eos_grid2d g);
  * Misc
  * ------------------------------------------------------------------------- */
 EOS_API const char* eos_status_str(eos_status s); /* static string, never NULL */
-EOS_API int32_t eos_abi_version(void);            /* 1 */
+EOS_API int32_t eos_abi_version(void);            /* 2 */
 /* Kernel launches issued by this library since load (all entry points). */
 EOS_API int64_t eos_launch_count(void);
 

@@ -30,10 +30,13 @@ __all__ = [
     "EOS_MAX_TABLE", "EOS_MAX_K", "EXPORTED_SYMBOLS", "EOS_HASH_AUTO", "EOS_HASH_EXPONENT",
     "EOS_HASH_LOG", "eos_plan_table_hash", "eos_search_create_hash", "eos_interp2d_ex",
     "eos_search_direct", "search_direct", "eos_grid2d_create_ex", "EOS_GRID_LINEAR",
-    "EOS_GRID_LOGLOG",
+    "EOS_GRID_LOGLOG", "EOS_MAX_TABLE_TIERED", "EOS_LEVELS_AUTO", "eos_search_create_levels",
+    "eos_plan_table_levels", "plan_table_levels",
 ]
 
 EOS_MAX_TABLE = 16384
+EOS_MAX_TABLE_TIERED = 1 << 30
+EOS_LEVELS_AUTO = -1
 EOS_MAX_K = 19
 EOS_K_AUTO = -1
 EOS_HASH_AUTO, EOS_HASH_EXPONENT, EOS_HASH_LOG = 0, 1, 2
@@ -52,6 +55,7 @@ EXPORTED_SYMBOLS = (
     "eos_interp2d", "eos_interp2d_host", "eos_grid2d_info", "eos_grid2d_destroy",
     "eos_status_str", "eos_abi_version", "eos_launch_count", "eos_plan_table_hash",
     "eos_search_create_hash", "eos_interp2d_ex", "eos_search_direct", "eos_grid2d_create_ex",
+    "eos_search_create_levels", "eos_plan_table_levels",
 )
 
 
@@ -67,7 +71,9 @@ class TableInfo(ctypes.Structure):
                 ("bins", ctypes.c_int32), ("max_occ", ctypes.c_int32), ("steps", ctypes.c_int32),
                 ("base", ctypes.c_int32), ("image_bytes", ctypes.c_int64),
                 ("device", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
-                ("hash_kind", ctypes.c_int32), ("hash_mult", ctypes.c_uint32)]
+                ("hash_kind", ctypes.c_int32), ("hash_mult", ctypes.c_uint32),
+                ("levels", ctypes.c_int32), ("pad_", ctypes.c_int32), ("top_n", ctypes.c_int64),
+                ("level_bytes", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -95,6 +101,8 @@ def load_library():
         "eos_plan_table": [_P, _I64, _I32, _P, _P, _I64],
         "eos_plan_table_hash": [_P, _I64, _I32, _I64, _P, _P, _I64],
         "eos_search_create_hash": [_P, _I64, _I32, _I64, _P],
+        "eos_search_create_levels": [_P, _I64, _I32, _I32, _I64, _P],
+        "eos_plan_table_levels": [_P, _I64, _I32, _I32, _I64, _P],
         "eos_search_create": [_P, _I64, _P],
         "eos_search_create_ex": [_P, _I64, _I32, _P],
         "eos_search": [_P, _P, _I64, _P, _P],
@@ -200,6 +208,20 @@ def eos_plan_table(table, k: int | None = EOS_K_AUTO, with_directory: bool = Tru
 plan_table = eos_plan_table
 
 
+def eos_plan_table_levels(table, levels: int = EOS_LEVELS_AUTO, k: int | None = EOS_K_AUTO,
+                          log_bins: int | None = None) -> TableInfo:
+    """Host-only plan of a (possibly tiered) table: levels = D (-1 = automatic)."""
+    X = _f64_host(table)
+    info = TableInfo()
+    kind, param = _hash_args(k, log_bins)
+    _check(load_library().eos_plan_table_levels(X.ctypes.data, X.size, levels, kind, param,
+                                                ctypes.byref(info)), "eos_plan_table_levels")
+    return info
+
+
+plan_table_levels = eos_plan_table_levels
+
+
 def eos_search_create(table) -> int:
     return eos_search_create_ex(table, EOS_K_AUTO)
 
@@ -218,6 +240,15 @@ def eos_search_create_hash(table, kind: int, param: int) -> int:
     h = ctypes.c_void_p()
     _check(L.eos_search_create_hash(X.ctypes.data, X.size, kind, param, ctypes.byref(h)),
            "eos_search_create")
+    return h.value
+
+
+def eos_search_create_levels(table, levels: int, kind: int, param: int) -> int:
+    L = load_library()
+    X = _f64_host(table)
+    h = ctypes.c_void_p()
+    _check(L.eos_search_create_levels(X.ctypes.data, X.size, levels, kind, param, ctypes.byref(h)),
+           "eos_search_create_levels")
     return h.value
 
 
@@ -311,11 +342,14 @@ def eos_grid2d_destroy(handle) -> None:
 class Table:
     """A search table bound to the current CUDA device (eos_search_create)."""
 
-    def __init__(self, table, k: int | None = None, log_bins: int | None = None):
+    def __init__(self, table, k: int | None = None, log_bins: int | None = None,
+                 levels: int = EOS_LEVELS_AUTO):
         """k: exponent hash with k mantissa bits; log_bins: logarithm hash with |H| bins;
-        neither: the automatic choice.  Results never depend on it."""
-        self.X = _f64_host(table).copy()
-        self._h = eos_search_create_hash(self.X, *_hash_args(k, log_bins))
+        neither: the automatic choice.  levels: D 4-ary global levels
+        under a shared-memory sample table (tables above EOS_MAX_TABLE entries need
+        D >= 1; -1 = automatic).  Results never depend on any of them."""
+        self.X = _f64_host(table)
+        self._h = eos_search_create_levels(self.X, levels, *_hash_args(k, log_bins))
         self.info = eos_table_info(self._h)
 
     @property

@@ -64,9 +64,32 @@ constexpr int64_t kMaxImage = 200 * 1024;  // explicit requests beyond this do n
 eos_status plan_table(const double* X, int64_t n, int kind, int64_t param, bool strict,
                       TablePlan* out);
 
+// Tables larger than shared memory (eossearch.h
+// eos_search_create_levels).  D 4-ary levels in global memory under a
+// shared-memory sample table T1[j] = X[j 4^D], j < n1 = ceil(n / 4^D).
+// Level d (stride 4^d, d = 0..D-1) has n1 4^(D-d) entries Lv_d[j] = X[j 4^d]
+// for j 4^d < n, NaN after (NaN <= y is false for every y, so padding is
+// never counted).  `lv` stores the levels coarsest first: D-1, D-2, .., 0,
+// so level d starts at element n1 (4^(D-d) - 4) / 3 and level 0 is X itself.
+constexpr int kMaxLevels = 8;  // n <= EOS_MAX_TABLE 4^8 = 2^30
+struct TieredPlan {
+  int levels = 0;             // D (0: single-level smem table, `top` is the table)
+  int64_t n = 0;              // entries of the full table
+  int64_t top_n = 0;          // n1
+  double x_last = 0.0;        // X[n-1]
+  TablePlan top;              // T1 and its directory (the smem image)
+  std::vector<double> lv;     // the levels (empty when levels == 0)
+};
+
+// levels: EOS_LEVELS_AUTO (0 if n <= EOS_MAX_TABLE, else the smallest D with
+// n1 <= EOS_MAX_TABLE) or 0..kMaxLevels.  kind/param: the hash of T1.
+eos_status plan_tiered(const double* X, int64_t n, int levels, int kind, int64_t param,
+                       TieredPlan* out);
+
 // Serialise X | dir into a 16-B padded byte image.
 std::vector<uint8_t> make_image(const TablePlan& p);
 
 void fill_info(const TablePlan& p, eos_table_info_t* info);
+void fill_info(const TieredPlan& t, eos_table_info_t* info);
 
 }  // namespace eos

@@ -23,7 +23,12 @@ namespace dv = eos::dev;
 static std::atomic<int64_t> g_launches{0};
 
 struct eos_table_s {
-  TablePlan plan;
+  TablePlan plan;          // the shared-memory table (T1 of a tiered table)
+  int levels = 0;          // D (tiered tables, eos_search_create_levels)
+  int64_t n = 0;           // entries of the full table
+  int64_t top_n = 0;       // n1
+  int64_t level_bytes = 0;
+  double* levels_dev = nullptr;  // the 4-ary levels, coarsest first
   int device = -1;
   int num_sms = 0;
   void* image_dev = nullptr;
@@ -84,6 +89,41 @@ const void* search_fn_shape(int mode, int steps, bool cnt) {
   return mode == 0 ? search_fn_mode<0, SH>(steps, cnt) : search_fn_mode<1, SH>(steps, cnt);
 }
 
+// tiered tables (levels >= 1): search1d_tiered_kernel
+template <int S, int MODE, class SH>
+const void* tiered_fn(bool cnt) {
+  return cnt ? (const void*)dv::search1d_tiered_kernel<S, MODE, true, dv::ShapeCnt>
+             : (const void*)dv::search1d_tiered_kernel<S, MODE, false, SH>;
+}
+
+template <int MODE, class SH>
+const void* tiered_fn_mode(int steps, bool cnt) {
+  switch (steps) {
+    case 1: return tiered_fn<1, MODE, SH>(cnt);
+    case 2: return tiered_fn<2, MODE, SH>(cnt);
+    case 3: return tiered_fn<3, MODE, SH>(cnt);
+    case 4: return tiered_fn<4, MODE, SH>(cnt);
+    case 5: return tiered_fn<5, MODE, SH>(cnt);
+    case 6: return tiered_fn<6, MODE, SH>(cnt);
+    case 7: return tiered_fn<7, MODE, SH>(cnt);
+    case 8: return tiered_fn<8, MODE, SH>(cnt);
+    default: return tiered_fn<0, MODE, SH>(cnt);
+  }
+}
+
+// Launch-shape variants of the tiered kernel (EOS_TIERED_VARIANT=<name>,
+// tuning experiments; mode 0, no counters, S <= 4).
+template <class SH, bool NA = true>
+const void* tiered_variant_fn(int steps) {
+  switch (steps) {
+    case 1: return (const void*)dv::search1d_tiered_kernel<1, 0, false, SH, NA>;
+    case 2: return (const void*)dv::search1d_tiered_kernel<2, 0, false, SH, NA>;
+    case 3: return (const void*)dv::search1d_tiered_kernel<3, 0, false, SH, NA>;
+    case 4: return (const void*)dv::search1d_tiered_kernel<4, 0, false, SH, NA>;
+    default: return nullptr;
+  }
+}
+
 struct LaunchShape {
   const void* fn;
   int threads, unroll;
@@ -126,6 +166,16 @@ const void* variant_fn(int steps) {
     default: return nullptr;
   }
 }
+
+const Variant kTieredVariants[] = {
+    {"static512u4", 512, 4, false, tiered_variant_fn<dv::Shape<512, 4, 1, false>>},
+    {"clc512u4", 512, 4, true, tiered_variant_fn<dv::Shape<512, 4, 1, true>>},
+    {"static1024u2", 1024, 2, false, tiered_variant_fn<dv::Shape<1024, 2, 1, false>>},
+    {"clc1024u2", 1024, 2, true, tiered_variant_fn<dv::Shape<1024, 2, 1, true>>},
+    {"static256u8", 256, 8, false, tiered_variant_fn<dv::Shape<256, 8, 1, false>>},
+    {"static512u4l1", 512, 4, false, tiered_variant_fn<dv::Shape<512, 4, 1, false>, false>},
+    {"static1024u2l1", 1024, 2, false, tiered_variant_fn<dv::Shape<1024, 2, 1, false>, false>},
+};
 
 const Variant kVariants[] = {
     {"static256u4", 256, 4, false, variant_fn<dv::Shape<256, 4, 4, false>>},
@@ -302,6 +352,9 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
   a.count = count;
   a.gofs = gofs;
   a.counters = (unsigned long long*)counters;
+  a.lv = t->levels_dev;
+  a.lv_top_len = 4 * t->top_n;
+  a.levels = t->levels;
   // Vector body needs Y+head 16-B aligned and out+head 8-B aligned.
   const uintptr_t ya = (uintptr_t)Y, oa = (uintptr_t)out;
   a.head = (ya & 15) ? 1 : 0;
@@ -434,7 +487,7 @@ const char* eos_status_str(eos_status s) {
   return "unknown status";
 }
 
-int32_t eos_abi_version(void) { return 1; }
+int32_t eos_abi_version(void) { return 2; }
 
 int64_t eos_launch_count(void) { return g_launches.load(); }
 
@@ -467,27 +520,81 @@ eos_status eos_search_create_ex(const double* table_host, int64_t n, int32_t k, 
 
 eos_status eos_search_create_hash(const double* table_host, int64_t n, int32_t kind, int64_t param,
                                   eos_table* out) {
+  return eos_search_create_levels(table_host, n, EOS_LEVELS_AUTO, kind, param, out);
+}
+
+eos_status eos_plan_table_levels(const double* table_host, int64_t n, int32_t levels, int32_t kind,
+                                 int64_t param, eos_table_info_t* info) {
+  if (!info) return EOS_ERR_NULL;
+  eos::TieredPlan tp;
+  eos_status st = eos::plan_tiered(table_host, n, levels, kind, param, &tp);
+  if (st != EOS_OK) return st;
+  eos::fill_info(tp, info);
+  return EOS_OK;
+}
+
+eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t levels,
+                                    int32_t kind, int64_t param, eos_table* out) {
   if (!out) return EOS_ERR_NULL;
   *out = nullptr;
   eos_table t = new (std::nothrow) eos_table_s();
   if (!t) return EOS_ERR_NOMEM;
-  eos_status st = eos::plan_table(table_host, n, kind, param, false, &t->plan);
-  if (st != EOS_OK) { delete t; return st; }
+  std::vector<double> lv;
+  {
+    eos::TieredPlan tp;
+    eos_status st = eos::plan_tiered(table_host, n, levels, kind, param, &tp);
+    if (st != EOS_OK) { delete t; return st; }
+    t->plan = std::move(tp.top);
+    t->levels = tp.levels;
+    t->n = tp.n;
+    t->top_n = tp.top_n;
+    t->level_bytes = 8 * (int64_t)tp.lv.size();
+    lv = std::move(tp.lv);
+    t->ax = axis_params(t->plan, 0);
+    t->ax.xlast = tp.x_last;  // X[n-1] of the full table (counter c4)
+  }
+  auto fail = [&](eos_status st) {
+    if (t->image_dev) cudaFree(t->image_dev);
+    if (t->levels_dev) cudaFree(t->levels_dev);
+    delete t;
+    return st;
+  };
   cudaError_t e = cudaGetDevice(&t->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, t->device);
-  if (e != cudaSuccess) { delete t; return cuda_status(e); }
-  st = upload(eos::make_image(t->plan), &t->image_dev);
-  if (st != EOS_OK) { delete t; return st; }
-  t->ax = axis_params(t->plan, 0);
+  if (e != cudaSuccess) return fail(cuda_status(e));
+  eos_status st = upload(eos::make_image(t->plan), &t->image_dev);
+  if (st != EOS_OK) return fail(st);
+  if (t->levels > 0) {
+    e = cudaMalloc((void**)&t->levels_dev, (size_t)t->level_bytes);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(t->levels_dev, lv.data(), (size_t)t->level_bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(cuda_status(e));
+    std::vector<double>().swap(lv);
+  }
   for (int c = 0; c < 2 && st == EOS_OK; ++c) {
-    LaunchShape ls = pick_search(t->plan.key_mode, t->plan.steps, c == 1, t->plan.image_bytes);
-    t->fn[c] = ls.fn;
-    t->threads[c] = ls.threads;
-    t->unroll[c] = ls.unroll;
-    t->clc[c] = ls.clc;
-    if (c == 0) {
-      const char* want = getenv("EOS_SEARCH_VARIANT");
-      for (const Variant& v : kVariants) {
+    const bool cnt = c == 1;
+    if (t->levels > 0) {
+      t->fn[c] = t->plan.key_mode == 0 ? tiered_fn_mode<0, dv::ShapeTiered>(t->plan.steps, cnt)
+                                       : tiered_fn_mode<1, dv::ShapeTiered>(t->plan.steps, cnt);
+      using SH = dv::ShapeTiered;
+      t->threads[c] = cnt ? dv::ShapeCnt::kThreads : SH::kThreads;
+      t->unroll[c] = cnt ? dv::ShapeCnt::kUnroll : SH::kUnroll;
+      t->clc[c] = cnt ? dv::ShapeCnt::kClc : SH::kClc;
+    } else {
+      LaunchShape ls = pick_search(t->plan.key_mode, t->plan.steps, cnt, t->plan.image_bytes);
+      t->fn[c] = ls.fn;
+      t->threads[c] = ls.threads;
+      t->unroll[c] = ls.unroll;
+      t->clc[c] = ls.clc;
+    }
+    if (c == 0) {  // tuning experiments: launch-shape variants by name
+      const bool tiered = t->levels > 0;
+      const char* want = getenv(tiered ? "EOS_TIERED_VARIANT" : "EOS_SEARCH_VARIANT");
+      const Variant* vs = tiered ? kTieredVariants : kVariants;
+      const size_t nv = tiered ? sizeof(kTieredVariants) / sizeof(Variant)
+                               : sizeof(kVariants) / sizeof(Variant);
+      for (size_t i = 0; i < nv; ++i) {
+        const Variant& v = vs[i];
         if (!want || strcmp(want, v.name) != 0 || t->plan.key_mode != 0) continue;
         const void* f = v.get(t->plan.steps);
         if (!f) break;
@@ -500,7 +607,7 @@ eos_status eos_search_create_hash(const double* table_host, int64_t n, int32_t k
     st = configure(t->fn[c], t->threads[c], t->plan.image_bytes, t->num_sms, &t->grid[c],
                    c == 0 ? &t->ctas_per_sm : nullptr);
   }
-  if (st != EOS_OK) { cudaFree(t->image_dev); delete t; return st; }
+  if (st != EOS_OK) return fail(st);
   *out = t;
   return EOS_OK;
 }
@@ -604,6 +711,10 @@ eos_status eos_search_direct(const double* table_dev, int64_t n, const double* t
 eos_status eos_table_info(eos_table t, eos_table_info_t* out) {
   if (!t || !out) return EOS_ERR_NULL;
   eos::fill_info(t->plan, out);
+  out->n = t->n;
+  out->levels = t->levels;
+  out->top_n = t->top_n;
+  out->level_bytes = t->level_bytes;
   out->device = t->device;
   out->ctas_per_sm = t->ctas_per_sm;
   return EOS_OK;
@@ -615,6 +726,10 @@ eos_status eos_search_destroy(eos_table t) {
   cudaGetDevice(&cur);
   if (cur != t->device) cudaSetDevice(t->device);
   cudaError_t e = cudaFree(t->image_dev);  // synchronises with in-flight work
+  if (t->levels_dev) {
+    cudaError_t e2 = cudaFree(t->levels_dev);
+    if (e == cudaSuccess) e = e2;
+  }
   if (cur != t->device && cur >= 0) cudaSetDevice(cur);
   delete t;
   return cuda_status(e);

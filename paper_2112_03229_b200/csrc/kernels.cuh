@@ -70,6 +70,13 @@ struct SearchArgs {
   int64_t count;
   int64_t gofs;                  // global offset (counters)
   unsigned long long* counters;  // u64[8] or null
+  // tiered tables (n > EOS_MAX_TABLE, search1d_tiered_kernel): the 4-ary
+  // global levels, coarsest first; level d (stride 4^d) holds n1 4^(D-d)
+  // entries X[j 4^d] (NaN past the end), level D-1 starts at lv.
+  const double* lv;
+  int64_t lv_top_len;            // 4 n1: length of level D-1
+  int32_t levels;                // D (0: single-level smem table)
+  int32_t pad2_;
 };
 
 // splitmix64 finalizer (the checksum of counter c2; independent of oracle/)
@@ -132,7 +139,7 @@ struct Counters {
 #pragma unroll
     for (int i = 0; i < 7; ++i) c[i] = 0;
   }
-  __device__ __forceinline__ void add(double y, int32_t idx, int64_t gpos, const double* sX,
+  __device__ __forceinline__ void add(double y, int32_t idx, int64_t gpos, double x_idx,
                                       const AxisParams& a) {
     c[0] += 1;
     c[1] += (uint64_t)(uint32_t)idx;
@@ -140,7 +147,7 @@ struct Counters {
     c[3] += !(y >= a.x0);
     c[4] += (y > a.xlast);
     c[5] += (y != y);
-    c[6] += (y == sX[idx]);
+    c[6] += (y == x_idx);
   }
   __device__ __forceinline__ void flush(unsigned long long* g) {
 #pragma unroll
@@ -153,6 +160,89 @@ struct Counters {
   }
 };
 
+// Lookup policies of the streaming tile loop (search_body).  `many` maps the
+// 2U targets of one thread's tile slice to their indices, `x_at(i)` = X[i]
+// (counter c6 only).
+//
+// SmemLookup: the whole table and its directory are in shared memory.
+template <int S, int MODE>
+struct SmemLookup {
+  const double* __restrict__ sX;
+  const uint32_t* __restrict__ sD;
+  AxisParams a;
+  template <int N>
+  __device__ __forceinline__ void many(const double (&y)[N], int32_t (&r)[N]) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = lookup<S, MODE>(y[i], sX, sD, a);
+  }
+  __device__ __forceinline__ double x_at(int32_t i) const { return sX[i]; }
+};
+
+// TieredLookup (tables larger than shared memory): the smem
+// table is the sample T1[j] = X[j 4^D] (n1 entries) with its directory; the
+// full table lives in global memory (L2-resident) as D 4-ary levels, level d
+// holding Lv_d[j] = X[j 4^d] (NaN past n).  Per target:
+//   b = max(#{T1 <= y} - 1, 0)                       (smem lookup, as above)
+//   for d = D-1 .. 0:  c = #{t < 4 : Lv_d[4b + t] <= y}   (one 32-B sector)
+//                      b = 4b + max(c - 1, 0)
+//   idx = (y >= X[0]) ? b : 0
+// Invariant: X[b 4^(d+1)] <= y < X[(b+1) 4^(d+1)] (or past the end), so
+// Lv_d[4b] <= y and c >= 1 for every y >= X[0]; NaN padding is never <= y.
+// At d = 0 the block has stride 1 and b = #{X <= y} - 1.  All targets
+// of a thread go through a level together (level-major) so their 2U sector
+// loads are in flight at once.
+// One 32-byte sector (4 fp64) with one 256-bit load (SASS LDG.E.ENL2.256):
+// one L1TEX wavefront per lane instead of two LDG.128 -- the gathers of a
+// warp hit 32 different lines, so wavefronts, not bytes, bound the L1 stage.
+// NA: L1::no_allocate (the levels are too large to live in L1).
+template <bool NA>
+__device__ __forceinline__ void ldg_sector(const double* p, double& a, double& b, double& c,
+                                           double& d) {
+  if (NA)
+    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+        : "l"(p));
+  else
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
+template <int S, int MODE, bool NA = true>
+struct TieredLookup {
+  const double* __restrict__ sX;  // T1 (smem)
+  const uint32_t* __restrict__ sD;
+  AxisParams a;                   // of T1, except xlast = X[n-1] (counter c4)
+  const double* __restrict__ lv;  // level D-1 (global)
+  int64_t top_len;                // 4 n1
+  int32_t levels;                 // D >= 1
+  const double* __restrict__ x_full;  // level 0 = X (counter c6)
+  template <int N>
+  __device__ __forceinline__ void many(const double (&y)[N], int32_t (&r)[N]) const {
+    int32_t b[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) b[i] = lookup<S, MODE>(y[i], sX, sD, a);
+    const double* L = lv;
+    int64_t len = top_len;
+    for (int d = levels - 1; d >= 0; --d) {
+      double q[N][4];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        EOS_DCHECK(b[i] >= 0 && 4 * (int64_t)b[i] + 3 < len);
+        ldg_sector<NA>(L + 4 * (int64_t)b[i], q[i][0], q[i][1], q[i][2], q[i][3]);
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int32_t c = (q[i][0] <= y[i]) + (q[i][1] <= y[i]) + (q[i][2] <= y[i]) +
+                          (q[i][3] <= y[i]);
+        b[i] = 4 * b[i] + max(c - 1, 0);
+      }
+      L += len;
+      len *= 4;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = (y[i] >= a.x0) ? b[i] : 0;
+  }
+  __device__ __forceinline__ double x_at(int32_t i) const { return __ldg(x_full + i); }
+};
 
 // ---- Blackwell cluster launch control + mbarrier (inline PTX, sm_100a) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -262,14 +352,17 @@ using ShapeBig = Shape<1024, 4, 1, true>;       // larger: 1 CTA x 1024 (one ima
 using ShapeDeepMid = Shape<512, 4, 2, false>;   // S >= 3, image <= 72 KB
 using ShapeDeepBig = Shape<1024, 4, 1, false>;  // S >= 3, larger
 using ShapeCnt = Shape<256, 4, 1, true>;        // validation launches (counters on)
+// Tiered tables: 1024 threads x 4 level-major lookup chains (56 registers),
+// static schedule.  Measured on `big` (n = 2^20, D = 3): 85 Glookups/s vs 77
+// for 512 x 8 chains, 72 for the CLC schedule (profiles/r01_exp_tiered.json).
+using ShapeTiered = Shape<1024, 2, 1, false>;
 
 // The streaming tile loop of search1d (after the image is in smem): CLC or
 // static tile schedule, 128-bit streaming loads, next-tile prefetch.
-template <int S, int MODE, bool CNT, class SH>
-__device__ __forceinline__ void search_body(const SearchArgs& args, const AxisParams& a,
-                                            const double* __restrict__ sX,
-                                            const uint32_t* __restrict__ sD, uint4* clc_resp_p,
+template <bool CNT, class SH, class LK>
+__device__ __forceinline__ void search_body(const SearchArgs& args, const LK& lk, uint4* clc_resp_p,
                                             uint64_t* clc_bar_p) {
+  const AxisParams& a = lk.a;
   constexpr int T = SH::kThreads;
   constexpr int U = SH::kUnroll;
   constexpr int TP = SH::kTilePairs;
@@ -291,10 +384,11 @@ __device__ __forceinline__ void search_body(const SearchArgs& args, const AxisPa
 
   // the leading unaligned element (if any) belongs to tile 0
   if (blockIdx.x == 0 && threadIdx.x == 0 && head) {
-    const double y = Y[0];
-    const int32_t r = lookup<S, MODE>(y, sX, sD, a);
-    out[0] = r;
-    if (CNT) cn.add(y, r, args.gofs, sX, a);
+    const double y[1] = {Y[0]};
+    int32_t r[1];
+    lk.many(y, r);
+    out[0] = r[0];
+    if (CNT) cn.add(y[0], r[0], args.gofs, lk.x_at(r[0]), a);
   }
 
   uint32_t phase = 0;
@@ -322,18 +416,23 @@ __device__ __forceinline__ void search_body(const SearchArgs& args, const AxisPa
     int64_t tn;
     if (full(t)) {
       const int64_t p0 = t * TP + threadIdx.x;
-      int2 r[U];
+      double y[2 * U];
+      int32_t ri[2 * U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        r[u].x = lookup<S, MODE>(v[u].x, sX, sD, a);
-        r[u].y = lookup<S, MODE>(v[u].y, sX, sD, a);
+        y[2 * u] = v[u].x;
+        y[2 * u + 1] = v[u].y;
       }
+      lk.many(y, ri);
+      int2 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) r[u] = make_int2(ri[2 * u], ri[2 * u + 1]);
       if (CNT) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int64_t g = args.gofs + head + 2 * (p0 + u * T);
-          cn.add(v[u].x, r[u].x, g, sX, a);
-          cn.add(v[u].y, r[u].y, g + 1, sX, a);
+          cn.add(v[u].x, r[u].x, g, lk.x_at(r[u].x), a);
+          cn.add(v[u].y, r[u].y, g + 1, lk.x_at(r[u].y), a);
         }
       }
       tn = next_tile(t);
@@ -349,10 +448,11 @@ __device__ __forceinline__ void search_body(const SearchArgs& args, const AxisPa
       const int64_t e1 = min(count, e0 + TE);
       EOS_DCHECK(e0 >= 0 && t >= 0);
       for (int64_t i = e0 + threadIdx.x; i < e1; i += T) {
-        const double y = Y[i];
-        const int32_t r = lookup<S, MODE>(y, sX, sD, a);
-        out[i] = r;
-        if (CNT) cn.add(y, r, args.gofs + i, sX, a);
+        const double y[1] = {Y[i]};
+        int32_t r[1];
+        lk.many(y, r);
+        out[i] = r[0];
+        if (CNT) cn.add(y[0], r[0], args.gofs + i, lk.x_at(r[0]), a);
       }
       tn = next_tile(t);
       if (tn < ntiles && full(tn)) {
@@ -376,11 +476,41 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
   const AxisParams a = args.ax;
   EOS_DCHECK(a.d_off + 4 * ((int64_t)a.bmax + 1) <= 16 * (int64_t)args.image_16 &&
              a.x_off + 8 * (int64_t)a.n <= a.d_off);
-  const double* __restrict__ sX =
-      reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
-  const uint32_t* __restrict__ sD =
-      reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(smem) + a.d_off);
-  search_body<S, MODE, CNT, SH>(args, a, sX, sD, &clc_resp, &clc_bar);
+  SmemLookup<S, MODE> lk;
+  lk.sX = reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
+  lk.sD = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(smem) + a.d_off);
+  lk.a = a;
+  search_body<CNT, SH>(args, lk, &clc_resp, &clc_bar);
+}
+
+// Tables larger than shared memory (TieredLookup): the smem image holds the
+// sample table T1 and its directory; the levels stay in global memory / L2.
+template <int S, int MODE, bool CNT, class SH, bool NA = true>
+__global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
+    search1d_tiered_kernel(const SearchArgs args) {
+  extern __shared__ __align__(16) uint4 smem[];
+  __shared__ __align__(16) uint4 clc_resp;
+  __shared__ __align__(8) uint64_t clc_bar, stage_bar;
+  if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
+  stage_image(smem, args.image, args.image_16, &stage_bar);
+  pdl_enter();
+  const AxisParams a = args.ax;
+  EOS_DCHECK(args.levels >= 1 && args.lv_top_len == 4 * (int64_t)a.n);
+  TieredLookup<S, MODE, NA> lk;
+  lk.sX = reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
+  lk.sD = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(smem) + a.d_off);
+  lk.a = a;
+  lk.lv = args.lv;
+  lk.top_len = args.lv_top_len;
+  lk.levels = args.levels;
+  // level 0 (= X) follows levels D-1 .. 1: offset n1 (4^D - 4) / 3
+  int64_t off = 0, len = args.lv_top_len;
+  for (int d = args.levels - 1; d > 0; --d) {
+    off += len;
+    len *= 4;
+  }
+  lk.x_full = args.lv + off;
+  search_body<CNT, SH>(args, lk, &clc_resp, &clc_bar);
 }
 
 // ------------------------------------------------ zero-setup search (f2) ----
@@ -505,10 +635,13 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
   int steps = 0;
   while ((1u << steps) < s_maxocc + 1) ++steps;
   a.steps = steps > 0 ? steps : 1;
-  if (a.mode)
-    search_body<0, 1, false, SH>(A.s, a, sX, sD, &clc_resp, &clc_bar);
-  else
-    search_body<0, 0, false, SH>(A.s, a, sX, sD, &clc_resp, &clc_bar);
+  if (a.mode) {
+    const SmemLookup<0, 1> lk{sX, sD, a};
+    search_body<false, SH>(A.s, lk, &clc_resp, &clc_bar);
+  } else {
+    const SmemLookup<0, 0> lk{sX, sD, a};
+    search_body<false, SH>(A.s, lk, &clc_resp, &clc_bar);
+  }
 }
 
 // ------------------------------------------------------------------ 2-D ----

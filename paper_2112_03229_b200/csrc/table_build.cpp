@@ -232,6 +232,65 @@ eos_status plan_table(const double* Xin, int64_t n, int kind, int64_t param, boo
   return EOS_OK;
 }
 
+eos_status plan_tiered(const double* Xin, int64_t n, int levels, int kind, int64_t param,
+                       TieredPlan* out) {
+  if (!Xin || !out) return EOS_ERR_NULL;
+  if (n < 1 || n > EOS_MAX_TABLE_TIERED) return EOS_ERR_SIZE;
+  if (levels == EOS_LEVELS_AUTO) {
+    levels = 0;
+    while ((n + (int64_t(1) << (2 * levels)) - 1) >> (2 * levels) > EOS_MAX_TABLE) ++levels;
+  }
+  if (levels < 0 || levels > kMaxLevels) return EOS_ERR_UNSUPPORTED;
+  const int64_t stride = int64_t(1) << (2 * levels);  // 4^D
+  const int64_t n1 = (n + stride - 1) / stride;
+  if (n1 > EOS_MAX_TABLE) return EOS_ERR_SIZE;
+  TieredPlan t;
+  t.levels = levels;
+  t.n = n;
+  t.top_n = n1;
+  if (levels == 0) {
+    eos_status st = plan_table(Xin, n, kind, param, false, &t.top);
+    if (st != EOS_OK) return st;
+    t.x_last = t.top.X[n - 1];
+    *out = std::move(t);
+    return EOS_OK;
+  }
+  // Level 0 = the validated, canonicalised table (same rules as plan_table).
+  const int64_t len0 = n1 * stride;
+  int64_t total = 0;
+  for (int d = 0; d < levels; ++d) total += len0 >> (2 * d);
+  try {
+    t.lv.assign((size_t)total, NAN);
+  } catch (...) {
+    return EOS_ERR_NOMEM;
+  }
+  const int64_t off0 = total - len0;
+  double* L0 = t.lv.data() + off0;
+  for (int64_t j = 0; j < n; ++j) {
+    const double v = Xin[j];
+    if (!isfinite(v)) return EOS_ERR_NONFINITE;
+    L0[j] = (v == 0.0) ? 0.0 : v;  // canonicalise -0.0 (R6)
+    if (j > 0 && L0[j] < L0[j - 1]) return EOS_ERR_UNSORTED;
+  }
+  // Coarser levels are strided samples of level 0 (NaN padding stays NaN).
+  int64_t off = off0, len = len0;
+  for (int d = 1; d < levels; ++d) {
+    const int64_t s = int64_t(1) << (2 * d);
+    len >>= 2;
+    off -= len;
+    double* Ld = t.lv.data() + off;
+    for (int64_t j = 0; j * s < n; ++j) Ld[j] = L0[j * s];
+  }
+  std::vector<double> T1((size_t)n1);
+  for (int64_t j = 0; j < n1; ++j) T1[j] = L0[j * stride];
+  eos_status st = plan_table(T1.data(), n1, kind, param, false, &t.top);
+  if (st != EOS_OK) return st;
+  // key mode of T1 is that of X (T1[0] = X[0])
+  t.x_last = L0[n - 1];
+  *out = std::move(t);
+  return EOS_OK;
+}
+
 std::vector<uint8_t> make_image(const TablePlan& p) {
   std::vector<uint8_t> img((size_t)p.image_bytes, 0);
   memcpy(img.data(), p.X.data(), (size_t)(8 * p.n));
@@ -252,6 +311,18 @@ void fill_info(const TablePlan& p, eos_table_info_t* info) {
   info->ctas_per_sm = 0;
   info->hash_kind = p.hash_kind;
   info->hash_mult = p.M;
+  info->levels = 0;
+  info->pad_ = 0;
+  info->top_n = p.n;
+  info->level_bytes = 0;
+}
+
+void fill_info(const TieredPlan& t, eos_table_info_t* info) {
+  fill_info(t.top, info);
+  info->n = t.n;
+  info->levels = t.levels;
+  info->top_n = t.top_n;
+  info->level_bytes = 8 * (int64_t)t.lv.size();
 }
 
 }  // namespace eos

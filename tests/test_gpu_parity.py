@@ -580,3 +580,147 @@ def test_loglog_host_pipeline():
     assert np.array_equal(iR, iRr) and np.array_equal(iT, iTr)
     check_interp(P, Pr)
     g.close()
+
+
+# ------------------------------------- tiered tables -----
+# Tables larger than shared memory: smem sample table T1 = X[::4^D] plus D
+# 4-ary levels in global memory (eossearch.h eos_search_create_levels).  The
+# answer is the same P:54 lower bound for every D; the oracle is unchanged.
+def tiered_search(X, Y, levels, k=None, log_bins=None, **kw):
+    t = eos.Table(X, k=k, log_bins=log_bins, levels=levels)
+    assert t.info.levels == (levels if levels >= 0 else t.info.levels)
+    out = t.search(to_dev(Y), **kw)
+    torch.cuda.synchronize()
+    r = out.cpu().numpy()
+    t.close()
+    return r
+
+
+@pytest.mark.parametrize("name", sorted(lower_bound_cases().keys()))
+def test_tiered_golden_every_depth(name):
+    X, cases = lower_bound_cases()[name]
+    ys = np.array([c[0] for c in cases] * 37)
+    exp = np.array([c[1] for c in cases] * 37, dtype=np.int32)
+    for D in (1, 2, 3, 5, 8):
+        assert_same(tiered_search(X, ys, D), exp, ys)
+
+
+def test_tiered_edge_tables_exhaustive_probes():
+    rng = np.random.default_rng(77)
+    checked = 0
+    for X in _edge_tables(rng, 140):
+        P = _probes(X)
+        P = np.concatenate([P, rng.permutation(np.repeat(P, 3))])
+        ref = oracle.search(X, P)
+        for D in (1, 2, 4):
+            assert_same(tiered_search(X, P, D), ref, P)
+            checked += P.size
+    assert checked > 50_000
+
+
+def _big_table(rng, n, kind):
+    if kind == "loguniform":
+        return np.sort(10.0 ** rng.uniform(-6, 10, n))
+    if kind == "dups":      # runs of equal entries straddling level blocks
+        return np.sort(np.repeat(10.0 ** rng.uniform(-3, 3, n // 7 + 1), 7)[:n])
+    if kind == "mixed":     # negatives (key mode 1), +-0 and subnormals
+        X = np.concatenate([rng.normal(0, 1e3, n - 4), [0.0, -0.0, 5e-324, -5e-324]])
+        return np.sort(X)
+    if kind == "zerohead":  # a 0.0 head, subnormals, then normals (mode 0)
+        X = np.concatenate([np.zeros(5), rng.uniform(0, 1e-308, n // 3),
+                            10.0 ** rng.uniform(-300, 300, n - 5 - n // 3)])
+        return np.sort(X)
+    raise KeyError(kind)
+
+
+def _big_probes(rng, X, m):
+    lo, hi = X[0], X[-1]
+    j = rng.integers(0, X.size, m // 4)
+    pos = X[X > 0]
+    a, b = (math.log10(pos[0]), math.log10(pos[-1])) if pos.size else (-300.0, 300.0)
+    Y = np.concatenate([
+        X[j], np.nextafter(X[j], np.inf), np.nextafter(X[j], -np.inf),
+        np.sign(rng.uniform(-1, 1, m // 8)) * 10.0 ** rng.uniform(a - 1, b + 1, m // 8),
+        rng.uniform(lo, hi, m // 8) if np.isfinite(hi - lo) else X[j[: m // 8]],
+        [np.nan, np.inf, -np.inf, 0.0, -0.0, lo, hi, 5e-324, -5e-324],
+    ])
+    return rng.permutation(Y)
+
+
+@pytest.mark.parametrize("n,kind", [(16385, "loguniform"), ((1 << 17) + 3, "dups"),
+                                    ((1 << 20), "loguniform"), (300_001, "mixed"),
+                                    (70_001, "zerohead"), ((1 << 22) + 12345, "loguniform")])
+def test_tiered_large_tables_full(n, kind):
+    rng = np.random.default_rng(n)
+    X = _big_table(rng, n, kind)
+    Y = _big_probes(rng, X, 1 << 20)
+    ref = oracle.search(X, Y)
+    t = eos.Table(X)
+    assert t.info.levels >= 1 and t.info.n == n
+    out = t.search(to_dev(Y))
+    torch.cuda.synchronize()
+    assert_same(out.cpu().numpy(), ref, Y)
+    # the same answers at a deeper structure and with another hash of T1
+    t2 = eos.Table(X, levels=t.info.levels + 1, log_bins=97)
+    out2 = t2.search(to_dev(Y))
+    torch.cuda.synchronize()
+    assert_same(out2.cpu().numpy(), ref, Y)
+    t.close()
+    t2.close()
+
+
+def test_tiered_big_workload_full_sampled_and_counters():
+    """The bench's `big` workload (n = 2^20, 2^27 targets) in the bench's launch
+    configuration: 2^20 sampled outputs vs the oracle, the bracketing invariant on
+    every output, and the counters of the whole stream vs the oracle's."""
+    w = datagen.workload("big")
+    t = eos.Table(w.table)
+    assert t.info.levels == 3
+    Yd = torch.empty(w.count, dtype=torch.float64, device=DEV)
+    w.targets.device_fill(Yd, 0)
+    out = t.search(Yd)
+    torch.cuda.synchronize()
+    _sampled_check(w, Yd, out)
+    invariant_on_device(to_dev(w.table), Yd, out)
+    c = torch.zeros(8, dtype=torch.int64, device=DEV)
+    out2 = t.search(Yd[: 1 << 24], counters=c)
+    torch.cuda.synchronize()
+    assert torch.equal(out2, out[: 1 << 24])
+    Yh = w.targets.host_fill(0, 1 << 24)
+    ref = oracle.counters(w.table, Yh, oracle.search(w.table, Yh), 0)
+    assert np.array_equal(c.cpu().numpy().view(np.uint64), ref)
+    t.close()
+
+
+@pytest.mark.parametrize("count", [1, 3, 2049, 65_537])
+@pytest.mark.parametrize("y_off,o_off", [(0, 0), (1, 1), (3, 2)])
+def test_tiered_ragged_and_misaligned(count, y_off, o_off):
+    rng = np.random.default_rng(count)
+    X = _big_table(rng, 50_000, "dups")
+    Yall = _big_probes(rng, X, count + 64)[: count + 8]
+    yd = to_dev(Yall)[y_off:y_off + count]
+    od_all = torch.full((count + 8,), -7, dtype=torch.int32, device=DEV)
+    od = od_all[o_off:o_off + count]
+    t = eos.Table(X)
+    t.search(yd, out=od)
+    torch.cuda.synchronize()
+    got = od_all.cpu().numpy()
+    assert_same(got[o_off:o_off + count], oracle.search(X, Yall[y_off:y_off + count]))
+    assert np.all(got[:o_off] == -7) and np.all(got[o_off + count:] == -7)
+    t.close()
+
+
+def test_tiered_host_pipeline_and_counters():
+    rng = np.random.default_rng(5)
+    X = _big_table(rng, 100_000, "loguniform")
+    Y = _big_probes(rng, X, 1 << 21)
+    ref = oracle.search(X, Y)
+    t = eos.Table(X)
+    got = t.search_host(np.ascontiguousarray(Y))
+    assert_same(got, ref, Y)
+    off = 123_456_789
+    c = torch.zeros(8, dtype=torch.int64, device=DEV)
+    t.search(to_dev(Y), counters=c, global_offset=off)
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy().view(np.uint64), oracle.counters(X, Y, ref, off))
+    t.close()

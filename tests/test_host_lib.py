@@ -36,7 +36,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert declared == set(eos.EXPORTED_SYMBOLS)
     for s in declared:
         assert hasattr(L, s), s
-    assert L.eos_abi_version() == 1
+    assert L.eos_abi_version() == 2
     assert eos.eos_status_str(0) == "ok"
     assert "sorted" in eos.eos_status_str(4)
 
@@ -292,3 +292,54 @@ def test_auto_choice_never_worse_in_steps_than_any_exponent_k():
             continue
         assert auto.steps <= e.steps or e.image_bytes > 144 * 1024
     assert auto.steps == 1 and auto.image_bytes <= 32 * 1024   # 4 CTAs x 256 per SM
+
+
+# ------------------------------------------------- tiered tables (f4) ------
+def test_tiered_plan_levels_and_sizes():
+    """eos_plan_table_levels (eossearch.h): D = 0 up to EOS_MAX_TABLE, then the
+    smallest D with n1 = ceil(n/4^D) <= EOS_MAX_TABLE; levels hold n1 4^(D-d)
+    fp64 each (d = 0..D-1); the smem table is the plan of X[::4^D]."""
+    rng = np.random.default_rng(7)
+    for n, D in [(1, 0), (16384, 0), (16385, 1), (65536, 1), (65537, 2), (262144, 2),
+                 (262145, 3), (1 << 20, 3), ((1 << 20) + 1, 4)]:
+        X = np.sort(10.0 ** rng.uniform(-6, 10, n))
+        info = eos.plan_table_levels(X)
+        assert info.levels == D and info.n == n, (n, info.levels)
+        n1 = -(-n // 4 ** D)
+        assert info.top_n == n1 <= eos.EOS_MAX_TABLE
+        assert info.level_bytes == 8 * sum(n1 * 4 ** (D - d) for d in range(D))
+        top, _ = eos.plan_table(X[::4 ** D], with_directory=False)
+        for f in ("bins", "max_occ", "steps", "k", "hash_kind", "hash_mult", "image_bytes"):
+            assert getattr(info, f) == getattr(top, f), (n, f)
+    # explicit D on small tables (testing the tiered path at any size)
+    X = np.sort(rng.uniform(1, 2, 1000))
+    for D in range(0, 9):
+        info = eos.plan_table_levels(X, levels=D)
+        assert info.levels == D and info.top_n == -(-1000 // 4 ** D)
+
+
+def test_tiered_plan_errors():
+    X = np.arange(1.0, 20001.0)
+    with pytest.raises(eos.EosError) as e:
+        eos.plan_table_levels(X, levels=0)          # n1 = n > EOS_MAX_TABLE
+    assert e.value.name == "EOS_ERR_SIZE"
+    with pytest.raises(eos.EosError) as e:
+        eos.plan_table_levels(X, levels=9)
+    assert e.value.name == "EOS_ERR_UNSUPPORTED"
+    with pytest.raises(eos.EosError) as e:
+        eos.plan_table_levels(np.empty(0))
+    assert e.value.name == "EOS_ERR_SIZE"
+    bad = X.copy()
+    bad[17_000] = np.nan
+    with pytest.raises(eos.EosError) as e:
+        eos.plan_table_levels(bad)
+    assert e.value.name == "EOS_ERR_NONFINITE"
+    bad = X.copy()
+    bad[17_000], bad[17_001] = bad[17_001], bad[17_000]
+    with pytest.raises(eos.EosError) as e:
+        eos.plan_table_levels(bad)
+    assert e.value.name == "EOS_ERR_UNSORTED"
+    # duplicates and a -0.0 head are valid (P:54-56 non-decreasing; R6)
+    dup = np.concatenate([[-0.0], np.repeat(np.arange(1.0, 9000.0), 3)])
+    info = eos.plan_table_levels(dup)
+    assert info.levels == 1 and info.key_mode == 0
