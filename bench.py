@@ -301,7 +301,8 @@ def run_ours(a, d: Dist):
             "unit": "GB/s",
             "frac": round(achieved / hbm_peak, 4),
             "traffic": ncu_traffic(a.workload),
-            "kernel": "interp2d_kernel" if is2d else "search1d_kernel",
+            "kernel": "interp2d_kernel" if is2d else (
+                "search1d_tiered_kernel" if obj.info.levels > 0 else "search1d_kernel"),
             "kernel_ms_avg": round(kern_ms, 5),
             "kernel_ms_avg_max_rank": round(kern_ms_max, 5),
             "algorithmic_bytes_per_launch": bytes_per * count,

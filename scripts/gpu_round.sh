@@ -71,6 +71,19 @@ if has tiered; then
     python -c "import json;d=json.load(open('$OUT/big_D$D.json'));r=d['roofline'];print('big D=$D', d['value'], r['frac'], r['l2']['frac'])" || tail -n 3 $OUT/big_D$D.err
   done
 fi
+if has ncubig; then
+  CMD="python bench.py --workload big --steps 6 --warmup 2 --no-e2e --no-cpu --eager"
+  $CMD > $OUT/ncubig_plain.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:search1d_tiered -s 2 -c 1 \
+      -o $OUT/prof_big -f $CMD > $OUT/ncubig_full.log 2>&1; echo "ncu big rc=$?"
+  python scripts/ncu_summary.py $OUT/prof_big.ncu-rep > $OUT/ncu_summary_big.json
+  ncu -i $OUT/prof_big.ncu-rep --page raw --csv > $OUT/ncu_raw_big.csv 2>/dev/null
+  ncu -i $OUT/prof_big.ncu-rep --page details --csv > $OUT/ncu_details_big.csv 2>/dev/null
+fi
+if has benchbig; then
+  timeout 900 python bench.py --workload big --steps 200 --warmup 5 > $OUT/bench_big.json 2> $OUT/bench_big.err; echo "bench big rc=$?"
+  cat $OUT/bench_big.json | head -c 1500; echo; tail -n 3 $OUT/bench_big.err
+fi
 if has exp; then
   timeout 900 python scripts/exp_search.py --workload cfg2 --ks 2,3,4,5,6,7,8 > $OUT/exp_cfg2.json 2> $OUT/exp_cfg2.err; echo "exp cfg2 rc=$?"
   timeout 900 python scripts/exp_search.py --workload cfg3 --steps 50 --ks 3,4,5,6,7,8 > $OUT/exp_cfg3.json 2> $OUT/exp_cfg3.err; echo "exp cfg3 rc=$?"
