@@ -84,6 +84,13 @@ if has benchbig; then
   timeout 900 python bench.py --workload big --steps 200 --warmup 5 > $OUT/bench_big.json 2> $OUT/bench_big.err; echo "bench big rc=$?"
   cat $OUT/bench_big.json | head -c 1500; echo; tail -n 3 $OUT/bench_big.err
 fi
+if has interpv; then
+  EOS_INTERP_VARIANT=7 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "interp or smoke" > $OUT/pytest_interp_v7.log 2>&1; echo "pytest interp v7 rc=$?"; tail -n 2 $OUT/pytest_interp_v7.log
+  for v in 0 7 8 0 7 8; do
+    EOS_INTERP_VARIANT=$v timeout 600 python bench.py --workload cfg4 --steps 200 --warmup 5 --no-cpu --no-e2e > $OUT/b4v.json 2>/dev/null
+    python -c "import json;d=json.load(open('$OUT/b4v.json'));print('cfg4 v$v', d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'], d['clocks']['reasons'])"
+  done
+fi
 if has exp; then
   timeout 900 python scripts/exp_search.py --workload cfg2 --ks 2,3,4,5,6,7,8 > $OUT/exp_cfg2.json 2> $OUT/exp_cfg2.err; echo "exp cfg2 rc=$?"
   timeout 900 python scripts/exp_search.py --workload cfg3 --steps 50 --ks 3,4,5,6,7,8 > $OUT/exp_cfg3.json 2> $OUT/exp_cfg3.err; echo "exp cfg3 rc=$?"
