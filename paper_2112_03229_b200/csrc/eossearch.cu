@@ -188,6 +188,7 @@ const Variant kVariants[] = {
     {"clc1024u4", 1024, 4, true, variant_fn<dv::Shape<1024, 4, 1, true>>},
     {"clc1024u2", 1024, 2, true, variant_fn<dv::Shape<1024, 2, 1, true>>},
     {"clc128u8", 128, 8, true, variant_fn<dv::Shape<128, 8, 8, true>>},
+    {"static1024u4", 1024, 4, false, variant_fn<dv::Shape<1024, 4, 1, false>>},
 };
 
 template <int S>

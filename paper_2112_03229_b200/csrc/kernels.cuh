@@ -98,16 +98,26 @@ __device__ __forceinline__ uint32_t key_hi(double y) {
 __device__ __forceinline__ uint32_t bin_of(uint32_t key, const AxisParams& a) {
   return min(__umulhi(max(key, a.hb) - a.hb, a.M), a.bmax);
 }
+// Same function for mode-0 keys (key, hb < 2^31): max(key, hb) - hb ==
+// max(key - hb, 0) in int32, one VIADDMNMX instead of VIMNMX + VIADD.
+__device__ __forceinline__ uint32_t bin_of_m0(uint32_t key, const AxisParams& a) {
+  return min(__umulhi((uint32_t)max((int32_t)(key - a.hb), 0), a.M), a.bmax);
+}
 
 // The hot per-target body:
 //   bin b = min(umulhi(max(key, hb) - hb, M), B-1)          (exponent / log hash)
 //   lo, occ = directory[b]                                  (count directory)
 //   c = #{j < occ : X[lo + j] <= y}  by S-step binary lifting (branchless)
 //   idx = (y >= X[0]) ? lo + c - 1 : 0                      (P:54 fix-up; NaN -> 0)
+// Probes past the bin (j > occ) are predicated off, so they move no smem
+// data: with fine bins most lanes probe nothing.  (Measured: dropping the
+// occupancy test -- NaN-padded X, 3 instructions per step -- is 11% slower on
+// cfg2 and 34% on cfg5, DESIGN.md tuning log.)
 template <int S, int MODE>
 __device__ __forceinline__ int32_t lookup(double y, const double* __restrict__ sX,
                                           const uint32_t* __restrict__ sD, const AxisParams& a) {
-  const uint32_t b = bin_of(key_hi<MODE>(y), a);
+  const uint32_t key = key_hi<MODE>(y);
+  const uint32_t b = MODE == 0 ? bin_of_m0(key, a) : bin_of(key, a);
   EOS_DCHECK(b <= a.bmax);
   const uint32_t d = sD[b];
   const int32_t lo = (int32_t)(d & 0xFFFFu);

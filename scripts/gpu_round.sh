@@ -91,6 +91,18 @@ if has interpv; then
     python -c "import json;d=json.load(open('$OUT/b4v.json'));print('cfg4 v$v', d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'], d['clocks']['reasons'])"
   done
 fi
+if has lift; then
+  for r in 1 2; do
+    for v in default clc256u4_lift1 clc256u4_lift2; do
+      EOS_SEARCH_VARIANT=$v timeout 600 python bench.py --workload cfg2 --steps 500 --warmup 5 --no-cpu --no-e2e > $OUT/lift.json 2>/dev/null
+      python -c "import json;d=json.load(open('$OUT/lift.json'));print('cfg2 $v', d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'])"
+    done
+    for v in default static1024u4_lift1 static1024u4_lift2; do
+      EOS_SEARCH_VARIANT=$v timeout 600 python bench.py --workload cfg5 --count 2147483648 --steps 20 --warmup 3 --no-cpu --no-e2e > $OUT/lift.json 2>/dev/null
+      python -c "import json;d=json.load(open('$OUT/lift.json'));print('cfg5 $v', d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'])"
+    done
+  done
+fi
 if has exp; then
   timeout 900 python scripts/exp_search.py --workload cfg2 --ks 2,3,4,5,6,7,8 > $OUT/exp_cfg2.json 2> $OUT/exp_cfg2.err; echo "exp cfg2 rc=$?"
   timeout 900 python scripts/exp_search.py --workload cfg3 --steps 50 --ks 3,4,5,6,7,8 > $OUT/exp_cfg3.json 2> $OUT/exp_cfg3.err; echo "exp cfg3 rc=$?"
