@@ -139,6 +139,8 @@ if has ncu2; then
     $CMD > $OUT/ncu_plain_$wl.log 2>&1 && \
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:'search1d|interp2d' -s 2 -c 1 \
         -o $OUT/prof_$wl -f $CMD > $OUT/ncu_full_$wl.log 2>&1; echo "ncu $wl rc=$?"
+    python scripts/ncu_summary.py $OUT/prof_$wl.ncu-rep > $OUT/ncu_summary_$wl.json
+    ncu -i $OUT/prof_$wl.ncu-rep --page details --csv > $OUT/ncu_details_$wl.csv 2>/dev/null
   done
 fi
 if has ncufinal; then
