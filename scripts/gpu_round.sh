@@ -79,6 +79,7 @@ if has ncubig; then
   python scripts/ncu_summary.py $OUT/prof_big.ncu-rep > $OUT/ncu_summary_big.json
   ncu -i $OUT/prof_big.ncu-rep --page raw --csv > $OUT/ncu_raw_big.csv 2>/dev/null
   ncu -i $OUT/prof_big.ncu-rep --page details --csv > $OUT/ncu_details_big.csv 2>/dev/null
+  rm -f $OUT/prof_big.ncu-rep
 fi
 if has benchbig; then
   timeout 900 python bench.py --workload big --steps 200 --warmup 5 > $OUT/bench_big.json 2> $OUT/bench_big.err; echo "bench big rc=$?"
@@ -141,6 +142,8 @@ if has ncu2; then
         -o $OUT/prof_$wl -f $CMD > $OUT/ncu_full_$wl.log 2>&1; echo "ncu $wl rc=$?"
     python scripts/ncu_summary.py $OUT/prof_$wl.ncu-rep > $OUT/ncu_summary_$wl.json
     ncu -i $OUT/prof_$wl.ncu-rep --page details --csv > $OUT/ncu_details_$wl.csv 2>/dev/null
+    ncu -i $OUT/prof_$wl.ncu-rep --page source --csv > $OUT/ncu_source_$wl.csv 2>/dev/null
+    rm -f $OUT/prof_$wl.ncu-rep
   done
 fi
 if has ncufinal; then
