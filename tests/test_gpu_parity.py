@@ -724,3 +724,36 @@ def test_tiered_host_pipeline_and_counters():
     torch.cuda.synchronize()
     assert np.array_equal(c.cpu().numpy().view(np.uint64), oracle.counters(X, Y, ref, off))
     t.close()
+
+
+# ------------------------------------ maximum sizes and deep bins (S > 8) ---
+@pytest.mark.parametrize("kind", ["all_equal", "three_values", "max_random", "dup_runs"])
+def test_max_table_and_runtime_steps(kind):
+    """n = EOS_MAX_TABLE (16384) tables, including bins deeper than the
+    template steps (S > 8: the runtime-S instantiation, kernels.cuh lookup<0>)."""
+    rng = np.random.default_rng(len(kind))
+    n = eos.EOS_MAX_TABLE
+    if kind == "all_equal":
+        X = np.full(n, 3.0)
+    elif kind == "three_values":
+        X = np.sort(rng.choice([0.5, 2.0, 1e3], n))
+    elif kind == "max_random":
+        X = np.sort(10.0 ** rng.uniform(-8, 8, n))
+    else:
+        X = np.sort(np.repeat(10.0 ** rng.uniform(-2, 2, n // 300 + 1), 300)[:n])
+    Y = _big_probes(rng, X, 1 << 19)
+    ref = oracle.search(X, Y)
+    for k in feasible_ks(X, [None, 0, 3]):
+        t = eos.Table(X, k=k)
+        if kind in ("all_equal", "three_values", "dup_runs"):
+            assert t.info.steps > 8
+        out = t.search(to_dev(Y))
+        torch.cuda.synchronize()
+        assert_same(out.cpu().numpy(), ref, Y)
+        c = torch.zeros(8, dtype=torch.int64, device=DEV)
+        t.search(to_dev(Y), counters=c, global_offset=7)
+        torch.cuda.synchronize()
+        assert np.array_equal(c.cpu().numpy().view(np.uint64), oracle.counters(X, Y, ref, 7))
+        t.close()
+    # the same tables tiered (the sample table inherits the deep bins)
+    assert_same(tiered_search(X, Y, 2), ref, Y)
