@@ -35,7 +35,7 @@ __all__ = [
 ]
 
 EOS_MAX_TABLE = 16384
-EOS_MAX_TABLE_TIERED = 1 << 30
+EOS_MAX_TABLE_TIERED = 1 << 29
 EOS_LEVELS_AUTO = -1
 EOS_MAX_K = 19
 EOS_K_AUTO = -1
@@ -345,7 +345,7 @@ class Table:
     def __init__(self, table, k: int | None = None, log_bins: int | None = None,
                  levels: int = EOS_LEVELS_AUTO):
         """k: exponent hash with k mantissa bits; log_bins: logarithm hash with |H| bins;
-        neither: the automatic choice.  levels: D 4-ary global levels
+        neither: the automatic choice.  levels: D 8-ary global levels
         under a shared-memory sample table (tables above EOS_MAX_TABLE entries need
         D >= 1; -1 = automatic).  Results never depend on any of them."""
         self.X = _f64_host(table)

@@ -65,20 +65,27 @@ eos_status plan_table(const double* X, int64_t n, int kind, int64_t param, bool 
                       TablePlan* out);
 
 // Tables larger than shared memory (eossearch.h
-// eos_search_create_levels).  D 4-ary levels in global memory under a
-// shared-memory sample table T1[j] = X[j 4^D], j < n1 = ceil(n / 4^D).
-// Level d (stride 4^d, d = 0..D-1) has n1 4^(D-d) entries Lv_d[j] = X[j 4^d]
-// for j 4^d < n, NaN after (NaN <= y is false for every y, so padding is
-// never counted).  `lv` stores the levels coarsest first: D-1, D-2, .., 0,
-// so level d starts at element n1 (4^(D-d) - 4) / 3 and level 0 is X itself.
-constexpr int kMaxLevels = 8;  // n <= EOS_MAX_TABLE 4^8 = 2^30
+// eos_search_create_levels).  D 8-ary levels in global memory under a
+// shared-memory sample table T1[j] = X[j 8^D], j < n1 = ceil(n / 8^D).
+// Level d (stride 8^d, d = 0..D-1) has n1 8^(D-d) entries
+//   F_d[j] = X[j 8^d]            (fp64; NaN past n: never <= y)
+//   K_d[j] = key_hi(F_d[j])      (u32 order-preserving upper word of the
+//                                 key; 0xFFFFFFFF past n)
+// A level step reads the 8 keys of a node (one 32-byte sector) and falls
+// back to the node's 8 fp64 values only when a key equals the target's.
+// Both arrays store their levels coarsest first (D-1, .., 0); level d starts
+// at element n1 (8^(D-d) - 8) / 7 and F level 0 is X itself.
+constexpr int kMaxLevels = 5;  // n <= EOS_MAX_TABLE 8^5 = 2^29
+constexpr int kFanout = 8;
 struct TieredPlan {
   int levels = 0;             // D (0: single-level smem table, `top` is the table)
   int64_t n = 0;              // entries of the full table
   int64_t top_n = 0;          // n1
   double x_last = 0.0;        // X[n-1]
   TablePlan top;              // T1 and its directory (the smem image)
-  std::vector<double> lv;     // the levels (empty when levels == 0)
+  std::vector<double> lv;     // F levels (empty when levels == 0)
+  std::vector<uint32_t> keys; // K levels
+  int64_t level_elems() const { return (int64_t)lv.size(); }
 };
 
 // levels: EOS_LEVELS_AUTO (0 if n <= EOS_MAX_TABLE, else the smallest D with

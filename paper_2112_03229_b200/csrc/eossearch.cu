@@ -28,7 +28,8 @@ struct eos_table_s {
   int64_t n = 0;           // entries of the full table
   int64_t top_n = 0;       // n1
   int64_t level_bytes = 0;
-  double* levels_dev = nullptr;  // the 4-ary levels, coarsest first
+  int64_t level_elems = 0;
+  double* levels_dev = nullptr;  // the 8-ary levels: F (fp64) then K (u32), coarsest first
   int device = -1;
   int num_sms = 0;
   void* image_dev = nullptr;
@@ -113,13 +114,13 @@ const void* tiered_fn_mode(int steps, bool cnt) {
 
 // Launch-shape variants of the tiered kernel (EOS_TIERED_VARIANT=<name>,
 // tuning experiments; mode 0, no counters, S <= 4).
-template <class SH, bool NA = true>
+template <class SH>
 const void* tiered_variant_fn(int steps) {
   switch (steps) {
-    case 1: return (const void*)dv::search1d_tiered_kernel<1, 0, false, SH, NA>;
-    case 2: return (const void*)dv::search1d_tiered_kernel<2, 0, false, SH, NA>;
-    case 3: return (const void*)dv::search1d_tiered_kernel<3, 0, false, SH, NA>;
-    case 4: return (const void*)dv::search1d_tiered_kernel<4, 0, false, SH, NA>;
+    case 1: return (const void*)dv::search1d_tiered_kernel<1, 0, false, SH>;
+    case 2: return (const void*)dv::search1d_tiered_kernel<2, 0, false, SH>;
+    case 3: return (const void*)dv::search1d_tiered_kernel<3, 0, false, SH>;
+    case 4: return (const void*)dv::search1d_tiered_kernel<4, 0, false, SH>;
     default: return nullptr;
   }
 }
@@ -169,12 +170,9 @@ const void* variant_fn(int steps) {
 
 const Variant kTieredVariants[] = {
     {"static512u4", 512, 4, false, tiered_variant_fn<dv::Shape<512, 4, 1, false>>},
-    {"clc512u4", 512, 4, true, tiered_variant_fn<dv::Shape<512, 4, 1, true>>},
     {"static1024u2", 1024, 2, false, tiered_variant_fn<dv::Shape<1024, 2, 1, false>>},
     {"clc1024u2", 1024, 2, true, tiered_variant_fn<dv::Shape<1024, 2, 1, true>>},
-    {"static256u8", 256, 8, false, tiered_variant_fn<dv::Shape<256, 8, 1, false>>},
-    {"static512u4l1", 512, 4, false, tiered_variant_fn<dv::Shape<512, 4, 1, false>, false>},
-    {"static1024u2l1", 1024, 2, false, tiered_variant_fn<dv::Shape<1024, 2, 1, false>, false>},
+    {"static1024u1", 1024, 1, false, tiered_variant_fn<dv::Shape<1024, 1, 1, false>>},
 };
 
 const Variant kVariants[] = {
@@ -354,7 +352,8 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
   a.gofs = gofs;
   a.counters = (unsigned long long*)counters;
   a.lv = t->levels_dev;
-  a.lv_top_len = 4 * t->top_n;
+  a.kv = t->levels_dev ? reinterpret_cast<const uint32_t*>(t->levels_dev + t->level_elems) : nullptr;
+  a.lv_top_len = 8 * t->top_n;
   a.levels = t->levels;
   // Vector body needs Y+head 16-B aligned and out+head 8-B aligned.
   const uintptr_t ya = (uintptr_t)Y, oa = (uintptr_t)out;
@@ -541,6 +540,7 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
   eos_table t = new (std::nothrow) eos_table_s();
   if (!t) return EOS_ERR_NOMEM;
   std::vector<double> lv;
+  std::vector<uint32_t> keys;
   {
     eos::TieredPlan tp;
     eos_status st = eos::plan_tiered(table_host, n, levels, kind, param, &tp);
@@ -549,8 +549,9 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
     t->levels = tp.levels;
     t->n = tp.n;
     t->top_n = tp.top_n;
-    t->level_bytes = 8 * (int64_t)tp.lv.size();
+    t->level_bytes = 12 * tp.level_elems();
     lv = std::move(tp.lv);
+    keys = std::move(tp.keys);
     t->ax = axis_params(t->plan, 0);
     t->ax.xlast = tp.x_last;  // X[n-1] of the full table (counter c4)
   }
@@ -566,11 +567,17 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
   eos_status st = upload(eos::make_image(t->plan), &t->image_dev);
   if (st != EOS_OK) return fail(st);
   if (t->levels > 0) {
+    // [F levels fp64][K levels u32], both coarsest first
     e = cudaMalloc((void**)&t->levels_dev, (size_t)t->level_bytes);
     if (e == cudaSuccess)
-      e = cudaMemcpy(t->levels_dev, lv.data(), (size_t)t->level_bytes, cudaMemcpyHostToDevice);
+      e = cudaMemcpy(t->levels_dev, lv.data(), 8 * lv.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(reinterpret_cast<char*>(t->levels_dev) + 8 * lv.size(), keys.data(),
+                     4 * keys.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return fail(cuda_status(e));
+    t->level_elems = (int64_t)lv.size();
     std::vector<double>().swap(lv);
+    std::vector<uint32_t>().swap(keys);
   }
   for (int c = 0; c < 2 && st == EOS_OK; ++c) {
     const bool cnt = c == 1;

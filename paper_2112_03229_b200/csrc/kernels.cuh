@@ -70,11 +70,13 @@ struct SearchArgs {
   int64_t count;
   int64_t gofs;                  // global offset (counters)
   unsigned long long* counters;  // u64[8] or null
-  // tiered tables (n > EOS_MAX_TABLE, search1d_tiered_kernel): the 4-ary
-  // global levels, coarsest first; level d (stride 4^d) holds n1 4^(D-d)
-  // entries X[j 4^d] (NaN past the end), level D-1 starts at lv.
+  // tiered tables (n > EOS_MAX_TABLE, search1d_tiered_kernel): the 8-ary
+  // global levels, coarsest first (eos_internal.h TieredPlan); level d
+  // (stride 8^d) holds n1 8^(D-d) entries: fp64 X[j 8^d] (NaN past the end)
+  // at lv, their u32 keys (0xFFFFFFFF past the end) at kv.
   const double* lv;
-  int64_t lv_top_len;            // 4 n1: length of level D-1
+  const uint32_t* kv;
+  int64_t lv_top_len;            // 8 n1: length of level D-1
   int32_t levels;                // D (0: single-level smem table)
   int32_t pad2_;
 };
@@ -188,65 +190,92 @@ struct SmemLookup {
   __device__ __forceinline__ double x_at(int32_t i) const { return sX[i]; }
 };
 
-// TieredLookup (tables larger than shared memory, SURVEY §8(f) f4): the smem
-// table is the sample T1[j] = X[j 4^D] (n1 entries) with its directory; the
-// full table lives in global memory (L2-resident) as D 4-ary levels, level d
-// holding Lv_d[j] = X[j 4^d] (NaN past n).  Per target:
-//   b = max(#{T1 <= y} - 1, 0)                       (smem lookup, as above)
-//   for d = D-1 .. 0:  c = #{t < 4 : Lv_d[4b + t] <= y}   (one 32-B sector)
-//                      b = 4b + max(c - 1, 0)
-//   idx = (y >= X[0]) ? b : 0
-// Invariant: X[b 4^(d+1)] <= y < X[(b+1) 4^(d+1)] (or past the end), so
-// Lv_d[4b] <= y and c >= 1 for every y >= X[0]; NaN padding is never <= y.
-// At d = 0 the block has stride 1 and b = #{X <= y} - 1.  All targets
-// of a thread go through a level together (level-major) so their 2U sector
-// loads are in flight at once.
-// One 32-byte sector (4 fp64) with one 256-bit load (SASS LDG.E.ENL2.256):
-// one L1TEX wavefront per lane instead of two LDG.128 -- the gathers of a
-// warp hit 32 different lines, so wavefronts, not bytes, bound the L1 stage.
-// NA: L1::no_allocate (the levels are too large to live in L1).
-template <bool NA>
-__device__ __forceinline__ void ldg_sector(const double* p, double& a, double& b, double& c,
-                                           double& d) {
-  if (NA)
-    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
-        : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
-        : "l"(p));
-  else
-    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+// One 32-byte sector with one 256-bit load (SASS LDG.E.NA.ENL2.256): one
+// L1TEX wavefront per lane -- the gathers of a warp hit 32 different lines,
+// so wavefronts, not bytes, bound the L1 stage.  L1::no_allocate: the levels
+// are too large to live in L1 (measured faster than allocating).
+__device__ __forceinline__ void ldg_keys8(const uint32_t* p, uint32_t (&k)[8]) {
+  asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(k[0]), "=r"(k[1]), "=r"(k[2]), "=r"(k[3]), "=r"(k[4]), "=r"(k[5]), "=r"(k[6]),
+        "=r"(k[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void ldg_f64x4(const double* p, double& a, double& b, double& c,
+                                          double& d) {
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+      : "l"(p));
 }
 
-template <int S, int MODE, bool NA = true>
+// TieredLookup (tables larger than shared memory, SURVEY §8(f) f4): the smem
+// table is the sample T1[j] = X[j 8^D] (n1 entries) with its directory; the
+// full table lives in global memory (L2-resident) as D 8-ary levels, level d
+// holding F_d[j] = X[j 8^d] (NaN past n) and their keys K_d[j] =
+// key_hi(F_d[j]) (0xFFFFFFFF past n).  Per target:
+//   b = max(#{T1 <= y} - 1, 0)                      (smem lookup, as above)
+//   for d = D-1 .. 0:  node = K_d[8b .. 8b+8)         (one 32-B sector)
+//     c = #{t : node[t] < key(y)}                      (key order = value order)
+//     if some node[t] == key(y): c = #{t : F_d[8b+t] <= y}   (exact; rare)
+//     b = 8b + max(c - 1, 0)
+//   idx = (y >= X[0]) ? b : 0
+// key_hi is the upper word of an order-preserving map of the fp64 bits, so
+// key(X) < key(y) implies X < y and key(X) > key(y) implies X > y; only
+// equal keys need the fp64 values.  Invariant: X[b 8^(d+1)] <= y <
+// X[(b+1) 8^(d+1)] (or past the end), so c >= 1 for every y >= X[0].  At
+// d = 0 the stride is 1 and b = #{X <= y} - 1.  All targets of a
+// thread go through a level together so their sector loads overlap.
+template <int S, int MODE>
 struct TieredLookup {
   const double* __restrict__ sX;  // T1 (smem)
   const uint32_t* __restrict__ sD;
   AxisParams a;                   // of T1, except xlast = X[n-1] (counter c4)
-  const double* __restrict__ lv;  // level D-1 (global)
-  int64_t top_len;                // 4 n1
+  const double* __restrict__ lv;  // F level D-1 (global)
+  const uint32_t* __restrict__ kv;  // K level D-1 (global)
+  int64_t top_len;                // 8 n1
   int32_t levels;                 // D >= 1
-  const double* __restrict__ x_full;  // level 0 = X (counter c6)
+  const double* __restrict__ x_full;  // F level 0 = X (counter c6)
   template <int N>
   __device__ __forceinline__ void many(const double (&y)[N], int32_t (&r)[N]) const {
     int32_t b[N];
+    uint32_t ky[N];
 #pragma unroll
-    for (int i = 0; i < N; ++i) b[i] = lookup<S, MODE>(y[i], sX, sD, a);
-    const double* L = lv;
+    for (int i = 0; i < N; ++i) {
+      b[i] = lookup<S, MODE>(y[i], sX, sD, a);
+      ky[i] = key_hi<MODE>(y[i]);
+    }
+    const double* F = lv;
+    const uint32_t* K = kv;
     int64_t len = top_len;
     for (int d = levels - 1; d >= 0; --d) {
-      double q[N][4];
+      uint32_t k[N][8];
 #pragma unroll
       for (int i = 0; i < N; ++i) {
-        EOS_DCHECK(b[i] >= 0 && 4 * (int64_t)b[i] + 3 < len);
-        ldg_sector<NA>(L + 4 * (int64_t)b[i], q[i][0], q[i][1], q[i][2], q[i][3]);
+        EOS_DCHECK(b[i] >= 0 && 8 * (int64_t)b[i] + 7 < len);
+        ldg_keys8(K + 8 * (int64_t)b[i], k[i]);
       }
 #pragma unroll
       for (int i = 0; i < N; ++i) {
-        const int32_t c = (q[i][0] <= y[i]) + (q[i][1] <= y[i]) + (q[i][2] <= y[i]) +
-                          (q[i][3] <= y[i]);
-        b[i] = 4 * b[i] + max(c - 1, 0);
+        int32_t c = 0;
+        bool tie = false;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          c += k[i][t] < ky[i];
+          tie |= k[i][t] == ky[i];
+        }
+        if (tie) {  // exact count from the fp64 node (two sectors)
+          const double* f = F + 8 * (int64_t)b[i];
+          double v[8];
+          ldg_f64x4(f, v[0], v[1], v[2], v[3]);
+          ldg_f64x4(f + 4, v[4], v[5], v[6], v[7]);
+          c = 0;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) c += v[t] <= y[i];
+        }
+        b[i] = 8 * b[i] + max(c - 1, 0);
       }
-      L += len;
-      len *= 4;
+      F += len;
+      K += len;
+      len *= 8;
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) r[i] = (y[i] >= a.x0) ? b[i] : 0;
@@ -362,9 +391,8 @@ using ShapeBig = Shape<1024, 4, 1, true>;       // larger: 1 CTA x 1024 (one ima
 using ShapeDeepMid = Shape<512, 4, 2, false>;   // S >= 3, image <= 72 KB
 using ShapeDeepBig = Shape<1024, 4, 1, false>;  // S >= 3, larger
 using ShapeCnt = Shape<256, 4, 1, true>;        // validation launches (counters on)
-// Tiered tables: 1024 threads x 4 level-major lookup chains (56 registers),
-// static schedule.  Measured on `big` (n = 2^20, D = 3): 85 Glookups/s vs 77
-// for 512 x 8 chains, 72 for the CLC schedule (profiles/r01_exp_tiered.json).
+// Tiered tables: 1024 threads x 4 level-major lookup chains, static
+// schedule (profiles/r01_exp_tiered.json).
 using ShapeTiered = Shape<1024, 2, 1, false>;
 
 // The streaming tile loop of search1d (after the image is in smem): CLC or
@@ -495,7 +523,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
 
 // Tables larger than shared memory (TieredLookup): the smem image holds the
 // sample table T1 and its directory; the levels stay in global memory / L2.
-template <int S, int MODE, bool CNT, class SH, bool NA = true>
+template <int S, int MODE, bool CNT, class SH>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
     search1d_tiered_kernel(const SearchArgs args) {
   extern __shared__ __align__(16) uint4 smem[];
@@ -505,19 +533,20 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
   stage_image(smem, args.image, args.image_16, &stage_bar);
   pdl_enter();
   const AxisParams a = args.ax;
-  EOS_DCHECK(args.levels >= 1 && args.lv_top_len == 4 * (int64_t)a.n);
-  TieredLookup<S, MODE, NA> lk;
+  EOS_DCHECK(args.levels >= 1 && args.lv_top_len == 8 * (int64_t)a.n);
+  TieredLookup<S, MODE> lk;
   lk.sX = reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
   lk.sD = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(smem) + a.d_off);
   lk.a = a;
   lk.lv = args.lv;
+  lk.kv = args.kv;
   lk.top_len = args.lv_top_len;
   lk.levels = args.levels;
-  // level 0 (= X) follows levels D-1 .. 1: offset n1 (4^D - 4) / 3
+  // F level 0 (= X) follows levels D-1 .. 1: offset n1 (8^D - 8) / 7
   int64_t off = 0, len = args.lv_top_len;
   for (int d = args.levels - 1; d > 0; --d) {
     off += len;
-    len *= 4;
+    len *= 8;
   }
   lk.x_full = args.lv + off;
   search_body<CNT, SH>(args, lk, &clc_resp, &clc_bar);

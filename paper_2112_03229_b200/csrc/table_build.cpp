@@ -236,12 +236,13 @@ eos_status plan_tiered(const double* Xin, int64_t n, int levels, int kind, int64
                        TieredPlan* out) {
   if (!Xin || !out) return EOS_ERR_NULL;
   if (n < 1 || n > EOS_MAX_TABLE_TIERED) return EOS_ERR_SIZE;
+  auto pow8 = [](int d) { return int64_t(1) << (3 * d); };
   if (levels == EOS_LEVELS_AUTO) {
     levels = 0;
-    while ((n + (int64_t(1) << (2 * levels)) - 1) >> (2 * levels) > EOS_MAX_TABLE) ++levels;
+    while ((n + pow8(levels) - 1) / pow8(levels) > EOS_MAX_TABLE) ++levels;
   }
   if (levels < 0 || levels > kMaxLevels) return EOS_ERR_UNSUPPORTED;
-  const int64_t stride = int64_t(1) << (2 * levels);  // 4^D
+  const int64_t stride = pow8(levels);  // 8^D
   const int64_t n1 = (n + stride - 1) / stride;
   if (n1 > EOS_MAX_TABLE) return EOS_ERR_SIZE;
   TieredPlan t;
@@ -255,12 +256,13 @@ eos_status plan_tiered(const double* Xin, int64_t n, int levels, int kind, int64
     *out = std::move(t);
     return EOS_OK;
   }
-  // Level 0 = the validated, canonicalised table (same rules as plan_table).
+  // F level 0 = the validated, canonicalised table (same rules as plan_table).
   const int64_t len0 = n1 * stride;
   int64_t total = 0;
-  for (int d = 0; d < levels; ++d) total += len0 >> (2 * d);
+  for (int d = 0; d < levels; ++d) total += len0 / pow8(d);
   try {
     t.lv.assign((size_t)total, NAN);
+    t.keys.assign((size_t)total, 0xFFFFFFFFu);
   } catch (...) {
     return EOS_ERR_NOMEM;
   }
@@ -272,14 +274,22 @@ eos_status plan_tiered(const double* Xin, int64_t n, int levels, int kind, int64
     L0[j] = (v == 0.0) ? 0.0 : v;  // canonicalise -0.0 (R6)
     if (j > 0 && L0[j] < L0[j - 1]) return EOS_ERR_UNSORTED;
   }
-  // Coarser levels are strided samples of level 0 (NaN padding stays NaN).
+  const int mode = (L0[0] >= 0.0) ? 0 : 1;
+  // Coarser F levels are strided samples of level 0 (NaN padding stays NaN);
+  // K levels are the keys of the F entries (padding keeps 0xFFFFFFFF).
   int64_t off = off0, len = len0;
-  for (int d = 1; d < levels; ++d) {
-    const int64_t s = int64_t(1) << (2 * d);
-    len >>= 2;
-    off -= len;
-    double* Ld = t.lv.data() + off;
-    for (int64_t j = 0; j * s < n; ++j) Ld[j] = L0[j * s];
+  for (int d = 0; d < levels; ++d) {
+    if (d > 0) {
+      len /= kFanout;
+      off -= len;
+    }
+    const int64_t s = pow8(d);
+    double* Fd = t.lv.data() + off;
+    uint32_t* Kd = t.keys.data() + off;
+    for (int64_t j = 0; j * s < n; ++j) {
+      Fd[j] = L0[j * s];
+      Kd[j] = key_hi(Fd[j], mode);
+    }
   }
   std::vector<double> T1((size_t)n1);
   for (int64_t j = 0; j < n1; ++j) T1[j] = L0[j * stride];
@@ -322,7 +332,7 @@ void fill_info(const TieredPlan& t, eos_table_info_t* info) {
   info->n = t.n;
   info->levels = t.levels;
   info->top_n = t.top_n;
-  info->level_bytes = 8 * (int64_t)t.lv.size();
+  info->level_bytes = 12 * t.level_elems();  // fp64 F + u32 K per level entry
 }
 
 }  // namespace eos

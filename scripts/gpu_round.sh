@@ -62,11 +62,11 @@ fi
 if has tiered; then
   timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "tiered or smoke or golden" > $OUT/pytest_tiered.log 2>&1; echo "pytest tiered rc=$?"
   tail -n 5 $OUT/pytest_tiered.log
-  for v in default static512u4 static512u4l1 static1024u2 static1024u2l1 clc512u4 static256u8; do
+  for v in default static512u4 static1024u2 clc1024u2 static1024u1; do
     EOS_TIERED_VARIANT=$v timeout 600 python bench.py --workload big --steps 200 --warmup 5 --no-cpu --no-e2e > $OUT/big_$v.json 2> $OUT/big_$v.err
     python -c "import json;d=json.load(open('$OUT/big_$v.json'));r=d['roofline'];print('big $v', d['value'], r['frac'], r['l2'], d['clocks']['sm_mhz'])" || tail -n 3 $OUT/big_$v.err
   done
-  for D in 4 5; do
+  for D in 3 4; do
     timeout 600 python bench.py --workload big --levels $D --steps 200 --warmup 5 --no-cpu --no-e2e > $OUT/big_D$D.json 2> $OUT/big_D$D.err
     python -c "import json;d=json.load(open('$OUT/big_D$D.json'));r=d['roofline'];print('big D=$D', d['value'], r['frac'], r['l2']['frac'])" || tail -n 3 $OUT/big_D$D.err
   done

@@ -297,25 +297,26 @@ def test_auto_choice_never_worse_in_steps_than_any_exponent_k():
 # ------------------------------------------------- tiered tables (f4) ------
 def test_tiered_plan_levels_and_sizes():
     """eos_plan_table_levels (eossearch.h): D = 0 up to EOS_MAX_TABLE, then the
-    smallest D with n1 = ceil(n/4^D) <= EOS_MAX_TABLE; levels hold n1 4^(D-d)
-    fp64 each (d = 0..D-1); the smem table is the plan of X[::4^D]."""
+    smallest D with n1 = ceil(n/8^D) <= EOS_MAX_TABLE; levels hold n1 8^(D-d)
+    entries each (d = 0..D-1), 8 B fp64 + 4 B key; the smem table is the plan
+    of X[::8^D]."""
     rng = np.random.default_rng(7)
-    for n, D in [(1, 0), (16384, 0), (16385, 1), (65536, 1), (65537, 2), (262144, 2),
-                 (262145, 3), (1 << 20, 3), ((1 << 20) + 1, 4)]:
+    for n, D in [(1, 0), (16384, 0), (16385, 1), (131072, 1), (131073, 2), (1 << 20, 2),
+                 ((1 << 20) + 1, 3)]:
         X = np.sort(10.0 ** rng.uniform(-6, 10, n))
         info = eos.plan_table_levels(X)
         assert info.levels == D and info.n == n, (n, info.levels)
-        n1 = -(-n // 4 ** D)
+        n1 = -(-n // 8 ** D)
         assert info.top_n == n1 <= eos.EOS_MAX_TABLE
-        assert info.level_bytes == 8 * sum(n1 * 4 ** (D - d) for d in range(D))
-        top, _ = eos.plan_table(X[::4 ** D], with_directory=False)
+        assert info.level_bytes == 12 * sum(n1 * 8 ** (D - d) for d in range(D))
+        top, _ = eos.plan_table(X[::8 ** D], with_directory=False)
         for f in ("bins", "max_occ", "steps", "k", "hash_kind", "hash_mult", "image_bytes"):
             assert getattr(info, f) == getattr(top, f), (n, f)
     # explicit D on small tables (testing the tiered path at any size)
     X = np.sort(rng.uniform(1, 2, 1000))
-    for D in range(0, 9):
+    for D in range(0, 6):
         info = eos.plan_table_levels(X, levels=D)
-        assert info.levels == D and info.top_n == -(-1000 // 4 ** D)
+        assert info.levels == D and info.top_n == -(-1000 // 8 ** D)
 
 
 def test_tiered_plan_errors():
@@ -324,7 +325,7 @@ def test_tiered_plan_errors():
         eos.plan_table_levels(X, levels=0)          # n1 = n > EOS_MAX_TABLE
     assert e.value.name == "EOS_ERR_SIZE"
     with pytest.raises(eos.EosError) as e:
-        eos.plan_table_levels(X, levels=9)
+        eos.plan_table_levels(X, levels=6)
     assert e.value.name == "EOS_ERR_UNSUPPORTED"
     with pytest.raises(eos.EosError) as e:
         eos.plan_table_levels(np.empty(0))
