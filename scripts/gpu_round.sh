@@ -104,6 +104,17 @@ if has lift; then
     done
   done
 fi
+if has guess; then
+  timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "interp or smoke or loglog" > $OUT/pytest_guess.log 2>&1; echo "pytest interp rc=$?"; tail -n 3 $OUT/pytest_guess.log
+  for r in 1 2; do
+    for gs in 1 0; do
+      for fl in "" "--derivatives" "--loglog"; do
+        EOS_INTERP_GUESS=$gs timeout 600 python bench.py --workload cfg4 $fl --steps 200 --warmup 5 --no-cpu --no-e2e > $OUT/g4.json 2>/dev/null
+        python -c "import json;d=json.load(open('$OUT/g4.json'));print('cfg4 guess=$gs [$fl]', d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'], d['config']['table']['rho'].get('cell_map'))"
+      done
+    done
+  done
+fi
 if has exp; then
   timeout 900 python scripts/exp_search.py --workload cfg2 --ks 2,3,4,5,6,7,8 > $OUT/exp_cfg2.json 2> $OUT/exp_cfg2.err; echo "exp cfg2 rc=$?"
   timeout 900 python scripts/exp_search.py --workload cfg3 --steps 50 --ks 3,4,5,6,7,8 > $OUT/exp_cfg3.json 2> $OUT/exp_cfg3.err; echo "exp cfg3 rc=$?"

@@ -760,3 +760,48 @@ def test_max_table_and_runtime_steps(kind):
         t.close()
     # the same tables tiered (the sample table inherits the deep bins)
     assert_same(tiered_search(X, Y, 2), ref, Y)
+
+
+# ------------------------------ 2-D regular axes, node and near-node targets --
+@pytest.mark.parametrize("axes", ["logspace", "linspace", "mixed", "perturbed"])
+@pytest.mark.parametrize("loglog", [False, True])
+def test_interp_regular_axes_node_targets(axes, loglog):
+    """Logspace / linspace axes (the EOSPAC table shapes) with targets at, just below
+    and just above every node, out of range and special values: brackets equal the
+    oracle's, values within the 1e-12 bar, derivative and plain kernels agree."""
+    rng = np.random.default_rng(sum(map(ord, axes)))
+    if axes == "logspace":
+        R, T = np.logspace(-6, 3, 200), np.logspace(0, 8, 100)
+    elif axes == "linspace":
+        R, T = np.linspace(0.5, 50.0, 150), np.linspace(1.0, 2.0, 77)
+    elif axes == "mixed":
+        R, T = np.logspace(-3, 3, 120), np.linspace(10.0, 1e4, 90)
+    else:  # nodes moved by up to 0.1%
+        R = np.logspace(-2, 2, 64) * (1 + 0.001 * rng.uniform(-1, 1, 64))
+        T = np.logspace(1, 5, 50)
+    G = np.exp(rng.uniform(0.0, 3.0, (R.size, T.size)))
+    m = 1 << 18
+    rho = 10 ** rng.uniform(np.log10(R[0]) - 0.5, np.log10(R[-1]) + 0.5, m)
+    tt = 10 ** rng.uniform(np.log10(T[0]) - 0.5, np.log10(T[-1]) + 0.5, m)
+    k = R.size
+    rho[:k], rho[k:2 * k], rho[2 * k:3 * k] = R, np.nextafter(R, 0), np.nextafter(R, np.inf)
+    kt = T.size
+    tt[-kt:], tt[-2 * kt:-kt], tt[-3 * kt:-2 * kt] = T, np.nextafter(T, 0), np.nextafter(T, np.inf)
+    rho[3 * k:3 * k + 6] = [np.nan, np.inf, -np.inf, 0.0, -0.0, -1.0]
+    tt[3 * k + 6:3 * k + 12] = [np.nan, np.inf, -np.inf, 0.0, -0.0, -1.0]
+    g = eos.Grid2D(R, T, G, loglog=loglog)
+    P, iR, iT, dR, dT = g.interp(to_dev(rho), to_dev(tt), derivatives=True)
+    P0, iR0, iT0 = g.interp(to_dev(rho), to_dev(tt))
+    torch.cuda.synchronize()
+    assert np.array_equal(P.cpu().numpy(), P0.cpu().numpy(), equal_nan=True)
+    assert torch.equal(iR, iR0) and torch.equal(iT, iT0)
+    if loglog:
+        Pr, iRr, iTr, dRr, dTr = oracle.interp2d_loglog(R, T, G, rho, tt)
+    else:
+        Pr, iRr, iTr = oracle.interp2d(R, T, G, rho, tt)
+        dRr, dTr = oracle.interp2d_deriv(R, T, G, rho, tt)
+    assert np.array_equal(iR.cpu().numpy(), iRr) and np.array_equal(iT.cpu().numpy(), iTr)
+    check_interp(P.cpu().numpy(), Pr)
+    _check_deriv(dR.cpu().numpy(), dRr)
+    _check_deriv(dT.cpu().numpy(), dTr)
+    g.close()
