@@ -430,13 +430,23 @@ eos_status upload(const std::vector<uint8_t>& img, void** dev) {
 template <class Body>
 eos_status host_pipeline(cudaStream_t caller, int64_t count, int64_t chunk, int64_t bytes_per_elem,
                          Body body) {
+  // tuning experiments: EOS_HOST_SLOTS (1..4), EOS_HOST_CHUNK_LOG2 (16..26)
+  static const int slots_env = [] {
+    const char* e = getenv("EOS_HOST_SLOTS");
+    return e ? std::max(1, std::min(4, atoi(e))) : 2;
+  }();
+  static const int chunk_log2 = [] {
+    const char* e = getenv("EOS_HOST_CHUNK_LOG2");
+    return e ? std::max(16, std::min(26, atoi(e))) : 0;
+  }();
+  if (chunk_log2) chunk = (int64_t(1) << chunk_log2) * chunk / (int64_t(1) << 23);
   const int64_t nchunk = (count + chunk - 1) / chunk;
-  const int nslot = nchunk > 1 ? 2 : 1;
+  const int nslot = (int)std::min<int64_t>(nchunk, slots_env);
   const int64_t slot_elems = (std::min(chunk, count) + 63) & ~int64_t(63);  // keeps 16-B alignment
   char* stage = nullptr;
   EOS_CUDA(cudaMallocAsync((void**)&stage, (size_t)(nslot * slot_elems * bytes_per_elem), caller));
-  cudaStream_t s[2] = {nullptr, nullptr};
-  cudaEvent_t ev_start = nullptr, ev_done[2] = {nullptr, nullptr};
+  cudaStream_t s[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr, ev_done[4] = {nullptr, nullptr, nullptr, nullptr};
   eos_status st = EOS_OK;
   auto fail = [&](cudaError_t e) { if (st == EOS_OK && e != cudaSuccess) st = cuda_status(e); };
   fail(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));

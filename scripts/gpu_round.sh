@@ -115,6 +115,15 @@ if has guess; then
     done
   done
 fi
+if has hostpipe; then
+  for r in 1 2; do
+    for cfg in "2 23" "3 22" "4 22" "3 23" "4 21" "2 22"; do
+      set -- $cfg
+      EOS_HOST_SLOTS=$1 EOS_HOST_CHUNK_LOG2=$2 timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu --e2e-steps 20 > $OUT/hp.json 2>/dev/null
+      python -c "import json;d=json.load(open('$OUT/hp.json'));print('slots=$1 chunk=2^$2 e2e', d['e2e']['value'], d['e2e']['ms_per_step'])"
+    done
+  done
+fi
 if has exp; then
   timeout 900 python scripts/exp_search.py --workload cfg2 --ks 2,3,4,5,6,7,8 > $OUT/exp_cfg2.json 2> $OUT/exp_cfg2.err; echo "exp cfg2 rc=$?"
   timeout 900 python scripts/exp_search.py --workload cfg3 --steps 50 --ks 3,4,5,6,7,8 > $OUT/exp_cfg3.json 2> $OUT/exp_cfg3.err; echo "exp cfg3 rc=$?"
