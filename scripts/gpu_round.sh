@@ -124,6 +124,18 @@ if has hostpipe; then
     done
   done
 fi
+if has roll; then
+  for r in 1 2; do
+    for v in default static1024u4_roll1 static1024u4_roll2; do
+      EOS_SEARCH_VARIANT=$v timeout 600 python bench.py --workload cfg5 --steps 30 --warmup 3 --no-cpu --no-e2e > $OUT/roll.json 2>/dev/null
+      python -c "import json;d=json.load(open('$OUT/roll.json'));print('cfg5 $v', d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'])"
+    done
+    for v in default static256u4 static256u4_roll1 static512u4_roll1; do
+      EOS_SEARCH_VARIANT=$v timeout 600 python bench.py --workload cfg2 --steps 500 --warmup 5 --no-cpu --no-e2e > $OUT/roll.json 2>/dev/null
+      python -c "import json;d=json.load(open('$OUT/roll.json'));print('cfg2 $v', d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'])"
+    done
+  done
+fi
 if has exp; then
   timeout 900 python scripts/exp_search.py --workload cfg2 --ks 2,3,4,5,6,7,8 > $OUT/exp_cfg2.json 2> $OUT/exp_cfg2.err; echo "exp cfg2 rc=$?"
   timeout 900 python scripts/exp_search.py --workload cfg3 --steps 50 --ks 3,4,5,6,7,8 > $OUT/exp_cfg3.json 2> $OUT/exp_cfg3.err; echo "exp cfg3 rc=$?"
