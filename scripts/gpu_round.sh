@@ -191,7 +191,7 @@ if has ncufinal; then
     python scripts/ncu_summary.py $OUT/prof_final_$wl.ncu-rep > $OUT/ncu_summary_$wl.json
     ncu -i $OUT/prof_final_$wl.ncu-rep --page details --csv > $OUT/ncu_details_$wl.csv 2>/dev/null
     ncu -i $OUT/prof_final_$wl.ncu-rep --page raw --csv > $OUT/ncu_raw_$wl.csv 2>/dev/null
-    [ "$wl" != "cfg2" ] && rm -f $OUT/prof_final_$wl.ncu-rep
+    rm -f $OUT/prof_final_$wl.ncu-rep
   done
 fi
 if has ncu; then
