@@ -805,3 +805,97 @@ def test_interp_regular_axes_node_targets(axes, loglog):
     _check_deriv(dR.cpu().numpy(), dRr)
     _check_deriv(dT.cpu().numpy(), dTr)
     g.close()
+
+
+# --------------------------------------- streams, host threads, CUDA graphs --
+def test_concurrent_streams_and_host_threads_share_handles():
+    """Handles are immutable (eossearch.h): concurrent calls on one table / grid
+    from several host threads, each on its own stream, give the oracle's answers."""
+    import threading
+    w = datagen.workload("cfg2", count=1 << 20)
+    g4 = datagen.workload("cfg4", count=1 << 18)
+    tab = eos.Table(w.table)
+    big = eos.Table(datagen.table_big(6))
+    grid = eos.Grid2D(g4.rho, g4.T, g4.P)
+    jobs, errors = [], []
+    for j in range(6):
+        Y = w.targets.host_fill(j * w.count, w.count, w.table)
+        rho = g4.rho_targets.host_fill(j * g4.count, g4.count)
+        T = g4.T_targets.host_fill(j * g4.count, g4.count)
+        jobs.append((Y, rho, T))
+
+    def run(j):
+        try:
+            Y, rho, T = jobs[j]
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                yd, rd, td = to_dev(Y), to_dev(rho), to_dev(T)
+                outs = []
+                for _ in range(3):
+                    outs.append((tab.search(yd, stream=s), big.search(yd, stream=s),
+                                 grid.interp(rd, td, stream=s)))
+            s.synchronize()
+            ref = oracle.search(w.table, Y)
+            refb = oracle.search(big.X, Y)
+            Pr, iRr, iTr = oracle.interp2d(g4.rho, g4.T, g4.P, rho, T)
+            for a, b, (P, iR, iT) in outs:
+                assert_same(a.cpu().numpy(), ref, Y)
+                assert_same(b.cpu().numpy(), refb, Y)
+                assert np.array_equal(iR.cpu().numpy(), iRr) and np.array_equal(iT.cpu().numpy(), iTr)
+                check_interp(P.cpu().numpy(), Pr)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    th = [threading.Thread(target=run, args=(j,)) for j in range(len(jobs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors[0]
+    tab.close()
+    big.close()
+    grid.close()
+
+
+def test_cuda_graph_capture_and_replay():
+    """eos_search / eos_interp2d launches (programmatic dependent launch included)
+    captured into a CUDA graph and replayed over changing inputs."""
+    w = datagen.workload("cfg5", count=(1 << 20) + 3)
+    g4 = datagen.workload("cfg4", count=(1 << 18) + 1)
+    tab = eos.Table(w.table)
+    big = eos.Table(datagen.table_big(6))
+    grid = eos.Grid2D(g4.rho, g4.T, g4.P)
+    Yd = torch.empty(w.count, dtype=torch.float64, device=DEV)
+    Rd = torch.empty(g4.count, dtype=torch.float64, device=DEV)
+    Td = torch.empty(g4.count, dtype=torch.float64, device=DEV)
+    o1 = torch.empty(w.count, dtype=torch.int32, device=DEV)
+    o2 = torch.empty(w.count, dtype=torch.int32, device=DEV)
+    P = torch.empty(g4.count, dtype=torch.float64, device=DEV)
+    iR = torch.empty(g4.count, dtype=torch.int32, device=DEV)
+    iT = torch.empty(g4.count, dtype=torch.int32, device=DEV)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(2):
+            tab.search(Yd, out=o1, stream=s)
+            big.search(Yd, out=o2, stream=s)
+            grid.interp(Rd, Td, P_out=P, irho_out=iR, iT_out=iT, stream=s)
+    for rep in range(3):
+        Y = w.targets.host_fill(rep * w.count, w.count, w.table)
+        rho = g4.rho_targets.host_fill(rep * g4.count, g4.count)
+        T = g4.T_targets.host_fill(rep * g4.count, g4.count)
+        Yd.copy_(torch.from_numpy(Y))
+        Rd.copy_(torch.from_numpy(rho))
+        Td.copy_(torch.from_numpy(T))
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        assert_same(o1.cpu().numpy(), oracle.search(w.table, Y), Y)
+        assert_same(o2.cpu().numpy(), oracle.search(big.X, Y), Y)
+        Pr, iRr, iTr = oracle.interp2d(g4.rho, g4.T, g4.P, rho, T)
+        assert np.array_equal(iR.cpu().numpy(), iRr) and np.array_equal(iT.cpu().numpy(), iTr)
+        check_interp(P.cpu().numpy(), Pr)
+    tab.close()
+    big.close()
+    grid.close()
