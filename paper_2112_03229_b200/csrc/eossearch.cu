@@ -59,6 +59,8 @@ struct eos_grid2d_s {
   bool clc = true;
   int32_t flags = 0;
   int32_t wr_off = 0, wt_off = 0, lr_off = 0, lt_off = 0;
+  int32_t rr_off = 0, rt_off = 0;
+  bool rep = false;  // bank-pinned axis copies in the image (REP kernels)
 };
 
 namespace {
@@ -198,13 +200,15 @@ const void* interp_fn_s(int variant) {
     case 4: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, true>, false, false>;
     case 5: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, false>, true, false>;
     case 6: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 1, 1, false>, true, false>;
+    case 10: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, false, true>;
     default: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false>;
   }
 }
 
 template <int S>
-const void* interp_deriv_fn_s() {
-  return (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true>;
+const void* interp_deriv_fn_s(bool rep) {
+  return rep ? (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, false, true>
+             : (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true>;
 }
 
 template <int S>
@@ -220,10 +224,11 @@ struct Interp2DShape {
   bool clc;
 };
 
-// EOS_INTERP_VARIANT (tuning experiments only): 0 static1024u1 (default),
-// 1 static512u2, 2 static1024u2, 3 static512u4, 4 clc512u2,
-// 5 static512u2+recip, 6 static1024u1+recip.
-Interp2DShape pick_interp(int steps, bool loglog) {
+// EOS_INTERP_VARIANT (tuning experiments only): 0 static1024u1 (default
+// without bank-pinned axis copies), 1 static512u2, 2 static1024u2,
+// 3 static512u4, 4 clc512u2, 5 static512u2+recip, 6 static1024u1+recip,
+// 10 static1024u1 with the bank-pinned axis copies (default when they fit).
+Interp2DShape pick_interp(int steps, bool loglog, bool rep) {
   if (loglog) {
     const void *fn, *fd;
     switch (steps) {
@@ -235,20 +240,21 @@ Interp2DShape pick_interp(int steps, bool loglog) {
     }
     return {fn, fd, dv::Shape2D::kThreads, dv::Shape2D::kUnroll, dv::Shape2D::kClc};
   }
-  int v = 0;
+  int v = rep ? 10 : 0;
   if (const char* e = getenv("EOS_INTERP_VARIANT")) v = atoi(e);
-  static const int thr[7] = {1024, 512, 1024, 512, 512, 512, 1024};
-  static const int unr[7] = {1, 2, 2, 4, 2, 2, 1};
-  static const bool clc[7] = {false, false, false, false, true, false, false};
-  if (v < 0 || v > 6) v = 0;
+  static const int thr[11] = {1024, 512, 1024, 512, 512, 512, 1024, 0, 0, 0, 1024};
+  static const int unr[11] = {1, 2, 2, 4, 2, 2, 1, 0, 0, 0, 1};
+  static const bool clc[11] = {false, false, false, false, true, false, false,
+                               false, false, false, false};
+  if (v < 0 || v > 10 || thr[v] == 0 || (v == 10) != rep) v = rep ? 10 : 0;
   const void* fn;
   const void* fd;
   switch (steps) {
-    case 1: fn = interp_fn_s<1>(v); fd = interp_deriv_fn_s<1>(); break;
-    case 2: fn = interp_fn_s<2>(v); fd = interp_deriv_fn_s<2>(); break;
-    case 3: fn = interp_fn_s<3>(v); fd = interp_deriv_fn_s<3>(); break;
-    case 4: fn = interp_fn_s<4>(v); fd = interp_deriv_fn_s<4>(); break;
-    default: fn = interp_fn_s<0>(v); fd = interp_deriv_fn_s<0>(); break;
+    case 1: fn = interp_fn_s<1>(v); fd = interp_deriv_fn_s<1>(rep); break;
+    case 2: fn = interp_fn_s<2>(v); fd = interp_deriv_fn_s<2>(rep); break;
+    case 3: fn = interp_fn_s<3>(v); fd = interp_deriv_fn_s<3>(rep); break;
+    case 4: fn = interp_fn_s<4>(v); fd = interp_deriv_fn_s<4>(rep); break;
+    default: fn = interp_fn_s<0>(v); fd = interp_deriv_fn_s<0>(rep); break;
   }
   return {fn, fd, thr[v], unr[v], clc[v]};
 }
@@ -385,6 +391,8 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   a.wt_off = g->wt_off;
   a.lr_off = g->lr_off;
   a.lt_off = g->lt_off;
+  a.rr_off = g->rr_off;
+  a.rt_off = g->rt_off;
   a.r = g->ar;
   a.t = g->at;
   a.rho = rho;
@@ -781,7 +789,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     for (int64_t q = 0; q < ncell && ok; ++q) ok = P_host[q] > 0.0;
     if (!ok) { delete g; return EOS_ERR_UNSUPPORTED; }
   }
-  // image: [rho X | rho dir][T X | T dir][G][1/dR][1/dT]
+  // image: [rho X | rho dir][T X | T dir][G][1/dR][1/dT][ln R][ln T][R x16][T x16]
   const int64_t r_bytes = g->pr.image_bytes, t_bytes = g->pt.image_bytes;
   const int64_t g_bytes = (8 * ncell + 15) & ~int64_t(15);
   const int64_t wr_bytes = (8 * (n_rho - 1) + 15) & ~int64_t(15);
@@ -790,6 +798,15 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   const int64_t lt_bytes = loglog ? (8 * n_T + 15) & ~int64_t(15) : 0;
   g->image_bytes = r_bytes + t_bytes + g_bytes + wr_bytes + wt_bytes + lr_bytes + lt_bytes;
   if (g->image_bytes > 220 * 1024) { delete g; return EOS_ERR_UNSUPPORTED; }
+  // bank-pinned axis copies (kernels.cuh axis_cell REP): 16 x 8 B per axis
+  // entry, linear grids only, if the image still fits one CTA's shared memory
+  // (227 KB opt-in less the kernel's static smem).  EOS_INTERP_REP=0: off.
+  {
+    const char* e = getenv("EOS_INTERP_REP");
+    const int64_t rep_bytes = 128 * (n_rho + n_T);
+    g->rep = !loglog && !(e && e[0] == '0') && g->image_bytes + rep_bytes <= 226 * 1024;
+    if (g->rep) g->image_bytes += rep_bytes;
+  }
   std::vector<uint8_t> img((size_t)g->image_bytes, 0);
   std::vector<uint8_t> ir = eos::make_image(g->pr), it = eos::make_image(g->pt);
   memcpy(img.data(), ir.data(), ir.size());
@@ -799,6 +816,14 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   g->wt_off = (int32_t)(g->wr_off + wr_bytes);
   g->lr_off = (int32_t)(g->wt_off + wt_bytes);
   g->lt_off = (int32_t)(g->lr_off + lr_bytes);
+  g->rr_off = (int32_t)(g->lt_off + lt_bytes);
+  g->rt_off = (int32_t)(g->rr_off + (g->rep ? 128 * n_rho : 0));
+  if (g->rep) {  // Xr[16 j + c] = X[j]
+    for (int64_t q = 0; q < n_rho; ++q)
+      for (int c = 0; c < 16; ++c) memcpy(img.data() + g->rr_off + 8 * (16 * q + c), &g->pr.X[q], 8);
+    for (int64_t q = 0; q < n_T; ++q)
+      for (int c = 0; c < 16; ++c) memcpy(img.data() + g->rt_off + 8 * (16 * q + c), &g->pt.X[q], 8);
+  }
   if (loglog) {  // the grid holds ln G; ln of the axes follow the reciprocal widths
     for (int64_t q = 0; q < ncell; ++q) {
       const double v = log(P_host[q]);
@@ -830,7 +855,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   if (e != cudaSuccess) { delete g; return cuda_status(e); }
   st = upload(img, &g->image_dev);
   if (st != EOS_OK) { delete g; return st; }
-  Interp2DShape sh = pick_interp(std::max(g->pr.steps, g->pt.steps), loglog);
+  Interp2DShape sh = pick_interp(std::max(g->pr.steps, g->pt.steps), loglog, g->rep);
   g->fn = sh.fn;
   g->fn_deriv = sh.fn_deriv;
   g->threads = sh.threads;

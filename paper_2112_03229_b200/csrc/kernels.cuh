@@ -692,6 +692,8 @@ struct Interp2DArgs {
   int32_t wt_off;   // byte offset of 1/(T[j+1]-T[j]) fp64[nT-1] (RECIP variant)
   int32_t lr_off;   // byte offset of ln R fp64[nR] (LOGLOG grids)
   int32_t lt_off;   // byte offset of ln T fp64[nT] (LOGLOG grids)
+  int32_t rr_off;   // byte offset of the bank-pinned copies of R: fp64[16 nR] (REP kernels)
+  int32_t rt_off;   // byte offset of the bank-pinned copies of T: fp64[16 nT] (REP kernels)
   int32_t vec_ok;
   int32_t pad_;
   int64_t ntiles;
@@ -721,30 +723,40 @@ __device__ __forceinline__ double clamp01(double t) {
 // ci = min(i, n-2) and its endpoints X[ci], X[ci+1].  With S = 1 (every bin
 // holds at most one entry) the in-bin probe value X[lo] is always one of the
 // two endpoints in the common case, so only one more gather is needed.
-template <int S>
+//
+// REP (bank-pinned axis copies): the axis values are also stored 16 times,
+// Xr[16 j + c] = X[j], so copy c lies entirely in bank pair c (an fp64 at
+// double index d sits in banks 2(d mod 16), 2(d mod 16) + 1).  A 64-bit
+// shared load is served per half-warp; lane l reads copy l mod 16, so the 16
+// lanes of a half-warp always hit 16 different bank pairs: the random
+// endpoint gathers become conflict-free (2 wavefronts per warp instead of
+// ~5.6 measured).  xr_ points at copy (lane mod 16).
+template <int S, bool REP = false>
 __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ sX,
                                           const uint32_t* __restrict__ sD, const AxisParams& a,
-                                          int32_t& i, int32_t& ci, double& xl, double& xr) {
+                                          int32_t& i, int32_t& ci, double& xl, double& xr,
+                                          const double* __restrict__ xr_ = nullptr) {
+  auto X = [&](int32_t j) { return REP ? xr_[16 * j] : sX[j]; };
   if (S == 1) {
     const uint32_t key = a.mode ? key_hi<1>(y) : key_hi<0>(y);
     const uint32_t d = sD[bin_of(key, a)];
     const int32_t lo = (int32_t)(d & 0xFFFFu);  // <= n-1: X[n-1] lies in the top bin
     const int32_t occ = (int32_t)(d >> 16);     // 0 or 1 when S == 1
     EOS_DCHECK(lo < a.n && occ <= 1);
-    const double pv = sX[lo];
+    const double pv = X(lo);
     const int32_t c = (occ >= 1 && pv <= y) ? 1 : 0;
     i = (y >= a.x0) ? lo + c - 1 : 0;
     ci = min(i, a.n - 2);
     const bool left = (ci == lo), right = (ci + 1 == lo);
-    const double ov = sX[left ? lo + 1 : (right ? lo - 1 : ci)];
+    const double ov = X(left ? lo + 1 : (right ? lo - 1 : ci));
     xl = left ? pv : ov;
-    xr = left ? ov : (right ? pv : sX[ci + 1]);
+    xr = left ? ov : (right ? pv : X(ci + 1));
     EOS_DCHECK(ci >= 0 && ci + 1 < a.n && (left ? lo + 1 : (right ? lo - 1 : ci)) < a.n);
   } else {
     i = a.mode ? lookup<S, 1>(y, sX, sD, a) : lookup<S, 0>(y, sX, sD, a);
     ci = min(i, a.n - 2);
-    xl = sX[ci];
-    xr = sX[ci + 1];
+    xl = X(ci);
+    xr = X(ci + 1);
   }
 }
 
@@ -754,7 +766,7 @@ __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ s
 // of that formula (bit-identical to a plain evaluation in that order).
 // RECIP: weights as (x - X[c]) * (1/(X[c+1]-X[c])) with the reciprocal
 // precomputed at create (a few ulp from the divide; within the 1e-12 bar).
-template <int S, bool RECIP, bool DERIV, bool LOGLOG>
+template <int S, bool RECIP, bool DERIV, bool LOGLOG, bool REP>
 __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, int32_t& j,
                                              double& dpr, double& dpt, const char* sm,
                                              const Interp2DArgs& A) {
@@ -765,8 +777,16 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   const double* sG = reinterpret_cast<const double*>(sm + A.g_off);  // G, or ln G (LOGLOG)
   int32_t ci, cj;
   double r0, r1, t0, t1;
-  axis_cell<S>(rho, sR, dR, A.r, i, ci, r0, r1);
-  axis_cell<S>(T, sT, dT, A.t, j, cj, t0, t1);
+  if (REP) {
+    const int32_t c = threadIdx.x & 15;  // the copy of this lane (bank pair c)
+    axis_cell<S, true>(rho, sR, dR, A.r, i, ci, r0, r1,
+                       reinterpret_cast<const double*>(sm + A.rr_off) + c);
+    axis_cell<S, true>(T, sT, dT, A.t, j, cj, t0, t1,
+                       reinterpret_cast<const double*>(sm + A.rt_off) + c);
+  } else {
+    axis_cell<S>(rho, sR, dR, A.r, i, ci, r0, r1);
+    axis_cell<S>(T, sT, dT, A.t, j, cj, t0, t1);
+  }
   double xr = rho, xt = T;  // interpolation coordinates
   if (LOGLOG) {             // R24: ln P bilinear in (ln rho, ln T)
     const double* lR = reinterpret_cast<const double*>(sm + A.lr_off);
@@ -824,7 +844,7 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
 using Shape2D = Shape<1024, 1, 1, false>;
 using Shape2DDeriv = Shape<512, 1, 1, false>;  // derivative outputs need > 64 registers
 
-template <int S, class SH, bool RECIP, bool DERIV, bool LOGLOG = false>
+template <int S, class SH, bool RECIP, bool DERIV, bool LOGLOG = false, bool REP = false>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {
   constexpr int T = SH::kThreads;
   constexpr int U = SH::kUnroll;
@@ -883,9 +903,9 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       int2 ir[U], it[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        p[u].x = interp_one<S, RECIP, DERIV, LOGLOG>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
+        p[u].x = interp_one<S, RECIP, DERIV, LOGLOG, REP>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
                                              sm, A);
-        p[u].y = interp_one<S, RECIP, DERIV, LOGLOG>(vr[u].y, vt[u].y, ir[u].y, it[u].y, dr[u].y, dt[u].y,
+        p[u].y = interp_one<S, RECIP, DERIV, LOGLOG, REP>(vr[u].y, vt[u].y, ir[u].y, it[u].y, dr[u].y, dt[u].y,
                                              sm, A);
       }
       tn = next_tile(t);
@@ -910,7 +930,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       for (int64_t q = e0 + threadIdx.x; q < e1; q += T) {
         int32_t i, j;
         double dpr, dpt;
-        const double pq = interp_one<S, RECIP, DERIV, LOGLOG>(A.rho[q], A.T[q], i, j, dpr, dpt, sm, A);
+        const double pq = interp_one<S, RECIP, DERIV, LOGLOG, REP>(A.rho[q], A.T[q], i, j, dpr, dpt, sm, A);
         A.P[q] = pq;
         if (br) A.iR[q] = i;
         if (bt) A.iT[q] = j;

@@ -136,6 +136,26 @@ if has roll; then
     done
   done
 fi
+if has rep; then
+  timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "interp or smoke or loglog or graph or concurrent" > $OUT/pytest_rep.log 2>&1; echo "pytest interp (rep) rc=$?"; tail -n 3 $OUT/pytest_rep.log
+  EOS_INTERP_REP=0 timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "interp" > $OUT/pytest_norep.log 2>&1; echo "pytest interp (no rep) rc=$?"; tail -n 2 $OUT/pytest_norep.log
+  for r in 1 2; do
+    for rp in 1 0; do
+      for fl in "" "--derivatives"; do
+        EOS_INTERP_REP=$rp timeout 600 python bench.py --workload cfg4 $fl --steps 200 --warmup 5 --no-cpu --no-e2e > $OUT/r4.json 2>/dev/null
+        python -c "import json;d=json.load(open('$OUT/r4.json'));print('cfg4 rep=$rp [$fl]', d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'])"
+      done
+    done
+  done
+  CMD="python bench.py --workload cfg4 --count 268435456 --steps 5 --warmup 2 --no-e2e --no-cpu --eager"
+  $CMD > $OUT/ncu_plain_rep.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:interp2d -s 2 -c 1 \
+      -o $OUT/prof_rep -f $CMD > $OUT/ncu_full_rep.log 2>&1; echo "ncu rep rc=$?"
+  python scripts/ncu_summary.py $OUT/prof_rep.ncu-rep > $OUT/ncu_summary_rep.json
+  ncu -i $OUT/prof_rep.ncu-rep --page details --csv > $OUT/ncu_details_rep.csv 2>/dev/null
+  ncu -i $OUT/prof_rep.ncu-rep --page source --csv > $OUT/ncu_source_rep.csv 2>/dev/null
+  rm -f $OUT/prof_rep.ncu-rep
+fi
 if has exp; then
   timeout 900 python scripts/exp_search.py --workload cfg2 --ks 2,3,4,5,6,7,8 > $OUT/exp_cfg2.json 2> $OUT/exp_cfg2.err; echo "exp cfg2 rc=$?"
   timeout 900 python scripts/exp_search.py --workload cfg3 --steps 50 --ks 3,4,5,6,7,8 > $OUT/exp_cfg3.json 2> $OUT/exp_cfg3.err; echo "exp cfg3 rc=$?"
