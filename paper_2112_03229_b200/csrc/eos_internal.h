@@ -61,8 +61,11 @@ constexpr int64_t kMaxImage = 200 * 1024;  // explicit requests beyond this do n
 // Validate + build (eos_plan_table_hash semantics).  kind/param: see
 // eossearch.h (EOS_HASH_AUTO ignores param).  strict: axes of a 2-D grid must
 // be strictly increasing and n >= 2.
+// fill_budget (grid axes only, strict): if > 0, among the automatic hash
+// candidates with the smallest S take the one with the most bins whose image
+// fits fill_budget bytes (instead of the smallest image).
 eos_status plan_table(const double* X, int64_t n, int kind, int64_t param, bool strict,
-                      TablePlan* out);
+                      TablePlan* out, int64_t fill_budget = 0);
 
 // Tables larger than shared memory (eossearch.h
 // eos_search_create_levels).  D 8-ary levels in global memory under a

@@ -60,7 +60,7 @@ struct eos_grid2d_s {
   int32_t flags = 0;
   int32_t wr_off = 0, wt_off = 0, lr_off = 0, lt_off = 0;
   int32_t rr_off = 0, rt_off = 0;
-  bool rep = false;  // bank-pinned axis copies in the image (REP kernels)
+  int rep = 0;  // bank-pinned axis layout in the image (REP kernels): 0 none, 1 copies, 2 records
 };
 
 namespace {
@@ -200,15 +200,19 @@ const void* interp_fn_s(int variant) {
     case 4: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, true>, false, false>;
     case 5: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, false>, true, false>;
     case 6: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 1, 1, false>, true, false>;
-    case 10: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, false, true>;
+    case 10: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, false, 1>;
+    case 11: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, false, 2>;
     default: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false>;
   }
 }
 
 template <int S>
-const void* interp_deriv_fn_s(bool rep) {
-  return rep ? (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, false, true>
-             : (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true>;
+const void* interp_deriv_fn_s(int rep) {
+  switch (rep) {
+    case 1: return (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, false, 1>;
+    case 2: return (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, false, 2>;
+    default: return (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true>;
+  }
 }
 
 template <int S>
@@ -227,8 +231,9 @@ struct Interp2DShape {
 // EOS_INTERP_VARIANT (tuning experiments only): 0 static1024u1 (default
 // without bank-pinned axis copies), 1 static512u2, 2 static1024u2,
 // 3 static512u4, 4 clc512u2, 5 static512u2+recip, 6 static1024u1+recip,
-// 10 static1024u1 with the bank-pinned axis copies (default when they fit).
-Interp2DShape pick_interp(int steps, bool loglog, bool rep) {
+// 10 static1024u1 with bank-pinned axis copies (REP 1), 11 static1024u1 with
+// bank-pinned cell records (REP 2, the default when they fit).
+Interp2DShape pick_interp(int steps, bool loglog, int rep) {
   if (loglog) {
     const void *fn, *fd;
     switch (steps) {
@@ -240,13 +245,15 @@ Interp2DShape pick_interp(int steps, bool loglog, bool rep) {
     }
     return {fn, fd, dv::Shape2D::kThreads, dv::Shape2D::kUnroll, dv::Shape2D::kClc};
   }
-  int v = rep ? 10 : 0;
+  const int vdef = rep == 2 ? 11 : (rep == 1 ? 10 : 0);
+  int v = vdef;
   if (const char* e = getenv("EOS_INTERP_VARIANT")) v = atoi(e);
-  static const int thr[11] = {1024, 512, 1024, 512, 512, 512, 1024, 0, 0, 0, 1024};
-  static const int unr[11] = {1, 2, 2, 4, 2, 2, 1, 0, 0, 0, 1};
-  static const bool clc[11] = {false, false, false, false, true, false, false,
-                               false, false, false, false};
-  if (v < 0 || v > 10 || thr[v] == 0 || (v == 10) != rep) v = rep ? 10 : 0;
+  static const int thr[12] = {1024, 512, 1024, 512, 512, 512, 1024, 0, 0, 0, 1024, 1024};
+  static const int unr[12] = {1, 2, 2, 4, 2, 2, 1, 0, 0, 0, 1, 1};
+  static const bool clc[12] = {false, false, false, false, true, false, false,
+                               false, false, false, false, false};
+  // variants 10/11 need the image of the matching REP layout
+  if (v < 0 || v > 11 || thr[v] == 0 || (v >= 10 && v != vdef)) v = vdef;
   const void* fn;
   const void* fd;
   switch (steps) {
@@ -790,7 +797,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     if (!ok) { delete g; return EOS_ERR_UNSUPPORTED; }
   }
   // image: [rho X | rho dir][T X | T dir][G][1/dR][1/dT][ln R][ln T][R x16][T x16]
-  const int64_t r_bytes = g->pr.image_bytes, t_bytes = g->pt.image_bytes;
+  int64_t r_bytes = g->pr.image_bytes, t_bytes = g->pt.image_bytes;
   const int64_t g_bytes = (8 * ncell + 15) & ~int64_t(15);
   const int64_t wr_bytes = (8 * (n_rho - 1) + 15) & ~int64_t(15);
   const int64_t wt_bytes = (8 * (n_T - 1) + 15) & ~int64_t(15);
@@ -802,10 +809,29 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   // entry, linear grids only, if the image still fits one CTA's shared memory
   // (227 KB opt-in less the kernel's static smem).  EOS_INTERP_REP=0: off.
   {
-    const char* e = getenv("EOS_INTERP_REP");
-    const int64_t rep_bytes = 128 * (n_rho + n_T);
-    g->rep = !loglog && !(e && e[0] == '0') && g->image_bytes + rep_bytes <= 226 * 1024;
+    const char* e = getenv("EOS_INTERP_REP");  // 0, 1 or 2 (default 2)
+    const int want = e ? std::max(0, std::min(2, atoi(e))) : 2;
+    const int64_t rep_bytes = 128 * (n_rho + n_T);  // both layouts: 128 B per axis entry
+    g->rep = (!loglog && want > 0 && g->image_bytes + rep_bytes <= 226 * 1024) ? want : 0;
     if (g->rep) g->image_bytes += rep_bytes;
+    // REP 2: spend the rest of the shared memory on sparser axis directories
+    // (split by axis length), so that the second record read is rare
+    const int64_t spare = 226 * 1024 - g->image_bytes - 512;
+    if (g->rep == 2 && spare > 1024) {
+      const int64_t avail = r_bytes + t_bytes + spare;
+      const int64_t br = avail * n_rho / (n_rho + n_T), bt = avail - br;
+      eos::TablePlan pr, pt;
+      if (eos::plan_table(rho_host, n_rho, EOS_HASH_AUTO, 0, true, &pr, br) == EOS_OK &&
+          eos::plan_table(T_host, n_T, EOS_HASH_AUTO, 0, true, &pt, bt) == EOS_OK &&
+          pr.steps <= g->pr.steps && pt.steps <= g->pt.steps &&
+          pr.image_bytes + pt.image_bytes <= avail) {
+        g->image_bytes += pr.image_bytes + pt.image_bytes - r_bytes - t_bytes;
+        g->pr = std::move(pr);
+        g->pt = std::move(pt);
+        r_bytes = g->pr.image_bytes;
+        t_bytes = g->pt.image_bytes;
+      }
+    }
   }
   std::vector<uint8_t> img((size_t)g->image_bytes, 0);
   std::vector<uint8_t> ir = eos::make_image(g->pr), it = eos::make_image(g->pt);
@@ -818,11 +844,20 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   g->lt_off = (int32_t)(g->lr_off + lr_bytes);
   g->rr_off = (int32_t)(g->lt_off + lt_bytes);
   g->rt_off = (int32_t)(g->rr_off + (g->rep ? 128 * n_rho : 0));
-  if (g->rep) {  // Xr[16 j + c] = X[j]
-    for (int64_t q = 0; q < n_rho; ++q)
-      for (int c = 0; c < 16; ++c) memcpy(img.data() + g->rr_off + 8 * (16 * q + c), &g->pr.X[q], 8);
-    for (int64_t q = 0; q < n_T; ++q)
-      for (int c = 0; c < 16; ++c) memcpy(img.data() + g->rt_off + 8 * (16 * q + c), &g->pt.X[q], 8);
+  auto put_rep = [&](const std::vector<double>& X, int32_t off) {
+    const int64_t n = (int64_t)X.size();
+    for (int64_t q = 0; q < n; ++q) {
+      if (g->rep == 1) {  // Xr[16 q + c] = X[q]
+        for (int c = 0; c < 16; ++c) memcpy(img.data() + off + 8 * (16 * q + c), &X[q], 8);
+      } else {  // Rec[8 q + c] = (X[q], 1/(X[q+1] - X[q])); the last record's width is unused
+        const double rec[2] = {X[q], q + 1 < n ? 1.0 / (X[q + 1] - X[q]) : 0.0};
+        for (int c = 0; c < 8; ++c) memcpy(img.data() + off + 16 * (8 * q + c), rec, 16);
+      }
+    }
+  };
+  if (g->rep) {
+    put_rep(g->pr.X, g->rr_off);
+    put_rep(g->pt.X, g->rt_off);
   }
   if (loglog) {  // the grid holds ln G; ln of the axes follow the reciprocal widths
     for (int64_t q = 0; q < ncell; ++q) {

@@ -692,8 +692,9 @@ struct Interp2DArgs {
   int32_t wt_off;   // byte offset of 1/(T[j+1]-T[j]) fp64[nT-1] (RECIP variant)
   int32_t lr_off;   // byte offset of ln R fp64[nR] (LOGLOG grids)
   int32_t lt_off;   // byte offset of ln T fp64[nT] (LOGLOG grids)
-  int32_t rr_off;   // byte offset of the bank-pinned copies of R: fp64[16 nR] (REP kernels)
-  int32_t rt_off;   // byte offset of the bank-pinned copies of T: fp64[16 nT] (REP kernels)
+  int32_t rr_off;   // byte offset of the bank-pinned copies of the R axis (REP kernels):
+                    //   REP 1: fp64[16 nR], REP 2: double2[8 nR] records (R[j], 1/(R[j+1]-R[j]))
+  int32_t rt_off;   // the same for the T axis
   int32_t vec_ok;
   int32_t pad_;
   int64_t ntiles;
@@ -760,13 +761,50 @@ __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ s
   }
 }
 
+// REP 2 (bank-pinned cell records): 16-byte records Rec[8 j + c] =
+// (X[j], 1/(X[j+1] - X[j])), 8 copies, copy c in bank quad c.  A 128-bit
+// shared load is served per quarter-warp, and lane l reads copy l mod 8, so
+// the gathers are conflict-free (4 wavefronts per warp).  One record gives
+// the cell's left endpoint and inverse width, so the interpolation weight
+// needs no fp64 divide: t = (x - X[ci]) * (1/dX[ci]) (a few ulp from the
+// divide; within the 1e-12 bar).  With S = 1: the first record is that of
+// the bin's entry (occ = 1, also the probe) or of the cell left of the bin
+// (occ = 0, then it is the cell); a second record is read only when the
+// probe moves the cell.
+template <int S>
+__device__ __forceinline__ void axis_cell_rec(double y, const double* __restrict__ sX,
+                                              const uint32_t* __restrict__ sD, const AxisParams& a,
+                                              int32_t& i, int32_t& ci, double& xl, double& inv,
+                                              const double2* __restrict__ rec_) {
+  double2 r;
+  int32_t p;
+  if (S == 1) {
+    const uint32_t key = a.mode ? key_hi<1>(y) : key_hi<0>(y);
+    const uint32_t d = sD[bin_of(key, a)];
+    const int32_t lo = (int32_t)(d & 0xFFFFu);  // <= n-1
+    const int32_t occ = (int32_t)(d >> 16);     // 0 or 1
+    p = occ >= 1 ? lo : max(lo - 1, 0);
+    EOS_DCHECK(lo < a.n && occ <= 1 && p < a.n);
+    r = rec_[8 * p];
+    const int32_t c = (occ >= 1 && r.x <= y) ? 1 : 0;
+    i = (y >= a.x0) ? lo + c - 1 : 0;
+  } else {
+    i = a.mode ? lookup<S, 1>(y, sX, sD, a) : lookup<S, 0>(y, sX, sD, a);
+    p = -1;
+  }
+  ci = min(i, a.n - 2);
+  if (ci != p) r = rec_[8 * ci];
+  xl = r.x;
+  inv = r.y;
+}
+
 // Bilinear on the bracket cell (R14).  Written with explicit
 // round-to-nearest intrinsics (no FMA contraction), in the order of the
 // formula in eossearch.h, so the value is the correctly-rounded evaluation
 // of that formula (bit-identical to a plain evaluation in that order).
 // RECIP: weights as (x - X[c]) * (1/(X[c+1]-X[c])) with the reciprocal
 // precomputed at create (a few ulp from the divide; within the 1e-12 bar).
-template <int S, bool RECIP, bool DERIV, bool LOGLOG, bool REP>
+template <int S, bool RECIP, bool DERIV, bool LOGLOG, int REP>
 __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, int32_t& j,
                                              double& dpr, double& dpt, const char* sm,
                                              const Interp2DArgs& A) {
@@ -777,7 +815,15 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   const double* sG = reinterpret_cast<const double*>(sm + A.g_off);  // G, or ln G (LOGLOG)
   int32_t ci, cj;
   double r0, r1, t0, t1;
-  if (REP) {
+  double ir = 0.0, it = 0.0;  // REP 2: inverse cell widths
+  if (REP == 2) {
+    const int32_t c = threadIdx.x & 7;  // the copy of this lane (bank quad c)
+    axis_cell_rec<S>(rho, sR, dR, A.r, i, ci, r0, ir,
+                     reinterpret_cast<const double2*>(sm + A.rr_off) + c);
+    axis_cell_rec<S>(T, sT, dT, A.t, j, cj, t0, it,
+                     reinterpret_cast<const double2*>(sm + A.rt_off) + c);
+    r1 = t1 = 0.0;  // unused
+  } else if (REP == 1) {
     const int32_t c = threadIdx.x & 15;  // the copy of this lane (bank pair c)
     axis_cell<S, true>(rho, sR, dR, A.r, i, ci, r0, r1,
                        reinterpret_cast<const double*>(sm + A.rr_off) + c);
@@ -799,7 +845,10 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
     xt = log(T);
   }
   double tx, ty;
-  if (RECIP && !LOGLOG) {
+  if (REP == 2 && !LOGLOG) {
+    tx = clamp01(__dmul_rn(__dsub_rn(xr, r0), ir));
+    ty = clamp01(__dmul_rn(__dsub_rn(xt, t0), it));
+  } else if (RECIP && !LOGLOG) {
     const double* wR = reinterpret_cast<const double*>(sm + A.wr_off);
     const double* wT = reinterpret_cast<const double*>(sm + A.wt_off);
     tx = clamp01(__dmul_rn(__dsub_rn(xr, r0), wR[ci]));
@@ -822,12 +871,10 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
     // Partial derivatives of the interpolant on the cell (R23 / R24); 0
     // outside an axis range (the clamped interpolant is constant there); NaN
     // kept.  LOGLOG: dP/drho = P * (d ln P / d ln rho) / rho.
-    const double sr = __ddiv_rn(__dadd_rn(__dmul_rn(uy, __dsub_rn(g10, g00)),
-                                          __dmul_rn(ty, __dsub_rn(g11, g01))),
-                                __dsub_rn(r1, r0));
-    const double st = __ddiv_rn(__dadd_rn(__dmul_rn(ux, __dsub_rn(g01, g00)),
-                                          __dmul_rn(tx, __dsub_rn(g11, g10))),
-                                __dsub_rn(t1, t0));
+    const double nr = __dadd_rn(__dmul_rn(uy, __dsub_rn(g10, g00)), __dmul_rn(ty, __dsub_rn(g11, g01)));
+    const double nt = __dadd_rn(__dmul_rn(ux, __dsub_rn(g01, g00)), __dmul_rn(tx, __dsub_rn(g11, g10)));
+    const double sr = REP == 2 ? __dmul_rn(nr, ir) : __ddiv_rn(nr, __dsub_rn(r1, r0));
+    const double st = REP == 2 ? __dmul_rn(nt, it) : __ddiv_rn(nt, __dsub_rn(t1, t0));
     const bool in_r = rho >= A.r.x0 && rho <= A.r.xlast;
     const bool in_t = T >= A.t.x0 && T <= A.t.xlast;
     const double dr = LOGLOG ? __ddiv_rn(__dmul_rn(p, sr), rho) : sr;
@@ -844,7 +891,7 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
 using Shape2D = Shape<1024, 1, 1, false>;
 using Shape2DDeriv = Shape<512, 1, 1, false>;  // derivative outputs need > 64 registers
 
-template <int S, class SH, bool RECIP, bool DERIV, bool LOGLOG = false, bool REP = false>
+template <int S, class SH, bool RECIP, bool DERIV, bool LOGLOG = false, int REP = 0>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {
   constexpr int T = SH::kThreads;
   constexpr int U = SH::kUnroll;

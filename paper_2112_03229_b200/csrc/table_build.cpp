@@ -162,9 +162,14 @@ double plan_cost(const TablePlan& p) {
 // 2-D kernel's smem is dominated by the grid and its S = 1 cell lookup reads
 // the probe unconditionally (kernels.cuh::axis_cell), so bigger directories
 // buy nothing there.
-eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, TablePlan* out) {
+// fill_budget > 0 (grid axes of REP 2 kernels, eossearch.cu): the smallest S,
+// then the MOST bins within fill_budget bytes -- there a sparser directory
+// makes the second cell-record read rarer (kernels.cuh axis_cell_rec).
+eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, TablePlan* out,
+                     int64_t fill_budget = 0) {
   const int64_t n = (int64_t)X.size();
-  const int64_t budget = compact ? kAxisImageBudget : kAutoImageBudget;
+  const bool fill = compact && fill_budget > 0;
+  const int64_t budget = fill ? fill_budget : (compact ? kAxisImageBudget : kAutoImageBudget);
   TablePlan best;
   double best_cost = 0.0;
   bool have = false;
@@ -174,8 +179,9 @@ eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, Table
     TablePlan p;
     if (build(X, mode, h, &p) != EOS_OK) return;
     const double c = compact ? (double)p.steps : plan_cost(p);
-    if (!have || c < best_cost - 1e-9 ||
-        (c < best_cost + 1e-9 && p.image_bytes < best.image_bytes)) {
+    if (have && fill && p.image_bytes > budget) return;
+    const bool tie_better = fill ? p.image_bytes > best.image_bytes : p.image_bytes < best.image_bytes;
+    if (!have || c < best_cost - 1e-9 || (c < best_cost + 1e-9 && tie_better)) {
       best = std::move(p);
       best_cost = c;
       have = true;
@@ -198,7 +204,7 @@ eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, Table
 }  // namespace
 
 eos_status plan_table(const double* Xin, int64_t n, int kind, int64_t param, bool strict,
-                      TablePlan* out) {
+                      TablePlan* out, int64_t fill_budget) {
   if (!Xin || !out) return EOS_ERR_NULL;
   if (n < (strict ? 2 : 1) || n > EOS_MAX_TABLE) return EOS_ERR_SIZE;
   if (kind == EOS_HASH_EXPONENT && (param < 0 || param > EOS_MAX_K)) return EOS_ERR_UNSUPPORTED;
@@ -219,7 +225,7 @@ eos_status plan_table(const double* Xin, int64_t n, int kind, int64_t param, boo
   TablePlan p;
   eos_status st;
   if (kind == EOS_HASH_AUTO) {
-    st = plan_auto(X, mode, strict, &p);
+    st = plan_auto(X, mode, strict, &p, fill_budget);
   } else {
     const HashParams h = kind == EOS_HASH_EXPONENT ? exponent_params(X, mode, (int)param)
                                                    : log_params(X, mode, param);
