@@ -216,7 +216,10 @@ const void* interp_deriv_fn_s(int rep) {
 }
 
 template <int S>
-const void* interp_loglog_fn_s(bool deriv) {
+const void* interp_loglog_fn_s(bool deriv, bool rep) {
+  if (rep)
+    return deriv ? (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, true, 2>
+                 : (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, true, 2>;
   return deriv ? (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, true>
                : (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, true>;
 }
@@ -236,12 +239,13 @@ struct Interp2DShape {
 Interp2DShape pick_interp(int steps, bool loglog, int rep) {
   if (loglog) {
     const void *fn, *fd;
+    const bool r2 = rep == 2;
     switch (steps) {
-      case 1: fn = interp_loglog_fn_s<1>(false); fd = interp_loglog_fn_s<1>(true); break;
-      case 2: fn = interp_loglog_fn_s<2>(false); fd = interp_loglog_fn_s<2>(true); break;
-      case 3: fn = interp_loglog_fn_s<3>(false); fd = interp_loglog_fn_s<3>(true); break;
-      case 4: fn = interp_loglog_fn_s<4>(false); fd = interp_loglog_fn_s<4>(true); break;
-      default: fn = interp_loglog_fn_s<0>(false); fd = interp_loglog_fn_s<0>(true); break;
+      case 1: fn = interp_loglog_fn_s<1>(false, r2); fd = interp_loglog_fn_s<1>(true, r2); break;
+      case 2: fn = interp_loglog_fn_s<2>(false, r2); fd = interp_loglog_fn_s<2>(true, r2); break;
+      case 3: fn = interp_loglog_fn_s<3>(false, r2); fd = interp_loglog_fn_s<3>(true, r2); break;
+      case 4: fn = interp_loglog_fn_s<4>(false, r2); fd = interp_loglog_fn_s<4>(true, r2); break;
+      default: fn = interp_loglog_fn_s<0>(false, r2); fd = interp_loglog_fn_s<0>(true, r2); break;
     }
     return {fn, fd, dv::Shape2D::kThreads, dv::Shape2D::kUnroll, dv::Shape2D::kClc};
   }
@@ -812,12 +816,14 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     const char* e = getenv("EOS_INTERP_REP");  // 0, 1 or 2 (default 2)
     const int want = e ? std::max(0, std::min(2, atoi(e))) : 2;
     const int64_t rep_bytes = 128 * (n_rho + n_T);  // both layouts: 128 B per axis entry
-    g->rep = (!loglog && want > 0 && g->image_bytes + rep_bytes <= 226 * 1024) ? want : 0;
+    // log-log grids: records of the log axes (REP 2 only)
+    const int w = loglog ? (want == 2 ? 2 : 0) : want;
+    g->rep = (w > 0 && g->image_bytes + rep_bytes <= 226 * 1024) ? w : 0;
     if (g->rep) g->image_bytes += rep_bytes;
     // REP 2: spend the rest of the shared memory on sparser axis directories
     // (split by axis length), so that the second record read is rare
     const int64_t spare = 226 * 1024 - g->image_bytes - 512;
-    if (g->rep == 2 && spare > 1024) {
+    if (g->rep == 2 && !loglog && spare > 1024) {
       const int64_t avail = r_bytes + t_bytes + spare;
       const int64_t br = avail * n_rho / (n_rho + n_T), bt = avail - br;
       eos::TablePlan pr, pt;
@@ -844,7 +850,10 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   g->lt_off = (int32_t)(g->lr_off + lr_bytes);
   g->rr_off = (int32_t)(g->lt_off + lt_bytes);
   g->rt_off = (int32_t)(g->rr_off + (g->rep ? 128 * n_rho : 0));
-  auto put_rep = [&](const std::vector<double>& X, int32_t off) {
+  auto put_rep = [&](const std::vector<double>& Xa, int32_t off) {
+    std::vector<double> X(Xa);
+    if (loglog)  // records of the log axis (the same host log as the ln R / ln T arrays)
+      for (double& v : X) v = log(v);
     const int64_t n = (int64_t)X.size();
     for (int64_t q = 0; q < n; ++q) {
       if (g->rep == 1) {  // Xr[16 q + c] = X[q]

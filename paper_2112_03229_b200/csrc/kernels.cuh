@@ -816,7 +816,19 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   int32_t ci, cj;
   double r0, r1, t0, t1;
   double ir = 0.0, it = 0.0;  // REP 2: inverse cell widths
-  if (REP == 2) {
+  if (REP == 2 && LOGLOG) {
+    // brackets from the plain axes; the cell records hold the log axes:
+    // (ln X[j], 1/(ln X[j+1] - ln X[j]))
+    axis_cell<S>(rho, sR, dR, A.r, i, ci, r0, r1);
+    axis_cell<S>(T, sT, dT, A.t, j, cj, t0, t1);
+    const int32_t c = threadIdx.x & 7;
+    const double2 er = reinterpret_cast<const double2*>(sm + A.rr_off)[8 * ci + c];
+    const double2 et = reinterpret_cast<const double2*>(sm + A.rt_off)[8 * cj + c];
+    r0 = er.x;
+    ir = er.y;
+    t0 = et.x;
+    it = et.y;
+  } else if (REP == 2) {
     const int32_t c = threadIdx.x & 7;  // the copy of this lane (bank quad c)
     axis_cell_rec<S>(rho, sR, dR, A.r, i, ci, r0, ir,
                      reinterpret_cast<const double2*>(sm + A.rr_off) + c);
@@ -835,17 +847,19 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   }
   double xr = rho, xt = T;  // interpolation coordinates
   if (LOGLOG) {             // R24: ln P bilinear in (ln rho, ln T)
-    const double* lR = reinterpret_cast<const double*>(sm + A.lr_off);
-    const double* lT = reinterpret_cast<const double*>(sm + A.lt_off);
-    r0 = lR[ci];
-    r1 = lR[ci + 1];
-    t0 = lT[cj];
-    t1 = lT[cj + 1];
+    if (REP != 2) {
+      const double* lR = reinterpret_cast<const double*>(sm + A.lr_off);
+      const double* lT = reinterpret_cast<const double*>(sm + A.lt_off);
+      r0 = lR[ci];
+      r1 = lR[ci + 1];
+      t0 = lT[cj];
+      t1 = lT[cj + 1];
+    }
     xr = log(rho);
     xt = log(T);
   }
   double tx, ty;
-  if (REP == 2 && !LOGLOG) {
+  if (REP == 2) {
     tx = clamp01(__dmul_rn(__dsub_rn(xr, r0), ir));
     ty = clamp01(__dmul_rn(__dsub_rn(xt, t0), it));
   } else if (RECIP && !LOGLOG) {
