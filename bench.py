@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--workload", default="cfg2",
-                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "paper", "big"])
+                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "paper", "big", "big2d"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--k", type=int, default=None, help="override the directory k (default: auto)")
     ap.add_argument("--levels", type=int, default=-1,
@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--count", type=int, default=None, help="override targets per GPU (testing)")
     ap.add_argument("--loglog", action="store_true", help="cfg4: log-log grid (EOS_GRID_LOGLOG)")
     ap.add_argument("--derivatives", action="store_true", help="cfg4: also write dP/drho, dP/dT")
+    ap.add_argument("--global-grid", action="store_true",
+                    help="2-D: keep the grid in device memory (EOS_GRID_GLOBAL)")
     ap.add_argument("--eager", action="store_true",
                     help="launch each step from Python with per-launch events instead of a CUDA graph")
     return ap.parse_args()
@@ -174,9 +176,12 @@ def run_ours(a, d: Dist):
         P = torch.empty(count, dtype=torch.float64, device=dev)
         iR = torch.empty(count, dtype=torch.int32, device=dev)
         iT = torch.empty(count, dtype=torch.int32, device=dev)
-        obj = eos.Grid2D(w.rho, w.T, w.P, loglog=a.loglog)
+        obj = eos.Grid2D(w.rho, w.T, w.P, loglog=a.loglog, global_grid=a.global_grid)
         info = {"rho": obj.rho_info.as_dict(), "T": obj.T_info.as_dict(),
-                "grid": "loglog" if a.loglog else "linear", "derivatives": a.derivatives}
+                "grid": "loglog" if a.loglog else "linear", "derivatives": a.derivatives,
+                "grid_cells": int(w.P.size),
+                "grid_in": "device memory" if (a.global_grid or 8 * w.P.size > 200 * 1024)
+                           else "shared memory"}
         dPr = torch.empty(count, dtype=torch.float64, device=dev) if a.derivatives else None
         dPt = torch.empty(count, dtype=torch.float64, device=dev) if a.derivatives else None
         if a.derivatives:

@@ -142,6 +142,16 @@ def grid_cfg4(seed: int = 3):
     return rho, T, np.ascontiguousarray(P)
 
 
+def grid_big2d(seed: int = 7):
+    """A grid larger than shared memory (the EOSPAC 2-D analogue of `big`): density axis 1000
+    log-spaced [1e-6, 1e3], temperature axis 800 log-spaced [1, 1e8], P as cfg4 -- 6.4 MB of P,
+    kept in device memory (L2-resident).  Not a BASELINE.json config."""
+    rho = np.logspace(-6.0, 3.0, 1000)
+    T = np.logspace(0.0, 8.0, 800)
+    P = rho[:, None] * T[None, :] ** 1.5 * (1.0 + 0.01 * np.sin(37.0 * np.log(rho)))[:, None]
+    return rho, T, np.ascontiguousarray(P)
+
+
 def table_cfg5(seed: int = 4) -> np.ndarray:
     """n=4096 clustered: 2867 entries log-uniform in [1e0,1e2], 1229 log-uniform over
     [1e-6,1e0) U [1e2,1e10).  Sorted, exact duplicates redrawn."""
@@ -320,6 +330,13 @@ def workload(name: str, count: int | None = None) -> Workload:
         return Workload(name, count or 5_000_000, X,
                         TargetSpec("loguniform", 5, a=-10.0, w=20.0),
                         note="paper-shaped: n=110 over [3e-6,5.4e4], 5e6 log-uniform over 1e-10..1e10")
+    if name == "big2d":
+        rho, T, P = grid_big2d(7)
+        return Workload(name, count or (1 << 28), rho=rho, T=T, P=P,
+                        rho_targets=TargetSpec("loguniform", 7, 0, a=-6.0, w=9.0),
+                        T_targets=TargetSpec("loguniform", 7, 1, a=0.0, w=8.0),
+                        note="1000x800 grid in device memory (larger than shared memory), "
+                             "2^28 log-uniform (rho,T) pairs")
     if name == "big":
         X = table_big(6)
         return Workload(name, count or (1 << 27), X, loguniform_over(X, 6),
@@ -328,4 +345,4 @@ def workload(name: str, count: int | None = None) -> Workload:
     raise KeyError(name)
 
 
-WORKLOADS = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "paper", "big")
+WORKLOADS = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "paper", "big", "big2d")

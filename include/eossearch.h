@@ -247,9 +247,11 @@ EOS_API eos_status eos_search_destroy(eos_table t);
 
 /* rho_host fp64[n_rho], T_host fp64[n_T]: strictly increasing, finite,
  * 2 <= n <= EOS_MAX_TABLE (negative axis values allowed: key mode 1);
- * P_host fp64[n_rho * n_T] row-major (T fastest), finite; the grid must fit
- * in shared memory (n_rho*n_T*8 + axes <= ~220 KB, else
- * EOS_ERR_UNSUPPORTED).  Copied; bound to the current device. */
+ * P_host fp64[n_rho * n_T] row-major (T fastest), finite, n_rho n_T <=
+ * EOS_MAX_GRID_CELLS.  P lives in shared memory when it fits (~200 KB with
+ * the axes), else in device memory (see EOS_GRID_GLOBAL); the axes must fit
+ * in shared memory (their images <= ~220 KB, else EOS_ERR_UNSUPPORTED).
+ * Copied; bound to the current device. */
 EOS_API eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double* T_host,
                              int64_t n_T, const double* P_host, eos_grid2d* out);
 
@@ -261,6 +263,12 @@ EOS_API eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, cons
                            *   Needs R, T, P > 0 (else EOS_ERR_UNSUPPORTED).  Brackets are
                            *   the same P:54 lower bounds.  Derivatives (eos_interp2d_ex):
                            *   dP/drho = P (d ln P / d ln rho) / rho on the cell. */
+#define EOS_GRID_GLOBAL 2 /* flag bit: keep the grid in device memory even if it would fit in
+                           * shared memory (grids whose P does not fit, n_rho n_T 8 B >
+                           * ~200 KB, always live there): row pairs (G[i][j], G[i][j+1]) read
+                           * with two 16-byte loads per pair; the axes stay in shared memory
+                           * (their images must fit: ~220 KB).  Same results. */
+#define EOS_MAX_GRID_CELLS ((int64_t)1 << 28) /* n_rho n_T (EOS_ERR_SIZE above) */
 EOS_API eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const double* T_host,
                                 int64_t n_T, const double* P_host, int32_t flags, eos_grid2d* out);
 

@@ -31,7 +31,7 @@ __all__ = [
     "EOS_HASH_LOG", "eos_plan_table_hash", "eos_search_create_hash", "eos_interp2d_ex",
     "eos_search_direct", "search_direct", "eos_grid2d_create_ex", "EOS_GRID_LINEAR",
     "EOS_GRID_LOGLOG", "EOS_MAX_TABLE_TIERED", "EOS_LEVELS_AUTO", "eos_search_create_levels",
-    "eos_plan_table_levels", "plan_table_levels",
+    "eos_plan_table_levels", "plan_table_levels", "EOS_GRID_GLOBAL", "EOS_MAX_GRID_CELLS",
 ]
 
 EOS_MAX_TABLE = 16384
@@ -40,7 +40,8 @@ EOS_LEVELS_AUTO = -1
 EOS_MAX_K = 19
 EOS_K_AUTO = -1
 EOS_HASH_AUTO, EOS_HASH_EXPONENT, EOS_HASH_LOG = 0, 1, 2
-EOS_GRID_LINEAR, EOS_GRID_LOGLOG = 0, 1
+EOS_GRID_LINEAR, EOS_GRID_LOGLOG, EOS_GRID_GLOBAL = 0, 1, 2
+EOS_MAX_GRID_CELLS = 1 << 28
 
 STATUS = {
     0: "EOS_OK", 1: "EOS_ERR_NULL", 2: "EOS_ERR_SIZE", 3: "EOS_ERR_NONFINITE",
@@ -416,13 +417,15 @@ class Table:
 class Grid2D:
     """EOSPAC-style 2-D table (density x temperature) for eos_interp2d."""
 
-    def __init__(self, rho, T, P, loglog: bool = False):
-        """loglog=True: interpolate ln P bilinearly in (ln rho, ln T) (EOS_GRID_LOGLOG, R24)."""
+    def __init__(self, rho, T, P, loglog: bool = False, global_grid: bool = False):
+        """loglog=True: interpolate ln P bilinearly in (ln rho, ln T) (EOS_GRID_LOGLOG, R24).
+        global_grid=True: keep P in device memory even if it fits in shared memory
+        (EOS_GRID_GLOBAL; grids too large for shared memory always are)."""
         self.rho, self.T = _f64_host(rho).copy(), _f64_host(T).copy()
         self.P = _f64_host(P).reshape(self.rho.size, self.T.size).copy()
         self.loglog = loglog
-        self._h = eos_grid2d_create(self.rho, self.T, self.P,
-                                    EOS_GRID_LOGLOG if loglog else EOS_GRID_LINEAR)
+        flags = (EOS_GRID_LOGLOG if loglog else EOS_GRID_LINEAR) | (EOS_GRID_GLOBAL if global_grid else 0)
+        self._h = eos_grid2d_create(self.rho, self.T, self.P, flags)
         self.rho_info, self.T_info = eos_grid2d_info(self._h)
 
     @property

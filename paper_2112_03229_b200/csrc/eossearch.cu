@@ -61,6 +61,11 @@ struct eos_grid2d_s {
   int32_t wr_off = 0, wt_off = 0, lr_off = 0, lt_off = 0;
   int32_t rr_off = 0, rt_off = 0;
   int rep = 0;  // bank-pinned axis layout in the image (REP kernels): 0 none, 1 copies, 2 records
+  int32_t rep_shift = 0;       // REP 2: log2 of the record copies
+  int64_t rep_bytes_axis = 0;  // image bytes per axis entry of the REP layout
+  bool gg = false;          // grid in device memory (GG kernels)
+  void* grid_dev = nullptr;  // GG: row pairs (double2[n_rho (n_T - 1)])
+  int64_t grid_bytes = 0;
 };
 
 namespace {
@@ -236,7 +241,26 @@ struct Interp2DShape {
 // 3 static512u4, 4 clc512u2, 5 static512u2+recip, 6 static1024u1+recip,
 // 10 static1024u1 with bank-pinned axis copies (REP 1), 11 static1024u1 with
 // bank-pinned cell records (REP 2, the default when they fit).
-Interp2DShape pick_interp(int steps, bool loglog, int rep) {
+template <bool LOGLOG, int REP, int S>
+Interp2DShape gg_shape() {
+  return {(const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, LOGLOG, REP, true>,
+          (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, LOGLOG, REP, true>,
+          dv::Shape2D::kThreads, dv::Shape2D::kUnroll, dv::Shape2D::kClc};
+}
+
+// Grids in device memory (GG): S = 1 or the runtime-S instantiation.
+template <bool LOGLOG, int REP>
+Interp2DShape gg_pick(int steps) {
+  return steps == 1 ? gg_shape<LOGLOG, REP, 1>() : gg_shape<LOGLOG, REP, 0>();
+}
+
+Interp2DShape pick_interp(int steps, bool loglog, int rep, bool gg) {
+  if (gg) {
+    if (loglog) return rep == 2 ? gg_pick<true, 2>(steps) : gg_pick<true, 0>(steps);
+    if (rep == 2) return gg_pick<false, 2>(steps);
+    if (rep == 1) return gg_pick<false, 1>(steps);
+    return gg_pick<false, 0>(steps);
+  }
   if (loglog) {
     const void *fn, *fd;
     const bool r2 = rep == 2;
@@ -404,6 +428,8 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   a.lt_off = g->lt_off;
   a.rr_off = g->rr_off;
   a.rt_off = g->rt_off;
+  a.gq = reinterpret_cast<const double2*>(g->grid_dev);
+  a.rep_shift = g->rep_shift;
   a.r = g->ar;
   a.t = g->at;
   a.rho = rho;
@@ -784,45 +810,75 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   if (!out) return EOS_ERR_NULL;
   *out = nullptr;
   if (!rho_host || !T_host || !P_host) return EOS_ERR_NULL;
-  if (flags != EOS_GRID_LINEAR && flags != EOS_GRID_LOGLOG) return EOS_ERR_UNSUPPORTED;
-  const bool loglog = flags == EOS_GRID_LOGLOG;
+  if (flags & ~(EOS_GRID_LOGLOG | EOS_GRID_GLOBAL)) return EOS_ERR_UNSUPPORTED;
+  const bool loglog = (flags & EOS_GRID_LOGLOG) != 0;
+  if (n_rho > 0 && n_T > 0 && n_rho * n_T > EOS_MAX_GRID_CELLS) return EOS_ERR_SIZE;
   eos_grid2d g = new (std::nothrow) eos_grid2d_s();
   if (!g) return EOS_ERR_NOMEM;
+  auto fail = [&](eos_status st) {
+    if (g->image_dev) cudaFree(g->image_dev);
+    if (g->grid_dev) cudaFree(g->grid_dev);
+    delete g;
+    return st;
+  };
   eos_status st = eos::plan_table(rho_host, n_rho, EOS_HASH_AUTO, 0, true, &g->pr);
   if (st == EOS_OK) st = eos::plan_table(T_host, n_T, EOS_HASH_AUTO, 0, true, &g->pt);
-  if (st != EOS_OK) { delete g; return st; }
+  if (st != EOS_OK) return fail(st);
   g->flags = flags;
   const int64_t ncell = n_rho * n_T;
   for (int64_t q = 0; q < ncell; ++q)
-    if (!isfinite(P_host[q])) { delete g; return EOS_ERR_NONFINITE; }
+    if (!isfinite(P_host[q])) return fail(EOS_ERR_NONFINITE);
   if (loglog) {  // ln of the axes and the grid must exist (R24)
     bool ok = g->pr.X[0] > 0.0 && g->pt.X[0] > 0.0;
     for (int64_t q = 0; q < ncell && ok; ++q) ok = P_host[q] > 0.0;
-    if (!ok) { delete g; return EOS_ERR_UNSUPPORTED; }
+    if (!ok) return fail(EOS_ERR_UNSUPPORTED);
   }
-  // image: [rho X | rho dir][T X | T dir][G][1/dR][1/dT][ln R][ln T][R x16][T x16]
+  // image: [rho X | rho dir][T X | T dir][G][1/dR][1/dT (RECIP variants)][ln R][ln T][R recs][T recs]
+  // G is absent for grids in device memory (GG: larger than ~220 KB, or
+  // EOS_GRID_GLOBAL), which keep it as row pairs in g->grid_dev instead.
   int64_t r_bytes = g->pr.image_bytes, t_bytes = g->pt.image_bytes;
-  const int64_t g_bytes = (8 * ncell + 15) & ~int64_t(15);
-  const int64_t wr_bytes = (8 * (n_rho - 1) + 15) & ~int64_t(15);
-  const int64_t wt_bytes = (8 * (n_T - 1) + 15) & ~int64_t(15);
+  // 1/dR, 1/dT arrays: only for the RECIP tuning variants (EOS_INTERP_VARIANT 5, 6)
+  const char* ev = getenv("EOS_INTERP_VARIANT");
+  const bool recip_arrays = ev && (atoi(ev) == 5 || atoi(ev) == 6);
+  const int64_t wr_bytes = recip_arrays ? (8 * (n_rho - 1) + 15) & ~int64_t(15) : 0;
+  const int64_t wt_bytes = recip_arrays ? (8 * (n_T - 1) + 15) & ~int64_t(15) : 0;
   const int64_t lr_bytes = loglog ? (8 * n_rho + 15) & ~int64_t(15) : 0;
   const int64_t lt_bytes = loglog ? (8 * n_T + 15) & ~int64_t(15) : 0;
-  g->image_bytes = r_bytes + t_bytes + g_bytes + wr_bytes + wt_bytes + lr_bytes + lt_bytes;
-  if (g->image_bytes > 220 * 1024) { delete g; return EOS_ERR_UNSUPPORTED; }
-  // bank-pinned axis copies (kernels.cuh axis_cell REP): 16 x 8 B per axis
-  // entry, linear grids only, if the image still fits one CTA's shared memory
-  // (227 KB opt-in less the kernel's static smem).  EOS_INTERP_REP=0: off.
+  const int64_t axes_bytes = r_bytes + t_bytes + wr_bytes + wt_bytes + lr_bytes + lt_bytes;
+  const int64_t smem_grid_bytes = (8 * ncell + 15) & ~int64_t(15);
+  g->gg = (flags & EOS_GRID_GLOBAL) != 0 || axes_bytes + smem_grid_bytes > 220 * 1024;
+  const int64_t g_bytes = g->gg ? 0 : smem_grid_bytes;
+  g->image_bytes = axes_bytes + g_bytes;
+  if (g->image_bytes > 220 * 1024) return fail(EOS_ERR_UNSUPPORTED);  // axes too long for smem
+  // bank-pinned axis records (kernels.cuh axis_cell REP): 128 B per axis
+  // entry, if the image still fits one CTA's shared memory (227 KB opt-in
+  // less the kernel's static smem).  EOS_INTERP_REP=0/1/2 (default 2).
   {
-    const char* e = getenv("EOS_INTERP_REP");  // 0, 1 or 2 (default 2)
+    const char* e = getenv("EOS_INTERP_REP");
     const int want = e ? std::max(0, std::min(2, atoi(e))) : 2;
-    const int64_t rep_bytes = 128 * (n_rho + n_T);  // both layouts: 128 B per axis entry
     // log-log grids: records of the log axes (REP 2 only)
     const int w = loglog ? (want == 2 ? 2 : 0) : want;
-    g->rep = (w > 0 && g->image_bytes + rep_bytes <= 226 * 1024) ? w : 0;
-    if (g->rep) g->image_bytes += rep_bytes;
-    // REP 2: spend the rest of the shared memory on sparser axis directories
-    // (split by axis length), so that the second record read is rare
-    const int64_t spare = 226 * 1024 - g->image_bytes - 512;
+    // REP 1 needs all 16 copies (128 B per axis entry); REP 2 takes 8 copies
+    // (conflict-free, 128 B per entry) or as many as fit, down to 1 (then it
+    // still saves the divides)
+    // Grids in device memory leave shared memory to L1, which holds their
+    // in-flight corner loads: the image is capped (EOS_GG_SMEM_KB, default 96).
+    const char* ec = getenv("EOS_GG_SMEM_KB");
+    const int64_t cap = g->gg ? (ec ? atoi(ec) : 96) * int64_t(1024) : 226 * 1024;
+    g->rep = 0;
+    for (int sh = (w == 1 ? 4 : 3); w > 0 && sh >= (w == 1 ? 4 : 0); --sh) {
+      const int64_t rep_bytes = (int64_t(16) << sh) * (n_rho + n_T);
+      if (g->image_bytes + rep_bytes <= cap) {
+        g->rep = w;
+        g->rep_shift = w == 2 ? sh : 0;
+        g->rep_bytes_axis = int64_t(16) << sh;
+        g->image_bytes += rep_bytes;
+        break;
+      }
+    }
+    // REP 2: spend the rest of the shared memory (at most 64 KB) on sparser
+    // axis directories (split by axis length), so the second record read is rare
+    const int64_t spare = std::min<int64_t>(cap - g->image_bytes - 512, 64 * 1024);
     if (g->rep == 2 && !loglog && spare > 1024) {
       const int64_t avail = r_bytes + t_bytes + spare;
       const int64_t br = avail * n_rho / (n_rho + n_T), bt = avail - br;
@@ -849,7 +905,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   g->lr_off = (int32_t)(g->wt_off + wt_bytes);
   g->lt_off = (int32_t)(g->lr_off + lr_bytes);
   g->rr_off = (int32_t)(g->lt_off + lt_bytes);
-  g->rt_off = (int32_t)(g->rr_off + (g->rep ? 128 * n_rho : 0));
+  g->rt_off = (int32_t)(g->rr_off + (g->rep ? g->rep_bytes_axis * n_rho : 0));
   auto put_rep = [&](const std::vector<double>& Xa, int32_t off) {
     std::vector<double> X(Xa);
     if (loglog)  // records of the log axis (the same host log as the ln R / ln T arrays)
@@ -858,9 +914,11 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     for (int64_t q = 0; q < n; ++q) {
       if (g->rep == 1) {  // Xr[16 q + c] = X[q]
         for (int c = 0; c < 16; ++c) memcpy(img.data() + off + 8 * (16 * q + c), &X[q], 8);
-      } else {  // Rec[8 q + c] = (X[q], 1/(X[q+1] - X[q])); the last record's width is unused
+      } else {  // Rec[C q + c] = (X[q], 1/(X[q+1] - X[q])), C = 2^rep_shift copies;
+                // the last record's width is unused
         const double rec[2] = {X[q], q + 1 < n ? 1.0 / (X[q + 1] - X[q]) : 0.0};
-        for (int c = 0; c < 8; ++c) memcpy(img.data() + off + 16 * (8 * q + c), rec, 16);
+        const int C = 1 << g->rep_shift;
+        for (int c = 0; c < C; ++c) memcpy(img.data() + off + 16 * (C * q + c), rec, 16);
       }
     }
   };
@@ -868,11 +926,15 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     put_rep(g->pr.X, g->rr_off);
     put_rep(g->pt.X, g->rt_off);
   }
-  if (loglog) {  // the grid holds ln G; ln of the axes follow the reciprocal widths
+  // the grid values (ln G for log-log grids)
+  auto gval = [&](int64_t q) { return loglog ? log(P_host[q]) : P_host[q]; };
+  if (!g->gg) {
     for (int64_t q = 0; q < ncell; ++q) {
-      const double v = log(P_host[q]);
+      const double v = gval(q);
       memcpy(img.data() + g->g_off + 8 * q, &v, 8);
     }
+  }
+  if (loglog) {  // ln of the axes
     for (int64_t q = 0; q < n_rho; ++q) {
       const double v = log(g->pr.X[q]);
       memcpy(img.data() + g->lr_off + 8 * q, &v, 8);
@@ -881,14 +943,12 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
       const double v = log(g->pt.X[q]);
       memcpy(img.data() + g->lt_off + 8 * q, &v, 8);
     }
-  } else {
-    memcpy(img.data() + g->g_off, P_host, 8 * (size_t)ncell);
   }
-  for (int64_t q = 0; q + 1 < n_rho; ++q) {
+  for (int64_t q = 0; recip_arrays && q + 1 < n_rho; ++q) {
     const double w = 1.0 / (g->pr.X[q + 1] - g->pr.X[q]);
     memcpy(img.data() + g->wr_off + 8 * q, &w, 8);
   }
-  for (int64_t q = 0; q + 1 < n_T; ++q) {
+  for (int64_t q = 0; recip_arrays && q + 1 < n_T; ++q) {
     const double w = 1.0 / (g->pt.X[q + 1] - g->pt.X[q]);
     memcpy(img.data() + g->wt_off + 8 * q, &w, 8);
   }
@@ -896,10 +956,29 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   g->at = axis_params(g->pt, (int32_t)r_bytes);
   cudaError_t e = cudaGetDevice(&g->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device);
-  if (e != cudaSuccess) { delete g; return cuda_status(e); }
+  if (e != cudaSuccess) return fail(cuda_status(e));
   st = upload(img, &g->image_dev);
-  if (st != EOS_OK) { delete g; return st; }
-  Interp2DShape sh = pick_interp(std::max(g->pr.steps, g->pt.steps), loglog, g->rep);
+  if (st != EOS_OK) return fail(st);
+  if (g->gg) {  // row pairs gq[i (nT-1) + j] = (G[i][j], G[i][j+1])
+    const int64_t w = n_T - 1;
+    std::vector<double> q2;
+    try {
+      q2.resize((size_t)(2 * n_rho * w));
+    } catch (...) {
+      return fail(EOS_ERR_NOMEM);
+    }
+    for (int64_t i = 0; i < n_rho; ++i)
+      for (int64_t j = 0; j < w; ++j) {
+        q2[2 * (i * w + j)] = gval(i * n_T + j);
+        q2[2 * (i * w + j) + 1] = gval(i * n_T + j + 1);
+      }
+    g->grid_bytes = 8 * (int64_t)q2.size();
+    e = cudaMalloc(&g->grid_dev, (size_t)g->grid_bytes);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(g->grid_dev, q2.data(), (size_t)g->grid_bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(cuda_status(e));
+  }
+  Interp2DShape sh = pick_interp(std::max(g->pr.steps, g->pt.steps), loglog, g->rep, g->gg);
   g->fn = sh.fn;
   g->fn_deriv = sh.fn_deriv;
   g->threads = sh.threads;
@@ -909,7 +988,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   if (st == EOS_OK)
     st = configure(g->fn_deriv, g->threads_deriv, g->image_bytes, g->num_sms, &g->grid_deriv,
                    nullptr);
-  if (st != EOS_OK) { cudaFree(g->image_dev); delete g; return st; }
+  if (st != EOS_OK) return fail(st);
   *out = g;
   return EOS_OK;
 }
@@ -990,6 +1069,10 @@ eos_status eos_grid2d_destroy(eos_grid2d g) {
   cudaGetDevice(&cur);
   if (cur != g->device) cudaSetDevice(g->device);
   cudaError_t e = cudaFree(g->image_dev);
+  if (g->grid_dev) {
+    cudaError_t e2 = cudaFree(g->grid_dev);
+    if (e == cudaSuccess) e = e2;
+  }
   if (cur != g->device && cur >= 0) cudaSetDevice(cur);
   delete g;
   return cuda_status(e);

@@ -695,6 +695,11 @@ struct Interp2DArgs {
   int32_t rr_off;   // byte offset of the bank-pinned copies of the R axis (REP kernels):
                     //   REP 1: fp64[16 nR], REP 2: double2[8 nR] records (R[j], 1/(R[j+1]-R[j]))
   int32_t rt_off;   // the same for the T axis
+  int32_t rep_shift;  // REP 2: log2 of the record copies per axis entry (3: 8 copies, the
+                      //   conflict-free layout; fewer when smem is short: 2-way .. 8-way)
+  int32_t pad2_;
+  const double2* gq;  // GG kernels: the grid in device memory as row pairs
+                      //   gq[i (nT-1) + j] = (G[i][j], G[i][j+1]) (ln G for LOGLOG)
   int32_t vec_ok;
   int32_t pad_;
   int64_t ntiles;
@@ -775,7 +780,7 @@ template <int S>
 __device__ __forceinline__ void axis_cell_rec(double y, const double* __restrict__ sX,
                                               const uint32_t* __restrict__ sD, const AxisParams& a,
                                               int32_t& i, int32_t& ci, double& xl, double& inv,
-                                              const double2* __restrict__ rec_) {
+                                              const double2* __restrict__ rec_, int32_t sh) {
   double2 r;
   int32_t p;
   if (S == 1) {
@@ -785,7 +790,7 @@ __device__ __forceinline__ void axis_cell_rec(double y, const double* __restrict
     const int32_t occ = (int32_t)(d >> 16);     // 0 or 1
     p = occ >= 1 ? lo : max(lo - 1, 0);
     EOS_DCHECK(lo < a.n && occ <= 1 && p < a.n);
-    r = rec_[8 * p];
+    r = rec_[p << sh];
     const int32_t c = (occ >= 1 && r.x <= y) ? 1 : 0;
     i = (y >= a.x0) ? lo + c - 1 : 0;
   } else {
@@ -793,7 +798,7 @@ __device__ __forceinline__ void axis_cell_rec(double y, const double* __restrict
     p = -1;
   }
   ci = min(i, a.n - 2);
-  if (ci != p) r = rec_[8 * ci];
+  if (ci != p) r = rec_[ci << sh];
   xl = r.x;
   inv = r.y;
 }
@@ -804,7 +809,12 @@ __device__ __forceinline__ void axis_cell_rec(double y, const double* __restrict
 // of that formula (bit-identical to a plain evaluation in that order).
 // RECIP: weights as (x - X[c]) * (1/(X[c+1]-X[c])) with the reciprocal
 // precomputed at create (a few ulp from the divide; within the 1e-12 bar).
-template <int S, bool RECIP, bool DERIV, bool LOGLOG, int REP>
+//
+// GG (grids larger than shared memory): the grid stays in device memory
+// (L2-resident up to ~10^7 cells) as row pairs, so the 4 corners are two
+// aligned 16-byte loads, (G[ci][cj], G[ci][cj+1]) and (G[ci+1][cj],
+// G[ci+1][cj+1]); the axes, their directories and records stay in smem.
+template <int S, bool RECIP, bool DERIV, bool LOGLOG, int REP, bool GG>
 __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, int32_t& j,
                                              double& dpr, double& dpt, const char* sm,
                                              const Interp2DArgs& A) {
@@ -821,19 +831,19 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
     // (ln X[j], 1/(ln X[j+1] - ln X[j]))
     axis_cell<S>(rho, sR, dR, A.r, i, ci, r0, r1);
     axis_cell<S>(T, sT, dT, A.t, j, cj, t0, t1);
-    const int32_t c = threadIdx.x & 7;
-    const double2 er = reinterpret_cast<const double2*>(sm + A.rr_off)[8 * ci + c];
-    const double2 et = reinterpret_cast<const double2*>(sm + A.rt_off)[8 * cj + c];
+    const int32_t sh = A.rep_shift, c = threadIdx.x & ((1 << sh) - 1);
+    const double2 er = reinterpret_cast<const double2*>(sm + A.rr_off)[(ci << sh) + c];
+    const double2 et = reinterpret_cast<const double2*>(sm + A.rt_off)[(cj << sh) + c];
     r0 = er.x;
     ir = er.y;
     t0 = et.x;
     it = et.y;
   } else if (REP == 2) {
-    const int32_t c = threadIdx.x & 7;  // the copy of this lane (bank quad c)
+    const int32_t sh = A.rep_shift, c = threadIdx.x & ((1 << sh) - 1);  // this lane's copy
     axis_cell_rec<S>(rho, sR, dR, A.r, i, ci, r0, ir,
-                     reinterpret_cast<const double2*>(sm + A.rr_off) + c);
+                     reinterpret_cast<const double2*>(sm + A.rr_off) + c, sh);
     axis_cell_rec<S>(T, sT, dT, A.t, j, cj, t0, it,
-                     reinterpret_cast<const double2*>(sm + A.rt_off) + c);
+                     reinterpret_cast<const double2*>(sm + A.rt_off) + c, sh);
     r1 = t1 = 0.0;  // unused
   } else if (REP == 1) {
     const int32_t c = threadIdx.x & 15;  // the copy of this lane (bank pair c)
@@ -872,9 +882,23 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
     ty = clamp01(__ddiv_rn(__dsub_rn(xt, t0), __dsub_rn(t1, t0)));
   }
   EOS_DCHECK(ci >= 0 && cj >= 0 && ci + 1 < A.r.n && cj + 1 < A.t.n);
-  const double* g0 = sG + (int64_t)ci * A.t.n + cj;
-  const double* g1 = g0 + A.t.n;
-  const double g00 = g0[0], g01 = g0[1], g10 = g1[0], g11 = g1[1];
+  double g00, g01, g10, g11;
+  if (GG) {
+    const int64_t w = A.t.n - 1;  // row-pair stride
+    const double2* q = A.gq + (int64_t)ci * w + cj;
+    const double2 q0 = __ldg(q), q1 = __ldg(q + w);
+    g00 = q0.x;
+    g01 = q0.y;
+    g10 = q1.x;
+    g11 = q1.y;
+  } else {
+    const double* g0 = sG + (int64_t)ci * A.t.n + cj;
+    const double* g1 = g0 + A.t.n;
+    g00 = g0[0];
+    g01 = g0[1];
+    g10 = g1[0];
+    g11 = g1[1];
+  }
   const double uy = __dsub_rn(1.0, ty);
   const double ux = __dsub_rn(1.0, tx);
   const double a0 = __dadd_rn(__dmul_rn(uy, g00), __dmul_rn(ty, g01));
@@ -905,7 +929,7 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
 using Shape2D = Shape<1024, 1, 1, false>;
 using Shape2DDeriv = Shape<512, 1, 1, false>;  // derivative outputs need > 64 registers
 
-template <int S, class SH, bool RECIP, bool DERIV, bool LOGLOG = false, int REP = 0>
+template <int S, class SH, bool RECIP, bool DERIV, bool LOGLOG = false, int REP = 0, bool GG = false>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {
   constexpr int T = SH::kThreads;
   constexpr int U = SH::kUnroll;
@@ -964,9 +988,9 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       int2 ir[U], it[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        p[u].x = interp_one<S, RECIP, DERIV, LOGLOG, REP>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
+        p[u].x = interp_one<S, RECIP, DERIV, LOGLOG, REP, GG>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
                                              sm, A);
-        p[u].y = interp_one<S, RECIP, DERIV, LOGLOG, REP>(vr[u].y, vt[u].y, ir[u].y, it[u].y, dr[u].y, dt[u].y,
+        p[u].y = interp_one<S, RECIP, DERIV, LOGLOG, REP, GG>(vr[u].y, vt[u].y, ir[u].y, it[u].y, dr[u].y, dt[u].y,
                                              sm, A);
       }
       tn = next_tile(t);
@@ -991,7 +1015,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       for (int64_t q = e0 + threadIdx.x; q < e1; q += T) {
         int32_t i, j;
         double dpr, dpt;
-        const double pq = interp_one<S, RECIP, DERIV, LOGLOG, REP>(A.rho[q], A.T[q], i, j, dpr, dpt, sm, A);
+        const double pq = interp_one<S, RECIP, DERIV, LOGLOG, REP, GG>(A.rho[q], A.T[q], i, j, dpr, dpt, sm, A);
         A.P[q] = pq;
         if (br) A.iR[q] = i;
         if (bt) A.iT[q] = j;

@@ -414,12 +414,39 @@ def test_interp_host_pipeline_matches():
 
 
 # ------------------------------------------------- f4: derivatives, mode 1 --
-def _check_deriv(got, ref):
+def _check_deriv(got, ref, cond=None):
+    """Derivatives within 1e-12 of max(|ref|, cond, 1e-3 max|ref|).  `cond` (optional) is the
+    magnitude of the terms of the derivative's difference quotient (deriv_cond): the
+    default linear kernels weight with a precomputed inverse cell width,
+    which perturbs t by an ulp, and a cancelling difference amplifies that relative to
+    |ref| but not relative to the terms."""
     nan_g, nan_r = np.isnan(got), np.isnan(ref)
     assert np.array_equal(nan_g, nan_r)
     ok = ~nan_r
     scale = max(np.abs(ref[ok]).max(), 1e-300) if ok.any() else 1.0
-    assert np.all(np.abs(got[ok] - ref[ok]) <= REL_TOL * np.maximum(np.abs(ref[ok]), 1e-3 * scale))
+    bar = np.maximum(np.abs(ref[ok]), 1e-3 * scale)
+    if cond is not None:
+        bar = np.maximum(bar, np.nan_to_num(cond[ok], nan=0.0))
+    assert np.all(np.abs(got[ok] - ref[ok]) <= REL_TOL * bar)
+
+
+def deriv_cond(R, T, G, rho, tt, iR, iT, P=None, loglog=False):
+    """Magnitudes of the two terms of dP/drho and dP/dT on each bracket cell (R23/R24),
+    used only as the tolerance scale of _check_deriv -- not an expected value."""
+    R, T, G = np.asarray(R), np.asarray(T), np.asarray(G)
+    ci = np.minimum(iR, R.size - 2)
+    cj = np.minimum(iT, T.size - 2)
+    xr, xt, ax, at, g = (np.log(rho), np.log(tt), np.log(R), np.log(T), np.log(G)) if loglog \
+        else (rho, tt, R, T, G)
+    with np.errstate(all="ignore"):
+        tx = np.clip((xr - ax[ci]) / (ax[ci + 1] - ax[ci]), 0, 1)
+        ty = np.clip((xt - at[cj]) / (at[cj + 1] - at[cj]), 0, 1)
+        g00, g01, g10, g11 = g[ci, cj], g[ci, cj + 1], g[ci + 1, cj], g[ci + 1, cj + 1]
+        kr = (np.abs((1 - ty) * (g10 - g00)) + np.abs(ty * (g11 - g01))) / (ax[ci + 1] - ax[ci])
+        kt = (np.abs((1 - tx) * (g01 - g00)) + np.abs(tx * (g11 - g10))) / (at[cj + 1] - at[cj])
+        if loglog:
+            kr, kt = kr * np.abs(P) / np.abs(rho), kt * np.abs(P) / np.abs(tt)
+    return kr, kt
 
 
 def test_interp_derivatives_match_oracle():
@@ -466,8 +493,9 @@ def test_interp_negative_axes_mode1_and_odd_sizes():
         dRr, dTr = oracle.interp2d_deriv(R, T, G, rho, tt)
         assert np.array_equal(iR.cpu().numpy(), iRr) and np.array_equal(iT.cpu().numpy(), iTr)
         check_interp(P.cpu().numpy(), Pr)
-        _check_deriv(dR.cpu().numpy(), dRr)
-        _check_deriv(dT.cpu().numpy(), dTr)
+        kr, kt = deriv_cond(R, T, G, rho, tt, iRr, iTr)
+        _check_deriv(dR.cpu().numpy(), dRr, kr)
+        _check_deriv(dT.cpu().numpy(), dTr, kt)
         g.close()
 
 
@@ -802,8 +830,9 @@ def test_interp_regular_axes_node_targets(axes, loglog):
         dRr, dTr = oracle.interp2d_deriv(R, T, G, rho, tt)
     assert np.array_equal(iR.cpu().numpy(), iRr) and np.array_equal(iT.cpu().numpy(), iTr)
     check_interp(P.cpu().numpy(), Pr)
-    _check_deriv(dR.cpu().numpy(), dRr)
-    _check_deriv(dT.cpu().numpy(), dTr)
+    kr, kt = deriv_cond(R, T, G, rho, tt, iRr, iTr, Pr, loglog)
+    _check_deriv(dR.cpu().numpy(), dRr, kr)
+    _check_deriv(dT.cpu().numpy(), dTr, kt)
     g.close()
 
 
@@ -899,3 +928,77 @@ def test_cuda_graph_capture_and_replay():
     tab.close()
     big.close()
     grid.close()
+
+
+# ------------------------- 2-D grids in device memory (EOS_GRID_GLOBAL) -----
+@pytest.mark.parametrize("loglog", [False, True])
+def test_global_grid_cfg4_matches_shared_and_oracle(loglog):
+    """The cfg4 grid forced into device memory gives the shared-memory kernel's
+    brackets and values (same arithmetic), hence the oracle's."""
+    w = datagen.workload("cfg4", count=(1 << 20) + 7)
+    rho = w.rho_targets.host_fill(0, w.count)
+    T = w.T_targets.host_fill(0, w.count)
+    rho[:3] = [np.nan, w.rho[0] / 3, w.rho[-1] * 3]
+    T[3:6] = [np.nan, w.T[0] / 3, w.T[-1] * 3]
+    rho[6:6 + w.rho.size] = w.rho
+    gs = eos.Grid2D(w.rho, w.T, w.P, loglog=loglog)
+    gg = eos.Grid2D(w.rho, w.T, w.P, loglog=loglog, global_grid=True)
+    a = gs.interp(to_dev(rho), to_dev(T), derivatives=True)
+    b = gg.interp(to_dev(rho), to_dev(T), derivatives=True)
+    torch.cuda.synchronize()
+    for x, y in zip(a, b):
+        assert np.array_equal(x.cpu().numpy(), y.cpu().numpy(), equal_nan=True)
+    ref = (oracle.interp2d_loglog if loglog else oracle.interp2d)(w.rho, w.T, w.P, rho, T)
+    assert np.array_equal(b[1].cpu().numpy(), ref[1]) and np.array_equal(b[2].cpu().numpy(), ref[2])
+    check_interp(b[0].cpu().numpy(), ref[0])
+    gs.close()
+    gg.close()
+
+
+@pytest.mark.parametrize("shape,loglog", [((600, 500), False), ((600, 500), True),
+                                          ((1000, 800), False), ((3000, 7), False),
+                                          ((2, 16000), False), ((8000, 3), True)])
+def test_large_grids_in_device_memory(shape, loglog):
+    """Grids larger than shared memory (P in device memory, axes in smem with as many
+    record copies as fit): brackets bit-exact, P and derivatives within the bar."""
+    rng = np.random.default_rng(shape[0] + shape[1])
+    nR, nT = shape
+    if loglog:  # jittered logspace axes: log-log derivatives amplify the device-vs-libm
+        # log rounding by 1/(cell width in ln), so the test avoids arbitrarily narrow cells
+        def axis(a, b, n):
+            u = np.linspace(a, b, n)
+            return 10 ** (u + (b - a) / (n - 1) * rng.uniform(-0.3, 0.3, n))
+        R, T = axis(-4, 4, nR), axis(0, 6, nT)
+    else:
+        R = np.sort(np.unique(10 ** rng.uniform(-4, 4, nR)))
+        T = np.sort(np.unique(10 ** rng.uniform(0, 6, nT)))
+        while R.size < nR or T.size < nT:   # redraw on (unlikely) duplicates
+            R = np.sort(np.unique(10 ** rng.uniform(-4, 4, nR)))
+            T = np.sort(np.unique(10 ** rng.uniform(0, 6, nT)))
+    if loglog:  # a smooth (EOS-like) surface: ln G varies little across one cell, so the
+        # device-vs-libm log rounding, amplified by 1/(cell width in ln), stays < 1e-13
+        G = R[:, None] ** 1.2 * T[None, :] ** 0.7 * (1 + 0.01 * rng.uniform(-1, 1, (nR, nT)))
+    else:
+        G = np.exp(rng.uniform(-2, 2, (nR, nT)))
+    m = 1 << 19
+    rho = 10 ** rng.uniform(-4.3, 4.3, m)
+    tt = 10 ** rng.uniform(-0.3, 6.3, m)
+    rho[:nR // 4] = R[: nR // 4]
+    tt[-(nT // 4 or 1):] = T[-(nT // 4 or 1):]
+    rho[nR:nR + 4] = [np.nan, np.inf, 0.0, -1.0]
+    g = eos.Grid2D(R, T, G, loglog=loglog)
+    P, iR, iT, dR, dT = g.interp(to_dev(rho), to_dev(tt), derivatives=True)
+    P0, _, _ = g.interp(to_dev(rho), to_dev(tt))
+    torch.cuda.synchronize()
+    if loglog:
+        Pr, iRr, iTr, dRr, dTr = oracle.interp2d_loglog(R, T, G, rho, tt)
+    else:
+        Pr, iRr, iTr = oracle.interp2d(R, T, G, rho, tt)
+        dRr, dTr = oracle.interp2d_deriv(R, T, G, rho, tt)
+    assert np.array_equal(iR.cpu().numpy(), iRr) and np.array_equal(iT.cpu().numpy(), iTr)
+    check_interp(P.cpu().numpy(), Pr)
+    assert np.array_equal(P0.cpu().numpy(), P.cpu().numpy(), equal_nan=True)
+    kr, kt = deriv_cond(R, T, G, rho, tt, iRr, iTr, Pr, loglog)
+    _check_deriv(dR.cpu().numpy(), dRr, kr)
+    _check_deriv(dT.cpu().numpy(), dTr, kt)
+    g.close()

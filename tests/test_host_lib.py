@@ -344,3 +344,23 @@ def test_tiered_plan_errors():
     dup = np.concatenate([[-0.0], np.repeat(np.arange(1.0, 9000.0), 3)])
     info = eos.plan_table_levels(dup)
     assert info.levels == 1 and info.key_mode == 0
+
+
+def test_grid_cell_limit_checked_before_any_work():
+    """eos_grid2d_create_ex rejects n_rho n_T > EOS_MAX_GRID_CELLS (EOS_ERR_SIZE) before
+    reading P or touching a device, and unknown flags (EOS_ERR_UNSUPPORTED)."""
+    import ctypes
+    L = eos.load_library()
+    L.eos_grid2d_create_ex.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                       ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32,
+                                       ctypes.c_void_p]
+    R = np.arange(1.0, 2.0 ** 15 + 1)
+    T = np.arange(1.0, 2.0 ** 14 + 1)
+    P = np.ones(4)
+    h = ctypes.c_void_p()
+    rc = L.eos_grid2d_create_ex(R.ctypes.data, R.size, T.ctypes.data, T.size, P.ctypes.data, 0,
+                                ctypes.byref(h))
+    assert rc == 2
+    rc = L.eos_grid2d_create_ex(R.ctypes.data, 4, T.ctypes.data, 4, P.ctypes.data, 8,
+                                ctypes.byref(h))
+    assert rc == 8
