@@ -485,7 +485,7 @@ def test_interp_negative_axes_mode1_and_odd_sizes():
         rho[:R.size] = R
         tt[-T.size:] = T
         rho[R.size:R.size + 2] = [-0.0, 0.0]
-        g = eos.Grid2D(R, T, G)
+        g = eos.Grid2D(R, T, G, global_grid=bool(t % 2))  # odd draws: P in device memory
         assert g.rho_info.key_mode == 1
         P, iR, iT, dR, dT = g.interp(to_dev(rho), to_dev(tt), derivatives=True)
         torch.cuda.synchronize()
