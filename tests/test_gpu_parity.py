@@ -401,11 +401,12 @@ def test_search_host_pipeline_matches():
     t.close()
 
 
-def test_interp_host_pipeline_matches():
+@pytest.mark.parametrize("global_grid", [False, True])
+def test_interp_host_pipeline_matches(global_grid):
     w = datagen.workload("cfg4", count=(1 << 23) + 3)
     rh = w.rho_targets.host_fill(0, w.count)
     th = w.T_targets.host_fill(0, w.count)
-    g = eos.Grid2D(w.rho, w.T, w.P)
+    g = eos.Grid2D(w.rho, w.T, w.P, global_grid=global_grid)
     P, iR, iT = g.interp_host(rh, th)
     Pr, iRr, iTr = oracle.interp2d(w.rho, w.T, w.P, rh, th)
     assert np.array_equal(iR, iRr) and np.array_equal(iT, iTr)
