@@ -1,11 +1,15 @@
 // kernels.cuh -- sm_100a kernels of the hot path.
 //
-//   search1d_kernel : per target y -> int32 lower bound
-//   interp2d_kernel : per (rho, T) pair -> brackets + bilinear P
+//   search1d_kernel        : per target y -> int32 lower bound
+//   search1d_tiered_kernel : the same for tables larger than shared memory
+//   search1d_direct_kernel : the same with the directory built on the device
+//   interp2d_kernel        : per (rho, T) pair -> brackets + bilinear P (P:14,
+//                            P:41), optionally dP/drho, dP/dT, log-log
 //
-// Design: HBM-bound streams.  The table X (fp64) and
-// its exponent-hash count directory (u32) are staged once per CTA into shared
-// memory.  The grid has one CTA per tile of the target stream, but resident
+// Design: HBM-bound streams.  The table X (fp64) and its
+// hash count directory (u32) are staged once per CTA into shared memory
+// (tables larger than shared memory: a sample of X, with the rest in L2-
+// resident 8-ary key levels, search1d_tiered_kernel).  The grid has one CTA per tile of the target stream, but resident
 // CTAs keep their staged image and steal the tiles of not-yet-launched CTAs
 // with Blackwell cluster launch control (clusterlaunchcontrol.try_cancel):
 // dynamic load balance at persistent-kernel cost, with no global counters.
@@ -719,12 +723,6 @@ __device__ __forceinline__ double clamp01(double t) {
   return t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
 }
 
-// Bilinear on the bracket cell (R14).  Written with explicit
-// round-to-nearest intrinsics (no FMA contraction), in the order of the
-// formula in eossearch.h, so the value is the correctly-rounded evaluation
-// of that formula (bit-identical to a plain evaluation in that order).
-// RECIP: weights as (x - X[c]) * (1/(X[c+1]-X[c])) with the reciprocal
-// precomputed at create (a few ulp from the divide; within the 1e-12 bar).
 // Bracket + cell endpoints on one axis: i (the P:54 lower bound), the cell
 // ci = min(i, n-2) and its endpoints X[ci], X[ci+1].  With S = 1 (every bin
 // holds at most one entry) the in-bin probe value X[lo] is always one of the
