@@ -56,14 +56,16 @@ struct TablePlan {
 // 18% (L1 starved).
 constexpr int64_t kAutoImageBudget = 144 * 1024;
 constexpr int64_t kAxisImageBudget = 16 * 1024;  // per axis of a 2-D grid (the grid owns smem)
+constexpr int64_t kTieredImageBudget = 160 * 1024;  // cap of a tiered table's sample-table image
 constexpr int64_t kMaxImage = 200 * 1024;  // explicit requests beyond this do not fit in smem
 
 // Validate + build (eos_plan_table_hash semantics).  kind/param: see
 // eossearch.h (EOS_HASH_AUTO ignores param).  strict: axes of a 2-D grid must
 // be strictly increasing and n >= 2.
-// fill_budget (grid axes only, strict): if > 0, among the automatic hash
+// fill_budget: grid axes (strict): if > 0, among the automatic hash
 // candidates with the smallest S take the one with the most bins whose image
-// fits fill_budget bytes (instead of the smallest image).
+// fits fill_budget bytes (instead of the smallest image); search tables: if
+// > 0, the image budget of the automatic choice (default kAutoImageBudget).
 eos_status plan_table(const double* X, int64_t n, int kind, int64_t param, bool strict,
                       TablePlan* out, int64_t fill_budget = 0);
 

@@ -141,18 +141,19 @@ struct LaunchShape {
 // Default launch shape by image size: as many threads per SM as registers
 // allow (~1024 at <= 64 regs), with all image copies of an SM <= ~144 KB of
 // smem so L1 keeps room for the in-flight streaming loads.
+// One 1024-thread CTA per SM (images > 72 KB) always takes the static
+// schedule: its per-tile CTA barrier makes CLC 13-15% slower there even at
+// S <= 2 (n = 4096 log-uniform, 143 KB image: 443 -> 508 Glookups/s;
+// profiles/r01_exp_table_size.json).
 LaunchShape pick_search(int mode, int steps, bool cnt, int64_t image_bytes) {
   if (cnt) return {search_fn_shape<dv::ShapeCnt>(mode, steps, true), 256, 4, true};
-  if (steps >= 3) {
-    if (image_bytes <= 72 * 1024)
-      return {search_fn_shape<dv::ShapeDeepMid>(mode, steps, false), 512, 4, false};
+  if (image_bytes > 72 * 1024)
     return {search_fn_shape<dv::ShapeDeepBig>(mode, steps, false), 1024, 4, false};
-  }
+  if (steps >= 3)
+    return {search_fn_shape<dv::ShapeDeepMid>(mode, steps, false), 512, 4, false};
   if (image_bytes <= 32 * 1024)
     return {search_fn_shape<dv::ShapeSmall>(mode, steps, false), 256, 4, true};
-  if (image_bytes <= 72 * 1024)
-    return {search_fn_shape<dv::ShapeMid>(mode, steps, false), 512, 4, true};
-  return {search_fn_shape<dv::ShapeBig>(mode, steps, false), 1024, 4, true};
+  return {search_fn_shape<dv::ShapeMid>(mode, steps, false), 512, 4, true};
 }
 
 // Launch-shape variants for tuning experiments (EOS_SEARCH_VARIANT=<name> at

@@ -391,7 +391,6 @@ struct Shape {
 // the CLC loop costs more than the static schedule's tail.
 using ShapeSmall = Shape<256, 4, 4, true>;      // image <= 32 KB: 4 CTAs x 256 threads per SM
 using ShapeMid = Shape<512, 4, 2, true>;        // image <= 72 KB: 2 CTAs x 512
-using ShapeBig = Shape<1024, 4, 1, true>;       // larger: 1 CTA x 1024 (one image copy per SM)
 using ShapeDeepMid = Shape<512, 4, 2, false>;   // S >= 3, image <= 72 KB
 using ShapeDeepBig = Shape<1024, 4, 1, false>;  // S >= 3, larger
 using ShapeCnt = Shape<256, 4, 1, true>;        // validation launches (counters on)

@@ -165,11 +165,14 @@ double plan_cost(const TablePlan& p) {
 // fill_budget > 0 (grid axes of REP 2 kernels, eossearch.cu): the smallest S,
 // then the MOST bins within fill_budget bytes -- there a sparser directory
 // makes the second cell-record read rarer (kernels.cuh axis_cell_rec).
+// For search tables (!compact) fill_budget > 0 replaces the image budget
+// (tiered sample tables, plan_tiered).
 eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, TablePlan* out,
                      int64_t fill_budget = 0) {
   const int64_t n = (int64_t)X.size();
   const bool fill = compact && fill_budget > 0;
-  const int64_t budget = fill ? fill_budget : (compact ? kAxisImageBudget : kAutoImageBudget);
+  const int64_t budget = fill_budget > 0 ? fill_budget
+                                         : (compact ? kAxisImageBudget : kAutoImageBudget);
   TablePlan best;
   double best_cost = 0.0;
   bool have = false;
@@ -299,7 +302,14 @@ eos_status plan_tiered(const double* Xin, int64_t n, int levels, int kind, int64
   }
   std::vector<double> T1((size_t)n1);
   for (int64_t j = 0; j < n1; ++j) T1[j] = L0[j * stride];
-  eos_status st = plan_table(T1.data(), n1, kind, param, false, &t.top);
+  // Image budget of the sample table (measured, profiles/r01_exp_table_size.json:
+  // a directory of ~2 bins per entry (S = 2) beats the single-level choice of
+  // a 140 KB directory -- n = 2^15: 211 against 119 Glookups/s -- while
+  // larger ones lose again): X + max(32 KB, 4 n1) bytes of directory, at
+  // most 160 KB in all.
+  const int64_t budget = std::min<int64_t>(kTieredImageBudget,
+                                           8 * n1 + std::max<int64_t>(32 * 1024, 4 * n1));
+  eos_status st = plan_table(T1.data(), n1, kind, param, false, &t.top, budget);
   if (st != EOS_OK) return st;
   // key mode of T1 is that of X (T1[0] = X[0])
   t.x_last = L0[n - 1];

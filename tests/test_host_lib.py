@@ -309,9 +309,18 @@ def test_tiered_plan_levels_and_sizes():
         n1 = -(-n // 8 ** D)
         assert info.top_n == n1 <= eos.EOS_MAX_TABLE
         assert info.level_bytes == 12 * sum(n1 * 8 ** (D - d) for d in range(D))
-        top, _ = eos.plan_table(X[::8 ** D], with_directory=False)
-        for f in ("bins", "max_occ", "steps", "k", "hash_kind", "hash_mult", "image_bytes"):
-            assert getattr(info, f) == getattr(top, f), (n, f)
+        if D == 0:   # the single-level plan
+            top, _ = eos.plan_table(X, with_directory=False)
+            for f in ("bins", "max_occ", "steps", "k", "hash_kind", "hash_mult", "image_bytes"):
+                assert getattr(info, f) == getattr(top, f), (n, f)
+        else:        # the sample table X[::8^D] under the tiered image budget
+            budget = min(160 * 1024, 8 * n1 + max(32 * 1024, 4 * n1))
+            pad16 = lambda b: (b + 15) // 16 * 16  # noqa: E731
+            assert info.image_bytes == pad16(8 * n1) + pad16(4 * info.bins) <= budget
+            assert info.steps == int(np.ceil(np.log2(info.max_occ + 1)))
+            if info.hash_kind == eos.EOS_HASH_EXPONENT:
+                ref, _ = eos.plan_table(X[::8 ** D], k=info.k, with_directory=False)
+                assert (ref.bins, ref.max_occ, ref.steps) == (info.bins, info.max_occ, info.steps)
     # explicit D on small tables (testing the tiered path at any size)
     X = np.sort(rng.uniform(1, 2, 1000))
     for D in range(0, 6):
