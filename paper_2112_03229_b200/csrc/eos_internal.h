@@ -50,11 +50,11 @@ struct TablePlan {
 };
 
 // Smem budget of the automatic hash choice (bytes of X + directory): one image
-// copy per SM at the 1024-thread shape, leaving >= ~80 KB of L1 for in-flight
-// loads.  Measured: a larger image that removes an in-bin step wins (cfg5
-// k=9/S=3 at 138 KB beats k=7/S=4 at 59 KB by 6%), but a 198 KB image loses
-// 18% (L1 starved).
-constexpr int64_t kAutoImageBudget = 144 * 1024;
+// copy per SM at the 1024-thread shape.  Images above 144 KB squeeze L1 and
+// carry a cost penalty (table_build.cpp plan_cost).  Measured: a larger image
+// that removes an in-bin step wins (cfg5 k=9/S=3 at 138 KB beats k=7/S=4 at
+// 59 KB by 6%), a 198 KB image loses 18% on cfg5 but wins 39% at n = 16384.
+constexpr int64_t kAutoImageBudget = 200 * 1024;
 constexpr int64_t kAxisImageBudget = 16 * 1024;  // per axis of a 2-D grid (the grid owns smem)
 constexpr int64_t kTieredImageBudget = 160 * 1024;  // cap of a tiered table's sample-table image
 constexpr int64_t kMaxImage = 200 * 1024;  // explicit requests beyond this do not fit in smem

@@ -130,10 +130,15 @@ double lifting_probes(int o, int S) {
 // The shape (eossearch.cu::pick_search) keeps the smem of all resident image
 // copies <= ~144 KB per SM, leaving L1 for the in-flight streaming loads:
 // image <= 32 KB: 4 CTAs x 256 threads (penalty 0); <= 72 KB: 2 x 512 (1);
-// <= 144 KB: 1 x 1024 (1.5).  Measured: directories that squeeze L1 below
-// ~80 KB lose 4-18% (profiles/r01_exp_hash_*.json), so the automatic choice
-// stays within 144 KB.  Targets are taken log-uniform over the table range,
-// i.e. uniform over the bins (equal key width).
+// <= 144 KB: 1 x 1024 (1.5); up to 200 KB: 1 x 1024 with L1 squeezed (4.5).
+// (Not modelled: n = 4096 log-uniform runs 11% faster with S = 3 at 95 KB than
+// with S = 2 at 143 KB, but cfg5 loses 1-4% with the same trade.)
+// Measured: for cfg5 a 198 KB directory loses 18% against 143 KB
+// (profiles/r01_exp_hash_*.json), but for n = 16384 (128 KB of X alone) a
+// 197 KB image with 4x the bins wins 39% over 146 KB
+// (profiles/r01_exp_table_size.json): the penalty lets only a large probe
+// saving buy the extra smem.  Targets are taken log-uniform over the table
+// range, i.e. uniform over the bins (equal key width).
 double plan_cost(const TablePlan& p) {
   std::vector<double> memo(64, -1.0);
   double probes = 0.0;
@@ -149,8 +154,10 @@ double plan_cost(const TablePlan& p) {
     probes += v;
   }
   probes /= (double)p.bins;
-  const double shape =
-      p.image_bytes <= 32 * 1024 ? 0.0 : (p.image_bytes <= 72 * 1024 ? 1.0 : 1.5);
+  const double shape = p.image_bytes <= 32 * 1024   ? 0.0
+                       : p.image_bytes <= 72 * 1024  ? 1.0
+                       : p.image_bytes <= 144 * 1024 ? 1.5
+                                                     : 4.5;
   return 3.5 + 6.1 * probes + 1.0 * p.steps + shape;
 }
 
