@@ -1,6 +1,15 @@
 // eossearch.cu -- the C ABI of include/eossearch.h: handle management, device
 // image upload, launch configuration and the end-to-end host-buffer pipelines.
 // Product path (never includes or links oracle/).
+//
+// Tuning knobs, read at create / first use, for A/B experiments only (the
+// defaults are the measured best):
+//   EOS_SEARCH_VARIANT, EOS_TIERED_VARIANT  launch-shape variants by name
+//   EOS_INTERP_VARIANT                      2-D launch variants by number
+//   EOS_INTERP_REP (0/1/2)                  2-D axis layout (plain / copies / records)
+//   EOS_GG_SMEM_KB                          smem cap of device-memory grids
+//   EOS_PDL (0/1)                           programmatic dependent launch
+//   EOS_HOST_SLOTS, EOS_HOST_CHUNK_LOG2     host-buffer pipeline depth / chunk
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
