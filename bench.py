@@ -338,7 +338,7 @@ def run_ours(a, d: Dist):
     if counters is not None:
         res["validation"] = {"counters_u64": counters}
     if d.world == 1 and d.rank == 0 and not a.no_cpu:
-        res["cpu_baseline"] = cpu_baseline(w, is2d)
+        res["cpu_baseline"] = cpu_baseline(w, is2d, loglog=a.loglog, deriv=a.derivatives)
     return res
 
 
@@ -418,14 +418,20 @@ def ncu_traffic(workload):
 
 
 # -------------------------------------------------------- CPU oracle -------
-def oracle_run(w, is2d, sample: int, threads: int):
-    """Time the oracle (as it stands) on the first `sample` units of the workload."""
+def oracle_run(w, is2d, sample: int, threads: int, loglog: bool = False, deriv: bool = False):
+    """Time the oracle (as it stands) on the first `sample` units of the workload -- the
+    oracle function of the same variant (log-log / derivatives) as the GPU arm."""
     import oracle
     if is2d:
         rho = w.rho_targets.host_fill(0, sample)
         T = w.T_targets.host_fill(0, sample)
         t = time.perf_counter()
-        oracle.interp2d(w.rho, w.T, w.P, rho, T, threads=threads)
+        if loglog:   # P, brackets and both derivatives in one call
+            oracle.interp2d_loglog(w.rho, w.T, w.P, rho, T, threads=threads)
+        else:
+            oracle.interp2d(w.rho, w.T, w.P, rho, T, threads=threads)
+            if deriv:
+                oracle.interp2d_deriv(w.rho, w.T, w.P, rho, T, threads=threads)
         return time.perf_counter() - t
     Y = np.empty(sample, dtype=np.float64)
     fill_host_parallel(w, 0, sample, Y)
@@ -438,14 +444,15 @@ def cpu_sample_size(w, is2d):
     return min(w.count, (1 << 25) if is2d else (1 << 27))
 
 
-def cpu_baseline(w, is2d, min_cpu_s: float = 12.0, max_passes: int = 20):
+def cpu_baseline(w, is2d, min_cpu_s: float = 12.0, max_passes: int = 20, loglog: bool = False,
+                 deriv: bool = False):
     """The oracle as it stands, on the first `sample` units of the workload, repeated
     until about `min_cpu_s` seconds of CPU work (threads x wall) are done."""
     threads = host_cores()
     sample = cpu_sample_size(w, is2d)
     times = []
     while not times or (sum(times) * threads < min_cpu_s and len(times) < max_passes):
-        times.append(oracle_run(w, is2d, sample, threads))
+        times.append(oracle_run(w, is2d, sample, threads, loglog, deriv))
     dt = float(np.sum(times))
     return {"value": round(len(times) * sample / dt / 1e9, 5),
             "unit": "Gpairs/s" if is2d else "Glookups/s", "cores": threads, "kind": "oracle",
@@ -463,8 +470,9 @@ def run_reference(a, d: Dist):
     threads = host_cores()
     sample = min(w.count, (1 << 22) if is2d else (1 << 24))
     for _ in range(min(a.warmup, 1)):
-        oracle_run(w, is2d, min(sample, 1 << 16), threads)
-    times = [oracle_run(w, is2d, sample, threads) for _ in range(max(1, min(a.steps, 10)))]
+        oracle_run(w, is2d, min(sample, 1 << 16), threads, a.loglog, a.derivatives)
+    times = [oracle_run(w, is2d, sample, threads, a.loglog, a.derivatives)
+             for _ in range(max(1, min(a.steps, 10)))]
     s = float(np.mean(times))
     value = sample / s / 1e9
     unit = "Gpairs/s" if is2d else "Glookups/s"
