@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--derivatives", action="store_true", help="cfg4: also write dP/drho, dP/dT")
     ap.add_argument("--global-grid", action="store_true",
                     help="2-D: keep the grid in device memory (EOS_GRID_GLOBAL)")
+    ap.add_argument("--direct", action="store_true",
+                    help="1-D: time the zero-setup eos_search_direct (f2; n <= 4096)")
     ap.add_argument("--eager", action="store_true",
                     help="launch each step from Python with per-launch events instead of a CUDA graph")
     return ap.parse_args()
@@ -201,9 +203,17 @@ def run_ours(a, d: Dist):
         out = torch.empty(count, dtype=torch.int32, device=dev)
         obj = eos.Table(w.table, k=a.k, log_bins=a.log_bins, levels=a.levels)
         info = obj.info.as_dict()
+        if a.direct:  # zero setup: the directory is built on the device by every CTA (f2)
+            Xd = torch.from_numpy(w.table).to(dev)
+            info = {"n": int(w.table.size), "api": "eos_search_direct (no handle)"}
 
-        def step(sp=None):
-            eos.eos_search(obj.handle, Y.data_ptr(), count, out.data_ptr(), sp or stream.cuda_stream)
+            def step(sp=None):
+                eos.eos_search_direct(Xd.data_ptr(), Xd.numel(), Y.data_ptr(), count, out.data_ptr(),
+                                      None, sp or stream.cuda_stream)
+        else:
+            def step(sp=None):
+                eos.eos_search(obj.handle, Y.data_ptr(), count, out.data_ptr(),
+                               sp or stream.cuda_stream)
     torch.cuda.synchronize()
 
     for _ in range(max(a.warmup, 0)):
@@ -309,6 +319,7 @@ def run_ours(a, d: Dist):
             "frac": round(achieved / hbm_peak, 4),
             "traffic": ncu_traffic(a.workload),
             "kernel": "interp2d_kernel" if is2d else (
+                "search1d_direct_kernel" if a.direct else
                 "search1d_tiered_kernel" if obj.info.levels > 0 else "search1d_kernel"),
             "kernel_ms_avg": round(kern_ms, 5),
             "kernel_ms_avg_max_rank": round(kern_ms_max, 5),
