@@ -6,7 +6,7 @@
 // defaults are the measured best):
 //   EOS_SEARCH_VARIANT, EOS_TIERED_VARIANT  launch-shape variants by name
 //   EOS_INTERP_VARIANT                      2-D launch variants by number
-//   EOS_INTERP_REP (0/1/2)                  2-D axis layout (plain / copies / records)
+//   EOS_INTERP_REP=0                        2-D plain axes (no cell records)
 //   EOS_GG_SMEM_KB                          smem cap of device-memory grids
 //   EOS_PDL (0/1)                           programmatic dependent launch
 //   EOS_HOST_SLOTS, EOS_HOST_CHUNK_LOG2     host-buffer pipeline depth / chunk
@@ -69,7 +69,7 @@ struct eos_grid2d_s {
   int32_t flags = 0;
   int32_t wr_off = 0, wt_off = 0, lr_off = 0, lt_off = 0;
   int32_t rr_off = 0, rt_off = 0;
-  int rep = 0;  // bank-pinned axis layout in the image (REP kernels): 0 none, 1 copies, 2 records
+  int rep = 0;  // 2: bank-pinned cell records in the image (REP kernels), 0: plain axes
   int32_t rep_shift = 0;       // REP 2: log2 of the record copies
   int64_t rep_bytes_axis = 0;  // image bytes per axis entry of the REP layout
   bool gg = false;          // grid in device memory (GG kernels)
@@ -215,7 +215,6 @@ const void* interp_fn_s(int variant) {
     case 4: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, true>, false, false>;
     case 5: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, false>, true, false>;
     case 6: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 1, 1, false>, true, false>;
-    case 10: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, false, 1>;
     case 11: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, false, 2>;
     default: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false>;
   }
@@ -224,7 +223,6 @@ const void* interp_fn_s(int variant) {
 template <int S>
 const void* interp_deriv_fn_s(int rep) {
   switch (rep) {
-    case 1: return (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, false, 1>;
     case 2: return (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, false, 2>;
     default: return (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true>;
   }
@@ -247,10 +245,10 @@ struct Interp2DShape {
 };
 
 // EOS_INTERP_VARIANT (tuning experiments only): 0 static1024u1 (default
-// without bank-pinned axis copies), 1 static512u2, 2 static1024u2,
+// without bank-pinned cell records), 1 static512u2, 2 static1024u2,
 // 3 static512u4, 4 clc512u2, 5 static512u2+recip, 6 static1024u1+recip,
-// 10 static1024u1 with bank-pinned axis copies (REP 1), 11 static1024u1 with
-// bank-pinned cell records (REP 2, the default when they fit).
+// 11 static1024u1 with bank-pinned cell records (REP 2, the default when they
+// fit).
 template <bool LOGLOG, int REP, int S>
 Interp2DShape gg_shape() {
   return {(const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, LOGLOG, REP, true>,
@@ -268,7 +266,6 @@ Interp2DShape pick_interp(int steps, bool loglog, int rep, bool gg) {
   if (gg) {
     if (loglog) return rep == 2 ? gg_pick<true, 2>(steps) : gg_pick<true, 0>(steps);
     if (rep == 2) return gg_pick<false, 2>(steps);
-    if (rep == 1) return gg_pick<false, 1>(steps);
     return gg_pick<false, 0>(steps);
   }
   if (loglog) {
@@ -283,11 +280,11 @@ Interp2DShape pick_interp(int steps, bool loglog, int rep, bool gg) {
     }
     return {fn, fd, dv::Shape2D::kThreads, dv::Shape2D::kUnroll, dv::Shape2D::kClc};
   }
-  const int vdef = rep == 2 ? 11 : (rep == 1 ? 10 : 0);
+  const int vdef = rep == 2 ? 11 : 0;
   int v = vdef;
   if (const char* e = getenv("EOS_INTERP_VARIANT")) v = atoi(e);
-  static const int thr[12] = {1024, 512, 1024, 512, 512, 512, 1024, 0, 0, 0, 1024, 1024};
-  static const int unr[12] = {1, 2, 2, 4, 2, 2, 1, 0, 0, 0, 1, 1};
+  static const int thr[12] = {1024, 512, 1024, 512, 512, 512, 1024, 0, 0, 0, 0, 1024};
+  static const int unr[12] = {1, 2, 2, 4, 2, 2, 1, 0, 0, 0, 0, 1};
   static const bool clc[12] = {false, false, false, false, true, false, false,
                                false, false, false, false, false};
   // variants 10/11 need the image of the matching REP layout
@@ -864,23 +861,22 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   // entry, if the image still fits one CTA's shared memory (227 KB opt-in
   // less the kernel's static smem).  EOS_INTERP_REP=0/1/2 (default 2).
   {
-    const char* e = getenv("EOS_INTERP_REP");
-    const int want = e ? std::max(0, std::min(2, atoi(e))) : 2;
-    // log-log grids: records of the log axes (REP 2 only)
-    const int w = loglog ? (want == 2 ? 2 : 0) : want;
-    // REP 1 needs all 16 copies (128 B per axis entry); REP 2 takes 8 copies
-    // (conflict-free, 128 B per entry) or as many as fit, down to 1 (then it
-    // still saves the divides)
+    const char* e = getenv("EOS_INTERP_REP");  // 0: plain axes (A/B)
+    const int want = (e && e[0] == '0') ? 0 : 2;
+    // (log-log grids: records of the log axes.)  8 copies are conflict-free
+    // (128 B per axis entry); take as many as fit, down to 1 (then the
+    // records still save the divides)
+    const int w = want;
     // Grids in device memory leave shared memory to L1, which holds their
     // in-flight corner loads: the image is capped (EOS_GG_SMEM_KB, default 96).
     const char* ec = getenv("EOS_GG_SMEM_KB");
     const int64_t cap = g->gg ? (ec ? atoi(ec) : 96) * int64_t(1024) : 226 * 1024;
     g->rep = 0;
-    for (int sh = (w == 1 ? 4 : 3); w > 0 && sh >= (w == 1 ? 4 : 0); --sh) {
+    for (int sh = 3; w > 0 && sh >= 0; --sh) {
       const int64_t rep_bytes = (int64_t(16) << sh) * (n_rho + n_T);
       if (g->image_bytes + rep_bytes <= cap) {
         g->rep = w;
-        g->rep_shift = w == 2 ? sh : 0;
+        g->rep_shift = sh;
         g->rep_bytes_axis = int64_t(16) << sh;
         g->image_bytes += rep_bytes;
         break;
@@ -922,14 +918,11 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
       for (double& v : X) v = log(v);
     const int64_t n = (int64_t)X.size();
     for (int64_t q = 0; q < n; ++q) {
-      if (g->rep == 1) {  // Xr[16 q + c] = X[q]
-        for (int c = 0; c < 16; ++c) memcpy(img.data() + off + 8 * (16 * q + c), &X[q], 8);
-      } else {  // Rec[C q + c] = (X[q], 1/(X[q+1] - X[q])), C = 2^rep_shift copies;
-                // the last record's width is unused
-        const double rec[2] = {X[q], q + 1 < n ? 1.0 / (X[q + 1] - X[q]) : 0.0};
-        const int C = 1 << g->rep_shift;
-        for (int c = 0; c < C; ++c) memcpy(img.data() + off + 16 * (C * q + c), rec, 16);
-      }
+      // Rec[C q + c] = (X[q], 1/(X[q+1] - X[q])), C = 2^rep_shift copies; the
+      // last record's width is unused
+      const double rec[2] = {X[q], q + 1 < n ? 1.0 / (X[q + 1] - X[q]) : 0.0};
+      const int C = 1 << g->rep_shift;
+      for (int c = 0; c < C; ++c) memcpy(img.data() + off + 16 * (C * q + c), rec, 16);
     }
   };
   if (g->rep) {

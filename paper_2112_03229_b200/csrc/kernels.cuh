@@ -695,8 +695,8 @@ struct Interp2DArgs {
   int32_t wt_off;   // byte offset of 1/(T[j+1]-T[j]) fp64[nT-1] (RECIP variant)
   int32_t lr_off;   // byte offset of ln R fp64[nR] (LOGLOG grids)
   int32_t lt_off;   // byte offset of ln T fp64[nT] (LOGLOG grids)
-  int32_t rr_off;   // byte offset of the bank-pinned copies of the R axis (REP kernels):
-                    //   REP 1: fp64[16 nR], REP 2: double2[8 nR] records (R[j], 1/(R[j+1]-R[j]))
+  int32_t rr_off;   // byte offset of the bank-pinned cell records of the R axis (REP 2
+                    //   kernels): double2[2^rep_shift nR], (R[j], 1/(R[j+1]-R[j]))
   int32_t rt_off;   // the same for the T axis
   int32_t rep_shift;  // REP 2: log2 of the record copies per axis entry (3: 8 copies, the
                       //   conflict-free layout; fewer when smem is short: 2-way .. 8-way)
@@ -726,20 +726,12 @@ __device__ __forceinline__ double clamp01(double t) {
 // ci = min(i, n-2) and its endpoints X[ci], X[ci+1].  With S = 1 (every bin
 // holds at most one entry) the in-bin probe value X[lo] is always one of the
 // two endpoints in the common case, so only one more gather is needed.
-//
-// REP (bank-pinned axis copies): the axis values are also stored 16 times,
-// Xr[16 j + c] = X[j], so copy c lies entirely in bank pair c (an fp64 at
-// double index d sits in banks 2(d mod 16), 2(d mod 16) + 1).  A 64-bit
-// shared load is served per half-warp; lane l reads copy l mod 16, so the 16
-// lanes of a half-warp always hit 16 different bank pairs: the random
-// endpoint gathers become conflict-free (2 wavefronts per warp instead of
-// ~5.6 measured).  xr_ points at copy (lane mod 16).
-template <int S, bool REP = false>
+
+template <int S>
 __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ sX,
                                           const uint32_t* __restrict__ sD, const AxisParams& a,
-                                          int32_t& i, int32_t& ci, double& xl, double& xr,
-                                          const double* __restrict__ xr_ = nullptr) {
-  auto X = [&](int32_t j) { return REP ? xr_[16 * j] : sX[j]; };
+                                          int32_t& i, int32_t& ci, double& xl, double& xr) {
+  auto X = [&](int32_t j) { return sX[j]; };
   if (S == 1) {
     const uint32_t key = a.mode ? key_hi<1>(y) : key_hi<0>(y);
     const uint32_t d = sD[bin_of(key, a)];
@@ -842,12 +834,6 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
     axis_cell_rec<S>(T, sT, dT, A.t, j, cj, t0, it,
                      reinterpret_cast<const double2*>(sm + A.rt_off) + c, sh);
     r1 = t1 = 0.0;  // unused
-  } else if (REP == 1) {
-    const int32_t c = threadIdx.x & 15;  // the copy of this lane (bank pair c)
-    axis_cell<S, true>(rho, sR, dR, A.r, i, ci, r0, r1,
-                       reinterpret_cast<const double*>(sm + A.rr_off) + c);
-    axis_cell<S, true>(T, sT, dT, A.t, j, cj, t0, t1,
-                       reinterpret_cast<const double*>(sm + A.rt_off) + c);
   } else {
     axis_cell<S>(rho, sR, dR, A.r, i, ci, r0, r1);
     axis_cell<S>(T, sT, dT, A.t, j, cj, t0, t1);

@@ -25,7 +25,7 @@ fi
 if has checked; then
   EOS_LIBRARY=checked timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $OUT/pytest_gpu_checked.log 2>&1; echo "pytest gpu (checked build) rc=$?"
   tail -n 2 $OUT/pytest_gpu_checked.log
-  for rp in 0 1; do
+  for rp in 0; do
     EOS_INTERP_REP=$rp EOS_LIBRARY=checked timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "interp or loglog" > $OUT/pytest_checked_rep$rp.log 2>&1; echo "pytest interp checked rep=$rp rc=$?"
   done
   tail -n 4 $OUT/pytest_gpu_checked.log
@@ -143,9 +143,8 @@ fi
 if has rep; then
   timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "interp or smoke or loglog or graph or concurrent" > $OUT/pytest_rep.log 2>&1; echo "pytest interp (rep) rc=$?"; tail -n 3 $OUT/pytest_rep.log
   EOS_INTERP_REP=0 timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "interp" > $OUT/pytest_norep.log 2>&1; echo "pytest interp (no rep) rc=$?"; tail -n 2 $OUT/pytest_norep.log
-  EOS_INTERP_REP=1 timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "interp" > $OUT/pytest_rep1.log 2>&1; echo "pytest interp (rep 1) rc=$?"; tail -n 2 $OUT/pytest_rep1.log
   for r in 1 2; do
-    for rp in 2 1 0; do
+    for rp in 2 0; do
       for fl in "" "--derivatives"; do
         EOS_INTERP_REP=$rp timeout 600 python bench.py --workload cfg4 $fl --steps 200 --warmup 5 --no-cpu --no-e2e > $OUT/r4.json 2>/dev/null
         python -c "import json;d=json.load(open('$OUT/r4.json'));print('cfg4 rep=$rp [$fl]', d['value'], d['roofline']['frac'], d['clocks']['sm_mhz'])"
