@@ -1003,3 +1003,33 @@ def test_large_grids_in_device_memory(shape, loglog):
     _check_deriv(dR.cpu().numpy(), dRr, kr)
     _check_deriv(dT.cpu().numpy(), dTr, kt)
     g.close()
+
+
+# ------------------------------------------------ the ABI from plain C -------
+def test_plain_c_program_uses_the_abi(tmp_path):
+    """examples/c_abi_example.c (gcc, libcudart, no Python on the call path) creates a
+    table, searches a device batch and the host-buffer path, and interpolates a grid."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2112_03229_b200", "lib")
+    exe = tmp_path / "c_abi_example"
+    subprocess.run(["gcc", "-std=c11", "-O2", "-I", os.path.join(root, "include"),
+                    "-I", "/usr/local/cuda/include", os.path.join(root, "examples", "c_abi_example.c"),
+                    "-L", lib, "-leossearch", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                    "-o", str(exe)], check=True)
+    env = dict(os.environ, LD_LIBRARY_PATH=lib + ":/usr/local/cuda/lib64:"
+               + os.environ.get("LD_LIBRARY_PATH", ""))
+    for X in (datagen.table_cfg2(1), datagen.table_big(6)):   # single-level and tiered
+        w = datagen.loguniform_over(X, 11)
+        Y = w.host_fill(0, (1 << 20) + 5)
+        Y[:6] = [np.nan, np.inf, -np.inf, -0.0, X[0], X[-1]]
+        (tmp_path / "t.f64").write_bytes(X.tobytes())
+        (tmp_path / "y.f64").write_bytes(Y.tobytes())
+        r = subprocess.run([str(exe), str(tmp_path / "t.f64"), str(tmp_path / "y.f64"),
+                            str(tmp_path / "i.i32"), str(tmp_path / "h.i32")],
+                           env=env, capture_output=True, text=True)
+        assert r.returncode == 0, r.stdout + r.stderr
+        ref = oracle.search(X, Y)
+        assert_same(np.frombuffer((tmp_path / "i.i32").read_bytes(), dtype=np.int32), ref, Y)
+        assert_same(np.frombuffer((tmp_path / "h.i32").read_bytes(), dtype=np.int32), ref, Y)

@@ -373,3 +373,16 @@ def test_grid_cell_limit_checked_before_any_work():
     rc = L.eos_grid2d_create_ex(R.ctypes.data, 4, T.ctypes.data, 4, P.ctypes.data, 8,
                                 ctypes.byref(h))
     assert rc == 8
+
+
+def test_header_is_plain_c_and_the_example_links(tmp_path):
+    """include/eossearch.h compiles as C11 and examples/c_abi_example.c links against the
+    library with gcc (the boundary needs no C++ or torch types)."""
+    import subprocess
+    lib = os.path.join(ROOT, "paper_2112_03229_b200", "lib")
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-O1", "-I",
+                        os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+                        os.path.join(ROOT, "examples", "c_abi_example.c"), "-L", lib,
+                        "-leossearch", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                        "-o", str(tmp_path / "ex")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
