@@ -40,28 +40,54 @@ def stale(lib: str = LIB) -> bool:
     return any(os.path.getmtime(d) > t for d in deps())
 
 
-def nvcc_cmd(out: str = LIB, extra: list[str] | None = None) -> list[str]:
-    return [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-            "-Xcompiler", "-fvisibility=hidden", "-cudart", "static", "-I", INCLUDE, "-I", CSRC,
-            "-Xptxas", "-v", *(extra or []), "-o", out, *sources()]
+COMMON = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
+          "-fvisibility=hidden", "-I", INCLUDE, "-I", CSRC]
+
+
+def nvcc_compile_cmd(src: str, obj: str, extra: list[str] | None = None) -> list[str]:
+    return [NVCC, *COMMON, "-Xptxas", "-v", *(extra or []), "-c", "-o", obj, src]
+
+
+def nvcc_link_cmd(out: str, objs: list[str]) -> list[str]:
+    return [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs]
 
 
 def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """Compile every source to an object in parallel (one nvcc per translation unit:
+    the kernel instantiations are split over runtime.cu, search_api.cu and
+    grid_api.cu), then link the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
     lib = CHECKED_LIB if checked else LIB
-    if force or stale(lib):
-        os.makedirs(LIBDIR, exist_ok=True)
-        tmp = lib + ".tmp"
-        r = subprocess.run(nvcc_cmd(tmp, ["-DEOS_DEVICE_CHECKS"] if checked else None),
-                           capture_output=True, text=True)
-        log = os.path.join(LIBDIR, "ptxas_checked.log" if checked else "ptxas.log")
-        with open(log, "w") as f:
-            f.write(r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError("nvcc failed building libeossearch.so")
-        os.replace(tmp, lib)
-        if verbose:
-            print(f"built {lib}")
+    if not (force or stale(lib)):
+        return lib
+    os.makedirs(LIBDIR, exist_ok=True)
+    tag = "checked" if checked else "product"
+    objdir = os.path.join(LIBDIR, "obj_" + tag)
+    os.makedirs(objdir, exist_ok=True)
+    extra = ["-DEOS_DEVICE_CHECKS"] if checked else None
+    jobs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        jobs.append((src, obj, nvcc_compile_cmd(src, obj, extra)))
+    with ThreadPoolExecutor(len(jobs)) as ex:
+        results = list(ex.map(lambda j: subprocess.run(j[2], capture_output=True, text=True), jobs))
+    log = os.path.join(LIBDIR, "ptxas_checked.log" if checked else "ptxas.log")
+    with open(log, "w") as f:
+        for (src, _, _), r in zip(jobs, results):
+            f.write(f"==== {os.path.basename(src)}\n" + r.stdout + r.stderr)
+    bad = [(src, r) for (src, _, _), r in zip(jobs, results) if r.returncode != 0]
+    if bad:
+        for src, r in bad:
+            sys.stderr.write(f"{src}:\n{r.stdout}{r.stderr}")
+        raise RuntimeError("nvcc failed building libeossearch.so")
+    tmp = lib + ".tmp"
+    r = subprocess.run(nvcc_link_cmd(tmp, [j[1] for j in jobs]), capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed linking libeossearch.so")
+    os.replace(tmp, lib)
+    if verbose:
+        print(f"built {lib}")
     return lib
 
 

@@ -1,0 +1,465 @@
+// search_api.cu -- the 1-D part of the C ABI (include/eossearch.h): table
+// handles (single-level and tiered), the search launches, the zero-setup
+// search, host-only planning.  Product path (never includes or links oracle/).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "eos_internal.h"
+#include "eossearch.h"
+#include "kernels.cuh"
+#include "runtime.h"
+
+using eos::TablePlan;
+namespace dv = eos::dev;
+using namespace eos::rt;
+
+struct eos_table_s {
+  TablePlan plan;          // the shared-memory table (T1 of a tiered table)
+  int levels = 0;          // D (tiered tables, eos_search_create_levels)
+  int64_t n = 0;           // entries of the full table
+  int64_t top_n = 0;       // n1
+  int64_t level_bytes = 0;
+  int64_t level_elems = 0;
+  double* levels_dev = nullptr;  // the 8-ary levels: F (fp64) then K (u32), coarsest first
+  int device = -1;
+  int num_sms = 0;
+  void* image_dev = nullptr;
+  dv::AxisParams ax{};
+  // launch configuration per counters on/off
+  const void* fn[2] = {nullptr, nullptr};
+  int grid[2] = {0, 0};
+  int threads[2] = {256, 256};
+  int unroll[2] = {4, 4};
+  bool clc[2] = {true, true};
+  int ctas_per_sm = 0;
+};
+
+namespace {
+
+// ---------------------------------------------------------- kernel table ---
+template <int S, int MODE, class SH>
+const void* search_fn(bool cnt) {
+  return cnt ? (const void*)dv::search1d_kernel<S, MODE, true, SH>
+             : (const void*)dv::search1d_kernel<S, MODE, false, SH>;
+}
+
+template <int MODE, class SH>
+const void* search_fn_mode(int steps, bool cnt) {
+  switch (steps) {
+    case 1: return search_fn<1, MODE, SH>(cnt);
+    case 2: return search_fn<2, MODE, SH>(cnt);
+    case 3: return search_fn<3, MODE, SH>(cnt);
+    case 4: return search_fn<4, MODE, SH>(cnt);
+    case 5: return search_fn<5, MODE, SH>(cnt);
+    case 6: return search_fn<6, MODE, SH>(cnt);
+    case 7: return search_fn<7, MODE, SH>(cnt);
+    case 8: return search_fn<8, MODE, SH>(cnt);
+    default: return search_fn<0, MODE, SH>(cnt);  // runtime S
+  }
+}
+
+template <class SH>
+const void* search_fn_shape(int mode, int steps, bool cnt) {
+  return mode == 0 ? search_fn_mode<0, SH>(steps, cnt) : search_fn_mode<1, SH>(steps, cnt);
+}
+
+// tiered tables (levels >= 1): search1d_tiered_kernel
+template <int S, int MODE, class SH>
+const void* tiered_fn(bool cnt) {
+  return cnt ? (const void*)dv::search1d_tiered_kernel<S, MODE, true, dv::ShapeCnt>
+             : (const void*)dv::search1d_tiered_kernel<S, MODE, false, SH>;
+}
+
+template <int MODE, class SH>
+const void* tiered_fn_mode(int steps, bool cnt) {
+  switch (steps) {
+    case 1: return tiered_fn<1, MODE, SH>(cnt);
+    case 2: return tiered_fn<2, MODE, SH>(cnt);
+    case 3: return tiered_fn<3, MODE, SH>(cnt);
+    case 4: return tiered_fn<4, MODE, SH>(cnt);
+    case 5: return tiered_fn<5, MODE, SH>(cnt);
+    case 6: return tiered_fn<6, MODE, SH>(cnt);
+    case 7: return tiered_fn<7, MODE, SH>(cnt);
+    case 8: return tiered_fn<8, MODE, SH>(cnt);
+    default: return tiered_fn<0, MODE, SH>(cnt);
+  }
+}
+
+// Launch-shape variants of the tiered kernel (EOS_TIERED_VARIANT=<name>,
+// tuning experiments; mode 0, no counters, S <= 4).
+template <class SH>
+const void* tiered_variant_fn(int steps) {
+  switch (steps) {
+    case 1: return (const void*)dv::search1d_tiered_kernel<1, 0, false, SH>;
+    case 2: return (const void*)dv::search1d_tiered_kernel<2, 0, false, SH>;
+    case 3: return (const void*)dv::search1d_tiered_kernel<3, 0, false, SH>;
+    case 4: return (const void*)dv::search1d_tiered_kernel<4, 0, false, SH>;
+    default: return nullptr;
+  }
+}
+
+struct LaunchShape {
+  const void* fn;
+  int threads, unroll;
+  bool clc;
+};
+
+// Default launch shape by image size: as many threads per SM as registers
+// allow (~1024 at <= 64 regs), with all image copies of an SM <= ~144 KB of
+// smem so L1 keeps room for the in-flight streaming loads.
+// One 1024-thread CTA per SM (images > 72 KB) always takes the static
+// schedule: its per-tile CTA barrier makes CLC 13-15% slower there even at
+// S <= 2 (n = 4096 log-uniform, 143 KB image: 443 -> 508 Glookups/s;
+// profiles/r01_exp_table_size.json).
+LaunchShape pick_search(int mode, int steps, bool cnt, int64_t image_bytes) {
+  if (cnt) return {search_fn_shape<dv::ShapeCnt>(mode, steps, true), 256, 4, true};
+  if (image_bytes > 72 * 1024)
+    return {search_fn_shape<dv::ShapeDeepBig>(mode, steps, false), 1024, 4, false};
+  if (steps >= 3)
+    return {search_fn_shape<dv::ShapeDeepMid>(mode, steps, false), 512, 4, false};
+  if (image_bytes <= 32 * 1024)
+    return {search_fn_shape<dv::ShapeSmall>(mode, steps, false), 256, 4, true};
+  return {search_fn_shape<dv::ShapeMid>(mode, steps, false), 512, 4, true};
+}
+
+// Launch-shape variants for tuning experiments (EOS_SEARCH_VARIANT=<name> at
+// create time; mode 0, S <= 4, no counters).  Not part of the C ABI.
+struct Variant {
+  const char* name;
+  int threads, unroll;
+  bool clc;
+  const void* (*get)(int steps);
+};
+
+template <class SH>
+const void* variant_fn(int steps) {
+  switch (steps) {
+    case 1: return (const void*)dv::search1d_kernel<1, 0, false, SH>;
+    case 2: return (const void*)dv::search1d_kernel<2, 0, false, SH>;
+    case 3: return (const void*)dv::search1d_kernel<3, 0, false, SH>;
+    case 4: return (const void*)dv::search1d_kernel<4, 0, false, SH>;
+    default: return nullptr;
+  }
+}
+
+const Variant kTieredVariants[] = {
+    {"static512u4", 512, 4, false, tiered_variant_fn<dv::Shape<512, 4, 1, false>>},
+    {"static1024u2", 1024, 2, false, tiered_variant_fn<dv::Shape<1024, 2, 1, false>>},
+    {"clc1024u2", 1024, 2, true, tiered_variant_fn<dv::Shape<1024, 2, 1, true>>},
+    {"static1024u1", 1024, 1, false, tiered_variant_fn<dv::Shape<1024, 1, 1, false>>},
+};
+
+const Variant kVariants[] = {
+    {"static256u4", 256, 4, false, variant_fn<dv::Shape<256, 4, 4, false>>},
+    {"static512u4", 512, 4, false, variant_fn<dv::Shape<512, 4, 2, false>>},
+    {"clc256u4", 256, 4, true, variant_fn<dv::Shape<256, 4, 4, true>>},
+    {"clc256u8", 256, 8, true, variant_fn<dv::Shape<256, 8, 4, true>>},
+    {"clc256u2", 256, 2, true, variant_fn<dv::Shape<256, 2, 4, true>>},
+    {"clc512u4", 512, 4, true, variant_fn<dv::Shape<512, 4, 2, true>>},
+    {"clc512u2", 512, 2, true, variant_fn<dv::Shape<512, 2, 2, true>>},
+    {"clc1024u4", 1024, 4, true, variant_fn<dv::Shape<1024, 4, 1, true>>},
+    {"clc1024u2", 1024, 2, true, variant_fn<dv::Shape<1024, 2, 1, true>>},
+    {"clc128u8", 128, 8, true, variant_fn<dv::Shape<128, 8, 8, true>>},
+    {"static1024u4", 1024, 4, false, variant_fn<dv::Shape<1024, 4, 1, false>>},
+};
+
+eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* out, int64_t gofs,
+                         uint64_t* counters, cudaStream_t st) {
+  const bool cnt = counters != nullptr;
+  dv::SearchArgs a{};
+  a.image = (const uint4*)t->image_dev;
+  a.image_16 = (int32_t)(t->plan.image_bytes / 16);
+  a.ax = t->ax;
+  a.Y = Y;
+  a.out = out;
+  a.count = count;
+  a.gofs = gofs;
+  a.counters = (unsigned long long*)counters;
+  a.lv = t->levels_dev;
+  a.kv = t->levels_dev ? reinterpret_cast<const uint32_t*>(t->levels_dev + t->level_elems) : nullptr;
+  a.lv_top_len = 8 * t->top_n;
+  a.levels = t->levels;
+  // Vector body needs Y+head 16-B aligned and out+head 8-B aligned.
+  const uintptr_t ya = (uintptr_t)Y, oa = (uintptr_t)out;
+  a.head = (ya & 15) ? 1 : 0;
+  a.vec_ok = ((ya & 7) == 0) && (((oa + 4 * (uintptr_t)a.head) & 7) == 0) && count > a.head;
+  // One CTA per tile (CLC work stealing keeps ~#SM x occupancy of them
+  // resident); the static schedule uses a persistent grid instead.
+  const int64_t per_tile = (int64_t)t->threads[cnt] * t->unroll[cnt] * 2;
+  const int64_t tiles = (count - a.head + per_tile - 1) / per_tile;
+  if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;  // > 2^31 tiles (~4.4e12 targets) per call
+  a.ntiles = tiles;
+  int64_t grid = t->clc[cnt] ? tiles : std::min<int64_t>(t->grid[cnt], tiles);
+  grid = std::max<int64_t>(grid, 1);
+  void* params[] = {&a};
+  EOS_CUDA(launch(t->fn[cnt], grid, t->threads[cnt], (size_t)t->plan.image_bytes, st, params));
+  count_launch();
+  return EOS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+static int kind_of_k(int32_t k) { return k == EOS_K_AUTO ? EOS_HASH_AUTO : EOS_HASH_EXPONENT; }
+
+eos_status eos_plan_table(const double* table_host, int64_t n, int32_t k, eos_table_info_t* info,
+                          uint32_t* dir_out, int64_t cap) {
+  if (k != EOS_K_AUTO && k < 0) return EOS_ERR_UNSUPPORTED;
+  return eos_plan_table_hash(table_host, n, kind_of_k(k), k, info, dir_out, cap);
+}
+
+eos_status eos_plan_table_hash(const double* table_host, int64_t n, int32_t kind, int64_t param,
+                               eos_table_info_t* info, uint32_t* dir_out, int64_t cap) {
+  if (!info) return EOS_ERR_NULL;
+  TablePlan p;
+  eos_status st = eos::plan_table(table_host, n, kind, param, false, &p);
+  if (st != EOS_OK) return st;
+  if (dir_out) {
+    if (cap < p.bins) return EOS_ERR_SIZE;
+    memcpy(dir_out, p.dir.data(), 4 * (size_t)p.bins);
+  }
+  eos::fill_info(p, info);
+  return EOS_OK;
+}
+
+eos_status eos_search_create_ex(const double* table_host, int64_t n, int32_t k, eos_table* out) {
+  if (k != EOS_K_AUTO && k < 0) return EOS_ERR_UNSUPPORTED;
+  return eos_search_create_hash(table_host, n, kind_of_k(k), k, out);
+}
+
+eos_status eos_search_create_hash(const double* table_host, int64_t n, int32_t kind, int64_t param,
+                                  eos_table* out) {
+  return eos_search_create_levels(table_host, n, EOS_LEVELS_AUTO, kind, param, out);
+}
+
+eos_status eos_plan_table_levels(const double* table_host, int64_t n, int32_t levels, int32_t kind,
+                                 int64_t param, eos_table_info_t* info) {
+  if (!info) return EOS_ERR_NULL;
+  eos::TieredPlan tp;
+  eos_status st = eos::plan_tiered(table_host, n, levels, kind, param, &tp);
+  if (st != EOS_OK) return st;
+  eos::fill_info(tp, info);
+  return EOS_OK;
+}
+
+eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t levels,
+                                    int32_t kind, int64_t param, eos_table* out) {
+  if (!out) return EOS_ERR_NULL;
+  *out = nullptr;
+  eos_table t = new (std::nothrow) eos_table_s();
+  if (!t) return EOS_ERR_NOMEM;
+  std::vector<double> lv;
+  std::vector<uint32_t> keys;
+  {
+    eos::TieredPlan tp;
+    eos_status st = eos::plan_tiered(table_host, n, levels, kind, param, &tp);
+    if (st != EOS_OK) { delete t; return st; }
+    t->plan = std::move(tp.top);
+    t->levels = tp.levels;
+    t->n = tp.n;
+    t->top_n = tp.top_n;
+    t->level_bytes = 12 * tp.level_elems();
+    lv = std::move(tp.lv);
+    keys = std::move(tp.keys);
+    t->ax = axis_params(t->plan, 0);
+    t->ax.xlast = tp.x_last;  // X[n-1] of the full table (counter c4)
+  }
+  auto fail = [&](eos_status st) {
+    if (t->image_dev) cudaFree(t->image_dev);
+    if (t->levels_dev) cudaFree(t->levels_dev);
+    delete t;
+    return st;
+  };
+  cudaError_t e = cudaGetDevice(&t->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, t->device);
+  if (e != cudaSuccess) return fail(cuda_status(e));
+  eos_status st = upload(eos::make_image(t->plan), &t->image_dev);
+  if (st != EOS_OK) return fail(st);
+  if (t->levels > 0) {
+    // [F levels fp64][K levels u32], both coarsest first
+    e = cudaMalloc((void**)&t->levels_dev, (size_t)t->level_bytes);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(t->levels_dev, lv.data(), 8 * lv.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(reinterpret_cast<char*>(t->levels_dev) + 8 * lv.size(), keys.data(),
+                     4 * keys.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(cuda_status(e));
+    t->level_elems = (int64_t)lv.size();
+    std::vector<double>().swap(lv);
+    std::vector<uint32_t>().swap(keys);
+  }
+  for (int c = 0; c < 2 && st == EOS_OK; ++c) {
+    const bool cnt = c == 1;
+    if (t->levels > 0) {
+      t->fn[c] = t->plan.key_mode == 0 ? tiered_fn_mode<0, dv::ShapeTiered>(t->plan.steps, cnt)
+                                       : tiered_fn_mode<1, dv::ShapeTiered>(t->plan.steps, cnt);
+      using SH = dv::ShapeTiered;
+      t->threads[c] = cnt ? dv::ShapeCnt::kThreads : SH::kThreads;
+      t->unroll[c] = cnt ? dv::ShapeCnt::kUnroll : SH::kUnroll;
+      t->clc[c] = cnt ? dv::ShapeCnt::kClc : SH::kClc;
+    } else {
+      LaunchShape ls = pick_search(t->plan.key_mode, t->plan.steps, cnt, t->plan.image_bytes);
+      t->fn[c] = ls.fn;
+      t->threads[c] = ls.threads;
+      t->unroll[c] = ls.unroll;
+      t->clc[c] = ls.clc;
+    }
+    if (c == 0) {  // tuning experiments: launch-shape variants by name
+      const bool tiered = t->levels > 0;
+      const char* want = getenv(tiered ? "EOS_TIERED_VARIANT" : "EOS_SEARCH_VARIANT");
+      const Variant* vs = tiered ? kTieredVariants : kVariants;
+      const size_t nv = tiered ? sizeof(kTieredVariants) / sizeof(Variant)
+                               : sizeof(kVariants) / sizeof(Variant);
+      for (size_t i = 0; i < nv; ++i) {
+        const Variant& v = vs[i];
+        if (!want || strcmp(want, v.name) != 0 || t->plan.key_mode != 0) continue;
+        const void* f = v.get(t->plan.steps);
+        if (!f) break;
+        t->fn[0] = f;
+        t->threads[0] = v.threads;
+        t->unroll[0] = v.unroll;
+        t->clc[0] = v.clc;
+      }
+    }
+    st = configure(t->fn[c], t->threads[c], t->plan.image_bytes, t->num_sms, &t->grid[c],
+                   c == 0 ? &t->ctas_per_sm : nullptr);
+  }
+  if (st != EOS_OK) return fail(st);
+  *out = t;
+  return EOS_OK;
+}
+
+eos_status eos_search_create(const double* table_host, int64_t n, eos_table* out) {
+  return eos_search_create_ex(table_host, n, EOS_K_AUTO, out);
+}
+
+eos_status eos_search_ex(eos_table t, const double* targets_dev, int64_t count,
+                         int32_t* idx_out_dev, int64_t global_offset, uint64_t* counters_dev,
+                         void* stream) {
+  if (!t) return EOS_ERR_NULL;
+  if (count < 0 || count > (int64_t(1) << 62)) return EOS_ERR_SIZE;
+  if (count == 0) return EOS_OK;
+  if (!targets_dev || !idx_out_dev) return EOS_ERR_NULL;
+  if (overlaps(targets_dev, 8 * count, idx_out_dev, 4 * count)) return EOS_ERR_ALIAS;
+  eos_status st = check_device(t->device);
+  if (st != EOS_OK) return st;
+  return launch_search(t, targets_dev, count, idx_out_dev, global_offset, counters_dev,
+                       (cudaStream_t)stream);
+}
+
+eos_status eos_search(eos_table t, const double* targets_dev, int64_t count, int32_t* idx_out_dev,
+                      void* stream) {
+  return eos_search_ex(t, targets_dev, count, idx_out_dev, 0, nullptr, stream);
+}
+
+eos_status eos_search_host(eos_table t, const double* targets_host, int64_t count,
+                           int32_t* idx_out_host, void* stream) {
+  if (!t) return EOS_ERR_NULL;
+  if (count < 0 || count > (int64_t(1) << 62)) return EOS_ERR_SIZE;
+  if (count == 0) return EOS_OK;
+  if (!targets_host || !idx_out_host) return EOS_ERR_NULL;
+  if (overlaps(targets_host, 8 * count, idx_out_host, 4 * count)) return EOS_ERR_ALIAS;
+  eos_status st = check_device(t->device);
+  if (st != EOS_OK) return st;
+  const int64_t chunk = int64_t(1) << 23;  // 8 Mi targets: 64 MiB in + 32 MiB out per slot
+  return host_pipeline(
+      (cudaStream_t)stream, count, chunk, 12,
+      [&](cudaStream_t s, char* stage, int64_t slot_elems, int64_t off, int64_t len) -> eos_status {
+        double* dY = (double*)stage;
+        int32_t* dI = (int32_t*)(stage + 8 * slot_elems);
+        EOS_CUDA(cudaMemcpyAsync(dY, targets_host + off, 8 * len, cudaMemcpyHostToDevice, s));
+        eos_status r = launch_search(t, dY, len, dI, off, nullptr, s);
+        if (r != EOS_OK) return r;
+        EOS_CUDA(cudaMemcpyAsync(idx_out_host + off, dI, 4 * len, cudaMemcpyDeviceToHost, s));
+        return EOS_OK;
+      });
+}
+
+eos_status eos_search_direct(const double* table_dev, int64_t n, const double* targets_dev,
+                             int64_t count, int32_t* idx_out_dev, int32_t* status_dev,
+                             void* stream) {
+  if (n < 1 || n > dv::kDirectMaxTable) return EOS_ERR_SIZE;
+  if (count < 0 || count > (int64_t(1) << 62)) return EOS_ERR_SIZE;
+  if (!table_dev) return EOS_ERR_NULL;
+  if (count == 0) return EOS_OK;
+  if (!targets_dev || !idx_out_dev) return EOS_ERR_NULL;
+  if (overlaps(targets_dev, 8 * count, idx_out_dev, 4 * count) ||
+      overlaps(table_dev, 8 * n, idx_out_dev, 4 * count))
+    return EOS_ERR_ALIAS;
+  int dev = 0;
+  EOS_CUDA(cudaGetDevice(&dev));
+  using SH = dv::ShapeDirect;
+  const void* fn = (const void*)dv::search1d_direct_kernel<SH>;
+  int32_t bins_max = 1;
+  while (bins_max < 4 * n && bins_max < dv::kDirectMaxBins) bins_max <<= 1;
+  const int64_t smem = ((8 * n + 15) & ~int64_t(15)) + 4 * (int64_t)bins_max;
+  {  // one-time per device: allow the largest dynamic smem this kernel uses
+    static std::mutex mu;
+    static bool done[64] = {false};
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 64 && !done[dev]) {
+      const int64_t mx = ((8 * dv::kDirectMaxTable + 15) & ~int64_t(15)) + 4 * dv::kDirectMaxBins;
+      EOS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+      done[dev] = true;
+    }
+  }
+  dv::DirectArgs a{};
+  a.table = table_dev;
+  a.n = (int32_t)n;
+  a.bins_max = bins_max;
+  a.status = status_dev;
+  a.s.Y = targets_dev;
+  a.s.out = idx_out_dev;
+  a.s.count = count;
+  const uintptr_t ya = (uintptr_t)targets_dev, oa = (uintptr_t)idx_out_dev;
+  a.s.head = (ya & 15) ? 1 : 0;
+  a.s.vec_ok = ((ya & 7) == 0) && (((oa + 4 * (uintptr_t)a.s.head) & 7) == 0) && count > a.s.head;
+  const int64_t per_tile = (int64_t)SH::kTileElems;
+  const int64_t tiles = (count - a.s.head + per_tile - 1) / per_tile;
+  if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;
+  a.s.ntiles = tiles;
+  void* params[] = {&a};
+  EOS_CUDA(launch(fn, std::max<int64_t>(tiles, 1), SH::kThreads, (size_t)smem,
+                  (cudaStream_t)stream, params));
+  count_launch();
+  return EOS_OK;
+}
+
+eos_status eos_table_info(eos_table t, eos_table_info_t* out) {
+  if (!t || !out) return EOS_ERR_NULL;
+  eos::fill_info(t->plan, out);
+  out->n = t->n;
+  out->levels = t->levels;
+  out->top_n = t->top_n;
+  out->level_bytes = t->level_bytes;
+  out->device = t->device;
+  out->ctas_per_sm = t->ctas_per_sm;
+  return EOS_OK;
+}
+
+eos_status eos_search_destroy(eos_table t) {
+  if (!t) return EOS_ERR_NULL;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != t->device) cudaSetDevice(t->device);
+  cudaError_t e = cudaFree(t->image_dev);  // synchronises with in-flight work
+  if (t->levels_dev) {
+    cudaError_t e2 = cudaFree(t->levels_dev);
+    if (e == cudaSuccess) e = e2;
+  }
+  if (cur != t->device && cur >= 0) cudaSetDevice(cur);
+  delete t;
+  return cuda_status(e);
+}
+
+}  // extern "C"

@@ -127,7 +127,7 @@ double lifting_probes(int o, int S) {
 // wavefronts per warp of 32 lookups plus issue and occupancy terms:
 //   3.5 (random 4-B directory read) + 6.1 x E[executed 8-B probes]
 //   + 1 per in-bin step (issue) + a launch-shape penalty.
-// The shape (eossearch.cu::pick_search) keeps the smem of all resident image
+// The shape (search_api.cu::pick_search) keeps the smem of all resident image
 // copies <= ~144 KB per SM, leaving L1 for the in-flight streaming loads:
 // image <= 32 KB: 4 CTAs x 256 threads (penalty 0); <= 72 KB: 2 x 512 (1);
 // <= 144 KB: 1 x 1024 (1.5); up to 200 KB: 1 x 1024 with L1 squeezed (4.5).
@@ -169,7 +169,7 @@ double plan_cost(const TablePlan& p) {
 // 2-D kernel's smem is dominated by the grid and its S = 1 cell lookup reads
 // the probe unconditionally (kernels.cuh::axis_cell), so bigger directories
 // buy nothing there.
-// fill_budget > 0 (grid axes of REP 2 kernels, eossearch.cu): the smallest S,
+// fill_budget > 0 (grid axes of REP 2 kernels, grid_api.cu): the smallest S,
 // then the MOST bins within fill_budget bytes -- there a sparser directory
 // makes the second cell-record read rarer (kernels.cuh axis_cell_rec).
 // For search tables (!compact) fill_budget > 0 replaces the image budget
