@@ -1,4 +1,4 @@
-"""N>1 host logic on CPU: sharding + the counter all_reduce, world_size 2 over gloo.
+"""N>1 host logic on CPU: sharding + the counter all_reduce, world sizes 2 and 4 over gloo.
 
 On the GPU box the same code path runs with NCCL (bench.py under torchrun);
 here each rank computes its shard with the oracle (the CUDA path needs a
@@ -56,7 +56,7 @@ def _worker(rank, world, port, total, q):
     d.close()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_counters_allreduce_over_gloo_equals_global(world):
     import datagen
     import oracle
