@@ -40,7 +40,7 @@ extern "C" {
 #endif
 
 #define EOS_MAX_TABLE 16384 /* table entries staged in shared memory (fp64) */
-#define EOS_MAX_TABLE_TIERED (1 << 29) /* entries of a tiered table (EOS_MAX_TABLE 8^5) */
+#define EOS_MAX_TABLE_TIERED (1 << 29) /* entries of a tiered table */
 #define EOS_LEVELS_AUTO (-1)           /* eos_search_create_levels: choose D */
 #define EOS_MAX_K 19        /* mantissa bits appended to the exponent hash */
 #define EOS_K_AUTO (-1)     /* let eos_search_create_ex choose the hash */
@@ -86,7 +86,7 @@ typedef struct {
    * describe the shared-memory sample table T1 of top_n entries. */
   int32_t levels;      /* D: 8-ary levels in global memory */
   int32_t pad_;
-  int64_t top_n;       /* n1 = ceil(n / 8^D) */
+  int64_t top_n;       /* n1 = ceil(n / 8^D) (image_bytes then counts 4 B per T1 entry) */
   int64_t level_bytes; /* device bytes of the levels (0 when D == 0) */
 } eos_table_info_t;
 
@@ -163,20 +163,21 @@ EOS_API eos_status eos_search_create_hash(const double* table_host, int64_t n, i
  * call this with levels = EOS_LEVELS_AUTO, so they accept the same n.
  *   levels = D: 0 = the whole table (and directory) in shared memory
  *     (n <= EOS_MAX_TABLE); D >= 1 (<= 5) = a two-level structure: the
- *     sample table T1[j] = X[j 8^D], j < n1 = ceil(n/8^D) <= EOS_MAX_TABLE,
- *     with its hash directory in shared memory, and D 8-ary levels in device
+ *     sample table T1[j] = X[j 8^D], j < n1 = ceil(n/8^D) <= 32768, held as
+ *     the 32-bit keys of its values with its hash directory in shared
+ *     memory (equal keys settled from the fp64 values), and D 8-ary levels in device
  *     memory, level d (d = D-1..0) holding F_d[j] = X[j 8^d] (fp64) and the
  *     32-bit order-preserving keys of those values (upper words), padded to
  *     n1 8^(D-d) entries (~1.7 x 8n bytes in all).  A level step reads the
  *     8 keys of a node (one 32-byte sector): c = #{t : key_t < key(y)}, and
  *     the node's fp64 values only when a key equals key(y); b = 8b + c - 1.
  *     EOS_LEVELS_AUTO: D = 0 if n <= EOS_MAX_TABLE, else the smallest D with
- *     n1 <= EOS_MAX_TABLE.
+ *     n1 <= 32768.
  *   kind/param: the hash of the shared-memory table (T1 when D >= 1), as in
  *     eos_search_create_hash.
- * Errors: EOS_ERR_SIZE (n out of range, or n1 > EOS_MAX_TABLE for the given
- * D), EOS_ERR_UNSUPPORTED (D > 5), EOS_ERR_NOMEM, plus the table errors of
- * eos_plan_table. */
+ * Errors: EOS_ERR_SIZE (n out of range, or n1 too large for the given D:
+ * > EOS_MAX_TABLE at D = 0, > 32768 at D >= 1), EOS_ERR_UNSUPPORTED (D > 5),
+ * EOS_ERR_NOMEM, plus the table errors of eos_plan_table. */
 EOS_API eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t levels,
                                             int32_t kind, int64_t param, eos_table* out);
 

@@ -56,7 +56,8 @@ struct TablePlan {
 // 59 KB by 6%), a 198 KB image loses 18% on cfg5 but wins 39% at n = 16384.
 constexpr int64_t kAutoImageBudget = 200 * 1024;
 constexpr int64_t kAxisImageBudget = 16 * 1024;  // per axis of a 2-D grid (the grid owns smem)
-constexpr int64_t kTieredImageBudget = 160 * 1024;  // cap of a tiered table's sample-table image
+constexpr int64_t kTieredImageBudget = 176 * 1024;  // cap of a tiered table's sample-table image
+constexpr int64_t kMaxTopKeys = 32768;  // sample-table entries of a tiered table (32-bit keys)
 constexpr int64_t kMaxImage = 200 * 1024;  // explicit requests beyond this do not fit in smem
 
 // Validate + build (eos_plan_table_hash semantics).  kind/param: see
@@ -67,11 +68,17 @@ constexpr int64_t kMaxImage = 200 * 1024;  // explicit requests beyond this do n
 // fits fill_budget bytes (instead of the smallest image); search tables: if
 // > 0, the image budget of the automatic choice (default kAutoImageBudget).
 eos_status plan_table(const double* X, int64_t n, int kind, int64_t param, bool strict,
-                      TablePlan* out, int64_t fill_budget = 0);
+                      TablePlan* out, int64_t fill_budget = 0, int64_t max_n = EOS_MAX_TABLE);
+
+// Shared-memory image of a tiered table's sample table: the 32-bit keys of
+// T1 (key_hi, the table's key mode) | directory, each 16-B padded.
+std::vector<uint8_t> make_key_image(const TablePlan& p);
+int64_t key_image_bytes(const TablePlan& p);
 
 // Tables larger than shared memory (eossearch.h
 // eos_search_create_levels).  D 8-ary levels in global memory under a
-// shared-memory sample table T1[j] = X[j 8^D], j < n1 = ceil(n / 8^D).
+// shared-memory sample table T1[j] = X[j 8^D], j < n1 = ceil(n / 8^D) <=
+// kMaxTopKeys, held as 32-bit keys (make_key_image).
 // Level d (stride 8^d, d = 0..D-1) has n1 8^(D-d) entries
 //   F_d[j] = X[j 8^d]            (fp64; NaN past n: never <= y)
 //   K_d[j] = key_hi(F_d[j])      (u32 order-preserving upper word of the
@@ -80,7 +87,7 @@ eos_status plan_table(const double* X, int64_t n, int kind, int64_t param, bool 
 // back to the node's 8 fp64 values only when a key equals the target's.
 // Both arrays store their levels coarsest first (D-1, .., 0); level d starts
 // at element n1 (8^(D-d) - 8) / 7 and F level 0 is X itself.
-constexpr int kMaxLevels = 5;  // n <= EOS_MAX_TABLE 8^5 = 2^29
+constexpr int kMaxLevels = 5;  // n <= 2^29 (EOS_MAX_TABLE_TIERED)
 constexpr int kFanout = 8;
 struct TieredPlan {
   int levels = 0;             // D (0: single-level smem table, `top` is the table)
@@ -94,7 +101,7 @@ struct TieredPlan {
 };
 
 // levels: EOS_LEVELS_AUTO (0 if n <= EOS_MAX_TABLE, else the smallest D with
-// n1 <= EOS_MAX_TABLE) or 0..kMaxLevels.  kind/param: the hash of T1.
+// n1 <= kMaxTopKeys) or 0..kMaxLevels.  kind/param: the hash of T1.
 eos_status plan_tiered(const double* X, int64_t n, int levels, int kind, int64_t param,
                        TieredPlan* out);
 

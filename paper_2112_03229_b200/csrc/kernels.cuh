@@ -212,7 +212,8 @@ __device__ __forceinline__ void ldg_f64x4(const double* p, double& a, double& b,
 }
 
 // TieredLookup (tables larger than shared memory): the smem
-// table is the sample T1[j] = X[j 8^D] (n1 entries) with its directory; the
+// table is the sample T1[j] = X[j 8^D] (n1 entries, as 32-bit keys:
+// lookup_keys) with its directory; the
 // full table lives in global memory (L2-resident) as D 8-ary levels, level d
 // holding F_d[j] = X[j 8^d] (NaN past n) and their keys K_d[j] =
 // key_hi(F_d[j]) (0xFFFFFFFF past n).  Per target:
@@ -228,9 +229,55 @@ __device__ __forceinline__ void ldg_f64x4(const double* p, double& a, double& b,
 // X[(b+1) 8^(d+1)] (or past the end), so c >= 1 for every y >= X[0].  At
 // d = 0 the stride is 1 and b = #{X <= y} - 1.  All targets of a
 // thread go through a level together so their sector loads overlap.
+// The shared-memory sample table of a tiered table holds the 32-bit keys of
+// T1 (4 B per entry, so up to 32768 entries fit), binned by the same hash.
+// Lifting counts the bin's keys < key(y) -- key order is value order -- and
+// the (rare) entries whose key equals key(y) are settled exactly from their
+// fp64 values, T1[j] = F_{D-1}[8 j] in global memory.
+template <int S, int MODE>
+__device__ __forceinline__ int32_t lookup_keys(double y, uint32_t ky,
+                                               const uint32_t* __restrict__ sK,
+                                               const uint32_t* __restrict__ sD,
+                                               const AxisParams& a,
+                                               const double* __restrict__ ftop) {
+  const uint32_t b = MODE == 0 ? bin_of_m0(ky, a) : bin_of(ky, a);
+  EOS_DCHECK(b <= a.bmax);
+  const uint32_t d = sD[b];
+  const int32_t lo = (int32_t)(d & 0xFFFFu);
+  const int32_t occ = (int32_t)(d >> 16);
+  EOS_DCHECK(lo + occ <= a.n && occ < (1 << (S > 0 ? S : a.steps)));
+  int32_t c = 0;
+  if (S > 0) {
+#pragma unroll
+    for (int s = 1 << (S > 0 ? S - 1 : 0); s > 0; s >>= 1) {
+      const int32_t j = c + s;
+      if (j <= occ) {
+        if (sK[lo + j - 1] < ky) c = j;
+      }
+    }
+  } else {
+    for (int s = 1 << (a.steps - 1); s > 0; s >>= 1) {
+      const int32_t j = c + s;
+      if (j <= occ) {
+        if (sK[lo + j - 1] < ky) c = j;
+      }
+    }
+  }
+  if (c < occ && sK[lo + c] == ky) {
+    // Equal keys (rare): binary lifting over the rest of the bin with the
+    // exact values.  "key == key(y) and X <= y" holds on a prefix of it (the
+    // equal keys come first, sorted by value; larger keys hold larger values).
+    for (int32_t st = 1 << (31 - __clz(occ - c)); st > 0; st >>= 1) {
+      const int32_t j = c + st;
+      if (j <= occ && sK[lo + j - 1] == ky && __ldg(ftop + 8 * (int64_t)(lo + j - 1)) <= y) c = j;
+    }
+  }
+  return (y >= a.x0) ? (lo + c - 1) : 0;
+}
+
 template <int S, int MODE>
 struct TieredLookup {
-  const double* __restrict__ sX;  // T1 (smem)
+  const uint32_t* __restrict__ sK;  // keys of T1 (smem)
   const uint32_t* __restrict__ sD;
   AxisParams a;                   // of T1, except xlast = X[n-1] (counter c4)
   const double* __restrict__ lv;  // F level D-1 (global)
@@ -244,8 +291,8 @@ struct TieredLookup {
     uint32_t ky[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      b[i] = lookup<S, MODE>(y[i], sX, sD, a);
       ky[i] = key_hi<MODE>(y[i]);
+      b[i] = lookup_keys<S, MODE>(y[i], ky[i], sK, sD, a, lv);
     }
     const double* F = lv;
     const uint32_t* K = kv;
@@ -538,7 +585,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
   const AxisParams a = args.ax;
   EOS_DCHECK(args.levels >= 1 && args.lv_top_len == 8 * (int64_t)a.n);
   TieredLookup<S, MODE> lk;
-  lk.sX = reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
+  lk.sK = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(smem) + a.x_off);
   lk.sD = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(smem) + a.d_off);
   lk.a = a;
   lk.lv = args.lv;

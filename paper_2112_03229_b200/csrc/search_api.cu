@@ -35,6 +35,7 @@ struct eos_table_s {
   void* image_dev = nullptr;
   dv::AxisParams ax{};
   // launch configuration per counters on/off
+  int64_t smem_bytes = 0;  // the staged image (fp64 table, or the keys of T1 when tiered)
   const void* fn[2] = {nullptr, nullptr};
   int grid[2] = {0, 0};
   int threads[2] = {256, 256};
@@ -177,7 +178,7 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
   const bool cnt = counters != nullptr;
   dv::SearchArgs a{};
   a.image = (const uint4*)t->image_dev;
-  a.image_16 = (int32_t)(t->plan.image_bytes / 16);
+  a.image_16 = (int32_t)(t->smem_bytes / 16);
   a.ax = t->ax;
   a.Y = Y;
   a.out = out;
@@ -201,7 +202,7 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
   int64_t grid = t->clc[cnt] ? tiles : std::min<int64_t>(t->grid[cnt], tiles);
   grid = std::max<int64_t>(grid, 1);
   void* params[] = {&a};
-  EOS_CUDA(launch(t->fn[cnt], grid, t->threads[cnt], (size_t)t->plan.image_bytes, st, params));
+  EOS_CUDA(launch(t->fn[cnt], grid, t->threads[cnt], (size_t)t->smem_bytes, st, params));
   count_launch();
   return EOS_OK;
 }
@@ -273,6 +274,12 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
     keys = std::move(tp.keys);
     t->ax = axis_params(t->plan, 0);
     t->ax.xlast = tp.x_last;  // X[n-1] of the full table (counter c4)
+    if (t->levels > 0) {  // the sample table is staged as 32-bit keys
+      t->ax.d_off = (int32_t)((4 * t->plan.n + 15) & ~int64_t(15));
+      t->smem_bytes = eos::key_image_bytes(t->plan);
+    } else {
+      t->smem_bytes = t->plan.image_bytes;
+    }
   }
   auto fail = [&](eos_status st) {
     if (t->image_dev) cudaFree(t->image_dev);
@@ -283,7 +290,8 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
   cudaError_t e = cudaGetDevice(&t->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, t->device);
   if (e != cudaSuccess) return fail(cuda_status(e));
-  eos_status st = upload(eos::make_image(t->plan), &t->image_dev);
+  eos_status st = upload(t->levels > 0 ? eos::make_key_image(t->plan) : eos::make_image(t->plan),
+                         &t->image_dev);
   if (st != EOS_OK) return fail(st);
   if (t->levels > 0) {
     // [F levels fp64][K levels u32], both coarsest first
@@ -308,7 +316,7 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
       t->unroll[c] = cnt ? dv::ShapeCnt::kUnroll : SH::kUnroll;
       t->clc[c] = cnt ? dv::ShapeCnt::kClc : SH::kClc;
     } else {
-      LaunchShape ls = pick_search(t->plan.key_mode, t->plan.steps, cnt, t->plan.image_bytes);
+      LaunchShape ls = pick_search(t->plan.key_mode, t->plan.steps, cnt, t->smem_bytes);
       t->fn[c] = ls.fn;
       t->threads[c] = ls.threads;
       t->unroll[c] = ls.unroll;
@@ -331,7 +339,7 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
         t->clc[0] = v.clc;
       }
     }
-    st = configure(t->fn[c], t->threads[c], t->plan.image_bytes, t->num_sms, &t->grid[c],
+    st = configure(t->fn[c], t->threads[c], t->smem_bytes, t->num_sms, &t->grid[c],
                    c == 0 ? &t->ctas_per_sm : nullptr);
   }
   if (st != EOS_OK) return fail(st);
@@ -442,6 +450,7 @@ eos_status eos_table_info(eos_table t, eos_table_info_t* out) {
   out->levels = t->levels;
   out->top_n = t->top_n;
   out->level_bytes = t->level_bytes;
+  out->image_bytes = t->smem_bytes;
   out->device = t->device;
   out->ctas_per_sm = t->ctas_per_sm;
   return EOS_OK;

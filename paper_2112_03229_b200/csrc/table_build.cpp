@@ -214,9 +214,9 @@ eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, Table
 }  // namespace
 
 eos_status plan_table(const double* Xin, int64_t n, int kind, int64_t param, bool strict,
-                      TablePlan* out, int64_t fill_budget) {
+                      TablePlan* out, int64_t fill_budget, int64_t max_n) {
   if (!Xin || !out) return EOS_ERR_NULL;
-  if (n < (strict ? 2 : 1) || n > EOS_MAX_TABLE) return EOS_ERR_SIZE;
+  if (n < (strict ? 2 : 1) || n > max_n) return EOS_ERR_SIZE;
   if (kind == EOS_HASH_EXPONENT && (param < 0 || param > EOS_MAX_K)) return EOS_ERR_UNSUPPORTED;
   if (kind == EOS_HASH_LOG && (param < 1 || param > (int64_t(1) << 22))) return EOS_ERR_UNSUPPORTED;
   if (kind != EOS_HASH_AUTO && kind != EOS_HASH_EXPONENT && kind != EOS_HASH_LOG)
@@ -255,12 +255,15 @@ eos_status plan_tiered(const double* Xin, int64_t n, int levels, int kind, int64
   auto pow8 = [](int d) { return int64_t(1) << (3 * d); };
   if (levels == EOS_LEVELS_AUTO) {
     levels = 0;
-    while ((n + pow8(levels) - 1) / pow8(levels) > EOS_MAX_TABLE) ++levels;
+    if (n > EOS_MAX_TABLE) {
+      levels = 1;
+      while ((n + pow8(levels) - 1) / pow8(levels) > kMaxTopKeys) ++levels;
+    }
   }
   if (levels < 0 || levels > kMaxLevels) return EOS_ERR_UNSUPPORTED;
   const int64_t stride = pow8(levels);  // 8^D
   const int64_t n1 = (n + stride - 1) / stride;
-  if (n1 > EOS_MAX_TABLE) return EOS_ERR_SIZE;
+  if (n1 > (levels == 0 ? EOS_MAX_TABLE : kMaxTopKeys)) return EOS_ERR_SIZE;
   TieredPlan t;
   t.levels = levels;
   t.n = n;
@@ -309,19 +312,33 @@ eos_status plan_tiered(const double* Xin, int64_t n, int levels, int kind, int64
   }
   std::vector<double> T1((size_t)n1);
   for (int64_t j = 0; j < n1; ++j) T1[j] = L0[j * stride];
-  // Image budget of the sample table (measured, profiles/r01_exp_table_size.json:
-  // a directory of ~2 bins per entry (S = 2) beats the single-level choice of
-  // a 140 KB directory -- n = 2^15: 211 against 119 Glookups/s -- while
-  // larger ones lose again): X + max(32 KB, 4 n1) bytes of directory, at
-  // most 160 KB in all.
+  // Image budget of the sample table, measured (profiles/r01_exp_table_size.json,
+  // r01_exp_tiered_bins.json): 4 n1 bytes of keys + max(48 KB, 8 n1) bytes of
+  // directory (~2-3 bins per entry, S = 2), at most kTieredImageBudget.  At
+  // n = 2^15 a 49-64 KB image runs at 196 Glookups/s and >= 80 KB at 131:
+  // the smaller carveout leaves L1 room for the 128 KB top key level.
+  // plan_table budgets fp64 entries, so it is given 4 n1 more.
   const int64_t budget = std::min<int64_t>(kTieredImageBudget,
-                                           8 * n1 + std::max<int64_t>(32 * 1024, 4 * n1));
-  eos_status st = plan_table(T1.data(), n1, kind, param, false, &t.top, budget);
+                                           4 * n1 + std::max<int64_t>(48 * 1024, 8 * n1));
+  eos_status st = plan_table(T1.data(), n1, kind, param, false, &t.top, budget + 4 * n1,
+                             kMaxTopKeys);
   if (st != EOS_OK) return st;
   // key mode of T1 is that of X (T1[0] = X[0])
   t.x_last = L0[n - 1];
   *out = std::move(t);
   return EOS_OK;
+}
+
+int64_t key_image_bytes(const TablePlan& p) { return pad16(4 * p.n) + pad16(4 * p.bins); }
+
+std::vector<uint8_t> make_key_image(const TablePlan& p) {
+  std::vector<uint8_t> img((size_t)key_image_bytes(p), 0);
+  for (int64_t j = 0; j < p.n; ++j) {
+    const uint32_t k = key_hi(p.X[j], p.key_mode);
+    memcpy(img.data() + 4 * j, &k, 4);
+  }
+  memcpy(img.data() + pad16(4 * p.n), p.dir.data(), (size_t)(4 * p.bins));
+  return img;
 }
 
 std::vector<uint8_t> make_image(const TablePlan& p) {
@@ -352,6 +369,7 @@ void fill_info(const TablePlan& p, eos_table_info_t* info) {
 
 void fill_info(const TieredPlan& t, eos_table_info_t* info) {
   fill_info(t.top, info);
+  if (t.levels > 0) info->image_bytes = key_image_bytes(t.top);  // keys, not fp64
   info->n = t.n;
   info->levels = t.levels;
   info->top_n = t.top_n;

@@ -297,26 +297,26 @@ def test_auto_choice_never_worse_in_steps_than_any_exponent_k():
 # ------------------------------------------------- tiered tables (f4) ------
 def test_tiered_plan_levels_and_sizes():
     """eos_plan_table_levels (eossearch.h): D = 0 up to EOS_MAX_TABLE, then the
-    smallest D with n1 = ceil(n/8^D) <= EOS_MAX_TABLE; levels hold n1 8^(D-d)
-    entries each (d = 0..D-1), 8 B fp64 + 4 B key; the smem table is the plan
-    of X[::8^D]."""
+    smallest D with n1 = ceil(n/8^D) <= 32768; levels hold n1 8^(D-d) entries each
+    (d = 0..D-1), 8 B fp64 + 4 B key; the smem image holds the sample table
+    X[::8^D] as 32-bit keys plus its directory."""
     rng = np.random.default_rng(7)
-    for n, D in [(1, 0), (16384, 0), (16385, 1), (131072, 1), (131073, 2), (1 << 20, 2),
-                 ((1 << 20) + 1, 3)]:
+    pad16 = lambda b: (b + 15) // 16 * 16  # noqa: E731
+    for n, D in [(1, 0), (16384, 0), (16385, 1), (262144, 1), (262145, 2), (1 << 20, 2),
+                 (1 << 21, 2), ((1 << 21) + 1, 3)]:
         X = np.sort(10.0 ** rng.uniform(-6, 10, n))
         info = eos.plan_table_levels(X)
         assert info.levels == D and info.n == n, (n, info.levels)
         n1 = -(-n // 8 ** D)
-        assert info.top_n == n1 <= eos.EOS_MAX_TABLE
+        assert info.top_n == n1 <= (eos.EOS_MAX_TABLE if D == 0 else 32768)
         assert info.level_bytes == 12 * sum(n1 * 8 ** (D - d) for d in range(D))
         if D == 0:   # the single-level plan
             top, _ = eos.plan_table(X, with_directory=False)
             for f in ("bins", "max_occ", "steps", "k", "hash_kind", "hash_mult", "image_bytes"):
                 assert getattr(info, f) == getattr(top, f), (n, f)
-        else:        # the sample table X[::8^D] under the tiered image budget
-            budget = min(160 * 1024, 8 * n1 + max(32 * 1024, 4 * n1))
-            pad16 = lambda b: (b + 15) // 16 * 16  # noqa: E731
-            assert info.image_bytes == pad16(8 * n1) + pad16(4 * info.bins) <= budget
+        else:        # keys of the sample table X[::8^D] under the tiered image budget
+            budget = min(176 * 1024, 4 * n1 + max(48 * 1024, 8 * n1))
+            assert info.image_bytes == pad16(4 * n1) + pad16(4 * info.bins) <= budget
             assert info.steps == int(np.ceil(np.log2(info.max_occ + 1)))
             if info.hash_kind == eos.EOS_HASH_EXPONENT:
                 ref, _ = eos.plan_table(X[::8 ** D], k=info.k, with_directory=False)
