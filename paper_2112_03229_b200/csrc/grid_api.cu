@@ -8,8 +8,6 @@
 #include <string.h>
 
 #include <algorithm>
-#include <atomic>
-#include <mutex>
 #include <new>
 #include <vector>
 

@@ -11,14 +11,11 @@
 //   EOS_PDL (0/1)                           programmatic dependent launch
 //   EOS_HOST_SLOTS, EOS_HOST_CHUNK_LOG2     host-buffer pipeline depth / chunk
 #include <cuda_runtime.h>
-#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
-#include <string.h>
 
 #include <algorithm>
 #include <atomic>
-#include <mutex>
 #include <new>
 #include <vector>
 

@@ -2,13 +2,11 @@
 // handles (single-level and tiered), the search launches, the zero-setup
 // search, host-only planning.  Product path (never includes or links oracle/).
 #include <cuda_runtime.h>
-#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
-#include <atomic>
 #include <mutex>
 #include <new>
 #include <vector>
@@ -33,9 +31,9 @@ struct eos_table_s {
   int device = -1;
   int num_sms = 0;
   void* image_dev = nullptr;
+  int64_t smem_bytes = 0;  // the staged image (fp64 table, or the keys of T1 when tiered)
   dv::AxisParams ax{};
   // launch configuration per counters on/off
-  int64_t smem_bytes = 0;  // the staged image (fp64 table, or the keys of T1 when tiered)
   const void* fn[2] = {nullptr, nullptr};
   int grid[2] = {0, 0};
   int threads[2] = {256, 256};
