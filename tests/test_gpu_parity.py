@@ -1033,3 +1033,21 @@ def test_plain_c_program_uses_the_abi(tmp_path):
         ref = oracle.search(X, Y)
         assert_same(np.frombuffer((tmp_path / "i.i32").read_bytes(), dtype=np.int32), ref, Y)
         assert_same(np.frombuffer((tmp_path / "h.i32").read_bytes(), dtype=np.int32), ref, Y)
+
+
+def test_paper_shaped_run_full_bit_exact():
+    """The paper-shaped run (R17): n = 110 log-spaced over [3e-6, 5.4e4],
+    5e6 targets log-uniform over 1e-10..1e10 (about half out of range), in full."""
+    w = datagen.workload("paper")
+    Yd = torch.empty(w.count, dtype=torch.float64, device=DEV)
+    w.targets.device_fill(Yd, 0)
+    t = eos.Table(w.table)
+    out = t.search(Yd)
+    torch.cuda.synchronize()
+    Y = w.targets.host_fill(0, w.count)
+    assert np.array_equal(Yd.cpu().numpy(), Y)
+    ref = oracle.search(w.table, Y)
+    assert_same(out.cpu().numpy(), ref, Y)
+    inside = np.mean((Y >= w.table[0]) & (Y <= w.table[-1]))
+    assert 0.45 < inside < 0.55
+    t.close()
