@@ -40,6 +40,10 @@ struct eos_table_s {
   int unroll[2] = {4, 4};
   bool clc[2] = {true, true};
   int ctas_per_sm = 0;
+  // small launches (pick_search_small; fn_small == nullptr: none)
+  const void* fn_small = nullptr;
+  int threads_small = 0, unroll_small = 0, grid_small = 0;
+  bool clc_small = true;
 };
 
 namespace {
@@ -130,6 +134,35 @@ LaunchShape pick_search(int mode, int steps, bool cnt, int64_t image_bytes) {
   return {search_fn_shape<dv::ShapeMid>(mode, steps, false), 512, 4, true};
 }
 
+// Small launches: the same shapes with one double2 per thread per tile (4x
+// smaller tiles), used when the default tiling would leave most SMs idle (fewer
+// tiles than half the SMs).  1e5 targets (25-49 default tiles): cfg1 37 -> 62,
+// cfg2 39 -> 64, cfg5 34 -> 48 Glookups/s; between 1.5e5 and 3e5 targets the two
+// are within launch noise, from 3.5e5 on they are the same kernel.
+template <int MODE, class SH>
+const void* small_fn_mode(int steps) {
+  switch (steps) {
+    case 1: return (const void*)dv::search1d_kernel<1, MODE, false, SH>;
+    case 2: return (const void*)dv::search1d_kernel<2, MODE, false, SH>;
+    case 3: return (const void*)dv::search1d_kernel<3, MODE, false, SH>;
+    case 4: return (const void*)dv::search1d_kernel<4, MODE, false, SH>;
+    default: return nullptr;  // deeper bins: the default tiles only
+  }
+}
+
+template <class SH>
+LaunchShape small_shape(int mode, int steps) {
+  return {mode == 0 ? small_fn_mode<0, SH>(steps) : small_fn_mode<1, SH>(steps), SH::kThreads,
+          SH::kUnroll, SH::kClc};
+}
+
+LaunchShape pick_search_small(int mode, int steps, int64_t image_bytes) {
+  if (image_bytes > 72 * 1024) return small_shape<dv::Shape<1024, 1, 1, false>>(mode, steps);
+  if (steps >= 3) return small_shape<dv::Shape<512, 1, 2, false>>(mode, steps);
+  if (image_bytes <= 32 * 1024) return small_shape<dv::Shape<256, 1, 4, true>>(mode, steps);
+  return small_shape<dv::Shape<512, 1, 2, true>>(mode, steps);
+}
+
 // Launch-shape variants for tuning experiments (EOS_SEARCH_VARIANT=<name> at
 // create time; mode 0, S <= 4, no counters).  Not part of the C ABI.
 struct Variant {
@@ -169,6 +202,10 @@ const Variant kVariants[] = {
     {"clc1024u2", 1024, 2, true, variant_fn<dv::Shape<1024, 2, 1, true>>},
     {"clc128u8", 128, 8, true, variant_fn<dv::Shape<128, 8, 8, true>>},
     {"static1024u4", 1024, 4, false, variant_fn<dv::Shape<1024, 4, 1, false>>},
+    {"clc256u1", 256, 1, true, variant_fn<dv::Shape<256, 1, 4, true>>},
+    {"clc512u1", 512, 1, true, variant_fn<dv::Shape<512, 1, 2, true>>},
+    {"clc128u2", 128, 2, true, variant_fn<dv::Shape<128, 2, 8, true>>},
+    {"static256u2", 256, 2, false, variant_fn<dv::Shape<256, 2, 4, false>>},
 };
 
 eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* out, int64_t gofs,
@@ -193,14 +230,22 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
   a.vec_ok = ((ya & 7) == 0) && (((oa + 4 * (uintptr_t)a.head) & 7) == 0) && count > a.head;
   // One CTA per tile (CLC work stealing keeps ~#SM x occupancy of them
   // resident); the static schedule uses a persistent grid instead.
-  const int64_t per_tile = (int64_t)t->threads[cnt] * t->unroll[cnt] * 2;
-  const int64_t tiles = (count - a.head + per_tile - 1) / per_tile;
+  int64_t per_tile = (int64_t)t->threads[cnt] * t->unroll[cnt] * 2;
+  int64_t tiles = (count - a.head + per_tile - 1) / per_tile;
+  // fewer tiles than half the SMs: the small-tile shape spreads the launch over 4x more CTAs
+  const bool sm = !cnt && t->fn_small && 2 * tiles < t->num_sms;
+  if (sm) {
+    per_tile = (int64_t)t->threads_small * t->unroll_small * 2;
+    tiles = (count - a.head + per_tile - 1) / per_tile;
+  }
   if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;  // > 2^31 tiles (~4.4e12 targets) per call
   a.ntiles = tiles;
-  int64_t grid = t->clc[cnt] ? tiles : std::min<int64_t>(t->grid[cnt], tiles);
+  const bool clc = sm ? t->clc_small : t->clc[cnt];
+  int64_t grid = clc ? tiles : std::min<int64_t>(sm ? t->grid_small : t->grid[cnt], tiles);
   grid = std::max<int64_t>(grid, 1);
   void* params[] = {&a};
-  EOS_CUDA(launch(t->fn[cnt], grid, t->threads[cnt], (size_t)t->smem_bytes, st, params));
+  EOS_CUDA(launch(sm ? t->fn_small : t->fn[cnt], grid, sm ? t->threads_small : t->threads[cnt],
+                  (size_t)t->smem_bytes, st, params));
   count_launch();
   return EOS_OK;
 }
@@ -341,6 +386,17 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
                    c == 0 ? &t->ctas_per_sm : nullptr);
   }
   if (st != EOS_OK) return fail(st);
+  const char* small_env = getenv("EOS_SMALL_TILES");  // "0": default tiles only
+  if (t->levels == 0 && !getenv("EOS_SEARCH_VARIANT") && !(small_env && small_env[0] == '0')) {
+    const LaunchShape ls = pick_search_small(t->plan.key_mode, t->plan.steps, t->smem_bytes);
+    if (ls.fn && configure(ls.fn, ls.threads, t->smem_bytes, t->num_sms, &t->grid_small,
+                           nullptr) == EOS_OK) {
+      t->fn_small = ls.fn;
+      t->threads_small = ls.threads;
+      t->unroll_small = ls.unroll;
+      t->clc_small = ls.clc;
+    }
+  }
   *out = t;
   return EOS_OK;
 }
