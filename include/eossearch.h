@@ -269,8 +269,10 @@ EOS_API eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, cons
                            *   dP/drho = P (d ln P / d ln rho) / rho on the cell. */
 #define EOS_GRID_GLOBAL 2 /* flag bit: keep the grid in device memory even if it would fit in
                            * shared memory (grids whose P does not fit, n_rho n_T 8 B >
-                           * ~200 KB, always live there): row pairs (G[i][j], G[i][j+1]) read
-                           * with two 16-byte loads per pair; the axes stay in shared memory
+                           * ~200 KB, always live there): cell quads (the 4 corners of a cell,
+                           * 32 B, read with one load per pair; 4x the grid) up to 1 GB of
+                           * quads, else row pairs (G[i][j], G[i][j+1]) read with two 16-byte
+                           * loads per pair (2x the grid); the axes stay in shared memory
                            * (their images must fit: ~220 KB).  Same results. */
 #define EOS_MAX_GRID_CELLS ((int64_t)1 << 28) /* n_rho n_T (EOS_ERR_SIZE above) */
 EOS_API eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const double* T_host,

@@ -41,7 +41,8 @@ struct eos_grid2d_s {
   int32_t rep_shift = 0;       // REP 2: log2 of the record copies
   int64_t rep_bytes_axis = 0;  // image bytes per axis entry of the REP layout
   bool gg = false;          // grid in device memory (GG kernels)
-  void* grid_dev = nullptr;  // GG: row pairs (double2[n_rho (n_T - 1)])
+  void* grid_dev = nullptr;  // GG: cell quads (double4[(n_rho - 1)(n_T - 1)]) or row pairs
+  bool gquad = false;        //     (double2[n_rho (n_T - 1)])
   int64_t grid_bytes = 0;
 };
 
@@ -157,6 +158,7 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   a.rr_off = g->rr_off;
   a.rt_off = g->rt_off;
   a.gq = reinterpret_cast<const double2*>(g->grid_dev);
+  a.gquad = g->gquad ? 1 : 0;
   a.rep_shift = g->rep_shift;
   a.r = g->ar;
   a.t = g->at;
@@ -228,7 +230,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   }
   // image: [rho X | rho dir][T X | T dir][G][1/dR][1/dT (RECIP variants)][ln R][ln T][R recs][T recs]
   // G is absent for grids in device memory (GG: larger than ~220 KB, or
-  // EOS_GRID_GLOBAL), which keep it as row pairs in g->grid_dev instead.
+  // EOS_GRID_GLOBAL), which keep it in g->grid_dev instead (cell quads or row pairs).
   int64_t r_bytes = g->pr.image_bytes, t_bytes = g->pt.image_bytes;
   // 1/dR, 1/dT arrays: only for the RECIP tuning variants (EOS_INTERP_VARIANT 5, 6)
   const char* ev = getenv("EOS_INTERP_VARIANT");
@@ -348,19 +350,36 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   if (e != cudaSuccess) return fail(cuda_status(e));
   st = upload(img, &g->image_dev);
   if (st != EOS_OK) return fail(st);
-  if (g->gg) {  // row pairs gq[i (nT-1) + j] = (G[i][j], G[i][j+1])
+  if (g->gg) {
+    // Cell quads (32 B per cell: the 4 corners in one sector) up to
+    // EOS_GG_QUAD_MB (default 1024 MB of quads), else row pairs
+    // gq[i (nT-1) + j] = (G[i][j], G[i][j+1]) (two 16-B loads per pair).
     const int64_t w = n_T - 1;
+    const char* eq = getenv("EOS_GG_QUAD_MB");
+    const int64_t quad_cap = (eq ? atoll(eq) : 1024) << 20;
+    g->gquad = 32 * (n_rho - 1) * w <= quad_cap;
     std::vector<double> q2;
     try {
-      q2.resize((size_t)(2 * n_rho * w));
+      q2.resize((size_t)(g->gquad ? 4 * (n_rho - 1) * w : 2 * n_rho * w));
     } catch (...) {
       return fail(EOS_ERR_NOMEM);
     }
-    for (int64_t i = 0; i < n_rho; ++i)
-      for (int64_t j = 0; j < w; ++j) {
-        q2[2 * (i * w + j)] = gval(i * n_T + j);
-        q2[2 * (i * w + j) + 1] = gval(i * n_T + j + 1);
-      }
+    if (g->gquad) {
+      for (int64_t i = 0; i + 1 < n_rho; ++i)
+        for (int64_t j = 0; j < w; ++j) {
+          double* c = q2.data() + 4 * (i * w + j);
+          c[0] = gval(i * n_T + j);
+          c[1] = gval(i * n_T + j + 1);
+          c[2] = gval((i + 1) * n_T + j);
+          c[3] = gval((i + 1) * n_T + j + 1);
+        }
+    } else {
+      for (int64_t i = 0; i < n_rho; ++i)
+        for (int64_t j = 0; j < w; ++j) {
+          q2[2 * (i * w + j)] = gval(i * n_T + j);
+          q2[2 * (i * w + j) + 1] = gval(i * n_T + j + 1);
+        }
+    }
     g->grid_bytes = 8 * (int64_t)q2.size();
     e = cudaMalloc(&g->grid_dev, (size_t)g->grid_bytes);
     if (e == cudaSuccess)

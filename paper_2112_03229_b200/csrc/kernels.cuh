@@ -747,9 +747,11 @@ struct Interp2DArgs {
   int32_t rt_off;   // the same for the T axis
   int32_t rep_shift;  // REP 2: log2 of the record copies per axis entry (3: 8 copies, the
                       //   conflict-free layout; fewer when smem is short: 2-way .. 8-way)
-  int32_t pad2_;
-  const double2* gq;  // GG kernels: the grid in device memory as row pairs
-                      //   gq[i (nT-1) + j] = (G[i][j], G[i][j+1]) (ln G for LOGLOG)
+  int32_t gquad;    // GG: 1 = gq holds cell quads, 0 = row pairs
+  const double2* gq;  // GG kernels: the grid in device memory (ln G for LOGLOG), either as
+                      //   cell quads gq[2 (i (nT-1) + j)] = (G[i][j], G[i][j+1]),
+                      //   gq[2 (i (nT-1) + j) + 1] = (G[i+1][j], G[i+1][j+1]) (32 B, one
+                      //   sector per pair), or as row pairs gq[i (nT-1) + j] = (G[i][j], G[i][j+1])
   int32_t vec_ok;
   int32_t pad_;
   int64_t ntiles;
@@ -847,9 +849,11 @@ __device__ __forceinline__ void axis_cell_rec(double y, const double* __restrict
 // precomputed at create (a few ulp from the divide; within the 1e-12 bar).
 //
 // GG (grids larger than shared memory): the grid stays in device memory
-// (L2-resident up to ~10^7 cells) as row pairs, so the 4 corners are two
-// aligned 16-byte loads, (G[ci][cj], G[ci][cj+1]) and (G[ci+1][cj],
-// G[ci+1][cj+1]); the axes, their directories and records stay in smem.
+// (L2-resident up to a few 10^6 cells) as cell quads, so the 4 corners are one
+// aligned 32-byte load (one L1/L2 sector), or, past the quad budget, as row
+// pairs: two aligned 16-byte loads, (G[ci][cj], G[ci][cj+1]) and
+// (G[ci+1][cj], G[ci+1][cj+1]).  The axes, their directories and records stay
+// in smem.
 template <int S, bool RECIP, bool DERIV, bool LOGLOG, int REP, bool GG>
 __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, int32_t& j,
                                              double& dpr, double& dpt, const char* sm,
@@ -914,13 +918,18 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   EOS_DCHECK(ci >= 0 && cj >= 0 && ci + 1 < A.r.n && cj + 1 < A.t.n);
   double g00, g01, g10, g11;
   if (GG) {
-    const int64_t w = A.t.n - 1;  // row-pair stride
-    const double2* q = A.gq + (int64_t)ci * w + cj;
-    const double2 q0 = __ldg(q), q1 = __ldg(q + w);
-    g00 = q0.x;
-    g01 = q0.y;
-    g10 = q1.x;
-    g11 = q1.y;
+    const int64_t w = A.t.n - 1;  // cells (quads) or row pairs per row
+    if (A.gquad) {  // one 256-bit load: the 4 corners share one 32-B sector
+      ldg_f64x4(reinterpret_cast<const double*>(A.gq + 2 * ((int64_t)ci * w + cj)), g00, g01,
+                g10, g11);
+    } else {
+      const double2* q = A.gq + (int64_t)ci * w + cj;
+      const double2 q0 = __ldg(q), q1 = __ldg(q + w);
+      g00 = q0.x;
+      g01 = q0.y;
+      g10 = q1.x;
+      g11 = q1.y;
+    }
   } else {
     const double* g0 = sG + (int64_t)ci * A.t.n + cj;
     const double* g1 = g0 + A.t.n;

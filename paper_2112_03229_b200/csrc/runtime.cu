@@ -9,6 +9,7 @@
 //   EOS_INTERP_VARIANT                      2-D launch variants by number
 //   EOS_INTERP_REP=0                        2-D plain axes (no cell records)
 //   EOS_GG_SMEM_KB                          smem cap of device-memory grids
+//   EOS_GG_QUAD_MB                          cell-quad budget of device-memory grids (0: row pairs)
 //   EOS_PDL (0/1)                           programmatic dependent launch
 //   EOS_HOST_SLOTS, EOS_HOST_CHUNK_LOG2     host-buffer pipeline depth / chunk
 #include <cuda_runtime.h>

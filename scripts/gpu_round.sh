@@ -85,6 +85,19 @@ if has ncubig; then
   ncu -i $OUT/prof_big.ncu-rep --page details --csv > $OUT/ncu_details_big.csv 2>/dev/null
   rm -f $OUT/prof_big.ncu-rep
 fi
+if has ncuw; then  # generic: NCU_W=<workload> NCU_K=<kernel regex> NCU_TAG=<name> [NCU_ARGS=...]
+  CMD="python bench.py --workload $NCU_W ${NCU_ARGS:-} --steps 6 --warmup 2 --no-e2e --no-cpu --eager"
+  $CMD > $OUT/ncuw_plain.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$NCU_K -s 2 -c 1 \
+      -o $OUT/prof_$NCU_TAG -f $CMD > $OUT/ncuw_full.log 2>&1; echo "ncu $NCU_TAG rc=$?"
+  python scripts/ncu_summary.py $OUT/prof_$NCU_TAG.ncu-rep > $OUT/ncu_summary_$NCU_TAG.json
+  ncu -i $OUT/prof_$NCU_TAG.ncu-rep --page details --csv > $OUT/ncu_details_$NCU_TAG.csv 2>/dev/null
+  rm -f $OUT/prof_$NCU_TAG.ncu-rep
+fi
+if has benchw; then  # BENCH_W=<workload> BENCH_TAG=<name> [BENCH_ARGS=...]
+  timeout 900 python bench.py --workload $BENCH_W ${BENCH_ARGS:-} > $OUT/bench_$BENCH_TAG.json 2> $OUT/bench_$BENCH_TAG.err; echo "bench $BENCH_TAG rc=$?"
+  head -c 600 $OUT/bench_$BENCH_TAG.json; echo
+fi
 if has benchbig; then
   timeout 900 python bench.py --workload big --steps 200 --warmup 5 > $OUT/bench_big.json 2> $OUT/bench_big.err; echo "bench big rc=$?"
   cat $OUT/bench_big.json | head -c 1500; echo; tail -n 3 $OUT/bench_big.err

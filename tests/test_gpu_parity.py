@@ -932,10 +932,14 @@ def test_cuda_graph_capture_and_replay():
 
 
 # ------------------------- 2-D grids in device memory (EOS_GRID_GLOBAL) -----
+@pytest.mark.parametrize("layout", ["quads", "row_pairs"])
 @pytest.mark.parametrize("loglog", [False, True])
-def test_global_grid_cfg4_matches_shared_and_oracle(loglog):
+def test_global_grid_cfg4_matches_shared_and_oracle(loglog, layout, monkeypatch):
     """The cfg4 grid forced into device memory gives the shared-memory kernel's
-    brackets and values (same arithmetic), hence the oracle's."""
+    brackets and values (same arithmetic), hence the oracle's, in both device-memory
+    layouts (cell quads, the default, and row pairs: EOS_GG_QUAD_MB=0)."""
+    if layout == "row_pairs":
+        monkeypatch.setenv("EOS_GG_QUAD_MB", "0")
     w = datagen.workload("cfg4", count=(1 << 20) + 7)
     rho = w.rho_targets.host_fill(0, w.count)
     T = w.T_targets.host_fill(0, w.count)
@@ -956,12 +960,16 @@ def test_global_grid_cfg4_matches_shared_and_oracle(loglog):
     gg.close()
 
 
-@pytest.mark.parametrize("shape,loglog", [((600, 500), False), ((600, 500), True),
-                                          ((1000, 800), False), ((3000, 7), False),
-                                          ((2, 16000), False), ((8000, 3), True)])
-def test_large_grids_in_device_memory(shape, loglog):
-    """Grids larger than shared memory (P in device memory, axes in smem with as many
-    record copies as fit): brackets bit-exact, P and derivatives within the bar."""
+@pytest.mark.parametrize("shape,loglog,quad_mb", [
+    ((600, 500), False, None), ((600, 500), True, None), ((1000, 800), False, None),
+    ((3000, 7), False, None), ((2, 16000), False, None), ((8000, 3), True, None),
+    ((1000, 800), False, "0"), ((600, 500), True, "0"), ((2, 16000), False, "0")])
+def test_large_grids_in_device_memory(shape, loglog, quad_mb, monkeypatch):
+    """Grids larger than shared memory (P in device memory as cell quads, or as row pairs
+    with EOS_GG_QUAD_MB=0; axes in smem with as many record copies as fit): brackets
+    bit-exact, P and derivatives within the bar."""
+    if quad_mb is not None:
+        monkeypatch.setenv("EOS_GG_QUAD_MB", quad_mb)
     rng = np.random.default_rng(shape[0] + shape[1])
     nR, nT = shape
     if loglog:  # jittered logspace axes: log-log derivatives amplify the device-vs-libm
