@@ -175,6 +175,35 @@ def test_ragged_and_misaligned(count, y_off, o_off):
     t.close()
 
 
+@pytest.mark.parametrize("table,kw", [("cfg1", {}), ("cfg2", {"log_bins": 12000}),
+                                      ("cfg5", {}), ("cfg5", {"log_bins": 5000}),
+                                      ("cfg2", {"k": 0})])
+def test_small_launch_tiles_match_default_tiles_and_oracle(table, kw, monkeypatch):
+    """Launches whose default tiling leaves most SMs idle run the small-tile shape
+    (runtime.cu EOS_SMALL_TILES): every shape family (image <= 32 KB / <= 72 KB / larger,
+    S <= 2 / S >= 3), counts on both sides of the switch, ragged heads and tails; bit-exact
+    against the oracle and against the default tiles."""
+    w = datagen.workload(table, count=400_003)
+    Yall = w.targets.host_fill(0, w.count, w.table)
+    Yall[:4] = [np.nan, -np.inf, np.inf, 0.0]
+    t_small = eos.Table(w.table, **kw)
+    monkeypatch.setenv("EOS_SMALL_TILES", "0")
+    t_def = eos.Table(w.table, **kw)
+    monkeypatch.delenv("EOS_SMALL_TILES")
+    for count, off in ((1, 0), (7, 1), (1000, 3), (50_001, 1), (151_553, 0), (151_552, 2),
+                       (300_001, 1), (400_000, 3)):
+        Y = Yall[off:off + count]
+        yd = to_dev(Yall)[off:off + count]
+        a = t_small.search(yd)
+        b = t_def.search(yd)
+        torch.cuda.synchronize()
+        ref = oracle.search(w.table, Y)
+        assert_same(a.cpu().numpy(), ref, Y)
+        assert_same(b.cpu().numpy(), ref, Y)
+    t_small.close()
+    t_def.close()
+
+
 def test_counters_match_oracle():
     w = datagen.workload("cfg1", count=777_777)
     Y = w.targets.host_fill(0, w.count, w.table)
