@@ -37,11 +37,15 @@ cudaError_t launch(const void* fn, int64_t grid, int threads, size_t smem, cudaS
                    void** params);
 // Count one kernel launch (eos_launch_count).
 void count_launch();
+// Stream-ordered staging allocation from the library's per-device pool (freed
+// with cudaFreeAsync).
+cudaError_t stage_alloc(void** p, size_t bytes, cudaStream_t st);
 eos_status upload(const std::vector<uint8_t>& img, void** dev);
 // The smem-image axis parameters of a planned table at byte offset x_off.
 dev::AxisParams axis_params(const TablePlan& p, int32_t x_off);
 
-// Two-stream chunked pipeline over host buffers: chunk c uses slot c % 2 (its
+// Two-stream chunked pipeline over host buffers (one chunk: the caller stream
+// alone): chunk c uses slot c % 2 (its
 // own stream and device staging), so H2D(c+1) overlaps search(c) / D2H(c).
 template <class Body>
 eos_status host_pipeline(cudaStream_t caller, int64_t count, int64_t chunk, int64_t bytes_per_elem,
@@ -55,12 +59,23 @@ eos_status host_pipeline(cudaStream_t caller, int64_t count, int64_t chunk, int6
     const char* e = getenv("EOS_HOST_CHUNK_LOG2");
     return e ? std::max(16, std::min(26, atoi(e))) : 0;
   }();
-  if (chunk_log2) chunk = (int64_t(1) << chunk_log2) * chunk / (int64_t(1) << 23);
+  if (chunk_log2) {
+    chunk = (int64_t(1) << chunk_log2) * chunk / (int64_t(1) << 23);
+  } else {  // mid-sized calls: ~8 chunks (>= chunk / 32 each), so H2D overlaps D2H
+    int64_t c = chunk / 32;
+    while (c < chunk && 8 * c < count) c *= 2;
+    chunk = c;
+  }
   const int64_t nchunk = (count + chunk - 1) / chunk;
   const int nslot = (int)std::min<int64_t>(nchunk, slots_env);
   const int64_t slot_elems = (std::min(chunk, count) + 63) & ~int64_t(63);  // keeps 16-B alignment
   char* stage = nullptr;
-  EOS_CUDA(cudaMallocAsync((void**)&stage, (size_t)(nslot * slot_elems * bytes_per_elem), caller));
+  EOS_CUDA(stage_alloc((void**)&stage, (size_t)(nslot * slot_elems * bytes_per_elem), caller));
+  if (nchunk == 1) {  // one chunk: nothing to overlap, so no side streams or events
+    const eos_status st1 = body(caller, stage, slot_elems, 0, count);
+    cudaFreeAsync(stage, caller);
+    return st1;
+  }
   cudaStream_t s[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_start = nullptr, ev_done[4] = {nullptr, nullptr, nullptr, nullptr};
   eos_status st = EOS_OK;
