@@ -54,11 +54,16 @@ cudaError_t stage_alloc(void** p, size_t bytes, cudaStream_t st) {
       props.handleTypes = cudaMemHandleTypeNone;
       props.location.type = cudaMemLocationTypeDevice;
       props.location.id = dev;
-      e = cudaMemPoolCreate(&pools[dev], &props);
+      cudaMemPool_t np = nullptr;
+      e = cudaMemPoolCreate(&np, &props);
       if (e != cudaSuccess) return e;
       uint64_t keep = uint64_t(1) << 30;
-      e = cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
-      if (e != cudaSuccess) return e;
+      e = cudaMemPoolSetAttribute(np, cudaMemPoolAttrReleaseThreshold, &keep);
+      if (e != cudaSuccess) {
+        cudaMemPoolDestroy(np);
+        return e;
+      }
+      pools[dev] = np;
     }
     pool = pools[dev];
   }
