@@ -386,3 +386,19 @@ def test_header_is_plain_c_and_the_example_links(tmp_path):
                         "-leossearch", "-L", "/usr/local/cuda/lib64", "-lcudart",
                         "-o", str(tmp_path / "ex")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_every_tuning_knob_is_documented():
+    """Every environment variable the library reads (getenv in csrc/) is listed in the
+    tuning-knob header of csrc/runtime.cu, so no hidden switch changes the product path."""
+    import glob
+    import re
+    csrc = os.path.join(ROOT, "paper_2112_03229_b200", "csrc")
+    names = set()
+    for f in glob.glob(os.path.join(csrc, "*")):
+        for call in re.findall(r"getenv\(([^;]*?)\)", open(f).read()):
+            names |= set(re.findall(r'"(EOS_[A-Z0-9_]+)"', call))
+    header = open(os.path.join(csrc, "runtime.cu")).read().split("\n\n")[0]
+    missing = sorted(n for n in names if n not in header)
+    assert {"EOS_SEARCH_VARIANT", "EOS_TIERED_VARIANT", "EOS_SMALL_TILES"} <= names
+    assert not missing, missing
