@@ -20,6 +20,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libeossearch.so")
 CHECKED_LIB = os.path.join(LIBDIR, "libeossearch_checked.so")  # -DEOS_DEVICE_CHECKS debug build
+EXP_LIB = os.path.join(LIBDIR, "libeossearch_exp.so")  # A/B builds with extra -D flags (EOS_LIBRARY=exp)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -52,26 +53,27 @@ def nvcc_link_cmd(out: str, objs: list[str]) -> list[str]:
     return [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs]
 
 
-def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False,
+          exp_flags: list[str] | None = None) -> str:
     """Compile every source to an object in parallel (one nvcc per translation unit:
     the kernel instantiations are split over runtime.cu, search_api.cu and
     grid_api.cu), then link the shared library."""
     from concurrent.futures import ThreadPoolExecutor
-    lib = CHECKED_LIB if checked else LIB
-    if not (force or stale(lib)):
+    lib = EXP_LIB if exp_flags is not None else (CHECKED_LIB if checked else LIB)
+    if not (force or exp_flags is not None or stale(lib)):
         return lib
     os.makedirs(LIBDIR, exist_ok=True)
-    tag = "checked" if checked else "product"
+    tag = "exp" if exp_flags is not None else ("checked" if checked else "product")
     objdir = os.path.join(LIBDIR, "obj_" + tag)
     os.makedirs(objdir, exist_ok=True)
-    extra = ["-DEOS_DEVICE_CHECKS"] if checked else None
+    extra = exp_flags if exp_flags is not None else (["-DEOS_DEVICE_CHECKS"] if checked else None)
     jobs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         jobs.append((src, obj, nvcc_compile_cmd(src, obj, extra)))
     with ThreadPoolExecutor(len(jobs)) as ex:
         results = list(ex.map(lambda j: subprocess.run(j[2], capture_output=True, text=True), jobs))
-    log = os.path.join(LIBDIR, "ptxas_checked.log" if checked else "ptxas.log")
+    log = os.path.join(LIBDIR, {"exp": "ptxas_exp.log", "checked": "ptxas_checked.log"}.get(tag, "ptxas.log"))
     with open(log, "w") as f:
         for (src, _, _), r in zip(jobs, results):
             f.write(f"==== {os.path.basename(src)}\n" + r.stdout + r.stderr)
@@ -92,4 +94,6 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv)
+    # --exp -DNAME[=V] ...: an A/B build of the same sources into libeossearch_exp.so
+    exp = [a for a in sys.argv[1:] if a.startswith("-D")] if "--exp" in sys.argv else None
+    build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv, exp_flags=exp)

@@ -198,6 +198,11 @@ struct SmemLookup {
 // L1TEX wavefront per lane -- the gathers of a warp hit 32 different lines,
 // so wavefronts, not bytes, bound the L1 stage.  L1::no_allocate: the levels
 // are too large to live in L1 (measured faster than allocating).
+// Read-once target stream: 128-bit evict-first loads.  (A/B, DESIGN.md §12:
+// the L2 256-byte prefetch hint and 256-bit loads / 128-bit stores per thread
+// were within +-1.5%.)
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+
 __device__ __forceinline__ void ldg_keys8(const uint32_t* p, uint32_t (&k)[8]) {
   asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=r"(k[0]), "=r"(k[1]), "=r"(k[2]), "=r"(k[3]), "=r"(k[4]), "=r"(k[5]), "=r"(k[6]),
@@ -492,10 +497,11 @@ __device__ __forceinline__ void search_body(const SearchArgs& args, const LK& lk
 
   int64_t t = blockIdx.x;
   double2 v[U];
-  if (t < ntiles && full(t)) {
+  auto load_tile = [&](int64_t tt) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = __ldcs(Y2 + t * TP + threadIdx.x + u * T);
-  }
+    for (int u = 0; u < U; ++u) v[u] = ld_stream(Y2 + tt * TP + threadIdx.x + u * T);
+  };
+  if (t < ntiles && full(t)) load_tile(t);
   while (t < ntiles) {
     if (SH::kClc && threadIdx.x == 0) {
       mbar_arrive_expect_tx(&clc_bar, 16);
@@ -524,10 +530,7 @@ __device__ __forceinline__ void search_body(const SearchArgs& args, const LK& lk
         }
       }
       tn = next_tile(t);
-      if (tn < ntiles && full(tn)) {  // prefetch the next tile before storing this one
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = __ldcs(Y2 + tn * TP + threadIdx.x + u * T);
-      }
+      if (tn < ntiles && full(tn)) load_tile(tn);  // prefetch the next tile before storing this one
 #pragma unroll
       for (int u = 0; u < U; ++u) __stcs(O2 + p0 + u * T, r[u]);
     } else {
@@ -543,10 +546,7 @@ __device__ __forceinline__ void search_body(const SearchArgs& args, const LK& lk
         if (CNT) cn.add(y[0], r[0], args.gofs + i, lk.x_at(r[0]), a);
       }
       tn = next_tile(t);
-      if (tn < ntiles && full(tn)) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = __ldcs(Y2 + tn * TP + threadIdx.x + u * T);
-      }
+      if (tn < ntiles && full(tn)) load_tile(tn);
     }
     t = tn;
   }
@@ -1010,8 +1010,8 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
   if (t < ntiles && full(t)) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      vr[u] = __ldcs(R2 + t * TP + threadIdx.x + u * T);
-      vt[u] = __ldcs(T2 + t * TP + threadIdx.x + u * T);
+      vr[u] = ld_stream(R2 + t * TP + threadIdx.x + u * T);
+      vt[u] = ld_stream(T2 + t * TP + threadIdx.x + u * T);
     }
   }
   while (t < ntiles) {
@@ -1036,8 +1036,8 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       if (tn < ntiles && full(tn)) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          vr[u] = __ldcs(R2 + tn * TP + threadIdx.x + u * T);
-          vt[u] = __ldcs(T2 + tn * TP + threadIdx.x + u * T);
+          vr[u] = ld_stream(R2 + tn * TP + threadIdx.x + u * T);
+          vt[u] = ld_stream(T2 + tn * TP + threadIdx.x + u * T);
         }
       }
 #pragma unroll
@@ -1065,8 +1065,8 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       if (tn < ntiles && full(tn)) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          vr[u] = __ldcs(R2 + tn * TP + threadIdx.x + u * T);
-          vt[u] = __ldcs(T2 + tn * TP + threadIdx.x + u * T);
+          vr[u] = ld_stream(R2 + tn * TP + threadIdx.x + u * T);
+          vt[u] = ld_stream(T2 + tn * TP + threadIdx.x + u * T);
         }
       }
     }
