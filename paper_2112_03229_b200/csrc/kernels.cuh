@@ -194,15 +194,15 @@ struct SmemLookup {
   __device__ __forceinline__ double x_at(int32_t i) const { return sX[i]; }
 };
 
-// One 32-byte sector with one 256-bit load (SASS LDG.E.NA.ENL2.256): one
-// L1TEX wavefront per lane -- the gathers of a warp hit 32 different lines,
-// so wavefronts, not bytes, bound the L1 stage.  L1::no_allocate: the levels
-// are too large to live in L1 (measured faster than allocating).
 // Read-once target stream: 128-bit evict-first loads.  (A/B, DESIGN.md §12:
 // the L2 256-byte prefetch hint and 256-bit loads / 128-bit stores per thread
 // were within +-1.5%.)
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 
+// One 32-byte sector with one 256-bit load (SASS LDG.E.NA.ENL2.256): one
+// L1TEX wavefront per lane -- the gathers of a warp hit 32 different lines,
+// so wavefronts, not bytes, bound the L1 stage.  L1::no_allocate: the levels
+// are too large to live in L1 (measured faster than allocating).
 __device__ __forceinline__ void ldg_keys8(const uint32_t* p, uint32_t (&k)[8]) {
   asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=r"(k[0]), "=r"(k[1]), "=r"(k[2]), "=r"(k[3]), "=r"(k[4]), "=r"(k[5]), "=r"(k[6]),
@@ -620,6 +620,11 @@ struct DirectArgs {
   int32_t* status;       // nullable: receives EOS_ERR_UNSORTED / EOS_ERR_NONFINITE
 };
 
+template <int V>
+struct IntTag {
+  static constexpr int value = V;
+};
+
 template <class SH>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
     search1d_direct_kernel(const DirectArgs A) {
@@ -724,12 +729,24 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
   int steps = 0;
   while ((1u << steps) < s_maxocc + 1) ++steps;
   a.steps = steps > 0 ? steps : 1;
-  if (a.mode) {
-    const SmemLookup<0, 1> lk{sX, sD, a};
-    search_body<false, SH>(A.s, lk, &clc_resp, &clc_bar);
-  } else {
-    const SmemLookup<0, 0> lk{sX, sD, a};
-    search_body<false, SH>(A.s, lk, &clc_resp, &clc_bar);
+  // S is known only now (block-uniform): fixed-S bodies for S <= 4, the
+  // runtime-S body above
+  auto body = [&](auto s_tag) {
+    constexpr int S = decltype(s_tag)::value;
+    if (a.mode) {
+      const SmemLookup<S, 1> lk{sX, sD, a};
+      search_body<false, SH>(A.s, lk, &clc_resp, &clc_bar);
+    } else {
+      const SmemLookup<S, 0> lk{sX, sD, a};
+      search_body<false, SH>(A.s, lk, &clc_resp, &clc_bar);
+    }
+  };
+  switch (a.steps) {
+    case 1: body(IntTag<1>{}); break;
+    case 2: body(IntTag<2>{}); break;
+    case 3: body(IntTag<3>{}); break;
+    case 4: body(IntTag<4>{}); break;
+    default: body(IntTag<0>{}); break;
   }
 }
 
