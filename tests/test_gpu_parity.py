@@ -560,6 +560,24 @@ def test_direct_edge_tables_and_configs():
         assert_same(out.cpu().numpy(), oracle.search(w.table, Y[1:]))
 
 
+@pytest.mark.parametrize("run", [1, 2, 3, 4, 7, 8, 15, 16, 31, 100])
+def test_direct_every_block_step_count(run):
+    """The zero-setup kernel learns S (in-bin steps) only after building the directory and
+    dispatches per CTA to a fixed-S body (S <= 4) or the runtime-S body: tables whose largest
+    bin holds `run` equal entries (S = ceil(log2(run + 1))), mixed signs for mode 1, with
+    probes at, between and around every entry, bit-exact against the oracle."""
+    rng = np.random.default_rng(run)
+    for neg in (False, True):
+        base = np.sort(10.0 ** rng.uniform(-5, 5, 300))
+        X = np.sort(np.concatenate([base, np.full(run - 1, base[137])]))
+        if neg:
+            X = np.sort(np.concatenate([-X[:40], X[40:]]))
+        P = _probes(X)
+        P = np.concatenate([P, rng.permutation(np.repeat(P, 5)),
+                            10.0 ** rng.uniform(-6, 6, 50_001) * rng.choice([-1.0, 1.0], 50_001)])
+        assert_same(direct(X, P), oracle.search(X, P), P)
+
+
 def test_direct_reports_invalid_tables_and_limits():
     st = torch.zeros(1, dtype=torch.int32, device=DEV)
     y = torch.linspace(0, 10, 5000, dtype=torch.float64, device=DEV)
