@@ -107,23 +107,23 @@ eos_status build(const std::vector<double>& X, int mode, const HashParams& h, Ta
 }
 
 // Expected executed (non-predicated) probes of S-step binary lifting in a bin
-// holding `o` entries, the target uniform among the o+1 gaps.
+// holding `o` entries (o < 2^S), the target uniform among the o+1 gaps.
+// Before the step of stride s the count c is the final count cf with its bits
+// below 2s cleared, and the probe j = c + s executes iff j <= o: so the step
+// executes for every cf whose block base (multiple of 2s) is <= o - s.  O(S).
 double lifting_probes(int o, int S) {
-  double total = 0.0;
-  for (int cf = 0; cf <= o; ++cf) {  // final count of entries <= target
-    int c = 0;
-    for (int s = S > 0 ? 1 << (S - 1) : 0; s > 0; s >>= 1) {
-      const int j = c + s;
-      if (j <= o) {
-        total += 1.0;
-        if (j <= cf) c = j;
-      }
-    }
+  int64_t total = 0;
+  for (int64_t s = S > 0 ? int64_t(1) << (S - 1) : 0; s > 0; s >>= 1) {
+    const int64_t last = o - s;  // largest block base whose probe executes
+    if (last < 0) continue;
+    const int64_t nb = last / (2 * s) + 1;  // blocks with an executed probe
+    const int64_t base = (nb - 1) * 2 * s;
+    total += base + std::min<int64_t>(2 * s, o + 1 - base);
   }
-  return total / (o + 1);
+  return (double)total / (o + 1);
 }
 
-// Modelled per-lookup cost of a plan, in shared-memory
+// Modelled per-lookup cost of a plan (evaluate below), in shared-memory
 // wavefronts per warp of 32 lookups plus issue and occupancy terms:
 //   3.5 (random 4-B directory read) + 6.1 x E[executed 8-B probes]
 //   + 1 per in-bin step (issue) + a launch-shape penalty.
@@ -139,26 +139,73 @@ double lifting_probes(int o, int S) {
 // (profiles/r01_exp_table_size.json): the penalty lets only a large probe
 // saving buy the extra smem.  Targets are taken log-uniform over the table
 // range, i.e. uniform over the bins (equal key width).
-double plan_cost(const TablePlan& p) {
-  std::vector<double> memo(64, -1.0);
-  double probes = 0.0;
-  for (uint32_t d : p.dir) {
-    const int o = (int)(d >> 16);
-    double v;
-    if (o < 64) {
-      if (memo[o] < 0) memo[o] = lifting_probes(o, p.steps);
-      v = memo[o];
-    } else {
-      v = lifting_probes(o, p.steps);
+double cost_of(double mean_probes, int steps, int64_t image_bytes) {
+  const double shape = image_bytes <= 32 * 1024   ? 0.0
+                       : image_bytes <= 72 * 1024  ? 1.0
+                       : image_bytes <= 144 * 1024 ? 1.5
+                                                   : 4.5;
+  return 3.5 + 6.1 * mean_probes + 1.0 * steps + shape;
+}
+
+// A candidate hash evaluated without building its directory: the table is
+// sorted, so the bins of its keys are non-decreasing and every non-empty bin
+// is one run of equal bin indices (empty bins execute no probe).  O(n) per
+// candidate instead of O(n + bins) plus two allocations; the sum runs over
+// the non-empty bins in bin order, as a sum over the whole directory would.
+struct CandidateEval {
+  bool ok = false;
+  int steps = 0;
+  double cost = 0.0;
+  int64_t image_bytes = 0;
+};
+
+CandidateEval evaluate(const std::vector<uint32_t>& keys, const HashParams& h, bool compact,
+                       std::vector<int64_t>& runs) {
+  CandidateEval e;
+  const int64_t n = (int64_t)keys.size();
+  if (h.bins < 1 || h.bins > (int64_t(1) << 22)) return e;
+  auto bin = [&](int64_t j) { return bin_of_key(keys[j], h.hb, h.M, h.bmax); };
+  // runs of equal bins, each found by galloping: O(log run) bin evaluations
+  runs.clear();
+  int64_t mx = 0;
+  for (int64_t j = 0; j < n;) {
+    const uint32_t b = bin(j);
+    int64_t lo = j, step = 1;  // bin(lo) == b; find the first r > j with bin(r) != b
+    while (lo + step < n && bin(lo + step) == b) {
+      lo += step;
+      step *= 2;
     }
-    probes += v;
+    int64_t hi = std::min(n, lo + step);  // bin(hi) != b or hi == n
+    while (hi - lo > 1) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (bin(mid) == b) lo = mid; else hi = mid;
+    }
+    if (hi < n && bin(hi) < b) return e;  // unsorted keys: cannot happen for a validated table
+    runs.push_back(hi - j);
+    mx = std::max(mx, hi - j);
+    j = hi;
   }
-  probes /= (double)p.bins;
-  const double shape = p.image_bytes <= 32 * 1024   ? 0.0
-                       : p.image_bytes <= 72 * 1024  ? 1.0
-                       : p.image_bytes <= 144 * 1024 ? 1.5
-                                                     : 4.5;
-  return 3.5 + 6.1 * probes + 1.0 * p.steps + shape;
+  e.ok = true;
+  e.steps = ceil_log2_plus1((int)mx);
+  e.image_bytes = image_of(n, h.bins);
+  if (compact) {
+    e.cost = (double)e.steps;
+    return e;
+  }
+  double memo[64];
+  for (double& m : memo) m = -1.0;
+  double probes = 0.0;
+  for (const int64_t len : runs) {
+    const int o = (int)len;
+    if (o < 64) {
+      if (memo[o] < 0) memo[o] = lifting_probes(o, e.steps);
+      probes += memo[o];
+    } else {
+      probes += lifting_probes(o, e.steps);
+    }
+  }
+  e.cost = cost_of(probes / (double)h.bins, e.steps, e.image_bytes);
+  return e;
 }
 
 // Automatic choice: the candidate of least plan_cost with an
@@ -180,20 +227,23 @@ eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, Table
   const bool fill = compact && fill_budget > 0;
   const int64_t budget = fill_budget > 0 ? fill_budget
                                          : (compact ? kAxisImageBudget : kAutoImageBudget);
-  TablePlan best;
-  double best_cost = 0.0;
+  std::vector<uint32_t> keys((size_t)n);
+  for (int64_t j = 0; j < n; ++j) keys[j] = key_hi(X[j], mode);
+  std::vector<int64_t> runs;
+  HashParams best;
+  CandidateEval best_e;
   bool have = false;
   auto consider = [&](const HashParams& h) {
     if (h.bins < 1) return;
     if (have && image_of(n, h.bins) > budget) return;
-    TablePlan p;
-    if (build(X, mode, h, &p) != EOS_OK) return;
-    const double c = compact ? (double)p.steps : plan_cost(p);
-    if (have && fill && p.image_bytes > budget) return;
-    const bool tie_better = fill ? p.image_bytes > best.image_bytes : p.image_bytes < best.image_bytes;
-    if (!have || c < best_cost - 1e-9 || (c < best_cost + 1e-9 && tie_better)) {
-      best = std::move(p);
-      best_cost = c;
+    const CandidateEval e = evaluate(keys, h, compact, runs);
+    if (!e.ok) return;
+    const double c = e.cost;
+    if (have && fill && e.image_bytes > budget) return;
+    const bool tie_better = fill ? e.image_bytes > best_e.image_bytes : e.image_bytes < best_e.image_bytes;
+    if (!have || c < best_e.cost - 1e-9 || (c < best_e.cost + 1e-9 && tie_better)) {
+      best = h;
+      best_e = e;
       have = true;
     }
   };
@@ -207,8 +257,7 @@ eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, Table
     consider(log_params(X, mode, (int64_t)H));
   }
   if (!have) return EOS_ERR_UNSUPPORTED;
-  *out = std::move(best);
-  return EOS_OK;
+  return build(X, mode, best, out);  // the directory of the chosen hash only
 }
 
 }  // namespace
