@@ -12,6 +12,7 @@ import re
 import numpy as np
 import pytest
 
+import datagen
 import oracle
 import paper_2112_03229_b200 as eos
 from paper_2112_03229_b200 import _build
@@ -402,3 +403,58 @@ def test_every_tuning_knob_is_documented():
     missing = sorted(n for n in names if n not in header)
     assert {"EOS_SEARCH_VARIANT", "EOS_TIERED_VARIANT", "EOS_SMALL_TILES"} <= names
     assert not missing, missing
+
+
+def _lifting_probes_brute(o, S):
+    """Executed probes of S-step predicated binary lifting in a bin of o entries, averaged
+    over the o+1 target gaps, by direct simulation (kernels.cuh lookup)."""
+    total = 0
+    for cf in range(o + 1):
+        c, s = 0, (1 << (S - 1)) if S > 0 else 0
+        while s > 0:
+            if c + s <= o:
+                total += 1
+                if c + s <= cf:
+                    c += s
+            s >>= 1
+    return total / (o + 1)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5", "paper"])
+def test_automatic_plan_is_the_argmin_of_the_cost_model(name):
+    """The automatic hash choice (table_build.cpp plan_auto, which evaluates candidates from
+    runs of the sorted keys) equals the argmin of the DESIGN.md §6.3 cost model recomputed
+    here from every candidate's full directory: 3.5 + 6.1 E[probes] + S + shape penalty,
+    ties to the smaller image, then the exponent hash, image budget 200 KB."""
+    X = datagen.workload(name, count=10).table
+    n = X.size
+    pad16 = lambda b: (b + 15) & ~15  # noqa: E731
+    budget = 200 * 1024
+
+    def cost(info, d):
+        occ = (d >> 16).astype(np.int64)
+        S = info.steps
+        vals, counts = np.unique(occ, return_counts=True)
+        probes = sum(int(c) * _lifting_probes_brute(int(o), S) for o, c in zip(vals, counts))
+        img = pad16(8 * n) + pad16(4 * info.bins)
+        shape = 0.0 if img <= 32768 else 1.0 if img <= 73728 else 1.5 if img <= 147456 else 4.5
+        return 3.5 + 6.1 * probes / info.bins + S + shape, img
+
+    best = None
+    cands = [(eos.EOS_HASH_EXPONENT, k) for k in range(eos.EOS_MAX_K + 1)]
+    H, max_bins = 1.0, (budget - pad16(8 * n)) // 4
+    while H <= max_bins:
+        cands.append((eos.EOS_HASH_LOG, int(H)))
+        H *= 2 ** 0.125
+    for kind, param in cands:
+        try:
+            info, d = eos.eos_plan_table_hash(X, kind, param)
+        except eos.EosError:   # image beyond what shared memory holds
+            continue
+        c, img = cost(info, d)
+        if best is not None and img > budget:
+            continue
+        if best is None or c < best[0] - 1e-9 or (c < best[0] + 1e-9 and img < best[1]):
+            best = (c, img, info.bins, info.hash_kind, info.steps)
+    auto, _ = eos.eos_plan_table(X, eos.EOS_K_AUTO, with_directory=False)
+    assert (auto.bins, auto.hash_kind, auto.steps) == best[2:], (auto.bins, best)
