@@ -609,7 +609,10 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
 // of a logarithm hash there (histogram + block scan, O(n + bins)), then runs
 // the same streaming tile loop with a runtime in-bin step count.
 constexpr int kDirectMaxTable = 4096;
-constexpr int kDirectMaxBins = 8192;
+#ifndef EOS_DIRECT_MAX_BINS
+#define EOS_DIRECT_MAX_BINS 8192
+#endif
+constexpr int kDirectMaxBins = EOS_DIRECT_MAX_BINS;
 using ShapeDirect = Shape<512, 4, 2, true>;
 
 struct DirectArgs {
@@ -641,10 +644,18 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
   double* sX = reinterpret_cast<double*>(smem);
   uint32_t* sD = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(smem) + x_bytes);
   uint32_t bad = 0;
-  for (int j = threadIdx.x; j < n; j += T) {
-    const double v = __ldg(A.table + j);
-    if (!isfinite(v)) bad = EOS_ERR_NONFINITE;
-    sX[j] = (v == 0.0) ? 0.0 : v;  // canonicalise -0.0 (R6)
+  constexpr int LU = 8;  // all of a thread's table loads in flight at once (n <= 4096 = 8 T)
+  for (int j0 = threadIdx.x; j0 < n; j0 += LU * T) {
+    double v[LU];
+#pragma unroll
+    for (int u = 0; u < LU; ++u) v[u] = j0 + u * T < n ? __ldg(A.table + j0 + u * T) : 0.0;
+#pragma unroll
+    for (int u = 0; u < LU; ++u) {
+      if (j0 + u * T < n) {
+        if (!isfinite(v[u])) bad = EOS_ERR_NONFINITE;
+        sX[j0 + u * T] = (v[u] == 0.0) ? 0.0 : v[u];  // canonicalise -0.0 (R6)
+      }
+    }
   }
   if (threadIdx.x == 0) {
     s_maxocc = 0;
@@ -692,34 +703,40 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
     atomicAdd(&sD[bin_of(key, sa)], 1u);
   }
   __syncthreads();
-  // exclusive scan of the counts -> packed directory lo | occ << 16
-  const int per = (bins + T - 1) / T;
-  const int b0 = min(bins, (int)threadIdx.x * per), b1 = min(bins, b0 + per);
-  uint32_t local = 0;
-  for (int b = b0; b < b1; ++b) local += sD[b];
-  uint32_t incl = local;
+  // exclusive scan of the counts -> packed directory lo | occ << 16.  Each
+  // warp owns a contiguous segment of bins and walks it 32 bins at a time
+  // (lane l reads bin base + l: conflict-free), with a shuffle scan per chunk.
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int W = T / 32;
+  const int seg = ((bins + W - 1) / W + 31) & ~31;
+  const int s0 = min(bins, warp * seg), s1 = min(bins, s0 + seg);
+  uint32_t part = 0;
+  for (int b = s0 + lane; b < s1; b += 32) part += sD[b];
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) s_warp[warp] = incl;
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, o);
+  if (lane == 0) s_warp[warp] = part;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t run = 0;
-    for (int w = 0; w < T / 32; ++w) {
+    for (int w = 0; w < W; ++w) {
       const uint32_t v = s_warp[w];
       s_warp[w] = run;
       run += v;
     }
   }
   __syncthreads();
-  uint32_t run = s_warp[warp] + incl - local, mx = 0;
-  for (int b = b0; b < b1; ++b) {
-    const uint32_t o = sD[b];
-    sD[b] = run | (o << 16);
-    run += o;
+  uint32_t carry = s_warp[warp], mx = 0;
+  for (int c = s0; c < s1; c += 32) {
+    const int b = c + lane;
+    const uint32_t o = b < s1 ? sD[b] : 0u;
+    uint32_t incl = o;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    if (b < s1) sD[b] = (carry + incl - o) | (o << 16);
+    carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
     mx = max(mx, o);
   }
   atomicMax(&s_maxocc, mx);

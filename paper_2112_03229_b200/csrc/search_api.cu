@@ -463,7 +463,10 @@ eos_status eos_search_direct(const double* table_dev, int64_t n, const double* t
   using SH = dv::ShapeDirect;
   const void* fn = (const void*)dv::search1d_direct_kernel<SH>;
   int32_t bins_max = 1;
-  while (bins_max < 4 * n && bins_max < dv::kDirectMaxBins) bins_max <<= 1;
+#ifndef EOS_DIRECT_BINS_PER_ENTRY
+#define EOS_DIRECT_BINS_PER_ENTRY 4
+#endif
+  while (bins_max < EOS_DIRECT_BINS_PER_ENTRY * n && bins_max < dv::kDirectMaxBins) bins_max <<= 1;
   const int64_t smem = ((8 * n + 15) & ~int64_t(15)) + 4 * (int64_t)bins_max;
   {  // one-time per device: allow the largest dynamic smem this kernel uses
     static std::mutex mu;
