@@ -12,6 +12,7 @@
 //   EOS_GG_QUAD_MB                          cell-quad budget of device-memory grids (0: row pairs)
 //   EOS_PDL (0/1)                           programmatic dependent launch
 //   EOS_HOST_SLOTS, EOS_HOST_CHUNK_LOG2     host-buffer pipeline depth / chunk
+//   EOS_PLAN_THREADS                        host threads of the automatic plan (n >= 1024)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>

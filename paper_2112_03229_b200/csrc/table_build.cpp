@@ -3,9 +3,11 @@
 // only once").  Validation, canonicalisation, bin key, count directory and the
 // choice of hash.  Product path: shares no code with oracle/.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <thread>
 
 #include "eos_internal.h"
 
@@ -229,32 +231,60 @@ eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, Table
                                          : (compact ? kAxisImageBudget : kAutoImageBudget);
   std::vector<uint32_t> keys((size_t)n);
   for (int64_t j = 0; j < n; ++j) keys[j] = key_hi(X[j], mode);
-  std::vector<int64_t> runs;
+  // candidates, in the order of preference of ties: exponent hash k = 0.., then
+  // the logarithm hash on a geometric |H| grid
+  std::vector<HashParams> cand;
+  for (int k = 0; k <= EOS_MAX_K; ++k) {
+    HashParams h = exponent_params(X, mode, k);
+    if (k > 0 && image_of(n, h.bins) > budget) break;
+    cand.push_back(h);
+  }
+  const int64_t max_bins = (budget - pad16(8 * n)) / 4;
+  for (double H = 1.0; H <= (double)max_bins; H *= 1.0905077326652577 /* 2^(1/8) */)
+    cand.push_back(log_params(X, mode, (int64_t)H));
+  // evaluate them (independently: over host threads for large tables) ...
+  std::vector<CandidateEval> ev(cand.size());
+  auto eval_range = [&](size_t i0, size_t step) {
+    std::vector<int64_t> runs;
+    for (size_t i = i0; i < cand.size(); i += step)
+      if (cand[i].bins >= 1) ev[i] = evaluate(keys, cand[i], compact, runs);
+  };
+  static const unsigned max_threads = [] {  // EOS_PLAN_THREADS: A/B knob (runtime.cu)
+    const char* e = getenv("EOS_PLAN_THREADS");
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    return e ? (unsigned)std::max(1, atoi(e)) : std::min(hw, 8u);
+  }();
+  const size_t nth = n >= 1024 ? max_threads : 1;
+  if (nth > 1) {
+    std::vector<std::thread> pool;
+    try {
+      for (size_t t = 1; t < nth; ++t) pool.emplace_back(eval_range, t, nth);
+    } catch (...) {  // no threads available: the remaining ranges run here
+      for (size_t t = pool.size() + 1; t < nth; ++t) eval_range(t, nth);
+    }
+    eval_range(0, nth);
+    for (auto& th : pool) th.join();
+  } else {
+    eval_range(0, 1);
+  }
+  // ... then choose sequentially, in candidate order (deterministic)
   HashParams best;
   CandidateEval best_e;
   bool have = false;
-  auto consider = [&](const HashParams& h) {
-    if (h.bins < 1) return;
-    if (have && image_of(n, h.bins) > budget) return;
-    const CandidateEval e = evaluate(keys, h, compact, runs);
-    if (!e.ok) return;
+  for (size_t i = 0; i < cand.size(); ++i) {
+    const HashParams& h = cand[i];
+    if (h.bins < 1) continue;
+    if (have && image_of(n, h.bins) > budget) continue;
+    const CandidateEval& e = ev[i];
+    if (!e.ok) continue;
     const double c = e.cost;
-    if (have && fill && e.image_bytes > budget) return;
+    if (have && fill && e.image_bytes > budget) continue;
     const bool tie_better = fill ? e.image_bytes > best_e.image_bytes : e.image_bytes < best_e.image_bytes;
     if (!have || c < best_e.cost - 1e-9 || (c < best_e.cost + 1e-9 && tie_better)) {
       best = h;
       best_e = e;
       have = true;
     }
-  };
-  for (int k = 0; k <= EOS_MAX_K; ++k) {
-    HashParams h = exponent_params(X, mode, k);
-    if (k > 0 && image_of(n, h.bins) > budget) break;
-    consider(h);
-  }
-  const int64_t max_bins = (budget - pad16(8 * n)) / 4;
-  for (double H = 1.0; H <= (double)max_bins; H *= 1.0905077326652577 /* 2^(1/8) */) {
-    consider(log_params(X, mode, (int64_t)H));
   }
   if (!have) return EOS_ERR_UNSUPPORTED;
   return build(X, mode, best, out);  // the directory of the chosen hash only
