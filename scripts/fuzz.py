@@ -4,7 +4,8 @@ fixed wall-clock budget.
 
     python scripts/fuzz.py [--minutes 5] [--seed 0]
 
-1-D: table sizes 1 .. 300000 of several shapes (log-uniform, exact powers of two, duplicate
+1-D: table sizes 1 .. 300000 of several shapes (tables up to 4096 entries also through the
+zero-setup eos_search_direct) (log-uniform, exact powers of two, duplicate
 runs, mixed signs with +-0, zero heads with subnormals, dense keys), every plan kind
 (automatic, exponent k, log |H|, forced tiered depth D), targets drawn around the entries
 (+-1 ulp, midpoints) plus log-uniform, out-of-range and special values.  Indices must be
@@ -90,6 +91,13 @@ def fuzz_1d(rng, dev, stats):
         stats["mismatches"].append({"n": n, "kind": kind, "plan": kw, "levels": t.info.levels,
                                     "first": [float(Y[bad[0]]), int(got[bad[0]]), int(ref[bad[0]])]})
     t.close()
+    if n <= 4096 and plan == 0:  # the zero-setup path on the same table and targets
+        gd = eos.search_direct(torch.from_numpy(X).to(dev), torch.from_numpy(Y).to(dev)).cpu().numpy()
+        stats["direct_tables"] += 1
+        bad = np.flatnonzero(gd != ref)
+        if bad.size:
+            stats["mismatches"].append({"n": n, "kind": kind, "direct": True,
+                                        "first": [float(Y[bad[0]]), int(gd[bad[0]]), int(ref[bad[0]])]})
 
 
 def fuzz_2d(rng, dev, stats):
@@ -145,7 +153,7 @@ def main():
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(a.seed)
-    stats = {"tables": 0, "lookups": 0, "tiered": 0, "max_n": 0, "rejected_plans": 0,
+    stats = {"tables": 0, "lookups": 0, "tiered": 0, "direct_tables": 0, "max_n": 0, "rejected_plans": 0,
              "grids": 0, "pairs": 0, "mismatches": []}
     t_end = time.time() + 60 * a.minutes
     it = 0
