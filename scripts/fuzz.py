@@ -79,7 +79,10 @@ def fuzz_1d(rng, dev, stats):
         if e.name not in ("EOS_ERR_UNSUPPORTED", "EOS_ERR_SIZE"):
             raise
         return
-    Y = targets_for(rng, X, int(rng.integers(1, 1 << 16)))
+    # mostly small launches (the small-tile shape); one in four large enough for the default
+    # tiles (>= half the SMs' worth of tiles)
+    m = int(rng.integers(1, 1 << 16)) if rng.integers(0, 4) else int(rng.integers(1 << 18, 1 << 19))
+    Y = targets_for(rng, X, m)
     got = t.search(torch.from_numpy(Y).to(dev)).cpu().numpy()
     ref = oracle.search(X, Y)
     bad = np.flatnonzero(got != ref)
