@@ -34,6 +34,10 @@ struct eos_grid2d_s {
   int threads_deriv = dv::Shape2DDeriv::kThreads, unroll_deriv = dv::Shape2DDeriv::kUnroll;
   int threads = 512, unroll = 2;
   bool clc = true;
+  // small launches (fewer default tiles than half the SMs; no derivative outputs):
+  // Shape2DSmall, 4x smaller tiles (nullptr: none)
+  const void* fn_small = nullptr;
+  int grid_small = 0, threads_small = 0;
   int32_t flags = 0;
   int32_t wr_off = 0, wt_off = 0, lr_off = 0, lt_off = 0;
   int32_t rr_off = 0, rt_off = 0;
@@ -102,6 +106,18 @@ Interp2DShape gg_shape() {
 template <bool LOGLOG, int REP>
 Interp2DShape gg_pick(int steps) {
   return steps == 1 ? gg_shape<LOGLOG, REP, 1>() : gg_shape<LOGLOG, REP, 0>();
+}
+
+// The small-launch kernel: the default layouts (bank-pinned records, S = 1) only.
+const void* pick_interp_small(int steps, bool loglog, int rep, bool gg) {
+  using SM = dv::Shape2DSmall;
+  using SG = dv::Shape2DSmallGG;
+  if (steps != 1 || rep != 2) return nullptr;
+  if (gg)
+    return loglog ? (const void*)dv::interp2d_kernel<1, SG, false, false, true, 2, true>
+                  : (const void*)dv::interp2d_kernel<1, SG, false, false, false, 2, true>;
+  return loglog ? (const void*)dv::interp2d_kernel<1, SM, false, false, true, 2>
+                : (const void*)dv::interp2d_kernel<1, SM, false, false, false, 2>;
 }
 
 Interp2DShape pick_interp(int steps, bool loglog, int rep, bool gg) {
@@ -174,17 +190,29 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
       (uintptr_t)rho | (uintptr_t)T | (uintptr_t)P | (uintptr_t)dPr | (uintptr_t)dPt;
   const uintptr_t al8 = (uintptr_t)iR | (uintptr_t)iT;
   a.vec_ok = ((al16 & 15) == 0) && ((al8 & 7) == 0);
-  const int threads = deriv ? g->threads_deriv : g->threads;
-  const int64_t per_tile = (int64_t)threads * (deriv ? g->unroll_deriv : g->unroll) * 2;
-  const int64_t tiles = (count + per_tile - 1) / per_tile;
+  int threads = deriv ? g->threads_deriv : g->threads;
+  int64_t per_tile = (int64_t)threads * (deriv ? g->unroll_deriv : g->unroll) * 2;
+  int64_t tiles = (count + per_tile - 1) / per_tile;
+  // fewer tiles than a quarter of the SMs: the small-tile shape spreads the launch over more
+  // CTAs.  (Every CTA stages the whole image, up to ~226 KB, so more CTAs also cost L2
+  // bandwidth: at cfg4 with 1e5 pairs, 49 default tiles, the small shape is slower;
+  // scripts/exp_small_tiles_2d.sh.)
+  const bool sm = !deriv && g->fn_small && 4 * tiles < g->num_sms;
+  if (sm) {  // unroll 1, static schedule (both small shapes)
+    threads = g->threads_small;
+    per_tile = (int64_t)threads * 2;
+    tiles = (count + per_tile - 1) / per_tile;
+  }
   if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;
   a.ntiles = tiles;
-  const bool clc = deriv ? dv::Shape2DDeriv::kClc : g->clc;
-  int64_t grid = clc ? tiles : std::min<int64_t>(deriv ? g->grid_deriv : g->grid, tiles);
+  const bool clc = sm ? false : (deriv ? dv::Shape2DDeriv::kClc : g->clc);
+  int64_t grid = clc ? tiles
+                     : std::min<int64_t>(sm ? g->grid_small : (deriv ? g->grid_deriv : g->grid),
+                                         tiles);
   grid = std::max<int64_t>(grid, 1);
   void* params[] = {&a};
-  EOS_CUDA(launch(deriv ? g->fn_deriv : g->fn, grid, threads, (size_t)g->image_bytes, st,
-                  params));
+  EOS_CUDA(launch(sm ? g->fn_small : (deriv ? g->fn_deriv : g->fn), grid, threads,
+                  (size_t)g->image_bytes, st, params));
   count_launch();
   return EOS_OK;
 }
@@ -397,6 +425,18 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     st = configure(g->fn_deriv, g->threads_deriv, g->image_bytes, g->num_sms, &g->grid_deriv,
                    nullptr);
   if (st != EOS_OK) return fail(st);
+  {
+    const char* small_env = getenv("EOS_SMALL_TILES");  // "0": default tiles only
+    const void* fs = (small_env && small_env[0] == '0') || getenv("EOS_INTERP_VARIANT")
+                         ? nullptr
+                         : pick_interp_small(std::max(g->pr.steps, g->pt.steps), loglog, g->rep,
+                                             g->gg);
+    const int ts = g->gg ? dv::Shape2DSmallGG::kThreads : dv::Shape2DSmall::kThreads;
+    if (fs && configure(fs, ts, g->image_bytes, g->num_sms, &g->grid_small, nullptr) == EOS_OK) {
+      g->fn_small = fs;
+      g->threads_small = ts;
+    }
+  }
   *out = g;
   return EOS_OK;
 }

@@ -5,7 +5,7 @@
 // Tuning knobs, read at create / first use, for A/B experiments only (the
 // defaults are the measured best):
 //   EOS_SEARCH_VARIANT, EOS_TIERED_VARIANT  launch-shape variants by name
-//   EOS_SMALL_TILES=0                       1-D small launches keep the default tiles
+//   EOS_SMALL_TILES=0                       small launches (1-D, 2-D) keep the default tiles
 //   EOS_INTERP_VARIANT                      2-D launch variants by number
 //   EOS_INTERP_REP=0                        2-D plain axes (no cell records)
 //   EOS_GG_SMEM_KB                          smem cap of device-memory grids
