@@ -204,6 +204,36 @@ def test_small_launch_tiles_match_default_tiles_and_oracle(table, kw, monkeypatc
     t_def.close()
 
 
+@pytest.mark.parametrize("loglog,global_grid", [(False, False), (True, False), (False, True),
+                                                (True, True)])
+def test_small_launch_tiles_2d_match_default_tiles_and_oracle(loglog, global_grid, monkeypatch):
+    """2-D launches with fewer default tiles than a quarter of the SMs run the small-tile
+    shape (grid_api.cu launch_interp): brackets and P bit-identical to the default tiles and
+    brackets equal to the oracle's, P within the bar, on both sides of the switch."""
+    w = datagen.workload("cfg4", count=90_001)
+    rho = w.rho_targets.host_fill(0, w.count)
+    T = w.T_targets.host_fill(0, w.count)
+    rho[:3] = [np.nan, w.rho[0] / 3, w.rho[-1] * 3]
+    rho[3:3 + w.rho.size] = w.rho
+    g_small = eos.Grid2D(w.rho, w.T, w.P, loglog=loglog, global_grid=global_grid)
+    monkeypatch.setenv("EOS_SMALL_TILES", "0")
+    g_def = eos.Grid2D(w.rho, w.T, w.P, loglog=loglog, global_grid=global_grid)
+    monkeypatch.delenv("EOS_SMALL_TILES")
+    ref_all = (oracle.interp2d_loglog if loglog else oracle.interp2d)(w.rho, w.T, w.P, rho, T)
+    for count, off in ((1, 0), (7, 1), (1000, 0), (20_001, 1), (73_727, 0), (90_000, 1)):
+        rd, td = to_dev(rho)[off:off + count], to_dev(T)[off:off + count]
+        a = g_small.interp(rd, td)
+        b = g_def.interp(rd, td)
+        torch.cuda.synchronize()
+        for x, y in zip(a, b):
+            assert np.array_equal(x.cpu().numpy(), y.cpu().numpy(), equal_nan=True)
+        assert np.array_equal(a[1].cpu().numpy(), ref_all[1][off:off + count])
+        assert np.array_equal(a[2].cpu().numpy(), ref_all[2][off:off + count])
+        check_interp(a[0].cpu().numpy(), ref_all[0][off:off + count])
+    g_small.close()
+    g_def.close()
+
+
 def test_counters_match_oracle():
     w = datagen.workload("cfg1", count=777_777)
     Y = w.targets.host_fill(0, w.count, w.table)
