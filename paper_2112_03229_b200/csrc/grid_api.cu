@@ -38,6 +38,7 @@ struct eos_grid2d_s {
   // Shape2DSmall, 4x smaller tiles (nullptr: none)
   const void* fn_small = nullptr;
   int grid_small = 0, threads_small = 0;
+  int64_t small_image_bytes = 0;  // the image without G (g_off)
   int32_t flags = 0;
   int32_t wr_off = 0, wt_off = 0, lr_off = 0, lt_off = 0;
   int32_t rr_off = 0, rt_off = 0;
@@ -109,15 +110,14 @@ Interp2DShape gg_pick(int steps) {
 }
 
 // The small-launch kernel: the default layouts (bank-pinned records, S = 1) only.
-const void* pick_interp_small(int steps, bool loglog, int rep, bool gg) {
-  using SM = dv::Shape2DSmall;
+// Always the device-memory-grid flavour: a small launch stages only the image
+// without G (axes, directories, records) and reads each cell's corners as one
+// 32-B quad, so its many CTAs do not each copy the whole grid from L2.
+const void* pick_interp_small(int steps, bool loglog, int rep) {
   using SG = dv::Shape2DSmallGG;
   if (steps != 1 || rep != 2) return nullptr;
-  if (gg)
-    return loglog ? (const void*)dv::interp2d_kernel<1, SG, false, false, true, 2, true>
-                  : (const void*)dv::interp2d_kernel<1, SG, false, false, false, 2, true>;
-  return loglog ? (const void*)dv::interp2d_kernel<1, SM, false, false, true, 2>
-                : (const void*)dv::interp2d_kernel<1, SM, false, false, false, 2>;
+  return loglog ? (const void*)dv::interp2d_kernel<1, SG, false, false, true, 2, true>
+                : (const void*)dv::interp2d_kernel<1, SG, false, false, false, 2, true>;
 }
 
 Interp2DShape pick_interp(int steps, bool loglog, int rep, bool gg) {
@@ -193,15 +193,15 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   int threads = deriv ? g->threads_deriv : g->threads;
   int64_t per_tile = (int64_t)threads * (deriv ? g->unroll_deriv : g->unroll) * 2;
   int64_t tiles = (count + per_tile - 1) / per_tile;
-  // fewer tiles than a quarter of the SMs: the small-tile shape spreads the launch over more
-  // CTAs.  (Every CTA stages the whole image, up to ~226 KB, so more CTAs also cost L2
-  // bandwidth: at cfg4 with 1e5 pairs, 49 default tiles, the small shape is slower;
-  // scripts/exp_small_tiles_2d.sh.)
-  const bool sm = !deriv && g->fn_small && 4 * tiles < g->num_sms;
-  if (sm) {  // unroll 1, static schedule (both small shapes)
+  // fewer tiles than half the SMs: the small-tile shape spreads the launch over more CTAs
+  // (scripts/exp_small_tiles_2d.sh)
+  const bool sm = !deriv && g->fn_small && 2 * tiles < g->num_sms;
+  if (sm) {  // unroll 1, static schedule; G from the cell quads
     threads = g->threads_small;
     per_tile = (int64_t)threads * 2;
     tiles = (count + per_tile - 1) / per_tile;
+    a.image_16 = (int32_t)(g->small_image_bytes / 16);
+    a.gquad = 1;
   }
   if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;
   a.ntiles = tiles;
@@ -212,7 +212,7 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   grid = std::max<int64_t>(grid, 1);
   void* params[] = {&a};
   EOS_CUDA(launch(sm ? g->fn_small : (deriv ? g->fn_deriv : g->fn), grid, threads,
-                  (size_t)g->image_bytes, st, params));
+                  (size_t)(sm ? g->small_image_bytes : g->image_bytes), st, params));
   count_launch();
   return EOS_OK;
 }
@@ -256,7 +256,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     for (int64_t q = 0; q < ncell && ok; ++q) ok = P_host[q] > 0.0;
     if (!ok) return fail(EOS_ERR_UNSUPPORTED);
   }
-  // image: [rho X | rho dir][T X | T dir][G][1/dR][1/dT (RECIP variants)][ln R][ln T][R recs][T recs]
+  // image: [rho X | rho dir][T X | T dir][1/dR][1/dT (RECIP variants)][ln R][ln T][R recs][T recs][G]
   // G is absent for grids in device memory (GG: larger than ~220 KB, or
   // EOS_GRID_GLOBAL), which keep it in g->grid_dev instead (cell quads or row pairs).
   int64_t r_bytes = g->pr.image_bytes, t_bytes = g->pt.image_bytes;
@@ -321,13 +321,16 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   std::vector<uint8_t> ir = eos::make_image(g->pr), it = eos::make_image(g->pt);
   memcpy(img.data(), ir.data(), ir.size());
   memcpy(img.data() + r_bytes, it.data(), it.size());
-  g->g_off = (int32_t)(r_bytes + t_bytes);
-  g->wr_off = (int32_t)(g->g_off + g_bytes);
+  // G last: the image without it (the first g_off bytes) serves the small-launch
+  // kernels, which read the corners from cell quads in device memory
+  g->wr_off = (int32_t)(r_bytes + t_bytes);
   g->wt_off = (int32_t)(g->wr_off + wr_bytes);
   g->lr_off = (int32_t)(g->wt_off + wt_bytes);
   g->lt_off = (int32_t)(g->lr_off + lr_bytes);
   g->rr_off = (int32_t)(g->lt_off + lt_bytes);
   g->rt_off = (int32_t)(g->rr_off + (g->rep ? g->rep_bytes_axis * n_rho : 0));
+  g->g_off = (int32_t)(g->rt_off + (g->rep ? g->rep_bytes_axis * n_T : 0));
+  if (g->g_off + g_bytes != g->image_bytes) return fail(EOS_ERR_CUDA);  // layout invariant
   auto put_rep = [&](const std::vector<double>& Xa, int32_t off) {
     std::vector<double> X(Xa);
     if (loglog)  // records of the log axis (the same host log as the ln R / ln T arrays)
@@ -378,14 +381,21 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   if (e != cudaSuccess) return fail(cuda_status(e));
   st = upload(img, &g->image_dev);
   if (st != EOS_OK) return fail(st);
-  if (g->gg) {
+  const char* small_env = getenv("EOS_SMALL_TILES");  // "0": default tiles only
+  const void* fn_small = (small_env && small_env[0] == '0') || getenv("EOS_INTERP_VARIANT")
+                             ? nullptr
+                             : pick_interp_small(std::max(g->pr.steps, g->pt.steps), loglog,
+                                                 g->rep);
+  // shared-memory grids keep cell quads in device memory too, for the small-launch kernel
+  const bool quads_for_small = !g->gg && fn_small && 32 * ncell <= (int64_t(64) << 20);
+  if (g->gg || quads_for_small) {
     // Cell quads (32 B per cell: the 4 corners in one sector) up to
     // EOS_GG_QUAD_MB (default 1024 MB of quads), else row pairs
     // gq[i (nT-1) + j] = (G[i][j], G[i][j+1]) (two 16-B loads per pair).
     const int64_t w = n_T - 1;
     const char* eq = getenv("EOS_GG_QUAD_MB");
     const int64_t quad_cap = (eq ? atoll(eq) : 1024) << 20;
-    g->gquad = 32 * (n_rho - 1) * w <= quad_cap;
+    g->gquad = quads_for_small || 32 * (n_rho - 1) * w <= quad_cap;
     std::vector<double> q2;
     try {
       q2.resize((size_t)(g->gquad ? 4 * (n_rho - 1) * w : 2 * n_rho * w));
@@ -425,16 +435,12 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     st = configure(g->fn_deriv, g->threads_deriv, g->image_bytes, g->num_sms, &g->grid_deriv,
                    nullptr);
   if (st != EOS_OK) return fail(st);
-  {
-    const char* small_env = getenv("EOS_SMALL_TILES");  // "0": default tiles only
-    const void* fs = (small_env && small_env[0] == '0') || getenv("EOS_INTERP_VARIANT")
-                         ? nullptr
-                         : pick_interp_small(std::max(g->pr.steps, g->pt.steps), loglog, g->rep,
-                                             g->gg);
-    const int ts = g->gg ? dv::Shape2DSmallGG::kThreads : dv::Shape2DSmall::kThreads;
-    if (fs && configure(fs, ts, g->image_bytes, g->num_sms, &g->grid_small, nullptr) == EOS_OK) {
-      g->fn_small = fs;
+  if (fn_small && g->gquad) {  // the small kernel reads quads (not row pairs)
+    const int ts = dv::Shape2DSmallGG::kThreads;
+    if (configure(fn_small, ts, g->g_off, g->num_sms, &g->grid_small, nullptr) == EOS_OK) {
+      g->fn_small = fn_small;
       g->threads_small = ts;
+      g->small_image_bytes = g->g_off;
     }
   }
   *out = g;

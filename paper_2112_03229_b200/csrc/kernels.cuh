@@ -1001,9 +1001,8 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
 // costs more than the static tail (profiles/r01_exp_interp.json).
 using Shape2D = Shape<1024, 1, 1, false>;
 using Shape2DDeriv = Shape<512, 1, 1, false>;  // derivative outputs need > 64 registers
-// launches with fewer tiles than half the SMs: grids in shared memory (one CTA per SM) take
-// half-size tiles, grids in device memory (smaller image, several CTAs per SM) quarter-size
-using Shape2DSmall = Shape<512, 1, 1, false>;
+// launches with fewer tiles than half the SMs: quarter-size tiles, the grid read from cell
+// quads in device memory (grid_api.cu pick_interp_small)
 using Shape2DSmallGG = Shape<256, 1, 1, false>;
 
 template <int S, class SH, bool RECIP, bool DERIV, bool LOGLOG = false, int REP = 0, bool GG = false>

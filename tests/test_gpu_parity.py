@@ -207,10 +207,11 @@ def test_small_launch_tiles_match_default_tiles_and_oracle(table, kw, monkeypatc
 @pytest.mark.parametrize("loglog,global_grid", [(False, False), (True, False), (False, True),
                                                 (True, True)])
 def test_small_launch_tiles_2d_match_default_tiles_and_oracle(loglog, global_grid, monkeypatch):
-    """2-D launches with fewer default tiles than a quarter of the SMs run the small-tile
-    shape (grid_api.cu launch_interp): brackets and P bit-identical to the default tiles and
-    brackets equal to the oracle's, P within the bar, on both sides of the switch."""
-    w = datagen.workload("cfg4", count=90_001)
+    """2-D launches with fewer default tiles than half the SMs run the small-tile kernel
+    (grid_api.cu launch_interp: the image without G, corners from cell quads in device
+    memory): brackets and P bit-identical to the default tiles, brackets equal to the
+    oracle's, P within the bar, on both sides of the switch (74 tiles = 151,552 pairs)."""
+    w = datagen.workload("cfg4", count=160_003)
     rho = w.rho_targets.host_fill(0, w.count)
     T = w.T_targets.host_fill(0, w.count)
     rho[:3] = [np.nan, w.rho[0] / 3, w.rho[-1] * 3]
@@ -220,7 +221,8 @@ def test_small_launch_tiles_2d_match_default_tiles_and_oracle(loglog, global_gri
     g_def = eos.Grid2D(w.rho, w.T, w.P, loglog=loglog, global_grid=global_grid)
     monkeypatch.delenv("EOS_SMALL_TILES")
     ref_all = (oracle.interp2d_loglog if loglog else oracle.interp2d)(w.rho, w.T, w.P, rho, T)
-    for count, off in ((1, 0), (7, 1), (1000, 0), (20_001, 1), (73_727, 0), (90_000, 1)):
+    for count, off in ((1, 0), (7, 1), (1000, 0), (20_001, 1), (151_551, 0), (151_553, 1),
+                       (160_000, 2)):
         rd, td = to_dev(rho)[off:off + count], to_dev(T)[off:off + count]
         a = g_small.interp(rd, td)
         b = g_def.interp(rd, td)
