@@ -36,8 +36,9 @@ struct eos_grid2d_s {
   bool clc = true;
   // small launches (fewer default tiles than half the SMs; no derivative outputs):
   // Shape2DSmall, 4x smaller tiles (nullptr: none)
-  const void* fn_small = nullptr;
-  int grid_small = 0, threads_small = 0;
+  const void* fn_small = nullptr;        // ... without derivative outputs
+  const void* fn_small_deriv = nullptr;  // ... with them
+  int grid_small = 0, grid_small_deriv = 0, threads_small = 0;
   int64_t small_image_bytes = 0;  // the image without G (g_off)
   int32_t flags = 0;
   int32_t wr_off = 0, wt_off = 0, lr_off = 0, lt_off = 0;
@@ -113,9 +114,12 @@ Interp2DShape gg_pick(int steps) {
 // Always the device-memory-grid flavour: a small launch stages only the image
 // without G (axes, directories, records) and reads each cell's corners as one
 // 32-B quad, so its many CTAs do not each copy the whole grid from L2.
-const void* pick_interp_small(int steps, bool loglog, int rep) {
+const void* pick_interp_small(int steps, bool loglog, int rep, bool deriv) {
   using SG = dv::Shape2DSmallGG;
   if (steps != 1 || rep != 2) return nullptr;
+  if (deriv)
+    return loglog ? (const void*)dv::interp2d_kernel<1, SG, false, true, true, 2, true>
+                  : (const void*)dv::interp2d_kernel<1, SG, false, true, false, 2, true>;
   return loglog ? (const void*)dv::interp2d_kernel<1, SG, false, false, true, 2, true>
                 : (const void*)dv::interp2d_kernel<1, SG, false, false, false, 2, true>;
 }
@@ -195,7 +199,8 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   int64_t tiles = (count + per_tile - 1) / per_tile;
   // fewer tiles than half the SMs: the small-tile shape spreads the launch over more CTAs
   // (scripts/exp_small_tiles_2d.sh)
-  const bool sm = !deriv && g->fn_small && 2 * tiles < g->num_sms;
+  const void* fsm = deriv ? g->fn_small_deriv : g->fn_small;
+  const bool sm = fsm && 2 * tiles < g->num_sms;
   if (sm) {  // unroll 1, static schedule; G from the cell quads
     threads = g->threads_small;
     per_tile = (int64_t)threads * 2;
@@ -206,12 +211,12 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;
   a.ntiles = tiles;
   const bool clc = sm ? false : (deriv ? dv::Shape2DDeriv::kClc : g->clc);
-  int64_t grid = clc ? tiles
-                     : std::min<int64_t>(sm ? g->grid_small : (deriv ? g->grid_deriv : g->grid),
-                                         tiles);
+  const int pgrid = sm ? (deriv ? g->grid_small_deriv : g->grid_small)
+                       : (deriv ? g->grid_deriv : g->grid);
+  int64_t grid = clc ? tiles : std::min<int64_t>(pgrid, tiles);
   grid = std::max<int64_t>(grid, 1);
   void* params[] = {&a};
-  EOS_CUDA(launch(sm ? g->fn_small : (deriv ? g->fn_deriv : g->fn), grid, threads,
+  EOS_CUDA(launch(sm ? fsm : (deriv ? g->fn_deriv : g->fn), grid, threads,
                   (size_t)(sm ? g->small_image_bytes : g->image_bytes), st, params));
   count_launch();
   return EOS_OK;
@@ -382,10 +387,11 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   st = upload(img, &g->image_dev);
   if (st != EOS_OK) return fail(st);
   const char* small_env = getenv("EOS_SMALL_TILES");  // "0": default tiles only
-  const void* fn_small = (small_env && small_env[0] == '0') || getenv("EOS_INTERP_VARIANT")
-                             ? nullptr
-                             : pick_interp_small(std::max(g->pr.steps, g->pt.steps), loglog,
-                                                 g->rep);
+  const bool small_ok = !((small_env && small_env[0] == '0') || getenv("EOS_INTERP_VARIANT"));
+  const int steps_max = std::max(g->pr.steps, g->pt.steps);
+  const void* fn_small = small_ok ? pick_interp_small(steps_max, loglog, g->rep, false) : nullptr;
+  const void* fn_small_deriv =
+      small_ok ? pick_interp_small(steps_max, loglog, g->rep, true) : nullptr;
   // shared-memory grids keep cell quads in device memory too, for the small-launch kernel
   const bool quads_for_small = !g->gg && fn_small && 32 * ncell <= (int64_t(64) << 20);
   if (g->gg || quads_for_small) {
@@ -435,10 +441,13 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     st = configure(g->fn_deriv, g->threads_deriv, g->image_bytes, g->num_sms, &g->grid_deriv,
                    nullptr);
   if (st != EOS_OK) return fail(st);
-  if (fn_small && g->gquad) {  // the small kernel reads quads (not row pairs)
+  if (fn_small && fn_small_deriv && g->gquad) {  // the small kernels read quads (not row pairs)
     const int ts = dv::Shape2DSmallGG::kThreads;
-    if (configure(fn_small, ts, g->g_off, g->num_sms, &g->grid_small, nullptr) == EOS_OK) {
+    if (configure(fn_small, ts, g->g_off, g->num_sms, &g->grid_small, nullptr) == EOS_OK &&
+        configure(fn_small_deriv, ts, g->g_off, g->num_sms, &g->grid_small_deriv, nullptr) ==
+            EOS_OK) {
       g->fn_small = fn_small;
+      g->fn_small_deriv = fn_small_deriv;
       g->threads_small = ts;
       g->small_image_bytes = g->g_off;
     }

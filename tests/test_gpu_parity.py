@@ -226,8 +226,10 @@ def test_small_launch_tiles_2d_match_default_tiles_and_oracle(loglog, global_gri
         rd, td = to_dev(rho)[off:off + count], to_dev(T)[off:off + count]
         a = g_small.interp(rd, td)
         b = g_def.interp(rd, td)
+        ad = g_small.interp(rd, td, derivatives=True)  # the derivative kernels switch too
+        bd = g_def.interp(rd, td, derivatives=True)
         torch.cuda.synchronize()
-        for x, y in zip(a, b):
+        for x, y in list(zip(a, b)) + list(zip(ad, bd)):
             assert np.array_equal(x.cpu().numpy(), y.cpu().numpy(), equal_nan=True)
         assert np.array_equal(a[1].cpu().numpy(), ref_all[1][off:off + count])
         assert np.array_equal(a[2].cpu().numpy(), ref_all[2][off:off + count])
