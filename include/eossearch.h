@@ -255,7 +255,10 @@ EOS_API eos_status eos_search_destroy(eos_table t);
  * EOS_MAX_GRID_CELLS.  P lives in shared memory when it fits (~200 KB with
  * the axes), else in device memory (see EOS_GRID_GLOBAL); the axes must fit
  * in shared memory (their images <= ~220 KB, else EOS_ERR_UNSUPPORTED).
- * Copied; bound to the current device. */
+ * Copied; bound to the current device.  A grid held in shared memory is also
+ * kept in device memory as 32-byte cell quads (4x its size, <= ~1 MB): small
+ * launches read their corners from there, so that their many CTAs do not each
+ * stage the whole grid (same results). */
 EOS_API eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, const double* T_host,
                              int64_t n_T, const double* P_host, eos_grid2d* out);
 
