@@ -183,6 +183,7 @@ struct Counters {
 // SmemLookup: the whole table and its directory are in shared memory.
 template <int S, int MODE>
 struct SmemLookup {
+  static constexpr bool kBatchTail = true;  // ragged tiles: one batched lookup per thread
   const double* __restrict__ sX;
   const uint32_t* __restrict__ sD;
   AxisParams a;
@@ -282,6 +283,7 @@ __device__ __forceinline__ int32_t lookup_keys(double y, uint32_t ky,
 
 template <int S, int MODE>
 struct TieredLookup {
+  static constexpr bool kBatchTail = false;  // (batching the tail made the kernel spill)
   const uint32_t* __restrict__ sK;  // keys of T1 (smem)
   const uint32_t* __restrict__ sD;
   AxisParams a;                   // of T1, except xlast = X[n-1] (counter c4)
@@ -534,16 +536,35 @@ __device__ __forceinline__ void search_body(const SearchArgs& args, const LK& lk
 #pragma unroll
       for (int u = 0; u < U; ++u) __stcs(O2 + p0 + u * T, r[u]);
     } else {
-      // ragged / unaligned tile: scalar over its elements
+      // ragged / unaligned tile: each thread's (at most 2U) elements at stride T,
+      // all loads first and one batched lookup, as in the vector body (a
+      // one-at-a-time loop here waited a load latency per element)
+      static_assert(TE == 2 * U * T, "tile = 2U elements per thread");
       const int64_t e0 = head + t * TE;
       const int64_t e1 = min(count, e0 + TE);
       EOS_DCHECK(e0 >= 0 && t >= 0);
-      for (int64_t i = e0 + threadIdx.x; i < e1; i += T) {
-        const double y[1] = {Y[i]};
-        int32_t r[1];
+      if (!CNT && LK::kBatchTail) {
+        double y[2 * U];
+        int32_t r[2 * U];
+#pragma unroll
+        for (int k = 0; k < 2 * U; ++k) {
+          const int64_t i = e0 + threadIdx.x + (int64_t)k * T;
+          y[k] = i < e1 ? Y[i] : 0.0;
+        }
         lk.many(y, r);
-        out[i] = r[0];
-        if (CNT) cn.add(y[0], r[0], args.gofs + i, lk.x_at(r[0]), a);
+#pragma unroll
+        for (int k = 0; k < 2 * U; ++k) {
+          const int64_t i = e0 + threadIdx.x + (int64_t)k * T;
+          if (i < e1) out[i] = r[k];
+        }
+      } else {  // counters / tiered tables: one element at a time (fewer live registers)
+        for (int64_t i = e0 + threadIdx.x; i < e1; i += T) {
+          const double y[1] = {Y[i]};
+          int32_t r[1];
+          lk.many(y, r);
+          out[i] = r[0];
+          if (CNT) cn.add(y[0], r[0], args.gofs + i, lk.x_at(r[0]), a);
+        }
       }
       tn = next_tile(t);
       if (tn < ntiles && full(tn)) load_tile(tn);
