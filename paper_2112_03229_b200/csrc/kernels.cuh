@@ -1109,15 +1109,34 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
     } else {
       const int64_t e0 = t * TE;
       const int64_t e1 = min(count, e0 + TE);
-      for (int64_t q = e0 + threadIdx.x; q < e1; q += T) {
-        int32_t i, j;
-        double dpr, dpt;
-        const double pq = interp_one<S, RECIP, DERIV, LOGLOG, REP, GG>(A.rho[q], A.T[q], i, j, dpr, dpt, sm, A);
-        A.P[q] = pq;
-        if (br) A.iR[q] = i;
-        if (bt) A.iT[q] = j;
-        if (bdr) A.dPr[q] = dpr;
-        if (bdt) A.dPt[q] = dpt;
+      // ragged tile: a thread's (2U) pairs at stride T; with U = 1 the second pair's
+      // coordinates are loaded before the first pair is computed (not where the
+      // 64-register cap of 1024-thread CTAs would make it spill: log-log, and
+      // device-memory grids at 1024 threads)
+      constexpr int E = (U == 1 && !LOGLOG && (!GG || T <= 512)) ? 2 : 1;
+      for (int64_t q0 = e0 + threadIdx.x; q0 < e1; q0 += E * T) {
+        double vr1[E], vt1[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          const int64_t q = q0 + (int64_t)k * T;
+          vr1[k] = q < e1 ? A.rho[q] : 1.0;
+          vt1[k] = q < e1 ? A.T[q] : 1.0;
+        }
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          const int64_t q = q0 + (int64_t)k * T;
+          if (q < e1) {
+            int32_t i, j;
+            double dpr, dpt;
+            const double pq = interp_one<S, RECIP, DERIV, LOGLOG, REP, GG>(vr1[k], vt1[k], i, j,
+                                                                          dpr, dpt, sm, A);
+            A.P[q] = pq;
+            if (br) A.iR[q] = i;
+            if (bt) A.iT[q] = j;
+            if (bdr) A.dPr[q] = dpr;
+            if (bdt) A.dPt[q] = dpt;
+          }
+        }
       }
       tn = next_tile(t);
       if (tn < ntiles && full(tn)) {
