@@ -97,6 +97,22 @@ const void* tiered_fn_mode(int steps, bool cnt) {
   }
 }
 
+// Small launches of tiered tables: 512 x 1 tiles (a quarter of the default
+// 1024 x 2), used like the single-level small shapes when the default tiles
+// would leave most SMs idle.  big (n = 2^20) at 1e4 / 1e5 / 2.5e5 targets:
+// 7.3 / 7.9 / 8.0 -> 3.7 / 4.6 / 6.9 us per launch.
+template <int MODE>
+const void* tiered_small_fn(int steps) {
+  using SH = dv::Shape<512, 1, 1, false>;
+  switch (steps) {
+    case 1: return (const void*)dv::search1d_tiered_kernel<1, MODE, false, SH>;
+    case 2: return (const void*)dv::search1d_tiered_kernel<2, MODE, false, SH>;
+    case 3: return (const void*)dv::search1d_tiered_kernel<3, MODE, false, SH>;
+    case 4: return (const void*)dv::search1d_tiered_kernel<4, MODE, false, SH>;
+    default: return nullptr;
+  }
+}
+
 // Launch-shape variants of the tiered kernel (EOS_TIERED_VARIANT=<name>,
 // tuning experiments; mode 0, no counters, S <= 4).
 template <class SH>
@@ -387,6 +403,16 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
   }
   if (st != EOS_OK) return fail(st);
   const char* small_env = getenv("EOS_SMALL_TILES");  // "0": default tiles only
+  if (t->levels > 0 && !getenv("EOS_TIERED_VARIANT") && !(small_env && small_env[0] == '0')) {
+    const void* fs = t->plan.key_mode == 0 ? tiered_small_fn<0>(t->plan.steps)
+                                           : tiered_small_fn<1>(t->plan.steps);
+    if (fs && configure(fs, 512, t->smem_bytes, t->num_sms, &t->grid_small, nullptr) == EOS_OK) {
+      t->fn_small = fs;
+      t->threads_small = 512;
+      t->unroll_small = 1;
+      t->clc_small = false;
+    }
+  }
   if (t->levels == 0 && !getenv("EOS_SEARCH_VARIANT") && !(small_env && small_env[0] == '0')) {
     const LaunchShape ls = pick_search_small(t->plan.key_mode, t->plan.steps, t->smem_bytes);
     if (ls.fn && configure(ls.fn, ls.threads, t->smem_bytes, t->num_sms, &t->grid_small,

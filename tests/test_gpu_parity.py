@@ -238,6 +238,33 @@ def test_small_launch_tiles_2d_match_default_tiles_and_oracle(loglog, global_gri
     g_def.close()
 
 
+@pytest.mark.parametrize("kind", ["loguniform", "mixed_sign"])
+def test_tiered_small_launch_tiles_match_default_tiles_and_oracle(kind, monkeypatch):
+    """Tiered tables: launches whose default tiles would leave most SMs idle use 512 x 1
+    tiles; bit-exact against the default tiles and the oracle on both sides of the switch."""
+    rng = np.random.default_rng(11)
+    X = np.sort(10.0 ** rng.uniform(-6, 10, 200_003))
+    if kind == "mixed_sign":
+        X = np.sort(np.concatenate([-X[:50_000], X[50_000:]]))
+    Yall = np.concatenate([10.0 ** rng.uniform(-7, 11, 320_000) * rng.choice([-1.0, 1.0], 320_000),
+                           X[::7], [np.nan, np.inf, -np.inf, 0.0]])
+    t_small = eos.Table(X, levels=1)
+    monkeypatch.setenv("EOS_SMALL_TILES", "0")
+    t_def = eos.Table(X, levels=1)
+    monkeypatch.delenv("EOS_SMALL_TILES")
+    for count, off in ((1, 0), (999, 3), (100_003, 1), (303_103, 0), (320_000, 5)):
+        Y = Yall[off:off + count]
+        yd = to_dev(Yall)[off:off + count]
+        a = t_small.search(yd)
+        b = t_def.search(yd)
+        torch.cuda.synchronize()
+        ref = oracle.search(X, Y)
+        assert_same(a.cpu().numpy(), ref, Y)
+        assert_same(b.cpu().numpy(), ref, Y)
+    t_small.close()
+    t_def.close()
+
+
 def test_counters_match_oracle():
     w = datagen.workload("cfg1", count=777_777)
     Y = w.targets.host_fill(0, w.count, w.table)
