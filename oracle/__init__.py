@@ -49,6 +49,8 @@ def lib():
         L.oracle_counters.argtypes = [P, I64, P, P, I64, I64, P]
         L.oracle_interp2d_deriv.argtypes = [P, I64, P, I64, P, P, P, I64, P, P]
         L.oracle_interp2d_loglog.argtypes = [P, I64, P, I64, P, P, P, I64, P, P, P, P, P]
+        L.oracle_mix64.argtypes = [ctypes.c_uint64]
+        L.oracle_mix64.restype = ctypes.c_uint64
         _lib = L
     return _lib
 
@@ -153,6 +155,11 @@ def interp2d_loglog(R, Tax, G, rho, T, threads: int | None = None):
     with ThreadPoolExecutor(threads) as ex:
         list(ex.map(run, _chunks(m, threads)))
     return P, iR, iT, dr, dt
+
+
+def mix64(z: int) -> int:
+    """The splitmix64 finalizer of counter c2 (eos_oracle.c oracle_mix64)."""
+    return int(lib().oracle_mix64(z & 0xFFFFFFFFFFFFFFFF))
 
 
 def counters(X, Y, idx, global_offset: int = 0) -> np.ndarray:

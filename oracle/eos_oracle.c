@@ -152,14 +152,18 @@ void oracle_interp2d_loglog(const double* R, int64_t nR, const double* Tax, int6
  * "Counters").  Accumulated (+=) into c[8], all sums modulo 2^64:
  *   c0 = number of targets
  *   c1 = sum of idx
- *   c2 = sum of mix64((global_position << 20) | idx)    (position-aware checksum)
+ *   c2 = sum of mix64(mix64(global_position) ^ idx)     (position-aware checksum;
+ *        DESIGN.md R25: mix64 is a bijection of 64-bit words, so for a fixed
+ *        position distinct indices give distinct terms, at any n and position)
  *   c3 = #{y : !(y >= X[0])}   (below range or NaN: "no such lower bound")
  *   c4 = #{y : y > X[n-1]}     (above range: "higher than the highest")
  *   c5 = #{y : y is NaN}
  *   c6 = #{y : y == X[idx]}    (exact ties with a table entry)
  *   c7 = 0 (reserved)
- * mix64 is the splitmix64 finalizer, written out here independently. */
-static uint64_t oracle_mix64(uint64_t z) {
+ * mix64 is the splitmix64 finalizer, written out here independently; it is
+ * pinned to the published splitmix64 output streams (tests/golden/
+ * splitmix64_vectors.txt: output k of seed s is mix64(s + k * 0x9E3779B97F4A7C15)). */
+uint64_t oracle_mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
   return z ^ (z >> 31);
@@ -172,7 +176,7 @@ void oracle_counters(const double* X, int64_t n, const double* Y, const int32_t*
     uint64_t k = (uint64_t)idx[i];
     c[0] += 1;
     c[1] += k;
-    c[2] += oracle_mix64(((uint64_t)(global_offset + i) << 20) | k);
+    c[2] += oracle_mix64(oracle_mix64((uint64_t)(global_offset + i)) ^ k);
     c[3] += !(y >= X[0]);
     c[4] += (y > X[n - 1]);
     c[5] += (y != y);

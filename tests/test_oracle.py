@@ -223,6 +223,38 @@ def _mix64_np(z):
     return z ^ (z >> np.uint64(31))
 
 
+def test_mix64_published_splitmix64_vectors():
+    """oracle_mix64 reproduces the published splitmix64 streams (tests/golden/
+    splitmix64_vectors.txt): output k of seed s = mix64(s + k * golden gamma)."""
+    import os
+    gamma = 0x9E3779B97F4A7C15
+    n = 0
+    with open(os.path.join(os.path.dirname(__file__), "golden", "splitmix64_vectors.txt")) as f:
+        for raw in f:
+            tok = raw.split("#", 1)[0].split()
+            if not tok:
+                continue
+            assert tok[0] == "seed"
+            s = int(tok[1], 0)
+            for k, want in enumerate(tok[2:], start=1):
+                assert oracle.mix64((s + k * gamma) & 0xFFFFFFFFFFFFFFFF) == int(want, 0)
+                n += 1
+    assert n == 8
+
+
+def test_counter_c2_distinguishes_position_and_index_at_large_n():
+    """R25: c2's term mix64(mix64(pos) ^ idx) differs for different indices at the same
+    position, also past 2^20 entries and positions (the round-1 packing (pos << 20) | idx
+    aliased there)."""
+    X = np.array([1.0, 2.0])
+    pos = (1 << 33) + 5
+    a = oracle.counters(X, np.array([1.5]), np.array([1 << 21], np.int32), pos)[2]
+    b = oracle.counters(X, np.array([1.5]), np.array([0], np.int32), pos)[2]
+    c = oracle.counters(X, np.array([1.5]), np.array([0], np.int32), pos + (1 << 1))[2]
+    assert len({int(a), int(b), int(c)}) == 3
+    assert int(b) == oracle.mix64(oracle.mix64(pos) ^ 0)
+
+
 def test_counters_match_definitions():
     rng = np.random.default_rng(3)
     X = np.sort(10.0 ** rng.uniform(-3, 3, 100))
@@ -234,7 +266,7 @@ def test_counters_match_definitions():
     c = oracle.counters(X, Y, idx, off)
     pos = np.arange(Y.size, dtype=np.uint64) + np.uint64(off)
     with np.errstate(over="ignore"):
-        c2 = np.sum(_mix64_np((pos << np.uint64(20)) | idx.astype(np.uint64)), dtype=np.uint64)
+        c2 = np.sum(_mix64_np(_mix64_np(pos) ^ idx.astype(np.uint64)), dtype=np.uint64)
     assert c[0] == Y.size
     assert c[1] == idx.astype(np.uint64).sum()
     assert c[2] == c2
