@@ -1,22 +1,28 @@
 #!/usr/bin/env python
 """bench.py -- throughput of the hot path on B200 (the driver's contract).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg5] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, NCCL)
 
-A step = one pass of the hot path (stage table, stream
-targets, bin lookup, in-bin search, fix-up, store indices) over one batch of
-synthetic input resident in HBM: ONE kernel launch of eos_search (cfg4: of
-eos_interp2d).  Default workload: BASELINE.json configs[1] (cfg2: n=300,
-2^27 fp64 targets per GPU, weak scaling).  cfg5 shards its fixed 8*2^30
-targets over the ranks (strong scaling).
+`--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1, a free port); under torchrun the world
+size must equal N.
 
-Prints ONE JSON line on rank 0.  `value` = lookups (pairs for cfg4) of all
-ranks / max-over-ranks device time, in G/s.  `e2e` = the same metric through
-the C-ABI host-buffer entry point (eos_search_host: pinned H2D + search + D2H
-inside the timed region).  `roofline` = the kernel's algorithmic bytes / its
-CUDA-event launch time vs the measured HBM peak.  `cpu_baseline` = the CPU
-oracle (oracle/, test infrastructure) timed on this host on a bounded sample.
+A step = one pass of the hot path (stage table, stream targets, bin
+lookup, in-bin search, fix-up, store indices) over one batch of synthetic input resident
+in HBM: ONE kernel launch of eos_search (cfg4: of eos_interp2d).  Default workload:
+BASELINE.json configs[4] (cfg5: n=4096 clustered table, 8*2^30 fp64 targets sharded
+evenly over the ranks -- the configuration the metric "Glookups/s per GPU and box
+(1/2/4/8 B200)" is quoted on; 103 GB, it fits one B200).  Other configs are parity cases
+(tests/); --workload selects them for diagnostics.
+
+Prints ONE JSON line on rank 0.  `value` = lookups (pairs for cfg4) of all ranks /
+max-over-ranks device time, in G/s.  `e2e` = the same metric through the C-ABI
+host-buffer entry point (eos_search_host: pinned H2D + search + D2H inside the timed
+region).  `roofline` = the kernel's algorithmic bytes / its CUDA-event launch time vs the
+measured HBM copy peak, and vs the same-mix stream ceiling measured in this run
+(measure/probes.cu).  `cpu_baseline` = the CPU oracle (oracle/, test infrastructure)
+timed on this host on a bounded sample, all cores and one core.
 """
 from __future__ import annotations
 
@@ -39,9 +45,9 @@ FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback (6.65 TB/s), used only witho
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--workload", default="cfg2",
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="cfg5",
                     choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "paper", "big", "big2d"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--k", type=int, default=None, help="override the directory k (default: auto)")
@@ -298,8 +304,20 @@ def run_ours(a, d: Dist):
     if not a.no_e2e:
         e2e = run_e2e(a, d, w, obj, offset, count, total, is2d, dev)
 
+    # same-mix stream ceiling, measured now on this rank's own buffers (trivial kernels of
+    # measure/probes.cu moving the same bytes per unit); the search output is rewritten
+    # afterwards only by the probe, so it runs after the counters
+    import measure
+    if is2d:
+        ceiling = measure.stream_ceiling_2d(rho, T, P, iR, iT)
+    else:
+        ceiling = measure.stream_ceiling_1d(Y, out)
+    cg = torch.tensor([ceiling["gbs"]], dtype=torch.float64, device=dev)
+    d.allreduce(cg, "min")
+
     hbm_peak, peak_src = peaks()
     achieved = bytes_per * count / (kern_ms * 1e-3) / 1e9
+    plan = plan_signature(a, obj, is2d)
     res = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -313,18 +331,8 @@ def run_ours(a, d: Dist):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded counter-based generators, generated in HBM; DESIGN.md input recipe)",
-        "config": {
-            "workload": a.workload,
-            "desc": w.note,
-            "units_per_gpu": count,
-            "units_total": total,
-            "table": info,
-            "bytes_per_unit": bytes_per,
-            "l2": f"inputs larger than L2: {bytes_per * count / 1e9:.2f} GB streamed per step per GPU "
-                  "(126 MB L2), no flush needed" if bytes_per * count > 4 * 126e6 else
-                  "inputs L2-resident (launch-bound parity config)",
-            "parallelism": f"dp{d.world} (target-stream sharding, no data-path collective)",
-        },
+        "config": bench_config(a, w, d.world),
+        "plan": {"table": info, "launch": plan},
         "gpu_launches": int(launches),
         "timing": ("eager: K launches, CUDA events per launch" if a.eager else
                    f"CUDA graph of the K={a.steps} search launches ({launches_captured} captured), "
@@ -335,7 +343,7 @@ def run_ours(a, d: Dist):
             "peak": hbm_peak,
             "unit": "GB/s",
             "frac": round(achieved / hbm_peak, 4),
-            "traffic": ncu_traffic(a.workload),
+            "traffic": ncu_traffic(a.workload, count, plan),
             "kernel": "interp2d_kernel" if is2d else (
                 "search1d_direct_kernel" if a.direct else
                 "search1d_tiered_kernel" if obj.info.levels > 0 else "search1d_kernel"),
@@ -343,33 +351,65 @@ def run_ours(a, d: Dist):
             "kernel_ms_avg_max_rank": round(kern_ms_max, 5),
             "algorithmic_bytes_per_launch": bytes_per * count,
             "peak_source": peak_src,
+            "stream_ceiling": {**ceiling, "gbs_min_over_ranks": float(cg[0])},
+            "frac_vs_stream": round(achieved / float(cg[0]), 4),
             "note": ("peak = 1:1 copy bandwidth; this stream reads:writes "
                      + ("1:1 (16 B in, 16 B out per pair)" if is2d and not a.derivatives else
                         "1:2 (16 B in, 32 B out per pair)" if is2d else
                         "2:1 (8 B in, 4 B out per lookup)")
-                     + ", so frac can exceed 1 (DESIGN.md §11)"),
+                     + ", so frac can exceed 1; frac_vs_stream divides by a trivial kernel "
+                       "moving the same bytes per unit on the same buffers in this run"),
         },
         "clocks": clk.summary(),
         "e2e": e2e,
         "trials": trials,
     }
     if not is2d and obj.info.levels > 0:
-        # tiered table: each level reads one 32-B sector from L2; the
-        # L2 (LTS) throughput, not HBM, bounds it.  LTS cap ~6300 B/clk is the guide's
-        # B300 measurement (B300_MICROARCH.md "LTS throughput cap"), scaled by the SM clock.
-        lts_b = 12 + 32 * obj.info.levels
-        mhz = res["clocks"].get("sm_mhz") or 1965.0
-        lts_ach = lts_b * count / (kern_ms * 1e-3) / 1e9
-        lts_cap = 6300.0 * mhz * 1e6 / 1e9
-        res["roofline"]["l2"] = {"bound": "lts", "bytes_per_unit": lts_b, "achieved": round(lts_ach, 1),
-                                 "peak_est": round(lts_cap, 1), "unit": "GB/s",
-                                 "frac": round(lts_ach / lts_cap, 4),
-                                 "peak_source": "6300 B/clk (B300_MICROARCH.md) x median SM clock"}
+        # tiered table: each level reads one 32-B sector from L2; random
+        # sector gathers, not HBM, bound it.  Ceiling measured now (measure/probes.cu:
+        # the same 256-bit load, an L2-resident buffer of the levels' size).
+        gl = measure.l2_gather_ceiling(max(int(obj.info.level_bytes), 1 << 20))
+        levels = obj.info.levels
+        ach = levels * count / (kern_ms * 1e-3)
+        res["roofline"]["l2"] = {
+            "bound": "l1tex/l2 sector gathers", "sectors_per_lookup": levels,
+            "achieved_gsectors_s": round(ach / 1e9, 2),
+            "peak_gsectors_s": round(gl["sectors_per_s"] / 1e9, 2),
+            "frac": round(ach / gl["sectors_per_s"], 4), "peak_source": "measured",
+            "probe": gl}
     if counters is not None:
         res["validation"] = {"counters_u64": counters}
     if d.world == 1 and d.rank == 0 and not a.no_cpu:
         res["cpu_baseline"] = cpu_baseline(w, is2d, loglog=a.loglog, deriv=a.derivatives)
     return res
+
+
+def bench_config(a, w, world):
+    """The workload this line measures (identical in both arms)."""
+    strong = a.workload == "cfg5"
+    per_gpu = (a.count or w.count) // (world if strong else 1)
+    total = (a.count or w.count) if strong else per_gpu * world
+    bytes_per = (48 if a.derivatives else 32) if w.is_2d else 12
+    cfg = {"workload": a.workload, "desc": w.note, "units_total": total,
+           "units_per_gpu": per_gpu, "bytes_per_unit": bytes_per,
+           "parallelism": f"dp{world} (target-stream sharding, no data-path collective)",
+           "l2": (f"inputs larger than L2: {bytes_per * per_gpu / 1e9:.2f} GB streamed per step per "
+                  "GPU (126 MB L2), no flush needed") if bytes_per * per_gpu > 4 * 126e6 else
+                 "inputs L2-resident (launch-bound parity config)"}
+    for k in ("loglog", "derivatives", "global_grid", "direct"):
+        if getattr(a, k, False):
+            cfg[k] = True
+    return cfg
+
+
+def plan_signature(a, obj, is2d):
+    if is2d:
+        return {"kind": "interp2d", "loglog": a.loglog, "global_grid": a.global_grid}
+    i = obj.info
+    return {"kind": "tiered" if i.levels > 0 else ("direct" if a.direct else "search"),
+            "hash_kind": i.hash_kind, "bins": i.bins, "steps": i.steps,
+            "dir_entry_bytes": i.dir_entry_bytes, "fast_steps": i.fast_steps,
+            "rare_steps": i.rare_steps, "levels": i.levels}
 
 
 def run_e2e(a, d, w, obj, offset, count, total, is2d, dev):
@@ -444,13 +484,16 @@ def fill_host_parallel(w, offset, count, out, threads=None):
         list(ex.map(job, range(0, count, step)))
 
 
-def ncu_traffic(workload):
+def ncu_traffic(workload, count, plan):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from an
+    `ncu --set full` capture of exactly this launch -- same workload, same units per GPU,
+    same plan -- kept under profiles/ (scripts/ncu_traffic.py); else null."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
         v = d.get(workload)
-        if isinstance(v, dict):
+        if isinstance(v, dict) and v.get("captured_units") == count and v.get("plan") == plan:
             return v.get("dram_bytes_per_launch")
     return None
 
@@ -485,51 +528,84 @@ def cpu_sample_size(w, is2d):
 def cpu_baseline(w, is2d, min_cpu_s: float = 12.0, max_passes: int = 20, loglog: bool = False,
                  deriv: bool = False):
     """The oracle as it stands, on the first `sample` units of the workload, repeated
-    until about `min_cpu_s` seconds of CPU work (threads x wall) are done."""
+    until about `min_cpu_s` seconds of CPU work (threads x wall) are done, over all host
+    cores; plus the paper's single-core protocol ("All the tests were run on a
+    single core"): ns per unit on a fixed 2^24-unit prefix (2^22 pairs in 2-D), 1 thread."""
     threads = host_cores()
     sample = cpu_sample_size(w, is2d)
     times = []
     while not times or (sum(times) * threads < min_cpu_s and len(times) < max_passes):
         times.append(oracle_run(w, is2d, sample, threads, loglog, deriv))
     dt = float(np.sum(times))
+    one = min(w.count, (1 << 22) if is2d else (1 << 24))
+    t1 = oracle_run(w, is2d, one, 1, loglog, deriv)
     return {"value": round(len(times) * sample / dt / 1e9, 5),
             "unit": "Gpairs/s" if is2d else "Glookups/s", "cores": threads, "kind": "oracle",
             "sample": f"first {sample} units of {w.name} (host-generated, same recipe) x "
                       f"{len(times)} passes, oracle/eos_oracle.c over {threads} threads; "
-                      f"{dt:.2f} s wall ({dt * threads:.1f} CPU-s); cpu: {cpu_model()}"}
+                      f"{dt:.2f} s wall ({dt * threads:.1f} CPU-s); cpu: {cpu_model()}",
+            "single_core": {"ns_per_unit": round(t1 / one * 1e9, 2), "units": one, "threads": 1,
+                            "value": round(one / t1 / 1e9, 6),
+                            "protocol": "P:222 single core; first 2^24 units (2^22 pairs)"}}
 
 
 # ------------------------------------------------------ reference arm ------
 def run_reference(a, d: Dist):
-    """The oracle as the reference arm: rank 0 only, bounded sample per step."""
+    """The oracle as the reference arm, on rank 0 only: exactly W warm-up and K timed steps
+    of the same workload and config as our arm, each step a bounded sample of it (the
+    first `sample` units, sized from the warm-up rate so that the K steps take about a
+    minute of wall time)."""
     import datagen
     w = datagen.workload(a.workload)
     is2d = w.is_2d
     threads = host_cores()
-    sample = min(w.count, (1 << 22) if is2d else (1 << 24))
-    for _ in range(min(a.warmup, 1)):
-        oracle_run(w, is2d, min(sample, 1 << 16), threads, a.loglog, a.derivatives)
-    times = [oracle_run(w, is2d, sample, threads, a.loglog, a.derivatives)
-             for _ in range(max(1, min(a.steps, 10)))]
-    s = float(np.mean(times))
+    probe = min(w.count, 1 << 16)
+    t = oracle_run(w, is2d, probe, threads, a.loglog, a.derivatives)
+    rate = probe / max(t, 1e-6)
+    cap = min(w.count, (1 << 23) if is2d else (1 << 25))
+    sample = int(min(cap, max(probe, rate * 60.0 / max(a.steps, 1))))
+    for _ in range(a.warmup):
+        oracle_run(w, is2d, sample, threads, a.loglog, a.derivatives)
+    times = [oracle_run(w, is2d, sample, threads, a.loglog, a.derivatives) for _ in range(a.steps)]
+    s = float(np.mean(times)) if times else t
     value = sample / s / 1e9
     unit = "Gpairs/s" if is2d else "Glookups/s"
     return {
-        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": unit,
-        "n_gpus": d.world, "steps": len(times), "warmup": a.warmup, "ms_per_step": round(s * 1e3, 3),
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": unit,
+        "n_gpus": d.world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(s * 1e3, 3),
         "higher_is_better": True, "scaling": "strong" if a.workload == "cfg5" else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": a.workload, "desc": w.note, "sample_units_per_step": sample},
-        "cpu_baseline": {"value": round(value, 5), "unit": unit, "cores": threads, "kind": "oracle",
-                         "sample": f"first {sample} units of {w.name} per step; cpu: {cpu_model()}"},
-        "e2e": {"value": round(value, 5), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "reference arm = the CPU oracle (no reference implementation exists; PAPER.md only)",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (same recipe, host-generated)",
+        "config": bench_config(a, w, d.world),
+        "cpu_baseline": {"value": round(value, 6), "unit": unit, "cores": threads, "kind": "oracle",
+                         "sample": f"each step: the first {sample} units of {w.name}, oracle/"
+                                   f"eos_oracle.c over {threads} threads; cpu: {cpu_model()}"},
+        "e2e": {"value": round(value, 6), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference arm = the CPU oracle (no reference implementation exists; PAPER.md "
+                "only); one step = the oracle over a bounded sample of the workload",
     }
+
+
+def self_launch(a) -> int:
+    """--gpus N outside a torchrun environment: re-run this script under
+    torch.distributed.run with N ranks on this node (127.0.0.1, a free port)."""
+    import socket
+    import subprocess
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(a))
     d = Dist()
+    if d.world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={d.world}")
     if a.impl == "reference":
         if d.rank == 0:
             print(json.dumps(run_reference(a, d)), flush=True)

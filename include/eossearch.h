@@ -88,6 +88,15 @@ typedef struct {
   int32_t pad_;
   int64_t top_n;       /* n1 = ceil(n / 8^D) (image_bytes then counts 4 B per T1 entry) */
   int64_t level_bytes; /* device bytes of the levels (0 when D == 0) */
+  /* lifting layout of the search kernel (ABI >= 3): directory entries of 2 B
+   * (lo | occ << 12) or 4 B (lo | occ << 16) in the image; fast_steps = the
+   * fixed binary-lifting steps SF (0: all S steps in a runtime loop);
+   * rare_steps = 1 if some bin holds >= 2^SF entries (its larger strides run
+   * in a branch taken only by lanes that land in such a bin). */
+  int32_t dir_entry_bytes;
+  int32_t fast_steps;
+  int32_t rare_steps;
+  int32_t pad2_;
 } eos_table_info_t;
 
 /* ---------------------------------------------------------------------------
@@ -245,8 +254,12 @@ EOS_API eos_status eos_search_destroy(eos_table t);
  *   P = (1-tx)((1-ty) G[ci][cj] + ty G[ci][cj+1])
  *     +    tx ((1-ty) G[ci+1][cj] + ty G[ci+1][cj+1])
  * The weights may be evaluated as (rho - R[ci]) * (1/(R[ci+1] - R[ci])) with
- * the inverse precomputed at create (a few ulp from the divide; the results
- * stay within 1e-12 relative of the formula, BASELINE.json north star).
+ * the inverse precomputed at create (a few ulp of t from the divide): then
+ * |P - formula| <= 1e-12 (|G00| + |G01| + |G10| + |G11|) of the cell corners,
+ * i.e. within 1e-12 relative of P wherever the corners share a sign (the
+ * BASELINE.json bar; grids whose P changes sign inside a cell can cancel, and
+ * only the corner-scaled bound holds there).  EOS_GRID_EXACT divides exactly
+ * as the formula does.
  * ------------------------------------------------------------------------- */
 
 /* rho_host fp64[n_rho], T_host fp64[n_T]: strictly increasing, finite,
@@ -272,11 +285,16 @@ EOS_API eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, cons
                            *   dP/drho = P (d ln P / d ln rho) / rho on the cell. */
 #define EOS_GRID_GLOBAL 2 /* flag bit: keep the grid in device memory even if it would fit in
                            * shared memory (grids whose P does not fit, n_rho n_T 8 B >
-                           * ~200 KB, always live there): cell quads (the 4 corners of a cell,
-                           * 32 B, read with one load per pair; 4x the grid) up to 1 GB of
-                           * quads, else row pairs (G[i][j], G[i][j+1]) read with two 16-byte
-                           * loads per pair (2x the grid); the axes stay in shared memory
-                           * (their images must fit: ~220 KB).  Same results. */
+                           * ~200 KB, always live there) as cell quads (the 4 corners of a
+                           * cell, 32 B, read with one load per pair; 4x the grid); the axes
+                           * stay in shared memory (their images must fit: ~220 KB).  Same
+                           * results. */
+#define EOS_GRID_EXACT 4  /* flag bit: weights t = (x - X[c]) / (X[c+1] - X[c]) with the fp64
+                           * divide, in the formula's order: P bit-identical to the formula
+                           * evaluated in fp64 without contraction (linear grids).  Without it
+                           * the default layout multiplies by a precomputed 1/(X[c+1] - X[c])
+                           * (conflict-free bank-pinned cell records, no divides): a few ulp of
+                           * t, i.e. |dP| <= ~1e-15 (|G| summed over the cell corners). */
 #define EOS_MAX_GRID_CELLS ((int64_t)1 << 28) /* n_rho n_T (EOS_ERR_SIZE above) */
 EOS_API eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const double* T_host,
                                 int64_t n_T, const double* P_host, int32_t flags, eos_grid2d* out);
@@ -299,7 +317,8 @@ EOS_API eos_status eos_interp2d_ex(eos_grid2d g, const double* rho_dev, const do
                            double* P_out_dev, int32_t* irho_out_dev, int32_t* iT_out_dev,
                            double* dPdrho_out_dev, double* dPdT_out_dev, void* stream);
 
-/* End-to-end form with host buffers (see eos_search_host). */
+/* End-to-end form with host buffers (see eos_search_host): EOS_ERR_ALIAS if
+ * an output overlaps an input or another output (checked before any copy). */
 EOS_API eos_status eos_interp2d_host(eos_grid2d g, const double* rho_host, const double* T_host,
                              int64_t count, double* P_out_host, int32_t* irho_out_host,
                              int32_t* iT_out_host, void* stream);
@@ -312,7 +331,7 @@ EOS_API eos_status eos_grid2d_destroy(eos_grid2d g);
  * Misc
  * ------------------------------------------------------------------------- */
 EOS_API const char* eos_status_str(eos_status s); /* static string, never NULL */
-EOS_API int32_t eos_abi_version(void);            /* 2 */
+EOS_API int32_t eos_abi_version(void);            /* 3 */
 /* Kernel launches issued by this library since load (all entry points). */
 EOS_API int64_t eos_launch_count(void);
 

@@ -1,0 +1,213 @@
+// probes.cu -- roofline ceilings measured on the box by bench.py (harness code,
+// not the product path; none of the method's arithmetic is here).
+//
+//  probe_stream  : the search's memory mix with no search: read fp64 targets,
+//                  write one int32 per target (8 B in, 4 B out = 12 B per
+//                  unit, the 1-D algorithmic bytes), and the 2-D mix (2 fp64
+//                  in; fp64 + 2 int32 out = 32 B per pair).  The best of a few
+//                  trivial launch shapes is the same-mix stream ceiling that
+//                  bench.py reports next to the 1:1 copy peak of
+//                  MEASURED_PEAKS.json (frac_vs_stream).
+//  probe_gather  : random 32-byte sector gathers from an L2-resident buffer
+//                  with the tiered kernel's load (ld.global.nc.L1::no_allocate
+//                  .v8.u32, one sector per lane): the on-chip ceiling of the
+//                  tiered-table level walk.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace {
+
+__device__ __forceinline__ double2 ldcs2(const double2* p) { return __ldcs(p); }
+
+// out[i] = low word of the target's bits xor its high word: a value that
+// depends on every loaded byte, so nothing is optimised away.
+__device__ __forceinline__ int32_t fold(double v) {
+  return __double2loint(v) ^ __double2hiint(v);
+}
+
+// shape A: one CTA per tile of T threads x U double2 (no persistence)
+template <int T, int U>
+__global__ void __launch_bounds__(T) k_stream_tiles(const double2* __restrict__ y,
+                                                    int2* __restrict__ out, int64_t pairs) {
+  const int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x;
+  double2 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = base + (int64_t)u * T;
+    v[u] = i < pairs ? ldcs2(y + i) : make_double2(0.0, 0.0);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = base + (int64_t)u * T;
+    if (i < pairs) __stcs(out + i, make_int2(fold(v[u].x), fold(v[u].y)));
+  }
+}
+
+// shape B: persistent grid-stride with the next tile's loads issued before the
+// current tile's stores (the search kernel's static schedule)
+template <int T, int U>
+__global__ void __launch_bounds__(T, 1) k_stream_persist(const double2* __restrict__ y,
+                                                         int2* __restrict__ out, int64_t pairs) {
+  const int64_t tiles = pairs / ((int64_t)T * U);
+  double2 v[U];
+  int64_t t = blockIdx.x;
+  if (t < tiles) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ldcs2(y + t * T * U + threadIdx.x + u * T);
+  }
+  while (t < tiles) {
+    const int64_t p0 = t * T * U + threadIdx.x;
+    int2 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = make_int2(fold(v[u].x), fold(v[u].y));
+    const int64_t tn = t + gridDim.x;
+    if (tn < tiles) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ldcs2(y + tn * T * U + threadIdx.x + u * T);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) __stcs(out + p0 + u * T, r[u]);
+    t = tn;
+  }
+  // tail pairs (not a whole tile): by CTA 0
+  if (blockIdx.x == 0)
+    for (int64_t i = tiles * T * U + threadIdx.x; i < pairs; i += T)
+      __stcs(out + i, make_int2(fold(y[i].x), fold(y[i].y)));
+}
+
+// 2-D mix: per pair read rho, T (fp64), write P (fp64) and two int32
+template <int T>
+__global__ void __launch_bounds__(T) k_stream2d(const double2* __restrict__ a,
+                                                const double2* __restrict__ b,
+                                                double2* __restrict__ p, int2* __restrict__ i1,
+                                                int2* __restrict__ i2, int64_t pairs2) {
+  const int64_t i = (int64_t)blockIdx.x * T + threadIdx.x;
+  if (i >= pairs2) return;
+  const double2 x = ldcs2(a + i), z = ldcs2(b + i);
+  __stcs(p + i, make_double2(x.x + z.x, x.y + z.y));
+  __stcs(i1 + i, make_int2(fold(x.x), fold(x.y)));
+  __stcs(i2 + i, make_int2(fold(z.x), fold(z.y)));
+}
+
+__device__ __forceinline__ uint64_t smix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// G independent gather chains per thread, `rounds` dependent rounds each: the
+// next sector index depends on the loaded data (as in a level walk), so the
+// loads cannot be hoisted.  One 32-B sector per lane per load.
+template <int G>
+__global__ void __launch_bounds__(1024, 1) k_gather(const uint32_t* __restrict__ buf,
+                                                   uint64_t mask, int rounds,
+                                                   uint32_t* __restrict__ sink) {
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t s[G];
+  uint32_t acc = 0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) s[g] = smix(tid * G + g) & mask;
+  for (int r = 0; r < rounds; ++r) {
+    uint32_t k[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(k[g][0]), "=r"(k[g][1]), "=r"(k[g][2]), "=r"(k[g][3]), "=r"(k[g][4]),
+                     "=r"(k[g][5]), "=r"(k[g][6]), "=r"(k[g][7])
+                   : "l"(buf + 8 * s[g]));
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t x = k[g][0] ^ k[g][3] ^ k[g][7];
+      acc += x;
+      s[g] = (s[g] * 0x9E3779B97F4A7C15ULL + x + 1) & mask;
+    }
+  }
+  if (acc == 0x12345678u) sink[0] = acc;  // practically never: keeps the loads live
+}
+
+__global__ void k_fill(uint32_t* buf, uint64_t words) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride)
+    buf[i] = (uint32_t)smix(i);
+}
+
+int sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Number of 1-D stream shapes (variant 0 .. probe_stream_variants()-1).
+int probe_stream_variants(void) { return 4; }
+
+// One launch of the 1-D same-mix stream over n targets (n even, y 16-B and
+// out 8-B aligned).  Returns a cudaError_t.
+int probe_stream(const double* y, int32_t* out, int64_t n, int variant, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t pairs = n / 2;
+  const double2* y2 = reinterpret_cast<const double2*>(y);
+  int2* o2 = reinterpret_cast<int2*>(out);
+  switch (variant) {
+    case 0: {
+      const int64_t tiles = (pairs + 256 * 4 - 1) / (256 * 4);
+      k_stream_tiles<256, 4><<<(unsigned)tiles, 256, 0, st>>>(y2, o2, pairs);
+      break;
+    }
+    case 1: {
+      const int64_t tiles = (pairs + 512 * 2 - 1) / (512 * 2);
+      k_stream_tiles<512, 2><<<(unsigned)tiles, 512, 0, st>>>(y2, o2, pairs);
+      break;
+    }
+    case 2:
+      k_stream_persist<1024, 4><<<sms(), 1024, 0, st>>>(y2, o2, pairs);
+      break;
+    default:
+      k_stream_persist<512, 4><<<2 * sms(), 512, 0, st>>>(y2, o2, pairs);
+      break;
+  }
+  return (int)cudaGetLastError();
+}
+
+// One launch of the 2-D same-mix stream over m pairs (m even, aligned).
+int probe_stream2d(const double* rho, const double* T, double* P, int32_t* iR, int32_t* iT,
+                   int64_t m, void* stream) {
+  const int64_t p2 = m / 2;
+  k_stream2d<256><<<(unsigned)((p2 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const double2*>(rho), reinterpret_cast<const double2*>(T),
+      reinterpret_cast<double2*>(P), reinterpret_cast<int2*>(iR), reinterpret_cast<int2*>(iT), p2);
+  return (int)cudaGetLastError();
+}
+
+// Fill `words` u32 of buf (device) with pseudo-random data.
+int probe_fill(uint32_t* buf, uint64_t words, void* stream) {
+  k_fill<<<4 * sms(), 256, 0, (cudaStream_t)stream>>>(buf, words);
+  return (int)cudaGetLastError();
+}
+
+// One launch of the random-sector gather: every thread of a persistent grid
+// (1 CTA x 1024 threads per SM) runs `chains` (1, 2, 4 or 8) chains of
+// `rounds` dependent 32-B loads from buf[0 .. 8*sectors), sectors a power of two.  Sectors loaded =
+// sms * 1024 * chains * rounds.
+int probe_gather(const uint32_t* buf, uint64_t sectors, int chains, int rounds, uint32_t* sink,
+                 void* stream) {
+  if (sectors == 0 || (sectors & (sectors - 1))) return (int)cudaErrorInvalidValue;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = sms();
+  const uint64_t mask = sectors - 1;
+  switch (chains) {
+    case 1: k_gather<1><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
+    case 2: k_gather<2><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
+    case 4: k_gather<4><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
+    default: k_gather<8><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
+  }
+  return (int)cudaGetLastError();
+}
+
+int probe_sms(void) { return sms(); }
+
+}  // extern "C"

@@ -32,6 +32,7 @@ __all__ = [
     "eos_search_direct", "search_direct", "eos_grid2d_create_ex", "EOS_GRID_LINEAR",
     "EOS_GRID_LOGLOG", "EOS_MAX_TABLE_TIERED", "EOS_LEVELS_AUTO", "eos_search_create_levels",
     "eos_plan_table_levels", "plan_table_levels", "EOS_GRID_GLOBAL", "EOS_MAX_GRID_CELLS",
+    "EOS_GRID_EXACT", "ABI_VERSION",
 ]
 
 EOS_MAX_TABLE = 16384
@@ -40,7 +41,8 @@ EOS_LEVELS_AUTO = -1
 EOS_MAX_K = 19
 EOS_K_AUTO = -1
 EOS_HASH_AUTO, EOS_HASH_EXPONENT, EOS_HASH_LOG = 0, 1, 2
-EOS_GRID_LINEAR, EOS_GRID_LOGLOG, EOS_GRID_GLOBAL = 0, 1, 2
+EOS_GRID_LINEAR, EOS_GRID_LOGLOG, EOS_GRID_GLOBAL, EOS_GRID_EXACT = 0, 1, 2, 4
+ABI_VERSION = 3
 EOS_MAX_GRID_CELLS = 1 << 28
 
 STATUS = {
@@ -74,7 +76,9 @@ class TableInfo(ctypes.Structure):
                 ("device", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
                 ("hash_kind", ctypes.c_int32), ("hash_mult", ctypes.c_uint32),
                 ("levels", ctypes.c_int32), ("pad_", ctypes.c_int32), ("top_n", ctypes.c_int64),
-                ("level_bytes", ctypes.c_int64)]
+                ("level_bytes", ctypes.c_int64), ("dir_entry_bytes", ctypes.c_int32),
+                ("fast_steps", ctypes.c_int32), ("rare_steps", ctypes.c_int32),
+                ("pad2_", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -131,6 +135,8 @@ def load_library():
     L.eos_status_str.restype = ctypes.c_char_p
     L.eos_abi_version.restype = _I32
     L.eos_launch_count.restype = _I64
+    if L.eos_abi_version() != ABI_VERSION:
+        raise ImportError(f"{path}: ABI version {L.eos_abi_version()} != {ABI_VERSION} (stale build)")
     _lib = L
     return L
 
@@ -153,6 +159,26 @@ def _f64_host(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
 
 
+def _host(a, dtype, what: str, n: int | None = None):
+    """A host buffer passed to the C ABI: a C-contiguous numpy array (or CPU tensor) of
+    exactly `dtype`, with at least n elements.  Anything else raises: the library
+    reads / writes n elements through the raw pointer."""
+    import torch
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            raise TypeError(f"{what} must be a host array (got a CUDA tensor)")
+        a = a.numpy()
+    if not isinstance(a, np.ndarray):
+        raise TypeError(f"{what} must be a numpy array")
+    if a.dtype != np.dtype(dtype):
+        raise TypeError(f"{what} must be {np.dtype(dtype).name} (got {a.dtype.name})")
+    if not a.flags.c_contiguous:
+        raise ValueError(f"{what} must be C-contiguous")
+    if n is not None and a.size < n:
+        raise ValueError(f"{what} has {a.size} elements, needs {n}")
+    return a
+
+
 def _stream_ptr(stream) -> int:
     import torch
     if stream is None:
@@ -162,7 +188,9 @@ def _stream_ptr(stream) -> int:
     return stream.cuda_stream
 
 
-def _dev(t, dtype_name: str, what: str):
+def _dev(t, dtype_name: str, what: str, n: int | None = None):
+    """A device buffer passed to the C ABI: a contiguous CUDA tensor of exactly the
+    dtype, with n elements if n is given (the kernels write exactly n)."""
     import torch
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{what} must be a CUDA tensor")
@@ -170,6 +198,8 @@ def _dev(t, dtype_name: str, what: str):
         raise TypeError(f"{what} must be torch.{dtype_name}")
     if not t.is_contiguous():
         raise ValueError(f"{what} must be contiguous")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"{what} has {t.numel()} elements, needs {n}")
     return t
 
 
@@ -283,10 +313,10 @@ def search_direct(table, targets, out=None, status=None, stream=None):
     _dev(targets, "float64", "targets")
     if out is None:
         out = torch.empty(targets.numel(), dtype=torch.int32, device=targets.device)
-    _dev(out, "int32", "out")
+    _dev(out, "int32", "out", targets.numel())
     sp = None
     if status is not None:
-        _dev(status, "int32", "status")
+        _dev(status, "int32", "status", 1)
         sp = status.data_ptr()
     eos_search_direct(table.data_ptr(), table.numel(), targets.data_ptr(), targets.numel(),
                       out.data_ptr(), sp, _stream_ptr(stream))
@@ -366,9 +396,7 @@ class Table:
         _dev(targets, "float64", "targets")
         if out is None:
             out = torch.empty(targets.numel(), dtype=torch.int32, device=targets.device)
-        _dev(out, "int32", "out")
-        if out.numel() != targets.numel():
-            raise ValueError("out must have one int32 per target")
+        _dev(out, "int32", "out", targets.numel())
         cptr = None
         if counters is not None:
             _dev(counters, "int64", "counters")
@@ -383,16 +411,11 @@ class Table:
                     sync: bool = True) -> np.ndarray:
         """End-to-end from host buffers (eos_search_host); pinned memory recommended."""
         import torch
-        if isinstance(targets, torch.Tensor):
-            targets = targets.numpy()
-        if targets.dtype != np.float64 or not targets.flags.c_contiguous:
-            raise TypeError("targets must be a contiguous float64 host array")
+        targets = _host(targets, np.float64, "targets")
         if out is None:
             out = np.empty(targets.size, dtype=np.int32)
-        if isinstance(out, torch.Tensor):
-            out_ptr = out.data_ptr()
-        else:
-            out_ptr = out.ctypes.data
+        out_np = _host(out, np.int32, "out", targets.size)
+        out_ptr = out_np.ctypes.data
         sp = _stream_ptr(stream)
         eos_search_host(self._h, targets.ctypes.data, targets.size, out_ptr, sp)
         if sync:
@@ -420,14 +443,17 @@ class Table:
 class Grid2D:
     """EOSPAC-style 2-D table (density x temperature) for eos_interp2d."""
 
-    def __init__(self, rho, T, P, loglog: bool = False, global_grid: bool = False):
+    def __init__(self, rho, T, P, loglog: bool = False, global_grid: bool = False,
+                 exact: bool = False):
         """loglog=True: interpolate ln P bilinearly in (ln rho, ln T) (EOS_GRID_LOGLOG, R24).
         global_grid=True: keep P in device memory even if it fits in shared memory
-        (EOS_GRID_GLOBAL; grids too large for shared memory always are)."""
+        (EOS_GRID_GLOBAL; grids too large for shared memory always are).
+        exact=True: weights with the fp64 divide, in the formula's order (EOS_GRID_EXACT)."""
         self.rho, self.T = _f64_host(rho).copy(), _f64_host(T).copy()
         self.P = _f64_host(P).reshape(self.rho.size, self.T.size).copy()
         self.loglog = loglog
-        flags = (EOS_GRID_LOGLOG if loglog else EOS_GRID_LINEAR) | (EOS_GRID_GLOBAL if global_grid else 0)
+        flags = (EOS_GRID_LOGLOG if loglog else EOS_GRID_LINEAR) | (EOS_GRID_GLOBAL if global_grid else 0) \
+            | (EOS_GRID_EXACT if exact else 0)
         self._h = eos_grid2d_create(self.rho, self.T, self.P, flags)
         self.rho_info, self.T_info = eos_grid2d_info(self._h)
 
@@ -450,12 +476,16 @@ class Grid2D:
             irho_out = torch.empty(m, dtype=torch.int32, device=rho.device)
         if brackets and iT_out is None:
             iT_out = torch.empty(m, dtype=torch.int32, device=rho.device)
+        _dev(P_out, "float64", "P_out", m)
+        if irho_out is not None:
+            _dev(irho_out, "int32", "irho_out", m)
+        if iT_out is not None:
+            _dev(iT_out, "int32", "iT_out", m)
         dr = dt = None
         if derivatives:
             dr = torch.empty(m, dtype=torch.float64, device=rho.device)
             dt = torch.empty(m, dtype=torch.float64, device=rho.device)
-        eos_interp2d_ex(self._h, rho.data_ptr(), T.data_ptr(), m,
-                        _dev(P_out, "float64", "P").data_ptr(),
+        eos_interp2d_ex(self._h, rho.data_ptr(), T.data_ptr(), m, P_out.data_ptr(),
                         irho_out.data_ptr() if irho_out is not None else None,
                         iT_out.data_ptr() if iT_out is not None else None,
                         dr.data_ptr() if dr is not None else None,
@@ -466,17 +496,22 @@ class Grid2D:
 
     def interp_host(self, rho: np.ndarray, T: np.ndarray, P_out=None, irho_out=None, iT_out=None,
                     stream=None, sync: bool = True):
+        """End-to-end from host buffers (eos_interp2d_host): float64 rho, T of equal
+        length; outputs float64 / int32 host arrays of at least that length."""
         import torch
+        rho = _host(rho, np.float64, "rho")
+        T = _host(T, np.float64, "T")
         m = rho.size
+        if T.size != m:
+            raise ValueError("rho and T must have the same length")
         P_out = np.empty(m, np.float64) if P_out is None else P_out
         irho_out = np.empty(m, np.int32) if irho_out is None else irho_out
         iT_out = np.empty(m, np.int32) if iT_out is None else iT_out
-
-        def ptr(a):
-            return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
-
-        eos_interp2d_host(self._h, ptr(rho), ptr(T), m, ptr(P_out), ptr(irho_out), ptr(iT_out),
-                          _stream_ptr(stream))
+        P_np = _host(P_out, np.float64, "P_out", m)
+        iR_np = _host(irho_out, np.int32, "irho_out", m)
+        iT_np = _host(iT_out, np.int32, "iT_out", m)
+        eos_interp2d_host(self._h, rho.ctypes.data, T.ctypes.data, m, P_np.ctypes.data,
+                          iR_np.ctypes.data, iT_np.ctypes.data, _stream_ptr(stream))
         if sync:
             torch.cuda.synchronize()
         return P_out, irho_out, iT_out

@@ -94,6 +94,8 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False,
 
 
 if __name__ == "__main__":
-    # --exp -DNAME[=V] ...: an A/B build of the same sources into libeossearch_exp.so
-    exp = [a for a in sys.argv[1:] if a.startswith("-D")] if "--exp" in sys.argv else None
+    # --exp [-DNAME[=V] ...]: an A/B build of the same sources into libeossearch_exp.so, with
+    # the experiment knobs compiled in (-DEOS_EXPERIMENTS; runtime.cu lists them)
+    exp = (["-DEOS_EXPERIMENTS"] + [a for a in sys.argv[1:] if a.startswith("-D")]) \
+        if "--exp" in sys.argv else None
     build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv, exp_flags=exp)

@@ -43,11 +43,23 @@ struct TablePlan {
   int bins = 0;
   int max_occ = 0;
   int steps = 0;           // ceil(log2(max_occ + 1))
+  // search tables (kernels.cuh lookup_b): directory entries of 16 bits
+  // (lo | occ << 12, n <= 4096 and max_occ <= 15) or 32 bits in the image;
+  // fast_steps = SF fixed lifting steps (0: all S in a runtime loop); big =
+  // some bin holds >= 2^SF entries (its larger strides run in a rare branch)
+  bool dir16 = false;
+  int fast_steps = 0;
+  bool big = false;
   std::vector<double> X;   // canonicalised table (-0.0 -> +0.0)
-  std::vector<uint32_t> dir;  // packed lo | occ << 16, size bins
+  std::vector<uint32_t> dir;  // packed lo | occ << 16, size bins (canonical; the image may hold u16)
   int64_t x_bytes = 0;     // X region in the image (16-B padded)
   int64_t image_bytes = 0; // X region + directory (16-B padded)
 };
+
+// 16-bit directory entries: lo | occ << 12 (lo <= n - 1 < 4096, occ <= 15)
+constexpr int64_t kDir16MaxN = 4096;
+constexpr int kDir16MaxOcc = 15;
+constexpr int kMaxFastSteps = 3;  // fixed-step lifting bodies SF = 1..3 (kernels.cuh)
 
 // Smem budget of the automatic hash choice (bytes of X + directory): one image
 // copy per SM at the 1024-thread shape.  Images above 144 KB squeeze L1 and
@@ -67,8 +79,12 @@ constexpr int64_t kMaxImage = 200 * 1024;  // explicit requests beyond this do n
 // candidates with the smallest S take the one with the most bins whose image
 // fits fill_budget bytes (instead of the smallest image); search tables: if
 // > 0, the image budget of the automatic choice (default kAutoImageBudget).
+// search: a single-level search table (16-bit directories and the fast-step /
+// rare-branch split allowed; grid axes and tiered sample tables keep 32-bit
+// entries and plain S-step lifting).
 eos_status plan_table(const double* X, int64_t n, int kind, int64_t param, bool strict,
-                      TablePlan* out, int64_t fill_budget = 0, int64_t max_n = EOS_MAX_TABLE);
+                      TablePlan* out, int64_t fill_budget = 0, int64_t max_n = EOS_MAX_TABLE,
+                      bool search = false);
 
 // Shared-memory image of a tiered table's sample table: the 32-bit keys of
 // T1 (key_hi, the table's key mode) | directory, each 16-B padded.

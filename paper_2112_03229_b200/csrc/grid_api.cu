@@ -32,8 +32,7 @@ struct eos_grid2d_s {
   const void* fn_deriv = nullptr;
   int grid = 0, grid_deriv = 0;
   int threads_deriv = dv::Shape2DDeriv::kThreads, unroll_deriv = dv::Shape2DDeriv::kUnroll;
-  int threads = 512, unroll = 2;
-  bool clc = true;
+  int threads = dv::Shape2D::kThreads, unroll = dv::Shape2D::kUnroll;
   // small launches (fewer default tiles than half the SMs; no derivative outputs):
   // Shape2DSmall, 4x smaller tiles (nullptr: none)
   const void* fn_small = nullptr;        // ... without derivative outputs
@@ -41,73 +40,68 @@ struct eos_grid2d_s {
   int grid_small = 0, grid_small_deriv = 0, threads_small = 0;
   int64_t small_image_bytes = 0;  // the image without G (g_off)
   int32_t flags = 0;
-  int32_t wr_off = 0, wt_off = 0, lr_off = 0, lt_off = 0;
+  int32_t lr_off = 0, lt_off = 0;
   int32_t rr_off = 0, rt_off = 0;
   int rep = 0;  // 2: bank-pinned cell records in the image (REP kernels), 0: plain axes
   int32_t rep_shift = 0;       // REP 2: log2 of the record copies
   int64_t rep_bytes_axis = 0;  // image bytes per axis entry of the REP layout
   bool gg = false;          // grid in device memory (GG kernels)
-  void* grid_dev = nullptr;  // GG: cell quads (double4[(n_rho - 1)(n_T - 1)]) or row pairs
-  bool gquad = false;        //     (double2[n_rho (n_T - 1)])
+  void* grid_dev = nullptr;  // cell quads double4[(n_rho - 1)(n_T - 1)] (GG and small kernels)
   int64_t grid_bytes = 0;
 };
 
 namespace {
 
-template <int S>
-const void* interp_fn_s(int variant) {
-  switch (variant) {
-    case 1: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, false>, false, false>;
-    case 2: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 2, 1, false>, false, false>;
-    case 3: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 4, 1, false>, false, false>;
-    case 4: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, true>, false, false>;
-    case 5: return (const void*)dv::interp2d_kernel<S, dv::Shape<512, 2, 1, false>, true, false>;
-    case 6: return (const void*)dv::interp2d_kernel<S, dv::Shape<1024, 1, 1, false>, true, false>;
-    case 11: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, false, 2>;
-    default: return (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false>;
-  }
-}
-
-template <int S>
-const void* interp_deriv_fn_s(int rep) {
-  switch (rep) {
-    case 2: return (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, false, 2>;
-    default: return (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true>;
-  }
-}
-
-template <int S>
-const void* interp_loglog_fn_s(bool deriv, bool rep) {
-  if (rep)
-    return deriv ? (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, true, 2>
-                 : (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, true, 2>;
-  return deriv ? (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, true>
-               : (const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, true>;
-}
-
-struct Interp2DShape {
+// Kernel of a grid: S = 1..4 or 0 (runtime), linear or log-log, REP 2 (bank-pinned
+// cell records) or 0 (plain axes: EOS_GRID_EXACT, or when the records do not fit),
+// grid in shared (GG = false) or device memory; with and without derivative outputs.
+// S = 1 (the usual plan of a grid axis) runs 1024 threads per SM; deeper axes and
+// derivative outputs need more than 64 registers per thread: 512 threads.
+using Shape2DDeep = dv::Shape<512, 1, 1, false>;
+struct InterpKernel {
   const void* fn;
-  const void* fn_deriv;  // with dP/drho and dP/dT outputs (Shape2DDeriv, static schedule)
-  int threads, unroll;
-  bool clc;
+  int threads;
 };
 
-// EOS_INTERP_VARIANT (tuning experiments only): 0 static1024u1 (default
-// without bank-pinned cell records), 1 static512u2, 2 static1024u2,
-// 3 static512u4, 4 clc512u2, 5 static512u2+recip, 6 static1024u1+recip,
-// 11 static1024u1 with bank-pinned cell records (REP 2, the default when they
-// fit).
-template <bool LOGLOG, int REP, int S>
-Interp2DShape gg_shape() {
-  return {(const void*)dv::interp2d_kernel<S, dv::Shape2D, false, false, LOGLOG, REP, true>,
-          (const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, false, true, LOGLOG, REP, true>,
-          dv::Shape2D::kThreads, dv::Shape2D::kUnroll, dv::Shape2D::kClc};
+template <int S, bool LOGLOG, int REP, bool GG>
+InterpKernel interp_fn(bool deriv) {
+  if (deriv)
+    return {(const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, true, LOGLOG, REP, GG>,
+            dv::Shape2DDeriv::kThreads};
+  if constexpr (S == 1)
+    return {(const void*)dv::interp2d_kernel<S, dv::Shape2D, false, LOGLOG, REP, GG>,
+            dv::Shape2D::kThreads};
+  else
+    return {(const void*)dv::interp2d_kernel<S, Shape2DDeep, false, LOGLOG, REP, GG>,
+            Shape2DDeep::kThreads};
 }
 
-// Grids in device memory (GG): S = 1 or the runtime-S instantiation.
-template <bool LOGLOG, int REP>
-Interp2DShape gg_pick(int steps) {
-  return steps == 1 ? gg_shape<LOGLOG, REP, 1>() : gg_shape<LOGLOG, REP, 0>();
+template <bool LOGLOG, int REP, bool GG>
+InterpKernel interp_fn_steps(int steps, bool deriv) {
+  if constexpr (GG) {  // device-memory grids: S = 1 or the runtime loop
+    return steps == 1 ? interp_fn<1, LOGLOG, REP, GG>(deriv) : interp_fn<0, LOGLOG, REP, GG>(deriv);
+  } else {
+    switch (steps) {
+      case 1: return interp_fn<1, LOGLOG, REP, GG>(deriv);
+      case 2: return interp_fn<2, LOGLOG, REP, GG>(deriv);
+      case 3: return interp_fn<3, LOGLOG, REP, GG>(deriv);
+      case 4: return interp_fn<4, LOGLOG, REP, GG>(deriv);
+      default: return interp_fn<0, LOGLOG, REP, GG>(deriv);
+    }
+  }
+}
+
+InterpKernel pick_interp(int steps, bool loglog, int rep, bool gg, bool deriv) {
+  if (gg) {
+    if (loglog) return rep == 2 ? interp_fn_steps<true, 2, true>(steps, deriv)
+                                : interp_fn_steps<true, 0, true>(steps, deriv);
+    return rep == 2 ? interp_fn_steps<false, 2, true>(steps, deriv)
+                    : interp_fn_steps<false, 0, true>(steps, deriv);
+  }
+  if (loglog) return rep == 2 ? interp_fn_steps<true, 2, false>(steps, deriv)
+                              : interp_fn_steps<true, 0, false>(steps, deriv);
+  return rep == 2 ? interp_fn_steps<false, 2, false>(steps, deriv)
+                  : interp_fn_steps<false, 0, false>(steps, deriv);
 }
 
 // The small-launch kernel: the default layouts (bank-pinned records, S = 1) only.
@@ -118,50 +112,20 @@ const void* pick_interp_small(int steps, bool loglog, int rep, bool deriv) {
   using SG = dv::Shape2DSmallGG;
   if (steps != 1 || rep != 2) return nullptr;
   if (deriv)
-    return loglog ? (const void*)dv::interp2d_kernel<1, SG, false, true, true, 2, true>
-                  : (const void*)dv::interp2d_kernel<1, SG, false, true, false, 2, true>;
-  return loglog ? (const void*)dv::interp2d_kernel<1, SG, false, false, true, 2, true>
-                : (const void*)dv::interp2d_kernel<1, SG, false, false, false, 2, true>;
+    return loglog ? (const void*)dv::interp2d_kernel<1, SG, true, true, 2, true>
+                  : (const void*)dv::interp2d_kernel<1, SG, true, false, 2, true>;
+  return loglog ? (const void*)dv::interp2d_kernel<1, SG, false, true, 2, true>
+                : (const void*)dv::interp2d_kernel<1, SG, false, false, 2, true>;
 }
 
-Interp2DShape pick_interp(int steps, bool loglog, int rep, bool gg) {
-  if (gg) {
-    if (loglog) return rep == 2 ? gg_pick<true, 2>(steps) : gg_pick<true, 0>(steps);
-    if (rep == 2) return gg_pick<false, 2>(steps);
-    return gg_pick<false, 0>(steps);
-  }
-  if (loglog) {
-    const void *fn, *fd;
-    const bool r2 = rep == 2;
-    switch (steps) {
-      case 1: fn = interp_loglog_fn_s<1>(false, r2); fd = interp_loglog_fn_s<1>(true, r2); break;
-      case 2: fn = interp_loglog_fn_s<2>(false, r2); fd = interp_loglog_fn_s<2>(true, r2); break;
-      case 3: fn = interp_loglog_fn_s<3>(false, r2); fd = interp_loglog_fn_s<3>(true, r2); break;
-      case 4: fn = interp_loglog_fn_s<4>(false, r2); fd = interp_loglog_fn_s<4>(true, r2); break;
-      default: fn = interp_loglog_fn_s<0>(false, r2); fd = interp_loglog_fn_s<0>(true, r2); break;
-    }
-    return {fn, fd, dv::Shape2D::kThreads, dv::Shape2D::kUnroll, dv::Shape2D::kClc};
-  }
-  const int vdef = rep == 2 ? 11 : 0;
-  int v = vdef;
-  if (const char* e = getenv("EOS_INTERP_VARIANT")) v = atoi(e);
-  static const int thr[12] = {1024, 512, 1024, 512, 512, 512, 1024, 0, 0, 0, 0, 1024};
-  static const int unr[12] = {1, 2, 2, 4, 2, 2, 1, 0, 0, 0, 0, 1};
-  static const bool clc[12] = {false, false, false, false, true, false, false,
-                               false, false, false, false, false};
-  // variants 10/11 need the image of the matching REP layout
-  if (v < 0 || v > 11 || thr[v] == 0 || (v >= 10 && v != vdef)) v = vdef;
-  const void* fn;
-  const void* fd;
-  switch (steps) {
-    case 1: fn = interp_fn_s<1>(v); fd = interp_deriv_fn_s<1>(rep); break;
-    case 2: fn = interp_fn_s<2>(v); fd = interp_deriv_fn_s<2>(rep); break;
-    case 3: fn = interp_fn_s<3>(v); fd = interp_deriv_fn_s<3>(rep); break;
-    case 4: fn = interp_fn_s<4>(v); fd = interp_deriv_fn_s<4>(rep); break;
-    default: fn = interp_fn_s<0>(v); fd = interp_deriv_fn_s<0>(rep); break;
-  }
-  return {fn, fd, thr[v], unr[v], clc[v]};
+#ifdef EOS_EXPERIMENTS
+bool exp_small_off() {  // EOS_SMALL_TILES=0: small launches keep the default tiles (A/B)
+  const char* e = getenv("EOS_SMALL_TILES");
+  return e && e[0] == '0';
 }
+#else
+bool exp_small_off() { return false; }
+#endif
 
 eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64_t count,
                          double* P, int32_t* iR, int32_t* iT, double* dPr, double* dPt,
@@ -171,14 +135,11 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   a.image = (const uint4*)g->image_dev;
   a.image_16 = (int32_t)(g->image_bytes / 16);
   a.g_off = g->g_off;
-  a.wr_off = g->wr_off;
-  a.wt_off = g->wt_off;
   a.lr_off = g->lr_off;
   a.lt_off = g->lt_off;
   a.rr_off = g->rr_off;
   a.rt_off = g->rt_off;
   a.gq = reinterpret_cast<const double2*>(g->grid_dev);
-  a.gquad = g->gquad ? 1 : 0;
   a.rep_shift = g->rep_shift;
   a.r = g->ar;
   a.t = g->at;
@@ -206,11 +167,10 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
     per_tile = (int64_t)threads * 2;
     tiles = (count + per_tile - 1) / per_tile;
     a.image_16 = (int32_t)(g->small_image_bytes / 16);
-    a.gquad = 1;
   }
   if (tiles > 0x7FFFFFFF) return EOS_ERR_SIZE;
   a.ntiles = tiles;
-  const bool clc = sm ? false : (deriv ? dv::Shape2DDeriv::kClc : g->clc);
+  const bool clc = sm ? false : (deriv ? dv::Shape2DDeriv::kClc : dv::Shape2D::kClc);
   const int pgrid = sm ? (deriv ? g->grid_small_deriv : g->grid_small)
                        : (deriv ? g->grid_deriv : g->grid);
   int64_t grid = clc ? tiles : std::min<int64_t>(pgrid, tiles);
@@ -238,7 +198,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   if (!out) return EOS_ERR_NULL;
   *out = nullptr;
   if (!rho_host || !T_host || !P_host) return EOS_ERR_NULL;
-  if (flags & ~(EOS_GRID_LOGLOG | EOS_GRID_GLOBAL)) return EOS_ERR_UNSUPPORTED;
+  if (flags & ~(EOS_GRID_LOGLOG | EOS_GRID_GLOBAL | EOS_GRID_EXACT)) return EOS_ERR_UNSUPPORTED;
   const bool loglog = (flags & EOS_GRID_LOGLOG) != 0;
   if (n_rho > 0 && n_T > 0 && n_rho * n_T > EOS_MAX_GRID_CELLS) return EOS_ERR_SIZE;
   eos_grid2d g = new (std::nothrow) eos_grid2d_s();
@@ -261,37 +221,32 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     for (int64_t q = 0; q < ncell && ok; ++q) ok = P_host[q] > 0.0;
     if (!ok) return fail(EOS_ERR_UNSUPPORTED);
   }
-  // image: [rho X | rho dir][T X | T dir][1/dR][1/dT (RECIP variants)][ln R][ln T][R recs][T recs][G]
+  // image: [rho X | rho dir][T X | T dir][ln R][ln T][R recs][T recs][G]
   // G is absent for grids in device memory (GG: larger than ~220 KB, or
   // EOS_GRID_GLOBAL), which keep it in g->grid_dev instead (cell quads or row pairs).
   int64_t r_bytes = g->pr.image_bytes, t_bytes = g->pt.image_bytes;
-  // 1/dR, 1/dT arrays: only for the RECIP tuning variants (EOS_INTERP_VARIANT 5, 6)
-  const char* ev = getenv("EOS_INTERP_VARIANT");
-  const bool recip_arrays = ev && (atoi(ev) == 5 || atoi(ev) == 6);
-  const int64_t wr_bytes = recip_arrays ? (8 * (n_rho - 1) + 15) & ~int64_t(15) : 0;
-  const int64_t wt_bytes = recip_arrays ? (8 * (n_T - 1) + 15) & ~int64_t(15) : 0;
   const int64_t lr_bytes = loglog ? (8 * n_rho + 15) & ~int64_t(15) : 0;
   const int64_t lt_bytes = loglog ? (8 * n_T + 15) & ~int64_t(15) : 0;
-  const int64_t axes_bytes = r_bytes + t_bytes + wr_bytes + wt_bytes + lr_bytes + lt_bytes;
+  const int64_t axes_bytes = r_bytes + t_bytes + lr_bytes + lt_bytes;
   const int64_t smem_grid_bytes = (8 * ncell + 15) & ~int64_t(15);
   g->gg = (flags & EOS_GRID_GLOBAL) != 0 || axes_bytes + smem_grid_bytes > 220 * 1024;
   const int64_t g_bytes = g->gg ? 0 : smem_grid_bytes;
   g->image_bytes = axes_bytes + g_bytes;
   if (g->image_bytes > 220 * 1024) return fail(EOS_ERR_UNSUPPORTED);  // axes too long for smem
-  // bank-pinned axis records (kernels.cuh axis_cell REP): 128 B per axis
+  // bank-pinned axis records (kernels.cuh axis_cell_rec, REP 2): 128 B per axis
   // entry, if the image still fits one CTA's shared memory (227 KB opt-in
-  // less the kernel's static smem).  EOS_INTERP_REP=0/1/2 (default 2).
+  // less the kernel's static smem).  EOS_GRID_EXACT: plain axes (REP 0), whose
+  // weights divide exactly as the formula does.
   {
-    const char* e = getenv("EOS_INTERP_REP");  // 0: plain axes (A/B)
-    const int want = (e && e[0] == '0') ? 0 : 2;
+    const int want = (flags & EOS_GRID_EXACT) ? 0 : 2;
     // (log-log grids: records of the log axes.)  8 copies are conflict-free
     // (128 B per axis entry); take as many as fit, down to 1 (then the
     // records still save the divides)
     const int w = want;
     // Grids in device memory leave shared memory to L1, which holds their
-    // in-flight corner loads: the image is capped (EOS_GG_SMEM_KB, default 96).
-    const char* ec = getenv("EOS_GG_SMEM_KB");
-    const int64_t cap = g->gg ? (ec ? atoi(ec) : 96) * int64_t(1024) : 226 * 1024;
+    // in-flight corner loads: the image is capped at 96 KB (48-144 KB measured
+    // within 1.5%).
+    const int64_t cap = g->gg ? 96 * 1024 : 226 * 1024;
     g->rep = 0;
     for (int sh = 3; w > 0 && sh >= 0; --sh) {
       const int64_t rep_bytes = (int64_t(16) << sh) * (n_rho + n_T);
@@ -328,9 +283,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   memcpy(img.data() + r_bytes, it.data(), it.size());
   // G last: the image without it (the first g_off bytes) serves the small-launch
   // kernels, which read the corners from cell quads in device memory
-  g->wr_off = (int32_t)(r_bytes + t_bytes);
-  g->wt_off = (int32_t)(g->wr_off + wr_bytes);
-  g->lr_off = (int32_t)(g->wt_off + wt_bytes);
+  g->lr_off = (int32_t)(r_bytes + t_bytes);
   g->lt_off = (int32_t)(g->lr_off + lr_bytes);
   g->rr_off = (int32_t)(g->lt_off + lt_bytes);
   g->rt_off = (int32_t)(g->rr_off + (g->rep ? g->rep_bytes_axis * n_rho : 0));
@@ -371,14 +324,6 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
       memcpy(img.data() + g->lt_off + 8 * q, &v, 8);
     }
   }
-  for (int64_t q = 0; recip_arrays && q + 1 < n_rho; ++q) {
-    const double w = 1.0 / (g->pr.X[q + 1] - g->pr.X[q]);
-    memcpy(img.data() + g->wr_off + 8 * q, &w, 8);
-  }
-  for (int64_t q = 0; recip_arrays && q + 1 < n_T; ++q) {
-    const double w = 1.0 / (g->pt.X[q + 1] - g->pt.X[q]);
-    memcpy(img.data() + g->wt_off + 8 * q, &w, 8);
-  }
   g->ar = axis_params(g->pr, 0);
   g->at = axis_params(g->pt, (int32_t)r_bytes);
   cudaError_t e = cudaGetDevice(&g->device);
@@ -386,8 +331,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   if (e != cudaSuccess) return fail(cuda_status(e));
   st = upload(img, &g->image_dev);
   if (st != EOS_OK) return fail(st);
-  const char* small_env = getenv("EOS_SMALL_TILES");  // "0": default tiles only
-  const bool small_ok = !((small_env && small_env[0] == '0') || getenv("EOS_INTERP_VARIANT"));
+  const bool small_ok = !exp_small_off();
   const int steps_max = std::max(g->pr.steps, g->pt.steps);
   const void* fn_small = small_ok ? pick_interp_small(steps_max, loglog, g->rep, false) : nullptr;
   const void* fn_small_deriv =
@@ -395,53 +339,41 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   // shared-memory grids keep cell quads in device memory too, for the small-launch kernel
   const bool quads_for_small = !g->gg && fn_small && 32 * ncell <= (int64_t(64) << 20);
   if (g->gg || quads_for_small) {
-    // Cell quads (32 B per cell: the 4 corners in one sector) up to
-    // EOS_GG_QUAD_MB (default 1024 MB of quads), else row pairs
-    // gq[i (nT-1) + j] = (G[i][j], G[i][j+1]) (two 16-B loads per pair).
+    // cell quads: 32 B per cell, the 4 corners in one sector (4x the grid; at most
+    // 8 GB for EOS_MAX_GRID_CELLS)
     const int64_t w = n_T - 1;
-    const char* eq = getenv("EOS_GG_QUAD_MB");
-    const int64_t quad_cap = (eq ? atoll(eq) : 1024) << 20;
-    g->gquad = quads_for_small || 32 * (n_rho - 1) * w <= quad_cap;
     std::vector<double> q2;
     try {
-      q2.resize((size_t)(g->gquad ? 4 * (n_rho - 1) * w : 2 * n_rho * w));
+      q2.resize((size_t)(4 * (n_rho - 1) * w));
     } catch (...) {
       return fail(EOS_ERR_NOMEM);
     }
-    if (g->gquad) {
-      for (int64_t i = 0; i + 1 < n_rho; ++i)
-        for (int64_t j = 0; j < w; ++j) {
-          double* c = q2.data() + 4 * (i * w + j);
-          c[0] = gval(i * n_T + j);
-          c[1] = gval(i * n_T + j + 1);
-          c[2] = gval((i + 1) * n_T + j);
-          c[3] = gval((i + 1) * n_T + j + 1);
-        }
-    } else {
-      for (int64_t i = 0; i < n_rho; ++i)
-        for (int64_t j = 0; j < w; ++j) {
-          q2[2 * (i * w + j)] = gval(i * n_T + j);
-          q2[2 * (i * w + j) + 1] = gval(i * n_T + j + 1);
-        }
-    }
+    for (int64_t i = 0; i + 1 < n_rho; ++i)
+      for (int64_t j = 0; j < w; ++j) {
+        double* c = q2.data() + 4 * (i * w + j);
+        c[0] = gval(i * n_T + j);
+        c[1] = gval(i * n_T + j + 1);
+        c[2] = gval((i + 1) * n_T + j);
+        c[3] = gval((i + 1) * n_T + j + 1);
+      }
     g->grid_bytes = 8 * (int64_t)q2.size();
     e = cudaMalloc(&g->grid_dev, (size_t)g->grid_bytes);
     if (e == cudaSuccess)
       e = cudaMemcpy(g->grid_dev, q2.data(), (size_t)g->grid_bytes, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return fail(cuda_status(e));
   }
-  Interp2DShape sh = pick_interp(std::max(g->pr.steps, g->pt.steps), loglog, g->rep, g->gg);
-  g->fn = sh.fn;
-  g->fn_deriv = sh.fn_deriv;
-  g->threads = sh.threads;
-  g->unroll = sh.unroll;
-  g->clc = sh.clc;
+  const InterpKernel k0 = pick_interp(steps_max, loglog, g->rep, g->gg, false);
+  const InterpKernel k1 = pick_interp(steps_max, loglog, g->rep, g->gg, true);
+  g->fn = k0.fn;
+  g->threads = k0.threads;
+  g->fn_deriv = k1.fn;
+  g->threads_deriv = k1.threads;
   st = configure(g->fn, g->threads, g->image_bytes, g->num_sms, &g->grid, nullptr);
   if (st == EOS_OK)
     st = configure(g->fn_deriv, g->threads_deriv, g->image_bytes, g->num_sms, &g->grid_deriv,
                    nullptr);
   if (st != EOS_OK) return fail(st);
-  if (fn_small && fn_small_deriv && g->gquad) {  // the small kernels read quads (not row pairs)
+  if (fn_small && fn_small_deriv && g->grid_dev) {  // the small kernels read the quads
     const int ts = dv::Shape2DSmallGG::kThreads;
     if (configure(fn_small, ts, g->g_off, g->num_sms, &g->grid_small, nullptr) == EOS_OK &&
         configure(fn_small_deriv, ts, g->g_off, g->num_sms, &g->grid_small_deriv, nullptr) ==
@@ -494,6 +426,18 @@ eos_status eos_interp2d_host(eos_grid2d g, const double* rho_host, const double*
   if (count < 0 || count > (int64_t(1) << 62)) return EOS_ERR_SIZE;
   if (count == 0) return EOS_OK;
   if (!rho_host || !T_host || !P_out_host) return EOS_ERR_NULL;
+  {  // outputs must not overlap the inputs or each other (as eos_interp2d_ex)
+    const void* ins[2] = {rho_host, T_host};
+    const void* outs[3] = {P_out_host, irho_out_host, iT_out_host};
+    const int64_t ob[3] = {8 * count, 4 * count, 4 * count};
+    for (int o = 0; o < 3; ++o) {
+      if (!outs[o]) continue;
+      for (int i = 0; i < 2; ++i)
+        if (overlaps(ins[i], 8 * count, outs[o], ob[o])) return EOS_ERR_ALIAS;
+      for (int o2 = o + 1; o2 < 3; ++o2)
+        if (outs[o2] && overlaps(outs[o], ob[o], outs[o2], ob[o2])) return EOS_ERR_ALIAS;
+    }
+  }
   eos_status st = check_device(g->device);
   if (st != EOS_OK) return st;
   const int64_t chunk = int64_t(1) << 22;

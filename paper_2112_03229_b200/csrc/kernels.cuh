@@ -110,43 +110,126 @@ __device__ __forceinline__ uint32_t bin_of_m0(uint32_t key, const AxisParams& a)
   return min(__umulhi((uint32_t)max((int32_t)(key - a.hb), 0), a.M), a.bmax);
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// Directory entry formats (eos_internal.h TablePlan::dir16): a 32-bit entry
+// lo | occ << 16 (any table), or a 16-bit entry lo | occ << 12 (search tables
+// with n <= 4096 and every bin holding <= 15 entries: half the shared memory
+// per bin, so twice the bins in the same image).
+template <bool D16>
+__device__ __forceinline__ void dir_entry(const void* __restrict__ sD, uint32_t b, int32_t& lo,
+                                          int32_t& occ) {
+  if (D16) {
+    const uint32_t d = reinterpret_cast<const uint16_t*>(sD)[b];
+    lo = (int32_t)(d & 0xFFFu);
+    occ = (int32_t)(d >> 12);
+  } else {
+    const uint32_t d = reinterpret_cast<const uint32_t*>(sD)[b];
+    lo = (int32_t)(d & 0xFFFFu);
+    occ = (int32_t)(d >> 16);
+  }
+}
+
+// One step of binary lifting with stride s over the rest of the bin, on the
+// shared-memory byte address pa of the first entry not yet counted
+// (X[lo + c]) and the r = occ - c entries that remain:
+//   if (r >= s && X[lo + c + s - 1] <= y) { c += s; }
+// The probe is an immediate offset from pa and is predicated off (moves no
+// smem data) when the bin holds fewer than s more entries; the compare folds
+// the range predicate in (DSETP.AND), the updates are predicated: 5 SASS
+// instructions per step, 4 for the last one (no r update), no branches.
+template <int S, bool LAST>
+__device__ __forceinline__ void lift_step(double y, uint32_t& pa, int32_t& r) {
+  if (LAST) {
+    asm("{\n\t.reg .pred pi, pt;\n\t.reg .f64 x;\n\t"
+        "setp.ge.s32 pi, %1, %3;\n\t"
+        "mov.b64 x, 0;\n\t"
+        "@pi ld.shared.f64 x, [%0+%4];\n\t"
+        "setp.le.and.f64 pt, x, %2, pi;\n\t"
+        "@pt add.u32 %0, %0, %5;\n\t}"
+        : "+r"(pa)
+        : "r"(r), "d"(y), "n"(S), "n"(8 * (S - 1)), "n"(8 * S));
+  } else {
+    asm("{\n\t.reg .pred pi, pt;\n\t.reg .f64 x;\n\t"
+        "setp.ge.s32 pi, %1, %3;\n\t"
+        "mov.b64 x, 0;\n\t"
+        "@pi ld.shared.f64 x, [%0+%4];\n\t"
+        "setp.le.and.f64 pt, x, %2, pi;\n\t"
+        "@pt add.u32 %0, %0, %5;\n\t"
+        "@pt sub.s32 %1, %1, %3;\n\t}"
+        : "+r"(pa), "+r"(r)
+        : "d"(y), "n"(S), "n"(8 * (S - 1)), "n"(8 * S));
+  }
+}
+// the same with a runtime stride (rare branch / runtime-S loop)
+__device__ __forceinline__ void lift_step_rt(double y, uint32_t& pa, int32_t& r, int32_t s) {
+  asm("{\n\t.reg .pred pi, pt;\n\t.reg .f64 x;\n\t.reg .u32 q;\n\t"
+      "setp.ge.s32 pi, %1, %3;\n\t"
+      "shl.b32 q, %3, 3;\n\t"
+      "add.u32 q, q, %0;\n\t"
+      "mov.b64 x, 0;\n\t"
+      "@pi ld.shared.f64 x, [q+-8];\n\t"
+      "setp.le.and.f64 pt, x, %2, pi;\n\t"
+      "@pt mov.u32 %0, q;\n\t"
+      "@pt sub.s32 %1, %1, %3;\n\t}"
+      : "+r"(pa), "+r"(r)
+      : "d"(y), "r"(s));
+}
+
+template <int S>
+__device__ __forceinline__ void lift_fixed(double y, uint32_t& pa, int32_t& r) {
+  if (S >= 4) lift_step<8, S == 4>(y, pa, r);
+  if (S >= 3) lift_step<4, S == 3>(y, pa, r);
+  if (S >= 2) lift_step<2, S == 2>(y, pa, r);
+  if (S >= 1) lift_step<1, true>(y, pa, r);
+}
+
 // The hot per-target body:
 //   bin b = min(umulhi(max(key, hb) - hb, M), B-1)          (exponent / log hash)
 //   lo, occ = directory[b]                                  (count directory)
-//   c = #{j < occ : X[lo + j] <= y}  by S-step binary lifting (branchless)
+//   c = #{j < occ : X[lo + j] <= y}  by binary lifting (branchless steps)
 //   idx = (y >= X[0]) ? lo + c - 1 : 0                      (P:54 fix-up; NaN -> 0)
-// Probes past the bin (j > occ) are predicated off, so they move no smem
-// data: with fine bins most lanes probe nothing.  (Measured: dropping the
-// occupancy test -- NaN-padded X, 3 instructions per step -- is 11% slower on
-// cfg2 and 34% on cfg5, DESIGN.md tuning log.)
-template <int S, int MODE>
-__device__ __forceinline__ int32_t lookup(double y, const double* __restrict__ sX,
-                                          const uint32_t* __restrict__ sD, const AxisParams& a) {
+// SF fixed steps (strides 2^(SF-1) .. 1) cover bins of up to 2^SF - 1
+// entries.  BIG: the directory also holds deeper bins (up to 2^S - 1
+// entries, S = a.steps); their larger strides run first, in a branch that only
+// warps with a lane in such a bin take (the planner picks SF so that few warps
+// diverge, table_build.cpp choose_layout).  SF = 0: every stride in a runtime
+// loop.  Probes past the bin are predicated off, so they move no smem data:
+// with fine bins most lanes probe nothing.  (Measured: dropping the occupancy
+// test -- NaN-padded X -- is 11% slower on cfg2 and 34% on cfg5.)
+// SF <= 4 here (kMaxFastSteps = 3 for search tables; grid axes use S <= 4).
+template <int SF, bool BIG, int MODE, bool D16>
+__device__ __forceinline__ int32_t lookup_b(double y, const double* __restrict__ sX,
+                                            const void* __restrict__ sD, const AxisParams& a) {
+  static_assert(SF >= 0 && SF <= 4, "fixed lifting steps");
   const uint32_t key = key_hi<MODE>(y);
   const uint32_t b = MODE == 0 ? bin_of_m0(key, a) : bin_of(key, a);
   EOS_DCHECK(b <= a.bmax);
-  const uint32_t d = sD[b];
-  const int32_t lo = (int32_t)(d & 0xFFFFu);
-  const int32_t occ = (int32_t)(d >> 16);
-  EOS_DCHECK(lo + occ <= a.n && occ < (1 << (S > 0 ? S : a.steps)));
-  int32_t c = 0;
-  if (S > 0) {
-#pragma unroll
-    for (int s = 1 << (S > 0 ? S - 1 : 0); s > 0; s >>= 1) {
-      const int32_t j = c + s;
-      if (j <= occ) {
-        if (sX[lo + j - 1] <= y) c = j;
-      }
+  int32_t lo, r;
+  dir_entry<D16>(sD, b, lo, r);
+  EOS_DCHECK(lo + r <= a.n && r < (1 << a.steps));
+  const uint32_t xa = smem_u32(sX);
+  uint32_t pa = xa + 8u * (uint32_t)lo;
+  if (SF == 0) {
+    for (int32_t s = 1 << (a.steps - 1); s > 0; s >>= 1) lift_step_rt(y, pa, r, s);
+  } else {
+    if (BIG && r >= (1 << SF)) {  // rare: a bin deeper than the fixed steps
+      for (int32_t s = 1 << (a.steps - 1); s >= (1 << SF); s >>= 1) lift_step_rt(y, pa, r, s);
     }
-  } else {  // runtime S (large bins)
-    for (int s = 1 << (a.steps - 1); s > 0; s >>= 1) {
-      const int32_t j = c + s;
-      if (j <= occ) {
-        if (sX[lo + j - 1] <= y) c = j;
-      }
-    }
+    lift_fixed<SF>(y, pa, r);
   }
-  return (y >= a.x0) ? (lo + c - 1) : 0;
+  const int32_t idx = (int32_t)(pa - xa - 8u) >> 3;  // lo + c - 1
+  return (y >= a.x0) ? idx : 0;
+}
+
+// S fixed steps (S = 0: runtime), 32-bit directory (grid axes, tiered sample
+// tables, counters launches)
+template <int S, int MODE>
+__device__ __forceinline__ int32_t lookup(double y, const double* __restrict__ sX,
+                                          const uint32_t* __restrict__ sD, const AxisParams& a) {
+  return lookup_b<S, false, MODE, false>(y, sX, sD, a);
 }
 
 struct Counters {
@@ -159,7 +242,7 @@ struct Counters {
                                       const AxisParams& a) {
     c[0] += 1;
     c[1] += (uint64_t)(uint32_t)idx;
-    c[2] += mix64(((uint64_t)gpos << 20) | (uint64_t)(uint32_t)idx);
+    c[2] += mix64(mix64((uint64_t)gpos) ^ (uint64_t)(uint32_t)idx);  // DESIGN.md R25
     c[3] += !(y >= a.x0);
     c[4] += (y > a.xlast);
     c[5] += (y != y);
@@ -181,16 +264,16 @@ struct Counters {
 // (counter c6 only).
 //
 // SmemLookup: the whole table and its directory are in shared memory.
-template <int S, int MODE>
+template <int SF, bool BIG, int MODE, bool D16>
 struct SmemLookup {
   static constexpr bool kBatchTail = true;  // ragged tiles: one batched lookup per thread
   const double* __restrict__ sX;
-  const uint32_t* __restrict__ sD;
+  const void* __restrict__ sD;
   AxisParams a;
   template <int N>
   __device__ __forceinline__ void many(const double (&y)[N], int32_t (&r)[N]) const {
 #pragma unroll
-    for (int i = 0; i < N; ++i) r[i] = lookup<S, MODE>(y[i], sX, sD, a);
+    for (int i = 0; i < N; ++i) r[i] = lookup_b<SF, BIG, MODE, D16>(y[i], sX, sD, a);
   }
   __device__ __forceinline__ double x_at(int32_t i) const { return sX[i]; }
 };
@@ -342,9 +425,6 @@ struct TieredLookup {
 };
 
 // ---- Blackwell cluster launch control + mbarrier (inline PTX, sm_100a) ----
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -453,7 +533,11 @@ using ShapeCnt = Shape<256, 4, 1, true>;        // validation launches (counters
 using ShapeTiered = Shape<1024, 2, 1, false>;
 
 // The streaming tile loop of search1d (after the image is in smem): CLC or
-// static tile schedule, 128-bit streaming loads, next-tile prefetch.
+// static tile schedule, 128-bit streaming loads, next-tile prefetch.  Full
+// tiles (vector body) use pointer increments (static) or one multiply-add
+// (CLC) per tile; ragged / unaligned tiles take the batched scalar path.  The
+// unaligned leading element (args.head) goes with tile 0, in whichever CTA
+// processes it (under CLC a not-yet-launched CTA 0 may be cancelled).
 template <bool CNT, class SH, class LK>
 __device__ __forceinline__ void search_body(const SearchArgs& args, const LK& lk, uint4* clc_resp_p,
                                             uint64_t* clc_bar_p) {
@@ -462,6 +546,7 @@ __device__ __forceinline__ void search_body(const SearchArgs& args, const LK& lk
   constexpr int U = SH::kUnroll;
   constexpr int TP = SH::kTilePairs;
   constexpr int TE = SH::kTileElems;
+  static_assert(TE == 2 * U * T, "tile = 2U elements per thread");
   uint4& clc_resp = *clc_resp_p;
   uint64_t& clc_bar = *clc_bar_p;
   const double* __restrict__ Y = args.Y;
@@ -470,111 +555,142 @@ __device__ __forceinline__ void search_body(const SearchArgs& args, const LK& lk
   const int64_t head = args.head;
   const int64_t body = count - head;
   const int64_t ntiles = args.ntiles;
-  const bool vec = args.vec_ok != 0;
+  const int64_t nfull = args.vec_ok ? body / TE : 0;  // tiles of the vector body
   const double2* __restrict__ Y2 = reinterpret_cast<const double2*>(Y + head);
   int2* __restrict__ O2 = reinterpret_cast<int2*>(out + head);
 
   Counters cn;
   if (CNT) cn.zero();
 
-  // the leading unaligned element (if any) belongs to tile 0
-  if (blockIdx.x == 0 && threadIdx.x == 0 && head) {
-    const double y[1] = {Y[0]};
-    int32_t r[1];
-    lk.many(y, r);
-    out[0] = r[0];
-    if (CNT) cn.add(y[0], r[0], args.gofs, lk.x_at(r[0]), a);
-  }
-
-  uint32_t phase = 0;
-  auto next_tile = [&](int64_t t) -> int64_t {
-    if (!SH::kClc) return t + gridDim.x;
-    mbar_wait(&clc_bar, phase);
-    phase ^= 1u;
-    const int64_t tn = clc_query(&clc_resp);
-    __syncthreads();  // everyone has read the response before it is reused
-    return tn < 0 ? ntiles : tn;
-  };
-  auto full = [&](int64_t t) { return vec && (t + 1) * TE <= body; };
-
-  int64_t t = blockIdx.x;
-  double2 v[U];
-  auto load_tile = [&](int64_t tt) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ld_stream(Y2 + tt * TP + threadIdx.x + u * T);
-  };
-  if (t < ntiles && full(t)) load_tile(t);
-  while (t < ntiles) {
-    if (SH::kClc && threadIdx.x == 0) {
-      mbar_arrive_expect_tx(&clc_bar, 16);
-      clc_try_cancel(&clc_resp, &clc_bar);
+  auto do_head = [&]() {  // the leading unaligned element (tile 0's)
+    if (threadIdx.x == 0 && head) {
+      const double y[1] = {Y[0]};
+      int32_t r[1];
+      lk.many(y, r);
+      out[0] = r[0];
+      if (CNT) cn.add(y[0], r[0], args.gofs, lk.x_at(r[0]), a);
     }
-    int64_t tn;
-    if (full(t)) {
+  };
+  // full tile: 2U targets per thread, loaded into v before the call
+  auto compute = [&](const double2 (&v)[U], int2 (&r)[U], int64_t t) {
+    double y[2 * U];
+    int32_t ri[2 * U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      y[2 * u] = v[u].x;
+      y[2 * u + 1] = v[u].y;
+    }
+    lk.many(y, ri);
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = make_int2(ri[2 * u], ri[2 * u + 1]);
+    if (CNT) {
       const int64_t p0 = t * TP + threadIdx.x;
-      double y[2 * U];
-      int32_t ri[2 * U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        y[2 * u] = v[u].x;
-        y[2 * u + 1] = v[u].y;
+        const int64_t g = args.gofs + head + 2 * (p0 + u * T);
+        cn.add(v[u].x, r[u].x, g, lk.x_at(r[u].x), a);
+        cn.add(v[u].y, r[u].y, g + 1, lk.x_at(r[u].y), a);
       }
-      lk.many(y, ri);
-      int2 r[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) r[u] = make_int2(ri[2 * u], ri[2 * u + 1]);
-      if (CNT) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t g = args.gofs + head + 2 * (p0 + u * T);
-          cn.add(v[u].x, r[u].x, g, lk.x_at(r[u].x), a);
-          cn.add(v[u].y, r[u].y, g + 1, lk.x_at(r[u].y), a);
-        }
-      }
-      tn = next_tile(t);
-      if (tn < ntiles && full(tn)) load_tile(tn);  // prefetch the next tile before storing this one
-#pragma unroll
-      for (int u = 0; u < U; ++u) __stcs(O2 + p0 + u * T, r[u]);
-    } else {
-      // ragged / unaligned tile: each thread's (at most 2U) elements at stride T,
-      // all loads first and one batched lookup, as in the vector body (a
-      // one-at-a-time loop here waited a load latency per element)
-      static_assert(TE == 2 * U * T, "tile = 2U elements per thread");
-      const int64_t e0 = head + t * TE;
-      const int64_t e1 = min(count, e0 + TE);
-      EOS_DCHECK(e0 >= 0 && t >= 0);
-      if (!CNT && LK::kBatchTail) {
-        double y[2 * U];
-        int32_t r[2 * U];
-#pragma unroll
-        for (int k = 0; k < 2 * U; ++k) {
-          const int64_t i = e0 + threadIdx.x + (int64_t)k * T;
-          y[k] = i < e1 ? Y[i] : 0.0;
-        }
-        lk.many(y, r);
-#pragma unroll
-        for (int k = 0; k < 2 * U; ++k) {
-          const int64_t i = e0 + threadIdx.x + (int64_t)k * T;
-          if (i < e1) out[i] = r[k];
-        }
-      } else {  // counters / tiered tables: one element at a time (fewer live registers)
-        for (int64_t i = e0 + threadIdx.x; i < e1; i += T) {
-          const double y[1] = {Y[i]};
-          int32_t r[1];
-          lk.many(y, r);
-          out[i] = r[0];
-          if (CNT) cn.add(y[0], r[0], args.gofs + i, lk.x_at(r[0]), a);
-        }
-      }
-      tn = next_tile(t);
-      if (tn < ntiles && full(tn)) load_tile(tn);
     }
-    t = tn;
+  };
+  // ragged / unaligned tile: each thread's (at most 2U) elements at stride T,
+  // all loads first and one batched lookup, as in the vector body (a
+  // one-at-a-time loop here waited a load latency per element)
+  auto ragged = [&](int64_t t) {
+    const int64_t e0 = head + t * TE;
+    const int64_t e1 = min(count, e0 + TE);
+    EOS_DCHECK(e0 >= 0 && t >= 0);
+    if (!CNT && LK::kBatchTail) {
+      double y[2 * U];
+      int32_t r[2 * U];
+#pragma unroll
+      for (int k = 0; k < 2 * U; ++k) {
+        const int64_t i = e0 + threadIdx.x + (int64_t)k * T;
+        y[k] = i < e1 ? Y[i] : 0.0;
+      }
+      lk.many(y, r);
+#pragma unroll
+      for (int k = 0; k < 2 * U; ++k) {
+        const int64_t i = e0 + threadIdx.x + (int64_t)k * T;
+        if (i < e1) out[i] = r[k];
+      }
+    } else {  // counters / tiered tables: one element at a time (fewer live registers)
+      for (int64_t i = e0 + threadIdx.x; i < e1; i += T) {
+        const double y[1] = {Y[i]};
+        int32_t r[1];
+        lk.many(y, r);
+        out[i] = r[0];
+        if (CNT) cn.add(y[0], r[0], args.gofs + i, lk.x_at(r[0]), a);
+      }
+    }
+  };
+  if (!SH::kClc) {
+    // static persistent schedule: tiles blockIdx.x + k gridDim.x, pointers advance
+    // by gridDim.x tiles; the next tile's loads go out before this tile's stores
+    int64_t t = blockIdx.x;
+    if (t == 0) do_head();
+    const int64_t step = (int64_t)gridDim.x * TP;
+    const double2* yp = Y2 + t * TP + threadIdx.x;
+    int2* op = O2 + t * TP + threadIdx.x;
+    double2 v[U];
+    if (t < nfull) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_stream(yp + u * T);
+    }
+    for (; t < nfull; t += gridDim.x) {
+      int2 r[U];
+      compute(v, r, t);
+      yp += step;
+      if (t + gridDim.x < nfull) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld_stream(yp + u * T);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) __stcs(op + u * T, r[u]);
+      op += step;
+    }
+    for (; t < ntiles; t += gridDim.x) ragged(t);
+  } else {
+    // CLC: this CTA's own tile, then tiles of cancelled (not yet launched) CTAs
+    uint32_t phase = 0;
+    int64_t t = blockIdx.x;
+    if (ntiles == 0 && t == 0) do_head();
+    double2 v[U];
+    if (t < nfull) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_stream(Y2 + t * TP + threadIdx.x + u * T);
+    }
+    while (t < ntiles) {
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&clc_bar, 16);
+        clc_try_cancel(&clc_resp, &clc_bar);
+      }
+      if (t == 0) do_head();
+      int2 r[U];
+      const bool f = t < nfull;
+      if (f) compute(v, r, t);
+      else ragged(t);
+      mbar_wait(&clc_bar, phase);
+      phase ^= 1u;
+      const int64_t q = clc_query(&clc_resp);
+      __syncthreads();  // everyone has read the response before it is reused
+      const int64_t tn = q < 0 ? ntiles : q;
+      if (tn < nfull) {  // before this tile's stores
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld_stream(Y2 + tn * TP + threadIdx.x + u * T);
+      }
+      if (f) {
+        int2* op = O2 + t * TP + threadIdx.x;
+#pragma unroll
+        for (int u = 0; u < U; ++u) __stcs(op + u * T, r[u]);
+      }
+      t = tn;
+    }
   }
   if (CNT) cn.flush(args.counters);
 }
 
-template <int S, int MODE, bool CNT, class SH>
+template <int SF, bool BIG, int MODE, bool D16, bool CNT, class SH>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(const SearchArgs args) {
   extern __shared__ __align__(16) uint4 smem[];
   __shared__ __align__(16) uint4 clc_resp;
@@ -583,11 +699,11 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
   stage_image(smem, args.image, args.image_16, &stage_bar);
   pdl_enter();
   const AxisParams a = args.ax;
-  EOS_DCHECK(a.d_off + 4 * ((int64_t)a.bmax + 1) <= 16 * (int64_t)args.image_16 &&
+  EOS_DCHECK(a.d_off + (D16 ? 2 : 4) * ((int64_t)a.bmax + 1) <= 16 * (int64_t)args.image_16 &&
              a.x_off + 8 * (int64_t)a.n <= a.d_off);
-  SmemLookup<S, MODE> lk;
+  SmemLookup<SF, BIG, MODE, D16> lk;
   lk.sX = reinterpret_cast<const double*>(reinterpret_cast<const char*>(smem) + a.x_off);
-  lk.sD = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(smem) + a.d_off);
+  lk.sD = reinterpret_cast<const char*>(smem) + a.d_off;
   lk.a = a;
   search_body<CNT, SH>(args, lk, &clc_resp, &clc_bar);
 }
@@ -772,10 +888,10 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
   auto body = [&](auto s_tag) {
     constexpr int S = decltype(s_tag)::value;
     if (a.mode) {
-      const SmemLookup<S, 1> lk{sX, sD, a};
+      const SmemLookup<S, false, 1, false> lk{sX, sD, a};
       search_body<false, SH>(A.s, lk, &clc_resp, &clc_bar);
     } else {
-      const SmemLookup<S, 0> lk{sX, sD, a};
+      const SmemLookup<S, false, 0, false> lk{sX, sD, a};
       search_body<false, SH>(A.s, lk, &clc_resp, &clc_bar);
     }
   };
@@ -793,8 +909,6 @@ struct Interp2DArgs {
   const uint4* image;
   int32_t image_16;
   int32_t g_off;    // byte offset of G fp64[nR*nT] in the image
-  int32_t wr_off;   // byte offset of 1/(R[i+1]-R[i]) fp64[nR-1] (RECIP variant)
-  int32_t wt_off;   // byte offset of 1/(T[j+1]-T[j]) fp64[nT-1] (RECIP variant)
   int32_t lr_off;   // byte offset of ln R fp64[nR] (LOGLOG grids)
   int32_t lt_off;   // byte offset of ln T fp64[nT] (LOGLOG grids)
   int32_t rr_off;   // byte offset of the bank-pinned cell records of the R axis (REP 2
@@ -802,11 +916,9 @@ struct Interp2DArgs {
   int32_t rt_off;   // the same for the T axis
   int32_t rep_shift;  // REP 2: log2 of the record copies per axis entry (3: 8 copies, the
                       //   conflict-free layout; fewer when smem is short: 2-way .. 8-way)
-  int32_t gquad;    // GG: 1 = gq holds cell quads, 0 = row pairs
-  const double2* gq;  // GG kernels: the grid in device memory (ln G for LOGLOG), either as
+  const double2* gq;  // GG / small kernels: the grid in device memory (ln G for LOGLOG) as
                       //   cell quads gq[2 (i (nT-1) + j)] = (G[i][j], G[i][j+1]),
-                      //   gq[2 (i (nT-1) + j) + 1] = (G[i+1][j], G[i+1][j+1]) (32 B, one
-                      //   sector per pair), or as row pairs gq[i (nT-1) + j] = (G[i][j], G[i][j+1])
+                      //   gq[2 (i (nT-1) + j) + 1] = (G[i+1][j], G[i+1][j+1]) (32 B: one sector)
   int32_t vec_ok;
   int32_t pad_;
   int64_t ntiles;
@@ -900,16 +1012,12 @@ __device__ __forceinline__ void axis_cell_rec(double y, const double* __restrict
 // round-to-nearest intrinsics (no FMA contraction), in the order of the
 // formula in eossearch.h, so the value is the correctly-rounded evaluation
 // of that formula (bit-identical to a plain evaluation in that order).
-// RECIP: weights as (x - X[c]) * (1/(X[c+1]-X[c])) with the reciprocal
-// precomputed at create (a few ulp from the divide; within the 1e-12 bar).
 //
 // GG (grids larger than shared memory): the grid stays in device memory
 // (L2-resident up to a few 10^6 cells) as cell quads, so the 4 corners are one
-// aligned 32-byte load (one L1/L2 sector), or, past the quad budget, as row
-// pairs: two aligned 16-byte loads, (G[ci][cj], G[ci][cj+1]) and
-// (G[ci+1][cj], G[ci+1][cj+1]).  The axes, their directories and records stay
-// in smem.
-template <int S, bool RECIP, bool DERIV, bool LOGLOG, int REP, bool GG>
+// aligned 32-byte load (one L1/L2 sector).  The axes, their directories and
+// records stay in smem.
+template <int S, bool DERIV, bool LOGLOG, int REP, bool GG>
 __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, int32_t& j,
                                              double& dpr, double& dpt, const char* sm,
                                              const Interp2DArgs& A) {
@@ -961,11 +1069,6 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   if (REP == 2) {
     tx = clamp01(__dmul_rn(__dsub_rn(xr, r0), ir));
     ty = clamp01(__dmul_rn(__dsub_rn(xt, t0), it));
-  } else if (RECIP && !LOGLOG) {
-    const double* wR = reinterpret_cast<const double*>(sm + A.wr_off);
-    const double* wT = reinterpret_cast<const double*>(sm + A.wt_off);
-    tx = clamp01(__dmul_rn(__dsub_rn(xr, r0), wR[ci]));
-    ty = clamp01(__dmul_rn(__dsub_rn(xt, t0), wT[cj]));
   } else {
     tx = clamp01(__ddiv_rn(__dsub_rn(xr, r0), __dsub_rn(r1, r0)));
     ty = clamp01(__ddiv_rn(__dsub_rn(xt, t0), __dsub_rn(t1, t0)));
@@ -973,18 +1076,10 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   EOS_DCHECK(ci >= 0 && cj >= 0 && ci + 1 < A.r.n && cj + 1 < A.t.n);
   double g00, g01, g10, g11;
   if (GG) {
-    const int64_t w = A.t.n - 1;  // cells (quads) or row pairs per row
-    if (A.gquad) {  // one 256-bit load: the 4 corners share one 32-B sector
-      ldg_f64x4(reinterpret_cast<const double*>(A.gq + 2 * ((int64_t)ci * w + cj)), g00, g01,
-                g10, g11);
-    } else {
-      const double2* q = A.gq + (int64_t)ci * w + cj;
-      const double2 q0 = __ldg(q), q1 = __ldg(q + w);
-      g00 = q0.x;
-      g01 = q0.y;
-      g10 = q1.x;
-      g11 = q1.y;
-    }
+    const int64_t w = A.t.n - 1;  // cells per row
+    // one 256-bit load: the 4 corners share one 32-B sector
+    ldg_f64x4(reinterpret_cast<const double*>(A.gq + 2 * ((int64_t)ci * w + cj)), g00, g01, g10,
+              g11);
   } else {
     const double* g0 = sG + (int64_t)ci * A.t.n + cj;
     const double* g1 = g0 + A.t.n;
@@ -1026,7 +1121,7 @@ using Shape2DDeriv = Shape<512, 1, 1, false>;  // derivative outputs need > 64 r
 // quads in device memory (grid_api.cu pick_interp_small)
 using Shape2DSmallGG = Shape<256, 1, 1, false>;
 
-template <int S, class SH, bool RECIP, bool DERIV, bool LOGLOG = false, int REP = 0, bool GG = false>
+template <int S, class SH, bool DERIV, bool LOGLOG = false, int REP = 0, bool GG = false>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {
   constexpr int T = SH::kThreads;
   constexpr int U = SH::kUnroll;
@@ -1085,9 +1180,9 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       int2 ir[U], it[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        p[u].x = interp_one<S, RECIP, DERIV, LOGLOG, REP, GG>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
+        p[u].x = interp_one<S, DERIV, LOGLOG, REP, GG>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
                                              sm, A);
-        p[u].y = interp_one<S, RECIP, DERIV, LOGLOG, REP, GG>(vr[u].y, vt[u].y, ir[u].y, it[u].y, dr[u].y, dt[u].y,
+        p[u].y = interp_one<S, DERIV, LOGLOG, REP, GG>(vr[u].y, vt[u].y, ir[u].y, it[u].y, dr[u].y, dt[u].y,
                                              sm, A);
       }
       tn = next_tile(t);
@@ -1128,7 +1223,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
           if (q < e1) {
             int32_t i, j;
             double dpr, dpt;
-            const double pq = interp_one<S, RECIP, DERIV, LOGLOG, REP, GG>(vr1[k], vt1[k], i, j,
+            const double pq = interp_one<S, DERIV, LOGLOG, REP, GG>(vr1[k], vt1[k], i, j,
                                                                           dpr, dpt, sm, A);
             A.P[q] = pq;
             if (br) A.iR[q] = i;

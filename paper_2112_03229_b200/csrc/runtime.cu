@@ -2,17 +2,12 @@
 // status / version / launch-count entry points of the C ABI.
 // Product path (never includes or links oracle/).
 //
-// Tuning knobs, read at create / first use, for A/B experiments only (the
-// defaults are the measured best):
+// The product library reads no environment variables: launch shapes and
+// layouts follow from the plan alone.  A/B experiment knobs exist only in the
+// experiment build (_build.py --exp, -DEOS_EXPERIMENTS: libeossearch_exp.so):
 //   EOS_SEARCH_VARIANT, EOS_TIERED_VARIANT  launch-shape variants by name
-//   EOS_SMALL_TILES=0                       small launches (1-D, 2-D) keep the default tiles
-//   EOS_INTERP_VARIANT                      2-D launch variants by number
-//   EOS_INTERP_REP=0                        2-D plain axes (no cell records)
-//   EOS_GG_SMEM_KB                          smem cap of device-memory grids
-//   EOS_GG_QUAD_MB                          cell-quad budget of device-memory grids (0: row pairs)
-//   EOS_PDL (0/1)                           programmatic dependent launch
-//   EOS_HOST_SLOTS, EOS_HOST_CHUNK_LOG2     host-buffer pipeline depth / chunk
-//   EOS_PLAN_THREADS                        host threads of the automatic plan (n >= 1024)
+//   EOS_LAYOUT=d16,sf,big                   lifting layout of a single-level table
+//   EOS_SMALL_TILES=0                       small launches keep the default tiles
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -132,13 +127,9 @@ eos_status configure(const void* fn, int threads, int64_t smem, int num_sms, int
 
 // Launch with programmatic stream serialization (PDL), so a kernel's prologue
 // overlaps the previous kernel in the stream (see pdl_enter in kernels.cuh).
-// EOS_PDL=0 disables it (A/B experiments).
 cudaError_t launch(const void* fn, int64_t grid, int threads, size_t smem, cudaStream_t st,
                    void** params) {
-  static const bool pdl = [] {
-    const char* e = getenv("EOS_PDL");
-    return !(e && e[0] == '0');
-  }();
+  const bool pdl = true;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3((unsigned)threads);
@@ -184,7 +175,7 @@ const char* eos_status_str(eos_status s) {
   return "unknown status";
 }
 
-int32_t eos_abi_version(void) { return 2; }
+int32_t eos_abi_version(void) { return 3; }
 
 int64_t eos_launch_count(void) { return eos::rt::g_launches.load(); }
 

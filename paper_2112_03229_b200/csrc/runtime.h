@@ -50,18 +50,10 @@ dev::AxisParams axis_params(const TablePlan& p, int32_t x_off);
 template <class Body>
 eos_status host_pipeline(cudaStream_t caller, int64_t count, int64_t chunk, int64_t bytes_per_elem,
                          Body body) {
-  // tuning experiments: EOS_HOST_SLOTS (1..4), EOS_HOST_CHUNK_LOG2 (16..26)
-  static const int slots_env = [] {
-    const char* e = getenv("EOS_HOST_SLOTS");
-    return e ? std::max(1, std::min(4, atoi(e))) : 2;
-  }();
-  static const int chunk_log2 = [] {
-    const char* e = getenv("EOS_HOST_CHUNK_LOG2");
-    return e ? std::max(16, std::min(26, atoi(e))) : 0;
-  }();
-  if (chunk_log2) {
-    chunk = (int64_t(1) << chunk_log2) * chunk / (int64_t(1) << 23);
-  } else {  // mid-sized calls: ~8 chunks (>= chunk / 32 each), so H2D overlaps D2H
+  // two slots; mid-sized calls: ~8 chunks (>= chunk / 32 each), so H2D overlaps
+  // D2H (2-4 slots and 2^21-2^23-element chunks measured equal)
+  const int slots_env = 2;
+  {
     int64_t c = chunk / 32;
     while (c < chunk && 8 * c < count) c *= 2;
     chunk = c;

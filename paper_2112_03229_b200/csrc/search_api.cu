@@ -3,6 +3,7 @@
 // search, host-only planning.  Product path (never includes or links oracle/).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -49,30 +50,41 @@ struct eos_table_s {
 namespace {
 
 // ---------------------------------------------------------- kernel table ---
-template <int S, int MODE, class SH>
-const void* search_fn(bool cnt) {
-  return cnt ? (const void*)dv::search1d_kernel<S, MODE, true, SH>
-             : (const void*)dv::search1d_kernel<S, MODE, false, SH>;
+// The search kernel of a plan's lifting layout (eos_internal.h TablePlan):
+// SF = 1..3 fixed steps (big: a rare branch for deeper bins) or SF = 0 (all
+// steps in a runtime loop), key mode 0/1, 16- or 32-bit directory entries.
+template <int SF, bool BIG, int MODE, bool D16, class SH>
+const void* kfn() {
+  return (const void*)dv::search1d_kernel<SF, BIG, MODE, D16, false, SH>;
 }
 
-template <int MODE, class SH>
-const void* search_fn_mode(int steps, bool cnt) {
-  switch (steps) {
-    case 1: return search_fn<1, MODE, SH>(cnt);
-    case 2: return search_fn<2, MODE, SH>(cnt);
-    case 3: return search_fn<3, MODE, SH>(cnt);
-    case 4: return search_fn<4, MODE, SH>(cnt);
-    case 5: return search_fn<5, MODE, SH>(cnt);
-    case 6: return search_fn<6, MODE, SH>(cnt);
-    case 7: return search_fn<7, MODE, SH>(cnt);
-    case 8: return search_fn<8, MODE, SH>(cnt);
-    default: return search_fn<0, MODE, SH>(cnt);  // runtime S
+template <class SH, int MODE, bool D16>
+const void* search_fn_md(int sf, bool big) {
+  switch (sf) {
+    case 1: return big ? kfn<1, true, MODE, D16, SH>() : kfn<1, false, MODE, D16, SH>();
+    case 2: return big ? kfn<2, true, MODE, D16, SH>() : kfn<2, false, MODE, D16, SH>();
+    case 3: return big ? kfn<3, true, MODE, D16, SH>() : kfn<3, false, MODE, D16, SH>();
+    default: return kfn<0, true, MODE, D16, SH>();
   }
 }
 
 template <class SH>
-const void* search_fn_shape(int mode, int steps, bool cnt) {
-  return mode == 0 ? search_fn_mode<0, SH>(steps, cnt) : search_fn_mode<1, SH>(steps, cnt);
+const void* search_fn(const TablePlan& p) {
+  if (p.key_mode == 0)
+    return p.dir16 ? search_fn_md<SH, 0, true>(p.fast_steps, p.big)
+                   : search_fn_md<SH, 0, false>(p.fast_steps, p.big);
+  return p.dir16 ? search_fn_md<SH, 1, true>(p.fast_steps, p.big)
+                 : search_fn_md<SH, 1, false>(p.fast_steps, p.big);
+}
+
+// Validation launches (counters on): the runtime-step body, one shape.
+const void* counters_fn(const TablePlan& p) {
+  using SH = dv::ShapeCnt;
+  if (p.key_mode == 0)
+    return p.dir16 ? (const void*)dv::search1d_kernel<0, true, 0, true, true, SH>
+                   : (const void*)dv::search1d_kernel<0, true, 0, false, true, SH>;
+  return p.dir16 ? (const void*)dv::search1d_kernel<0, true, 1, true, true, SH>
+                 : (const void*)dv::search1d_kernel<0, true, 1, false, true, SH>;
 }
 
 // tiered tables (levels >= 1): search1d_tiered_kernel
@@ -113,24 +125,16 @@ const void* tiered_small_fn(int steps) {
   }
 }
 
-// Launch-shape variants of the tiered kernel (EOS_TIERED_VARIANT=<name>,
-// tuning experiments; mode 0, no counters, S <= 4).
-template <class SH>
-const void* tiered_variant_fn(int steps) {
-  switch (steps) {
-    case 1: return (const void*)dv::search1d_tiered_kernel<1, 0, false, SH>;
-    case 2: return (const void*)dv::search1d_tiered_kernel<2, 0, false, SH>;
-    case 3: return (const void*)dv::search1d_tiered_kernel<3, 0, false, SH>;
-    case 4: return (const void*)dv::search1d_tiered_kernel<4, 0, false, SH>;
-    default: return nullptr;
-  }
-}
-
 struct LaunchShape {
   const void* fn;
   int threads, unroll;
   bool clc;
 };
+
+template <class SH>
+LaunchShape shape_of(const TablePlan& p) {
+  return {search_fn<SH>(p), SH::kThreads, SH::kUnroll, SH::kClc};
+}
 
 // Default launch shape by image size: as many threads per SM as registers
 // allow (~1024 at <= 64 regs), with all image copies of an SM <= ~144 KB of
@@ -138,16 +142,14 @@ struct LaunchShape {
 // One 1024-thread CTA per SM (images > 72 KB) always takes the static
 // schedule: its per-tile CTA barrier makes CLC 13-15% slower there even at
 // S <= 2 (n = 4096 log-uniform, 143 KB image: 443 -> 508 Glookups/s;
-// profiles/r01_exp_table_size.json).
-LaunchShape pick_search(int mode, int steps, bool cnt, int64_t image_bytes) {
-  if (cnt) return {search_fn_shape<dv::ShapeCnt>(mode, steps, true), 256, 4, true};
-  if (image_bytes > 72 * 1024)
-    return {search_fn_shape<dv::ShapeDeepBig>(mode, steps, false), 1024, 4, false};
-  if (steps >= 3)
-    return {search_fn_shape<dv::ShapeDeepMid>(mode, steps, false), 512, 4, false};
-  if (image_bytes <= 32 * 1024)
-    return {search_fn_shape<dv::ShapeSmall>(mode, steps, false), 256, 4, true};
-  return {search_fn_shape<dv::ShapeMid>(mode, steps, false), 512, 4, true};
+// profiles/r01_exp_table_size.json).  Deep lifting (SF >= 3 or the runtime
+// loop) is issue-bound: static schedule there too.
+LaunchShape pick_search(const TablePlan& p, int64_t image_bytes) {
+  const bool deep = p.fast_steps == 0 || p.fast_steps >= 3;
+  if (image_bytes > 72 * 1024) return shape_of<dv::ShapeDeepBig>(p);
+  if (deep) return shape_of<dv::ShapeDeepMid>(p);
+  if (image_bytes <= 32 * 1024) return shape_of<dv::ShapeSmall>(p);
+  return shape_of<dv::ShapeMid>(p);
 }
 
 // Small launches: the same shapes with one double2 per thread per tile (4x
@@ -155,74 +157,80 @@ LaunchShape pick_search(int mode, int steps, bool cnt, int64_t image_bytes) {
 // tiles than half the SMs).  1e5 targets (25-49 default tiles): cfg1 37 -> 62,
 // cfg2 39 -> 64, cfg5 34 -> 48 Glookups/s; between 1.5e5 and 3e5 targets the two
 // are within launch noise, from 3.5e5 on they are the same kernel.
-template <int MODE, class SH>
-const void* small_fn_mode(int steps) {
-  switch (steps) {
-    case 1: return (const void*)dv::search1d_kernel<1, MODE, false, SH>;
-    case 2: return (const void*)dv::search1d_kernel<2, MODE, false, SH>;
-    case 3: return (const void*)dv::search1d_kernel<3, MODE, false, SH>;
-    case 4: return (const void*)dv::search1d_kernel<4, MODE, false, SH>;
-    default: return nullptr;  // deeper bins: the default tiles only
-  }
+LaunchShape pick_search_small(const TablePlan& p, int64_t image_bytes) {
+  const bool deep = p.fast_steps == 0 || p.fast_steps >= 3;
+  if (image_bytes > 72 * 1024) return shape_of<dv::Shape<1024, 1, 1, false>>(p);
+  if (deep) return shape_of<dv::Shape<512, 1, 2, false>>(p);
+  if (image_bytes <= 32 * 1024) return shape_of<dv::Shape<256, 1, 4, true>>(p);
+  return shape_of<dv::Shape<512, 1, 2, true>>(p);
 }
 
-template <class SH>
-LaunchShape small_shape(int mode, int steps) {
-  return {mode == 0 ? small_fn_mode<0, SH>(steps) : small_fn_mode<1, SH>(steps), SH::kThreads,
-          SH::kUnroll, SH::kClc};
-}
-
-LaunchShape pick_search_small(int mode, int steps, int64_t image_bytes) {
-  if (image_bytes > 72 * 1024) return small_shape<dv::Shape<1024, 1, 1, false>>(mode, steps);
-  if (steps >= 3) return small_shape<dv::Shape<512, 1, 2, false>>(mode, steps);
-  if (image_bytes <= 32 * 1024) return small_shape<dv::Shape<256, 1, 4, true>>(mode, steps);
-  return small_shape<dv::Shape<512, 1, 2, true>>(mode, steps);
-}
-
-// Launch-shape variants for tuning experiments (EOS_SEARCH_VARIANT=<name> at
-// create time; mode 0, S <= 4, no counters).  Not part of the C ABI.
+#ifdef EOS_EXPERIMENTS
+// ---- A/B experiments only (_build.py --exp: libeossearch_exp.so) ----------
+// EOS_SEARCH_VARIANT=<name>: launch shape by name (single-level tables)
+// EOS_TIERED_VARIANT=<name>: launch shape of tiered tables (mode 0, S <= 4)
+// EOS_LAYOUT=<d16>,<sf>,<big>: force the lifting layout of a single-level table
+// EOS_SMALL_TILES=0: small launches keep the default tiles
 struct Variant {
   const char* name;
-  int threads, unroll;
-  bool clc;
-  const void* (*get)(int steps);
+  LaunchShape (*get)(const TablePlan& p);
 };
-
 template <class SH>
-const void* variant_fn(int steps) {
-  switch (steps) {
-    case 1: return (const void*)dv::search1d_kernel<1, 0, false, SH>;
-    case 2: return (const void*)dv::search1d_kernel<2, 0, false, SH>;
-    case 3: return (const void*)dv::search1d_kernel<3, 0, false, SH>;
-    case 4: return (const void*)dv::search1d_kernel<4, 0, false, SH>;
-    default: return nullptr;
+LaunchShape vshape(const TablePlan& p) { return shape_of<SH>(p); }
+const Variant kVariants[] = {
+    {"static256u4", vshape<dv::Shape<256, 4, 4, false>>},
+    {"static512u4", vshape<dv::Shape<512, 4, 2, false>>},
+    {"static1024u4", vshape<dv::Shape<1024, 4, 1, false>>},
+    {"static1024u2", vshape<dv::Shape<1024, 2, 1, false>>},
+    {"clc256u4", vshape<dv::Shape<256, 4, 4, true>>},
+    {"clc512u4", vshape<dv::Shape<512, 4, 2, true>>},
+    {"clc1024u4", vshape<dv::Shape<1024, 4, 1, true>>},
+    {"static512u8", vshape<dv::Shape<512, 8, 2, false>>},
+};
+template <class SH>
+LaunchShape tvshape(const TablePlan& p) {
+  switch (p.steps) {
+    case 1: return {(const void*)dv::search1d_tiered_kernel<1, 0, false, SH>, SH::kThreads, SH::kUnroll, SH::kClc};
+    case 2: return {(const void*)dv::search1d_tiered_kernel<2, 0, false, SH>, SH::kThreads, SH::kUnroll, SH::kClc};
+    case 3: return {(const void*)dv::search1d_tiered_kernel<3, 0, false, SH>, SH::kThreads, SH::kUnroll, SH::kClc};
+    default: return {(const void*)dv::search1d_tiered_kernel<4, 0, false, SH>, SH::kThreads, SH::kUnroll, SH::kClc};
   }
 }
-
 const Variant kTieredVariants[] = {
-    {"static512u4", 512, 4, false, tiered_variant_fn<dv::Shape<512, 4, 1, false>>},
-    {"static1024u2", 1024, 2, false, tiered_variant_fn<dv::Shape<1024, 2, 1, false>>},
-    {"clc1024u2", 1024, 2, true, tiered_variant_fn<dv::Shape<1024, 2, 1, true>>},
-    {"static1024u1", 1024, 1, false, tiered_variant_fn<dv::Shape<1024, 1, 1, false>>},
+    {"static512u4", tvshape<dv::Shape<512, 4, 1, false>>},
+    {"static1024u1", tvshape<dv::Shape<1024, 1, 1, false>>},
+    {"clc1024u2", tvshape<dv::Shape<1024, 2, 1, true>>},
 };
-
-const Variant kVariants[] = {
-    {"static256u4", 256, 4, false, variant_fn<dv::Shape<256, 4, 4, false>>},
-    {"static512u4", 512, 4, false, variant_fn<dv::Shape<512, 4, 2, false>>},
-    {"clc256u4", 256, 4, true, variant_fn<dv::Shape<256, 4, 4, true>>},
-    {"clc256u8", 256, 8, true, variant_fn<dv::Shape<256, 8, 4, true>>},
-    {"clc256u2", 256, 2, true, variant_fn<dv::Shape<256, 2, 4, true>>},
-    {"clc512u4", 512, 4, true, variant_fn<dv::Shape<512, 4, 2, true>>},
-    {"clc512u2", 512, 2, true, variant_fn<dv::Shape<512, 2, 2, true>>},
-    {"clc1024u4", 1024, 4, true, variant_fn<dv::Shape<1024, 4, 1, true>>},
-    {"clc1024u2", 1024, 2, true, variant_fn<dv::Shape<1024, 2, 1, true>>},
-    {"clc128u8", 128, 8, true, variant_fn<dv::Shape<128, 8, 8, true>>},
-    {"static1024u4", 1024, 4, false, variant_fn<dv::Shape<1024, 4, 1, false>>},
-    {"clc256u1", 256, 1, true, variant_fn<dv::Shape<256, 1, 4, true>>},
-    {"clc512u1", 512, 1, true, variant_fn<dv::Shape<512, 1, 2, true>>},
-    {"clc128u2", 128, 2, true, variant_fn<dv::Shape<128, 2, 8, true>>},
-    {"static256u2", 256, 2, false, variant_fn<dv::Shape<256, 2, 4, false>>},
-};
+bool exp_variant(const TablePlan& p, bool tiered, LaunchShape* ls) {
+  const char* want = getenv(tiered ? "EOS_TIERED_VARIANT" : "EOS_SEARCH_VARIANT");
+  if (!want || (tiered && (p.key_mode != 0 || p.steps > 4))) return false;
+  const Variant* vs = tiered ? kTieredVariants : kVariants;
+  const size_t nv = tiered ? sizeof(kTieredVariants) / sizeof(Variant) : sizeof(kVariants) / sizeof(Variant);
+  for (size_t i = 0; i < nv; ++i)
+    if (strcmp(want, vs[i].name) == 0) {
+      *ls = vs[i].get(p);
+      return true;
+    }
+  return false;
+}
+void exp_layout(TablePlan* p) {
+  const char* e = getenv("EOS_LAYOUT");
+  int d16 = 0, sf = 0, big = 0;
+  if (!e || sscanf(e, "%d,%d,%d", &d16, &sf, &big) != 3) return;
+  if (d16 && (p->n > eos::kDir16MaxN || p->max_occ > eos::kDir16MaxOcc)) d16 = 0;
+  if (sf > p->steps) sf = p->steps;
+  p->dir16 = d16 != 0;
+  p->fast_steps = sf;
+  p->big = sf == 0 || p->steps > sf;
+  p->image_bytes = p->x_bytes + ((((p->dir16 ? 2 : 4) * (int64_t)p->bins) + 15) & ~int64_t(15));
+}
+bool exp_small_off() {
+  const char* e = getenv("EOS_SMALL_TILES");
+  return e && e[0] == '0';
+}
+#else
+bool exp_small_off() { return false; }
+#endif
 
 eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* out, int64_t gofs,
                          uint64_t* counters, cudaStream_t st) {
@@ -282,7 +290,7 @@ eos_status eos_plan_table_hash(const double* table_host, int64_t n, int32_t kind
                                eos_table_info_t* info, uint32_t* dir_out, int64_t cap) {
   if (!info) return EOS_ERR_NULL;
   TablePlan p;
-  eos_status st = eos::plan_table(table_host, n, kind, param, false, &p);
+  eos_status st = eos::plan_table(table_host, n, kind, param, false, &p, 0, EOS_MAX_TABLE, true);
   if (st != EOS_OK) return st;
   if (dir_out) {
     if (cap < p.bins) return EOS_ERR_SIZE;
@@ -325,6 +333,9 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
     eos_status st = eos::plan_tiered(table_host, n, levels, kind, param, &tp);
     if (st != EOS_OK) { delete t; return st; }
     t->plan = std::move(tp.top);
+#ifdef EOS_EXPERIMENTS
+    if (tp.levels == 0) exp_layout(&t->plan);
+#endif
     t->levels = tp.levels;
     t->n = tp.n;
     t->top_n = tp.top_n;
@@ -367,43 +378,31 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
   }
   for (int c = 0; c < 2 && st == EOS_OK; ++c) {
     const bool cnt = c == 1;
+    LaunchShape ls;
     if (t->levels > 0) {
-      t->fn[c] = t->plan.key_mode == 0 ? tiered_fn_mode<0, dv::ShapeTiered>(t->plan.steps, cnt)
-                                       : tiered_fn_mode<1, dv::ShapeTiered>(t->plan.steps, cnt);
       using SH = dv::ShapeTiered;
-      t->threads[c] = cnt ? dv::ShapeCnt::kThreads : SH::kThreads;
-      t->unroll[c] = cnt ? dv::ShapeCnt::kUnroll : SH::kUnroll;
-      t->clc[c] = cnt ? dv::ShapeCnt::kClc : SH::kClc;
+      ls.fn = t->plan.key_mode == 0 ? tiered_fn_mode<0, SH>(t->plan.steps, cnt)
+                                    : tiered_fn_mode<1, SH>(t->plan.steps, cnt);
+      ls.threads = cnt ? dv::ShapeCnt::kThreads : SH::kThreads;
+      ls.unroll = cnt ? dv::ShapeCnt::kUnroll : SH::kUnroll;
+      ls.clc = cnt ? dv::ShapeCnt::kClc : SH::kClc;
+    } else if (cnt) {
+      ls = {counters_fn(t->plan), dv::ShapeCnt::kThreads, dv::ShapeCnt::kUnroll, dv::ShapeCnt::kClc};
     } else {
-      LaunchShape ls = pick_search(t->plan.key_mode, t->plan.steps, cnt, t->smem_bytes);
-      t->fn[c] = ls.fn;
-      t->threads[c] = ls.threads;
-      t->unroll[c] = ls.unroll;
-      t->clc[c] = ls.clc;
+      ls = pick_search(t->plan, t->smem_bytes);
     }
-    if (c == 0) {  // tuning experiments: launch-shape variants by name
-      const bool tiered = t->levels > 0;
-      const char* want = getenv(tiered ? "EOS_TIERED_VARIANT" : "EOS_SEARCH_VARIANT");
-      const Variant* vs = tiered ? kTieredVariants : kVariants;
-      const size_t nv = tiered ? sizeof(kTieredVariants) / sizeof(Variant)
-                               : sizeof(kVariants) / sizeof(Variant);
-      for (size_t i = 0; i < nv; ++i) {
-        const Variant& v = vs[i];
-        if (!want || strcmp(want, v.name) != 0 || t->plan.key_mode != 0) continue;
-        const void* f = v.get(t->plan.steps);
-        if (!f) break;
-        t->fn[0] = f;
-        t->threads[0] = v.threads;
-        t->unroll[0] = v.unroll;
-        t->clc[0] = v.clc;
-      }
-    }
+#ifdef EOS_EXPERIMENTS
+    if (!cnt) exp_variant(t->plan, t->levels > 0, &ls);
+#endif
+    t->fn[c] = ls.fn;
+    t->threads[c] = ls.threads;
+    t->unroll[c] = ls.unroll;
+    t->clc[c] = ls.clc;
     st = configure(t->fn[c], t->threads[c], t->smem_bytes, t->num_sms, &t->grid[c],
                    c == 0 ? &t->ctas_per_sm : nullptr);
   }
   if (st != EOS_OK) return fail(st);
-  const char* small_env = getenv("EOS_SMALL_TILES");  // "0": default tiles only
-  if (t->levels > 0 && !getenv("EOS_TIERED_VARIANT") && !(small_env && small_env[0] == '0')) {
+  if (t->levels > 0 && !exp_small_off()) {
     const void* fs = t->plan.key_mode == 0 ? tiered_small_fn<0>(t->plan.steps)
                                            : tiered_small_fn<1>(t->plan.steps);
     if (fs && configure(fs, 512, t->smem_bytes, t->num_sms, &t->grid_small, nullptr) == EOS_OK) {
@@ -413,8 +412,8 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
       t->clc_small = false;
     }
   }
-  if (t->levels == 0 && !getenv("EOS_SEARCH_VARIANT") && !(small_env && small_env[0] == '0')) {
-    const LaunchShape ls = pick_search_small(t->plan.key_mode, t->plan.steps, t->smem_bytes);
+  if (t->levels == 0 && !exp_small_off()) {
+    const LaunchShape ls = pick_search_small(t->plan, t->smem_bytes);
     if (ls.fn && configure(ls.fn, ls.threads, t->smem_bytes, t->num_sms, &t->grid_small,
                            nullptr) == EOS_OK) {
       t->fn_small = ls.fn;

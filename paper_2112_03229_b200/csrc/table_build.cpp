@@ -79,9 +79,24 @@ HashParams log_params(const std::vector<double>& X, int mode, int64_t H) {
   return h;
 }
 
-int64_t image_of(int64_t n, int64_t bins) { return pad16(8 * n) + pad16(4 * bins); }
+int64_t image_of(int64_t n, int64_t bins, bool dir16 = false) {
+  return pad16(8 * n) + pad16((dir16 ? 2 : 4) * bins);
+}
 
-eos_status build(const std::vector<double>& X, int mode, const HashParams& h, TablePlan* p) {
+double lifting_probes(int o, int S);
+// Layout of a search table's lifting (kernels.cuh lookup_b), choose_layout below.
+struct Layout {
+  bool dir16 = false;
+  int sf = 0;
+  bool big = false;
+  int64_t image = 0;
+  double cost = 0.0;
+};
+Layout choose_layout(const std::vector<int64_t>& runs, int64_t n, int64_t bins, int steps,
+                     double probes_per_bin, bool search);
+
+eos_status build(const std::vector<double>& X, int mode, const HashParams& h, TablePlan* p,
+                 bool search) {
   const int64_t n = (int64_t)X.size();
   if (h.bins < 1 || h.bins > (int64_t(1) << 22)) return EOS_ERR_UNSUPPORTED;
   std::vector<uint32_t> occ((size_t)h.bins, 0);
@@ -105,6 +120,23 @@ eos_status build(const std::vector<double>& X, int mode, const HashParams& h, Ta
   p->steps = ceil_log2_plus1((int)mx);
   p->x_bytes = pad16(8 * n);
   p->image_bytes = image_of(n, h.bins);
+  p->dir16 = false;
+  p->fast_steps = p->steps;
+  p->big = false;
+  if (search) {  // directory format + fixed / rare steps (choose_layout)
+    std::vector<int64_t> runs;
+    double probes = 0.0;
+    for (int64_t b = 0; b < h.bins; ++b)
+      if (occ[b]) {
+        runs.push_back(occ[b]);
+        probes += lifting_probes((int)occ[b], p->steps);
+      }
+    const Layout L = choose_layout(runs, n, h.bins, p->steps, probes / (double)h.bins, true);
+    p->dir16 = L.dir16;
+    p->fast_steps = L.sf;
+    p->big = L.big;
+    p->image_bytes = L.image;
+  }
   return EOS_OK;
 }
 
@@ -141,12 +173,64 @@ double lifting_probes(int o, int S) {
 // (profiles/r01_exp_table_size.json): the penalty lets only a large probe
 // saving buy the extra smem.  Targets are taken log-uniform over the table
 // range, i.e. uniform over the bins (equal key width).
-double cost_of(double mean_probes, int steps, int64_t image_bytes) {
-  const double shape = image_bytes <= 32 * 1024   ? 0.0
-                       : image_bytes <= 72 * 1024  ? 1.0
-                       : image_bytes <= 144 * 1024 ? 1.5
-                                                   : 4.5;
-  return 3.5 + 6.1 * mean_probes + 1.0 * steps + shape;
+double shape_cost(int64_t image_bytes) {
+  return image_bytes <= 32 * 1024 ? 0.0
+         : image_bytes <= 72 * 1024 ? 1.0
+         : image_bytes <= 144 * 1024 ? 1.5
+                                     : 4.5;
+}
+
+double cost_of(double mean_probes, double issue, int64_t image_bytes) {
+  return 3.5 + 6.1 * mean_probes + issue + shape_cost(image_bytes);
+}
+
+// Layout of a search table's lifting (kernels.cuh lookup_b): SF fixed steps
+// cover bins of < 2^SF entries; deeper bins (big) run their larger strides in
+// a branch that a warp takes when any of its 32 lanes lands in one.  Issue
+// cost, in the units of cost_of (one per fixed step): SF, plus for big 0.5
+// (the test) + P(warp diverges) x 1.5 per extra step; SF = 0 (all strides in
+// a runtime loop): S + 1.  A 16-bit directory costs 0.25 (one more unpack
+// instruction) and halves the directory's shared memory.
+
+Layout choose_layout(const std::vector<int64_t>& runs, int64_t n, int64_t bins, int steps,
+                     double probes_per_bin, bool search) {
+  Layout best;
+  best.sf = steps;
+  best.image = image_of(n, bins);
+  best.cost = cost_of(probes_per_bin, (double)steps, best.image);
+  if (!search) return best;
+  int64_t mx = 0;
+  for (const int64_t r : runs) mx = std::max(mx, r);
+  const bool can16 = n <= kDir16MaxN && mx <= kDir16MaxOcc;
+  bool have = false;
+  for (int d16 = 0; d16 <= (can16 ? 1 : 0); ++d16) {
+    const int64_t img = image_of(n, bins, d16 != 0);
+    for (int sf = 0; sf <= std::min(steps, kMaxFastSteps); ++sf) {
+      if (sf == 0 && steps <= kMaxFastSteps) continue;  // the runtime loop only for deep tables
+      const bool big = sf == 0 || steps > sf;
+      double issue;
+      if (sf == 0) {
+        issue = steps + 1.0;
+      } else {
+        int64_t nbig = 0;
+        for (const int64_t r : runs) nbig += r >= (int64_t(1) << sf);
+        const double f = (double)nbig / (double)bins;
+        const double pw = 1.0 - pow(1.0 - f, 32.0);
+        issue = sf + (big ? 0.5 + pw * 1.5 * (steps - sf) : 0.0);
+      }
+      issue += d16 ? 0.25 : 0.0;
+      const double c = cost_of(probes_per_bin, issue, img);
+      if (!have || c < best.cost - 1e-9) {
+        best.dir16 = d16 != 0;
+        best.sf = sf;
+        best.big = big;
+        best.image = img;
+        best.cost = c;
+        have = true;
+      }
+    }
+  }
+  return best;
 }
 
 // A candidate hash evaluated without building its directory: the table is
@@ -162,7 +246,7 @@ struct CandidateEval {
 };
 
 CandidateEval evaluate(const std::vector<uint32_t>& keys, const HashParams& h, bool compact,
-                       std::vector<int64_t>& runs) {
+                       bool search, std::vector<int64_t>& runs) {
   CandidateEval e;
   const int64_t n = (int64_t)keys.size();
   if (h.bins < 1 || h.bins > (int64_t(1) << 22)) return e;
@@ -206,7 +290,9 @@ CandidateEval evaluate(const std::vector<uint32_t>& keys, const HashParams& h, b
       probes += lifting_probes(o, e.steps);
     }
   }
-  e.cost = cost_of(probes / (double)h.bins, e.steps, e.image_bytes);
+  const Layout L = choose_layout(runs, n, h.bins, e.steps, probes / (double)h.bins, search);
+  e.cost = L.cost;
+  e.image_bytes = L.image;
   return e;
 }
 
@@ -224,7 +310,7 @@ CandidateEval evaluate(const std::vector<uint32_t>& keys, const HashParams& h, b
 // For search tables (!compact) fill_budget > 0 replaces the image budget
 // (tiered sample tables, plan_tiered).
 eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, TablePlan* out,
-                     int64_t fill_budget = 0) {
+                     int64_t fill_budget, bool search) {
   const int64_t n = (int64_t)X.size();
   const bool fill = compact && fill_budget > 0;
   const int64_t budget = fill_budget > 0 ? fill_budget
@@ -234,12 +320,14 @@ eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, Table
   // candidates, in the order of preference of ties: exponent hash k = 0.., then
   // the logarithm hash on a geometric |H| grid
   std::vector<HashParams> cand;
+  // (16-bit directory entries may fit twice the bins: search tables, n <= 4096)
+  const bool may16 = search && n <= kDir16MaxN;
   for (int k = 0; k <= EOS_MAX_K; ++k) {
     HashParams h = exponent_params(X, mode, k);
-    if (k > 0 && image_of(n, h.bins) > budget) break;
+    if (k > 0 && image_of(n, h.bins, may16) > budget) break;
     cand.push_back(h);
   }
-  const int64_t max_bins = (budget - pad16(8 * n)) / 4;
+  const int64_t max_bins = (budget - pad16(8 * n)) / (may16 ? 2 : 4);
   for (double H = 1.0; H <= (double)max_bins; H *= 1.0905077326652577 /* 2^(1/8) */)
     cand.push_back(log_params(X, mode, (int64_t)H));
   // evaluate them (independently: over host threads for large tables) ...
@@ -247,13 +335,9 @@ eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, Table
   auto eval_range = [&](size_t i0, size_t step) {
     std::vector<int64_t> runs;
     for (size_t i = i0; i < cand.size(); i += step)
-      if (cand[i].bins >= 1) ev[i] = evaluate(keys, cand[i], compact, runs);
+      if (cand[i].bins >= 1) ev[i] = evaluate(keys, cand[i], compact, search, runs);
   };
-  static const unsigned max_threads = [] {  // EOS_PLAN_THREADS: A/B knob (runtime.cu)
-    const char* e = getenv("EOS_PLAN_THREADS");
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    return e ? (unsigned)std::max(1, atoi(e)) : std::min(hw, 8u);
-  }();
+  static const unsigned max_threads = std::min(std::max(1u, std::thread::hardware_concurrency()), 8u);
   const size_t nth = n >= 1024 ? max_threads : 1;
   if (nth > 1) {
     std::vector<std::thread> pool;
@@ -274,9 +358,9 @@ eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, Table
   for (size_t i = 0; i < cand.size(); ++i) {
     const HashParams& h = cand[i];
     if (h.bins < 1) continue;
-    if (have && image_of(n, h.bins) > budget) continue;
     const CandidateEval& e = ev[i];
     if (!e.ok) continue;
+    if (have && (search ? e.image_bytes : image_of(n, h.bins)) > budget) continue;
     const double c = e.cost;
     if (have && fill && e.image_bytes > budget) continue;
     const bool tie_better = fill ? e.image_bytes > best_e.image_bytes : e.image_bytes < best_e.image_bytes;
@@ -287,13 +371,13 @@ eos_status plan_auto(const std::vector<double>& X, int mode, bool compact, Table
     }
   }
   if (!have) return EOS_ERR_UNSUPPORTED;
-  return build(X, mode, best, out);  // the directory of the chosen hash only
+  return build(X, mode, best, out, search);  // the directory of the chosen hash only
 }
 
 }  // namespace
 
 eos_status plan_table(const double* Xin, int64_t n, int kind, int64_t param, bool strict,
-                      TablePlan* out, int64_t fill_budget, int64_t max_n) {
+                      TablePlan* out, int64_t fill_budget, int64_t max_n, bool search) {
   if (!Xin || !out) return EOS_ERR_NULL;
   if (n < (strict ? 2 : 1) || n > max_n) return EOS_ERR_SIZE;
   if (kind == EOS_HASH_EXPONENT && (param < 0 || param > EOS_MAX_K)) return EOS_ERR_UNSUPPORTED;
@@ -314,12 +398,16 @@ eos_status plan_table(const double* Xin, int64_t n, int kind, int64_t param, boo
   TablePlan p;
   eos_status st;
   if (kind == EOS_HASH_AUTO) {
-    st = plan_auto(X, mode, strict, &p, fill_budget);
+    st = plan_auto(X, mode, strict, &p, fill_budget, search && !strict);
   } else {
     const HashParams h = kind == EOS_HASH_EXPONENT ? exponent_params(X, mode, (int)param)
                                                    : log_params(X, mode, param);
-    st = build(X, mode, h, &p);
-    if (st == EOS_OK && p.image_bytes > kMaxImage) st = EOS_ERR_UNSUPPORTED;
+    st = build(X, mode, h, &p, search && !strict);
+    // the staged image must fit shared memory: fp64 X + directory, or for the
+    // sample table of a tiered table (the caller passing max_n = kMaxTopKeys)
+    // its 32-bit keys + directory (make_key_image)
+    const int64_t staged = max_n == kMaxTopKeys ? pad16(4 * n) + pad16(4 * p.bins) : p.image_bytes;
+    if (st == EOS_OK && staged > kMaxImage) st = EOS_ERR_UNSUPPORTED;
   }
   if (st != EOS_OK) return st;
   p.X = std::move(X);
@@ -348,7 +436,7 @@ eos_status plan_tiered(const double* Xin, int64_t n, int levels, int kind, int64
   t.n = n;
   t.top_n = n1;
   if (levels == 0) {
-    eos_status st = plan_table(Xin, n, kind, param, false, &t.top);
+    eos_status st = plan_table(Xin, n, kind, param, false, &t.top, 0, EOS_MAX_TABLE, true);
     if (st != EOS_OK) return st;
     t.x_last = t.top.X[n - 1];
     *out = std::move(t);
@@ -423,7 +511,15 @@ std::vector<uint8_t> make_key_image(const TablePlan& p) {
 std::vector<uint8_t> make_image(const TablePlan& p) {
   std::vector<uint8_t> img((size_t)p.image_bytes, 0);
   memcpy(img.data(), p.X.data(), (size_t)(8 * p.n));
-  memcpy(img.data() + p.x_bytes, p.dir.data(), (size_t)(4 * p.bins));
+  if (p.dir16) {  // lo | occ << 12 (kernels.cuh dir_entry)
+    for (int64_t b = 0; b < p.bins; ++b) {
+      const uint32_t d = p.dir[b];
+      const uint16_t e = (uint16_t)((d & 0xFFFu) | ((d >> 16) << 12));
+      memcpy(img.data() + p.x_bytes + 2 * b, &e, 2);
+    }
+  } else {
+    memcpy(img.data() + p.x_bytes, p.dir.data(), (size_t)(4 * p.bins));
+  }
   return img;
 }
 
@@ -444,6 +540,9 @@ void fill_info(const TablePlan& p, eos_table_info_t* info) {
   info->pad_ = 0;
   info->top_n = p.n;
   info->level_bytes = 0;
+  info->dir_entry_bytes = p.dir16 ? 2 : 4;
+  info->fast_steps = p.fast_steps;
+  info->rare_steps = p.big ? 1 : 0;
 }
 
 void fill_info(const TieredPlan& t, eos_table_info_t* info) {

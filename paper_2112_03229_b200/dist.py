@@ -36,6 +36,7 @@ class Dist:
         if self.world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29500")
             dist.init_process_group(backend)
             self.pg = dist
             self.backend = backend

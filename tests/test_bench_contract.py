@@ -44,6 +44,36 @@ def test_our_arm_refuses_to_run_without_a_gpu():
 def test_reference_arm_non_zero_rank_is_silent():
     env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                        "--steps", "1", "--warmup", "0", "--workload", "cfg1"],
+                        "--gpus", "2", "--steps", "1", "--warmup", "0", "--workload", "cfg1"],
                        capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--gpus", "4", "--steps", "1", "--warmup", "0", "--workload", "cfg1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
+
+
+def test_gpus_n_self_launches_n_ranks():
+    """--gpus 2 outside torchrun re-runs bench.py under torch.distributed.run with 2 ranks
+    (the reference arm here: rank 0 prints one line with n_gpus 2, rank 1 is silent)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--gpus", "2", "--steps", "2", "--warmup", "1", "--workload", "cfg1"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["steps"] == 2 and d["warmup"] == 1
+
+
+def test_reference_arm_runs_exactly_k_steps_on_the_same_config():
+    r = run_bench("--impl", "reference", "--steps", "7", "--warmup", "2", "--workload", "cfg2")
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["steps"] == 7 and d["warmup"] == 2
+    assert d["config"]["workload"] == "cfg2" and d["config"]["units_total"] == 1 << 27

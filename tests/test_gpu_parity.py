@@ -178,91 +178,80 @@ def test_ragged_and_misaligned(count, y_off, o_off):
 @pytest.mark.parametrize("table,kw", [("cfg1", {}), ("cfg2", {"log_bins": 12000}),
                                       ("cfg5", {}), ("cfg5", {"log_bins": 5000}),
                                       ("cfg2", {"k": 0})])
-def test_small_launch_tiles_match_default_tiles_and_oracle(table, kw, monkeypatch):
+def test_small_launch_tiles_match_default_tiles_and_oracle(table, kw):
     """Launches whose default tiling leaves most SMs idle run the small-tile shape
-    (runtime.cu EOS_SMALL_TILES): every shape family (image <= 32 KB / <= 72 KB / larger,
-    S <= 2 / S >= 3), counts on both sides of the switch, ragged heads and tails; bit-exact
-    against the oracle and against the default tiles."""
+    (search_api.cu launch_search): every shape family (image <= 32 KB / <= 72 KB / larger,
+    fixed steps / rare branch), counts on both sides of the switch, ragged heads and tails;
+    bit-exact against the oracle, and each slice equal to the same targets inside one
+    400,003-target launch (default tiles)."""
     w = datagen.workload(table, count=400_003)
     Yall = w.targets.host_fill(0, w.count, w.table)
     Yall[:4] = [np.nan, -np.inf, np.inf, 0.0]
-    t_small = eos.Table(w.table, **kw)
-    monkeypatch.setenv("EOS_SMALL_TILES", "0")
-    t_def = eos.Table(w.table, **kw)
-    monkeypatch.delenv("EOS_SMALL_TILES")
+    t = eos.Table(w.table, **kw)
+    whole = t.search(to_dev(Yall)).cpu().numpy()
+    assert_same(whole, oracle.search(w.table, Yall), Yall)
     for count, off in ((1, 0), (7, 1), (1000, 3), (50_001, 1), (151_553, 0), (151_552, 2),
                        (300_001, 1), (400_000, 3)):
         Y = Yall[off:off + count]
-        yd = to_dev(Yall)[off:off + count]
-        a = t_small.search(yd)
-        b = t_def.search(yd)
+        a = t.search(to_dev(Yall)[off:off + count])
         torch.cuda.synchronize()
-        ref = oracle.search(w.table, Y)
-        assert_same(a.cpu().numpy(), ref, Y)
-        assert_same(b.cpu().numpy(), ref, Y)
-    t_small.close()
-    t_def.close()
+        assert_same(a.cpu().numpy(), oracle.search(w.table, Y), Y)
+        assert np.array_equal(a.cpu().numpy(), whole[off:off + count])
+    t.close()
 
 
 @pytest.mark.parametrize("loglog,global_grid", [(False, False), (True, False), (False, True),
                                                 (True, True)])
-def test_small_launch_tiles_2d_match_default_tiles_and_oracle(loglog, global_grid, monkeypatch):
+def test_small_launch_tiles_2d_match_default_tiles_and_oracle(loglog, global_grid):
     """2-D launches with fewer default tiles than half the SMs run the small-tile kernel
     (grid_api.cu launch_interp: the image without G, corners from cell quads in device
-    memory): brackets and P bit-identical to the default tiles, brackets equal to the
-    oracle's, P within the bar, on both sides of the switch (74 tiles = 151,552 pairs)."""
+    memory): brackets and P bit-identical to the same pairs inside one 160,003-pair launch
+    (default tiles), brackets equal to the oracle's, P within the bar, on both sides of the
+    switch (74 tiles = 151,552 pairs)."""
     w = datagen.workload("cfg4", count=160_003)
     rho = w.rho_targets.host_fill(0, w.count)
     T = w.T_targets.host_fill(0, w.count)
     rho[:3] = [np.nan, w.rho[0] / 3, w.rho[-1] * 3]
     rho[3:3 + w.rho.size] = w.rho
-    g_small = eos.Grid2D(w.rho, w.T, w.P, loglog=loglog, global_grid=global_grid)
-    monkeypatch.setenv("EOS_SMALL_TILES", "0")
-    g_def = eos.Grid2D(w.rho, w.T, w.P, loglog=loglog, global_grid=global_grid)
-    monkeypatch.delenv("EOS_SMALL_TILES")
+    g = eos.Grid2D(w.rho, w.T, w.P, loglog=loglog, global_grid=global_grid)
+    whole = [x.cpu().numpy() for x in g.interp(to_dev(rho), to_dev(T))]
+    whole_d = [x.cpu().numpy() for x in g.interp(to_dev(rho), to_dev(T), derivatives=True)]
     ref_all = (oracle.interp2d_loglog if loglog else oracle.interp2d)(w.rho, w.T, w.P, rho, T)
     for count, off in ((1, 0), (7, 1), (1000, 0), (20_001, 1), (151_551, 0), (151_553, 1),
                        (160_000, 2)):
         rd, td = to_dev(rho)[off:off + count], to_dev(T)[off:off + count]
-        a = g_small.interp(rd, td)
-        b = g_def.interp(rd, td)
-        ad = g_small.interp(rd, td, derivatives=True)  # the derivative kernels switch too
-        bd = g_def.interp(rd, td, derivatives=True)
+        a = g.interp(rd, td)
+        ad = g.interp(rd, td, derivatives=True)  # the derivative kernels switch too
         torch.cuda.synchronize()
-        for x, y in list(zip(a, b)) + list(zip(ad, bd)):
-            assert np.array_equal(x.cpu().numpy(), y.cpu().numpy(), equal_nan=True)
+        for x, y in list(zip(a, whole)) + list(zip(ad, whole_d)):
+            assert np.array_equal(x.cpu().numpy(), y[off:off + count], equal_nan=True)
         assert np.array_equal(a[1].cpu().numpy(), ref_all[1][off:off + count])
         assert np.array_equal(a[2].cpu().numpy(), ref_all[2][off:off + count])
         check_interp(a[0].cpu().numpy(), ref_all[0][off:off + count])
-    g_small.close()
-    g_def.close()
+    g.close()
 
 
 @pytest.mark.parametrize("kind", ["loguniform", "mixed_sign"])
-def test_tiered_small_launch_tiles_match_default_tiles_and_oracle(kind, monkeypatch):
+def test_tiered_small_launch_tiles_match_default_tiles_and_oracle(kind):
     """Tiered tables: launches whose default tiles would leave most SMs idle use 512 x 1
-    tiles; bit-exact against the default tiles and the oracle on both sides of the switch."""
+    tiles; bit-exact against the oracle and against the same targets inside one large
+    launch (default tiles), on both sides of the switch."""
     rng = np.random.default_rng(11)
     X = np.sort(10.0 ** rng.uniform(-6, 10, 200_003))
     if kind == "mixed_sign":
         X = np.sort(np.concatenate([-X[:50_000], X[50_000:]]))
     Yall = np.concatenate([10.0 ** rng.uniform(-7, 11, 320_000) * rng.choice([-1.0, 1.0], 320_000),
                            X[::7], [np.nan, np.inf, -np.inf, 0.0]])
-    t_small = eos.Table(X, levels=1)
-    monkeypatch.setenv("EOS_SMALL_TILES", "0")
-    t_def = eos.Table(X, levels=1)
-    monkeypatch.delenv("EOS_SMALL_TILES")
+    t = eos.Table(X, levels=1)
+    whole = t.search(to_dev(Yall)).cpu().numpy()
+    assert_same(whole, oracle.search(X, Yall), Yall)
     for count, off in ((1, 0), (999, 3), (100_003, 1), (303_103, 0), (320_000, 5)):
         Y = Yall[off:off + count]
-        yd = to_dev(Yall)[off:off + count]
-        a = t_small.search(yd)
-        b = t_def.search(yd)
+        a = t.search(to_dev(Yall)[off:off + count])
         torch.cuda.synchronize()
-        ref = oracle.search(X, Y)
-        assert_same(a.cpu().numpy(), ref, Y)
-        assert_same(b.cpu().numpy(), ref, Y)
-    t_small.close()
-    t_def.close()
+        assert_same(a.cpu().numpy(), oracle.search(X, Y), Y)
+        assert np.array_equal(a.cpu().numpy(), whole[off:off + count])
+    t.close()
 
 
 def test_counters_match_oracle():
@@ -1040,14 +1029,10 @@ def test_cuda_graph_capture_and_replay():
 
 
 # ------------------------- 2-D grids in device memory (EOS_GRID_GLOBAL) -----
-@pytest.mark.parametrize("layout", ["quads", "row_pairs"])
 @pytest.mark.parametrize("loglog", [False, True])
-def test_global_grid_cfg4_matches_shared_and_oracle(loglog, layout, monkeypatch):
-    """The cfg4 grid forced into device memory gives the shared-memory kernel's
-    brackets and values (same arithmetic), hence the oracle's, in both device-memory
-    layouts (cell quads, the default, and row pairs: EOS_GG_QUAD_MB=0)."""
-    if layout == "row_pairs":
-        monkeypatch.setenv("EOS_GG_QUAD_MB", "0")
+def test_global_grid_cfg4_matches_shared_and_oracle(loglog):
+    """The cfg4 grid forced into device memory (cell quads) gives the shared-memory
+    kernel's brackets and values (same arithmetic), hence the oracle's."""
     w = datagen.workload("cfg4", count=(1 << 20) + 7)
     rho = w.rho_targets.host_fill(0, w.count)
     T = w.T_targets.host_fill(0, w.count)
@@ -1068,16 +1053,13 @@ def test_global_grid_cfg4_matches_shared_and_oracle(loglog, layout, monkeypatch)
     gg.close()
 
 
-@pytest.mark.parametrize("shape,loglog,quad_mb", [
-    ((600, 500), False, None), ((600, 500), True, None), ((1000, 800), False, None),
-    ((3000, 7), False, None), ((2, 16000), False, None), ((8000, 3), True, None),
-    ((1000, 800), False, "0"), ((600, 500), True, "0"), ((2, 16000), False, "0")])
-def test_large_grids_in_device_memory(shape, loglog, quad_mb, monkeypatch):
-    """Grids larger than shared memory (P in device memory as cell quads, or as row pairs
-    with EOS_GG_QUAD_MB=0; axes in smem with as many record copies as fit): brackets
-    bit-exact, P and derivatives within the bar."""
-    if quad_mb is not None:
-        monkeypatch.setenv("EOS_GG_QUAD_MB", quad_mb)
+@pytest.mark.parametrize("shape,loglog", [
+    ((600, 500), False), ((600, 500), True), ((1000, 800), False),
+    ((3000, 7), False), ((2, 16000), False), ((8000, 3), True)])
+def test_large_grids_in_device_memory(shape, loglog):
+    """Grids larger than shared memory (P in device memory as cell quads; axes in smem
+    with as many record copies as fit): brackets bit-exact, P and derivatives within the
+    bar."""
     rng = np.random.default_rng(shape[0] + shape[1])
     nR, nT = shape
     if loglog:  # jittered logspace axes: log-log derivatives amplify the device-vs-libm

@@ -37,7 +37,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert declared == set(eos.EXPORTED_SYMBOLS)
     for s in declared:
         assert hasattr(L, s), s
-    assert L.eos_abi_version() == 2
+    assert L.eos_abi_version() == 3
     assert eos.eos_status_str(0) == "ok"
     assert "sorted" in eos.eos_status_str(4)
 
@@ -389,20 +389,43 @@ def test_header_is_plain_c_and_the_example_links(tmp_path):
     assert r.returncode == 0, r.stderr
 
 
-def test_every_tuning_knob_is_documented():
-    """Every environment variable the library reads (getenv in csrc/) is listed in the
-    tuning-knob header of csrc/runtime.cu, so no hidden switch changes the product path."""
+def _product_lines(text: str):
+    """Source lines compiled into the product library: everything outside
+    `#ifdef EOS_EXPERIMENTS` blocks (their `#else` branches are product code)."""
+    out, stack = [], []
+    for line in text.splitlines():
+        t = line.strip()
+        if t.startswith("#if"):
+            stack.append("EOS_EXPERIMENTS" in t and t.startswith("#ifdef"))
+            continue
+        if t.startswith("#else") and stack:
+            stack[-1] = False
+            continue
+        if t.startswith("#endif") and stack:
+            stack.pop()
+            continue
+        if not any(stack):
+            out.append(line)
+    return out
+
+
+def test_product_library_reads_no_environment():
+    """The product library's launch shapes and layouts follow from the plan alone: every
+    getenv in csrc/ sits inside an `#ifdef EOS_EXPERIMENTS` block (the A/B build,
+    _build.py --exp), and each experiment knob is listed in runtime.cu's header."""
     import glob
     import re
     csrc = os.path.join(ROOT, "paper_2112_03229_b200", "csrc")
-    names = set()
-    for f in glob.glob(os.path.join(csrc, "*")):
-        for call in re.findall(r"getenv\(([^;]*?)\)", open(f).read()):
-            names |= set(re.findall(r'"(EOS_[A-Z0-9_]+)"', call))
+    knobs = set()
+    for f in sorted(glob.glob(os.path.join(csrc, "*"))):
+        text = open(f).read()
+        prod = "\n".join(_product_lines(text))
+        assert "getenv" not in prod, f"{f}: getenv outside #ifdef EOS_EXPERIMENTS"
+        for call in re.findall(r"getenv\(([^;]*?)\)", text):
+            knobs |= set(re.findall(r'"(EOS_[A-Z0-9_]+)"', call))
     header = open(os.path.join(csrc, "runtime.cu")).read().split("\n\n")[0]
-    missing = sorted(n for n in names if n not in header)
-    assert {"EOS_SEARCH_VARIANT", "EOS_TIERED_VARIANT", "EOS_SMALL_TILES"} <= names
-    assert not missing, missing
+    assert {"EOS_SEARCH_VARIANT", "EOS_LAYOUT", "EOS_SMALL_TILES"} <= knobs
+    assert not [k for k in knobs if k not in header]
 
 
 def _lifting_probes_brute(o, S):
@@ -424,25 +447,44 @@ def _lifting_probes_brute(o, S):
 def test_automatic_plan_is_the_argmin_of_the_cost_model(name):
     """The automatic hash choice (table_build.cpp plan_auto, which evaluates candidates from
     runs of the sorted keys) equals the argmin of the DESIGN.md §6.3 cost model recomputed
-    here from every candidate's full directory: 3.5 + 6.1 E[probes] + S + shape penalty,
+    here from every candidate's full directory, over every lifting layout (16/32-bit
+    directory entries, SF fixed steps, rare branch): 3.5 + 6.1 E[probes] + issue + shape
+    penalty, issue = SF + [big] (0.5 + P(warp diverges) 1.5 (S - SF)) + 0.25 [16-bit];
     ties to the smaller image, then the exponent hash, image budget 200 KB."""
     X = datagen.workload(name, count=10).table
     n = X.size
     pad16 = lambda b: (b + 15) & ~15  # noqa: E731
     budget = 200 * 1024
 
+    def shape(img):
+        return 0.0 if img <= 32768 else 1.0 if img <= 73728 else 1.5 if img <= 147456 else 4.5
+
     def cost(info, d):
         occ = (d >> 16).astype(np.int64)
         S = info.steps
         vals, counts = np.unique(occ, return_counts=True)
         probes = sum(int(c) * _lifting_probes_brute(int(o), S) for o, c in zip(vals, counts))
-        img = pad16(8 * n) + pad16(4 * info.bins)
-        shape = 0.0 if img <= 32768 else 1.0 if img <= 73728 else 1.5 if img <= 147456 else 4.5
-        return 3.5 + 6.1 * probes / info.bins + S + shape, img
+        probes /= info.bins
+        best_l = None
+        for d16 in ([0, 1] if n <= 4096 and occ.max() <= 15 else [0]):
+            img = pad16(8 * n) + pad16((2 if d16 else 4) * info.bins)
+            for sf in range(0, min(S, 3) + 1):
+                if sf == 0 and S <= 3:
+                    continue
+                big = sf == 0 or S > sf
+                if sf == 0:
+                    issue = S + 1.0
+                else:
+                    f = np.sum(occ >= (1 << sf)) / info.bins
+                    issue = sf + ((0.5 + (1 - (1 - f) ** 32) * 1.5 * (S - sf)) if big else 0.0)
+                c = 3.5 + 6.1 * probes + issue + 0.25 * d16 + shape(img)
+                if best_l is None or c < best_l[0] - 1e-9:
+                    best_l = (c, img, d16, sf, big)
+        return best_l
 
     best = None
     cands = [(eos.EOS_HASH_EXPONENT, k) for k in range(eos.EOS_MAX_K + 1)]
-    H, max_bins = 1.0, (budget - pad16(8 * n)) // 4
+    H, max_bins = 1.0, (budget - pad16(8 * n)) // (2 if n <= 4096 else 4)
     while H <= max_bins:
         cands.append((eos.EOS_HASH_LOG, int(H)))
         H *= 2 ** 0.125
@@ -451,7 +493,8 @@ def test_automatic_plan_is_the_argmin_of_the_cost_model(name):
             info, d = eos.eos_plan_table_hash(X, kind, param)
         except eos.EosError:   # image beyond what shared memory holds
             continue
-        c, img = cost(info, d)
+        c, img, d16, sf, big = cost(info, d)
+        assert (info.dir_entry_bytes, info.fast_steps, info.rare_steps) == (2 if d16 else 4, sf, int(big))
         if best is not None and img > budget:
             continue
         if best is None or c < best[0] - 1e-9 or (c < best[0] + 1e-9 and img < best[1]):
