@@ -117,6 +117,11 @@ void oracle_interp2d_deriv(const double* R, int64_t nR, const double* Tax, int64
  *   tx = clamp01((ln rho - ln R[ci]) / (ln R[ci+1] - ln R[ci])), ty likewise
  *   P  = exp((1-tx)((1-ty) ln G[ci][cj] + ty ln G[ci][cj+1])
  *            + tx ((1-ty) ln G[ci+1][cj] + ty ln G[ci+1][cj+1]))
+ * The log differences are evaluated as ln(a) - ln(b) = log1p((a - b) / b),
+ * the same real number (R24): written as a difference of two logs, fp64
+ * loses ~|ln a| / (ln a - ln b) ulps of the weight to cancellation on narrow
+ * cells, which the weight's error then carries into P (pinned against
+ * 40-digit decimal logarithms in tests/test_oracle.py).
  * Requires R, T, G > 0.  Exact for power laws G = C rho^a T^b.  Derivatives
  * (NULL-able): dP/drho = P * s_rho / rho with s_rho the cell slope of ln P in
  * ln rho, 0 outside the axis range, NaN for NaN; likewise dP/dT. */
@@ -128,10 +133,10 @@ void oracle_interp2d_loglog(const double* R, int64_t nR, const double* Tax, int6
     int32_t j = oracle_lower_bound(Tax, nT, T[q]);
     int64_t ci = i < nR - 2 ? i : nR - 2;
     int64_t cj = j < nT - 2 ? j : nT - 2;
-    double lr0 = log(R[ci]), lr1 = log(R[ci + 1]);
-    double lt0 = log(Tax[cj]), lt1 = log(Tax[cj + 1]);
-    double tx = clamp01((log(rho[q]) - lr0) / (lr1 - lr0));
-    double ty = clamp01((log(T[q]) - lt0) / (lt1 - lt0));
+    double wr = log1p((R[ci + 1] - R[ci]) / R[ci]);    /* ln R[ci+1] - ln R[ci] */
+    double wt = log1p((Tax[cj + 1] - Tax[cj]) / Tax[cj]);
+    double tx = clamp01(log1p((rho[q] - R[ci]) / R[ci]) / wr);  /* (ln rho - ln R[ci]) / wr */
+    double ty = clamp01(log1p((T[q] - Tax[cj]) / Tax[cj]) / wt);
     double l00 = log(G[ci * nT + cj]), l01 = log(G[ci * nT + cj + 1]);
     double l10 = log(G[(ci + 1) * nT + cj]), l11 = log(G[(ci + 1) * nT + cj + 1]);
     double lp = (1.0 - tx) * ((1.0 - ty) * l00 + ty * l01) + tx * ((1.0 - ty) * l10 + ty * l11);
@@ -139,8 +144,8 @@ void oracle_interp2d_loglog(const double* R, int64_t nR, const double* Tax, int6
     P[q] = p;
     if (iR) iR[q] = i;
     if (iT) iT[q] = j;
-    double sr = ((1.0 - ty) * (l10 - l00) + ty * (l11 - l01)) / (lr1 - lr0);
-    double st = ((1.0 - tx) * (l01 - l00) + tx * (l11 - l10)) / (lt1 - lt0);
+    double sr = ((1.0 - ty) * (l10 - l00) + ty * (l11 - l01)) / wr;
+    double st = ((1.0 - tx) * (l01 - l00) + tx * (l11 - l10)) / wt;
     int in_r = rho[q] >= R[0] && rho[q] <= R[nR - 1];
     int in_t = T[q] >= Tax[0] && T[q] <= Tax[nT - 1];
     if (dPdrho) dPdrho[q] = (rho[q] != rho[q]) ? rho[q] : (in_r ? p * sr / rho[q] : 0.0);

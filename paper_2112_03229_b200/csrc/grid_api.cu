@@ -40,7 +40,6 @@ struct eos_grid2d_s {
   int grid_small = 0, grid_small_deriv = 0, threads_small = 0;
   int64_t small_image_bytes = 0;  // the image without G (g_off)
   int32_t flags = 0;
-  int32_t lr_off = 0, lt_off = 0;
   int32_t rr_off = 0, rt_off = 0;
   int rep = 0;  // 2: bank-pinned cell records in the image (REP kernels), 0: plain axes
   int32_t rep_shift = 0;       // REP 2: log2 of the record copies
@@ -68,7 +67,7 @@ InterpKernel interp_fn(bool deriv) {
   if (deriv)
     return {(const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, true, LOGLOG, REP, GG>,
             dv::Shape2DDeriv::kThreads};
-  if constexpr (S == 1)
+  if constexpr (S == 1 && !(LOGLOG && REP == 0))  // (plain log-log axes: 2 log1p per axis)
     return {(const void*)dv::interp2d_kernel<S, dv::Shape2D, false, LOGLOG, REP, GG>,
             dv::Shape2D::kThreads};
   else
@@ -135,8 +134,6 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   a.image = (const uint4*)g->image_dev;
   a.image_16 = (int32_t)(g->image_bytes / 16);
   a.g_off = g->g_off;
-  a.lr_off = g->lr_off;
-  a.lt_off = g->lt_off;
   a.rr_off = g->rr_off;
   a.rt_off = g->rt_off;
   a.gq = reinterpret_cast<const double2*>(g->grid_dev);
@@ -221,13 +218,11 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     for (int64_t q = 0; q < ncell && ok; ++q) ok = P_host[q] > 0.0;
     if (!ok) return fail(EOS_ERR_UNSUPPORTED);
   }
-  // image: [rho X | rho dir][T X | T dir][ln R][ln T][R recs][T recs][G]
+  // image: [rho X | rho dir][T X | T dir][R recs][T recs][G]
   // G is absent for grids in device memory (GG: larger than ~220 KB, or
   // EOS_GRID_GLOBAL), which keep it in g->grid_dev instead (cell quads or row pairs).
   int64_t r_bytes = g->pr.image_bytes, t_bytes = g->pt.image_bytes;
-  const int64_t lr_bytes = loglog ? (8 * n_rho + 15) & ~int64_t(15) : 0;
-  const int64_t lt_bytes = loglog ? (8 * n_T + 15) & ~int64_t(15) : 0;
-  const int64_t axes_bytes = r_bytes + t_bytes + lr_bytes + lt_bytes;
+  const int64_t axes_bytes = r_bytes + t_bytes;
   const int64_t smem_grid_bytes = (8 * ncell + 15) & ~int64_t(15);
   g->gg = (flags & EOS_GRID_GLOBAL) != 0 || axes_bytes + smem_grid_bytes > 220 * 1024;
   const int64_t g_bytes = g->gg ? 0 : smem_grid_bytes;
@@ -283,21 +278,20 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   memcpy(img.data() + r_bytes, it.data(), it.size());
   // G last: the image without it (the first g_off bytes) serves the small-launch
   // kernels, which read the corners from cell quads in device memory
-  g->lr_off = (int32_t)(r_bytes + t_bytes);
-  g->lt_off = (int32_t)(g->lr_off + lr_bytes);
-  g->rr_off = (int32_t)(g->lt_off + lt_bytes);
+  g->rr_off = (int32_t)(r_bytes + t_bytes);
   g->rt_off = (int32_t)(g->rr_off + (g->rep ? g->rep_bytes_axis * n_rho : 0));
   g->g_off = (int32_t)(g->rt_off + (g->rep ? g->rep_bytes_axis * n_T : 0));
   if (g->g_off + g_bytes != g->image_bytes) return fail(EOS_ERR_CUDA);  // layout invariant
-  auto put_rep = [&](const std::vector<double>& Xa, int32_t off) {
-    std::vector<double> X(Xa);
-    if (loglog)  // records of the log axis (the same host log as the ln R / ln T arrays)
-      for (double& v : X) v = log(v);
+  auto put_rep = [&](const std::vector<double>& X, int32_t off) {
     const int64_t n = (int64_t)X.size();
     for (int64_t q = 0; q < n; ++q) {
-      // Rec[C q + c] = (X[q], 1/(X[q+1] - X[q])), C = 2^rep_shift copies; the
-      // last record's width is unused
-      const double rec[2] = {X[q], q + 1 < n ? 1.0 / (X[q + 1] - X[q]) : 0.0};
+      // Rec[C q + c] = (X[q], 1/(X[q+1] - X[q])), or for log-log grids
+      // (1/X[q], 1/ln(X[q+1]/X[q])) with ln(X[q+1]/X[q]) = log1p((X[q+1] - X[q])/X[q])
+      // (R24); C = 2^rep_shift copies; the last record's width is unused
+      const bool last = q + 1 >= n;
+      const double rec[2] = {
+          loglog ? 1.0 / X[q] : X[q],
+          last ? 0.0 : (loglog ? 1.0 / log1p((X[q + 1] - X[q]) / X[q]) : 1.0 / (X[q + 1] - X[q]))};
       const int C = 1 << g->rep_shift;
       for (int c = 0; c < C; ++c) memcpy(img.data() + off + 16 * (C * q + c), rec, 16);
     }
@@ -312,16 +306,6 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     for (int64_t q = 0; q < ncell; ++q) {
       const double v = gval(q);
       memcpy(img.data() + g->g_off + 8 * q, &v, 8);
-    }
-  }
-  if (loglog) {  // ln of the axes
-    for (int64_t q = 0; q < n_rho; ++q) {
-      const double v = log(g->pr.X[q]);
-      memcpy(img.data() + g->lr_off + 8 * q, &v, 8);
-    }
-    for (int64_t q = 0; q < n_T; ++q) {
-      const double v = log(g->pt.X[q]);
-      memcpy(img.data() + g->lt_off + 8 * q, &v, 8);
     }
   }
   g->ar = axis_params(g->pr, 0);

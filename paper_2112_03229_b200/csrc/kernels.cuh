@@ -178,11 +178,12 @@ __device__ __forceinline__ void lift_step_rt(double y, uint32_t& pa, int32_t& r,
       : "d"(y), "r"(s));
 }
 
+// strides 2^(S-1) .. 1; only the stride-1 step (the last) skips the r update
 template <int S>
 __device__ __forceinline__ void lift_fixed(double y, uint32_t& pa, int32_t& r) {
-  if (S >= 4) lift_step<8, S == 4>(y, pa, r);
-  if (S >= 3) lift_step<4, S == 3>(y, pa, r);
-  if (S >= 2) lift_step<2, S == 2>(y, pa, r);
+  if (S >= 4) lift_step<8, false>(y, pa, r);
+  if (S >= 3) lift_step<4, false>(y, pa, r);
+  if (S >= 2) lift_step<2, false>(y, pa, r);
   if (S >= 1) lift_step<1, true>(y, pa, r);
 }
 
@@ -909,10 +910,9 @@ struct Interp2DArgs {
   const uint4* image;
   int32_t image_16;
   int32_t g_off;    // byte offset of G fp64[nR*nT] in the image
-  int32_t lr_off;   // byte offset of ln R fp64[nR] (LOGLOG grids)
-  int32_t lt_off;   // byte offset of ln T fp64[nT] (LOGLOG grids)
   int32_t rr_off;   // byte offset of the bank-pinned cell records of the R axis (REP 2
-                    //   kernels): double2[2^rep_shift nR], (R[j], 1/(R[j+1]-R[j]))
+                    //   kernels): double2[2^rep_shift nR], (R[j], 1/(R[j+1]-R[j])), or
+                    //   for LOGLOG grids (1/R[j], 1/ln(R[j+1]/R[j]))
   int32_t rt_off;   // the same for the T axis
   int32_t rep_shift;  // REP 2: log2 of the record copies per axis entry (3: 8 copies, the
                       //   conflict-free layout; fewer when smem is short: 2-way .. 8-way)
@@ -1028,50 +1028,45 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   const double* sG = reinterpret_cast<const double*>(sm + A.g_off);  // G, or ln G (LOGLOG)
   int32_t ci, cj;
   double r0, r1, t0, t1;
-  double ir = 0.0, it = 0.0;  // REP 2: inverse cell widths
-  if (REP == 2 && LOGLOG) {
-    // brackets from the plain axes; the cell records hold the log axes:
-    // (ln X[j], 1/(ln X[j+1] - ln X[j]))
+  double ir = 0.0, it = 0.0;  // REP 2: inverse cell widths (in x, or in ln x for LOGLOG)
+  double wr = 0.0, wt = 0.0;  // REP 0: cell widths (in x, or in ln x for LOGLOG)
+  double tx, ty;              // the bilinear weights
+  if (LOGLOG) {
+    // R24: t = (ln x - ln X[c]) / (ln X[c+1] - ln X[c]), evaluated as
+    // log1p((x - X[c]) / X[c]) / log1p((X[c+1] - X[c]) / X[c]) -- the same real
+    // numbers, without the cancellation of ln x - ln X[c] (which loses
+    // ~|ln x| / (cell width in ln) ulps).  Brackets and X[c] from the plain axes.
     axis_cell<S>(rho, sR, dR, A.r, i, ci, r0, r1);
     axis_cell<S>(T, sT, dT, A.t, j, cj, t0, t1);
-    const int32_t sh = A.rep_shift, c = threadIdx.x & ((1 << sh) - 1);
-    const double2 er = reinterpret_cast<const double2*>(sm + A.rr_off)[(ci << sh) + c];
-    const double2 et = reinterpret_cast<const double2*>(sm + A.rt_off)[(cj << sh) + c];
-    r0 = er.x;
-    ir = er.y;
-    t0 = et.x;
-    it = et.y;
+    if (REP == 2) {  // records (1/X[j], 1/ln(X[j+1]/X[j])): no divides
+      const int32_t sh = A.rep_shift, c = threadIdx.x & ((1 << sh) - 1);
+      const double2 er = reinterpret_cast<const double2*>(sm + A.rr_off)[(ci << sh) + c];
+      const double2 et = reinterpret_cast<const double2*>(sm + A.rt_off)[(cj << sh) + c];
+      ir = er.y;
+      it = et.y;
+      tx = clamp01(__dmul_rn(log1p(__dmul_rn(__dsub_rn(rho, r0), er.x)), ir));
+      ty = clamp01(__dmul_rn(log1p(__dmul_rn(__dsub_rn(T, t0), et.x)), it));
+    } else {
+      wr = log1p(__ddiv_rn(__dsub_rn(r1, r0), r0));
+      wt = log1p(__ddiv_rn(__dsub_rn(t1, t0), t0));
+      tx = clamp01(__ddiv_rn(log1p(__ddiv_rn(__dsub_rn(rho, r0), r0)), wr));
+      ty = clamp01(__ddiv_rn(log1p(__ddiv_rn(__dsub_rn(T, t0), t0)), wt));
+    }
   } else if (REP == 2) {
     const int32_t sh = A.rep_shift, c = threadIdx.x & ((1 << sh) - 1);  // this lane's copy
     axis_cell_rec<S>(rho, sR, dR, A.r, i, ci, r0, ir,
                      reinterpret_cast<const double2*>(sm + A.rr_off) + c, sh);
     axis_cell_rec<S>(T, sT, dT, A.t, j, cj, t0, it,
                      reinterpret_cast<const double2*>(sm + A.rt_off) + c, sh);
-    r1 = t1 = 0.0;  // unused
+    tx = clamp01(__dmul_rn(__dsub_rn(rho, r0), ir));
+    ty = clamp01(__dmul_rn(__dsub_rn(T, t0), it));
   } else {
     axis_cell<S>(rho, sR, dR, A.r, i, ci, r0, r1);
     axis_cell<S>(T, sT, dT, A.t, j, cj, t0, t1);
-  }
-  double xr = rho, xt = T;  // interpolation coordinates
-  if (LOGLOG) {             // R24: ln P bilinear in (ln rho, ln T)
-    if (REP != 2) {
-      const double* lR = reinterpret_cast<const double*>(sm + A.lr_off);
-      const double* lT = reinterpret_cast<const double*>(sm + A.lt_off);
-      r0 = lR[ci];
-      r1 = lR[ci + 1];
-      t0 = lT[cj];
-      t1 = lT[cj + 1];
-    }
-    xr = log(rho);
-    xt = log(T);
-  }
-  double tx, ty;
-  if (REP == 2) {
-    tx = clamp01(__dmul_rn(__dsub_rn(xr, r0), ir));
-    ty = clamp01(__dmul_rn(__dsub_rn(xt, t0), it));
-  } else {
-    tx = clamp01(__ddiv_rn(__dsub_rn(xr, r0), __dsub_rn(r1, r0)));
-    ty = clamp01(__ddiv_rn(__dsub_rn(xt, t0), __dsub_rn(t1, t0)));
+    wr = __dsub_rn(r1, r0);
+    wt = __dsub_rn(t1, t0);
+    tx = clamp01(__ddiv_rn(__dsub_rn(rho, r0), wr));
+    ty = clamp01(__ddiv_rn(__dsub_rn(T, t0), wt));
   }
   EOS_DCHECK(ci >= 0 && cj >= 0 && ci + 1 < A.r.n && cj + 1 < A.t.n);
   double g00, g01, g10, g11;
@@ -1100,8 +1095,8 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
     // kept.  LOGLOG: dP/drho = P * (d ln P / d ln rho) / rho.
     const double nr = __dadd_rn(__dmul_rn(uy, __dsub_rn(g10, g00)), __dmul_rn(ty, __dsub_rn(g11, g01)));
     const double nt = __dadd_rn(__dmul_rn(ux, __dsub_rn(g01, g00)), __dmul_rn(tx, __dsub_rn(g11, g10)));
-    const double sr = REP == 2 ? __dmul_rn(nr, ir) : __ddiv_rn(nr, __dsub_rn(r1, r0));
-    const double st = REP == 2 ? __dmul_rn(nt, it) : __ddiv_rn(nt, __dsub_rn(t1, t0));
+    const double sr = REP == 2 ? __dmul_rn(nr, ir) : __ddiv_rn(nr, wr);
+    const double st = REP == 2 ? __dmul_rn(nt, it) : __ddiv_rn(nt, wt);
     const bool in_r = rho >= A.r.x0 && rho <= A.r.xlast;
     const bool in_t = T >= A.t.x0 && T <= A.t.xlast;
     const double dr = LOGLOG ? __ddiv_rn(__dmul_rn(p, sr), rho) : sr;

@@ -184,14 +184,15 @@ double cost_of(double mean_probes, double issue, int64_t image_bytes) {
   return 3.5 + 6.1 * mean_probes + issue + shape_cost(image_bytes);
 }
 
-// Layout of a search table's lifting (kernels.cuh lookup_b): SF fixed steps
-// cover bins of < 2^SF entries; deeper bins (big) run their larger strides in
-// a branch that a warp takes when any of its 32 lanes lands in one.  Issue
-// cost, in the units of cost_of (one per fixed step): SF, plus for big 0.5
-// (the test) + P(warp diverges) x 1.5 per extra step; SF = 0 (all strides in
-// a runtime loop): S + 1.  A 16-bit directory costs 0.25 (one more unpack
-// instruction) and halves the directory's shared memory.
-
+// Layout of a search table's lifting (kernels.cuh lookup_b): S <= 3 runs all
+// S steps as fixed, branch-free steps (SF = S); deeper tables run 3 fixed steps
+// after a branch for their larger strides (big).  (A rare branch in front of
+// fewer fixed steps -- SF < S for S <= 3 -- was measured 3-10% slower on cfg5
+// in spite of 30% fewer instructions: each branch is a reconvergence point, so
+// the 8 lookups of a thread no longer overlap their shared-memory latencies;
+// DESIGN.md §12.)  16-bit directory entries (n <= 4096, occupancy <= 15) are
+// taken when their smaller image is cheaper (cost_of shape term) despite the
+// extra unpack instruction (0.25).
 Layout choose_layout(const std::vector<int64_t>& runs, int64_t n, int64_t bins, int steps,
                      double probes_per_bin, bool search) {
   Layout best;
@@ -202,32 +203,19 @@ Layout choose_layout(const std::vector<int64_t>& runs, int64_t n, int64_t bins, 
   int64_t mx = 0;
   for (const int64_t r : runs) mx = std::max(mx, r);
   const bool can16 = n <= kDir16MaxN && mx <= kDir16MaxOcc;
-  bool have = false;
-  for (int d16 = 0; d16 <= (can16 ? 1 : 0); ++d16) {
-    const int64_t img = image_of(n, bins, d16 != 0);
-    for (int sf = 0; sf <= std::min(steps, kMaxFastSteps); ++sf) {
-      if (sf == 0 && steps <= kMaxFastSteps) continue;  // the runtime loop only for deep tables
-      const bool big = sf == 0 || steps > sf;
-      double issue;
-      if (sf == 0) {
-        issue = steps + 1.0;
-      } else {
-        int64_t nbig = 0;
-        for (const int64_t r : runs) nbig += r >= (int64_t(1) << sf);
-        const double f = (double)nbig / (double)bins;
-        const double pw = 1.0 - pow(1.0 - f, 32.0);
-        issue = sf + (big ? 0.5 + pw * 1.5 * (steps - sf) : 0.0);
-      }
-      issue += d16 ? 0.25 : 0.0;
-      const double c = cost_of(probes_per_bin, issue, img);
-      if (!have || c < best.cost - 1e-9) {
-        best.dir16 = d16 != 0;
-        best.sf = sf;
-        best.big = big;
-        best.image = img;
-        best.cost = c;
-        have = true;
-      }
+  const int sf = std::min(steps, kMaxFastSteps);
+  const bool big = steps > sf;
+  const double issue = steps + (big ? 1.0 : 0.0);  // the deep strides' loop and branch
+  best.sf = sf;
+  best.big = big;
+  best.cost = cost_of(probes_per_bin, issue, best.image);
+  if (can16) {
+    const int64_t img = image_of(n, bins, true);
+    const double c = cost_of(probes_per_bin, issue + 0.25, img);
+    if (c < best.cost - 1e-9) {
+      best.dir16 = true;
+      best.image = img;
+      best.cost = c;
     }
   }
   return best;

@@ -449,7 +449,7 @@ def test_automatic_plan_is_the_argmin_of_the_cost_model(name):
     runs of the sorted keys) equals the argmin of the DESIGN.md §6.3 cost model recomputed
     here from every candidate's full directory, over every lifting layout (16/32-bit
     directory entries, SF fixed steps, rare branch): 3.5 + 6.1 E[probes] + issue + shape
-    penalty, issue = SF + [big] (0.5 + P(warp diverges) 1.5 (S - SF)) + 0.25 [16-bit];
+    penalty, issue = S + [S > 3] + 0.25 [16-bit entries], SF = min(S, 3);
     ties to the smaller image, then the exponent hash, image budget 200 KB."""
     X = datagen.workload(name, count=10).table
     n = X.size
@@ -465,21 +465,16 @@ def test_automatic_plan_is_the_argmin_of_the_cost_model(name):
         vals, counts = np.unique(occ, return_counts=True)
         probes = sum(int(c) * _lifting_probes_brute(int(o), S) for o, c in zip(vals, counts))
         probes /= info.bins
-        best_l = None
-        for d16 in ([0, 1] if n <= 4096 and occ.max() <= 15 else [0]):
-            img = pad16(8 * n) + pad16((2 if d16 else 4) * info.bins)
-            for sf in range(0, min(S, 3) + 1):
-                if sf == 0 and S <= 3:
-                    continue
-                big = sf == 0 or S > sf
-                if sf == 0:
-                    issue = S + 1.0
-                else:
-                    f = np.sum(occ >= (1 << sf)) / info.bins
-                    issue = sf + ((0.5 + (1 - (1 - f) ** 32) * 1.5 * (S - sf)) if big else 0.0)
-                c = 3.5 + 6.1 * probes + issue + 0.25 * d16 + shape(img)
-                if best_l is None or c < best_l[0] - 1e-9:
-                    best_l = (c, img, d16, sf, big)
+        sf = min(S, 3)
+        big = S > sf
+        issue = S + (1.0 if big else 0.0)
+        img32 = pad16(8 * n) + pad16(4 * info.bins)
+        best_l = (3.5 + 6.1 * probes + issue + shape(img32), img32, 0, sf, big)
+        if n <= 4096 and occ.max() <= 15:
+            img16 = pad16(8 * n) + pad16(2 * info.bins)
+            c16 = 3.5 + 6.1 * probes + issue + 0.25 + shape(img16)
+            if c16 < best_l[0] - 1e-9:
+                best_l = (c16, img16, 1, sf, big)
         return best_l
 
     best = None

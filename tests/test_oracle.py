@@ -246,11 +246,12 @@ def test_counter_c2_distinguishes_position_and_index_at_large_n():
     """R25: c2's term mix64(mix64(pos) ^ idx) differs for different indices at the same
     position, also past 2^20 entries and positions (the round-1 packing (pos << 20) | idx
     aliased there)."""
-    X = np.array([1.0, 2.0])
+    X = np.arange((1 << 21) + 2, dtype=np.float64)   # indices up to 2^21 are valid
     pos = (1 << 33) + 5
-    a = oracle.counters(X, np.array([1.5]), np.array([1 << 21], np.int32), pos)[2]
-    b = oracle.counters(X, np.array([1.5]), np.array([0], np.int32), pos)[2]
-    c = oracle.counters(X, np.array([1.5]), np.array([0], np.int32), pos + (1 << 1))[2]
+    y = np.array([1.5])
+    a = oracle.counters(X, y, np.array([1 << 21], np.int32), pos)[2]
+    b = oracle.counters(X, y, np.array([0], np.int32), pos)[2]
+    c = oracle.counters(X, y, np.array([0], np.int32), pos + (1 << 1))[2]
     assert len({int(a), int(b), int(c)}) == 3
     assert int(b) == oracle.mix64(oracle.mix64(pos) ^ 0)
 
@@ -362,3 +363,61 @@ def test_loglog_nodes_outside_and_nan():
     assert dr[0] == 0.0 and dr[1] == 0.0
     assert np.isnan(P[2]) and np.isnan(dr[2]) and np.isnan(P[3]) and np.isnan(dt[3])
     assert np.isnan(P[4])                                         # ln of a negative density
+
+
+def _loglog_decimal(R, T, G, rho, t, digits=40):
+    """R24 evaluated with 40-digit decimal logarithms and exponentials (Python's decimal
+    module: ln/exp correctly rounded at the context precision), brackets from bisect.
+    Returns P and dP/drho as Python floats."""
+    import bisect
+    from decimal import Decimal, localcontext
+    out_p, out_d = [], []
+    with localcontext() as ctx:
+        ctx.prec = digits
+        D = Decimal
+        for x, y in zip(rho, t):
+            i = max(bisect.bisect_right(list(R), x) - 1, 0)
+            j = max(bisect.bisect_right(list(T), y) - 1, 0)
+            ci, cj = min(i, len(R) - 2), min(j, len(T) - 2)
+            lr0, lr1 = D(R[ci]).ln(), D(R[ci + 1]).ln()
+            lt0, lt1 = D(T[cj]).ln(), D(T[cj + 1]).ln()
+            tx = min(max((D(x).ln() - lr0) / (lr1 - lr0), D(0)), D(1))
+            ty = min(max((D(y).ln() - lt0) / (lt1 - lt0), D(0)), D(1))
+            l00, l01 = D(G[ci][cj]).ln(), D(G[ci][cj + 1]).ln()
+            l10, l11 = D(G[ci + 1][cj]).ln(), D(G[ci + 1][cj + 1]).ln()
+            lp = (1 - tx) * ((1 - ty) * l00 + ty * l01) + tx * ((1 - ty) * l10 + ty * l11)
+            p = lp.exp()
+            sr = ((1 - ty) * (l10 - l00) + ty * (l11 - l01)) / (lr1 - lr0)
+            out_p.append(float(p))
+            out_d.append(float(p * sr / D(x)))
+    return np.array(out_p), np.array(out_d)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_loglog_matches_40_digit_evaluation_on_narrow_cells_rough_surfaces(seed):
+    """R24 pinned against the formula evaluated with 40-digit logarithms: random rough
+    surfaces (ln G uniform over [-10, 10] per node, no smoothness) on axes with cells
+    1e-4 .. 1e-2 wide in ln.  The oracle's log1p form keeps P within 1e-13 relative;
+    the literal fp64 ln(rho) - ln(R) form loses ~|ln rho| / 1e-4 ulps of the weight
+    there, i.e. > 1e-12 of P (checked below, so the pin tells the two apart)."""
+    rng = np.random.default_rng(40 + seed)
+    def axis(a, n):
+        return np.exp(a + np.cumsum(np.concatenate([[0.0], 10 ** rng.uniform(-4, -2, n - 1)])))
+    R, T = axis(-12.0, 40), axis(14.0, 30)
+    G = np.exp(rng.uniform(-10, 10, (R.size, T.size)))
+    m = 400
+    rho = np.exp(rng.uniform(np.log(R[0]), np.log(R[-1]), m))
+    t = np.exp(rng.uniform(np.log(T[0]), np.log(T[-1]), m))
+    P, iR, iT, dr, dt = oracle.interp2d_loglog(R, T, G, rho, t)
+    Pd, drd = _loglog_decimal(R, T, G, rho, t)
+    assert np.max(np.abs(P / Pd - 1)) < 1e-13
+    assert np.max(np.abs(dr - drd) / np.abs(drd)) < 1e-11
+    # the literal difference-of-logs form in fp64, for contrast
+    ci = np.minimum(iR, R.size - 2)
+    cj = np.minimum(iT, T.size - 2)
+    tx = np.clip((np.log(rho) - np.log(R[ci])) / (np.log(R[ci + 1]) - np.log(R[ci])), 0, 1)
+    ty = np.clip((np.log(t) - np.log(T[cj])) / (np.log(T[cj + 1]) - np.log(T[cj])), 0, 1)
+    L = np.log(G)
+    lp = (1 - tx) * ((1 - ty) * L[ci, cj] + ty * L[ci, cj + 1]) + tx * ((1 - ty) * L[ci + 1, cj]
+                                                                     + ty * L[ci + 1, cj + 1])
+    assert np.max(np.abs(np.exp(lp) / Pd - 1)) > 1e-12
