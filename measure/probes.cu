@@ -89,6 +89,128 @@ __global__ void __launch_bounds__(T) k_stream2d(const double2* __restrict__ a,
   __stcs(i2 + i, make_int2(fold(z.x), fold(z.y)));
 }
 
+// shape C: persistent, 2U double2 per thread in flight (next tile loaded two ahead)
+template <int T, int U>
+__global__ void __launch_bounds__(T, 1) k_stream_persist2(const double2* __restrict__ y,
+                                                          int2* __restrict__ out, int64_t pairs) {
+  const int64_t tiles = pairs / ((int64_t)T * U);
+  double2 v[2][U];
+  int64_t t = blockIdx.x;
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+    if (t + b * gridDim.x < tiles) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[b][u] = ldcs2(y + (t + b * gridDim.x) * T * U + threadIdx.x + u * T);
+    }
+  int cur = 0;
+  while (t < tiles) {
+    const int64_t p0 = t * T * U + threadIdx.x;
+    int2 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = make_int2(fold(v[cur][u].x), fold(v[cur][u].y));
+    const int64_t tn = t + 2 * (int64_t)gridDim.x;
+    if (tn < tiles) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[cur][u] = ldcs2(y + tn * T * U + threadIdx.x + u * T);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) __stcs(out + p0 + u * T, r[u]);
+    t += gridDim.x;
+    cur ^= 1;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = tiles * T * U + threadIdx.x; i < pairs; i += T)
+      __stcs(out + i, make_int2(fold(y[i].x), fold(y[i].y)));
+}
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+                 "selp.b32 %0, 1, 0, P;\n\t}"
+                 : "=r"(ok) : "r"(s_u32(b)), "r"(parity) : "memory");
+  } while (!ok);
+}
+
+// shape D: persistent TMA ring.  One producer warp streams tiles (31 x 32 x 4 targets)
+// into NS shared-memory stages with cp.async.bulk (optionally with an L2 evict-first
+// hint); 31 consumer warps wait on the stage's full barrier, read their targets from
+// shared memory, store the int32 results with st.global.cs and release the stage.
+template <int NS, bool HINT>
+__global__ void __launch_bounds__(1024, 1) k_stream_tma(const double* __restrict__ y,
+                                                       int32_t* __restrict__ out, int64_t n) {
+  constexpr int CW = 31;
+  constexpr int PL = 4;                 // targets per lane per stage
+  constexpr int ST = CW * 32 * PL;      // targets per stage
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntiles = (n + ST - 1) / ST;
+  if (warp == CW) {
+    if (lane == 0) {
+      uint64_t pol = 0;
+      if (HINT) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      int k = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int s = k % NS;
+        if (k >= NS) bar_wait(&empty[s], ((k / NS) - 1) & 1);
+        const int64_t e0 = t * ST;
+        const uint32_t bytes = (uint32_t)(8 * min((int64_t)ST, n - e0));
+        bar_expect(&full[s], bytes);
+        if (HINT)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+              "[%0], [%1], %2, [%3], %4;" ::"r"(s_u32(ring + s * ST)), "l"(y + e0), "r"(bytes),
+              "r"(s_u32(&full[s])), "l"(pol) : "memory");
+        else
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              ::"r"(s_u32(ring + s * ST)), "l"(y + e0), "r"(bytes), "r"(s_u32(&full[s])) : "memory");
+      }
+    }
+    return;
+  }
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k % NS;
+    bar_wait(&full[s], (k / NS) & 1);
+    const double2* st = reinterpret_cast<const double2*>(ring + s * ST + warp * 32 * PL);
+    const double2 a = st[lane], b = st[32 + lane];
+    const int64_t e0 = t * ST + warp * 32 * PL;
+    int2* o = reinterpret_cast<int2*>(out + e0);
+    if (e0 + 32 * PL <= n) {
+      __stcs(o + lane, make_int2(fold(a.x), fold(a.y)));
+      __stcs(o + 32 + lane, make_int2(fold(b.x), fold(b.y)));
+    } else {
+      if (e0 + 2 * lane + 1 < n) __stcs(o + lane, make_int2(fold(a.x), fold(a.y)));
+      if (e0 + 64 + 2 * lane + 1 < n) __stcs(o + 32 + lane, make_int2(fold(b.x), fold(b.y)));
+    }
+    __syncwarp();
+    if (lane == 0) bar_arrive(&empty[s]);
+  }
+}
+
 __device__ __forceinline__ uint64_t smix(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
@@ -143,7 +265,7 @@ int sms() {
 extern "C" {
 
 // Number of 1-D stream shapes (variant 0 .. probe_stream_variants()-1).
-int probe_stream_variants(void) { return 4; }
+int probe_stream_variants(void) { return 9; }
 
 // One launch of the 1-D same-mix stream over n targets (n even, y 16-B and
 // out 8-B aligned).  Returns a cudaError_t.
@@ -166,9 +288,31 @@ int probe_stream(const double* y, int32_t* out, int64_t n, int variant, void* st
     case 2:
       k_stream_persist<1024, 4><<<sms(), 1024, 0, st>>>(y2, o2, pairs);
       break;
-    default:
+    case 3:
       k_stream_persist<512, 4><<<2 * sms(), 512, 0, st>>>(y2, o2, pairs);
       break;
+    case 4:
+      k_stream_persist<1024, 8><<<sms(), 1024, 0, st>>>(y2, o2, pairs);
+      break;
+    case 5:
+      k_stream_persist2<1024, 4><<<sms(), 1024, 0, st>>>(y2, o2, pairs);
+      break;
+    case 6:
+    case 7:
+    case 8: {  // TMA ring: 4 stages (127 KB), 4 stages + L2 evict-first, 6 stages (190 KB)
+      const int ns = variant == 8 ? 6 : 4;
+      const size_t smem = (size_t)ns * 31 * 32 * 4 * 8;
+      const void* fn = variant == 6 ? (const void*)k_stream_tma<4, false>
+                       : variant == 7 ? (const void*)k_stream_tma<4, true>
+                                      : (const void*)k_stream_tma<6, false>;
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (variant == 6) k_stream_tma<4, false><<<sms(), 1024, smem, st>>>(y, out, 2 * pairs);
+      else if (variant == 7) k_stream_tma<4, true><<<sms(), 1024, smem, st>>>(y, out, 2 * pairs);
+      else k_stream_tma<6, false><<<sms(), 1024, smem, st>>>(y, out, 2 * pairs);
+      break;
+    }
+    default:
+      return (int)cudaErrorInvalidValue;
   }
   return (int)cudaGetLastError();
 }

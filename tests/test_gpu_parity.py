@@ -679,9 +679,10 @@ def test_handles_sharing_a_kernel_do_not_interfere():
     rng = np.random.default_rng(3)
     Xb = np.logspace(-3, 3, 1000)
     Xs = np.logspace(-3, 3, 100)
-    big = eos.Table(Xb, log_bins=12000)        # S=1, ~56 KB image: 2 x 512 shape
-    small = eos.Table(Xs, log_bins=8300)       # S=1, ~34 KB image: same kernel instantiation
+    big = eos.Table(Xb, log_bins=30000)   # S=1, 16-bit directory, ~68 KB image: 2 x 512 shape
+    small = eos.Table(Xs, log_bins=30000)  # S=1, 16-bit directory, ~61 KB: same kernel instantiation
     assert big.info.steps == small.info.steps == 1
+    assert big.info.dir_entry_bytes == small.info.dir_entry_bytes == 2
     assert 32 * 1024 < small.info.image_bytes < big.info.image_bytes <= 72 * 1024
     Y = 10.0 ** rng.uniform(-4, 4, 100_003)
     yd = to_dev(Y)
