@@ -409,7 +409,7 @@ def plan_signature(a, obj, is2d):
     return {"kind": "tiered" if i.levels > 0 else ("direct" if a.direct else "search"),
             "hash_kind": i.hash_kind, "bins": i.bins, "steps": i.steps,
             "dir_entry_bytes": i.dir_entry_bytes, "fast_steps": i.fast_steps,
-            "rare_steps": i.rare_steps, "levels": i.levels}
+            "rare_steps": i.rare_steps, "levels": i.levels, "ring_stages": i.ring_stages}
 
 
 def run_e2e(a, d, w, obj, offset, count, total, is2d, dev):

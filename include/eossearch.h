@@ -92,11 +92,13 @@ typedef struct {
    * (lo | occ << 12) or 4 B (lo | occ << 16) in the image; fast_steps = the
    * fixed binary-lifting steps SF (0: all S steps in a runtime loop);
    * rare_steps = 1 if some bin holds >= 2^SF entries (its larger strides run
-   * in a branch taken only by lanes that land in such a bin). */
+   * in a branch taken only by lanes that land in such a bin); ring_stages =
+   * shared-memory stages of the streaming ring that large launches use (0:
+   * none; eos_table_info only). */
   int32_t dir_entry_bytes;
   int32_t fast_steps;
   int32_t rare_steps;
-  int32_t pad2_;
+  int32_t ring_stages;
 } eos_table_info_t;
 
 /* ---------------------------------------------------------------------------

@@ -211,6 +211,130 @@ __global__ void __launch_bounds__(1024, 1) k_stream_tma(const double* __restrict
   }
 }
 
+__device__ __forceinline__ void clc_cancel(uint4* resp, uint64_t* bar) {
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];"
+      ::"r"(s_u32(resp)), "r"(s_u32(bar)) : "memory");
+}
+__device__ __forceinline__ int64_t clc_get(const uint4* resp) {
+  uint32_t valid = 0, x = 0;
+  asm volatile(
+      "{\n\t.reg .b128 R;\n\t.reg .pred P;\n\t"
+      "ld.shared.b128 R, [%2];\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 P, R;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t"
+      "@P clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, R;\n\t}"
+      : "=r"(valid), "=r"(x) : "r"(s_u32(resp)) : "memory");
+  return valid ? (int64_t)x : -1;
+}
+
+// shape E: TMA ring whose producer takes tiles with cluster launch control: the grid
+// has one CTA per tile; a resident CTA's producer cancels not-yet-launched CTAs and
+// streams their tiles, so tiles are processed in launch order (a compact front).
+template <int NS>
+__global__ void __launch_bounds__(1024, 1) k_stream_tma_clc(const double* __restrict__ y,
+                                                           int32_t* __restrict__ out, int64_t n) {
+  constexpr int CW = 31, PL = 4, ST = CW * 32 * PL;
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[NS], empty[NS], cbar;
+  __shared__ __align__(16) uint4 resp;
+  __shared__ int64_t tile_of[NS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], CW);
+    }
+    bar_init(&cbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == CW) {
+    if (lane == 0) {
+      int64_t t = blockIdx.x;
+      uint32_t cph = 0;
+      for (int k = 0;; ++k) {
+        const int s = k % NS;
+        if (k >= NS) bar_wait(&empty[s], ((k / NS) - 1) & 1);
+        tile_of[s] = t;
+        if (t < 0) {  // no more tiles: wake the consumers on this stage
+          bar_arrive(&full[s]);
+          break;
+        }
+        const int64_t e0 = t * ST;
+        const uint32_t bytes = (uint32_t)(8 * min((int64_t)ST, n - e0));
+        bar_expect(&full[s], bytes);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(s_u32(ring + s * ST)), "l"(y + e0), "r"(bytes), "r"(s_u32(&full[s])) : "memory");
+        bar_expect(&cbar, 16);
+        clc_cancel(&resp, &cbar);
+        bar_wait(&cbar, cph);
+        cph ^= 1;
+        t = clc_get(&resp);
+      }
+    }
+    return;
+  }
+  for (int k = 0;; ++k) {
+    const int s = k % NS;
+    bar_wait(&full[s], (k / NS) & 1);
+    const int64_t t = tile_of[s];
+    if (t < 0) break;
+    const double2* st = reinterpret_cast<const double2*>(ring + s * ST + warp * 32 * PL);
+    const double2 a = st[lane], b = st[32 + lane];
+    __syncwarp();
+    if (lane == 0) bar_arrive(&empty[s]);
+    const int64_t e0 = t * ST + warp * 32 * PL;
+    int2* o = reinterpret_cast<int2*>(out + e0);
+    if (e0 + 32 * PL <= n) {
+      __stcs(o + lane, make_int2(fold(a.x), fold(a.y)));
+      __stcs(o + 32 + lane, make_int2(fold(b.x), fold(b.y)));
+    } else {
+      if (e0 + 2 * lane + 1 < n) __stcs(o + lane, make_int2(fold(a.x), fold(a.y)));
+      if (e0 + 64 + 2 * lane + 1 < n) __stcs(o + 32 + lane, make_int2(fold(b.x), fold(b.y)));
+    }
+  }
+}
+
+// shape F: persistent register loop (1024 x 4) whose tiles come from a global atomic
+// counter (zeroed before the launch): tiles are taken in order, a compact front.
+template <int T, int U>
+__global__ void __launch_bounds__(T, 1) k_stream_atomic(const double2* __restrict__ y,
+                                                        int2* __restrict__ out, int64_t pairs,
+                                                        unsigned long long* ctr) {
+  __shared__ int64_t nxt;
+  const int64_t tiles = pairs / ((int64_t)T * U);
+  if (threadIdx.x == 0) nxt = (int64_t)atomicAdd(ctr, 1ull);
+  __syncthreads();
+  int64_t t = nxt;
+  double2 v[U];
+  if (t < tiles) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ldcs2(y + t * T * U + threadIdx.x + u * T);
+  }
+  while (t < tiles) {
+    __syncthreads();
+    if (threadIdx.x == 0) nxt = (int64_t)atomicAdd(ctr, 1ull);
+    const int64_t p0 = t * T * U + threadIdx.x;
+    int2 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = make_int2(fold(v[u].x), fold(v[u].y));
+    __syncthreads();
+    const int64_t tn = nxt;
+    if (tn < tiles) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ldcs2(y + tn * T * U + threadIdx.x + u * T);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) __stcs(out + p0 + u * T, r[u]);
+    t = tn;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = tiles * T * U + threadIdx.x; i < pairs; i += T)
+      __stcs(out + i, make_int2(fold(y[i].x), fold(y[i].y)));
+}
+
 __device__ __forceinline__ uint64_t smix(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
@@ -265,7 +389,7 @@ int sms() {
 extern "C" {
 
 // Number of 1-D stream shapes (variant 0 .. probe_stream_variants()-1).
-int probe_stream_variants(void) { return 9; }
+int probe_stream_variants(void) { return 11; }
 
 // One launch of the 1-D same-mix stream over n targets (n even, y 16-B and
 // out 8-B aligned).  Returns a cudaError_t.
@@ -309,6 +433,21 @@ int probe_stream(const double* y, int32_t* out, int64_t n, int variant, void* st
       if (variant == 6) k_stream_tma<4, false><<<sms(), 1024, smem, st>>>(y, out, 2 * pairs);
       else if (variant == 7) k_stream_tma<4, true><<<sms(), 1024, smem, st>>>(y, out, 2 * pairs);
       else k_stream_tma<6, false><<<sms(), 1024, smem, st>>>(y, out, 2 * pairs);
+      break;
+    }
+    case 9: {
+      const int64_t ntiles = (2 * pairs + 3967) / 3968;
+      const size_t smem = (size_t)4 * 3968 * 8;
+      cudaFuncSetAttribute((const void*)k_stream_tma_clc<4>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_stream_tma_clc<4><<<(unsigned)ntiles, 1024, smem, st>>>(y, out, 2 * pairs);
+      break;
+    }
+    case 10: {
+      static unsigned long long* ctr = nullptr;
+      if (!ctr) cudaMalloc(&ctr, 8);
+      cudaMemsetAsync(ctr, 0, 8, st);
+      k_stream_atomic<1024, 4><<<sms(), 1024, 0, st>>>(y2, o2, pairs, ctr);
       break;
     }
     default:

@@ -78,7 +78,7 @@ class TableInfo(ctypes.Structure):
                 ("levels", ctypes.c_int32), ("pad_", ctypes.c_int32), ("top_n", ctypes.c_int64),
                 ("level_bytes", ctypes.c_int64), ("dir_entry_bytes", ctypes.c_int32),
                 ("fast_steps", ctypes.c_int32), ("rare_steps", ctypes.c_int32),
-                ("pad2_", ctypes.c_int32)]
+                ("ring_stages", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}

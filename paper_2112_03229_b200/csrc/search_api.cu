@@ -41,6 +41,10 @@ struct eos_table_s {
   int unroll[2] = {4, 4};
   bool clc[2] = {true, true};
   int ctas_per_sm = 0;
+  // large launches through the shared-memory ring (search1d_ring_kernel; nullptr: none)
+  const void* fn_ring = nullptr;
+  int ring_ns = 0, grid_ring = 0;
+  int64_t ring_smem = 0;
   // small launches (pick_search_small; fn_small == nullptr: none)
   const void* fn_small = nullptr;
   int threads_small = 0, unroll_small = 0, grid_small = 0;
@@ -124,6 +128,25 @@ const void* tiered_small_fn(int steps) {
     default: return nullptr;
   }
 }
+
+// The ring kernel of a layout (search1d_ring_kernel; the stage count is a launch argument).
+template <int MODE, bool D16>
+const void* ring_fn_md(int sf, bool big) {
+  switch (sf) {
+    case 1: return (const void*)dv::search1d_ring_kernel<1, false, MODE, D16>;
+    case 2: return (const void*)dv::search1d_ring_kernel<2, false, MODE, D16>;
+    case 3: return big ? (const void*)dv::search1d_ring_kernel<3, true, MODE, D16>
+                       : (const void*)dv::search1d_ring_kernel<3, false, MODE, D16>;
+    default: return (const void*)dv::search1d_ring_kernel<0, true, MODE, D16>;
+  }
+}
+const void* ring_fn(const TablePlan& p) {
+  if (p.key_mode == 0)
+    return p.dir16 ? ring_fn_md<0, true>(p.fast_steps, p.big) : ring_fn_md<0, false>(p.fast_steps, p.big);
+  return p.dir16 ? ring_fn_md<1, true>(p.fast_steps, p.big) : ring_fn_md<1, false>(p.fast_steps, p.big);
+}
+// Launches with at least this many ring stages per SM take the ring kernel.
+constexpr int64_t kRingMinStagesPerSm = 4;
 
 struct LaunchShape {
   const void* fn;
@@ -228,12 +251,18 @@ bool exp_small_off() {
   const char* e = getenv("EOS_SMALL_TILES");
   return e && e[0] == '0';
 }
+int exp_ring(int ns) {  // EOS_RING=0: no ring kernel; EOS_RING=<n>: at most n stages
+  const char* e = getenv("EOS_RING");
+  return e ? std::min(ns, atoi(e)) : ns;
+}
 #else
 bool exp_small_off() { return false; }
+int exp_ring(int ns) { return ns; }
 #endif
 
 eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* out, int64_t gofs,
-                         uint64_t* counters, cudaStream_t st) {
+                         uint64_t* counters, cudaStream_t st_) {
+  cudaStream_t st = st_;
   const bool cnt = counters != nullptr;
   dv::SearchArgs a{};
   a.image = (const uint4*)t->image_dev;
@@ -254,6 +283,18 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
   a.vec_ok = ((ya & 7) == 0) && (((oa + 4 * (uintptr_t)a.head) & 7) == 0) && count > a.head;
   // One CTA per tile (CLC work stealing keeps ~#SM x occupancy of them
   // resident); the static schedule uses a persistent grid instead.
+  // large launches with an aligned vector body: the shared-memory ring
+  if (!cnt && t->fn_ring && a.vec_ok &&
+      (count - a.head) / dv::kRingStage >= kRingMinStagesPerSm * t->num_sms) {
+    a.ring_ns = t->ring_ns;
+    const int64_t st = ((count - a.head) / 2 * 2 + dv::kRingStage - 1) / dv::kRingStage;
+    a.ntiles = st;
+    void* params[] = {&a};
+    EOS_CUDA(launch(t->fn_ring, std::min<int64_t>(t->grid_ring, st), 1024, (size_t)t->ring_smem,
+                    st_, params));
+    count_launch();
+    return EOS_OK;
+  }
   int64_t per_tile = (int64_t)t->threads[cnt] * t->unroll[cnt] * 2;
   int64_t tiles = (count - a.head + per_tile - 1) / per_tile;
   // fewer tiles than half the SMs: the small-tile shape spreads the launch over 4x more CTAs
@@ -412,6 +453,20 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
       t->clc_small = false;
     }
   }
+  if (t->levels == 0) {  // the ring kernel: as many stages as shared memory holds
+    const void* fr = ring_fn(t->plan);
+    const int64_t img = (t->smem_bytes + 127) & ~int64_t(127);
+    for (int ns = exp_ring(dv::kRingMaxStages); ns >= 2; --ns) {
+      const int64_t smem = img + (int64_t)ns * dv::kRingStage * 8;
+      int per_sm = 0;
+      if (configure(fr, 1024, smem, t->num_sms, &t->grid_ring, &per_sm) == EOS_OK && per_sm >= 1) {
+        t->fn_ring = fr;
+        t->ring_ns = ns;
+        t->ring_smem = smem;
+        break;
+      }
+    }
+  }
   if (t->levels == 0 && !exp_small_off()) {
     const LaunchShape ls = pick_search_small(t->plan, t->smem_bytes);
     if (ls.fn && configure(ls.fn, ls.threads, t->smem_bytes, t->num_sms, &t->grid_small,
@@ -535,6 +590,7 @@ eos_status eos_table_info(eos_table t, eos_table_info_t* out) {
   out->image_bytes = t->smem_bytes;
   out->device = t->device;
   out->ctas_per_sm = t->ctas_per_sm;
+  out->ring_stages = t->fn_ring ? t->ring_ns : 0;
   return EOS_OK;
 }
 

@@ -531,6 +531,7 @@ void fill_info(const TablePlan& p, eos_table_info_t* info) {
   info->dir_entry_bytes = p.dir16 ? 2 : 4;
   info->fast_steps = p.fast_steps;
   info->rare_steps = p.big ? 1 : 0;
+  info->ring_stages = 0;
 }
 
 void fill_info(const TieredPlan& t, eos_table_info_t* info) {

@@ -8,6 +8,7 @@ import measure
 from bench import ClockSampler
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else (8 << 30)
+only = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else None
 Y = torch.empty(n, dtype=torch.float64, device="cuda")
 Y.uniform_(1.0, 2.0)
 o = torch.empty(n, dtype=torch.int32, device="cuda")
@@ -15,6 +16,8 @@ L = measure.lib()
 st = torch.cuda.current_stream()
 res = {}
 for v in range(L.probe_stream_variants()):
+    if only is not None and v not in only:
+        continue
     f = lambda: measure._check(L.probe_stream(Y.data_ptr(), o.data_ptr(), n, v, st.cuda_stream), "p")
     f(); torch.cuda.synchronize()
     reps = 5 if n >= (1 << 30) else 50
