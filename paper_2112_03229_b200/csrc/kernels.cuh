@@ -710,30 +710,34 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
 }
 
 // ---- streaming through a shared-memory ring (TMA bulk copies) ----------------
-// A persistent CTA per SM (1024 threads): warp 31 is the producer, one elected
-// lane of which streams the CTA's tiles (t = blockIdx.x + k gridDim.x) of the
-// vector body into NS shared-memory stages with cp.async.bulk (L2 evict-first:
-// the stream is read once), each completing on the stage's `full` mbarrier.
-// Warps 0..30 consume: wait `full`, read their 128 targets from shared memory
-// (two conflict-free 16-byte loads per lane), look them up, store the int32
-// indices with st.global.cs, and release the stage (`empty`, one arrival per
-// warp).  No CTA-wide barrier in the loop; the loads in flight (NS - 1 stages,
-// ~95 KB per SM) do not occupy registers.  (The register-prefetch persistent
-// loop reaches ~6.35 TB/s on the same-mix stream, one CTA per tile 7.18:
-// measure/probes.cu.)
+// The grid has one CTA per tile of kRingStage targets; a resident CTA (one per SM,
+// 1024 threads) keeps its staged image and takes over the tiles of CTAs that have
+// not launched yet with cluster launch control, so tiles are processed in launch
+// order.  Warp 31 is the producer: one elected lane claims the tiles (its own,
+// then cancelled CTAs') and streams each into the next of NS shared-memory stages
+// with cp.async.bulk (L2 evict-first: read once), completing on the stage's `full`
+// mbarrier, the tile number in a shared slot.  Warps 0..30 consume: wait `full`,
+// read their 128 targets (two conflict-free 16-byte loads per lane), release the
+// stage (`empty`, one arrival per warp), look the targets up and store the int32
+// indices with st.global.cs.  No CTA-wide barrier in the loop, and the loads in
+// flight (up to NS stages) hold no registers.
+// Measured on the same-mix stream (measure/probes.cu): a static
+// persistent schedule reaches 6.35 TB/s with register prefetch and 6.63 with this
+// ring, one CTA per tile 7.17, this ring with launch-order tiles 7.14: DRAM
+// bandwidth follows the compactness of the address front, not the bytes in flight.
 constexpr int kRingWarps = 31;                  // consumer warps
 constexpr int kRingPerLane = 4;                 // targets per lane per stage
 constexpr int kRingStage = kRingWarps * 32 * kRingPerLane;  // 3968 targets, 31 KB
+constexpr int kRingMaxStages = 6;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-constexpr int kRingMaxStages = 6;
-
 template <class LK>
 __device__ __forceinline__ void ring_body(const SearchArgs& args, const LK& lk, double* ring,
-                                          uint64_t* full, uint64_t* empty) {
+                                          uint64_t* full, uint64_t* empty, int64_t* tile_of,
+                                          uint4* clc_resp, uint64_t* clc_bar) {
   constexpr int ST = kRingStage;
   const int NS = args.ring_ns;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -742,15 +746,20 @@ __device__ __forceinline__ void ring_body(const SearchArgs& args, const LK& lk, 
   const int64_t count = args.count;
   const int64_t head = args.head;
   const int64_t body = (count - head) & ~int64_t(1);  // even: whole 16-B pairs
-  const int64_t ntiles = (body + ST - 1) / ST;
   if (warp == kRingWarps) {  // producer
     if (lane == 0) {
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-      int k = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+      int64_t t = blockIdx.x;
+      uint32_t cph = 0;
+      for (int k = 0;; ++k) {
         const int s = k % NS;
         if (k >= NS) mbar_wait(&empty[s], ((k / NS) - 1) & 1);
+        tile_of[s] = t;
+        if (t < 0) {  // no tile left: the stage carries the end mark
+          mbar_arrive(&full[s]);
+          break;
+        }
         const int64_t e0 = t * ST;
         const uint32_t bytes = (uint32_t)(8 * min((int64_t)ST, body - e0));
         mbar_arrive_expect_tx(&full[s], bytes);
@@ -759,36 +768,41 @@ __device__ __forceinline__ void ring_body(const SearchArgs& args, const LK& lk, 
             "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(ring + (size_t)s * ST)), "l"(Y + head + e0),
             "r"(bytes), "r"(smem_u32(&full[s])), "l"(pol)
             : "memory");
+        mbar_arrive_expect_tx(clc_bar, 16);
+        clc_try_cancel(clc_resp, clc_bar);
+        mbar_wait(clc_bar, cph);
+        cph ^= 1u;
+        t = clc_query(clc_resp);
       }
     }
     return;
   }
-  // the scalar ends: the unaligned leading element and an odd last one
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (head) {
-      const double y[1] = {Y[0]};
-      int32_t r[1];
-      lk.many(y, r);
-      out[0] = r[0];
-    }
-    if (head + body < count) {
-      const double y[1] = {Y[count - 1]};
-      int32_t r[1];
-      lk.many(y, r);
-      out[count - 1] = r[0];
-    }
-  }
-  int k = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+  for (int k = 0;; ++k) {
     const int s = k % NS;
     mbar_wait(&full[s], (k / NS) & 1);
+    const int64_t t = tile_of[s];
+    if (t < 0) break;
     const double2* st = reinterpret_cast<const double2*>(ring + (size_t)s * ST + warp * 32 * kRingPerLane);
     const double2 v0 = st[lane], v1 = st[32 + lane];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // the stage's targets are in registers
+    if (t == 0 && threadIdx.x == 0) {  // the scalar ends go with tile 0
+      if (head) {
+        const double y[1] = {Y[0]};
+        int32_t r[1];
+        lk.many(y, r);
+        out[0] = r[0];
+      }
+      if (head + body < count) {
+        const double y[1] = {Y[count - 1]};
+        int32_t r[1];
+        lk.many(y, r);
+        out[count - 1] = r[0];
+      }
+    }
     const double y[4] = {v0.x, v0.y, v1.x, v1.y};
     int32_t r[4];
     lk.many(y, r);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);  // the stage's targets are in registers
     const int64_t e0 = t * ST + warp * 32 * kRingPerLane;  // first target of this warp's slice
     int2* o = reinterpret_cast<int2*>(out + head + e0);
     if (e0 + 32 * kRingPerLane <= body) {
@@ -804,13 +818,16 @@ __device__ __forceinline__ void ring_body(const SearchArgs& args, const LK& lk, 
 template <int SF, bool BIG, int MODE, bool D16>
 __global__ void __launch_bounds__(1024, 1) search1d_ring_kernel(const SearchArgs args) {
   extern __shared__ __align__(128) uint4 smem[];
-  __shared__ __align__(8) uint64_t full[kRingMaxStages], empty[kRingMaxStages], stage_bar;
+  __shared__ __align__(8) uint64_t full[kRingMaxStages], empty[kRingMaxStages], stage_bar, clc_bar;
+  __shared__ __align__(16) uint4 clc_resp;
+  __shared__ int64_t tile_of[kRingMaxStages];
   EOS_DCHECK(args.ring_ns >= 2 && args.ring_ns <= kRingMaxStages);
   if (threadIdx.x == 0) {
     for (int s = 0; s < args.ring_ns; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kRingWarps);
     }
+    mbar_init(&clc_bar, 1);
   }
   stage_image(smem, args.image, args.image_16, &stage_bar);  // (its barrier orders the inits)
   pdl_enter();
@@ -821,7 +838,7 @@ __global__ void __launch_bounds__(1024, 1) search1d_ring_kernel(const SearchArgs
   lk.a = a;
   double* ring = reinterpret_cast<double*>(reinterpret_cast<char*>(smem) +
                                            ((16 * (size_t)args.image_16 + 127) & ~size_t(127)));
-  ring_body(args, lk, ring, full, empty);
+  ring_body(args, lk, ring, full, empty, tile_of, &clc_resp, &clc_bar);
 }
 
 // Tables larger than shared memory (TieredLookup): the smem image holds the

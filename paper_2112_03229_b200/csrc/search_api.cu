@@ -289,9 +289,8 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
     a.ring_ns = t->ring_ns;
     const int64_t st = ((count - a.head) / 2 * 2 + dv::kRingStage - 1) / dv::kRingStage;
     a.ntiles = st;
-    void* params[] = {&a};
-    EOS_CUDA(launch(t->fn_ring, std::min<int64_t>(t->grid_ring, st), 1024, (size_t)t->ring_smem,
-                    st_, params));
+    void* params[] = {&a};  // one CTA per tile (cluster launch control, kernels.cuh ring_body)
+    EOS_CUDA(launch(t->fn_ring, st, 1024, (size_t)t->ring_smem, st_, params));
     count_launch();
     return EOS_OK;
   }

@@ -175,6 +175,31 @@ def test_ragged_and_misaligned(count, y_off, o_off):
     t.close()
 
 
+@pytest.mark.parametrize("count", [2_350_077, 2_350_078, 4_000_001, 9_999_999])
+@pytest.mark.parametrize("y_off,o_off", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("table,kw", [("cfg2", {}), ("cfg5", {}), ("cfg5", {"k": 0})])
+def test_ring_launches_ragged_and_misaligned(count, y_off, o_off, table, kw):
+    """Launches large enough for the shared-memory ring kernel (>= 4 stages of 3968 targets
+    per SM): odd and even lengths, an unaligned first target (scalar head), an odd last
+    one (scalar tail), and outputs that are not 8-byte aligned (the register kernels
+    take those); bit-exact, no stray writes.  (k = 0 on cfg5: S = 9, the rare-branch
+    layout.)"""
+    w = datagen.workload(table, count=count + 8)
+    Yall = w.targets.host_fill(0, count + 8, w.table)
+    Yall[y_off] = np.nan
+    Yall[y_off + count - 1] = w.table[-1]
+    yd = to_dev(Yall)[y_off:y_off + count]
+    od_all = torch.full((count + 8,), -7, dtype=torch.int32, device=DEV)
+    od = od_all[o_off:o_off + count]
+    t = eos.Table(w.table, **kw)
+    t.search(yd, out=od)
+    torch.cuda.synchronize()
+    got = od_all.cpu().numpy()
+    assert_same(got[o_off:o_off + count], oracle.search(w.table, Yall[y_off:y_off + count]))
+    assert np.all(got[:o_off] == -7) and np.all(got[o_off + count:] == -7)  # no stray writes
+    t.close()
+
+
 @pytest.mark.parametrize("table,kw", [("cfg1", {}), ("cfg2", {"log_bins": 12000}),
                                       ("cfg5", {}), ("cfg5", {"log_bins": 5000}),
                                       ("cfg2", {"k": 0})])
