@@ -129,7 +129,9 @@ const void* tiered_small_fn(int steps) {
   }
 }
 
+#ifdef EOS_EXPERIMENTS
 // The ring kernel of a layout (search1d_ring_kernel; the stage count is a launch argument).
+// Experiment build only (EOS_RING): measured no faster than the register kernels.
 template <int MODE, bool D16>
 const void* ring_fn_md(int sf, bool big) {
   switch (sf) {
@@ -145,6 +147,9 @@ const void* ring_fn(const TablePlan& p) {
     return p.dir16 ? ring_fn_md<0, true>(p.fast_steps, p.big) : ring_fn_md<0, false>(p.fast_steps, p.big);
   return p.dir16 ? ring_fn_md<1, true>(p.fast_steps, p.big) : ring_fn_md<1, false>(p.fast_steps, p.big);
 }
+#else
+const void* ring_fn(const TablePlan&) { return nullptr; }
+#endif
 // Launches with at least this many ring stages per SM take the ring kernel.
 constexpr int64_t kRingMinStagesPerSm = 4;
 
@@ -251,13 +256,16 @@ bool exp_small_off() {
   const char* e = getenv("EOS_SMALL_TILES");
   return e && e[0] == '0';
 }
-int exp_ring(int ns) {  // EOS_RING=0: no ring kernel; EOS_RING=<n>: at most n stages
+int exp_ring(int ns) {  // EOS_RING=<n>: the ring kernel with at most n stages (default: none)
   const char* e = getenv("EOS_RING");
-  return e ? std::min(ns, atoi(e)) : ns;
+  return e ? std::min(ns, atoi(e)) : 0;
 }
 #else
 bool exp_small_off() { return false; }
-int exp_ring(int ns) { return ns; }
+// The ring kernel measured equal on S = 1 tables (cfg2 579-585 vs 584-586, cfg3 594 vs
+// 588-595 Glookups/s) and 8% slower on cfg5 (495 vs 536): the product keeps the
+// register-prefetch kernels; the ring stays an experiment.
+int exp_ring(int) { return 0; }
 #endif
 
 eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* out, int64_t gofs,
@@ -452,7 +460,7 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
       t->clc_small = false;
     }
   }
-  if (t->levels == 0) {  // the ring kernel: as many stages as shared memory holds
+  if (t->levels == 0 && ring_fn(t->plan)) {  // the ring kernel: as many stages as fit
     const void* fr = ring_fn(t->plan);
     const int64_t img = (t->smem_bytes + 127) & ~int64_t(127);
     for (int ns = exp_ring(dv::kRingMaxStages); ns >= 2; --ns) {

@@ -496,3 +496,54 @@ def test_automatic_plan_is_the_argmin_of_the_cost_model(name):
             best = (c, img, info.bins, info.hash_kind, info.steps)
     auto, _ = eos.eos_plan_table(X, eos.EOS_K_AUTO, with_directory=False)
     assert (auto.bins, auto.hash_kind, auto.steps) == best[2:], (auto.bins, best)
+
+
+# ------------------------------------------- binding argument checks (CPU) --
+def _unbound(cls):
+    """An object of the binding class with a dummy handle: the argument checks run before
+    any C call, so a rejected call never reaches the library (no device needed)."""
+    o = cls.__new__(cls)
+    o._h = 0xDEAD
+    return o
+
+
+@pytest.mark.parametrize("bad", ["f32", "short", "strided", "i64_out"])
+def test_search_host_rejects_bad_host_buffers(bad):
+    t = _unbound(eos.Table)
+    y = np.linspace(1.0, 2.0, 1000)
+    out = np.empty(1000, np.int32)
+    if bad == "f32":
+        y = y.astype(np.float32)
+    elif bad == "short":
+        out = np.empty(999, np.int32)
+    elif bad == "strided":
+        y = np.linspace(1.0, 2.0, 2000)[::2]
+    else:
+        out = np.empty(1000, np.int64)
+    with pytest.raises((TypeError, ValueError)):
+        t.search_host(y, out=out, sync=False)
+    t._h = None
+
+
+@pytest.mark.parametrize("bad", ["f32_rho", "len_T", "short_P", "i64_bracket", "f32_out",
+                                 "strided_T"])
+def test_interp_host_rejects_bad_host_buffers(bad):
+    g = _unbound(eos.Grid2D)
+    m = 500
+    rho, T = np.linspace(1, 2, m), np.linspace(3, 4, m)
+    P, iR, iT = np.empty(m), np.empty(m, np.int32), np.empty(m, np.int32)
+    if bad == "f32_rho":
+        rho = rho.astype(np.float32)
+    elif bad == "len_T":
+        T = T[:-1]
+    elif bad == "short_P":
+        P = P[:-1]
+    elif bad == "i64_bracket":
+        iR = np.empty(m, np.int64)
+    elif bad == "f32_out":
+        P = np.empty(m, np.float32)
+    else:
+        T = np.linspace(3, 4, 2 * m)[::2]
+    with pytest.raises((TypeError, ValueError)):
+        g.interp_host(rho, T, P, iR, iT, sync=False)
+    g._h = None
