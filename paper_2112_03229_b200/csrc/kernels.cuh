@@ -435,15 +435,18 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+// Wait for the phase of `bar` with parity `parity`.  try_wait suspends the
+// thread until the phase completes or the suspend-time hint (ns) runs out, so
+// waiting warps leave their issue slots to working ones instead of spinning.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok = 0;
   do {
     asm volatile(
         "{\n\t.reg .pred P;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
         "selp.b32 %0, 1, 0, P;\n\t}"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
         : "memory");
   } while (!ok);
 }
@@ -710,7 +713,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
 }
 
 // ---- streaming through a shared-memory ring (TMA bulk copies) ----------------
-// The grid has one CTA per tile of kRingStage targets; a resident CTA (one per SM,
+// The grid has one CTA per tile of 31 x 32 x PL targets; a resident CTA (one per SM,
 // 1024 threads) keeps its staged image and takes over the tiles of CTAs that have
 // not launched yet with cluster launch control, so tiles are processed in launch
 // order.  Warp 31 is the producer: one elected lane claims the tiles (its own,
@@ -726,19 +729,18 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(
 // ring, one CTA per tile 7.17, this ring with launch-order tiles 7.14: DRAM
 // bandwidth follows the compactness of the address front, not the bytes in flight.
 constexpr int kRingWarps = 31;                  // consumer warps
-constexpr int kRingPerLane = 4;                 // targets per lane per stage
-constexpr int kRingStage = kRingWarps * 32 * kRingPerLane;  // 3968 targets, 31 KB
+// targets per lane per stage: PL (template) = 4 or 8; a stage is 31 x 32 x PL targets
 constexpr int kRingMaxStages = 6;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <class LK>
+template <int PL, class LK>
 __device__ __forceinline__ void ring_body(const SearchArgs& args, const LK& lk, double* ring,
                                           uint64_t* full, uint64_t* empty, int64_t* tile_of,
                                           uint4* clc_resp, uint64_t* clc_bar) {
-  constexpr int ST = kRingStage;
+  constexpr int ST = kRingWarps * 32 * PL;  // targets per stage
   const int NS = args.ring_ns;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* __restrict__ Y = args.Y;
@@ -751,10 +753,9 @@ __device__ __forceinline__ void ring_body(const SearchArgs& args, const LK& lk, 
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
       int64_t t = blockIdx.x;
-      uint32_t cph = 0;
-      for (int k = 0;; ++k) {
-        const int s = k % NS;
-        if (k >= NS) mbar_wait(&empty[s], ((k / NS) - 1) & 1);
+      uint32_t cph = 0, eph = 1;  // phases of the CLC barrier and of the empty barriers
+      for (int k = 0, s = 0;; ++k) {
+        if (k >= NS) mbar_wait(&empty[s], eph);
         tile_of[s] = t;
         if (t < 0) {  // no tile left: the stage carries the end mark
           mbar_arrive(&full[s]);
@@ -773,49 +774,63 @@ __device__ __forceinline__ void ring_body(const SearchArgs& args, const LK& lk, 
         mbar_wait(clc_bar, cph);
         cph ^= 1u;
         t = clc_query(clc_resp);
+        if (++s == NS) {
+          s = 0;
+          eph ^= 1u;
+        }
       }
     }
     return;
   }
-  for (int k = 0;; ++k) {
-    const int s = k % NS;
-    mbar_wait(&full[s], (k / NS) & 1);
+  uint32_t fph = 0;  // phase of the full barriers
+  for (int s = 0;;) {
+    mbar_wait(&full[s], fph);
     const int64_t t = tile_of[s];
     if (t < 0) break;
-    const double2* st = reinterpret_cast<const double2*>(ring + (size_t)s * ST + warp * 32 * kRingPerLane);
-    const double2 v0 = st[lane], v1 = st[32 + lane];
+    const double2* st = reinterpret_cast<const double2*>(ring + (size_t)s * ST + warp * 32 * PL);
+    double y[PL];
+#pragma unroll
+    for (int h = 0; h < PL / 2; ++h) {
+      const double2 v = st[32 * h + lane];
+      y[2 * h] = v.x;
+      y[2 * h + 1] = v.y;
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // the stage's targets are in registers
+    if (++s == NS) {
+      s = 0;
+      fph ^= 1u;
+    }
     if (t == 0 && threadIdx.x == 0) {  // the scalar ends go with tile 0
       if (head) {
-        const double y[1] = {Y[0]};
-        int32_t r[1];
-        lk.many(y, r);
-        out[0] = r[0];
+        const double y1[1] = {Y[0]};
+        int32_t r1[1];
+        lk.many(y1, r1);
+        out[0] = r1[0];
       }
       if (head + body < count) {
-        const double y[1] = {Y[count - 1]};
-        int32_t r[1];
-        lk.many(y, r);
-        out[count - 1] = r[0];
+        const double y1[1] = {Y[count - 1]};
+        int32_t r1[1];
+        lk.many(y1, r1);
+        out[count - 1] = r1[0];
       }
     }
-    const double y[4] = {v0.x, v0.y, v1.x, v1.y};
-    int32_t r[4];
+    int32_t r[PL];
     lk.many(y, r);
-    const int64_t e0 = t * ST + warp * 32 * kRingPerLane;  // first target of this warp's slice
+    const int64_t e0 = t * ST + warp * 32 * PL;  // first target of this warp's slice
     int2* o = reinterpret_cast<int2*>(out + head + e0);
-    if (e0 + 32 * kRingPerLane <= body) {
-      __stcs(o + lane, make_int2(r[0], r[1]));
-      __stcs(o + 32 + lane, make_int2(r[2], r[3]));
+    if (e0 + 32 * PL <= body) {
+#pragma unroll
+      for (int h = 0; h < PL / 2; ++h) __stcs(o + 32 * h + lane, make_int2(r[2 * h], r[2 * h + 1]));
     } else {  // the last tile
-      if (e0 + 2 * lane < body) __stcs(o + lane, make_int2(r[0], r[1]));
-      if (e0 + 64 + 2 * lane < body) __stcs(o + 32 + lane, make_int2(r[2], r[3]));
+#pragma unroll
+      for (int h = 0; h < PL / 2; ++h)
+        if (e0 + 64 * h + 2 * lane < body) __stcs(o + 32 * h + lane, make_int2(r[2 * h], r[2 * h + 1]));
     }
   }
 }
 
-template <int SF, bool BIG, int MODE, bool D16>
+template <int SF, bool BIG, int MODE, bool D16, int PL>
 __global__ void __launch_bounds__(1024, 1) search1d_ring_kernel(const SearchArgs args) {
   extern __shared__ __align__(128) uint4 smem[];
   __shared__ __align__(8) uint64_t full[kRingMaxStages], empty[kRingMaxStages], stage_bar, clc_bar;
@@ -838,7 +853,7 @@ __global__ void __launch_bounds__(1024, 1) search1d_ring_kernel(const SearchArgs
   lk.a = a;
   double* ring = reinterpret_cast<double*>(reinterpret_cast<char*>(smem) +
                                            ((16 * (size_t)args.image_16 + 127) & ~size_t(127)));
-  ring_body(args, lk, ring, full, empty, tile_of, &clc_resp, &clc_bar);
+  ring_body<PL>(args, lk, ring, full, empty, tile_of, &clc_resp, &clc_bar);
 }
 
 // Tables larger than shared memory (TieredLookup): the smem image holds the

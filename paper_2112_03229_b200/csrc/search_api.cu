@@ -132,23 +132,34 @@ const void* tiered_small_fn(int steps) {
 #ifdef EOS_EXPERIMENTS
 // The ring kernel of a layout (search1d_ring_kernel; the stage count is a launch argument).
 // Experiment build only (EOS_RING): measured no faster than the register kernels.
-template <int MODE, bool D16>
+template <int MODE, bool D16, int PL>
 const void* ring_fn_md(int sf, bool big) {
   switch (sf) {
-    case 1: return (const void*)dv::search1d_ring_kernel<1, false, MODE, D16>;
-    case 2: return (const void*)dv::search1d_ring_kernel<2, false, MODE, D16>;
-    case 3: return big ? (const void*)dv::search1d_ring_kernel<3, true, MODE, D16>
-                       : (const void*)dv::search1d_ring_kernel<3, false, MODE, D16>;
-    default: return (const void*)dv::search1d_ring_kernel<0, true, MODE, D16>;
+    case 1: return (const void*)dv::search1d_ring_kernel<1, false, MODE, D16, PL>;
+    case 2: return (const void*)dv::search1d_ring_kernel<2, false, MODE, D16, PL>;
+    case 3: return big ? (const void*)dv::search1d_ring_kernel<3, true, MODE, D16, PL>
+                       : (const void*)dv::search1d_ring_kernel<3, false, MODE, D16, PL>;
+    default: return (const void*)dv::search1d_ring_kernel<0, true, MODE, D16, PL>;
   }
 }
-const void* ring_fn(const TablePlan& p) {
-  if (p.key_mode == 0)
-    return p.dir16 ? ring_fn_md<0, true>(p.fast_steps, p.big) : ring_fn_md<0, false>(p.fast_steps, p.big);
-  return p.dir16 ? ring_fn_md<1, true>(p.fast_steps, p.big) : ring_fn_md<1, false>(p.fast_steps, p.big);
+int ring_per_lane() {  // EOS_RING_PL=8: 8 targets per lane per stage (default 4)
+  const char* e = getenv("EOS_RING_PL");
+  return (e && atoi(e) == 8) ? 8 : 4;
 }
+const void* ring_fn(const TablePlan& p) {
+  if (ring_per_lane() == 8) {
+    if (p.key_mode == 0)
+      return p.dir16 ? ring_fn_md<0, true, 8>(p.fast_steps, p.big) : ring_fn_md<0, false, 8>(p.fast_steps, p.big);
+    return p.dir16 ? ring_fn_md<1, true, 8>(p.fast_steps, p.big) : ring_fn_md<1, false, 8>(p.fast_steps, p.big);
+  }
+  if (p.key_mode == 0)
+    return p.dir16 ? ring_fn_md<0, true, 4>(p.fast_steps, p.big) : ring_fn_md<0, false, 4>(p.fast_steps, p.big);
+  return p.dir16 ? ring_fn_md<1, true, 4>(p.fast_steps, p.big) : ring_fn_md<1, false, 4>(p.fast_steps, p.big);
+}
+int ring_stage() { return dv::kRingWarps * 32 * ring_per_lane(); }
 #else
 const void* ring_fn(const TablePlan&) { return nullptr; }
+int ring_stage() { return dv::kRingWarps * 32 * 4; }
 #endif
 // Launches with at least this many ring stages per SM take the ring kernel.
 constexpr int64_t kRingMinStagesPerSm = 4;
@@ -293,9 +304,9 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
   // resident); the static schedule uses a persistent grid instead.
   // large launches with an aligned vector body: the shared-memory ring
   if (!cnt && t->fn_ring && a.vec_ok &&
-      (count - a.head) / dv::kRingStage >= kRingMinStagesPerSm * t->num_sms) {
+      (count - a.head) / ring_stage() >= kRingMinStagesPerSm * t->num_sms) {
     a.ring_ns = t->ring_ns;
-    const int64_t st = ((count - a.head) / 2 * 2 + dv::kRingStage - 1) / dv::kRingStage;
+    const int64_t st = ((count - a.head) / 2 * 2 + ring_stage() - 1) / ring_stage();
     a.ntiles = st;
     void* params[] = {&a};  // one CTA per tile (cluster launch control, kernels.cuh ring_body)
     EOS_CUDA(launch(t->fn_ring, st, 1024, (size_t)t->ring_smem, st_, params));
@@ -464,7 +475,7 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
     const void* fr = ring_fn(t->plan);
     const int64_t img = (t->smem_bytes + 127) & ~int64_t(127);
     for (int ns = exp_ring(dv::kRingMaxStages); ns >= 2; --ns) {
-      const int64_t smem = img + (int64_t)ns * dv::kRingStage * 8;
+      const int64_t smem = img + (int64_t)ns * ring_stage() * 8;
       int per_sm = 0;
       if (configure(fr, 1024, smem, t->num_sms, &t->grid_ring, &per_sm) == EOS_OK && per_sm >= 1) {
         t->fn_ring = fr;
