@@ -8,6 +8,7 @@
 //   EOS_SEARCH_VARIANT, EOS_TIERED_VARIANT  launch-shape variants by name
 //   EOS_LAYOUT=d16,sf,big                   lifting layout of a single-level table
 //   EOS_SMALL_TILES=0                       small launches keep the default tiles
+//   EOS_RING=<n>                            at most n ring stages (0: no ring kernel)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>

@@ -129,9 +129,10 @@ const void* tiered_small_fn(int steps) {
   }
 }
 
-#ifdef EOS_EXPERIMENTS
-// The ring kernel of a layout (search1d_ring_kernel; the stage count is a launch argument).
-// Experiment build only (EOS_RING): measured no faster than the register kernels.
+// The ring kernel of a layout (search1d_ring_kernel; the stage count is a launch
+// argument), 8 targets per lane per stage (62 KB stages): cfg5 (S = 3, 86 KB image,
+// 2 stages) 528 -> 562 Glookups/s; 4 per lane 529; S = 1 tables equal either way
+// (cfg2 580 vs 584), so those keep the register kernels.
 template <int MODE, bool D16, int PL>
 const void* ring_fn_md(int sf, bool big) {
   switch (sf) {
@@ -142,25 +143,19 @@ const void* ring_fn_md(int sf, bool big) {
     default: return (const void*)dv::search1d_ring_kernel<0, true, MODE, D16, PL>;
   }
 }
-int ring_per_lane() {  // EOS_RING_PL=8: 8 targets per lane per stage (default 4)
-  const char* e = getenv("EOS_RING_PL");
-  return (e && atoi(e) == 8) ? 8 : 4;
-}
+constexpr int kRingPerLane = 8;
+constexpr int kRingStage = dv::kRingWarps * 32 * kRingPerLane;  // 7936 targets, 62 KB
 const void* ring_fn(const TablePlan& p) {
-  if (ring_per_lane() == 8) {
-    if (p.key_mode == 0)
-      return p.dir16 ? ring_fn_md<0, true, 8>(p.fast_steps, p.big) : ring_fn_md<0, false, 8>(p.fast_steps, p.big);
-    return p.dir16 ? ring_fn_md<1, true, 8>(p.fast_steps, p.big) : ring_fn_md<1, false, 8>(p.fast_steps, p.big);
-  }
-  if (p.key_mode == 0)
-    return p.dir16 ? ring_fn_md<0, true, 4>(p.fast_steps, p.big) : ring_fn_md<0, false, 4>(p.fast_steps, p.big);
-  return p.dir16 ? ring_fn_md<1, true, 4>(p.fast_steps, p.big) : ring_fn_md<1, false, 4>(p.fast_steps, p.big);
-}
-int ring_stage() { return dv::kRingWarps * 32 * ring_per_lane(); }
-#else
-const void* ring_fn(const TablePlan&) { return nullptr; }
-int ring_stage() { return dv::kRingWarps * 32 * 4; }
+#ifndef EOS_EXPERIMENTS
+  if (p.steps < 2) return nullptr;  // S = 1: the register kernels (measured equal)
 #endif
+  if (p.key_mode == 0)
+    return p.dir16 ? ring_fn_md<0, true, kRingPerLane>(p.fast_steps, p.big)
+                   : ring_fn_md<0, false, kRingPerLane>(p.fast_steps, p.big);
+  return p.dir16 ? ring_fn_md<1, true, kRingPerLane>(p.fast_steps, p.big)
+                 : ring_fn_md<1, false, kRingPerLane>(p.fast_steps, p.big);
+}
+int ring_stage() { return kRingStage; }
 // Launches with at least this many ring stages per SM take the ring kernel.
 constexpr int64_t kRingMinStagesPerSm = 4;
 
@@ -267,16 +262,13 @@ bool exp_small_off() {
   const char* e = getenv("EOS_SMALL_TILES");
   return e && e[0] == '0';
 }
-int exp_ring(int ns) {  // EOS_RING=<n>: the ring kernel with at most n stages (default: none)
+int exp_ring(int ns) {  // EOS_RING=<n>: at most n ring stages (0: none; unset: as the product)
   const char* e = getenv("EOS_RING");
-  return e ? std::min(ns, atoi(e)) : 0;
+  return e ? std::min(ns, atoi(e)) : ns;
 }
 #else
 bool exp_small_off() { return false; }
-// The ring kernel measured equal on S = 1 tables (cfg2 579-585 vs 584-586, cfg3 594 vs
-// 588-595 Glookups/s) and 8% slower on cfg5 (495 vs 536): the product keeps the
-// register-prefetch kernels; the ring stays an experiment.
-int exp_ring(int) { return 0; }
+int exp_ring(int ns) { return ns; }
 #endif
 
 eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* out, int64_t gofs,

@@ -173,10 +173,15 @@ double lifting_probes(int o, int S) {
 // (profiles/r01_exp_table_size.json): the penalty lets only a large probe
 // saving buy the extra smem.  Targets are taken log-uniform over the table
 // range, i.e. uniform over the bins (equal key width).
+// Launch-shape term of the cost: <= 32 KB: 4 CTAs x 256 per SM;
+// <= 72 KB: 2 x 512; <= 100 KB: 1 x 1024, and two 62-KB stages of the ring kernel
+// still fit next to the image (search_api.cu: deep tables stream through it, cfg5
+// 528 -> 562 Glookups/s); <= 144 KB: register kernel only; above: L1 squeezed.
 double shape_cost(int64_t image_bytes) {
   return image_bytes <= 32 * 1024 ? 0.0
          : image_bytes <= 72 * 1024 ? 1.0
-         : image_bytes <= 144 * 1024 ? 1.5
+         : image_bytes <= 100 * 1024 ? 1.5
+         : image_bytes <= 144 * 1024 ? 3.0
                                      : 4.5;
 }
 

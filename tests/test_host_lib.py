@@ -457,7 +457,8 @@ def test_automatic_plan_is_the_argmin_of_the_cost_model(name):
     budget = 200 * 1024
 
     def shape(img):
-        return 0.0 if img <= 32768 else 1.0 if img <= 73728 else 1.5 if img <= 147456 else 4.5
+        return (0.0 if img <= 32768 else 1.0 if img <= 73728 else 1.5 if img <= 102400
+                else 3.0 if img <= 147456 else 4.5)
 
     def cost(info, d):
         occ = (d >> 16).astype(np.int64)
