@@ -89,7 +89,7 @@ typedef struct {
   int64_t top_n;       /* n1 = ceil(n / 8^D) (image_bytes then counts 4 B per T1 entry) */
   int64_t level_bytes; /* device bytes of the levels (0 when D == 0) */
   /* lifting layout of the search kernel (ABI >= 3): directory entries of 2 B
-   * (lo | occ << 12) or 4 B (lo | occ << 16) in the image; fast_steps = the
+   * (8 lo | occ) or 4 B (lo | occ << 16) in the image; fast_steps = the
    * fixed binary-lifting steps SF (0: all S steps in a runtime loop);
    * rare_steps = 1 if some bin holds >= 2^SF entries (its larger strides run
    * in a branch taken only by lanes that land in such a bin); ring_stages =

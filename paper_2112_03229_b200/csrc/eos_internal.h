@@ -44,7 +44,7 @@ struct TablePlan {
   int max_occ = 0;
   int steps = 0;           // ceil(log2(max_occ + 1))
   // search tables (kernels.cuh lookup_b): directory entries of 16 bits
-  // (lo | occ << 12, n <= 4096 and max_occ <= 15) or 32 bits in the image;
+  // (8 lo | occ, n <= 8192 and max_occ <= 7) or 32 bits in the image;
   // fast_steps = SF fixed lifting steps (0: all S in a runtime loop); big =
   // some bin holds >= 2^SF entries (its larger strides run in a rare branch)
   bool dir16 = false;
@@ -56,9 +56,9 @@ struct TablePlan {
   int64_t image_bytes = 0; // X region + directory (16-B padded)
 };
 
-// 16-bit directory entries: lo | occ << 12 (lo <= n - 1 < 4096, occ <= 15)
-constexpr int64_t kDir16MaxN = 4096;
-constexpr int kDir16MaxOcc = 15;
+// 16-bit directory entries: 8 lo | occ (8 (n - 1) + 7 < 2^16, occ <= 7)
+constexpr int64_t kDir16MaxN = 8192;
+constexpr int kDir16MaxOcc = 7;
 constexpr int kMaxFastSteps = 3;  // fixed-step lifting bodies SF = 1..3 (kernels.cuh)
 
 // Smem budget of the automatic hash choice (bytes of X + directory): one image

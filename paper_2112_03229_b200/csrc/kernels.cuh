@@ -115,20 +115,23 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // Directory entry formats (eos_internal.h TablePlan::dir16): a 32-bit entry
-// lo | occ << 16 (any table), or a 16-bit entry lo | occ << 12 (search tables
-// with n <= 4096 and every bin holding <= 15 entries: half the shared memory
-// per bin, so twice the bins in the same image).
+// lo | occ << 16 (any table), or a 16-bit entry 8 lo | occ (search tables with
+// n <= 8192 and every bin holding <= 7 entries: half the shared memory per bin,
+// so twice the bins in the same image).  The 16-bit entry holds the byte offset
+// of X[lo] with the occupancy in its three low (alignment) bits, so the entry's
+// address is one add away: pa = &X[0] + d - occ.
+// Sets pa = shared address of X[lo] and r = occ.
 template <bool D16>
-__device__ __forceinline__ void dir_entry(const void* __restrict__ sD, uint32_t b, int32_t& lo,
-                                          int32_t& occ) {
+__device__ __forceinline__ void dir_entry(const void* __restrict__ sD, uint32_t b, uint32_t xa,
+                                          uint32_t& pa, int32_t& r) {
   if (D16) {
     const uint32_t d = reinterpret_cast<const uint16_t*>(sD)[b];
-    lo = (int32_t)(d & 0xFFFu);
-    occ = (int32_t)(d >> 12);
+    r = (int32_t)(d & 7u);
+    pa = xa + d - (uint32_t)r;
   } else {
     const uint32_t d = reinterpret_cast<const uint32_t*>(sD)[b];
-    lo = (int32_t)(d & 0xFFFFu);
-    occ = (int32_t)(d >> 16);
+    r = (int32_t)(d >> 16);
+    pa = xa + 8u * (d & 0xFFFFu);
   }
 }
 
@@ -208,11 +211,11 @@ __device__ __forceinline__ int32_t lookup_b(double y, const double* __restrict__
   const uint32_t key = key_hi<MODE>(y);
   const uint32_t b = MODE == 0 ? bin_of_m0(key, a) : bin_of(key, a);
   EOS_DCHECK(b <= a.bmax);
-  int32_t lo, r;
-  dir_entry<D16>(sD, b, lo, r);
-  EOS_DCHECK(lo + r <= a.n && r < (1 << a.steps));
   const uint32_t xa = smem_u32(sX);
-  uint32_t pa = xa + 8u * (uint32_t)lo;
+  uint32_t pa;
+  int32_t r;
+  dir_entry<D16>(sD, b, xa, pa, r);
+  EOS_DCHECK((int32_t)((pa - xa) >> 3) + r <= a.n && r < (1 << a.steps));
   if (SF == 0) {
     for (int32_t s = 1 << (a.steps - 1); s > 0; s >>= 1) lift_step_rt(y, pa, r, s);
   } else {

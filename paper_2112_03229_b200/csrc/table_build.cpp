@@ -196,8 +196,8 @@ double cost_of(double mean_probes, double issue, int64_t image_bytes) {
 // in spite of 30% fewer instructions: each branch is a reconvergence point, so
 // the 8 lookups of a thread no longer overlap their shared-memory latencies;
 // DESIGN.md §12.)  16-bit directory entries (n <= 4096, occupancy <= 15) are
-// taken when their smaller image is cheaper (cost_of shape term) despite the
-// extra unpack instruction (0.25).
+// taken whenever they fit (8 lo | occ: n <= 8192, occupancy <= 7): their unpack
+// costs the same two instructions as the 32-bit entry's, and the image is smaller.
 Layout choose_layout(const std::vector<int64_t>& runs, int64_t n, int64_t bins, int steps,
                      double probes_per_bin, bool search) {
   Layout best;
@@ -214,10 +214,10 @@ Layout choose_layout(const std::vector<int64_t>& runs, int64_t n, int64_t bins, 
   best.sf = sf;
   best.big = big;
   best.cost = cost_of(probes_per_bin, issue, best.image);
-  if (can16) {
+  if (can16) {  // (unpacking either format takes two instructions; smaller image wins ties)
     const int64_t img = image_of(n, bins, true);
-    const double c = cost_of(probes_per_bin, issue + 0.25, img);
-    if (c < best.cost - 1e-9) {
+    const double c = cost_of(probes_per_bin, issue, img);
+    if (c < best.cost + 1e-9) {
       best.dir16 = true;
       best.image = img;
       best.cost = c;
@@ -504,10 +504,10 @@ std::vector<uint8_t> make_key_image(const TablePlan& p) {
 std::vector<uint8_t> make_image(const TablePlan& p) {
   std::vector<uint8_t> img((size_t)p.image_bytes, 0);
   memcpy(img.data(), p.X.data(), (size_t)(8 * p.n));
-  if (p.dir16) {  // lo | occ << 12 (kernels.cuh dir_entry)
+  if (p.dir16) {  // 8 lo | occ (kernels.cuh dir_entry)
     for (int64_t b = 0; b < p.bins; ++b) {
       const uint32_t d = p.dir[b];
-      const uint16_t e = (uint16_t)((d & 0xFFFu) | ((d >> 16) << 12));
+      const uint16_t e = (uint16_t)(((d & 0xFFFFu) << 3) | (d >> 16));
       memcpy(img.data() + p.x_bytes + 2 * b, &e, 2);
     }
   } else {

@@ -449,7 +449,7 @@ def test_automatic_plan_is_the_argmin_of_the_cost_model(name):
     runs of the sorted keys) equals the argmin of the DESIGN.md §6.3 cost model recomputed
     here from every candidate's full directory, over every lifting layout (16/32-bit
     directory entries, SF fixed steps, rare branch): 3.5 + 6.1 E[probes] + issue + shape
-    penalty, issue = S + [S > 3] + 0.25 [16-bit entries], SF = min(S, 3);
+    penalty, issue = S + [S > 3], SF = min(S, 3), 16-bit entries whenever they fit;
     ties to the smaller image, then the exponent hash, image budget 200 KB."""
     X = datagen.workload(name, count=10).table
     n = X.size
@@ -471,10 +471,10 @@ def test_automatic_plan_is_the_argmin_of_the_cost_model(name):
         issue = S + (1.0 if big else 0.0)
         img32 = pad16(8 * n) + pad16(4 * info.bins)
         best_l = (3.5 + 6.1 * probes + issue + shape(img32), img32, 0, sf, big)
-        if n <= 4096 and occ.max() <= 15:
+        if n <= 8192 and occ.max() <= 7:
             img16 = pad16(8 * n) + pad16(2 * info.bins)
-            c16 = 3.5 + 6.1 * probes + issue + 0.25 + shape(img16)
-            if c16 < best_l[0] - 1e-9:
+            c16 = 3.5 + 6.1 * probes + issue + shape(img16)
+            if c16 < best_l[0] + 1e-9:
                 best_l = (c16, img16, 1, sf, big)
         return best_l
 
