@@ -80,8 +80,11 @@ def fuzz_1d(rng, dev, stats):
             raise
         return
     # mostly small launches (the small-tile shape); one in four large enough for the default
-    # tiles (>= half the SMs' worth of tiles)
-    m = int(rng.integers(1, 1 << 16)) if rng.integers(0, 4) else int(rng.integers(1 << 18, 1 << 19))
+    # tiles (>= half the SMs' worth of tiles); one in sixteen large enough for the ring
+    # kernel of deep tables (>= 4 stages of 7936 targets per SM)
+    u = int(rng.integers(0, 16))
+    m = int(rng.integers(1, 1 << 16)) if u >= 4 else (
+        int(rng.integers(1 << 18, 1 << 19)) if u >= 1 else int(rng.integers(4_700_000, 6_000_000)))
     Y = targets_for(rng, X, m)
     got = t.search(torch.from_numpy(Y).to(dev)).cpu().numpy()
     ref = oracle.search(X, Y)
@@ -116,8 +119,8 @@ def fuzz_2d(rng, dev, stats):
     R, T = axis(nR, -4, 4), axis(nT, 0, 6)
     if R.size < 2 or T.size < 2:
         return
-    if loglog:
-        G = R[:, None] ** 1.1 * T[None, :] ** 0.6 * (1 + 0.01 * rng.uniform(-1, 1, (R.size, T.size)))
+    if loglog:  # rough surfaces (R24's log1p form needs no smoothness)
+        G = np.exp(rng.uniform(-10, 10, (R.size, T.size)))
     else:
         G = rng.uniform(-5, 5, (R.size, T.size))
     gl = bool(rng.integers(0, 2))
