@@ -42,6 +42,7 @@ struct eos_grid2d_s {
   int32_t flags = 0;
   int32_t rr_off = 0, rt_off = 0;
   int rep = 0;  // 2: bank-pinned cell records in the image (REP kernels), 0: plain axes
+  bool narrow = false;  // log-log: every cell ratio X[j+1]/X[j] <= 1.5 (kernels.cuh log1p_cell)
   int32_t rep_shift = 0;       // REP 2: log2 of the record copies
   int64_t rep_bytes_axis = 0;  // image bytes per axis entry of the REP layout
   bool gg = false;          // grid in device memory (GG kernels)
@@ -138,6 +139,7 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   a.rt_off = g->rt_off;
   a.gq = reinterpret_cast<const double2*>(g->grid_dev);
   a.rep_shift = g->rep_shift;
+  a.narrow = g->narrow ? 1 : 0;
   a.r = g->ar;
   a.t = g->at;
   a.rho = rho;
@@ -307,6 +309,12 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
       const double v = gval(q);
       memcpy(img.data() + g->g_off + 8 * q, &v, 8);
     }
+  }
+  if (loglog) {  // the short log1p series of the weights needs every cell ratio <= 1.5
+    bool nw = true;
+    for (const std::vector<double>* ax : {&g->pr.X, &g->pt.X})
+      for (size_t q = 0; q + 1 < ax->size(); ++q) nw = nw && (*ax)[q + 1] <= 1.5 * (*ax)[q];
+    g->narrow = nw;
   }
   g->ar = axis_params(g->pr, 0);
   g->at = axis_params(g->pt, (int32_t)r_bytes);
