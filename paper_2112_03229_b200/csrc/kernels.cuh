@@ -1089,15 +1089,22 @@ struct Interp2DArgs {
 // log1p(d) for the log-log weight of a cell with X[c+1]/X[c] <= 1.5 (grids whose
 // cells all are, Interp2DArgs::narrow): inside the cell d = (x - X[c])/X[c] is in
 // [0, 0.5], and log1p(d) = 2 atanh(u), u = d/(2+d) in [0, 0.2], is the odd series
-// 2u (1 + u^2/3 + ... + u^22/23): 12 terms reach 2^-53 (u^2 <= 0.04), one divide and
-// 11 FMAs against ~60 instructions of the general log1p.  Outside the cell only the
+// 2u (1 + u^2/3 + ... + u^22/23): 12 terms reach 2^-53 (u^2 <= 0.04): a reciprocal
+// estimate, 15 FMAs and no branch, against the general log1p's called routine.  Outside the cell only the
 // clamped weight matters: d < 0 gives a negative value, d > 0.5 a value above
 // ln 1.5 >= the cell width (the partial sums grow with u), so both clamp as the
 // exact log1p would; d = +inf is held at 1e300 (weight 1), d < -1 (x < 0) and NaN
 // give NaN as log1p does, d = -1 (x = 0) a negative value (weight 0, as -inf).
 __device__ __forceinline__ double log1p_cell(double d) {
   const double dd = d > 1e300 ? 1e300 : d;  // (NaN passes through)
-  const double u = __ddiv_rn(dd, __dadd_rn(2.0, dd));
+  // u = dd / (2 + dd) by the hardware reciprocal estimate and two Newton steps (the
+  // correctly rounded divide is a called routine with slow paths): within ~2 ulp
+  const double a = __dadd_rn(2.0, dd);
+  double rc;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(a));
+  rc = __fma_rn(rc, __fma_rn(-a, rc, 1.0), rc);
+  rc = __fma_rn(rc, __fma_rn(-a, rc, 1.0), rc);
+  const double u = __dmul_rn(dd, rc);
   const double u2 = __dmul_rn(u, u);
   double p = 2.0 / 23.0;
   p = __fma_rn(p, u2, 2.0 / 21.0);
