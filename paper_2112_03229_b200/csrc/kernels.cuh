@@ -276,44 +276,8 @@ struct SmemLookup {
   AxisParams a;
   template <int N>
   __device__ __forceinline__ void many(const double (&y)[N], int32_t (&r)[N]) const {
-    if (SF == 3 && !BIG && N > 1) {
-      many_s3(y, r);
-      return;
-    }
 #pragma unroll
     for (int i = 0; i < N; ++i) r[i] = lookup_b<SF, BIG, MODE, D16>(y[i], sX, sD, a);
-  }
-  // S = 3 tables, a batch of N lookups: the directory entries first, then one vote of the
-  // (active lanes of the) warp -- if no lane's batch holds a bin of >= 4 entries, every
-  // lookup skips the stride-4 step (six instructions that would move no data).  One
-  // warp-uniform branch per batch, not per lookup, so the N lookups still overlap.
-  template <int N>
-  __device__ __forceinline__ void many_s3(const double (&y)[N], int32_t (&r)[N]) const {
-    const uint32_t xa = smem_u32(sX);
-    uint32_t pa[N];
-    int32_t rr[N];
-    bool deep = false;
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const uint32_t key = key_hi<MODE>(y[i]);
-      const uint32_t b = MODE == 0 ? bin_of_m0(key, a) : bin_of(key, a);
-      EOS_DCHECK(b <= a.bmax);
-      dir_entry<D16>(sD, b, xa, pa[i], rr[i]);
-      EOS_DCHECK((int32_t)((pa[i] - xa) >> 3) + rr[i] <= a.n && rr[i] < 8);
-      deep |= rr[i] >= 4;
-    }
-    if (__any_sync(__activemask(), deep)) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) lift_fixed<3>(y[i], pa[i], rr[i]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < N; ++i) lift_fixed<2>(y[i], pa[i], rr[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const int32_t idx = (int32_t)(pa[i] - xa - 8u) >> 3;  // lo + c - 1
-      r[i] = (y[i] >= a.x0) ? idx : 0;
-    }
   }
   __device__ __forceinline__ double x_at(int32_t i) const { return sX[i]; }
 };
