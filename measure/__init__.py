@@ -45,7 +45,8 @@ def lib():
         L.probe_stream2d.argtypes = [_P, _P, _P, _P, _P, _I64, _P]
         L.probe_fill.argtypes = [_P, _U64, _P]
         L.probe_gather.argtypes = [_P, _U64, _I, _I, _P, _P]
-        for f in (L.probe_stream, L.probe_stream2d, L.probe_fill, L.probe_gather,
+        L.probe_gather_line.argtypes = [_P, _U64, _I, _I, _P, _P]
+        for f in (L.probe_stream, L.probe_stream2d, L.probe_fill, L.probe_gather, L.probe_gather_line,
                   L.probe_stream_variants, L.probe_sms):
             f.restype = _I
         _lib = L
@@ -129,3 +130,27 @@ def l2_gather_ceiling(buffer_bytes: int, rounds: int = 64, reps: int = 5) -> dic
             "all_gsectors_per_s": {str(k): round(v / 1e9, 2) for k, v in res.items()},
             "what": f"random 32-B sector gathers, {nsm} SMs x 1024 threads x chains, {rounds} "
                     "dependent rounds, ld.global.nc.L1::no_allocate.v8.u32"}
+
+
+def l2_line_gather_ceiling(buffer_bytes: int, rounds: int = 64, reps: int = 5) -> dict:
+    """Random 128-B line gathers where 4 lanes load the 4 sectors of one line with one
+    instruction (measure/probes.cu k_gather_line); best lines/s over 1..8 chains."""
+    import torch
+    L = lib()
+    lines = 1
+    while 2 * lines * 128 <= buffer_bytes:
+        lines *= 2
+    buf = torch.empty(32 * lines, dtype=torch.int32, device="cuda")
+    sink = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream()
+    _check(L.probe_fill(buf.data_ptr(), 32 * lines, st.cuda_stream), "probe_fill")
+    nsm = L.probe_sms()
+    res = {}
+    for g in (1, 2, 4, 8):
+        ms = _time(lambda: _check(L.probe_gather_line(buf.data_ptr(), lines, g, rounds,
+                                                      sink.data_ptr(), st.cuda_stream),
+                                  "probe_gather_line"), reps, st)
+        res[g] = nsm * 1024 // 4 * g * rounds / (ms * 1e-3)
+    best = max(res, key=res.get)
+    return {"lines_per_s": res[best], "chains": best, "buffer_bytes": 128 * lines,
+            "all_glines_per_s": {str(k): round(v / 1e9, 2) for k, v in res.items()}}

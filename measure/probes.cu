@@ -371,6 +371,40 @@ __global__ void __launch_bounds__(1024, 1) k_gather(const uint32_t* __restrict__
   if (acc == 0x12345678u) sink[0] = acc;  // practically never: keeps the loads live
 }
 
+// Cooperative line gathers: groups of 4 lanes load the 4 sectors of one random 128-B
+// line (one 256-bit load per lane), G chains per thread: how many random LINES per second
+// the L1TEX t-stage serves when each line is requested whole by one instruction.
+template <int G>
+__global__ void __launch_bounds__(1024, 1) k_gather_line(const uint32_t* __restrict__ buf,
+                                                        uint64_t lmask, int rounds,
+                                                        uint32_t* __restrict__ sink) {
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = threadIdx.x & 3;             // this lane's sector of the group's line
+  const uint64_t grp = tid >> 2;
+  uint64_t s[G];
+  uint32_t acc = 0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) s[g] = smix(grp * G + g) & lmask;
+  for (int r = 0; r < rounds; ++r) {
+    uint32_t k[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(k[g][0]), "=r"(k[g][1]), "=r"(k[g][2]), "=r"(k[g][3]), "=r"(k[g][4]),
+                     "=r"(k[g][5]), "=r"(k[g][6]), "=r"(k[g][7])
+                   : "l"(buf + 32 * s[g] + 8 * q));
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      uint32_t x = k[g][0] ^ k[g][3] ^ k[g][7];
+      x ^= __shfl_xor_sync(0xFFFFFFFFu, x, 1);  // the group agrees on the next line
+      x ^= __shfl_xor_sync(0xFFFFFFFFu, x, 2);
+      acc += x;
+      s[g] = (s[g] * 0x9E3779B97F4A7C15ULL + x + 1) & lmask;
+    }
+  }
+  if (acc == 0x12345678u) sink[0] = acc;
+}
+
 __global__ void k_fill(uint32_t* buf, uint64_t words) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride)
@@ -487,6 +521,23 @@ int probe_gather(const uint32_t* buf, uint64_t sectors, int chains, int rounds, 
     case 2: k_gather<2><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
     case 4: k_gather<4><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
     default: k_gather<8><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
+  }
+  return (int)cudaGetLastError();
+}
+
+// Random 128-B line gathers by 4-lane groups (one 32-B sector per lane); lines loaded =
+// sms * 1024 / 4 * chains * rounds.  lines a power of two.
+int probe_gather_line(const uint32_t* buf, uint64_t lines, int chains, int rounds, uint32_t* sink,
+                      void* stream) {
+  if (lines == 0 || (lines & (lines - 1))) return (int)cudaErrorInvalidValue;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = sms();
+  const uint64_t mask = lines - 1;
+  switch (chains) {
+    case 1: k_gather_line<1><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
+    case 2: k_gather_line<2><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
+    case 4: k_gather_line<4><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
+    default: k_gather_line<8><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
   }
   return (int)cudaGetLastError();
 }

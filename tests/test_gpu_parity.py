@@ -200,6 +200,51 @@ def test_ring_launches_ragged_and_misaligned(count, y_off, o_off, table, kw):
     t.close()
 
 
+@pytest.mark.parametrize("case", ["mode1_s2", "mode1_deep", "dups_s3", "zero_head_s3", "s2_d16",
+                                  "n8192_s3", "k0_deep", "d32_deep"])
+def test_ring_kernel_layouts(case):
+    """Ring-kernel launches (>= 4 stages per SM) over every layout it can get: key modes 0
+    and 1, S = 2 and 3 (16-bit entries), deep tables with the stride branch (S >= 4, 32-bit
+    entries), a 0.0 head with subnormals, duplicate runs, the largest 16-bit table; bit-exact
+    against the oracle."""
+    rng = np.random.default_rng(sum(map(ord, case)))
+    kw = {}
+    if case == "mode1_s2":       # key mode 1 (all negative), S = 2
+        X = np.sort(rng.uniform(-5, -1, 1000))
+    elif case == "mode1_deep":   # key mode 1 (both signs), S = 6
+        X = np.sort(rng.uniform(-50, 50, 1000))
+    elif case == "dups_s3":
+        X = np.sort(np.repeat(10 ** rng.uniform(-2, 4, 500), 3))
+    elif case == "zero_head_s3":
+        X = np.concatenate([np.zeros(3), np.sort(10 ** rng.uniform(-300, 2, 2000))])
+        kw = {"log_bins": 1500}
+    elif case == "s2_d16":
+        X = np.sort(10 ** rng.uniform(-3, 5, 2000))
+        kw = {"log_bins": 16000}
+    elif case == "n8192_s3":     # the largest table with 16-bit entries, a 101 KB image
+        X = np.sort(10 ** rng.uniform(-6, 10, 8192))
+    elif case == "k0_deep":      # the paper's exponent hash on cfg5: S = 9
+        X = datagen.table_cfg5(4)
+        kw = {"k": 0}
+    else:                        # S = 4, 32-bit entries
+        X = np.sort(10 ** rng.uniform(-3, 5, 6000))
+        kw = {"log_bins": 3000}
+    t = eos.Table(X, **kw)
+    assert t.info.steps >= 2, t.info.as_dict()
+    m = 5_000_003
+    lo, hi = float(X[0]), float(X[-1])
+    if lo > 0:
+        Y = 10 ** rng.uniform(np.log10(lo) - 0.3, np.log10(hi) + 0.3, m)
+    else:
+        Y = rng.uniform(lo - 1, hi + 1, m)
+    Y[:X.size] = X
+    Y[X.size:X.size + 6] = [np.nan, np.inf, -np.inf, 0.0, -0.0, 5e-324]
+    got = t.search(to_dev(Y)).cpu().numpy()
+    assert t.info.ring_stages >= 2, t.info.as_dict()
+    assert_same(got, oracle.search(X, Y), Y)
+    t.close()
+
+
 @pytest.mark.parametrize("table,kw", [("cfg1", {}), ("cfg2", {"log_bins": 12000}),
                                       ("cfg5", {}), ("cfg5", {"log_bins": 5000}),
                                       ("cfg2", {"k": 0})])
