@@ -548,3 +548,14 @@ def test_interp_host_rejects_bad_host_buffers(bad):
     with pytest.raises((TypeError, ValueError)):
         g.interp_host(rho, T, P, iR, iT, sync=False)
     g._h = None
+
+
+@pytest.mark.parametrize("kw", [{"k": 0}, {"k": 3}, {"log_bins": 4096}, {}])
+def test_tiered_explicit_hash_fits_its_key_image(kw):
+    """A tiered table's sample table is staged as 32-bit keys: an explicit hash is accepted
+    when the KEY image fits shared memory (the fp64 image of a 31250-entry sample table
+    would not), as the automatic choice is."""
+    X = np.sort(10.0 ** np.random.default_rng(5).uniform(-6, 10, 250_000))
+    info = eos.eos_plan_table_levels(X, eos.EOS_LEVELS_AUTO, **kw)
+    assert info.levels == 1 and info.top_n == 31250
+    assert info.image_bytes <= 200 * 1024
