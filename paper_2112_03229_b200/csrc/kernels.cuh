@@ -144,25 +144,25 @@ __device__ __forceinline__ void dir_entry(const void* __restrict__ sD, uint32_t 
 // the range predicate in (DSETP.AND), the updates are predicated: 5 SASS
 // instructions per step, 4 for the last one (no r update), no branches.
 template <int S, bool LAST>
-__device__ __forceinline__ void lift_step(double y, uint32_t& pa, int32_t& r) {
+__device__ __forceinline__ void lift_step(double y, uint32_t& pa, int32_t& r, double& x) {
+  // x: the probe register, defined once per lookup (its value is never used when the
+  // probe is predicated off: the compare ANDs the range predicate in)
   if (LAST) {
-    asm("{\n\t.reg .pred pi, pt;\n\t.reg .f64 x;\n\t"
-        "setp.ge.s32 pi, %1, %3;\n\t"
-        "mov.b64 x, 0;\n\t"
-        "@pi ld.shared.f64 x, [%0+%4];\n\t"
-        "setp.le.and.f64 pt, x, %2, pi;\n\t"
-        "@pt add.u32 %0, %0, %5;\n\t}"
-        : "+r"(pa)
+    asm("{\n\t.reg .pred pi, pt;\n\t"
+        "setp.ge.s32 pi, %2, %4;\n\t"
+        "@pi ld.shared.f64 %1, [%0+%5];\n\t"
+        "setp.le.and.f64 pt, %1, %3, pi;\n\t"
+        "@pt add.u32 %0, %0, %6;\n\t}"
+        : "+r"(pa), "+d"(x)
         : "r"(r), "d"(y), "n"(S), "n"(8 * (S - 1)), "n"(8 * S));
   } else {
-    asm("{\n\t.reg .pred pi, pt;\n\t.reg .f64 x;\n\t"
-        "setp.ge.s32 pi, %1, %3;\n\t"
-        "mov.b64 x, 0;\n\t"
-        "@pi ld.shared.f64 x, [%0+%4];\n\t"
-        "setp.le.and.f64 pt, x, %2, pi;\n\t"
-        "@pt add.u32 %0, %0, %5;\n\t"
-        "@pt sub.s32 %1, %1, %3;\n\t}"
-        : "+r"(pa), "+r"(r)
+    asm("{\n\t.reg .pred pi, pt;\n\t"
+        "setp.ge.s32 pi, %1, %4;\n\t"
+        "@pi ld.shared.f64 %2, [%0+%5];\n\t"
+        "setp.le.and.f64 pt, %2, %3, pi;\n\t"
+        "@pt add.u32 %0, %0, %6;\n\t"
+        "@pt sub.s32 %1, %1, %4;\n\t}"
+        : "+r"(pa), "+r"(r), "+d"(x)
         : "d"(y), "n"(S), "n"(8 * (S - 1)), "n"(8 * S));
   }
 }
@@ -184,10 +184,11 @@ __device__ __forceinline__ void lift_step_rt(double y, uint32_t& pa, int32_t& r,
 // strides 2^(S-1) .. 1; only the stride-1 step (the last) skips the r update
 template <int S>
 __device__ __forceinline__ void lift_fixed(double y, uint32_t& pa, int32_t& r) {
-  if (S >= 4) lift_step<8, false>(y, pa, r);
-  if (S >= 3) lift_step<4, false>(y, pa, r);
-  if (S >= 2) lift_step<2, false>(y, pa, r);
-  if (S >= 1) lift_step<1, true>(y, pa, r);
+  double x = 0.0;
+  if (S >= 4) lift_step<8, false>(y, pa, r, x);
+  if (S >= 3) lift_step<4, false>(y, pa, r, x);
+  if (S >= 2) lift_step<2, false>(y, pa, r, x);
+  if (S >= 1) lift_step<1, true>(y, pa, r, x);
 }
 
 // The hot per-target body:
@@ -699,7 +700,7 @@ __device__ __forceinline__ void search_body(const SearchArgs& args, const LK& lk
 
 template <int SF, bool BIG, int MODE, bool D16, bool CNT, class SH>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) search1d_kernel(const SearchArgs args) {
-  extern __shared__ __align__(16) uint4 smem[];
+  extern __shared__ __align__(128) uint4 smem[];
   __shared__ __align__(16) uint4 clc_resp;
   __shared__ __align__(8) uint64_t clc_bar, stage_bar;
   if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
@@ -864,7 +865,7 @@ __global__ void __launch_bounds__(1024, 1) search1d_ring_kernel(const SearchArgs
 template <int S, int MODE, bool CNT, class SH>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
     search1d_tiered_kernel(const SearchArgs args) {
-  extern __shared__ __align__(16) uint4 smem[];
+  extern __shared__ __align__(128) uint4 smem[];
   __shared__ __align__(16) uint4 clc_resp;
   __shared__ __align__(8) uint64_t clc_bar, stage_bar;
   if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
@@ -920,7 +921,7 @@ template <class SH>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
     search1d_direct_kernel(const DirectArgs A) {
   constexpr int T = SH::kThreads;
-  extern __shared__ __align__(16) uint4 smem[];
+  extern __shared__ __align__(128) uint4 smem[];
   __shared__ __align__(16) uint4 clc_resp;
   __shared__ __align__(8) uint64_t clc_bar;
   __shared__ AxisParams sa;
@@ -1317,7 +1318,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
   constexpr int U = SH::kUnroll;
   constexpr int TP = SH::kTilePairs;
   constexpr int TE = SH::kTileElems;
-  extern __shared__ __align__(16) uint4 smem[];
+  extern __shared__ __align__(128) uint4 smem[];
   __shared__ __align__(16) uint4 clc_resp;
   __shared__ __align__(8) uint64_t clc_bar, stage_bar;
   if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
