@@ -346,6 +346,7 @@ def run_ours(a, d: Dist):
             "traffic": ncu_traffic(a.workload, count, plan),
             "kernel": "interp2d_kernel" if is2d else (
                 "search1d_direct_kernel" if a.direct else
+                "search1d_packed_kernel" if obj.info.node_width == 15 else
                 "search1d_tiered_kernel" if obj.info.levels > 0 else "search1d_kernel"),
             "kernel_ms_avg": round(kern_ms, 5),
             "kernel_ms_avg_max_rank": round(kern_ms_max, 5),
@@ -365,10 +366,12 @@ def run_ours(a, d: Dist):
         "trials": trials,
     }
     if not is2d and obj.info.levels > 0:
-        # tiered table: each level reads one 32-B sector from L2; random
-        # sector gathers, not HBM, bound it.  Ceiling measured now (measure/probes.cu:
-        # the same 256-bit load, an L2-resident buffer of the levels' size).
-        gl = measure.l2_gather_ceiling(max(int(obj.info.level_bytes), 1 << 20))
+        # tiered table: each level reads one 32-B sector from L2 (packed
+        # tables: one level of nodes); random sector gathers, not HBM, bound it.  Ceiling
+        # measured now (measure/probes.cu: the same 256-bit load, an L2-resident buffer of
+        # the gathered levels' size).
+        gathered = (32 * obj.info.top_n if obj.info.node_width == 15 else obj.info.level_bytes)
+        gl = measure.l2_gather_ceiling(max(int(gathered), 1 << 20))
         levels = obj.info.levels
         ach = levels * count / (kern_ms * 1e-3)
         res["roofline"]["l2"] = {
@@ -409,7 +412,8 @@ def plan_signature(a, obj, is2d):
     return {"kind": "tiered" if i.levels > 0 else ("direct" if a.direct else "search"),
             "hash_kind": i.hash_kind, "bins": i.bins, "steps": i.steps,
             "dir_entry_bytes": i.dir_entry_bytes, "fast_steps": i.fast_steps,
-            "rare_steps": i.rare_steps, "levels": i.levels, "ring_stages": i.ring_stages}
+            "rare_steps": i.rare_steps, "levels": i.levels, "node_width": i.node_width,
+            "ring_stages": i.ring_stages}
 
 
 def run_e2e(a, d, w, obj, offset, count, total, is2d, dev):

@@ -41,7 +41,8 @@ extern "C" {
 
 #define EOS_MAX_TABLE 16384 /* table entries staged in shared memory (fp64) */
 #define EOS_MAX_TABLE_TIERED (1 << 29) /* entries of a tiered table */
-#define EOS_LEVELS_AUTO (-1)           /* eos_search_create_levels: choose D */
+#define EOS_LEVELS_AUTO (-1)           /* eos_search_create_levels: choose the structure */
+#define EOS_LEVELS_PACKED (-2)         /* eos_search_create_levels: one level of packed nodes */
 #define EOS_MAX_K 19        /* mantissa bits appended to the exponent hash */
 #define EOS_K_AUTO (-1)     /* let eos_search_create_ex choose the hash */
 
@@ -84,9 +85,10 @@ typedef struct {
   /* tiered tables (eos_search_create_levels); levels == 0: the fields above
    * describe the whole table.  levels = D >= 1: the fields above (except n)
    * describe the shared-memory sample table T1 of top_n entries. */
-  int32_t levels;      /* D: 8-ary levels in global memory */
-  int32_t pad_;
-  int64_t top_n;       /* n1 = ceil(n / 8^D) (image_bytes then counts 4 B per T1 entry) */
+  int32_t levels;      /* D: levels of nodes in global memory */
+  int32_t node_width;  /* entries per node: 8 (8-ary key levels), 15 (packed), 0 (D = 0) */
+  int64_t top_n;       /* n1 = ceil(n / 8^D), or ceil(n / 15) packed (image_bytes then counts
+                        * 4 B, packed 2 B, per T1 entry) */
   int64_t level_bytes; /* device bytes of the levels (0 when D == 0) */
   /* lifting layout of the search kernel (ABI >= 3): directory entries of 2 B
    * (8 lo | occ) or 4 B (lo | occ << 16) in the image; fast_steps = the
@@ -170,8 +172,9 @@ EOS_API eos_status eos_search_create_hash(const double* table_host, int64_t n, i
                                   eos_table* out);
 
 /* Tables of any size ("tables larger than smem"), 1 <= n <=
- * EOS_MAX_TABLE_TIERED.  Same result for every n; eos_search_create*
- * call this with levels = EOS_LEVELS_AUTO, so they accept the same n.
+ * EOS_MAX_TABLE_TIERED.  Same result for every n and structure;
+ * eos_search_create* call this with levels = EOS_LEVELS_AUTO, so they accept
+ * the same n.
  *   levels = D: 0 = the whole table (and directory) in shared memory
  *     (n <= EOS_MAX_TABLE); D >= 1 (<= 5) = a two-level structure: the
  *     sample table T1[j] = X[j 8^D], j < n1 = ceil(n/8^D) <= 32768, held as
@@ -182,13 +185,27 @@ EOS_API eos_status eos_search_create_hash(const double* table_host, int64_t n, i
  *     n1 8^(D-d) entries (~1.7 x 8n bytes in all).  A level step reads the
  *     8 keys of a node (one 32-byte sector): c = #{t : key_t < key(y)}, and
  *     the node's fp64 values only when a key equals key(y); b = 8b + c - 1.
- *     EOS_LEVELS_AUTO: D = 0 if n <= EOS_MAX_TABLE, else the smallest D with
- *     n1 <= 32768.
+ *   levels = EOS_LEVELS_PACKED: one level of packed nodes (info: levels = 1,
+ *     node_width = 15).  Node j is one 32-byte sector holding the key of
+ *     X[15j] (rounded down to a multiple of 32, its low 5 bits a shift s_j)
+ *     and the 16-bit residuals ((key(X[15j+t]) - base) >> s_j) + 0x400,
+ *     t = 1..14 (<= 0x7BFF: positive normal fp16 patterns; 0x7C00 past n); the
+ *     sample table T1[j] = X[15j], j < n1 = ceil(n/15), is held in shared
+ *     memory as the low sh <= 16 bits of its keys, binned by the key's upper
+ *     bits (the exponent hash with k = 20 - sh), with 32-bit directory entries.
+ *     A lookup reads one node from L2; equal residuals are settled from the
+ *     fp64 table in device memory (8n + 32 n1 bytes in all).  Fits while the
+ *     sample table and its directory take <= 224 KB (n up to ~1.5e6 for
+ *     log-spread tables); otherwise EOS_ERR_UNSUPPORTED.  kind/param ignored.
+ *     EOS_LEVELS_AUTO: D = 0 if n <= EOS_MAX_TABLE; else packed if n > 8 x
+ *     32768 (where 8-ary levels need D >= 2), it fits and kind is
+ *     EOS_HASH_AUTO; else the smallest D with n1 <= 32768.
  *   kind/param: the hash of the shared-memory table (T1 when D >= 1), as in
  *     eos_search_create_hash.
  * Errors: EOS_ERR_SIZE (n out of range, or n1 too large for the given D:
- * > EOS_MAX_TABLE at D = 0, > 32768 at D >= 1), EOS_ERR_UNSUPPORTED (D > 5),
- * EOS_ERR_NOMEM, plus the table errors of eos_plan_table. */
+ * > EOS_MAX_TABLE at D = 0, > 32768 at D >= 1), EOS_ERR_UNSUPPORTED (D > 5,
+ * or a packed table that does not fit), EOS_ERR_NOMEM, plus the table errors
+ * of eos_plan_table. */
 EOS_API eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t levels,
                                             int32_t kind, int64_t param, eos_table* out);
 
@@ -333,7 +350,7 @@ EOS_API eos_status eos_grid2d_destroy(eos_grid2d g);
  * Misc
  * ------------------------------------------------------------------------- */
 EOS_API const char* eos_status_str(eos_status s); /* static string, never NULL */
-EOS_API int32_t eos_abi_version(void);            /* 3 */
+EOS_API int32_t eos_abi_version(void);            /* 4 */
 /* Kernel launches issued by this library since load (all entry points). */
 EOS_API int64_t eos_launch_count(void);
 

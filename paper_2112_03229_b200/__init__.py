@@ -32,17 +32,18 @@ __all__ = [
     "eos_search_direct", "search_direct", "eos_grid2d_create_ex", "EOS_GRID_LINEAR",
     "EOS_GRID_LOGLOG", "EOS_MAX_TABLE_TIERED", "EOS_LEVELS_AUTO", "eos_search_create_levels",
     "eos_plan_table_levels", "plan_table_levels", "EOS_GRID_GLOBAL", "EOS_MAX_GRID_CELLS",
-    "EOS_GRID_EXACT", "ABI_VERSION",
+    "EOS_GRID_EXACT", "ABI_VERSION", "EOS_LEVELS_PACKED",
 ]
 
 EOS_MAX_TABLE = 16384
 EOS_MAX_TABLE_TIERED = 1 << 29
 EOS_LEVELS_AUTO = -1
+EOS_LEVELS_PACKED = -2
 EOS_MAX_K = 19
 EOS_K_AUTO = -1
 EOS_HASH_AUTO, EOS_HASH_EXPONENT, EOS_HASH_LOG = 0, 1, 2
 EOS_GRID_LINEAR, EOS_GRID_LOGLOG, EOS_GRID_GLOBAL, EOS_GRID_EXACT = 0, 1, 2, 4
-ABI_VERSION = 3
+ABI_VERSION = 4
 EOS_MAX_GRID_CELLS = 1 << 28
 
 STATUS = {
@@ -75,7 +76,7 @@ class TableInfo(ctypes.Structure):
                 ("base", ctypes.c_int32), ("image_bytes", ctypes.c_int64),
                 ("device", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
                 ("hash_kind", ctypes.c_int32), ("hash_mult", ctypes.c_uint32),
-                ("levels", ctypes.c_int32), ("pad_", ctypes.c_int32), ("top_n", ctypes.c_int64),
+                ("levels", ctypes.c_int32), ("node_width", ctypes.c_int32), ("top_n", ctypes.c_int64),
                 ("level_bytes", ctypes.c_int64), ("dir_entry_bytes", ctypes.c_int32),
                 ("fast_steps", ctypes.c_int32), ("rare_steps", ctypes.c_int32),
                 ("ring_stages", ctypes.c_int32)]
@@ -244,7 +245,8 @@ plan_table = eos_plan_table
 
 def eos_plan_table_levels(table, levels: int = EOS_LEVELS_AUTO, k: int | None = EOS_K_AUTO,
                           log_bins: int | None = None) -> TableInfo:
-    """Host-only plan of a (possibly tiered) table: levels = D (-1 = automatic)."""
+    """Host-only plan of a (possibly tiered) table: levels = D (-1 = automatic, -2 =
+    packed)."""
     X = _f64_host(table)
     info = TableInfo()
     kind, param = _hash_args(k, log_bins)
@@ -381,7 +383,8 @@ class Table:
         """k: exponent hash with k mantissa bits; log_bins: logarithm hash with |H| bins;
         neither: the automatic choice.  levels: D 8-ary global levels
         under a shared-memory sample table (tables above EOS_MAX_TABLE entries need
-        D >= 1; -1 = automatic).  Results never depend on any of them."""
+        D >= 1), EOS_LEVELS_PACKED (one level of packed 16-bit residual nodes, DESIGN.md
+        §6.5) or EOS_LEVELS_AUTO.  Results never depend on any of them."""
         self.X = _f64_host(table)
         self._h = eos_search_create_levels(self.X, levels, *_hash_args(k, log_bins))
         self.info = eos_table_info(self._h)

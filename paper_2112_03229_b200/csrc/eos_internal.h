@@ -121,6 +121,52 @@ struct TieredPlan {
 eos_status plan_tiered(const double* X, int64_t n, int levels, int kind, int64_t param,
                        TieredPlan* out);
 
+// Packed tables (eossearch.h EOS_LEVELS_PACKED): one level of 32-byte nodes
+// of 16-bit residual keys under a shared-memory sample table of 16-bit
+// residual keys, so a lookup gathers ONE sector from L2 (the 8-ary levels
+// above gather D).
+//   nodes:  node j covers X[15 j .. 15 j + 15) (kPackedNode entries); word 0 is
+//           B_j | s_j with B_j = key(X[15 j]) & ~31 and s_j (< 32) the
+//           smallest shift with (key(X[last of node]) - B_j) >> s_j <= 0x77FF;
+//           words 1..7 hold the 14 residuals r_t = ((key(X[15 j + t]) - B_j) >>
+//           s_j) + 0x400, t = 1..14, two per word (t odd in the low half), and
+//           0x7C00 past n: as fp16 bit patterns these are normal positive
+//           halves (or +inf past n) in the order of the keys, so the kernel
+//           compares two per HSET2.
+//   sample: T1[j] = X[15 j], j < n1 = ceil(n / 15), binned by the key-bit hash
+//           bin = min((max(key, hb) - hb) >> sh, bmax) (hb aligned to 2^sh: the
+//           exponent hash of k = 20 - sh mantissa bits); the image holds the
+//           residuals key(T1[j]) & (2^sh - 1) as u16, sh <= 16, then the
+//           directory u32 lo | occ << 24.
+// Truncation keeps the order: r(X) < r(y) => X < y and r(X) > r(y) => X > y;
+// equal residuals are settled from the fp64 values (X in device memory).
+constexpr int kPackedNode = 15;
+constexpr uint32_t kPackedResMax = 0x77FFu;   // largest residual (biased: 0x7BFF)
+constexpr uint32_t kPackedResBias = 0x0400u;  // smallest normal fp16
+constexpr uint32_t kPackedResPad = 0x7C00u;   // +inf: past n
+constexpr int kPackedMaxSteps = 8;                 // occ <= 255 (8-bit field)
+constexpr int64_t kPackedMaxTop = int64_t(1) << 24;  // lo field
+constexpr int64_t kPackedImageBudget = 224 * 1024;   // one 1024-thread CTA per SM
+struct PackedPlan {
+  int64_t n = 0;              // entries
+  int64_t n1 = 0;             // sample entries (nodes)
+  int key_mode = 0;
+  int sh = 0;                 // residual bits of the sample table
+  uint32_t hb = 0, bmax = 0;
+  int bins = 0, max_occ = 0, steps = 0;
+  double x0 = 0.0, x_last = 0.0;
+  std::vector<double> X;      // canonicalised table (device: X then the nodes)
+  std::vector<uint32_t> nodes;  // 8 words per node
+  std::vector<uint8_t> image;   // smem image: u16 residuals | u32 directory
+};
+// EOS_ERR_UNSUPPORTED when no sh <= 16 gives an image within `budget` and bins of
+// <= 255 entries (eos_search_create_levels then uses 8-ary levels under AUTO).
+eos_status plan_packed(const double* X, int64_t n, PackedPlan* out,
+                       int64_t budget = kPackedImageBudget);
+void fill_info(const PackedPlan& p, eos_table_info_t* info);
+// The sample table of a packed plan as a TablePlan (hash fields, occupancy, T1).
+TablePlan packed_top(const PackedPlan& p);
+
 // Serialise X | dir into a 16-B padded byte image.
 std::vector<uint8_t> make_image(const TablePlan& p);
 

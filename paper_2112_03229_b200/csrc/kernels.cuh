@@ -20,6 +20,7 @@
 // template constant of the launch).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -82,7 +83,7 @@ struct SearchArgs {
   const uint32_t* kv;
   int64_t lv_top_len;            // 8 n1: length of level D-1
   int32_t levels;                // D (0: single-level smem table)
-  int32_t pad2_;
+  int32_t sh;                    // packed tables: residual bits of the sample table
 };
 
 // splitmix64 finalizer (the checksum of counter c2; independent of oracle/)
@@ -427,6 +428,137 @@ struct TieredLookup {
     for (int i = 0; i < N; ++i) r[i] = (y[i] >= a.x0) ? b[i] : 0;
   }
   __device__ __forceinline__ double x_at(int32_t i) const { return __ldg(x_full + i); }
+};
+
+// PackedLookup (packed tables, eossearch.h EOS_LEVELS_PACKED; layout in
+// eos_internal.h PackedPlan): ONE L2 sector per lookup.  Per target:
+//   sample (smem): u = max(key, hb) - hb, bin b = min(u >> sh, bmax), rk = the
+//     low sh bits of u (0xFFFF past the last bin); lifting counts the bin's
+//     residuals < rk, equal residuals settled from X[15 j] (global);
+//     j = max(#{T1 <= y} - 1, 0)
+//   node j (one 32-B sector, ld.global.nc, L1 no-allocate): B | s, r_1..r_14;
+//     ry = min((max(key, B) - B) >> s, 0x77FF); the residuals are sorted, so
+//     lt = #{r_t < ry} and le = #{r_t <= ry} (fp16x2 compares of the biased
+//     values, 14 at a time in 7 HSET2 each) bound the run of equal residuals,
+//     settled from X[15 j + t] (rare)
+//   idx = (y >= X[0]) ? 15 j + lt + #{ties <= y} : 0
+// Invariant: X[15 j] <= y < X[15 (j + 1)] for X[0] <= y, so the node's first
+// entry counts and idx = #{X <= y} - 1.
+// Node residuals are stored biased by kResBias (the smallest normal fp16) so
+// that two of them compare as one fp16x2 (HSET2): every stored value is a
+// normal positive half or +inf (0x7C00, past the end), whose bit order is its
+// value order.  eos_internal.h kPackedResMax / kPackedResBias.
+constexpr uint32_t kResMax = 0x77FFu;
+constexpr uint32_t kResBias = 0x0400u;
+__device__ __forceinline__ __half2 u32_as_h2(uint32_t w) {
+  __half2 h;
+  memcpy(&h, &w, 4);
+  return h;
+}
+__device__ __forceinline__ uint32_t h2_as_u32(__half2 h) {
+  uint32_t w;
+  memcpy(&w, &h, 4);
+  return w;
+}
+
+template <int S, int MODE>
+struct PackedLookup {
+  static constexpr bool kBatchTail = false;
+  const uint16_t* __restrict__ sR;  // sample residuals (smem)
+  const uint32_t* __restrict__ sD;  // directory lo | occ << 24 (smem)
+  AxisParams a;                     // n = n1; hb, bmax of the sample hash; x0, xlast of X
+  uint32_t sh;
+  const double* __restrict__ X;       // the table (global)
+  const uint32_t* __restrict__ nodes;  // 8 words per node (global, 32-B aligned)
+
+  // Sample lookups of N targets, step-major (the N lifting chains interleave);
+  // equal residuals are settled after all chains, in a branch taken rarely.
+  template <int N>
+  __device__ __forceinline__ void sample(const double (&y)[N], const uint32_t (&ky)[N],
+                                         int32_t (&j)[N]) const {
+    uint32_t rk[N];
+    int32_t lo[N], occ[N], c[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const uint32_t u =
+          MODE == 0 ? (uint32_t)max((int32_t)(ky[i] - a.hb), 0) : max(ky[i], a.hb) - a.hb;
+      const uint32_t q = u >> sh;
+      const uint32_t b = min(q, a.bmax);
+      rk[i] = q > a.bmax ? 0xFFFFu : (u & ((1u << sh) - 1u));
+      const uint32_t d = sD[b];
+      lo[i] = (int32_t)(d & 0xFFFFFFu);
+      occ[i] = (int32_t)(d >> 24);
+      c[i] = 0;
+      EOS_DCHECK(lo[i] + occ[i] <= a.n && occ[i] < (1 << S));
+    }
+#pragma unroll
+    for (int s = 1 << (S - 1); s > 0; s >>= 1) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int32_t t = c[i] + s;
+        if (t <= occ[i] && sR[lo[i] + t - 1] < rk[i]) c[i] = t;
+      }
+    }
+    bool tie[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) tie[i] = c[i] < occ[i] && sR[lo[i] + c[i]] == rk[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (tie[i]) {
+        // equal residuals (a prefix of the rest of the bin): the exact values
+        for (int32_t st = 1 << (31 - __clz(occ[i] - c[i])); st > 0; st >>= 1) {
+          const int32_t t = c[i] + st;
+          if (t <= occ[i] && sR[lo[i] + t - 1] == rk[i] &&
+              __ldg(X + 15 * (int64_t)(lo[i] + t - 1)) <= y[i])
+            c[i] = t;
+        }
+      }
+      j[i] = max(lo[i] + c[i] - 1, 0);
+    }
+  }
+
+  template <int N>
+  __device__ __forceinline__ void many(const double (&y)[N], int32_t (&r)[N]) const {
+    int32_t j[N];
+    uint32_t ky[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) ky[i] = key_hi<MODE>(y[i]);
+    sample(y, ky, j);
+    uint32_t k[N][8];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      EOS_DCHECK(j[i] >= 0 && j[i] < a.n);
+      ldg_keys8(nodes + 8 * (int64_t)j[i], k[i]);
+    }
+    int32_t lt[N], le[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const uint32_t B = k[i][0] & ~31u, s = k[i][0] & 31u;
+      const uint32_t ry = min((max(ky[i], B) - B) >> s, kResMax) + kResBias;
+      const __half2 hy = u32_as_h2(ry * 0x10001u);
+      // lane sums start at 512 (ulp 0.5) so the final 1024 + count is exact
+      __half2 a = u32_as_h2(0x60006000u), e = a;
+#pragma unroll
+      for (int w = 1; w < 8; ++w) {
+        a = __hadd2(a, __hlt2(u32_as_h2(k[i][w]), hy));
+        e = __hadd2(e, __hle2(u32_as_h2(k[i][w]), hy));
+      }
+      const uint32_t t = h2_as_u32(__hadd2(__lows2half2(a, e), __highs2half2(a, e)));
+      lt[i] = (int32_t)(t & 0xFFFFu) - 0x6400;  // 1024.0 = 0x6400, ulp 1
+      le[i] = (int32_t)(t >> 16) - 0x6400;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      int32_t cnt = lt[i];
+      if (le[i] > lt[i]) {  // equal residuals (rare): the fp64 values of the run
+        const double* f = X + 15 * (int64_t)j[i] + 1;
+#pragma unroll 1
+        for (int32_t e = lt[i]; e < le[i]; ++e) cnt += __ldg(f + e) <= y[i];
+      }
+      r[i] = (y[i] >= a.x0) ? 15 * j[i] + cnt : 0;
+    }
+  }
+  __device__ __forceinline__ double x_at(int32_t i) const { return __ldg(X + i); }
 };
 
 // ---- Blackwell cluster launch control + mbarrier (inline PTX, sm_100a) ----
@@ -888,6 +1020,31 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
     len *= 8;
   }
   lk.x_full = args.lv + off;
+  search_body<CNT, SH>(args, lk, &clc_resp, &clc_bar);
+}
+
+// Packed tables (PackedLookup): the smem image holds the sample residuals and
+// their directory; X and the nodes stay in global memory / L2.
+template <int S, int MODE, bool CNT, class SH>
+__global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
+    search1d_packed_kernel(const SearchArgs args) {
+  extern __shared__ __align__(128) uint4 smem[];
+  __shared__ __align__(16) uint4 clc_resp;
+  __shared__ __align__(8) uint64_t clc_bar, stage_bar;
+  if (SH::kClc && threadIdx.x == 0) mbar_init(&clc_bar, 1);
+  stage_image(smem, args.image, args.image_16, &stage_bar);
+  pdl_enter();
+  const AxisParams a = args.ax;
+  EOS_DCHECK(args.levels == 1 && args.sh >= 1 && args.sh <= 16 &&
+             a.d_off + 4 * ((int64_t)a.bmax + 1) <= 16 * (int64_t)args.image_16 &&
+             2 * (int64_t)a.n <= a.d_off && 15 * ((int64_t)a.n - 1) < args.lv_top_len);
+  PackedLookup<S, MODE> lk;
+  lk.sR = reinterpret_cast<const uint16_t*>(reinterpret_cast<const char*>(smem) + a.x_off);
+  lk.sD = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(smem) + a.d_off);
+  lk.a = a;
+  lk.sh = (uint32_t)args.sh;
+  lk.X = args.lv;
+  lk.nodes = args.kv;
   search_body<CNT, SH>(args, lk, &clc_resp, &clc_bar);
 }
 

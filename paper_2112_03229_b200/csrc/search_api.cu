@@ -24,6 +24,9 @@ using namespace eos::rt;
 struct eos_table_s {
   TablePlan plan;          // the shared-memory table (T1 of a tiered table)
   int levels = 0;          // D (tiered tables, eos_search_create_levels)
+  int node_width = 0;      // 8: 8-ary key levels; 15: packed nodes (eos_internal.h PackedPlan)
+  int sh = 0;              // packed: residual bits of the sample table
+  const uint32_t* nodes_dev = nullptr;  // packed: the nodes (inside levels_dev, after X)
   int64_t n = 0;           // entries of the full table
   int64_t top_n = 0;       // n1
   int64_t level_bytes = 0;
@@ -112,6 +115,26 @@ const void* tiered_fn_mode(int steps, bool cnt) {
     default: return tiered_fn<0, MODE, SH>(cnt);
   }
 }
+
+// packed tables: search1d_packed_kernel, S = 1..kPackedMaxSteps
+template <int MODE, class SH, bool CNT>
+const void* packed_fn(int steps) {
+  switch (steps) {
+    case 1: return (const void*)dv::search1d_packed_kernel<1, MODE, CNT, SH>;
+    case 2: return (const void*)dv::search1d_packed_kernel<2, MODE, CNT, SH>;
+    case 3: return (const void*)dv::search1d_packed_kernel<3, MODE, CNT, SH>;
+    case 4: return (const void*)dv::search1d_packed_kernel<4, MODE, CNT, SH>;
+    case 5: return (const void*)dv::search1d_packed_kernel<5, MODE, CNT, SH>;
+    case 6: return (const void*)dv::search1d_packed_kernel<6, MODE, CNT, SH>;
+    case 7: return (const void*)dv::search1d_packed_kernel<7, MODE, CNT, SH>;
+    default: return (const void*)dv::search1d_packed_kernel<8, MODE, CNT, SH>;
+  }
+}
+template <class SH, bool CNT>
+const void* packed_fn_mode(int mode, int steps) {
+  return mode == 0 ? packed_fn<0, SH, CNT>(steps) : packed_fn<1, SH, CNT>(steps);
+}
+static_assert(eos::kPackedMaxSteps == 8, "packed_fn covers S = 1..8");
 
 // Small launches of tiered tables: 512 x 1 tiles (a quarter of the default
 // 1024 x 2), used like the single-level small shapes when the default tiles
@@ -288,6 +311,11 @@ eos_status launch_search(eos_table t, const double* Y, int64_t count, int32_t* o
   a.kv = t->levels_dev ? reinterpret_cast<const uint32_t*>(t->levels_dev + t->level_elems) : nullptr;
   a.lv_top_len = 8 * t->top_n;
   a.levels = t->levels;
+  if (t->node_width == eos::kPackedNode) {  // X, then the nodes
+    a.kv = t->nodes_dev;
+    a.lv_top_len = t->n;
+    a.sh = t->sh;
+  }
   // Vector body needs Y+head 16-B aligned and out+head 8-B aligned.
   const uintptr_t ya = (uintptr_t)Y, oa = (uintptr_t)out;
   a.head = (ya & 15) ? 1 : 0;
@@ -361,9 +389,41 @@ eos_status eos_search_create_hash(const double* table_host, int64_t n, int32_t k
   return eos_search_create_levels(table_host, n, EOS_LEVELS_AUTO, kind, param, out);
 }
 
+// Packed plan for levels = EOS_LEVELS_PACKED, or EOS_LEVELS_AUTO above
+// EOS_MAX_TABLE with the automatic hash (an explicit hash is honoured by the
+// 8-ary levels).  *use = false: take the other structures (AUTO and the packed
+// plan does not fit, or levels >= 0).
+static eos_status try_packed(const double* table_host, int64_t n, int32_t levels, int32_t kind,
+                             eos::PackedPlan* pp, bool* use) {
+  *use = false;
+  // AUTO: packed where the 8-ary structure needs two or more levels, i.e. two
+  // or more L2 gathers per lookup (n > 8 kMaxTopKeys); one 8-ary level beats a
+  // packed table's deeper sample bins
+  if (levels != EOS_LEVELS_PACKED &&
+      !(levels == EOS_LEVELS_AUTO && kind == EOS_HASH_AUTO && n > 8 * eos::kMaxTopKeys))
+    return EOS_OK;
+  const eos_status st = eos::plan_packed(table_host, n, pp);
+  if (st == EOS_OK) {
+    *use = true;
+    return EOS_OK;
+  }
+  if (levels == EOS_LEVELS_AUTO && (st == EOS_ERR_UNSUPPORTED || st == EOS_ERR_SIZE)) return EOS_OK;
+  return st;
+}
+
 eos_status eos_plan_table_levels(const double* table_host, int64_t n, int32_t levels, int32_t kind,
                                  int64_t param, eos_table_info_t* info) {
   if (!info) return EOS_ERR_NULL;
+  {
+    eos::PackedPlan pp;
+    bool use = false;
+    const eos_status st = try_packed(table_host, n, levels, kind, &pp, &use);
+    if (st != EOS_OK) return st;
+    if (use) {
+      eos::fill_info(pp, info);
+      return EOS_OK;
+    }
+  }
   eos::TieredPlan tp;
   eos_status st = eos::plan_tiered(table_host, n, levels, kind, param, &tp);
   if (st != EOS_OK) return st;
@@ -371,10 +431,86 @@ eos_status eos_plan_table_levels(const double* table_host, int64_t n, int32_t le
   return EOS_OK;
 }
 
+// A packed table's handle: the sample image in smem, X and the nodes in one
+// device allocation (X first; the nodes 32-B aligned after it).
+static eos_status create_packed(eos::PackedPlan&& pp, eos_table* out) {
+  eos_table t = new (std::nothrow) eos_table_s();
+  if (!t) return EOS_ERR_NOMEM;
+  auto fail = [&](eos_status st) {
+    if (t->image_dev) cudaFree(t->image_dev);
+    if (t->levels_dev) cudaFree(t->levels_dev);
+    delete t;
+    return st;
+  };
+  t->plan = eos::packed_top(pp);
+  t->levels = 1;
+  t->node_width = eos::kPackedNode;
+  t->sh = pp.sh;
+  t->n = pp.n;
+  t->top_n = pp.n1;
+  t->smem_bytes = (int64_t)pp.image.size();
+  const int64_t x_bytes = (8 * pp.n + 31) & ~int64_t(31);
+  t->level_bytes = x_bytes + 32 * pp.n1;
+  dv::AxisParams& a = t->ax;
+  a.n = (int32_t)pp.n1;
+  a.x_off = 0;
+  a.d_off = (int32_t)t->plan.x_bytes;
+  a.hb = pp.hb;
+  a.M = t->plan.M;
+  a.bmax = pp.bmax;
+  a.steps = pp.steps;
+  a.mode = pp.key_mode;
+  a.x0 = pp.x0;
+  a.xlast = pp.x_last;
+  cudaError_t e = cudaGetDevice(&t->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, t->device);
+  if (e != cudaSuccess) return fail(cuda_status(e));
+  eos_status st = upload(pp.image, &t->image_dev);
+  if (st != EOS_OK) return fail(st);
+  e = cudaMalloc((void**)&t->levels_dev, (size_t)t->level_bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(t->levels_dev, pp.X.data(), 8 * pp.X.size(), cudaMemcpyHostToDevice);
+  t->nodes_dev = reinterpret_cast<const uint32_t*>(reinterpret_cast<char*>(t->levels_dev) + x_bytes);
+  if (e == cudaSuccess)
+    e = cudaMemcpy((void*)t->nodes_dev, pp.nodes.data(), 4 * pp.nodes.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return fail(cuda_status(e));
+  const int mode = pp.key_mode, S = pp.steps;
+  t->fn[0] = packed_fn_mode<dv::ShapeTiered, false>(mode, S);
+  t->threads[0] = dv::ShapeTiered::kThreads;
+  t->unroll[0] = dv::ShapeTiered::kUnroll;
+  t->clc[0] = dv::ShapeTiered::kClc;
+  t->fn[1] = packed_fn_mode<dv::ShapeCnt, true>(mode, S);
+  t->threads[1] = dv::ShapeCnt::kThreads;
+  t->unroll[1] = dv::ShapeCnt::kUnroll;
+  t->clc[1] = dv::ShapeCnt::kClc;
+  for (int c = 0; c < 2 && st == EOS_OK; ++c)
+    st = configure(t->fn[c], t->threads[c], t->smem_bytes, t->num_sms, &t->grid[c],
+                   c == 0 ? &t->ctas_per_sm : nullptr);
+  if (st != EOS_OK) return fail(st);
+  if (!exp_small_off()) {
+    using SS = dv::Shape<512, 1, 1, false>;
+    const void* fs = packed_fn_mode<SS, false>(mode, S);
+    if (configure(fs, SS::kThreads, t->smem_bytes, t->num_sms, &t->grid_small, nullptr) == EOS_OK) {
+      t->fn_small = fs;
+      t->threads_small = SS::kThreads;
+      t->unroll_small = SS::kUnroll;
+      t->clc_small = SS::kClc;
+    }
+  }
+  *out = t;
+  return EOS_OK;
+}
+
 eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t levels,
                                     int32_t kind, int64_t param, eos_table* out) {
   if (!out) return EOS_ERR_NULL;
   *out = nullptr;
+  {
+    eos::PackedPlan pp;
+    bool use = false;
+    const eos_status st = try_packed(table_host, n, levels, kind, &pp, &use);
+    if (st != EOS_OK) return st;
+    if (use) return create_packed(std::move(pp), out);
+  }
   eos_table t = new (std::nothrow) eos_table_s();
   if (!t) return EOS_ERR_NOMEM;
   std::vector<double> lv;
@@ -388,6 +524,7 @@ eos_status eos_search_create_levels(const double* table_host, int64_t n, int32_t
     if (tp.levels == 0) exp_layout(&t->plan);
 #endif
     t->levels = tp.levels;
+    t->node_width = tp.levels > 0 ? 8 : 0;
     t->n = tp.n;
     t->top_n = tp.top_n;
     t->level_bytes = 12 * tp.level_elems();
@@ -595,6 +732,7 @@ eos_status eos_table_info(eos_table t, eos_table_info_t* out) {
   eos::fill_info(t->plan, out);
   out->n = t->n;
   out->levels = t->levels;
+  out->node_width = t->node_width;
   out->top_n = t->top_n;
   out->level_bytes = t->level_bytes;
   out->image_bytes = t->smem_bytes;

@@ -489,6 +489,137 @@ eos_status plan_tiered(const double* Xin, int64_t n, int levels, int kind, int64
   return EOS_OK;
 }
 
+eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t budget) {
+  if (!Xin || !out) return EOS_ERR_NULL;
+  if (n < 1 || n > EOS_MAX_TABLE_TIERED) return EOS_ERR_SIZE;
+  const int64_t n1 = (n + kPackedNode - 1) / kPackedNode;
+  if (n1 > kPackedMaxTop) return EOS_ERR_SIZE;
+  if (pad16(2 * n1) + 16 > budget) return EOS_ERR_UNSUPPORTED;  // before touching X
+  PackedPlan p;
+  p.n = n;
+  p.n1 = n1;
+  try {
+    p.X.resize((size_t)n);
+  } catch (...) {
+    return EOS_ERR_NOMEM;
+  }
+  for (int64_t j = 0; j < n; ++j) {  // same rules as plan_table
+    const double v = Xin[j];
+    if (!isfinite(v)) return EOS_ERR_NONFINITE;
+    p.X[j] = (v == 0.0) ? 0.0 : v;  // canonicalise -0.0 (R6)
+    if (j > 0 && p.X[j] < p.X[j - 1]) return EOS_ERR_UNSORTED;
+  }
+  const int mode = (p.X[0] >= 0.0) ? 0 : 1;
+  p.key_mode = mode;
+  p.x0 = p.X[0];
+  p.x_last = p.X[n - 1];
+  std::vector<uint32_t> K1((size_t)n1);
+  std::vector<double> T1((size_t)n1);
+  for (int64_t j = 0; j < n1; ++j) {
+    T1[j] = p.X[j * kPackedNode];
+    K1[j] = key_hi(T1[j], mode);
+  }
+  const uint32_t lowk = low_key(T1, mode), top = K1[n1 - 1];
+  // sample hash: the residual width sh (16 .. 1) with the fewest lifting
+  // steps whose image fits; ties go to the smaller image
+  const int64_t rbytes = pad16(2 * n1);
+  std::vector<int32_t> cnt;
+  for (int sh = 16; sh >= 1; --sh) {
+    const uint32_t hb = lowk & ~((1u << sh) - 1u);
+    const int64_t bins = (int64_t)((top > hb ? top - hb : 0) >> sh) + 1;
+    if (rbytes + pad16(4 * bins) > budget) break;  // more bins at smaller sh
+    cnt.assign((size_t)bins, 0);
+    int max_occ = 0;
+    for (int64_t j = 0; j < n1; ++j) {
+      const uint32_t b = bin_of_key(K1[j], hb, 1u << (32 - sh), (uint32_t)(bins - 1));
+      max_occ = std::max(max_occ, ++cnt[b]);
+    }
+    if (max_occ > (1 << kPackedMaxSteps) - 1) continue;
+    const int S = ceil_log2_plus1(max_occ);
+    if (p.sh == 0 || S < p.steps) {
+      p.sh = sh;
+      p.hb = hb;
+      p.bins = (int)bins;
+      p.bmax = (uint32_t)(bins - 1);
+      p.max_occ = max_occ;
+      p.steps = S;
+    }
+  }
+  if (p.sh == 0) return EOS_ERR_UNSUPPORTED;
+  const int sh = p.sh;
+  const uint32_t mask = (1u << sh) - 1u;
+  try {
+    p.image.assign((size_t)(rbytes + pad16(4 * (int64_t)p.bins)), 0);
+    p.nodes.assign((size_t)(8 * n1), 0);
+  } catch (...) {
+    return EOS_ERR_NOMEM;
+  }
+  // sample residuals (the kernel's rk of the entry's own key) and directory
+  std::vector<uint32_t> lo((size_t)p.bins, 0), occ((size_t)p.bins, 0);
+  for (int64_t j = 0; j < n1; ++j) {
+    const uint32_t u = (K1[j] > p.hb ? K1[j] : p.hb) - p.hb;
+    const uint16_t r = (uint16_t)(u & mask);
+    memcpy(p.image.data() + 2 * j, &r, 2);
+    const uint32_t b = std::min(u >> sh, p.bmax);
+    if (occ[b]++ == 0) lo[b] = (uint32_t)j;
+  }
+  uint32_t next = 0;  // empty bins: lo = first entry of the next non-empty bin
+  for (int64_t b = p.bins - 1; b >= 0; --b) {
+    if (occ[b] == 0) lo[b] = next;
+    else next = lo[b];
+  }
+  for (int64_t b = 0; b < p.bins; ++b) {
+    const uint32_t d = lo[b] | (occ[b] << 24);
+    memcpy(p.image.data() + rbytes + 4 * b, &d, 4);
+  }
+  // nodes
+  for (int64_t j = 0; j < n1; ++j) {
+    const int64_t i0 = j * kPackedNode;
+    const int64_t last = std::min<int64_t>(i0 + kPackedNode - 1, n - 1);
+    const uint32_t Bm = key_hi(p.X[i0], mode) & ~31u;
+    const uint32_t span = key_hi(p.X[last], mode) - Bm;
+    uint32_t s = 0;
+    while ((span >> s) > kPackedResMax) ++s;
+    uint32_t* w = p.nodes.data() + 8 * j;
+    w[0] = Bm | s;
+    for (int t = 1; t < kPackedNode; ++t) {
+      const int64_t i = i0 + t;
+      const uint32_t r =
+          i < n ? ((key_hi(p.X[i], mode) - Bm) >> s) + kPackedResBias : kPackedResPad;
+      w[(t + 1) / 2] |= (t & 1) ? r : (r << 16);
+    }
+  }
+  *out = std::move(p);
+  return EOS_OK;
+}
+
+TablePlan packed_top(const PackedPlan& p) {
+  TablePlan t;
+  t.n = p.n1;
+  t.key_mode = p.key_mode;
+  t.hash_kind = EOS_HASH_EXPONENT;
+  t.k = 20 - p.sh;
+  t.hb = p.hb;
+  t.M = 1u << (32 - p.sh);
+  t.bmax = p.bmax;
+  t.bins = p.bins;
+  t.max_occ = p.max_occ;
+  t.steps = p.steps;
+  t.fast_steps = p.steps;
+  t.x_bytes = pad16(2 * p.n1);
+  t.image_bytes = (int64_t)p.image.size();
+  return t;
+}
+
+void fill_info(const PackedPlan& p, eos_table_info_t* info) {
+  fill_info(packed_top(p), info);
+  info->n = p.n;
+  info->levels = 1;
+  info->node_width = kPackedNode;
+  info->top_n = p.n1;
+  info->level_bytes = ((8 * p.n + 31) & ~int64_t(31)) + 32 * p.n1;  // X, then the nodes
+}
+
 int64_t key_image_bytes(const TablePlan& p) { return pad16(4 * p.n) + pad16(4 * p.bins); }
 
 std::vector<uint8_t> make_key_image(const TablePlan& p) {
@@ -530,7 +661,7 @@ void fill_info(const TablePlan& p, eos_table_info_t* info) {
   info->hash_kind = p.hash_kind;
   info->hash_mult = p.M;
   info->levels = 0;
-  info->pad_ = 0;
+  info->node_width = 0;
   info->top_n = p.n;
   info->level_bytes = 0;
   info->dir_entry_bytes = p.dir16 ? 2 : 4;
@@ -544,6 +675,7 @@ void fill_info(const TieredPlan& t, eos_table_info_t* info) {
   if (t.levels > 0) info->image_bytes = key_image_bytes(t.top);  // keys, not fp64
   info->n = t.n;
   info->levels = t.levels;
+  info->node_width = t.levels > 0 ? 8 : 0;
   info->top_n = t.top_n;
   info->level_bytes = 12 * t.level_elems();  // fp64 F + u32 K per level entry
 }

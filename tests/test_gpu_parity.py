@@ -934,11 +934,12 @@ def test_tiered_large_tables_full(n, kind):
 
 def test_tiered_big_workload_full_sampled_and_counters():
     """The bench's `big` workload (n = 2^20, 2^27 targets) in the bench's launch
-    configuration: 2^20 sampled outputs vs the oracle, the bracketing invariant on
-    every output, and the counters of the whole stream vs the oracle's."""
+    configuration (the automatic structure: packed nodes): 2^20 sampled outputs vs the
+    oracle, the bracketing invariant on every output, and the counters of the whole
+    stream vs the oracle's."""
     w = datagen.workload("big")
     t = eos.Table(w.table)
-    assert t.info.levels == 2
+    assert t.info.levels == 1 and t.info.node_width == 15
     Yd = torch.empty(w.count, dtype=torch.float64, device=DEV)
     w.targets.device_fill(Yd, 0)
     out = t.search(Yd)
@@ -986,6 +987,106 @@ def test_tiered_host_pipeline_and_counters():
     t.search(to_dev(Y), counters=c, global_offset=off)
     torch.cuda.synchronize()
     assert np.array_equal(c.cpu().numpy().view(np.uint64), oracle.counters(X, Y, ref, off))
+    t.close()
+
+
+# ------------------------------ packed tables (EOS_LEVELS_PACKED, §6.5) -----
+# One level of 15-entry nodes of 16-bit residual keys (one 32-B sector) under a
+# sample table of 16-bit residuals: the same P:54 lower bound, settled exactly
+# from the fp64 values wherever residuals tie.
+PACKED = eos.EOS_LEVELS_PACKED
+
+
+def _packed(X):
+    t = eos.Table(X, levels=PACKED)
+    assert t.info.levels == 1 and t.info.node_width == 15
+    assert t.info.top_n == (X.size + 14) // 15
+    return t
+
+
+@pytest.mark.parametrize("name", sorted(lower_bound_cases().keys()))
+def test_packed_golden(name):
+    X, cases = lower_bound_cases()[name]
+    ys = np.array([c[0] for c in cases] * 37)
+    exp = np.array([c[1] for c in cases] * 37, dtype=np.int32)
+    t = _packed(X)
+    assert_same(t.search(to_dev(ys)).cpu().numpy(), exp, ys)
+    t.close()
+
+
+def test_packed_edge_tables_exhaustive_probes():
+    rng = np.random.default_rng(78)
+    checked = 0
+    for X in _edge_tables(rng, 140):
+        P = _probes(X)
+        P = np.concatenate([P, rng.permutation(np.repeat(P, 3))])
+        t = _packed(X)
+        assert_same(t.search(to_dev(P)).cpu().numpy(), oracle.search(X, P), P)
+        t.close()
+        checked += P.size
+    assert checked > 20_000
+
+
+def _clustered(rng, n):
+    """Tight clusters at log-spread centres: nodes straddle the gaps, so their key
+    spans need shifts s_j > 0 and truncated residuals tie often."""
+    c = 10.0 ** rng.uniform(-30, 30, n // 40 + 1)
+    X = np.repeat(c, 40)[:n] * (1.0 + rng.uniform(0, 1e-9, n))
+    X = np.sort(X)
+    X[:n // 50] = np.sort(rng.uniform(1e-300, 1e-290, n // 50))
+    return np.sort(X)
+
+
+@pytest.mark.parametrize("n,kind", [((1 << 20), "loguniform"), (300_001, "zerohead"),
+                                    (500_003, "dups"), (1_500_001, "loguniform"),
+                                    (333_337, "clustered"), (16_385, "loguniform"),
+                                    (400_001, "mixed")])
+def test_packed_large_tables_full(n, kind):
+    rng = np.random.default_rng(n + 1)
+    X = _clustered(rng, n) if kind == "clustered" else _big_table(rng, n, kind)
+    Y = _big_probes(rng, X, 1 << 20)
+    ref = oracle.search(X, Y)
+    try:
+        t = _packed(X)
+    except eos.EosError as e:  # the sample table does not fit: AUTO takes 8-ary levels
+        assert "UNSUPPORTED" in str(e) and kind in ("mixed", "zerohead"), e
+        t = eos.Table(X)
+        assert t.info.node_width == 8
+    out = t.search(to_dev(Y))
+    torch.cuda.synchronize()
+    assert_same(out.cpu().numpy(), ref, Y)
+    c = torch.zeros(8, dtype=torch.int64, device=DEV)
+    t.search(to_dev(Y[: 1 << 18]), counters=c, global_offset=12345)
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy().view(np.uint64),
+                          oracle.counters(X, Y[: 1 << 18], ref[: 1 << 18], 12345))
+    t.close()
+
+
+@pytest.mark.parametrize("count", [1, 3, 2049, 65_537, 300_001])
+@pytest.mark.parametrize("y_off,o_off", [(0, 0), (1, 1), (3, 2)])
+def test_packed_ragged_misaligned_and_small_launches(count, y_off, o_off):
+    rng = np.random.default_rng(count + 3)
+    X = _big_table(rng, 400_000, "loguniform")
+    Yall = _big_probes(rng, X, count + 64)[: count + 8]
+    yd = to_dev(Yall)[y_off:y_off + count]
+    od_all = torch.full((count + 8,), -7, dtype=torch.int32, device=DEV)
+    od = od_all[o_off:o_off + count]
+    t = _packed(X)
+    t.search(yd, out=od)
+    torch.cuda.synchronize()
+    got = od_all.cpu().numpy()
+    assert_same(got[o_off:o_off + count], oracle.search(X, Yall[y_off:y_off + count]))
+    assert np.all(got[:o_off] == -7) and np.all(got[o_off + count:] == -7)
+    t.close()
+
+
+def test_packed_host_pipeline():
+    rng = np.random.default_rng(6)
+    X = _big_table(rng, 700_001, "loguniform")
+    Y = _big_probes(rng, X, 1 << 21)
+    t = _packed(X)
+    assert_same(t.search_host(np.ascontiguousarray(Y)), oracle.search(X, Y), Y)
     t.close()
 
 

@@ -37,7 +37,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert declared == set(eos.EXPORTED_SYMBOLS)
     for s in declared:
         assert hasattr(L, s), s
-    assert L.eos_abi_version() == 3
+    assert L.eos_abi_version() == 4
     assert eos.eos_status_str(0) == "ok"
     assert "sorted" in eos.eos_status_str(4)
 
@@ -303,11 +303,15 @@ def test_tiered_plan_levels_and_sizes():
     X[::8^D] as 32-bit keys plus its directory."""
     rng = np.random.default_rng(7)
     pad16 = lambda b: (b + 15) // 16 * 16  # noqa: E731
-    for n, D in [(1, 0), (16384, 0), (16385, 1), (262144, 1), (262145, 2), (1 << 20, 2),
+    for n, D in [(1, 0), (16384, 0), (16385, 1), (262144, 1), (262145, -2), (1 << 20, -2),
                  (1 << 21, 2), ((1 << 21) + 1, 3)]:
         X = np.sort(10.0 ** rng.uniform(-6, 10, n))
         info = eos.plan_table_levels(X)
+        if D == -2:  # 8-ary levels would need D = 2: the packed structure (its own test)
+            assert info.levels == 1 and info.node_width == 15, n
+            continue
         assert info.levels == D and info.n == n, (n, info.levels)
+        assert info.node_width == (8 if D else 0)
         n1 = -(-n // 8 ** D)
         assert info.top_n == n1 <= (eos.EOS_MAX_TABLE if D == 0 else 32768)
         assert info.level_bytes == 12 * sum(n1 * 8 ** (D - d) for d in range(D))
@@ -327,6 +331,73 @@ def test_tiered_plan_levels_and_sizes():
     for D in range(0, 6):
         info = eos.plan_table_levels(X, levels=D)
         assert info.levels == D and info.top_n == -(-1000 // 8 ** D)
+
+
+def _keys_mode0(v):
+    return (np.ascontiguousarray(v).view(np.uint64) >> np.uint64(32)).astype(np.int64) & 0x7FFFFFFF
+
+
+@pytest.mark.parametrize("n", [300_001, 1 << 20, 1_500_000, 16_385, 1000])
+def test_packed_plan_fields_and_sample_hash(n):
+    """eos_plan_table_levels(EOS_LEVELS_PACKED) (eos_internal.h PackedPlan): n1 =
+    ceil(n/15) nodes of 32 B after the 32-B padded fp64 table; the sample table
+    X[::15] as u16 residuals plus u32 directory entries within 224 KB; the bins are the
+    key's bits above sh = 20 - k (hb aligned), recounted here, and S is the fewest
+    lifting steps over every residual width that fits."""
+    rng = np.random.default_rng(n)
+    X = np.sort(10.0 ** rng.uniform(-6, 10, n))
+    info = eos.plan_table_levels(X, levels=eos.EOS_LEVELS_PACKED)
+    pad16 = lambda b: (b + 15) // 16 * 16  # noqa: E731
+    n1 = -(-n // 15)
+    assert (info.levels, info.node_width, info.top_n, info.n) == (1, 15, n1, n)
+    assert info.level_bytes == (8 * n + 31) // 32 * 32 + 32 * n1
+    assert info.hash_kind == eos.EOS_HASH_EXPONENT and 4 <= info.k <= 19
+    assert info.dir_entry_bytes == 4
+    budget = 224 * 1024
+    assert info.image_bytes == pad16(2 * n1) + pad16(4 * info.bins) <= budget
+
+    K = _keys_mode0(X[::15])
+
+    def plan(sh):
+        hb = int(K[0]) & ~((1 << sh) - 1)
+        bins = ((int(K[-1]) - hb) >> sh) + 1
+        occ = np.bincount((K - hb) >> sh, minlength=bins)
+        return hb, bins, int(occ.max())
+    sh = 20 - info.k
+    hb, bins, mo = plan(sh)
+    assert (info.base, info.bins, info.max_occ) == (hb, bins, mo)
+    assert info.steps == int(np.ceil(np.log2(mo + 1))) <= 8
+    for other in range(1, 17):
+        _, b2, m2 = plan(other)
+        if pad16(2 * n1) + pad16(4 * b2) <= budget and m2 <= 255:
+            assert int(np.ceil(np.log2(m2 + 1))) >= info.steps, other
+
+
+def test_packed_plan_auto_choice_and_errors():
+    rng = np.random.default_rng(9)
+    X = np.sort(10.0 ** rng.uniform(-6, 10, 400_000))
+    assert eos.plan_table_levels(X).node_width == 15                 # AUTO, n > 8 x 32768
+    assert eos.plan_table_levels(X, k=8).node_width == 8             # explicit hash: 8-ary
+    assert eos.plan_table_levels(X[:200_000]).node_width == 8        # one 8-ary level
+    assert eos.plan_table_levels(X, levels=2).node_width == 8
+    for bad, code in [(np.full(300_000, 2.5), "EOS_ERR_UNSUPPORTED"),   # one bin of 20000
+                      (np.sort(10.0 ** rng.uniform(-6, 10, 4_000_000)), "EOS_ERR_UNSUPPORTED"),
+                      (np.empty(0), "EOS_ERR_SIZE")]:
+        with pytest.raises(eos.EosError) as e:
+            eos.plan_table_levels(bad, levels=eos.EOS_LEVELS_PACKED)
+        assert e.value.name == code
+    # AUTO falls back to 8-ary levels when packed does not fit
+    assert eos.plan_table_levels(np.full(300_000, 2.5)).node_width == 8
+    bad = X.copy()
+    bad[1000] = np.nan
+    with pytest.raises(eos.EosError) as e:
+        eos.plan_table_levels(bad, levels=eos.EOS_LEVELS_PACKED)
+    assert e.value.name == "EOS_ERR_NONFINITE"
+    bad = X.copy()
+    bad[1000], bad[1001] = bad[1001], bad[1000]
+    with pytest.raises(eos.EosError) as e:
+        eos.plan_table_levels(bad)
+    assert e.value.name == "EOS_ERR_UNSORTED"
 
 
 def test_tiered_plan_errors():
