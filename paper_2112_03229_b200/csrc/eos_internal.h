@@ -137,15 +137,16 @@ eos_status plan_tiered(const double* X, int64_t n, int levels, int kind, int64_t
 //           bin = min((max(key, hb) - hb) >> sh, bmax) (hb aligned to 2^sh: the
 //           exponent hash of k = 20 - sh mantissa bits); the image holds the
 //           residuals key(T1[j]) & (2^sh - 1) as u16, sh <= 16, then the
-//           directory u32 lo | occ << 24.
+//           directory: one u32 per pair of bins (2g, 2g + 1), lo(2g) | occ(2g)
+//           << 20 | occ(2g + 1) << 26 (occ <= 63, n1 <= 2^20).
 // Truncation keeps the order: r(X) < r(y) => X < y and r(X) > r(y) => X > y;
 // equal residuals are settled from the fp64 values (X in device memory).
 constexpr int kPackedNode = 15;
 constexpr uint32_t kPackedResMax = 0x77FFu;   // largest residual (biased: 0x7BFF)
 constexpr uint32_t kPackedResBias = 0x0400u;  // smallest normal fp16
 constexpr uint32_t kPackedResPad = 0x7C00u;   // +inf: past n
-constexpr int kPackedMaxSteps = 8;                 // occ <= 255 (8-bit field)
-constexpr int64_t kPackedMaxTop = int64_t(1) << 24;  // lo field
+constexpr int kPackedMaxSteps = 6;                 // occ <= 63 (6-bit fields)
+constexpr int64_t kPackedMaxTop = int64_t(1) << 20;  // lo field
 constexpr int64_t kPackedImageBudget = 224 * 1024;   // one 1024-thread CTA per SM
 struct PackedPlan {
   int64_t n = 0;              // entries
@@ -160,7 +161,7 @@ struct PackedPlan {
   std::vector<uint8_t> image;   // smem image: u16 residuals | u32 directory
 };
 // EOS_ERR_UNSUPPORTED when no sh <= 16 gives an image within `budget` and bins of
-// <= 255 entries (eos_search_create_levels then uses 8-ary levels under AUTO).
+// <= 63 entries (eos_search_create_levels then uses 8-ary levels under AUTO).
 eos_status plan_packed(const double* X, int64_t n, PackedPlan* out,
                        int64_t budget = kPackedImageBudget);
 void fill_info(const PackedPlan& p, eos_table_info_t* info);

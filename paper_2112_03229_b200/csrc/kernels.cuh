@@ -434,7 +434,7 @@ struct TieredLookup {
 // eos_internal.h PackedPlan): ONE L2 sector per lookup.  Per target:
 //   sample (smem): u = max(key, hb) - hb, bin b = min(u >> sh, bmax), rk = the
 //     low sh bits of u (0xFFFF past the last bin); lifting counts the bin's
-//     residuals < rk, equal residuals settled from X[15 j] (global);
+//     residuals <= rk, a run equal to rk settled from X[15 j] (global);
 //     j = max(#{T1 <= y} - 1, 0)
 //   node j (one 32-B sector, ld.global.nc, L1 no-allocate): B | s, r_1..r_14;
 //     ry = min((max(key, B) - B) >> s, 0x77FF); the residuals are sorted, so
@@ -465,18 +465,21 @@ template <int S, int MODE>
 struct PackedLookup {
   static constexpr bool kBatchTail = false;
   const uint16_t* __restrict__ sR;  // sample residuals (smem)
-  const uint32_t* __restrict__ sD;  // directory lo | occ << 24 (smem)
+  const uint32_t* __restrict__ sD;  // directory, one u32 per bin pair (smem)
   AxisParams a;                     // n = n1; hb, bmax of the sample hash; x0, xlast of X
   uint32_t sh;
   const double* __restrict__ X;       // the table (global)
   const uint32_t* __restrict__ nodes;  // 8 words per node (global, 32-B aligned)
 
-  // Sample lookups of N targets, step-major (the N lifting chains interleave);
-  // equal residuals are settled after all chains, in a branch taken rarely.
+  // Sample lookups of N targets, step-major (the N lifting chains interleave).
+  // Lifting counts the residuals <= rk and keeps the last one it accepted, which
+  // is the bin's entry c - 1: equal to rk only when a run of equal residuals
+  // may hold entries > y.  That run is settled after all chains, from its end,
+  // in a branch taken rarely (no extra shared load on the common path).
   template <int N>
   __device__ __forceinline__ void sample(const double (&y)[N], const uint32_t (&ky)[N],
                                          int32_t (&j)[N]) const {
-    uint32_t rk[N];
+    uint32_t rk[N], last[N];
     int32_t lo[N], occ[N], c[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -485,10 +488,13 @@ struct PackedLookup {
       const uint32_t q = u >> sh;
       const uint32_t b = min(q, a.bmax);
       rk[i] = q > a.bmax ? 0xFFFFu : (u & ((1u << sh) - 1u));
-      const uint32_t d = sD[b];
-      lo[i] = (int32_t)(d & 0xFFFFFFu);
-      occ[i] = (int32_t)(d >> 24);
+      // one u32 entry per bin pair: lo(pair) | occ(even bin) << 20 | occ(odd bin) << 26
+      const uint32_t d = sD[b >> 1];
+      const uint32_t o0 = (d >> 20) & 63u;
+      lo[i] = (int32_t)((d & 0xFFFFFu) + ((b & 1u) ? o0 : 0u));
+      occ[i] = (int32_t)((b & 1u) ? (d >> 26) : o0);
       c[i] = 0;
+      last[i] = 0xFFFFFFFFu;
       EOS_DCHECK(lo[i] + occ[i] <= a.n && occ[i] < (1 << S));
     }
 #pragma unroll
@@ -496,22 +502,21 @@ struct PackedLookup {
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         const int32_t t = c[i] + s;
-        if (t <= occ[i] && sR[lo[i] + t - 1] < rk[i]) c[i] = t;
+        const uint32_t v = t <= occ[i] ? (uint32_t)sR[lo[i] + t - 1] : 0xFFFFFFFFu;
+        if (v <= rk[i]) {
+          c[i] = t;
+          last[i] = v;
+        }
       }
     }
-    bool tie[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) tie[i] = c[i] < occ[i] && sR[lo[i] + c[i]] == rk[i];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      if (tie[i]) {
-        // equal residuals (a prefix of the rest of the bin): the exact values
-        for (int32_t st = 1 << (31 - __clz(occ[i] - c[i])); st > 0; st >>= 1) {
-          const int32_t t = c[i] + st;
-          if (t <= occ[i] && sR[lo[i] + t - 1] == rk[i] &&
-              __ldg(X + 15 * (int64_t)(lo[i] + t - 1)) <= y[i])
-            c[i] = t;
-        }
+      if (last[i] == rk[i]) {
+        // entries lo .. lo + c - 1 are <= rk and the run of residuals == rk ends
+        // at c - 1; its entries > y (fp64) form the run's tail
+        while (c[i] > 0 && sR[lo[i] + c[i] - 1] == rk[i] &&
+               !(__ldg(X + 15 * (int64_t)(lo[i] + c[i] - 1)) <= y[i]))
+          --c[i];
       }
       j[i] = max(lo[i] + c[i] - 1, 0);
     }
@@ -1036,7 +1041,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
   pdl_enter();
   const AxisParams a = args.ax;
   EOS_DCHECK(args.levels == 1 && args.sh >= 1 && args.sh <= 16 &&
-             a.d_off + 4 * ((int64_t)a.bmax + 1) <= 16 * (int64_t)args.image_16 &&
+             a.d_off + 4 * (((int64_t)a.bmax + 2) / 2) <= 16 * (int64_t)args.image_16 &&
              2 * (int64_t)a.n <= a.d_off && 15 * ((int64_t)a.n - 1) < args.lv_top_len);
   PackedLookup<S, MODE> lk;
   lk.sR = reinterpret_cast<const uint16_t*>(reinterpret_cast<const char*>(smem) + a.x_off);

@@ -125,16 +125,14 @@ const void* packed_fn(int steps) {
     case 3: return (const void*)dv::search1d_packed_kernel<3, MODE, CNT, SH>;
     case 4: return (const void*)dv::search1d_packed_kernel<4, MODE, CNT, SH>;
     case 5: return (const void*)dv::search1d_packed_kernel<5, MODE, CNT, SH>;
-    case 6: return (const void*)dv::search1d_packed_kernel<6, MODE, CNT, SH>;
-    case 7: return (const void*)dv::search1d_packed_kernel<7, MODE, CNT, SH>;
-    default: return (const void*)dv::search1d_packed_kernel<8, MODE, CNT, SH>;
+    default: return (const void*)dv::search1d_packed_kernel<6, MODE, CNT, SH>;
   }
 }
 template <class SH, bool CNT>
 const void* packed_fn_mode(int mode, int steps) {
   return mode == 0 ? packed_fn<0, SH, CNT>(steps) : packed_fn<1, SH, CNT>(steps);
 }
-static_assert(eos::kPackedMaxSteps == 8, "packed_fn covers S = 1..8");
+static_assert(eos::kPackedMaxSteps == 6, "packed_fn covers S = 1..6");
 
 // Small launches of tiered tables: 512 x 1 tiles (a quarter of the default
 // 1024 x 2), used like the single-level small shapes when the default tiles

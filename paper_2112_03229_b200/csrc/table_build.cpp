@@ -527,7 +527,7 @@ eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t bu
   for (int sh = 16; sh >= 1; --sh) {
     const uint32_t hb = lowk & ~((1u << sh) - 1u);
     const int64_t bins = (int64_t)((top > hb ? top - hb : 0) >> sh) + 1;
-    if (rbytes + pad16(4 * bins) > budget) break;  // more bins at smaller sh
+    if (rbytes + pad16(4 * ((bins + 1) / 2)) > budget) break;  // more bins at smaller sh
     cnt.assign((size_t)bins, 0);
     int max_occ = 0;
     for (int64_t j = 0; j < n1; ++j) {
@@ -549,7 +549,7 @@ eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t bu
   const int sh = p.sh;
   const uint32_t mask = (1u << sh) - 1u;
   try {
-    p.image.assign((size_t)(rbytes + pad16(4 * (int64_t)p.bins)), 0);
+    p.image.assign((size_t)(rbytes + pad16(4 * (((int64_t)p.bins + 1) / 2))), 0);
     p.nodes.assign((size_t)(8 * n1), 0);
   } catch (...) {
     return EOS_ERR_NOMEM;
@@ -568,9 +568,10 @@ eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t bu
     if (occ[b] == 0) lo[b] = next;
     else next = lo[b];
   }
-  for (int64_t b = 0; b < p.bins; ++b) {
-    const uint32_t d = lo[b] | (occ[b] << 24);
-    memcpy(p.image.data() + rbytes + 4 * b, &d, 4);
+  for (int64_t g = 0; 2 * g < p.bins; ++g) {  // bin pairs
+    const uint32_t o1 = 2 * g + 1 < p.bins ? occ[2 * g + 1] : 0;
+    const uint32_t d = lo[2 * g] | (occ[2 * g] << 20) | (o1 << 26);
+    memcpy(p.image.data() + rbytes + 4 * g, &d, 4);
   }
   // nodes
   for (int64_t j = 0; j < n1; ++j) {
@@ -608,6 +609,7 @@ TablePlan packed_top(const PackedPlan& p) {
   t.fast_steps = p.steps;
   t.x_bytes = pad16(2 * p.n1);
   t.image_bytes = (int64_t)p.image.size();
+  t.dir16 = true;  // 2 B per bin (one u32 per bin pair)
   return t;
 }
 

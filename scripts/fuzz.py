@@ -7,7 +7,7 @@ fixed wall-clock budget.
 1-D: table sizes 1 .. 300000 of several shapes (tables up to 4096 entries also through the
 zero-setup eos_search_direct) (log-uniform, exact powers of two, duplicate
 runs, mixed signs with +-0, zero heads with subnormals, dense keys), every plan kind
-(automatic, exponent k, log |H|, forced tiered depth D), targets drawn around the entries
+(automatic, exponent k, log |H|, forced tiered depth D, packed nodes), targets drawn around the entries
 (+-1 ulp, midpoints) plus log-uniform, out-of-range and special values.  Indices must be
 bit-exact.  2-D: random grids (logspace with jitter / random axes, mode 0 and 1, shared or
 device memory, linear or log-log, with derivatives); brackets bit-exact, P within 1e-12.
@@ -64,7 +64,7 @@ def targets_for(rng, X, m):
 def fuzz_1d(rng, dev, stats):
     X, kind = rand_table(rng)
     n = X.size
-    plan = rng.integers(0, 4)
+    plan = rng.integers(0, 5)
     kw = {}
     if plan == 1:
         kw["k"] = int(rng.integers(0, 12))
@@ -72,6 +72,8 @@ def fuzz_1d(rng, dev, stats):
         kw["log_bins"] = int(np.exp(rng.uniform(0, np.log(40000))))
     elif plan == 3:
         kw["levels"] = int(rng.integers(1, 6))
+    elif plan == 4:
+        kw["levels"] = eos.EOS_LEVELS_PACKED
     try:
         t = eos.Table(X, **kw)
     except eos.EosError as e:
@@ -93,6 +95,7 @@ def fuzz_1d(rng, dev, stats):
     stats["lookups"] += Y.size
     stats["max_n"] = max(stats["max_n"], n)
     stats["tiered"] += int(t.info.levels > 0)
+    stats["packed"] += int(t.info.node_width == 15)
     if bad.size:
         stats["mismatches"].append({"n": n, "kind": kind, "plan": kw, "levels": t.info.levels,
                                     "first": [float(Y[bad[0]]), int(got[bad[0]]), int(ref[bad[0]])]})
@@ -159,7 +162,7 @@ def main():
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(a.seed)
-    stats = {"tables": 0, "lookups": 0, "tiered": 0, "direct_tables": 0, "max_n": 0, "rejected_plans": 0,
+    stats = {"tables": 0, "lookups": 0, "tiered": 0, "packed": 0, "direct_tables": 0, "max_n": 0, "rejected_plans": 0,
              "grids": 0, "pairs": 0, "mismatches": []}
     t_end = time.time() + 60 * a.minutes
     it = 0

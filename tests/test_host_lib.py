@@ -341,9 +341,9 @@ def _keys_mode0(v):
 def test_packed_plan_fields_and_sample_hash(n):
     """eos_plan_table_levels(EOS_LEVELS_PACKED) (eos_internal.h PackedPlan): n1 =
     ceil(n/15) nodes of 32 B after the 32-B padded fp64 table; the sample table
-    X[::15] as u16 residuals plus u32 directory entries within 224 KB; the bins are the
-    key's bits above sh = 20 - k (hb aligned), recounted here, and S is the fewest
-    lifting steps over every residual width that fits."""
+    X[::15] as u16 residuals plus one u32 directory entry per bin pair within 224 KB; the
+    bins are the key's bits above sh = 20 - k (hb aligned), recounted here, and S is the
+    fewest lifting steps over every residual width that fits (bins of <= 63 entries)."""
     rng = np.random.default_rng(n)
     X = np.sort(10.0 ** rng.uniform(-6, 10, n))
     info = eos.plan_table_levels(X, levels=eos.EOS_LEVELS_PACKED)
@@ -352,9 +352,9 @@ def test_packed_plan_fields_and_sample_hash(n):
     assert (info.levels, info.node_width, info.top_n, info.n) == (1, 15, n1, n)
     assert info.level_bytes == (8 * n + 31) // 32 * 32 + 32 * n1
     assert info.hash_kind == eos.EOS_HASH_EXPONENT and 4 <= info.k <= 19
-    assert info.dir_entry_bytes == 4
+    assert info.dir_entry_bytes == 2
     budget = 224 * 1024
-    assert info.image_bytes == pad16(2 * n1) + pad16(4 * info.bins) <= budget
+    assert info.image_bytes == pad16(2 * n1) + pad16(4 * ((info.bins + 1) // 2)) <= budget
 
     K = _keys_mode0(X[::15])
 
@@ -366,10 +366,10 @@ def test_packed_plan_fields_and_sample_hash(n):
     sh = 20 - info.k
     hb, bins, mo = plan(sh)
     assert (info.base, info.bins, info.max_occ) == (hb, bins, mo)
-    assert info.steps == int(np.ceil(np.log2(mo + 1))) <= 8
+    assert info.steps == int(np.ceil(np.log2(mo + 1))) <= 6
     for other in range(1, 17):
         _, b2, m2 = plan(other)
-        if pad16(2 * n1) + pad16(4 * b2) <= budget and m2 <= 255:
+        if pad16(2 * n1) + pad16(4 * ((b2 + 1) // 2)) <= budget and m2 <= 63:
             assert int(np.ceil(np.log2(m2 + 1))) >= info.steps, other
 
 
