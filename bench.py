@@ -380,6 +380,12 @@ def run_ours(a, d: Dist):
             "peak_gsectors_s": round(gl["sectors_per_s"] / 1e9, 2),
             "frac": round(ach / gl["sectors_per_s"], 4), "peak_source": "measured",
             "probe": gl}
+        if obj.info.node_width == 15:
+            # one sector per lookup: the same mix (stream + one gather per unit) as a
+            # trivial kernel is the kernel's own ceiling, measured on the same buffers
+            sg = measure.stream_gather_ceiling(Y, out, max(int(gathered), 1 << 20))
+            res["roofline"]["l2"]["stream_gather_ceiling"] = sg
+            res["roofline"]["l2"]["frac_vs_stream_gather"] = round(count / (kern_ms * 1e-3) / sg["units_per_s"], 4)
     if counters is not None:
         res["validation"] = {"counters_u64": counters}
     if d.world == 1 and d.rank == 0 and not a.no_cpu:

@@ -340,7 +340,7 @@ def workload(name: str, count: int | None = None) -> Workload:
     if name == "big":
         X = table_big(6)
         return Workload(name, count or (1 << 27), X, loguniform_over(X, 6),
-                        note="n=2^20 table (tiered: smem sample + L2-resident 4-ary levels), "
+                        note="n=2^20 table (beyond shared memory: smem sample table + L2-resident packed nodes), "
                              "2^27 log-uniform targets")
     raise KeyError(name)
 

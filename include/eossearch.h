@@ -192,7 +192,8 @@ EOS_API eos_status eos_search_create_hash(const double* table_host, int64_t n, i
  *     t = 1..14 (<= 0x7BFF: positive normal fp16 patterns; 0x7C00 past n); the
  *     sample table T1[j] = X[15j], j < n1 = ceil(n/15), is held in shared
  *     memory as the low sh <= 16 bits of its keys, binned by the key's upper
- *     bits (the exponent hash with k = 20 - sh), with 32-bit directory entries.
+ *     bits (the exponent hash with k = 20 - sh), with one 32-bit directory
+ *     entry per pair of bins (the pair's first index, both occupancies).
  *     A lookup reads one node from L2; equal residuals are settled from the
  *     fp64 table in device memory (8n + 32 n1 bytes in all).  Fits while the
  *     sample table and its directory take <= 224 KB (n up to ~1.5e6 for

@@ -9,6 +9,9 @@ stream they are launched on.
   stream_ceiling_2d(...)     best GB/s of the 2-D mix (16 B in, 16 B out per pair)
   l2_gather_ceiling(bytes)   random 32-B sector gathers from an L2-resident
                              buffer with the tiered kernel's load instruction
+  stream_gather_ceiling(Y, out, bytes)
+                             the packed-table mix: the 1-D stream plus one
+                             random 32-B sector gather per unit (same buffers)
 """
 from __future__ import annotations
 
@@ -46,8 +49,10 @@ def lib():
         L.probe_fill.argtypes = [_P, _U64, _P]
         L.probe_gather.argtypes = [_P, _U64, _I, _I, _P, _P]
         L.probe_gather_line.argtypes = [_P, _U64, _I, _I, _P, _P]
+        L.probe_stream_gather.argtypes = [_P, _P, _I64, _P, _U64, _I, _P]
         for f in (L.probe_stream, L.probe_stream2d, L.probe_fill, L.probe_gather, L.probe_gather_line,
-                  L.probe_stream_variants, L.probe_sms):
+                  L.probe_stream_variants, L.probe_sms, L.probe_stream_gather,
+                  L.probe_stream_gather_variants):
             f.restype = _I
         _lib = L
     return _lib
@@ -154,3 +159,30 @@ def l2_line_gather_ceiling(buffer_bytes: int, rounds: int = 64, reps: int = 5) -
     best = max(res, key=res.get)
     return {"lines_per_s": res[best], "chains": best, "buffer_bytes": 128 * lines,
             "all_glines_per_s": {str(k): round(v / 1e9, 2) for k, v in res.items()}}
+
+
+def stream_gather_ceiling(Y, out, buffer_bytes: int, reps: int = 5) -> dict:
+    """Best-of-shapes units/s of the packed-table same mix over the bench's own buffers:
+    read fp64 Y, gather one random 32-B sector per unit from an L2-resident buffer of
+    `buffer_bytes` (rounded down to a power of two of sectors), write int32 out."""
+    import torch
+    L = lib()
+    sectors = 1
+    while 2 * sectors * 32 <= buffer_bytes:
+        sectors *= 2
+    buf = torch.empty(8 * sectors, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream()
+    _check(L.probe_fill(buf.data_ptr(), 8 * sectors, st.cuda_stream), "probe_fill")
+    n = Y.numel() - (Y.numel() & 1)
+    res = {}
+    for v in range(L.probe_stream_gather_variants()):
+        ms = _time(lambda: _check(L.probe_stream_gather(Y.data_ptr(), out.data_ptr(), n, buf.data_ptr(),
+                                                        sectors, v, st.cuda_stream),
+                                  "probe_stream_gather"), reps, st)
+        res[v] = n / (ms * 1e-3)
+    best = max(res, key=res.get)
+    return {"units_per_s": res[best], "variant": best, "buffer_bytes": 32 * sectors,
+            "all_gunits_per_s": {str(k): round(v / 1e9, 2) for k, v in res.items()},
+            "what": "read fp64 + one random 32-B sector gather (ld.global.nc.L1::no_allocate.v8.u32, "
+                    "L2-resident buffer) + write int32 per unit, trivial kernel, best of "
+                    f"{len(res)} launch shapes, {reps} launches each, same buffers as the bench"}

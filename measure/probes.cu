@@ -12,6 +12,8 @@
 //                  with the tiered kernel's load (ld.global.nc.L1::no_allocate
 //                  .v8.u32, one sector per lane): the on-chip ceiling of the
 //                  tiered-table level walk.
+//  probe_stream_gather : the packed-table mix: the 1-D stream plus one random
+//                  32-B sector gather per unit from an L2-resident buffer.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -405,6 +407,42 @@ __global__ void __launch_bounds__(1024, 1) k_gather_line(const uint32_t* __restr
   if (acc == 0x12345678u) sink[0] = acc;
 }
 
+// The packed-table memory mix with no search: per unit, read an
+// fp64 target (stream), gather ONE random 32-B sector of an L2-resident node
+// buffer at an index hashed from the target's bits, write an int32 that
+// depends on both.  One CTA per tile of T threads x U double2: the same-mix
+// ceiling of a one-sector-per-lookup kernel.
+template <int T, int U>
+__global__ void __launch_bounds__(T) k_stream_gather(const double2* __restrict__ y,
+                                                     int2* __restrict__ out, int64_t pairs,
+                                                     const uint32_t* __restrict__ buf,
+                                                     uint64_t mask) {
+  const int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x;
+  double2 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = base + (int64_t)u * T;
+    v[u] = i < pairs ? ldcs2(y + i) : make_double2(0.0, 0.0);
+  }
+  uint32_t k[2 * U][8];
+#pragma unroll
+  for (int u = 0; u < 2 * U; ++u) {
+    const double x = (u & 1) ? v[u >> 1].y : v[u >> 1].x;
+    const uint64_t s = smix((uint64_t)__double_as_longlong(x)) & mask;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(k[u][0]), "=r"(k[u][1]), "=r"(k[u][2]), "=r"(k[u][3]), "=r"(k[u][4]),
+                   "=r"(k[u][5]), "=r"(k[u][6]), "=r"(k[u][7])
+                 : "l"(buf + 8 * s));
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = base + (int64_t)u * T;
+    const int2 r = make_int2(fold(v[u].x) ^ (int32_t)(k[2 * u][0] ^ k[2 * u][7]),
+                             fold(v[u].y) ^ (int32_t)(k[2 * u + 1][0] ^ k[2 * u + 1][7]));
+    if (i < pairs) __stcs(out + i, r);
+  }
+}
+
 __global__ void k_fill(uint32_t* buf, uint64_t words) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride)
@@ -538,6 +576,30 @@ int probe_gather_line(const uint32_t* buf, uint64_t lines, int chains, int round
     case 2: k_gather_line<2><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
     case 4: k_gather_line<4><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
     default: k_gather_line<8><<<g, 1024, 0, st>>>(buf, mask, rounds, sink); break;
+  }
+  return (int)cudaGetLastError();
+}
+
+// Number of stream+gather shapes (variant 0 .. probe_stream_gather_variants()-1).
+int probe_stream_gather_variants(void) { return 4; }
+
+// One launch of the packed-table same mix over n targets (n even, aligned):
+// read y, gather one 32-B sector of buf[0 .. 8*sectors) per target (sectors a
+// power of two), write out.
+int probe_stream_gather(const double* y, int32_t* out, int64_t n, const uint32_t* buf,
+                        uint64_t sectors, int variant, void* stream) {
+  if (sectors == 0 || (sectors & (sectors - 1))) return (int)cudaErrorInvalidValue;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t pairs = n / 2;
+  const double2* y2 = reinterpret_cast<const double2*>(y);
+  int2* o2 = reinterpret_cast<int2*>(out);
+  const uint64_t mask = sectors - 1;
+  switch (variant) {
+    case 0: k_stream_gather<256, 2><<<(unsigned)((pairs + 511) / 512), 256, 0, st>>>(y2, o2, pairs, buf, mask); break;
+    case 1: k_stream_gather<256, 4><<<(unsigned)((pairs + 1023) / 1024), 256, 0, st>>>(y2, o2, pairs, buf, mask); break;
+    case 2: k_stream_gather<512, 2><<<(unsigned)((pairs + 1023) / 1024), 512, 0, st>>>(y2, o2, pairs, buf, mask); break;
+    case 3: k_stream_gather<1024, 2><<<(unsigned)((pairs + 2047) / 2048), 1024, 0, st>>>(y2, o2, pairs, buf, mask); break;
+    default: return (int)cudaErrorInvalidValue;
   }
   return (int)cudaGetLastError();
 }

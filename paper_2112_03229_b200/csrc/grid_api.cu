@@ -42,7 +42,7 @@ struct eos_grid2d_s {
   int32_t flags = 0;
   int32_t rr_off = 0, rt_off = 0;
   int rep = 0;  // 2: bank-pinned cell records in the image (REP kernels), 0: plain axes
-  bool narrow = false;  // log-log: every cell ratio X[j+1]/X[j] <= 1.5 (kernels.cuh log1p_cell)
+  int narrow = 0;  // log-log: 2 if every cell ratio X[j+1]/X[j] <= 1.25, 1 if <= 1.5 (kernels.cuh log1p_cell)
   int32_t rep_shift = 0;       // REP 2: log2 of the record copies
   int64_t rep_bytes_axis = 0;  // image bytes per axis entry of the REP layout
   bool gg = false;          // grid in device memory (GG kernels)
@@ -139,7 +139,7 @@ eos_status launch_interp(eos_grid2d g, const double* rho, const double* T, int64
   a.rt_off = g->rt_off;
   a.gq = reinterpret_cast<const double2*>(g->grid_dev);
   a.rep_shift = g->rep_shift;
-  a.narrow = g->narrow ? 1 : 0;
+  a.narrow = g->narrow;
   a.r = g->ar;
   a.t = g->at;
   a.rho = rho;
@@ -235,7 +235,12 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   // less the kernel's static smem).  EOS_GRID_EXACT: plain axes (REP 0), whose
   // weights divide exactly as the formula does.
   {
-    const int want = (flags & EOS_GRID_EXACT) ? 0 : 2;
+    // Log-log records need 1/X[c] on the device from the reciprocal estimate (its ftz
+    // form): every axis value and its reciprocal must be normal doubles, else REP 0.
+    bool rcp_ok = true;
+    for (const std::vector<double>* ax : {&g->pr.X, &g->pt.X})
+      rcp_ok = rcp_ok && ax->front() >= 0x1p-1020 && ax->back() <= 0x1p1020;
+    const int want = ((flags & EOS_GRID_EXACT) || (loglog && !rcp_ok)) ? 0 : 2;
     // (log-log grids: records of the log axes.)  8 copies are conflict-free
     // (128 B per axis entry); take as many as fit, down to 1 (then the
     // records still save the divides)
@@ -258,7 +263,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     // REP 2: spend the rest of the shared memory (at most 64 KB) on sparser
     // axis directories (split by axis length), so the second record read is rare
     const int64_t spare = std::min<int64_t>(cap - g->image_bytes - 512, 64 * 1024);
-    if (g->rep == 2 && !loglog && spare > 1024) {
+    if (g->rep == 2 && spare > 1024) {
       const int64_t avail = r_bytes + t_bytes + spare;
       const int64_t br = avail * n_rho / (n_rho + n_T), bt = avail - br;
       eos::TablePlan pr, pt;
@@ -288,11 +293,11 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
     const int64_t n = (int64_t)X.size();
     for (int64_t q = 0; q < n; ++q) {
       // Rec[C q + c] = (X[q], 1/(X[q+1] - X[q])), or for log-log grids
-      // (1/X[q], 1/ln(X[q+1]/X[q])) with ln(X[q+1]/X[q]) = log1p((X[q+1] - X[q])/X[q])
+      // (X[q], 1/ln(X[q+1]/X[q])) with ln(X[q+1]/X[q]) = log1p((X[q+1] - X[q])/X[q])
       // (R24); C = 2^rep_shift copies; the last record's width is unused
       const bool last = q + 1 >= n;
       const double rec[2] = {
-          loglog ? 1.0 / X[q] : X[q],
+          X[q],
           last ? 0.0 : (loglog ? 1.0 / log1p((X[q + 1] - X[q]) / X[q]) : 1.0 / (X[q + 1] - X[q]))};
       const int C = 1 << g->rep_shift;
       for (int c = 0; c < C; ++c) memcpy(img.data() + off + 16 * (C * q + c), rec, 16);
@@ -310,11 +315,15 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
       memcpy(img.data() + g->g_off + 8 * q, &v, 8);
     }
   }
-  if (loglog) {  // the short log1p series of the weights needs every cell ratio <= 1.5
-    bool nw = true;
+  if (loglog) {  // the short log1p series of the weights: every cell ratio <= 1.5 (12
+                 // terms) or <= 1.25 (8 terms), kernels.cuh log1p_cell
+    bool n15 = true, n125 = true;
     for (const std::vector<double>* ax : {&g->pr.X, &g->pt.X})
-      for (size_t q = 0; q + 1 < ax->size(); ++q) nw = nw && (*ax)[q + 1] <= 1.5 * (*ax)[q];
-    g->narrow = nw;
+      for (size_t q = 0; q + 1 < ax->size(); ++q) {
+        n15 = n15 && (*ax)[q + 1] <= 1.5 * (*ax)[q];
+        n125 = n125 && (*ax)[q + 1] <= 1.25 * (*ax)[q];
+      }
+    g->narrow = n125 ? 2 : (n15 ? 1 : 0);
   }
   g->ar = axis_params(g->pr, 0);
   g->at = axis_params(g->pt, (int32_t)r_bytes);

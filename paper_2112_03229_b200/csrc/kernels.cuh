@@ -1229,7 +1229,7 @@ struct Interp2DArgs {
   int32_t rt_off;   // the same for the T axis
   int32_t rep_shift;  // REP 2: log2 of the record copies per axis entry (3: 8 copies, the
                       //   conflict-free layout; fewer when smem is short: 2-way .. 8-way)
-  int32_t narrow;     // LOGLOG: 1 if every cell of both axes has X[j+1]/X[j] <= 1.5
+  int32_t narrow;     // LOGLOG: 2 if every cell of both axes has X[j+1]/X[j] <= 1.25, else 1 if <= 1.5, else 0
   int32_t pad3_;
   const double2* gq;  // GG / small kernels: the grid in device memory (ln G for LOGLOG) as
                       //   cell quads gq[2 (i (nT-1) + j)] = (G[i][j], G[i][j+1]),
@@ -1249,40 +1249,75 @@ struct Interp2DArgs {
   int64_t count;
 };
 
-// log1p(d) for the log-log weight of a cell with X[c+1]/X[c] <= 1.5 (grids whose
-// cells all are, Interp2DArgs::narrow): inside the cell d = (x - X[c])/X[c] is in
-// [0, 0.5], and log1p(d) = 2 atanh(u), u = d/(2+d) in [0, 0.2], is the odd series
-// 2u (1 + u^2/3 + ... + u^22/23): 12 terms reach 2^-53 (u^2 <= 0.04): a reciprocal
-// estimate, 15 FMAs and no branch, against the general log1p's called routine.  Outside the cell only the
-// clamped weight matters: d < 0 gives a negative value, d > 0.5 a value above
-// ln 1.5 >= the cell width (the partial sums grow with u), so both clamp as the
-// exact log1p would; d = +inf is held at 1e300 (weight 1), d < -1 (x < 0) and NaN
-// give NaN as log1p does, d = -1 (x = 0) a negative value (weight 0, as -inf).
-__device__ __forceinline__ double log1p_cell(double d) {
-  const double dd = d > 1e300 ? 1e300 : d;  // (NaN passes through)
-  // u = dd / (2 + dd) by the hardware reciprocal estimate and two Newton steps (the
-  // correctly rounded divide is a called routine with slow paths): within ~2 ulp
-  const double a = __dadd_rn(2.0, dd);
-  double rc;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(a));
-  rc = __fma_rn(rc, __fma_rn(-a, rc, 1.0), rc);
-  rc = __fma_rn(rc, __fma_rn(-a, rc, 1.0), rc);
-  const double u = __dmul_rn(dd, rc);
+// 1/x for a normal x whose reciprocal is normal: the hardware estimate (ftz) and two
+// Newton steps, within an ulp of the correctly rounded 1/x.
+__device__ __forceinline__ double rcp_newton(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = __fma_rn(r, __fma_rn(-x, r, 1.0), r);
+  return __fma_rn(r, __fma_rn(-x, r, 1.0), r);
+}
+
+// ln(x / X) for the log-log weight of a cell [X, X r] with r <= 1.5 (grids whose
+// cells all are, Interp2DArgs::narrow), X normal in [2^-1020, 2^1020]: the same real
+// number as log1p((x - X)/X) (R24), as 2 atanh(u) with u = (x - X)/(x + X) -- inside
+// the cell x - X is exact (Sterbenz) and u in [0, (r-1)/(r+1)] <= 0.2 -- by the odd
+// series 2u (1 + u^2/3 + ... + u^(2K-2)/(2K-1)): K = 12 terms reach 2^-53 for u^2 <=
+// 0.04 (r = 1.5), K = 8 for u^2 <= 1/81 (r = 1.25, narrow == 2; the first omitted term
+// is <= 3.2e-17 relative).  One reciprocal estimate, K + 4 FMAs, no branch (the
+// general log1p is a called routine).  The coefficients 2/(2i+1) live in the
+// constant bank (as immediates each costs two uniform moves per call).  Outside the
+// cell only the clamped weight matters: x < X gives a negative value, x above the
+// cell a value above its log width (the partial sums grow with u), so both clamp as
+// the exact logarithm would; x = +inf is held at 2^1021 (> every axis value: weight
+// 1), x = +-0 gives u = -1, a negative value (weight 0, as ln 0 = -inf), x < 0 and
+// NaN give NaN as log1p does.
+__constant__ double kAtanhCoef[12] = {2.0,        2.0 / 3.0,  2.0 / 5.0,  2.0 / 7.0,
+                                      2.0 / 9.0,  2.0 / 11.0, 2.0 / 13.0, 2.0 / 15.0,
+                                      2.0 / 17.0, 2.0 / 19.0, 2.0 / 21.0, 2.0 / 23.0};
+template <int K>
+__device__ __forceinline__ double ln_ratio_cell(double x, double X) {
+  static_assert(K >= 2 && K <= 12, "series length");
+  const double xc = x > 0x1p1021 ? 0x1p1021 : x;  // (NaN passes through)
+  const double u = __dmul_rn(__dsub_rn(xc, X), rcp_newton(__dadd_rn(xc, X)));
   const double u2 = __dmul_rn(u, u);
-  double p = 2.0 / 23.0;
-  p = __fma_rn(p, u2, 2.0 / 21.0);
-  p = __fma_rn(p, u2, 2.0 / 19.0);
-  p = __fma_rn(p, u2, 2.0 / 17.0);
-  p = __fma_rn(p, u2, 2.0 / 15.0);
-  p = __fma_rn(p, u2, 2.0 / 13.0);
-  p = __fma_rn(p, u2, 2.0 / 11.0);
-  p = __fma_rn(p, u2, 2.0 / 9.0);
-  p = __fma_rn(p, u2, 2.0 / 7.0);
-  p = __fma_rn(p, u2, 2.0 / 5.0);
-  p = __fma_rn(p, u2, 2.0 / 3.0);
-  p = __fma_rn(p, u2, 2.0);
+  double p = kAtanhCoef[K - 1];
+#pragma unroll
+  for (int i = K - 2; i >= 0; --i) p = __fma_rn(p, u2, kAtanhCoef[i]);
   const double r = __dmul_rn(u, p);
-  return d < -1.0 ? __longlong_as_double(0x7FF8000000000000LL) : r;
+  return x < 0.0 ? __longlong_as_double(0x7FF8000000000000LL) : r;
+}
+
+// e^v for the log-log value P = exp(bilinear of ln G) (R24): n = rint(v / ln 2) by
+// the 1.5 2^52 rounding constant, r = v - n ln 2 by two FMAs (ln 2 and its tail),
+// |r| <= ln(2)/2, e^r by its Taylor polynomial of degree 13 (the first omitted term
+// is < 5e-18 relative), scaled by 2^n in the exponent field.  Within ~2 ulp.
+// |v| >= 708 (where 2^n could leave the normal range), inf and NaN take CUDA's exp.
+__constant__ double kExpCoef[14] = {
+    1.0,
+    1.0,
+    1.0 / 2.0,
+    1.0 / 6.0,
+    1.0 / 24.0,
+    1.0 / 120.0,
+    1.0 / 720.0,
+    1.0 / 5040.0,
+    1.0 / 40320.0,
+    1.0 / 362880.0,
+    1.0 / 3628800.0,
+    1.0 / 39916800.0,
+    1.0 / 479001600.0,
+    1.0 / 6227020800.0};
+__device__ __forceinline__ double exp_cell(double v) {
+  if (!(fabs(v) < 708.0)) return exp(v);
+  const double kd = __fma_rn(v, 0x1.71547652b82fep+0, 0x1.8p+52);  // v log2(e) + 1.5 2^52
+  const double n = __dsub_rn(kd, 0x1.8p+52);
+  double r = __fma_rn(-n, 0x1.62e42fefa39efp-1, v);  // ln 2 rounded ...
+  r = __fma_rn(-n, 0x1.abc9e3b39803fp-56, r);        // ... and its tail
+  double p = kExpCoef[13];
+#pragma unroll
+  for (int i = 12; i >= 0; --i) p = __fma_rn(p, r, kExpCoef[i]);
+  return __hiloint2double(__double2hiint(p) + (__double2loint(kd) << 20), __double2loint(p));
 }
 
 __device__ __forceinline__ double clamp01(double t) {
@@ -1387,24 +1422,28 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
     // log1p((x - X[c]) / X[c]) / log1p((X[c+1] - X[c]) / X[c]) -- the same real
     // numbers, without the cancellation of ln x - ln X[c] (which loses
     // ~|ln x| / (cell width in ln) ulps).  Brackets and X[c] from the plain axes.
-    axis_cell<S>(rho, sR, dR, A.r, i, ci, r0, r1);
-    axis_cell<S>(T, sT, dT, A.t, j, cj, t0, t1);
-    if (REP == 2) {  // records (1/X[j], 1/ln(X[j+1]/X[j])): no divides
+    if (REP == 2) {
+      // bank-pinned records (X[j], 1/ln(X[j+1]/X[j])), read as the linear grids read
+      // theirs (the record is also the probe); no divides on the narrow-cell paths
+      // (axes within [2^-1020, 2^1020], grid_api.cu)
       const int32_t sh = A.rep_shift, c = threadIdx.x & ((1 << sh) - 1);
-      const double2 er = reinterpret_cast<const double2*>(sm + A.rr_off)[(ci << sh) + c];
-      const double2 et = reinterpret_cast<const double2*>(sm + A.rt_off)[(cj << sh) + c];
-      ir = er.y;
-      it = et.y;
-      const double dx = __dmul_rn(__dsub_rn(rho, r0), er.x);
-      const double dy = __dmul_rn(__dsub_rn(T, t0), et.x);
-      if (A.narrow) {  // every cell ratio <= 1.5: the short series (launch-uniform branch)
-        tx = clamp01(__dmul_rn(log1p_cell(dx), ir));
-        ty = clamp01(__dmul_rn(log1p_cell(dy), it));
-      } else {
-        tx = clamp01(__dmul_rn(log1p(dx), ir));
-        ty = clamp01(__dmul_rn(log1p(dy), it));
+      axis_cell_rec<S>(rho, sR, dR, A.r, i, ci, r0, ir,
+                       reinterpret_cast<const double2*>(sm + A.rr_off) + c, sh);
+      axis_cell_rec<S>(T, sT, dT, A.t, j, cj, t0, it,
+                       reinterpret_cast<const double2*>(sm + A.rt_off) + c, sh);
+      if (A.narrow == 2) {  // every cell ratio <= 1.25: 8 terms (launch-uniform branch)
+        tx = clamp01(__dmul_rn(ln_ratio_cell<8>(rho, r0), ir));
+        ty = clamp01(__dmul_rn(ln_ratio_cell<8>(T, t0), it));
+      } else if (A.narrow) {  // every cell ratio <= 1.5: 12 terms
+        tx = clamp01(__dmul_rn(ln_ratio_cell<12>(rho, r0), ir));
+        ty = clamp01(__dmul_rn(ln_ratio_cell<12>(T, t0), it));
+      } else {  // wide cells: log1p((x - X)/X)
+        tx = clamp01(__dmul_rn(log1p(__ddiv_rn(__dsub_rn(rho, r0), r0)), ir));
+        ty = clamp01(__dmul_rn(log1p(__ddiv_rn(__dsub_rn(T, t0), t0)), it));
       }
     } else {
+      axis_cell<S>(rho, sR, dR, A.r, i, ci, r0, r1);
+      axis_cell<S>(T, sT, dT, A.t, j, cj, t0, t1);
       wr = log1p(__ddiv_rn(__dsub_rn(r1, r0), r0));
       wt = log1p(__ddiv_rn(__dsub_rn(t1, t0), t0));
       tx = clamp01(__ddiv_rn(log1p(__ddiv_rn(__dsub_rn(rho, r0), r0)), wr));
@@ -1446,7 +1485,7 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   const double a0 = __dadd_rn(__dmul_rn(uy, g00), __dmul_rn(ty, g01));
   const double a1 = __dadd_rn(__dmul_rn(uy, g10), __dmul_rn(ty, g11));
   const double v = __dadd_rn(__dmul_rn(ux, a0), __dmul_rn(tx, a1));
-  const double p = LOGLOG ? exp(v) : v;
+  const double p = LOGLOG ? exp_cell(v) : v;
   if (DERIV) {
     // Partial derivatives of the interpolant on the cell (R23 / R24); 0
     // outside an axis range (the clamped interpolant is constant there); NaN

@@ -793,14 +793,15 @@ def test_loglog_grid_matches_oracle():
 
 @pytest.mark.parametrize("seed", range(4))
 @pytest.mark.parametrize("global_grid", [False, True])
-@pytest.mark.parametrize("max_ln_width", [1.0, 0.4])
+@pytest.mark.parametrize("max_ln_width", [1.0, 0.4, 0.2])
 def test_loglog_rough_surfaces_narrow_cells(seed, global_grid, max_ln_width):
     """Log-log grids with no smoothness: every ln G node independent over +-10, axes with
     cells from 1e-4 to `max_ln_width` wide in ln (so |ln G| jumps of ~20 across a 1e-4
     cell).  P within 1e-12 relative of the oracle at every point (R24's log1p form keeps
     both sides well-conditioned), brackets exact, derivatives within their condition
-    scale.  max_ln_width 0.4 (every cell ratio <= 1.5) takes the kernel's short log1p
-    series (log1p_cell), 1.0 the general log1p."""
+    scale.  max_ln_width 0.2 (every cell ratio <= e^0.2 < 1.25) takes the kernel's
+    8-term log1p series (log1p_cell<8>), 0.4 (every ratio <= 1.5) the 12-term one, 1.0
+    the general log1p."""
     rng = np.random.default_rng(500 + seed)
     def axis(a, n):
         return np.exp(a + np.cumsum(np.concatenate(
