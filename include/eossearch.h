@@ -101,6 +101,15 @@ typedef struct {
   int32_t fast_steps;
   int32_t rare_steps;
   int32_t ring_stages;
+  /* 2-D grid axes (eos_grid2d_info, ABI >= 5): how the kernels find a cell.
+   * 0: through the directory above; 1: fitted log map -- the cell of x is
+   * floor(a log2(x) + b) or the one below, a and b fitted to the axis at create
+   * and checked at every node against the device's error bound (fp32,
+   * lg2.approx); 2: the same with x in place of log2(x).  Maps are used when
+   * both axes have one and the grid has bank-pinned records (not with
+   * EOS_GRID_EXACT or EOS_GRID_DIRECTORY).  Same results either way.  0 for
+   * 1-D tables. */
+  int32_t cell_map;
 } eos_table_info_t;
 
 /* ---------------------------------------------------------------------------
@@ -315,6 +324,9 @@ EOS_API eos_status eos_grid2d_create(const double* rho_host, int64_t n_rho, cons
                            * the default layout multiplies by a precomputed 1/(X[c+1] - X[c])
                            * (conflict-free bank-pinned cell records, no divides): a few ulp of
                            * t, i.e. |dP| <= ~1e-15 (|G| summed over the cell corners). */
+#define EOS_GRID_DIRECTORY 8 /* flag bit: find the cells through the axis directories even
+                            * where both axes follow a fitted map (eos_table_info_t
+                            * cell_map); same results */
 #define EOS_MAX_GRID_CELLS ((int64_t)1 << 28) /* n_rho n_T (EOS_ERR_SIZE above) */
 EOS_API eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const double* T_host,
                                 int64_t n_T, const double* P_host, int32_t flags, eos_grid2d* out);
@@ -351,7 +363,7 @@ EOS_API eos_status eos_grid2d_destroy(eos_grid2d g);
  * Misc
  * ------------------------------------------------------------------------- */
 EOS_API const char* eos_status_str(eos_status s); /* static string, never NULL */
-EOS_API int32_t eos_abi_version(void);            /* 4 */
+EOS_API int32_t eos_abi_version(void);            /* 5 */
 /* Kernel launches issued by this library since load (all entry points). */
 EOS_API int64_t eos_launch_count(void);
 

@@ -32,7 +32,7 @@ __all__ = [
     "eos_search_direct", "search_direct", "eos_grid2d_create_ex", "EOS_GRID_LINEAR",
     "EOS_GRID_LOGLOG", "EOS_MAX_TABLE_TIERED", "EOS_LEVELS_AUTO", "eos_search_create_levels",
     "eos_plan_table_levels", "plan_table_levels", "EOS_GRID_GLOBAL", "EOS_MAX_GRID_CELLS",
-    "EOS_GRID_EXACT", "ABI_VERSION", "EOS_LEVELS_PACKED",
+    "EOS_GRID_EXACT", "ABI_VERSION", "EOS_LEVELS_PACKED", "EOS_GRID_DIRECTORY",
 ]
 
 EOS_MAX_TABLE = 16384
@@ -42,8 +42,8 @@ EOS_LEVELS_PACKED = -2
 EOS_MAX_K = 19
 EOS_K_AUTO = -1
 EOS_HASH_AUTO, EOS_HASH_EXPONENT, EOS_HASH_LOG = 0, 1, 2
-EOS_GRID_LINEAR, EOS_GRID_LOGLOG, EOS_GRID_GLOBAL, EOS_GRID_EXACT = 0, 1, 2, 4
-ABI_VERSION = 4
+EOS_GRID_LINEAR, EOS_GRID_LOGLOG, EOS_GRID_GLOBAL, EOS_GRID_EXACT, EOS_GRID_DIRECTORY = 0, 1, 2, 4, 8
+ABI_VERSION = 5
 EOS_MAX_GRID_CELLS = 1 << 28
 
 STATUS = {
@@ -79,7 +79,7 @@ class TableInfo(ctypes.Structure):
                 ("levels", ctypes.c_int32), ("node_width", ctypes.c_int32), ("top_n", ctypes.c_int64),
                 ("level_bytes", ctypes.c_int64), ("dir_entry_bytes", ctypes.c_int32),
                 ("fast_steps", ctypes.c_int32), ("rare_steps", ctypes.c_int32),
-                ("ring_stages", ctypes.c_int32)]
+                ("ring_stages", ctypes.c_int32), ("cell_map", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -447,16 +447,18 @@ class Grid2D:
     """EOSPAC-style 2-D table (density x temperature) for eos_interp2d."""
 
     def __init__(self, rho, T, P, loglog: bool = False, global_grid: bool = False,
-                 exact: bool = False):
+                 exact: bool = False, directory: bool = False):
         """loglog=True: interpolate ln P bilinearly in (ln rho, ln T) (EOS_GRID_LOGLOG, R24).
         global_grid=True: keep P in device memory even if it fits in shared memory
         (EOS_GRID_GLOBAL; grids too large for shared memory always are).
-        exact=True: weights with the fp64 divide, in the formula's order (EOS_GRID_EXACT)."""
+        exact=True: weights with the fp64 divide, in the formula's order (EOS_GRID_EXACT).
+        directory=True: cells through the axis directories, not fitted cell maps
+        (EOS_GRID_DIRECTORY; same results)."""
         self.rho, self.T = _f64_host(rho).copy(), _f64_host(T).copy()
         self.P = _f64_host(P).reshape(self.rho.size, self.T.size).copy()
         self.loglog = loglog
         flags = (EOS_GRID_LOGLOG if loglog else EOS_GRID_LINEAR) | (EOS_GRID_GLOBAL if global_grid else 0) \
-            | (EOS_GRID_EXACT if exact else 0)
+            | (EOS_GRID_EXACT if exact else 0) | (EOS_GRID_DIRECTORY if directory else 0)
         self._h = eos_grid2d_create(self.rho, self.T, self.P, flags)
         self.rho_info, self.T_info = eos_grid2d_info(self._h)
 

@@ -3,6 +3,8 @@
 // interpolation launches.  Product path (never includes or links oracle/).
 #include <cuda_runtime.h>
 #include <math.h>
+
+#include <cmath>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -52,6 +54,48 @@ struct eos_grid2d_s {
 
 namespace {
 
+// Fitted cell map of a grid axis (kernels.cuh axis_cell_rec, S = kMapped): the
+// kernel takes p = floor(a w(x) + b) in fp32 (w = log2 x by lg2.approx.ftz.f32, or
+// x), clamped to [0, n-2], and needs p in {c, c+1} for every x in cell c =
+// [X[c], X[c+1]).  The exact map u(x) = a w(x) + b is monotone, so that holds if
+// every node maps inside its own unit, c + E <= u(X[c]) <= c + 1 - E, where E
+// bounds the device's error: the fp32 rounding of x (2^-24 relative: 2^-24/ln 2 of
+// log2 x, or 2^-24 |x|), lg2.approx (2^-22 absolute plus the rounding of its
+// exponent add, 2^-24 |log2 x|) and the fp32 fma (2^-24 |u|), times a, then 4x.
+// b puts the nodes 1e-4 above their unit's floor, so p = c + 1 -- and a second
+// record read -- is rare.  Kind 1 (log) is tried first; none fits: kind 0.
+struct CellMap {
+  int kind = 0;
+  float a = 0.0f, b = 0.0f;
+};
+CellMap fit_cell_map(const std::vector<double>& X) {
+  const int64_t n = (int64_t)X.size();
+  for (int kind = 1; kind <= 2; ++kind) {
+    if (kind == 1 ? !(X[0] >= 1e-30 && X[n - 1] <= 1e30)
+                  : !(std::fabs(X[0]) <= 1e30 && std::fabs(X[n - 1]) <= 1e30))
+      continue;
+    std::vector<double> L((size_t)n);
+    for (int64_t j = 0; j < n; ++j) L[j] = kind == 1 ? std::log2(X[j]) : X[j];
+    const double a = (double)(n - 1) / (L[n - 1] - L[0]);
+    if (!(a > 0.0 && a < 1e30)) continue;
+    const float af = (float)a;
+    const double lmax = std::max(std::fabs(L[0]), std::fabs(L[n - 1]));
+    const double u24 = std::ldexp(1.0, -24);
+    const double ew = kind == 1 ? u24 / M_LN2 + std::ldexp(1.0, -22) + lmax * u24 : lmax * u24;
+    const double E = 4.0 * ((double)af * ew + (double)(n + 1) * u24) + 1e-6;
+    double lo = HUGE_VAL;
+    for (int64_t j = 0; j < n; ++j) lo = std::min(lo, (double)af * L[j] - (double)j);
+    const float bf = (float)(E + 1e-4 - lo);
+    bool ok = std::isfinite(bf);
+    for (int64_t j = 0; j < n && ok; ++j) {
+      const double v = (double)af * L[j] + (double)bf - (double)j;
+      ok = v >= E && v <= 1.0 - E;
+    }
+    if (ok) return {kind, af, bf};
+  }
+  return {};
+}
+
 // Kernel of a grid: S = 1..4 or 0 (runtime), linear or log-log, REP 2 (bank-pinned
 // cell records) or 0 (plain axes: EOS_GRID_EXACT, or when the records do not fit),
 // grid in shared (GG = false) or device memory; with and without derivative outputs.
@@ -68,7 +112,7 @@ InterpKernel interp_fn(bool deriv) {
   if (deriv)
     return {(const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, true, LOGLOG, REP, GG>,
             dv::Shape2DDeriv::kThreads};
-  if constexpr (S == 1 && !(LOGLOG && REP == 0))  // (plain log-log axes: 2 log1p per axis)
+  if constexpr ((S == 1 || S == dv::kMapped) && !(LOGLOG && REP == 0))  // (plain log-log axes: 2 log1p per axis)
     return {(const void*)dv::interp2d_kernel<S, dv::Shape2D, false, LOGLOG, REP, GG>,
             dv::Shape2D::kThreads};
   else
@@ -78,6 +122,9 @@ InterpKernel interp_fn(bool deriv) {
 
 template <bool LOGLOG, int REP, bool GG>
 InterpKernel interp_fn_steps(int steps, bool deriv) {
+  if constexpr (REP == 2) {
+    if (steps == dv::kMapped) return interp_fn<dv::kMapped, LOGLOG, REP, GG>(deriv);
+  }
   if constexpr (GG) {  // device-memory grids: S = 1 or the runtime loop
     return steps == 1 ? interp_fn<1, LOGLOG, REP, GG>(deriv) : interp_fn<0, LOGLOG, REP, GG>(deriv);
   } else {
@@ -110,7 +157,15 @@ InterpKernel pick_interp(int steps, bool loglog, int rep, bool gg, bool deriv) {
 // 32-B quad, so its many CTAs do not each copy the whole grid from L2.
 const void* pick_interp_small(int steps, bool loglog, int rep, bool deriv) {
   using SG = dv::Shape2DSmallGG;
-  if (steps != 1 || rep != 2) return nullptr;
+  if (rep != 2) return nullptr;
+  if (steps == dv::kMapped) {
+    if (deriv)
+      return loglog ? (const void*)dv::interp2d_kernel<dv::kMapped, SG, true, true, 2, true>
+                    : (const void*)dv::interp2d_kernel<dv::kMapped, SG, true, false, 2, true>;
+    return loglog ? (const void*)dv::interp2d_kernel<dv::kMapped, SG, false, true, 2, true>
+                  : (const void*)dv::interp2d_kernel<dv::kMapped, SG, false, false, 2, true>;
+  }
+  if (steps != 1) return nullptr;
   if (deriv)
     return loglog ? (const void*)dv::interp2d_kernel<1, SG, true, true, 2, true>
                   : (const void*)dv::interp2d_kernel<1, SG, true, false, 2, true>;
@@ -197,7 +252,8 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   if (!out) return EOS_ERR_NULL;
   *out = nullptr;
   if (!rho_host || !T_host || !P_host) return EOS_ERR_NULL;
-  if (flags & ~(EOS_GRID_LOGLOG | EOS_GRID_GLOBAL | EOS_GRID_EXACT)) return EOS_ERR_UNSUPPORTED;
+  if (flags & ~(EOS_GRID_LOGLOG | EOS_GRID_GLOBAL | EOS_GRID_EXACT | EOS_GRID_DIRECTORY))
+    return EOS_ERR_UNSUPPORTED;
   const bool loglog = (flags & EOS_GRID_LOGLOG) != 0;
   if (n_rho > 0 && n_T > 0 && n_rho * n_T > EOS_MAX_GRID_CELLS) return EOS_ERR_SIZE;
   eos_grid2d g = new (std::nothrow) eos_grid2d_s();
@@ -327,13 +383,25 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   }
   g->ar = axis_params(g->pr, 0);
   g->at = axis_params(g->pt, (int32_t)r_bytes);
+  // fitted cell maps: both axes, bank-pinned records, not EOS_GRID_DIRECTORY
+  if (g->rep == 2 && !(flags & EOS_GRID_DIRECTORY)) {
+    const CellMap mr = fit_cell_map(g->pr.X), mt = fit_cell_map(g->pt.X);
+    if (mr.kind && mt.kind) {
+      g->ar.map_kind = mr.kind;
+      g->ar.map_a = mr.a;
+      g->ar.map_b = mr.b;
+      g->at.map_kind = mt.kind;
+      g->at.map_a = mt.a;
+      g->at.map_b = mt.b;
+    }
+  }
   cudaError_t e = cudaGetDevice(&g->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device);
   if (e != cudaSuccess) return fail(cuda_status(e));
   st = upload(img, &g->image_dev);
   if (st != EOS_OK) return fail(st);
   const bool small_ok = !exp_small_off();
-  const int steps_max = std::max(g->pr.steps, g->pt.steps);
+  const int steps_max = g->ar.map_kind ? dv::kMapped : std::max(g->pr.steps, g->pt.steps);
   const void* fn_small = small_ok ? pick_interp_small(steps_max, loglog, g->rep, false) : nullptr;
   const void* fn_small_deriv =
       small_ok ? pick_interp_small(steps_max, loglog, g->rep, true) : nullptr;
@@ -466,8 +534,16 @@ eos_status eos_interp2d_host(eos_grid2d g, const double* rho_host, const double*
 
 eos_status eos_grid2d_info(eos_grid2d g, eos_table_info_t* rho_info, eos_table_info_t* T_info) {
   if (!g) return EOS_ERR_NULL;
-  if (rho_info) { eos::fill_info(g->pr, rho_info); rho_info->device = g->device; }
-  if (T_info) { eos::fill_info(g->pt, T_info); T_info->device = g->device; }
+  if (rho_info) {
+    eos::fill_info(g->pr, rho_info);
+    rho_info->device = g->device;
+    rho_info->cell_map = g->ar.map_kind;
+  }
+  if (T_info) {
+    eos::fill_info(g->pt, T_info);
+    T_info->device = g->device;
+    T_info->cell_map = g->at.map_kind;
+  }
   return EOS_OK;
 }
 

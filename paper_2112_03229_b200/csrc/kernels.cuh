@@ -60,7 +60,16 @@ struct AxisParams {
   int32_t mode;     // key mode (0: X[0] >= 0, sign-masked key; 1: order-preserving key)
   double x0;        // X[0]
   double xlast;     // X[n-1]
+  // 2-D grid axes with a fitted cell map (axis_cell_rec, S = kMapped; grid_api.cu
+  // fit_cell_map): cell(x) in {c, c + 1} for floor(map_a w(x) + map_b) = c (fp32),
+  // w = log2 x (map_kind 1) or x (map_kind 2); map_kind 0: none
+  float map_a;
+  float map_b;
+  int32_t map_kind;
 };
+// S of the 2-D kernels whose axes use their fitted cell maps instead of the
+// directories (bank-pinned records only)
+constexpr int kMapped = -1;
 
 struct SearchArgs {
   const uint4* image;   // device image (16-B aligned)
@@ -613,6 +622,12 @@ __device__ __forceinline__ int64_t clc_query(const uint4* resp) {
       : "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   return valid ? (int64_t)x : -1;
+}
+
+// TMA 1-D bulk prefetch of [src, src + bytes) into L2 (16-B aligned, bytes a
+// multiple of 16): no registers, no completion to wait for.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // TMA 1-D bulk copy global -> this CTA's shared memory, completing on `bar`.
@@ -1367,6 +1382,12 @@ __device__ __forceinline__ void axis_cell(double y, const double* __restrict__ s
 // the bin's entry (occ = 1, also the probe) or of the cell left of the bin
 // (occ = 0, then it is the cell); a second record is read only when the
 // probe moves the cell.
+//
+// S = kMapped (axes whose nodes follow a fitted map, grid_api.cu fit_cell_map): no
+// directory read.  p = floor(map_a w(y) + map_b), w = log2 y (MUFU.LG2) or y, in
+// fp32 and clamped to [0, n-2], is the cell of y or the one above (the host checks
+// every node against the device error bound), so the record at p is the cell's or,
+// when y < X[p], the next record down is (read only then).
 template <int S>
 __device__ __forceinline__ void axis_cell_rec(double y, const double* __restrict__ sX,
                                               const uint32_t* __restrict__ sD, const AxisParams& a,
@@ -1374,7 +1395,17 @@ __device__ __forceinline__ void axis_cell_rec(double y, const double* __restrict
                                               const double2* __restrict__ rec_, int32_t sh) {
   double2 r;
   int32_t p;
-  if (S == 1) {
+  if constexpr (S == kMapped) {
+    const float yf = __double2float_rn(y);
+    float l2;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(yf));
+    const float w = a.map_kind == 1 ? l2 : yf;
+    p = min(max(__float2int_rd(__fmaf_rn(w, a.map_a, a.map_b)), 0), a.n - 2);
+    r = rec_[p << sh];
+    // NaN: p = 0 (cvt of NaN), i = 0; y >= X[n-1]: p = n - 2 (the map), i = n - 1
+    i = (y >= a.x0) ? ((y >= a.xlast) ? a.n - 1 : p - (y < r.x ? 1 : 0)) : 0;
+    EOS_DCHECK(p >= 0 && p + 1 < a.n);
+  } else if constexpr (S == 1) {
     const uint32_t key = a.mode ? key_hi<1>(y) : key_hi<0>(y);
     const uint32_t d = sD[bin_of(key, a)];
     const int32_t lo = (int32_t)(d & 0xFFFFu);  // <= n-1
@@ -1417,12 +1448,12 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
   double ir = 0.0, it = 0.0;  // REP 2: inverse cell widths (in x, or in ln x for LOGLOG)
   double wr = 0.0, wt = 0.0;  // REP 0: cell widths (in x, or in ln x for LOGLOG)
   double tx, ty;              // the bilinear weights
-  if (LOGLOG) {
+  if constexpr (LOGLOG) {
     // R24: t = (ln x - ln X[c]) / (ln X[c+1] - ln X[c]), evaluated as
     // log1p((x - X[c]) / X[c]) / log1p((X[c+1] - X[c]) / X[c]) -- the same real
     // numbers, without the cancellation of ln x - ln X[c] (which loses
     // ~|ln x| / (cell width in ln) ulps).  Brackets and X[c] from the plain axes.
-    if (REP == 2) {
+    if constexpr (REP == 2) {
       // bank-pinned records (X[j], 1/ln(X[j+1]/X[j])), read as the linear grids read
       // theirs (the record is also the probe); no divides on the narrow-cell paths
       // (axes within [2^-1020, 2^1020], grid_api.cu)
@@ -1449,7 +1480,7 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
       tx = clamp01(__ddiv_rn(log1p(__ddiv_rn(__dsub_rn(rho, r0), r0)), wr));
       ty = clamp01(__ddiv_rn(log1p(__ddiv_rn(__dsub_rn(T, t0), t0)), wt));
     }
-  } else if (REP == 2) {
+  } else if constexpr (REP == 2) {
     const int32_t sh = A.rep_shift, c = threadIdx.x & ((1 << sh) - 1);  // this lane's copy
     axis_cell_rec<S>(rho, sR, dR, A.r, i, ci, r0, ir,
                      reinterpret_cast<const double2*>(sm + A.rr_off) + c, sh);
@@ -1515,6 +1546,7 @@ using Shape2DSmallGG = Shape<256, 1, 1, false>;
 
 template <int S, class SH, bool DERIV, bool LOGLOG = false, int REP = 0, bool GG = false>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {
+  static_assert(S != kMapped || REP == 2, "fitted cell maps read the bank-pinned records");
   constexpr int T = SH::kThreads;
   constexpr int U = SH::kUnroll;
   constexpr int TP = SH::kTilePairs;
@@ -1585,6 +1617,19 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
           vt[u] = ld_stream(T2 + tn * TP + threadIdx.x + u * T);
         }
       }
+#ifndef EOS_EXP_NO_L2_PREFETCH
+      if (!SH::kClc && !GG && threadIdx.x == 0) {
+        // the tile after next into L2 (static schedule): the register prefetch above
+        // then waits on L2, not DRAM -- one tile of loads per thread in flight is
+        // too few bytes to cover the DRAM latency at this rate.  (Not for grids in
+        // device memory, whose corner gathers share L2: big2d 128 -> 120 with it.)
+        const int64_t t2 = tn + gridDim.x;
+        if (t2 < ntiles && full(t2)) {
+          bulk_prefetch_l2(R2 + t2 * TP, (uint32_t)(TP * sizeof(double2)));
+          bulk_prefetch_l2(T2 + t2 * TP, (uint32_t)(TP * sizeof(double2)));
+        }
+      }
+#endif
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         __stcs(P2 + p0 + u * T, p[u]);

@@ -176,7 +176,7 @@ const char* eos_status_str(eos_status s) {
   return "unknown status";
 }
 
-int32_t eos_abi_version(void) { return 4; }
+int32_t eos_abi_version(void) { return 5; }
 
 int64_t eos_launch_count(void) { return eos::rt::g_launches.load(); }
 

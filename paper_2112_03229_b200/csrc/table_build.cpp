@@ -670,6 +670,7 @@ void fill_info(const TablePlan& p, eos_table_info_t* info) {
   info->fast_steps = p.fast_steps;
   info->rare_steps = p.big ? 1 : 0;
   info->ring_stages = 0;
+  info->cell_map = 0;
 }
 
 void fill_info(const TieredPlan& t, eos_table_info_t* info) {

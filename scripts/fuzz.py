@@ -115,7 +115,10 @@ def fuzz_2d(rng, dev, stats):
     mode1 = (not loglog) and bool(rng.integers(0, 3) == 0)
 
     def axis(n, lo, hi):
-        u = np.linspace(lo, hi, n) + (hi - lo) / max(n - 1, 1) * rng.uniform(-0.3, 0.3, n)
+        # logspace with a jitter of up to +-0.55 cells: fitted cell maps are accepted
+        # below a spread of ~1 cell and refused above (kernels.cuh axis_cell_rec)
+        amp = rng.uniform(0.0, 0.55)
+        u = np.linspace(lo, hi, n) + (hi - lo) / max(n - 1, 1) * rng.uniform(-amp, amp, n)
         v = 10.0 ** np.sort(u)
         return np.unique(v) if not mode1 else np.unique(np.sort(rng.normal(0, 50, n)))
 
@@ -135,6 +138,10 @@ def fuzz_2d(rng, dev, stats):
         rng.uniform(T[0] - 1, T[-1] + 1, m)
     k = min(m, R.size)
     rho[:k] = R[:k]
+    if m > 3 * k:  # next to the nodes: one ulp below, and within 1e-7 below
+        rho[k:2 * k] = np.nextafter(R[:k], -np.inf)
+        rho[2 * k:3 * k] = R[:k] - np.abs(R[:k]) * rng.uniform(0, 1e-7, k)
+    stats["mapped_grids"] += int(g.rho_info.cell_map != 0)
     P, iR, iT = g.interp(torch.from_numpy(rho).to(dev), torch.from_numpy(tt).to(dev))
     if loglog:
         Pr, iRr, iTr = oracle.interp2d_loglog(R, T, G, rho, tt)[:3]
@@ -163,7 +170,7 @@ def main():
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(a.seed)
     stats = {"tables": 0, "lookups": 0, "tiered": 0, "packed": 0, "direct_tables": 0, "max_n": 0, "rejected_plans": 0,
-             "grids": 0, "pairs": 0, "mismatches": []}
+             "grids": 0, "mapped_grids": 0, "pairs": 0, "mismatches": []}
     t_end = time.time() + 60 * a.minutes
     it = 0
     while time.time() < t_end:

@@ -1152,6 +1152,9 @@ def test_interp_regular_axes_node_targets(axes, loglog):
     rho[3 * k:3 * k + 6] = [np.nan, np.inf, -np.inf, 0.0, -0.0, -1.0]
     tt[3 * k + 6:3 * k + 12] = [np.nan, np.inf, -np.inf, 0.0, -0.0, -1.0]
     g = eos.Grid2D(R, T, G, loglog=loglog)
+    # regular axes take fitted cell maps (1: log, 2: linear), both axes or neither
+    assert (g.rho_info.cell_map, g.T_info.cell_map) == {
+        "logspace": (1, 1), "linspace": (2, 2), "mixed": (1, 2), "perturbed": (1, 1)}[axes]
     P, iR, iT, dR, dT = g.interp(to_dev(rho), to_dev(tt), derivatives=True)
     P0, iR0, iT0 = g.interp(to_dev(rho), to_dev(tt))
     torch.cuda.synchronize()
@@ -1167,6 +1170,85 @@ def test_interp_regular_axes_node_targets(axes, loglog):
     kr, kt = deriv_cond(R, T, G, rho, tt, iRr, iTr, Pr, loglog)
     _check_deriv(dR.cpu().numpy(), dRr, kr)
     _check_deriv(dT.cpu().numpy(), dTr, kt)
+    g.close()
+
+
+def _near_node_targets(rng, X, m):
+    """m targets: random in range and beyond, every node, its neighbours one ulp away,
+    and points within 1e-7 relative below each node (where a fitted map is near the top
+    of its unit)."""
+    n = X.size
+    lo, hi = (np.log(X[0]), np.log(X[-1])) if X[0] > 0 else (None, None)
+    y = (np.exp(rng.uniform(lo - 0.3, hi + 0.3, m)) if lo is not None
+         else rng.uniform(X[0] - 0.1 * (X[-1] - X[0]), X[-1] + 0.1 * (X[-1] - X[0]), m))
+    k = 0
+    for part in (X, np.nextafter(X, -np.inf), np.nextafter(X, np.inf),
+                 X - np.abs(X) * rng.uniform(0, 1e-7, n)):
+        y[k:k + n] = part
+        k += n
+    return y
+
+
+@pytest.mark.parametrize("loglog,global_grid", [(False, False), (True, False), (False, True),
+                                                (True, True)])
+def test_cell_map_equals_directory_lookup_cfg4(loglog, global_grid):
+    """cfg4's log-spaced axes take the fitted log map; the mapped kernels give results
+    bit-identical to the directory kernels (EOS_GRID_DIRECTORY) -- P, brackets and both
+    derivatives -- on random, node, near-node and special targets, and the brackets
+    equal the oracle's."""
+    w = datagen.workload("cfg4", count=1 << 20)
+    rng = np.random.default_rng(44)
+    rho = np.concatenate([w.rho_targets.host_fill(0, w.count), _near_node_targets(rng, w.rho, 4096)])
+    tt = np.concatenate([w.T_targets.host_fill(0, w.count), _near_node_targets(rng, w.T, 4096)])
+    tt[-4096:] = tt[-4096:][rng.permutation(4096)]
+    rho[:8] = [np.nan, np.inf, -np.inf, 0.0, -0.0, -1.0, 5e-324, 1e308]
+    tt[8:16] = [np.nan, np.inf, -np.inf, 0.0, -0.0, -1.0, 5e-324, 1e308]
+    gm = eos.Grid2D(w.rho, w.T, w.P, loglog=loglog, global_grid=global_grid)
+    gd = eos.Grid2D(w.rho, w.T, w.P, loglog=loglog, global_grid=global_grid, directory=True)
+    assert (gm.rho_info.cell_map, gm.T_info.cell_map) == (1, 1)
+    assert (gd.rho_info.cell_map, gd.T_info.cell_map) == (0, 0)
+    outs = []
+    for g in (gm, gd):
+        outs.append([t.cpu().numpy() for t in g.interp(to_dev(rho), to_dev(tt), derivatives=True)])
+        outs.append([t.cpu().numpy() for t in g.interp(to_dev(rho), to_dev(tt))])
+    for a, b in zip(outs[0] + outs[1], outs[2] + outs[3]):
+        assert np.array_equal(a.view(np.uint64) if a.dtype == np.float64 else a,
+                              b.view(np.uint64) if b.dtype == np.float64 else b)
+    iRr, iTr = oracle.search(w.rho, rho), oracle.search(w.T, tt)
+    assert np.array_equal(outs[0][1], iRr) and np.array_equal(outs[0][2], iTr)
+    gm.close()
+    gd.close()
+
+
+@pytest.mark.parametrize("dev", [0.2, 0.45, 0.49, 0.7])
+@pytest.mark.parametrize("kind", ["log", "linear"])
+def test_cell_map_near_its_acceptance_bound(dev, kind):
+    """Axes whose nodes drift off a regular grid by up to 2 dev cells (0 at the ends,
+    the most in the middle, plus an alternating +-dev/4 jitter): the fitted map is
+    accepted while the nodes' spread leaves room for the device error bound (dev <=
+    0.49) and refused above (0.7); either way brackets equal the oracle's and P is
+    within the bar, including targets at the nodes, one ulp around them and within
+    1e-7 below them."""
+    rng = np.random.default_rng(int(dev * 100) + (kind == "log"))
+    def axis(n, a, b):
+        j = np.arange(n)
+        wob = np.sin(np.pi * j / (n - 1))
+        u = j + (2 * dev - dev / 2) * wob + dev / 4 * np.where(j % 2 == 0, -1.0, 1.0) * wob
+        u[0], u[-1] = 0.0, n - 1.0
+        return np.exp(a + (b - a) * u / (n - 1)) if kind == "log" else a + (b - a) * u / (n - 1)
+    R, T = axis(150, -5.0, 4.0), axis(90, 0.5, 9.0)
+    G = rng.uniform(1.0, 2.0, (R.size, T.size))
+    m = 1 << 18
+    rho, tt = _near_node_targets(rng, R, m), _near_node_targets(rng, T, m)
+    tt = tt[rng.permutation(m)]
+    g = eos.Grid2D(R, T, G)
+    want = (1 if kind == "log" else 2) if dev < 0.5 else 0
+    assert (g.rho_info.cell_map, g.T_info.cell_map) == (want, want)
+    P, iR, iT = g.interp(to_dev(rho), to_dev(tt))
+    torch.cuda.synchronize()
+    Pr, iRr, iTr = oracle.interp2d(R, T, G, rho, tt)
+    assert np.array_equal(iR.cpu().numpy(), iRr) and np.array_equal(iT.cpu().numpy(), iTr)
+    check_interp(P.cpu().numpy(), Pr)
     g.close()
 
 

@@ -37,9 +37,30 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert declared == set(eos.EXPORTED_SYMBOLS)
     for s in declared:
         assert hasattr(L, s), s
-    assert L.eos_abi_version() == 4
+    assert L.eos_abi_version() == 5
     assert eos.eos_status_str(0) == "ok"
     assert "sorted" in eos.eos_status_str(4)
+
+
+def test_table_info_struct_layout_matches_the_header(tmp_path):
+    """The ctypes mirror of eos_table_info_t has the C struct's size and field offsets
+    (gcc on include/eossearch.h), so eos_*_info never writes past a Python buffer."""
+    import ctypes
+    import subprocess
+    fields = [f for f, _ in eos.TableInfo._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "eossearch.h"\n'
+                   "int main(void) {\n"
+                   '  printf("%zu\\n", sizeof(eos_table_info_t));\n'
+                   + "".join(f'  printf("%zu\\n", offsetof(eos_table_info_t, {f}));\n' for f in fields)
+                   + "  return 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(_build.ROOT, "include"), "-o", str(exe),
+                    str(src)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    assert got[0] == ctypes.sizeof(eos.TableInfo)
+    assert got[1:] == [getattr(eos.TableInfo, f).offset for f in fields]
 
 
 def test_sm100a_cubin_embedded():
@@ -442,7 +463,7 @@ def test_grid_cell_limit_checked_before_any_work():
     rc = L.eos_grid2d_create_ex(R.ctypes.data, R.size, T.ctypes.data, T.size, P.ctypes.data, 0,
                                 ctypes.byref(h))
     assert rc == 2
-    rc = L.eos_grid2d_create_ex(R.ctypes.data, 4, T.ctypes.data, 4, P.ctypes.data, 8,
+    rc = L.eos_grid2d_create_ex(R.ctypes.data, 4, T.ctypes.data, 4, P.ctypes.data, 16,
                                 ctypes.byref(h))
     assert rc == 8
 
