@@ -413,7 +413,8 @@ def bench_config(a, w, world):
 
 def plan_signature(a, obj, is2d):
     if is2d:
-        return {"kind": "interp2d", "loglog": a.loglog, "global_grid": a.global_grid}
+        return {"kind": "interp2d", "loglog": a.loglog, "global_grid": a.global_grid,
+                "derivatives": a.derivatives}
     i = obj.info
     return {"kind": "tiered" if i.levels > 0 else ("direct" if a.direct else "search"),
             "hash_kind": i.hash_kind, "bins": i.bins, "steps": i.steps,

@@ -9,6 +9,9 @@
 //   EOS_LAYOUT=d16,sf,big                   lifting layout of a single-level table
 //   EOS_SMALL_TILES=0                       small launches keep the default tiles
 //   EOS_RING=<n>                            at most n ring stages (0: no ring kernel)
+// and compile-time A/B flags of that build (-D...):
+//   EOS_EXP_NO_L2_PREFETCH                  2-D kernels without the L2 prefetch of the
+//                                           tile after next
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
