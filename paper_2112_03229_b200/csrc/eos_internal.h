@@ -19,6 +19,9 @@ namespace eos {
 //   mode 1 (negatives present): order-preserving transform of the bits of
 //     (v + 0.0) (canonicalises -0.0), monotone over all non-NaN doubles.
 uint32_t key_hi(double v, int mode);
+// The whole 64-bit order-preserving key of which key_hi is the upper word (the
+// packed tables' residuals take bits below it, PackedPlan).
+uint64_t key64(double v, int mode);
 
 // The one bin function of both hashes (host copy of kernels.cuh::bin_of):
 //   bin(v) = min( umulhi( max(key_hi(v), hb) - hb, M ), bmax )
@@ -126,17 +129,20 @@ eos_status plan_tiered(const double* X, int64_t n, int levels, int kind, int64_t
 // residual keys, so a lookup gathers ONE sector from L2 (the 8-ary levels
 // above gather D).
 //   nodes:  node j covers X[15 j .. 15 j + 15) (kPackedNode entries); word 0 is
-//           B_j | s_j with B_j = key(X[15 j]) & ~31 and s_j (< 32) the
-//           smallest shift with (key(X[last of node]) - B_j) >> s_j <= 0x77FF;
-//           words 1..7 hold the 14 residuals r_t = ((key(X[15 j + t]) - B_j) >>
-//           s_j) + 0x400, t = 1..14, two per word (t odd in the low half), and
-//           0x7C00 past n: as fp16 bit patterns these are normal positive
-//           halves (or +inf past n) in the order of the keys, so the kernel
-//           compares two per HSET2.
+//           B_j | s_j with B_j = key_hi(X[15 j]) & ~63 and s_j (< 64) the
+//           smallest shift with (key64(X[last of node]) - (B_j << 32)) >> s_j <=
+//           0x77FF; words 1..7 hold the 14 residuals r_t = ((key64(X[15 j + t])
+//           - (B_j << 32)) >> s_j) + 0x400, t = 1..14, two per word (t odd in the
+//           low half), and 0x7C00 past n: as fp16 bit patterns these are normal
+//           positive halves (or +inf past n) in the order of the keys, so the
+//           kernel compares two per HSET2.  (64-bit keys: a node of a dense
+//           table spans only a few hundred units of the 32-bit key, where equal
+//           residuals -- each settled from X -- came for ~2% of lookups.)
 //   sample: T1[j] = X[15 j], j < n1 = ceil(n / 15), binned by the key-bit hash
 //           bin = min((max(key, hb) - hb) >> sh, bmax) (hb aligned to 2^sh: the
 //           exponent hash of k = 20 - sh mantissa bits); the image holds the
-//           residuals key(T1[j]) & (2^sh - 1) as u16, sh <= 16, then the
+//           residuals -- the 16 key64 bits right below the bin bits, ((key64 -
+//           (hb << 32)) >> (16 + sh)) & 0xFFFF, sh <= 16 -- as u16, then the
 //           directory: one u32 per pair of bins (2g, 2g + 1), lo(2g) | occ(2g)
 //           << 20 | occ(2g + 1) << 26 (occ <= 63, n1 <= 2^20).
 // Truncation keeps the order: r(X) < r(y) => X < y and r(X) > r(y) => X > y;

@@ -110,6 +110,14 @@ __device__ __forceinline__ uint32_t key_hi(double y) {
   return h ^ ((uint32_t)((int32_t)h >> 31) | 0x80000000u);
 }
 
+// The whole 64-bit key (host: eos_internal.h key64); key_hi is its upper word.
+template <int MODE>
+__device__ __forceinline__ uint64_t key64(double y) {
+  if (MODE == 0) return (uint64_t)__double_as_longlong(y) & 0x7FFFFFFFFFFFFFFFull;
+  const uint64_t b = (uint64_t)__double_as_longlong(__dadd_rn(y, 0.0));
+  return b ^ ((uint64_t)((int64_t)b >> 63) | 0x8000000000000000ull);
+}
+
 // The bin function of both hashes (host copy: eos_internal.h::bin_of_key).
 __device__ __forceinline__ uint32_t bin_of(uint32_t key, const AxisParams& a) {
   return min(__umulhi(max(key, a.hb) - a.hb, a.M), a.bmax);
@@ -282,6 +290,7 @@ struct Counters {
 template <int SF, bool BIG, int MODE, bool D16>
 struct SmemLookup {
   static constexpr bool kBatchTail = true;  // ragged tiles: one batched lookup per thread
+  static constexpr bool kEarlyLoad = true;  // static schedule: next tile's loads first
   const double* __restrict__ sX;
   const void* __restrict__ sD;
   AxisParams a;
@@ -382,6 +391,7 @@ __device__ __forceinline__ int32_t lookup_keys(double y, uint32_t ky,
 template <int S, int MODE>
 struct TieredLookup {
   static constexpr bool kBatchTail = false;  // (batching the tail made the kernel spill)
+  static constexpr bool kEarlyLoad = false;  // (n = 2^18: 185 -> 181; D = 2: +1.3%)
   const uint32_t* __restrict__ sK;  // keys of T1 (smem)
   const uint32_t* __restrict__ sD;
   AxisParams a;                   // of T1, except xlast = X[n-1] (counter c4)
@@ -442,11 +452,11 @@ struct TieredLookup {
 // PackedLookup (packed tables, eossearch.h EOS_LEVELS_PACKED; layout in
 // eos_internal.h PackedPlan): ONE L2 sector per lookup.  Per target:
 //   sample (smem): u = max(key, hb) - hb, bin b = min(u >> sh, bmax), rk = the
-//     low sh bits of u (0xFFFF past the last bin); lifting counts the bin's
-//     residuals <= rk, a run equal to rk settled from X[15 j] (global);
-//     j = max(#{T1 <= y} - 1, 0)
+//     16 bits of key64 - (hb << 32) below the bin bits (0xFFFF past the last
+//     bin); lifting counts the bin's residuals <= rk, a run equal to rk settled
+//     from X[15 j] (global); j = max(#{T1 <= y} - 1, 0)
 //   node j (one 32-B sector, ld.global.nc, L1 no-allocate): B | s, r_1..r_14;
-//     ry = min((max(key, B) - B) >> s, 0x77FF); the residuals are sorted, so
+//     ry = min((max(key64, B << 32) - (B << 32)) >> s, 0x77FF); the residuals are sorted, so
 //     lt = #{r_t < ry} and le = #{r_t <= ry} (fp16x2 compares of the biased
 //     values, 14 at a time in 7 HSET2 each) bound the run of equal residuals,
 //     settled from X[15 j + t] (rare)
@@ -473,6 +483,7 @@ __device__ __forceinline__ uint32_t h2_as_u32(__half2 h) {
 template <int S, int MODE>
 struct PackedLookup {
   static constexpr bool kBatchTail = false;
+  static constexpr bool kEarlyLoad = true;
   const uint16_t* __restrict__ sR;  // sample residuals (smem)
   const uint32_t* __restrict__ sD;  // directory, one u32 per bin pair (smem)
   AxisParams a;                     // n = n1; hb, bmax of the sample hash; x0, xlast of X
@@ -496,7 +507,9 @@ struct PackedLookup {
           MODE == 0 ? (uint32_t)max((int32_t)(ky[i] - a.hb), 0) : max(ky[i], a.hb) - a.hb;
       const uint32_t q = u >> sh;
       const uint32_t b = min(q, a.bmax);
-      rk[i] = q > a.bmax ? 0xFFFFu : (u & ((1u << sh) - 1u));
+      // (u : low word of key64) >> (16 + sh), the low word 0 below hb
+      const uint32_t lw = ky[i] >= a.hb ? (uint32_t)key64<MODE>(y[i]) : 0u;
+      rk[i] = q > a.bmax ? 0xFFFFu : (__funnelshift_rc(lw, u, 16u + sh) & 0xFFFFu);
       // one u32 entry per bin pair: lo(pair) | occ(even bin) << 20 | occ(odd bin) << 26
       const uint32_t d = sD[b >> 1];
       const uint32_t o0 = (d >> 20) & 63u;
@@ -547,8 +560,10 @@ struct PackedLookup {
     int32_t lt[N], le[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const uint32_t B = k[i][0] & ~31u, s = k[i][0] & 31u;
-      const uint32_t ry = min((max(ky[i], B) - B) >> s, kResMax) + kResBias;
+      const uint64_t B = (uint64_t)(k[i][0] & ~63u) << 32;
+      const uint32_t s = k[i][0] & 63u;
+      const uint64_t k64 = key64<MODE>(y[i]);
+      const uint32_t ry = (uint32_t)min((max(k64, B) - B) >> s, (uint64_t)kResMax) + kResBias;
       const __half2 hy = u32_as_h2(ry * 0x10001u);
       // lane sums start at 512 (ulp 0.5) so the final 1024 + count is exact
       __half2 a = u32_as_h2(0x60006000u), e = a;
@@ -799,11 +814,27 @@ __device__ __forceinline__ void search_body(const SearchArgs& args, const LK& lk
     }
     for (; t < nfull; t += gridDim.x) {
       int2 r[U];
+      if constexpr (!CNT && LK::kEarlyLoad) {
+        // the next tile's loads go out before this tile's lookups (a whole tile of
+        // lookups to cover their latency, not just the stores); v is copied first.
+        // Packed tables 191 -> 211 Glookups/s; single-level tables +1.5%; 8-ary
+        // levels mixed
+        double2 w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) w[u] = v[u];
+        yp += step;
+        if (t + gridDim.x < nfull) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) v[u] = ld_stream(yp + u * T);
+        }
+        compute(w, r, t);
+      } else {
       compute(v, r, t);
       yp += step;
       if (t + gridDim.x < nfull) {
 #pragma unroll
         for (int u = 0; u < U; ++u) v[u] = ld_stream(yp + u * T);
+      }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) __stcs(op + u * T, r[u]);
@@ -1602,6 +1633,32 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       EOS_DCHECK(2 * (p0 + (U - 1) * T) + 1 < count);
       double2 p[U], dr[U], dt[U];
       int2 ir[U], it[U];
+#ifdef EOS_EXP_EARLY_LOAD_2D
+      if constexpr (!SH::kClc) {  // static: the next tile's loads before this tile's pairs
+        double2 cr[U], ct[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          cr[u] = vr[u];
+          ct[u] = vt[u];
+        }
+        tn = t + gridDim.x;
+        if (tn < ntiles && full(tn)) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            vr[u] = ld_stream(R2 + tn * TP + threadIdx.x + u * T);
+            vt[u] = ld_stream(T2 + tn * TP + threadIdx.x + u * T);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          p[u].x = interp_one<S, DERIV, LOGLOG, REP, GG>(cr[u].x, ct[u].x, ir[u].x, it[u].x, dr[u].x,
+                                                         dt[u].x, sm, A);
+          p[u].y = interp_one<S, DERIV, LOGLOG, REP, GG>(cr[u].y, ct[u].y, ir[u].y, it[u].y, dr[u].y,
+                                                         dt[u].y, sm, A);
+        }
+      } else
+#endif
+      {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         p[u].x = interp_one<S, DERIV, LOGLOG, REP, GG>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
@@ -1616,6 +1673,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
           vr[u] = ld_stream(R2 + tn * TP + threadIdx.x + u * T);
           vt[u] = ld_stream(T2 + tn * TP + threadIdx.x + u * T);
         }
+      }
       }
 #ifndef EOS_EXP_NO_L2_PREFETCH
       if (!SH::kClc && !GG && threadIdx.x == 0) {

@@ -25,6 +25,17 @@ uint32_t key_hi(double v, int mode) {
   return (h & 0x80000000u) ? ~h : (h | 0x80000000u);
 }
 
+uint64_t key64(double v, int mode) {
+  uint64_t b;
+  if (mode == 0) {
+    memcpy(&b, &v, 8);
+    return b & 0x7FFFFFFFFFFFFFFFull;
+  }
+  double c = v + 0.0;  // -0.0 -> +0.0 (round-to-nearest)
+  memcpy(&b, &c, 8);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
 namespace {
 
 int ceil_log2_plus1(int occ) {  // S = ceil(log2(occ + 1)), occ >= 0
@@ -547,7 +558,6 @@ eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t bu
   }
   if (p.sh == 0) return EOS_ERR_UNSUPPORTED;
   const int sh = p.sh;
-  const uint32_t mask = (1u << sh) - 1u;
   try {
     p.image.assign((size_t)(rbytes + pad16(4 * (((int64_t)p.bins + 1) / 2))), 0);
     p.nodes.assign((size_t)(8 * n1), 0);
@@ -557,8 +567,10 @@ eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t bu
   // sample residuals (the kernel's rk of the entry's own key) and directory
   std::vector<uint32_t> lo((size_t)p.bins, 0), occ((size_t)p.bins, 0);
   for (int64_t j = 0; j < n1; ++j) {
+    // the 16 bits of key64 - (hb << 32) right below the bin bits (entries >= hb)
     const uint32_t u = (K1[j] > p.hb ? K1[j] : p.hb) - p.hb;
-    const uint16_t r = (uint16_t)(u & mask);
+    const uint64_t u64 = K1[j] >= p.hb ? key64(T1[j], mode) - ((uint64_t)p.hb << 32) : 0;
+    const uint16_t r = (uint16_t)(u64 >> (16 + sh));
     memcpy(p.image.data() + 2 * j, &r, 2);
     const uint32_t b = std::min(u >> sh, p.bmax);
     if (occ[b]++ == 0) lo[b] = (uint32_t)j;
@@ -577,8 +589,9 @@ eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t bu
   for (int64_t j = 0; j < n1; ++j) {
     const int64_t i0 = j * kPackedNode;
     const int64_t last = std::min<int64_t>(i0 + kPackedNode - 1, n - 1);
-    const uint32_t Bm = key_hi(p.X[i0], mode) & ~31u;
-    const uint32_t span = key_hi(p.X[last], mode) - Bm;
+    const uint32_t Bm = key_hi(p.X[i0], mode) & ~63u;
+    const uint64_t base = (uint64_t)Bm << 32;
+    const uint64_t span = key64(p.X[last], mode) - base;
     uint32_t s = 0;
     while ((span >> s) > kPackedResMax) ++s;
     uint32_t* w = p.nodes.data() + 8 * j;
@@ -586,7 +599,7 @@ eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t bu
     for (int t = 1; t < kPackedNode; ++t) {
       const int64_t i = i0 + t;
       const uint32_t r =
-          i < n ? ((key_hi(p.X[i], mode) - Bm) >> s) + kPackedResBias : kPackedResPad;
+          i < n ? (uint32_t)((key64(p.X[i], mode) - base) >> s) + kPackedResBias : kPackedResPad;
       w[(t + 1) / 2] |= (t & 1) ? r : (r << 16);
     }
   }
