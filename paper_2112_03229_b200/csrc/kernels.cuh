@@ -1633,32 +1633,6 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       EOS_DCHECK(2 * (p0 + (U - 1) * T) + 1 < count);
       double2 p[U], dr[U], dt[U];
       int2 ir[U], it[U];
-#ifdef EOS_EXP_EARLY_LOAD_2D
-      if constexpr (!SH::kClc) {  // static: the next tile's loads before this tile's pairs
-        double2 cr[U], ct[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          cr[u] = vr[u];
-          ct[u] = vt[u];
-        }
-        tn = t + gridDim.x;
-        if (tn < ntiles && full(tn)) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            vr[u] = ld_stream(R2 + tn * TP + threadIdx.x + u * T);
-            vt[u] = ld_stream(T2 + tn * TP + threadIdx.x + u * T);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          p[u].x = interp_one<S, DERIV, LOGLOG, REP, GG>(cr[u].x, ct[u].x, ir[u].x, it[u].x, dr[u].x,
-                                                         dt[u].x, sm, A);
-          p[u].y = interp_one<S, DERIV, LOGLOG, REP, GG>(cr[u].y, ct[u].y, ir[u].y, it[u].y, dr[u].y,
-                                                         dt[u].y, sm, A);
-        }
-      } else
-#endif
-      {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         p[u].x = interp_one<S, DERIV, LOGLOG, REP, GG>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
@@ -1674,13 +1648,13 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
           vt[u] = ld_stream(T2 + tn * TP + threadIdx.x + u * T);
         }
       }
-      }
 #ifndef EOS_EXP_NO_L2_PREFETCH
       if (!SH::kClc && !GG && threadIdx.x == 0) {
-        // the tile after next into L2 (static schedule): the register prefetch above
-        // then waits on L2, not DRAM -- one tile of loads per thread in flight is
-        // too few bytes to cover the DRAM latency at this rate.  (Not for grids in
-        // device memory, whose corner gathers share L2: big2d 128 -> 120 with it.)
+        // the tile after next into L2 (static schedule): the register loads above,
+        // issued only after this tile's pairs (a register double buffer issued
+        // before them measured 175 -> 153 Gpairs/s at the 64-register cap), then
+        // wait on L2, not DRAM.  (Not for grids in device memory, whose corner
+        // gathers share L2: big2d 128 -> 120 with it.)
         const int64_t t2 = tn + gridDim.x;
         if (t2 < ntiles && full(t2)) {
           bulk_prefetch_l2(R2 + t2 * TP, (uint32_t)(TP * sizeof(double2)));
