@@ -42,7 +42,8 @@ extern "C" {
 #define EOS_MAX_TABLE 16384 /* table entries staged in shared memory (fp64) */
 #define EOS_MAX_TABLE_TIERED (1 << 29) /* entries of a tiered table */
 #define EOS_LEVELS_AUTO (-1)           /* eos_search_create_levels: choose the structure */
-#define EOS_LEVELS_PACKED (-2)         /* eos_search_create_levels: one level of packed nodes */
+#define EOS_LEVELS_PACKED (-2)         /* eos_search_create_levels: packed nodes, the fewest levels that fit */
+#define EOS_LEVELS_PACKED_DEPTH(d) (-16 - (d)) /* ... packed nodes, exactly d = 1..4 levels */
 #define EOS_MAX_K 19        /* mantissa bits appended to the exponent hash */
 #define EOS_K_AUTO (-1)     /* let eos_search_create_ex choose the hash */
 
@@ -194,22 +195,26 @@ EOS_API eos_status eos_search_create_hash(const double* table_host, int64_t n, i
  *     n1 8^(D-d) entries (~1.7 x 8n bytes in all).  A level step reads the
  *     8 keys of a node (one 32-byte sector): c = #{t : key_t < key(y)}, and
  *     the node's fp64 values only when a key equals key(y); b = 8b + c - 1.
- *   levels = EOS_LEVELS_PACKED: one level of packed nodes (info: levels = 1,
- *     node_width = 15).  Node j is one 32-byte sector holding the key of
- *     X[15j] (rounded down to a multiple of 32, its low 5 bits a shift s_j)
- *     and the 16-bit residuals ((key(X[15j+t]) - base) >> s_j) + 0x400,
- *     t = 1..14 (<= 0x7BFF: positive normal fp16 patterns; 0x7C00 past n); the
- *     sample table T1[j] = X[15j], j < n1 = ceil(n/15), is held in shared
- *     memory as the low sh <= 16 bits of its keys, binned by the key's upper
- *     bits (the exponent hash with k = 20 - sh), with one 32-bit directory
- *     entry per pair of bins (the pair's first index, both occupancies).
- *     A lookup reads one node from L2; equal residuals are settled from the
- *     fp64 table in device memory (8n + 32 n1 bytes in all).  Fits while the
- *     sample table and its directory take <= 224 KB (n up to ~1.5e6 for
- *     log-spread tables); otherwise EOS_ERR_UNSUPPORTED.  kind/param ignored.
+ *   levels = EOS_LEVELS_PACKED / EOS_LEVELS_PACKED_DEPTH(D): D = 1..4 levels
+ *     of packed nodes (info: levels = D, node_width = 15; EOS_LEVELS_PACKED
+ *     takes the smallest D that fits).  Node j of level d (d = D-1..0) is one
+ *     32-byte sector covering X[15^(d+1) j + 15^d t], t = 0..14: the upper
+ *     key word of its first entry rounded down to a multiple of 64 (B, its low
+ *     6 bits a shift s) and the 16-bit residuals ((key64(entry t) - (B << 32))
+ *     >> s) + 0x400, t = 1..14 (<= 0x7BFF: positive normal fp16 patterns;
+ *     0x7C00 past n), key64 the 64-bit order-preserving key.  The sample table
+ *     T1[j] = X[15^D j], j < n1 = ceil(n/15^D), is held in shared memory as the
+ *     16 key bits below its bin bits (binned by the key's upper bits: the
+ *     exponent hash with k = 20 - sh), with one 32-bit directory entry per pair
+ *     of bins.  A lookup reads D nodes from L2; equal residuals are settled
+ *     from the fp64 table in device memory (8n + ~34 n / 15 bytes in all).
+ *     The sample table and its directory must fit 224 KB (D = 1: n up to
+ *     ~1.5e6 for log-spread tables; D = 4 covers 2^29); otherwise
+ *     EOS_ERR_UNSUPPORTED.  kind/param ignored.
  *     EOS_LEVELS_AUTO: D = 0 if n <= EOS_MAX_TABLE; else packed if n > 8 x
- *     32768 (where 8-ary levels need D >= 2), it fits and kind is
- *     EOS_HASH_AUTO; else the smallest D with n1 <= 32768.
+ *     32768 (where 8-ary levels need D >= 2), kind is EOS_HASH_AUTO and the
+ *     packed depth that fits is not larger than the 8-ary depth; else the
+ *     smallest 8-ary D with n1 <= 32768.
  *   kind/param: the hash of the shared-memory table (T1 when D >= 1), as in
  *     eos_search_create_hash.
  * Errors: EOS_ERR_SIZE (n out of range, or n1 too large for the given D:

@@ -33,12 +33,18 @@ __all__ = [
     "EOS_GRID_LOGLOG", "EOS_MAX_TABLE_TIERED", "EOS_LEVELS_AUTO", "eos_search_create_levels",
     "eos_plan_table_levels", "plan_table_levels", "EOS_GRID_GLOBAL", "EOS_MAX_GRID_CELLS",
     "EOS_GRID_EXACT", "ABI_VERSION", "EOS_LEVELS_PACKED", "EOS_GRID_DIRECTORY",
+    "EOS_LEVELS_PACKED_DEPTH",
 ]
 
 EOS_MAX_TABLE = 16384
 EOS_MAX_TABLE_TIERED = 1 << 29
 EOS_LEVELS_AUTO = -1
 EOS_LEVELS_PACKED = -2
+
+
+def EOS_LEVELS_PACKED_DEPTH(d: int) -> int:
+    """eos_search_create_levels: packed nodes with exactly d = 1..4 levels."""
+    return -16 - d
 EOS_MAX_K = 19
 EOS_K_AUTO = -1
 EOS_HASH_AUTO, EOS_HASH_EXPONENT, EOS_HASH_LOG = 0, 1, 2
@@ -383,8 +389,9 @@ class Table:
         """k: exponent hash with k mantissa bits; log_bins: logarithm hash with |H| bins;
         neither: the automatic choice.  levels: D 8-ary global levels
         under a shared-memory sample table (tables above EOS_MAX_TABLE entries need
-        D >= 1), EOS_LEVELS_PACKED (one level of packed 16-bit residual nodes, DESIGN.md
-        §6.5) or EOS_LEVELS_AUTO.  Results never depend on any of them."""
+        D >= 1), EOS_LEVELS_PACKED (packed 16-bit residual nodes, the fewest levels that
+        fit), EOS_LEVELS_PACKED_DEPTH(d) (exactly d levels of them) or
+        EOS_LEVELS_AUTO.  Results never depend on any of them."""
         self.X = _f64_host(table)
         self._h = eos_search_create_levels(self.X, levels, *_hash_args(k, log_bins))
         self.info = eos_table_info(self._h)

@@ -124,10 +124,12 @@ struct TieredPlan {
 eos_status plan_tiered(const double* X, int64_t n, int levels, int kind, int64_t param,
                        TieredPlan* out);
 
-// Packed tables (eossearch.h EOS_LEVELS_PACKED): one level of 32-byte nodes
-// of 16-bit residual keys under a shared-memory sample table of 16-bit
-// residual keys, so a lookup gathers ONE sector from L2 (the 8-ary levels
-// above gather D).
+// Packed tables (eossearch.h EOS_LEVELS_PACKED): D levels of 32-byte nodes of
+// 16-bit residual keys under a shared-memory sample table of 16-bit residual
+// keys, so a lookup gathers D sectors from L2 -- one for tables up to ~1.5e6
+// entries (the 8-ary levels gather ~log8 of n / 32768 more).  Level d (stored
+// D-1 .. 0) holds ceil(n / 15^(d+1)) nodes; node j of level d covers the 15
+// entries X[15^(d+1) j + 15^d t], t = 0..14 (below: d = 0, stride 1).
 //   nodes:  node j covers X[15 j .. 15 j + 15) (kPackedNode entries); word 0 is
 //           B_j | s_j with B_j = key_hi(X[15 j]) & ~63 and s_j (< 64) the
 //           smallest shift with (key64(X[last of node]) - (B_j << 32)) >> s_j <=
@@ -138,16 +140,18 @@ eos_status plan_tiered(const double* X, int64_t n, int levels, int kind, int64_t
 //           kernel compares two per HSET2.  (64-bit keys: a node of a dense
 //           table spans only a few hundred units of the 32-bit key, where equal
 //           residuals -- each settled from X -- came for ~2% of lookups.)
-//   sample: T1[j] = X[15 j], j < n1 = ceil(n / 15), binned by the key-bit hash
+//   sample: T1[j] = X[15^D j], j < n1 = ceil(n / 15^D), binned by the key-bit hash
 //           bin = min((max(key, hb) - hb) >> sh, bmax) (hb aligned to 2^sh: the
 //           exponent hash of k = 20 - sh mantissa bits); the image holds the
 //           residuals -- the 16 key64 bits right below the bin bits, ((key64 -
 //           (hb << 32)) >> (16 + sh)) & 0xFFFF, sh <= 16 -- as u16, then the
 //           directory: one u32 per pair of bins (2g, 2g + 1), lo(2g) | occ(2g)
-//           << 20 | occ(2g + 1) << 26 (occ <= 63, n1 <= 2^20).
+//           << 20 | occ(2g + 1) << 26 (occ <= 63, n1 <= 2^20), 16-B padded, then
+//           the level table: int32 first node of level d [4], 15^d [4].
 // Truncation keeps the order: r(X) < r(y) => X < y and r(X) > r(y) => X > y;
 // equal residuals are settled from the fp64 values (X in device memory).
 constexpr int kPackedNode = 15;
+constexpr int kPackedMaxDepth = 4;  // levels of nodes (n <= 2^29 needs 4)
 constexpr uint32_t kPackedResMax = 0x77FFu;   // largest residual (biased: 0x7BFF)
 constexpr uint32_t kPackedResBias = 0x0400u;  // smallest normal fp16
 constexpr uint32_t kPackedResPad = 0x7C00u;   // +inf: past n
@@ -156,20 +160,24 @@ constexpr int64_t kPackedMaxTop = int64_t(1) << 20;  // lo field
 constexpr int64_t kPackedImageBudget = 224 * 1024;   // one 1024-thread CTA per SM
 struct PackedPlan {
   int64_t n = 0;              // entries
-  int64_t n1 = 0;             // sample entries (nodes)
+  int depth = 1;              // D: levels of nodes; node j of level d covers X[15^(d+1) j + 15^d t]
+  int64_t n1 = 0;             // sample entries T1[j] = X[15^D j] (= nodes of level D-1)
+  int64_t level_off[kPackedMaxDepth] = {};     // first node of level d (levels D-1 .. 0 stored in that order)
+  int64_t level_stride[kPackedMaxDepth] = {};  // 15^d
   int key_mode = 0;
   int sh = 0;                 // residual bits of the sample table
   uint32_t hb = 0, bmax = 0;
   int bins = 0, max_occ = 0, steps = 0;
   double x0 = 0.0, x_last = 0.0;
   std::vector<double> X;      // canonicalised table (device: X then the nodes)
-  std::vector<uint32_t> nodes;  // 8 words per node
+  std::vector<uint32_t> nodes;  // 8 words per node, levels D-1 .. 0
   std::vector<uint8_t> image;   // smem image: u16 residuals | u32 directory
 };
 // EOS_ERR_UNSUPPORTED when no sh <= 16 gives an image within `budget` and bins of
 // <= 63 entries (eos_search_create_levels then uses 8-ary levels under AUTO).
+// depth 0: the smallest D <= kPackedMaxDepth whose sample table fits.
 eos_status plan_packed(const double* X, int64_t n, PackedPlan* out,
-                       int64_t budget = kPackedImageBudget);
+                       int64_t budget = kPackedImageBudget, int depth = 0);
 void fill_info(const PackedPlan& p, eos_table_info_t* info);
 // The sample table of a packed plan as a TablePlan (hash fields, occupancy, T1).
 TablePlan packed_top(const PackedPlan& p);

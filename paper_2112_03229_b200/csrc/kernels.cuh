@@ -467,6 +467,7 @@ struct TieredLookup {
 // that two of them compare as one fp16x2 (HSET2): every stored value is a
 // normal positive half or +inf (0x7C00, past the end), whose bit order is its
 // value order.  eos_internal.h kPackedResMax / kPackedResBias.
+constexpr int kPackedMaxDepthDev = 4;  // eos_internal.h kPackedMaxDepth
 constexpr uint32_t kResMax = 0x77FFu;
 constexpr uint32_t kResBias = 0x0400u;
 __device__ __forceinline__ __half2 u32_as_h2(uint32_t w) {
@@ -480,14 +481,16 @@ __device__ __forceinline__ uint32_t h2_as_u32(__half2 h) {
   return w;
 }
 
-template <int S, int MODE>
+template <int S, int MODE, bool ML>
 struct PackedLookup {
   static constexpr bool kBatchTail = false;
   static constexpr bool kEarlyLoad = true;
   const uint16_t* __restrict__ sR;  // sample residuals (smem)
   const uint32_t* __restrict__ sD;  // directory, one u32 per bin pair (smem)
+  const int32_t* __restrict__ sL;   // level table (smem): first node of level d [0..3], 15^d [4..7]
   AxisParams a;                     // n = n1; hb, bmax of the sample hash; x0, xlast of X
   uint32_t sh;
+  int32_t depth;                    // D levels of nodes; T1[j] = X[15^D j]
   const double* __restrict__ X;       // the table (global)
   const uint32_t* __restrict__ nodes;  // 8 words per node (global, 32-B aligned)
 
@@ -537,7 +540,8 @@ struct PackedLookup {
         // entries lo .. lo + c - 1 are <= rk and the run of residuals == rk ends
         // at c - 1; its entries > y (fp64) form the run's tail
         while (c[i] > 0 && sR[lo[i] + c[i] - 1] == rk[i] &&
-               !(__ldg(X + 15 * (int64_t)(lo[i] + c[i] - 1)) <= y[i]))
+               !(__ldg(X + 15 * (ML ? (int64_t)sL[kPackedMaxDepthDev + depth - 1] : 1) *
+                               (int64_t)(lo[i] + c[i] - 1)) <= y[i]))
           --c[i];
       }
       j[i] = max(lo[i] + c[i] - 1, 0);
@@ -551,11 +555,27 @@ struct PackedLookup {
 #pragma unroll
     for (int i = 0; i < N; ++i) ky[i] = key_hi<MODE>(y[i]);
     sample(y, ky, j);
+    // levels D-1 .. 0 (first node, entry stride 15^d from the image's level table);
+    // ML = false: one level, no loop (the loop costs one-level tables 2%)
+    if constexpr (ML) {
+#pragma unroll 1
+      for (int d = depth - 1; d >= 0; --d) level<N>(d, y, j);
+    } else {
+      EOS_DCHECK(depth == 1);
+      level<N>(0, y, j);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = (y[i] >= a.x0) ? j[i] : 0;
+  }
+  // One level d: j (nodes of level d) -> 15 j + #{entries of the node <= y} (nodes of
+  // level d - 1; at d = 0 the index).
+  template <int N>
+  __device__ __forceinline__ void level(int d, const double (&y)[N], int32_t (&j)[N]) const {
     uint32_t k[N][8];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      EOS_DCHECK(j[i] >= 0 && j[i] < a.n);
-      ldg_keys8(nodes + 8 * (int64_t)j[i], k[i]);
+      EOS_DCHECK(j[i] >= 0 && (d < depth - 1 || j[i] < a.n));
+      ldg_keys8(nodes + 8 * (int64_t)((ML ? sL[d] : 0) + j[i]), k[i]);
     }
     int32_t lt[N], le[N];
 #pragma unroll
@@ -580,11 +600,12 @@ struct PackedLookup {
     for (int i = 0; i < N; ++i) {
       int32_t cnt = lt[i];
       if (le[i] > lt[i]) {  // equal residuals (rare): the fp64 values of the run
-        const double* f = X + 15 * (int64_t)j[i] + 1;
+        const int64_t stride = ML ? sL[kPackedMaxDepthDev + d] : 1;  // 15^d
+        const double* f = X + stride * (15 * (int64_t)j[i] + 1);
 #pragma unroll 1
-        for (int32_t e = lt[i]; e < le[i]; ++e) cnt += __ldg(f + e) <= y[i];
+        for (int32_t e = lt[i]; e < le[i]; ++e) cnt += __ldg(f + stride * e) <= y[i];
       }
-      r[i] = (y[i] >= a.x0) ? 15 * j[i] + cnt : 0;
+      j[i] = 15 * j[i] + cnt;
     }
   }
   __device__ __forceinline__ double x_at(int32_t i) const { return __ldg(X + i); }
@@ -1076,7 +1097,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
 
 // Packed tables (PackedLookup): the smem image holds the sample residuals and
 // their directory; X and the nodes stay in global memory / L2.
-template <int S, int MODE, bool CNT, class SH>
+template <int S, int MODE, bool CNT, class SH, bool ML = true>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
     search1d_packed_kernel(const SearchArgs args) {
   extern __shared__ __align__(128) uint4 smem[];
@@ -1086,14 +1107,18 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks)
   stage_image(smem, args.image, args.image_16, &stage_bar);
   pdl_enter();
   const AxisParams a = args.ax;
-  EOS_DCHECK(args.levels == 1 && args.sh >= 1 && args.sh <= 16 &&
-             a.d_off + 4 * (((int64_t)a.bmax + 2) / 2) <= 16 * (int64_t)args.image_16 &&
-             2 * (int64_t)a.n <= a.d_off && 15 * ((int64_t)a.n - 1) < args.lv_top_len);
-  PackedLookup<S, MODE> lk;
+  EOS_DCHECK(args.levels >= 1 && args.levels <= kPackedMaxDepthDev && args.sh >= 1 && args.sh <= 16 &&
+             a.d_off + 4 * ((((int64_t)a.bmax + 2) / 2 + 3) & ~int64_t(3)) + 32 <=
+                 16 * (int64_t)args.image_16 &&
+             2 * (int64_t)a.n <= a.d_off);
+  PackedLookup<S, MODE, ML> lk;
   lk.sR = reinterpret_cast<const uint16_t*>(reinterpret_cast<const char*>(smem) + a.x_off);
   lk.sD = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(smem) + a.d_off);
+  // the level table follows the directory (16-B padded): eos_internal.h PackedPlan
+  lk.sL = reinterpret_cast<const int32_t*>(lk.sD + ((((int64_t)a.bmax + 2) / 2 + 3) & ~int64_t(3)));
   lk.a = a;
   lk.sh = (uint32_t)args.sh;
+  lk.depth = args.levels;
   lk.X = args.lv;
   lk.nodes = args.kv;
   search_body<CNT, SH>(args, lk, &clc_resp, &clc_bar);

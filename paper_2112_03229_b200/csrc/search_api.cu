@@ -116,21 +116,22 @@ const void* tiered_fn_mode(int steps, bool cnt) {
   }
 }
 
-// packed tables: search1d_packed_kernel, S = 1..kPackedMaxSteps
-template <int MODE, class SH, bool CNT>
+// packed tables: search1d_packed_kernel, S = 1..kPackedMaxSteps; ML = false: the
+// one-level instantiation (no level loop) of the main launch shape
+template <int MODE, class SH, bool CNT, bool ML>
 const void* packed_fn(int steps) {
   switch (steps) {
-    case 1: return (const void*)dv::search1d_packed_kernel<1, MODE, CNT, SH>;
-    case 2: return (const void*)dv::search1d_packed_kernel<2, MODE, CNT, SH>;
-    case 3: return (const void*)dv::search1d_packed_kernel<3, MODE, CNT, SH>;
-    case 4: return (const void*)dv::search1d_packed_kernel<4, MODE, CNT, SH>;
-    case 5: return (const void*)dv::search1d_packed_kernel<5, MODE, CNT, SH>;
-    default: return (const void*)dv::search1d_packed_kernel<6, MODE, CNT, SH>;
+    case 1: return (const void*)dv::search1d_packed_kernel<1, MODE, CNT, SH, ML>;
+    case 2: return (const void*)dv::search1d_packed_kernel<2, MODE, CNT, SH, ML>;
+    case 3: return (const void*)dv::search1d_packed_kernel<3, MODE, CNT, SH, ML>;
+    case 4: return (const void*)dv::search1d_packed_kernel<4, MODE, CNT, SH, ML>;
+    case 5: return (const void*)dv::search1d_packed_kernel<5, MODE, CNT, SH, ML>;
+    default: return (const void*)dv::search1d_packed_kernel<6, MODE, CNT, SH, ML>;
   }
 }
-template <class SH, bool CNT>
+template <class SH, bool CNT, bool ML = true>
 const void* packed_fn_mode(int mode, int steps) {
-  return mode == 0 ? packed_fn<0, SH, CNT>(steps) : packed_fn<1, SH, CNT>(steps);
+  return mode == 0 ? packed_fn<0, SH, CNT, ML>(steps) : packed_fn<1, SH, CNT, ML>(steps);
 }
 static_assert(eos::kPackedMaxSteps == 6, "packed_fn covers S = 1..6");
 
@@ -395,17 +396,26 @@ static eos_status try_packed(const double* table_host, int64_t n, int32_t levels
                              eos::PackedPlan* pp, bool* use) {
   *use = false;
   // AUTO: packed where the 8-ary structure needs two or more levels, i.e. two
-  // or more L2 gathers per lookup (n > 8 kMaxTopKeys); one 8-ary level beats a
-  // packed table's deeper sample bins
-  if (levels != EOS_LEVELS_PACKED &&
-      !(levels == EOS_LEVELS_AUTO && kind == EOS_HASH_AUTO && n > 8 * eos::kMaxTopKeys))
-    return EOS_OK;
-  const eos_status st = eos::plan_packed(table_host, n, pp);
+  // or more L2 gathers per lookup (n > 8 kMaxTopKeys), and the packed depth is
+  // not larger than the 8-ary depth; one 8-ary level beats a packed table's
+  // deeper sample bins
+  const bool explicit_depth =
+      levels <= EOS_LEVELS_PACKED_DEPTH(1) && levels >= EOS_LEVELS_PACKED_DEPTH(eos::kPackedMaxDepth);
+  const bool auto_packed = levels == EOS_LEVELS_AUTO && kind == EOS_HASH_AUTO && n > 8 * eos::kMaxTopKeys;
+  if (levels != EOS_LEVELS_PACKED && !explicit_depth && !auto_packed) return EOS_OK;
+  if (auto_packed && n > EOS_MAX_TABLE_TIERED) return EOS_OK;  // (plan_tiered reports it)
+  const int depth = explicit_depth ? EOS_LEVELS_PACKED_DEPTH(0) - levels : 0;
+  const eos_status st = eos::plan_packed(table_host, n, pp, eos::kPackedImageBudget, depth);
   if (st == EOS_OK) {
+    if (auto_packed) {
+      int d8 = 1;  // depth of the 8-ary structure: n1 = ceil(n / 8^D) <= kMaxTopKeys
+      for (int64_t s = 8; (n + s - 1) / s > eos::kMaxTopKeys; s *= 8) ++d8;
+      if (pp->depth > d8) return EOS_OK;
+    }
     *use = true;
     return EOS_OK;
   }
-  if (levels == EOS_LEVELS_AUTO && (st == EOS_ERR_UNSUPPORTED || st == EOS_ERR_SIZE)) return EOS_OK;
+  if (auto_packed && (st == EOS_ERR_UNSUPPORTED || st == EOS_ERR_SIZE)) return EOS_OK;
   return st;
 }
 
@@ -441,14 +451,14 @@ static eos_status create_packed(eos::PackedPlan&& pp, eos_table* out) {
     return st;
   };
   t->plan = eos::packed_top(pp);
-  t->levels = 1;
+  t->levels = pp.depth;
   t->node_width = eos::kPackedNode;
   t->sh = pp.sh;
   t->n = pp.n;
   t->top_n = pp.n1;
   t->smem_bytes = (int64_t)pp.image.size();
   const int64_t x_bytes = (8 * pp.n + 31) & ~int64_t(31);
-  t->level_bytes = x_bytes + 32 * pp.n1;
+  t->level_bytes = x_bytes + 4 * (int64_t)pp.nodes.size();
   dv::AxisParams& a = t->ax;
   a.n = (int32_t)pp.n1;
   a.x_off = 0;
@@ -472,7 +482,8 @@ static eos_status create_packed(eos::PackedPlan&& pp, eos_table* out) {
     e = cudaMemcpy((void*)t->nodes_dev, pp.nodes.data(), 4 * pp.nodes.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return fail(cuda_status(e));
   const int mode = pp.key_mode, S = pp.steps;
-  t->fn[0] = packed_fn_mode<dv::ShapeTiered, false>(mode, S);
+  t->fn[0] = pp.depth == 1 ? packed_fn_mode<dv::ShapeTiered, false, false>(mode, S)
+                           : packed_fn_mode<dv::ShapeTiered, false>(mode, S);
   t->threads[0] = dv::ShapeTiered::kThreads;
   t->unroll[0] = dv::ShapeTiered::kUnroll;
   t->clc[0] = dv::ShapeTiered::kClc;

@@ -500,34 +500,24 @@ eos_status plan_tiered(const double* Xin, int64_t n, int levels, int kind, int64
   return EOS_OK;
 }
 
-eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t budget) {
-  if (!Xin || !out) return EOS_ERR_NULL;
-  if (n < 1 || n > EOS_MAX_TABLE_TIERED) return EOS_ERR_SIZE;
-  const int64_t n1 = (n + kPackedNode - 1) / kPackedNode;
+// One depth of a packed plan: the sample table over X[15^D j] and its hash, the
+// nodes of levels D-1 .. 0 (X must be validated).  EOS_ERR_UNSUPPORTED when the
+// sample image does not fit `budget` at any residual width.
+static eos_status plan_packed_depth(PackedPlan& p, int D, int64_t budget) {
+  const int64_t n = p.n;
+  int64_t stride = 1;  // 15^D
+  for (int d = 0; d < D; ++d) stride *= kPackedNode;
+  const int64_t n1 = (n + stride - 1) / stride;
   if (n1 > kPackedMaxTop) return EOS_ERR_SIZE;
-  if (pad16(2 * n1) + 16 > budget) return EOS_ERR_UNSUPPORTED;  // before touching X
-  PackedPlan p;
-  p.n = n;
+  if (pad16(2 * n1) + 16 > budget) return EOS_ERR_UNSUPPORTED;
+  p.depth = D;
   p.n1 = n1;
-  try {
-    p.X.resize((size_t)n);
-  } catch (...) {
-    return EOS_ERR_NOMEM;
-  }
-  for (int64_t j = 0; j < n; ++j) {  // same rules as plan_table
-    const double v = Xin[j];
-    if (!isfinite(v)) return EOS_ERR_NONFINITE;
-    p.X[j] = (v == 0.0) ? 0.0 : v;  // canonicalise -0.0 (DESIGN.md R6)
-    if (j > 0 && p.X[j] < p.X[j - 1]) return EOS_ERR_UNSORTED;
-  }
-  const int mode = (p.X[0] >= 0.0) ? 0 : 1;
-  p.key_mode = mode;
-  p.x0 = p.X[0];
-  p.x_last = p.X[n - 1];
+  p.sh = 0;
+  const int mode = p.key_mode;
   std::vector<uint32_t> K1((size_t)n1);
   std::vector<double> T1((size_t)n1);
   for (int64_t j = 0; j < n1; ++j) {
-    T1[j] = p.X[j * kPackedNode];
+    T1[j] = p.X[j * stride];
     K1[j] = key_hi(T1[j], mode);
   }
   const uint32_t lowk = low_key(T1, mode), top = K1[n1 - 1];
@@ -558,9 +548,17 @@ eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t bu
   }
   if (p.sh == 0) return EOS_ERR_UNSUPPORTED;
   const int sh = p.sh;
-  try {
-    p.image.assign((size_t)(rbytes + pad16(4 * (((int64_t)p.bins + 1) / 2))), 0);
-    p.nodes.assign((size_t)(8 * n1), 0);
+  // nodes of levels D-1 .. 0, coarsest first: level d has ceil(n / 15^(d+1)) nodes
+  int64_t total = 0;
+  for (int d = 0; d < D; ++d) {
+    int64_t sd = kPackedNode;  // 15^(d+1)
+    for (int e = 0; e < d; ++e) sd *= kPackedNode;
+    total += (n + sd - 1) / sd;
+  }
+  const int64_t dbytes = pad16(4 * (((int64_t)p.bins + 1) / 2));
+  try {  // residuals | directory | level table (int32 first node [4], 15^d [4])
+    p.image.assign((size_t)(rbytes + dbytes + 32), 0);
+    p.nodes.assign((size_t)(8 * total), 0);
   } catch (...) {
     return EOS_ERR_NOMEM;
   }
@@ -585,24 +583,76 @@ eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t bu
     const uint32_t d = lo[2 * g] | (occ[2 * g] << 20) | (o1 << 26);
     memcpy(p.image.data() + rbytes + 4 * g, &d, 4);
   }
-  // nodes
-  for (int64_t j = 0; j < n1; ++j) {
-    const int64_t i0 = j * kPackedNode;
-    const int64_t last = std::min<int64_t>(i0 + kPackedNode - 1, n - 1);
-    const uint32_t Bm = key_hi(p.X[i0], mode) & ~63u;
-    const uint64_t base = (uint64_t)Bm << 32;
-    const uint64_t span = key64(p.X[last], mode) - base;
-    uint32_t s = 0;
-    while ((span >> s) > kPackedResMax) ++s;
-    uint32_t* w = p.nodes.data() + 8 * j;
-    w[0] = Bm | s;
-    for (int t = 1; t < kPackedNode; ++t) {
-      const int64_t i = i0 + t;
-      const uint32_t r =
-          i < n ? (uint32_t)((key64(p.X[i], mode) - base) >> s) + kPackedResBias : kPackedResPad;
-      w[(t + 1) / 2] |= (t & 1) ? r : (r << 16);
+  // nodes: node j of level d covers X[15^(d+1) j + 15^d t], t = 0..14
+  int64_t off = 0;
+  for (int d = D - 1; d >= 0; --d) {
+    int64_t sd = 1;  // 15^d
+    for (int e = 0; e < d; ++e) sd *= kPackedNode;
+    const int64_t m = (n + kPackedNode * sd - 1) / (kPackedNode * sd);
+    p.level_off[d] = off;
+    p.level_stride[d] = sd;
+    for (int64_t j = 0; j < m; ++j) {
+      const int64_t i0 = kPackedNode * sd * j;
+      const int64_t last = std::min<int64_t>(i0 + (kPackedNode - 1) * sd, (n - 1 - i0) / sd * sd + i0);
+      const uint32_t Bm = key_hi(p.X[i0], mode) & ~63u;
+      const uint64_t base = (uint64_t)Bm << 32;
+      const uint64_t span = key64(p.X[last], mode) - base;
+      uint32_t s = 0;
+      while ((span >> s) > kPackedResMax) ++s;
+      uint32_t* w = p.nodes.data() + 8 * (off + j);
+      w[0] = Bm | s;
+      for (int t = 1; t < kPackedNode; ++t) {
+        const int64_t i = i0 + t * sd;
+        const uint32_t r =
+            i < n ? (uint32_t)((key64(p.X[i], mode) - base) >> s) + kPackedResBias : kPackedResPad;
+        w[(t + 1) / 2] |= (t & 1) ? r : (r << 16);
+      }
     }
+    off += m;
   }
+  int32_t lt[2 * kPackedMaxDepth] = {};
+  for (int d = 0; d < D; ++d) {
+    lt[d] = (int32_t)p.level_off[d];
+    lt[kPackedMaxDepth + d] = (int32_t)p.level_stride[d];
+  }
+  memcpy(p.image.data() + rbytes + dbytes, lt, sizeof(lt));
+  return EOS_OK;
+}
+
+eos_status plan_packed(const double* Xin, int64_t n, PackedPlan* out, int64_t budget, int depth) {
+  if (!Xin || !out) return EOS_ERR_NULL;
+  if (n < 1 || n > EOS_MAX_TABLE_TIERED) return EOS_ERR_SIZE;
+  if (depth < 0 || depth > kPackedMaxDepth) return EOS_ERR_UNSUPPORTED;
+  {  // fail early (before touching X) when no allowed depth can fit
+    const int dmax = depth ? depth : kPackedMaxDepth;
+    int64_t stride = 1;
+    for (int d = 0; d < dmax; ++d) stride *= kPackedNode;
+    if (pad16(2 * ((n + stride - 1) / stride)) + 16 > budget) return EOS_ERR_UNSUPPORTED;
+  }
+  PackedPlan p;
+  p.n = n;
+  try {
+    p.X.resize((size_t)n);
+  } catch (...) {
+    return EOS_ERR_NOMEM;
+  }
+  for (int64_t j = 0; j < n; ++j) {  // same rules as plan_table
+    const double v = Xin[j];
+    if (!isfinite(v)) return EOS_ERR_NONFINITE;
+    p.X[j] = (v == 0.0) ? 0.0 : v;  // canonicalise -0.0 (DESIGN.md R6)
+    if (j > 0 && p.X[j] < p.X[j - 1]) return EOS_ERR_UNSORTED;
+  }
+  p.key_mode = (p.X[0] >= 0.0) ? 0 : 1;
+  p.x0 = p.X[0];
+  p.x_last = p.X[n - 1];
+  // the given depth, or the smallest that fits (each level is one more L2 gather)
+  eos_status st = EOS_ERR_UNSUPPORTED;
+  for (int D = depth ? depth : 1; D <= (depth ? depth : kPackedMaxDepth); ++D) {
+    st = plan_packed_depth(p, D, budget);
+    if (st == EOS_OK) break;
+    if (st != EOS_ERR_UNSUPPORTED && st != EOS_ERR_SIZE) return st;
+  }
+  if (st != EOS_OK) return st;
   *out = std::move(p);
   return EOS_OK;
 }
@@ -629,10 +679,10 @@ TablePlan packed_top(const PackedPlan& p) {
 void fill_info(const PackedPlan& p, eos_table_info_t* info) {
   fill_info(packed_top(p), info);
   info->n = p.n;
-  info->levels = 1;
+  info->levels = p.depth;
   info->node_width = kPackedNode;
   info->top_n = p.n1;
-  info->level_bytes = ((8 * p.n + 31) & ~int64_t(31)) + 32 * p.n1;  // X, then the nodes
+  info->level_bytes = ((8 * p.n + 31) & ~int64_t(31)) + 4 * (int64_t)p.nodes.size();  // X, then the nodes
 }
 
 int64_t key_image_bytes(const TablePlan& p) { return pad16(4 * p.n) + pad16(4 * p.bins); }

@@ -72,8 +72,9 @@ def fuzz_1d(rng, dev, stats):
         kw["log_bins"] = int(np.exp(rng.uniform(0, np.log(40000))))
     elif plan == 3:
         kw["levels"] = int(rng.integers(1, 6))
-    elif plan == 4:
-        kw["levels"] = eos.EOS_LEVELS_PACKED
+    elif plan == 4:  # packed nodes: the fewest levels, or 1..4 levels
+        d = int(rng.integers(0, 5))
+        kw["levels"] = eos.EOS_LEVELS_PACKED if d == 0 else eos.EOS_LEVELS_PACKED_DEPTH(d)
     try:
         t = eos.Table(X, **kw)
     except eos.EosError as e:

@@ -992,36 +992,41 @@ def test_tiered_host_pipeline_and_counters():
 
 
 # ------------------------------ packed tables (EOS_LEVELS_PACKED, §6.5) -----
-# One level of 15-entry nodes of 16-bit residual keys (one 32-B sector) under a
-# sample table of 16-bit residuals: the same P:54 lower bound, settled exactly
+# D levels of 15-entry nodes of 16-bit residual keys (one 32-B sector each) under
+# a sample table of 16-bit residuals: the same P:54 lower bound, settled exactly
 # from the fp64 values wherever residuals tie.
 PACKED = eos.EOS_LEVELS_PACKED
 
 
-def _packed(X):
-    t = eos.Table(X, levels=PACKED)
-    assert t.info.levels == 1 and t.info.node_width == 15
-    assert t.info.top_n == (X.size + 14) // 15
+def _packed(X, depth=1):
+    """depth: exactly that many levels (EOS_LEVELS_PACKED_DEPTH), or None: the fewest
+    that fit (EOS_LEVELS_PACKED)."""
+    t = eos.Table(X, levels=PACKED if depth is None else eos.EOS_LEVELS_PACKED_DEPTH(depth))
+    D = t.info.levels
+    assert t.info.node_width == 15 and (depth is None or D == depth)
+    assert t.info.top_n == -(-X.size // 15 ** D)
     return t
 
 
+@pytest.mark.parametrize("depth", [1, 2, 3])
 @pytest.mark.parametrize("name", sorted(lower_bound_cases().keys()))
-def test_packed_golden(name):
+def test_packed_golden(name, depth):
     X, cases = lower_bound_cases()[name]
     ys = np.array([c[0] for c in cases] * 37)
     exp = np.array([c[1] for c in cases] * 37, dtype=np.int32)
-    t = _packed(X)
+    t = _packed(X, depth)
     assert_same(t.search(to_dev(ys)).cpu().numpy(), exp, ys)
     t.close()
 
 
-def test_packed_edge_tables_exhaustive_probes():
-    rng = np.random.default_rng(78)
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_packed_edge_tables_exhaustive_probes(depth):
+    rng = np.random.default_rng(78 + depth)
     checked = 0
     for X in _edge_tables(rng, 140):
         P = _probes(X)
         P = np.concatenate([P, rng.permutation(np.repeat(P, 3))])
-        t = _packed(X)
+        t = _packed(X, depth)
         assert_same(t.search(to_dev(P)).cpu().numpy(), oracle.search(X, P), P)
         t.close()
         checked += P.size
@@ -1038,21 +1043,24 @@ def _clustered(rng, n):
     return np.sort(X)
 
 
-@pytest.mark.parametrize("n,kind", [((1 << 20), "loguniform"), (300_001, "zerohead"),
-                                    (500_003, "dups"), (1_500_001, "loguniform"),
-                                    (333_337, "clustered"), (16_385, "loguniform"),
-                                    (400_001, "mixed")])
-def test_packed_large_tables_full(n, kind):
+@pytest.mark.parametrize("n,kind,depth", [((1 << 20), "loguniform", 1), (300_001, "zerohead", 1),
+                                          (500_003, "dups", 1), (1_500_001, "loguniform", 1),
+                                          (333_337, "clustered", 1), (16_385, "loguniform", 1),
+                                          (400_001, "mixed", 1), ((1 << 20), "loguniform", 2),
+                                          (4_000_037, "loguniform", None), (500_003, "dups", 3),
+                                          (333_337, "clustered", 2), (300_001, "zerohead", 4),
+                                          (400_001, "dense", None)])
+def test_packed_large_tables_full(n, kind, depth):
     rng = np.random.default_rng(n + 1)
     X = _clustered(rng, n) if kind == "clustered" else _big_table(rng, n, kind)
     Y = _big_probes(rng, X, 1 << 20)
     ref = oracle.search(X, Y)
     try:
-        t = _packed(X)
-    except eos.EosError as e:  # the sample table does not fit: AUTO takes 8-ary levels
+        t = _packed(X, depth)
+    except eos.EosError as e:  # the sample table does not fit at this depth: AUTO's choice
         assert "UNSUPPORTED" in str(e) and kind in ("mixed", "zerohead"), e
         t = eos.Table(X)
-        assert t.info.node_width == 8
+        assert t.info.node_width == 8 or t.info.levels > depth
     out = t.search(to_dev(Y))
     torch.cuda.synchronize()
     assert_same(out.cpu().numpy(), ref, Y)
@@ -1065,15 +1073,15 @@ def test_packed_large_tables_full(n, kind):
 
 
 @pytest.mark.parametrize("count", [1, 3, 2049, 65_537, 300_001])
-@pytest.mark.parametrize("y_off,o_off", [(0, 0), (1, 1), (3, 2)])
-def test_packed_ragged_misaligned_and_small_launches(count, y_off, o_off):
+@pytest.mark.parametrize("y_off,o_off,depth", [(0, 0, 1), (1, 1, 1), (3, 2, 1), (1, 1, 2)])
+def test_packed_ragged_misaligned_and_small_launches(count, y_off, o_off, depth):
     rng = np.random.default_rng(count + 3)
     X = _big_table(rng, 400_000, "loguniform")
     Yall = _big_probes(rng, X, count + 64)[: count + 8]
     yd = to_dev(Yall)[y_off:y_off + count]
     od_all = torch.full((count + 8,), -7, dtype=torch.int32, device=DEV)
     od = od_all[o_off:o_off + count]
-    t = _packed(X)
+    t = _packed(X, depth)
     t.search(yd, out=od)
     torch.cuda.synchronize()
     got = od_all.cpu().numpy()

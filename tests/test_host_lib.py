@@ -324,12 +324,12 @@ def test_tiered_plan_levels_and_sizes():
     X[::8^D] as 32-bit keys plus its directory."""
     rng = np.random.default_rng(7)
     pad16 = lambda b: (b + 15) // 16 * 16  # noqa: E731
-    for n, D in [(1, 0), (16384, 0), (16385, 1), (262144, 1), (262145, -2), (1 << 20, -2),
-                 (1 << 21, 2), ((1 << 21) + 1, 3)]:
+    for n, D in [(1, 0), (16384, 0), (16385, 1), (262144, 1), (262145, -1), (1 << 20, -1),
+                 (1 << 21, -2), ((1 << 21) + 1, -2)]:
         X = np.sort(10.0 ** rng.uniform(-6, 10, n))
         info = eos.plan_table_levels(X)
-        if D == -2:  # 8-ary levels would need D = 2: the packed structure (its own test)
-            assert info.levels == 1 and info.node_width == 15, n
+        if D < 0:  # 8-ary levels would need D >= 2: packed nodes, -D levels (their own test)
+            assert info.levels == -D and info.node_width == 15, n
             continue
         assert info.levels == D and info.n == n, (n, info.levels)
         assert info.node_width == (8 if D else 0)
@@ -358,26 +358,33 @@ def _keys_mode0(v):
     return (np.ascontiguousarray(v).view(np.uint64) >> np.uint64(32)).astype(np.int64) & 0x7FFFFFFF
 
 
-@pytest.mark.parametrize("n", [300_001, 1 << 20, 1_500_000, 16_385, 1000])
-def test_packed_plan_fields_and_sample_hash(n):
-    """eos_plan_table_levels(EOS_LEVELS_PACKED) (eos_internal.h PackedPlan): n1 =
-    ceil(n/15) nodes of 32 B after the 32-B padded fp64 table; the sample table
-    X[::15] as u16 residuals plus one u32 directory entry per bin pair within 224 KB; the
-    bins are the key's bits above sh = 20 - k (hb aligned), recounted here, and S is the
-    fewest lifting steps over every residual width that fits (bins of <= 63 entries)."""
+@pytest.mark.parametrize("n,depth", [(300_001, 1), (1 << 20, 1), (1_500_000, 1), (16_385, 1),
+                                     (1000, 1), (4_000_000, 2), (1000, 2), (300_001, 3),
+                                     (40_000, 4)])
+def test_packed_plan_fields_and_sample_hash(n, depth):
+    """eos_plan_table_levels(EOS_LEVELS_PACKED[_DEPTH(D)]) (eos_internal.h PackedPlan):
+    levels d = D-1..0 of ceil(n/15^(d+1)) nodes of 32 B after the 32-B padded fp64 table;
+    the sample table X[::15^D] as u16 residuals, one u32 directory entry per bin pair and
+    the 32-B level table within 224 KB; the bins are the key's bits above sh = 20 - k (hb
+    aligned), recounted here, and S is the fewest lifting steps over every residual width
+    that fits (bins of <= 63 entries).  EOS_LEVELS_PACKED takes the fewest levels."""
     rng = np.random.default_rng(n)
     X = np.sort(10.0 ** rng.uniform(-6, 10, n))
-    info = eos.plan_table_levels(X, levels=eos.EOS_LEVELS_PACKED)
+    info = eos.plan_table_levels(X, levels=eos.EOS_LEVELS_PACKED_DEPTH(depth))
+    if n in (4_000_000, 1_500_000, 1 << 20):  # the fewest levels that fit
+        auto = eos.plan_table_levels(X, levels=eos.EOS_LEVELS_PACKED)
+        assert auto.levels == depth and auto.as_dict() == info.as_dict()
     pad16 = lambda b: (b + 15) // 16 * 16  # noqa: E731
-    n1 = -(-n // 15)
-    assert (info.levels, info.node_width, info.top_n, info.n) == (1, 15, n1, n)
-    assert info.level_bytes == (8 * n + 31) // 32 * 32 + 32 * n1
+    n1 = -(-n // 15 ** depth)
+    assert (info.levels, info.node_width, info.top_n, info.n) == (depth, 15, n1, n)
+    nodes = sum(-(-n // 15 ** (d + 1)) for d in range(depth))
+    assert info.level_bytes == (8 * n + 31) // 32 * 32 + 32 * nodes
     assert info.hash_kind == eos.EOS_HASH_EXPONENT and 4 <= info.k <= 19
     assert info.dir_entry_bytes == 2
     budget = 224 * 1024
-    assert info.image_bytes == pad16(2 * n1) + pad16(4 * ((info.bins + 1) // 2)) <= budget
+    assert info.image_bytes == pad16(2 * n1) + pad16(4 * ((info.bins + 1) // 2)) + 32 <= budget
 
-    K = _keys_mode0(X[::15])
+    K = _keys_mode0(X[::15 ** depth])
 
     def plan(sh):
         hb = int(K[0]) & ~((1 << sh) - 1)
@@ -390,7 +397,7 @@ def test_packed_plan_fields_and_sample_hash(n):
     assert info.steps == int(np.ceil(np.log2(mo + 1))) <= 6
     for other in range(1, 17):
         _, b2, m2 = plan(other)
-        if pad16(2 * n1) + pad16(4 * ((b2 + 1) // 2)) <= budget and m2 <= 63:
+        if pad16(2 * n1) + pad16(4 * ((b2 + 1) // 2)) + 32 <= budget and m2 <= 63:
             assert int(np.ceil(np.log2(m2 + 1))) >= info.steps, other
 
 
@@ -405,8 +412,14 @@ def test_packed_plan_auto_choice_and_errors():
                       (np.sort(10.0 ** rng.uniform(-6, 10, 4_000_000)), "EOS_ERR_UNSUPPORTED"),
                       (np.empty(0), "EOS_ERR_SIZE")]:
         with pytest.raises(eos.EosError) as e:
-            eos.plan_table_levels(bad, levels=eos.EOS_LEVELS_PACKED)
+            eos.plan_table_levels(bad, levels=eos.EOS_LEVELS_PACKED_DEPTH(1))
         assert e.value.name == code
+    # more levels fit: one bin of 89 entries at D = 3, of 6 at D = 4
+    assert eos.plan_table_levels(np.full(300_000, 2.5), levels=eos.EOS_LEVELS_PACKED).levels == 4
+    for lv in (eos.EOS_LEVELS_PACKED_DEPTH(0), eos.EOS_LEVELS_PACKED_DEPTH(5), -3):
+        with pytest.raises(eos.EosError) as e:
+            eos.plan_table_levels(X, levels=lv)
+        assert e.value.name == "EOS_ERR_UNSUPPORTED"
     # AUTO falls back to 8-ary levels when packed does not fit
     assert eos.plan_table_levels(np.full(300_000, 2.5)).node_width == 8
     bad = X.copy()
