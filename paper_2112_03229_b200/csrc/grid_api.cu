@@ -109,9 +109,16 @@ struct InterpKernel {
 
 template <int S, bool LOGLOG, int REP, bool GG>
 InterpKernel interp_fn(bool deriv) {
-  if (deriv)
+  if (deriv) {
+    if constexpr (LOGLOG && !GG && REP == 2 && (S == 1 || S == dv::kMapped))
+      return {(const void*)dv::interp2d_kernel<S, dv::Shape2DDerivFull, true, LOGLOG, REP, GG>,
+              dv::Shape2DDerivFull::kThreads};
+    if constexpr (GG && REP == 2 && (S == 1 || S == dv::kMapped))
+      return {(const void*)dv::interp2d_kernel<S, dv::Shape2DDerivWide, true, LOGLOG, REP, GG>,
+              dv::Shape2DDerivWide::kThreads};
     return {(const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, true, LOGLOG, REP, GG>,
             dv::Shape2DDeriv::kThreads};
+  }
   if constexpr ((S == 1 || S == dv::kMapped) && !(LOGLOG && REP == 0))  // (plain log-log axes: 2 log1p per axis)
     return {(const void*)dv::interp2d_kernel<S, dv::Shape2D, false, LOGLOG, REP, GG>,
             dv::Shape2D::kThreads};

@@ -1596,6 +1596,11 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
 // costs more than the static tail (profiles/r01_exp_interp.json).
 using Shape2D = Shape<1024, 1, 1, false>;
 using Shape2DDeriv = Shape<512, 1, 1, false>;  // derivative outputs need > 64 registers
+// derivative kernels of log-log or device-memory grids with one-step (or mapped) axes
+// and bank-pinned records: latency-bound at 16 warps per SM; they fit 768 threads (80
+// registers) or, log-log grids in shared memory, 1024 (64) without spills
+using Shape2DDerivWide = Shape<768, 1, 1, false>;
+using Shape2DDerivFull = Shape<1024, 1, 1, false>;
 // launches with fewer tiles than half the SMs: quarter-size tiles, the grid read from cell
 // quads in device memory (grid_api.cu pick_interp_small)
 using Shape2DSmallGG = Shape<256, 1, 1, false>;
