@@ -107,11 +107,11 @@ struct InterpKernel {
   int threads;
 };
 
-template <int S, bool LOGLOG, int REP, bool GG>
+template <int S, bool LOGLOG, int REP, bool GG, int NK = 0>
 InterpKernel interp_fn(bool deriv) {
   if (deriv) {
     if constexpr (LOGLOG && !GG && REP == 2 && (S == 1 || S == dv::kMapped))
-      return {(const void*)dv::interp2d_kernel<S, dv::Shape2DDerivFull, true, LOGLOG, REP, GG>,
+      return {(const void*)dv::interp2d_kernel<S, dv::Shape2DDerivFull, true, LOGLOG, REP, GG, NK>,
               dv::Shape2DDerivFull::kThreads};
     if constexpr (GG && REP == 2 && (S == 1 || S == dv::kMapped))
       return {(const void*)dv::interp2d_kernel<S, dv::Shape2DDerivWide, true, LOGLOG, REP, GG>,
@@ -120,7 +120,7 @@ InterpKernel interp_fn(bool deriv) {
             dv::Shape2DDeriv::kThreads};
   }
   if constexpr ((S == 1 || S == dv::kMapped) && !(LOGLOG && REP == 0))  // (plain log-log axes: 2 log1p per axis)
-    return {(const void*)dv::interp2d_kernel<S, dv::Shape2D, false, LOGLOG, REP, GG>,
+    return {(const void*)dv::interp2d_kernel<S, dv::Shape2D, false, LOGLOG, REP, GG, NK>,
             dv::Shape2D::kThreads};
   else
     return {(const void*)dv::interp2d_kernel<S, Shape2DDeep, false, LOGLOG, REP, GG>,
@@ -128,7 +128,16 @@ InterpKernel interp_fn(bool deriv) {
 }
 
 template <bool LOGLOG, int REP, bool GG>
-InterpKernel interp_fn_steps(int steps, bool deriv) {
+InterpKernel interp_fn_steps(int steps, bool deriv, int narrow) {
+  if constexpr (LOGLOG && REP == 2 && !GG) {  // the series length fixed at compile time
+    if (narrow && (steps == dv::kMapped || steps == 1)) {
+      if (steps == dv::kMapped)
+        return narrow == 2 ? interp_fn<dv::kMapped, LOGLOG, REP, GG, 8>(deriv)
+                           : interp_fn<dv::kMapped, LOGLOG, REP, GG, 12>(deriv);
+      return narrow == 2 ? interp_fn<1, LOGLOG, REP, GG, 8>(deriv)
+                         : interp_fn<1, LOGLOG, REP, GG, 12>(deriv);
+    }
+  }
   if constexpr (REP == 2) {
     if (steps == dv::kMapped) return interp_fn<dv::kMapped, LOGLOG, REP, GG>(deriv);
   }
@@ -145,17 +154,17 @@ InterpKernel interp_fn_steps(int steps, bool deriv) {
   }
 }
 
-InterpKernel pick_interp(int steps, bool loglog, int rep, bool gg, bool deriv) {
+InterpKernel pick_interp(int steps, bool loglog, int rep, bool gg, bool deriv, int narrow) {
   if (gg) {
-    if (loglog) return rep == 2 ? interp_fn_steps<true, 2, true>(steps, deriv)
-                                : interp_fn_steps<true, 0, true>(steps, deriv);
-    return rep == 2 ? interp_fn_steps<false, 2, true>(steps, deriv)
-                    : interp_fn_steps<false, 0, true>(steps, deriv);
+    if (loglog) return rep == 2 ? interp_fn_steps<true, 2, true>(steps, deriv, narrow)
+                                : interp_fn_steps<true, 0, true>(steps, deriv, narrow);
+    return rep == 2 ? interp_fn_steps<false, 2, true>(steps, deriv, narrow)
+                    : interp_fn_steps<false, 0, true>(steps, deriv, narrow);
   }
-  if (loglog) return rep == 2 ? interp_fn_steps<true, 2, false>(steps, deriv)
-                              : interp_fn_steps<true, 0, false>(steps, deriv);
-  return rep == 2 ? interp_fn_steps<false, 2, false>(steps, deriv)
-                  : interp_fn_steps<false, 0, false>(steps, deriv);
+  if (loglog) return rep == 2 ? interp_fn_steps<true, 2, false>(steps, deriv, narrow)
+                              : interp_fn_steps<true, 0, false>(steps, deriv, narrow);
+  return rep == 2 ? interp_fn_steps<false, 2, false>(steps, deriv, narrow)
+                  : interp_fn_steps<false, 0, false>(steps, deriv, narrow);
 }
 
 // The small-launch kernel: the default layouts (bank-pinned records, S = 1) only.
@@ -438,8 +447,8 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
       e = cudaMemcpy(g->grid_dev, q2.data(), (size_t)g->grid_bytes, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return fail(cuda_status(e));
   }
-  const InterpKernel k0 = pick_interp(steps_max, loglog, g->rep, g->gg, false);
-  const InterpKernel k1 = pick_interp(steps_max, loglog, g->rep, g->gg, true);
+  const InterpKernel k0 = pick_interp(steps_max, loglog, g->rep, g->gg, false, g->narrow);
+  const InterpKernel k1 = pick_interp(steps_max, loglog, g->rep, g->gg, true, g->narrow);
   g->fn = k0.fn;
   g->threads = k0.threads;
   g->fn_deriv = k1.fn;

@@ -1490,7 +1490,10 @@ __device__ __forceinline__ void axis_cell_rec(double y, const double* __restrict
 // (L2-resident up to a few 10^6 cells) as cell quads, so the 4 corners are one
 // aligned 32-byte load (one L1/L2 sector).  The axes, their directories and
 // records stay in smem.
-template <int S, bool DERIV, bool LOGLOG, int REP, bool GG>
+// NK (log-log grids with bank-pinned records): 8 or 12 = the series length of every
+// cell fixed at compile time (no launch-uniform branch, so a thread's two pairs
+// interleave); 0 = chosen per launch from Interp2DArgs::narrow.
+template <int S, bool DERIV, bool LOGLOG, int REP, bool GG, int NK = 0>
 __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, int32_t& j,
                                              double& dpr, double& dpt, const char* sm,
                                              const Interp2DArgs& A) {
@@ -1518,7 +1521,10 @@ __device__ __forceinline__ double interp_one(double rho, double T, int32_t& i, i
                        reinterpret_cast<const double2*>(sm + A.rr_off) + c, sh);
       axis_cell_rec<S>(T, sT, dT, A.t, j, cj, t0, it,
                        reinterpret_cast<const double2*>(sm + A.rt_off) + c, sh);
-      if (A.narrow == 2) {  // every cell ratio <= 1.25: 8 terms (launch-uniform branch)
+      if constexpr (NK > 0) {
+        tx = clamp01(__dmul_rn(ln_ratio_cell<NK>(rho, r0), ir));
+        ty = clamp01(__dmul_rn(ln_ratio_cell<NK>(T, t0), it));
+      } else if (A.narrow == 2) {  // every cell ratio <= 1.25: 8 terms (launch-uniform branch)
         tx = clamp01(__dmul_rn(ln_ratio_cell<8>(rho, r0), ir));
         ty = clamp01(__dmul_rn(ln_ratio_cell<8>(T, t0), it));
       } else if (A.narrow) {  // every cell ratio <= 1.5: 12 terms
@@ -1605,7 +1611,7 @@ using Shape2DDerivFull = Shape<1024, 1, 1, false>;
 // quads in device memory (grid_api.cu pick_interp_small)
 using Shape2DSmallGG = Shape<256, 1, 1, false>;
 
-template <int S, class SH, bool DERIV, bool LOGLOG = false, int REP = 0, bool GG = false>
+template <int S, class SH, bool DERIV, bool LOGLOG = false, int REP = 0, bool GG = false, int NK = 0>
 __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(const Interp2DArgs A) {
   static_assert(S != kMapped || REP == 2, "fitted cell maps read the bank-pinned records");
   constexpr int T = SH::kThreads;
@@ -1665,9 +1671,9 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
       int2 ir[U], it[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        p[u].x = interp_one<S, DERIV, LOGLOG, REP, GG>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
+        p[u].x = interp_one<S, DERIV, LOGLOG, REP, GG, NK>(vr[u].x, vt[u].x, ir[u].x, it[u].x, dr[u].x, dt[u].x,
                                              sm, A);
-        p[u].y = interp_one<S, DERIV, LOGLOG, REP, GG>(vr[u].y, vt[u].y, ir[u].y, it[u].y, dr[u].y, dt[u].y,
+        p[u].y = interp_one<S, DERIV, LOGLOG, REP, GG, NK>(vr[u].y, vt[u].y, ir[u].y, it[u].y, dr[u].y, dt[u].y,
                                              sm, A);
       }
       tn = next_tile(t);
@@ -1722,7 +1728,7 @@ __global__ void __launch_bounds__(SH::kThreads, SH::kMinBlocks) interp2d_kernel(
           if (q < e1) {
             int32_t i, j;
             double dpr, dpt;
-            const double pq = interp_one<S, DERIV, LOGLOG, REP, GG>(vr1[k], vt1[k], i, j,
+            const double pq = interp_one<S, DERIV, LOGLOG, REP, GG, NK>(vr1[k], vt1[k], i, j,
                                                                           dpr, dpt, sm, A);
             A.P[q] = pq;
             if (br) A.iR[q] = i;
