@@ -365,6 +365,16 @@ def run_ours(a, d: Dist):
         "e2e": e2e,
         "trials": trials,
     }
+    if is2d and not a.global_grid and not a.derivatives and 8 * len(w.rho) * len(w.T) <= 200 * 1024:
+        # shared-memory grids: L1TEX data-pipe bound; the same mix of
+        # shared-memory reads and stream as a trivial kernel, measured now
+        im = measure.interp_mix_ceiling(rho, T, P, iR, iT, len(w.rho), len(w.T))
+        res["roofline"]["l1"] = {
+            "bound": "l1tex data pipe (shared-memory gathers + stream)",
+            "achieved_gunits_s": round(count / (kern_ms * 1e-3) / 1e9, 2),
+            "ceiling_gunits_s": round(im["units_per_s"] / 1e9, 2),
+            "frac": round(count / (kern_ms * 1e-3) / im["units_per_s"], 4), "peak_source": "measured",
+            "probe": im}
     if not is2d and obj.info.levels > 0:
         # tiered table: each level reads one 32-B sector from L2 (packed
         # tables: one level of nodes); random sector gathers, not HBM, bound it.  Ceiling

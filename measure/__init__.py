@@ -9,6 +9,8 @@ stream they are launched on.
   stream_ceiling_2d(...)     best GB/s of the 2-D mix (16 B in, 16 B out per pair)
   l2_gather_ceiling(bytes)   random 32-B sector gathers from an L2-resident
                              buffer with the tiered kernel's load instruction
+  interp_mix_ceiling(...)    the shared-memory grid interpolation mix (2-D stream +
+                             record and corner reads from shared memory)
   stream_gather_ceiling(Y, out, bytes)
                              the packed-table mix: the 1-D stream plus one
                              random 32-B sector gather per unit (same buffers)
@@ -50,9 +52,10 @@ def lib():
         L.probe_gather.argtypes = [_P, _U64, _I, _I, _P, _P]
         L.probe_gather_line.argtypes = [_P, _U64, _I, _I, _P, _P]
         L.probe_stream_gather.argtypes = [_P, _P, _I64, _P, _U64, _I, _P]
+        L.probe_interp_mix.argtypes = [_P, _P, _P, _P, _P, _I64, _I, _I, _P]
         for f in (L.probe_stream, L.probe_stream2d, L.probe_fill, L.probe_gather, L.probe_gather_line,
                   L.probe_stream_variants, L.probe_sms, L.probe_stream_gather,
-                  L.probe_stream_gather_variants):
+                  L.probe_stream_gather_variants, L.probe_interp_mix):
             f.restype = _I
         _lib = L
     return _lib
@@ -186,3 +189,20 @@ def stream_gather_ceiling(Y, out, buffer_bytes: int, reps: int = 5) -> dict:
             "what": "read fp64 + one random 32-B sector gather (ld.global.nc.L1::no_allocate.v8.u32, "
                     "L2-resident buffer) + write int32 per unit, trivial kernel, best of "
                     f"{len(res)} launch shapes, {reps} launches each, same buffers as the bench"}
+
+
+def interp_mix_ceiling(rho, T, P, iR, iT, nR: int, nT: int, reps: int = 5) -> dict:
+    """Pairs/s of the shared-memory interpolation mix (measure/probes.cu k_interp_mix) on
+    the bench's own buffers with an nR x nT grid: the ceiling of interp2d_kernel's
+    L1TEX data-pipe traffic (its shared-memory reads plus the 2-D stream)."""
+    import torch
+    L = lib()
+    m = rho.numel() - rho.numel() % 2048
+    st = torch.cuda.current_stream()
+    ms = _time(lambda: _check(L.probe_interp_mix(rho.data_ptr(), T.data_ptr(), P.data_ptr(), iR.data_ptr(),
+                                                 iT.data_ptr(), m, nR, nT, st.cuda_stream),
+                              "probe_interp_mix"), reps, st)
+    return {"units_per_s": m / (ms * 1e-3), "grid": [nR, nT],
+            "what": "2-D stream + per pair 2 bank-pinned 16-B record reads and 4 random 8-B corner "
+                    "reads from an nR x nT fp64 grid in shared memory, no search and no "
+                    f"interpolation arithmetic; interp2d_kernel's launch shape; {reps} launches"}

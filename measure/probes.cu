@@ -14,6 +14,9 @@
 //                  tiered-table level walk.
 //  probe_stream_gather : the packed-table mix: the 1-D stream plus one random
 //                  32-B sector gather per unit from an L2-resident buffer.
+//  probe_interp_mix : the shared-memory grid interpolation mix: the 2-D stream
+//                  plus two bank-pinned record reads and four random corner reads
+//                  per pair from shared memory (interp2d_kernel's data-pipe traffic).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -443,6 +446,68 @@ __global__ void __launch_bounds__(T) k_stream_gather(const double2* __restrict__
   }
 }
 
+// The shared-memory grid interpolation mix with no search and no interpolation
+// arithmetic: the 2-D stream (rho, T in; P, two int32 out) plus,
+// per pair, one bank-pinned 16-B record read per axis (lane l reads copy l mod 8)
+// and the 4 corner reads G[i][j], G[i][j+1], G[i+1][j], G[i+1][j+1] (8 B each) of a
+// cell (i, j) hashed from the coordinates' bits, from a grid of nR x nT fp64 in
+// shared memory: 1 CTA x 1024 threads per SM, static tiles, the next tile's loads
+// after this tile's pairs and an L2 prefetch of the tile after next -- the launch
+// shape of interp2d_kernel.  Its rate is the ceiling of that kernel's data-pipe
+// traffic (shared wavefronts + the stream).
+__device__ __forceinline__ void pf_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__global__ void __launch_bounds__(1024, 1) k_interp_mix(const double2* __restrict__ rho,
+                                                       const double2* __restrict__ T,
+                                                       double2* __restrict__ P, int2* __restrict__ iR,
+                                                       int2* __restrict__ iT, int64_t pairs2,
+                                                       int nR, int nT) {
+  extern __shared__ __align__(16) double sm[];
+  double* G = sm;                                                       // nR nT
+  double2* recR = reinterpret_cast<double2*>(sm + (((int64_t)nR * nT + 1) & ~int64_t(1)));  // 8 nR
+  double2* recT = recR + 8 * nR;                                        // 8 nT
+  for (int q = threadIdx.x; q < nR * nT; q += blockDim.x) G[q] = 1.0 + q;
+  for (int q = threadIdx.x; q < 8 * (nR + nT); q += blockDim.x) recR[q] = make_double2(q, 1.0 / (q + 1));
+  __syncthreads();
+  const int c8 = threadIdx.x & 7;
+  const int64_t tiles = pairs2 / 1024;
+  auto one = [&](double x, double y, int32_t& i, int32_t& j) {
+    const uint32_t hx = (uint32_t)__double2loint(x) ^ (uint32_t)__double2hiint(x);
+    const uint32_t hy = (uint32_t)__double2loint(y) ^ (uint32_t)__double2hiint(y);
+    i = (int32_t)__umulhi(hx * 0x9E3779B1u, (uint32_t)(nR - 1));
+    j = (int32_t)__umulhi(hy * 0x85EBCA77u, (uint32_t)(nT - 1));
+    const double2 rr = recR[(i << 3) + c8], rt = recT[(j << 3) + c8];
+    const double* g = G + i * nT + j;
+    return ((g[0] + g[1]) * rr.y + (g[nT] + g[nT + 1]) * rt.y) + rr.x * rt.x;
+  };
+  int64_t t = blockIdx.x;
+  double2 vr = make_double2(0, 0), vt = vr;
+  if (t < tiles) {
+    vr = ldcs2(rho + t * 1024 + threadIdx.x);
+    vt = ldcs2(T + t * 1024 + threadIdx.x);
+  }
+  for (; t < tiles; t += gridDim.x) {
+    int2 a, b;
+    double2 p;
+    p.x = one(vr.x, vt.x, a.x, b.x);
+    p.y = one(vr.y, vt.y, a.y, b.y);
+    const int64_t tn = t + gridDim.x;
+    if (tn < tiles) {
+      vr = ldcs2(rho + tn * 1024 + threadIdx.x);
+      vt = ldcs2(T + tn * 1024 + threadIdx.x);
+    }
+    if (threadIdx.x == 0 && tn + gridDim.x < tiles) {
+      pf_l2(rho + (tn + gridDim.x) * 1024, 1024 * 16);
+      pf_l2(T + (tn + gridDim.x) * 1024, 1024 * 16);
+    }
+    const int64_t i = t * 1024 + threadIdx.x;
+    __stcs(P + i, p);
+    __stcs(iR + i, a);
+    __stcs(iT + i, b);
+  }
+}
+
 __global__ void k_fill(uint32_t* buf, uint64_t words) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride)
@@ -601,6 +666,20 @@ int probe_stream_gather(const double* y, int32_t* out, int64_t n, const uint32_t
     case 3: k_stream_gather<1024, 2><<<(unsigned)((pairs + 2047) / 2048), 1024, 0, st>>>(y2, o2, pairs, buf, mask); break;
     default: return (int)cudaErrorInvalidValue;
   }
+  return (int)cudaGetLastError();
+}
+
+// One launch of the shared-memory interpolation mix over m pairs (m a multiple of
+// 2048, aligned) with an nR x nT grid in shared memory (k_interp_mix).
+int probe_interp_mix(const double* rho, const double* T, double* P, int32_t* iR, int32_t* iT,
+                     int64_t m, int nR, int nT, void* stream) {
+  const size_t smem = (size_t)((((int64_t)nR * nT + 1) & ~int64_t(1)) * 8 + 16 * 8 * ((int64_t)nR + nT));
+  if (nR < 2 || nT < 2 || smem > 227 * 1024 || m % 2048) return (int)cudaErrorInvalidValue;
+  cudaFuncSetAttribute((const void*)k_interp_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_interp_mix<<<sms(), 1024, smem, (cudaStream_t)stream>>>(
+      reinterpret_cast<const double2*>(rho), reinterpret_cast<const double2*>(T),
+      reinterpret_cast<double2*>(P), reinterpret_cast<int2*>(iR), reinterpret_cast<int2*>(iT), m / 2,
+      nR, nT);
   return (int)cudaGetLastError();
 }
 
