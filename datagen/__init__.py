@@ -82,6 +82,9 @@ def host_lib():
         lib.gen_sample_copies.argtypes = [_U64, _P, _I64, _D, _D, _P, _I64, _U64, _P]
         lib.gen_fill_walk.argtypes = [_U64, _I64, _I64, _D, _D, _D, _D, _P]
         lib.gen_sample_walk.argtypes = [_U64, _P, _I64, _D, _D, _D, _D, _P]
+        lib.gen_walk_sum.argtypes = [_U64, _I64, _I64]
+        lib.gen_walk_sum.restype = _U64
+        lib.gen_fill_walk_from.argtypes = [_U64, _I64, _I64, _U64, _D, _D, _D, _D, _P]
         _host = lib
     return _host
 
@@ -222,6 +225,46 @@ class TargetSpec:
         else:
             raise ValueError(self.kind)
         return out
+
+    def host_fill_parallel(self, offset: int, count: int, table: np.ndarray | None = None,
+                           threads: int | None = None, walk_base: int | None = None,
+                           out: np.ndarray | None = None):
+        """host_fill over host threads (the ctypes calls release the GIL); the same bits
+        as host_fill.  Returns (out, walk_end) where walk_end is the walk's step sum
+        through offset+count-1 (pass it as walk_base of the next chunk to stream a walk
+        in order without re-summing its prefix; None for the other kinds)."""
+        from concurrent.futures import ThreadPoolExecutor
+        threads = threads or len(os.sched_getaffinity(0))
+        out = np.empty(count, dtype=np.float64) if out is None else out
+        assert out.dtype == np.float64 and out.flags.c_contiguous and out.size >= count
+        step = max(1, (count + threads - 1) // threads)
+        parts = [(s, min(count, s + step)) for s in range(0, count, step)]
+        L = host_lib()
+        with ThreadPoolExecutor(max(1, len(parts))) as ex:
+            if self.kind != "walk":
+                def job(p):
+                    s, e = p
+                    out[s:e] = self.host_fill(offset + s, e - s, table)
+                list(ex.map(job, parts))
+                return out, None
+            M = (1 << 64) - 1
+            if walk_base is None:   # sum of the steps before offset, split over threads
+                st = max(1, (offset + threads - 1) // threads)
+                walk_base = sum(ex.map(lambda b: L.gen_walk_sum(self.seed, b, min(offset, b + st)),
+                                       range(0, offset, st))) & M
+            sums = list(ex.map(lambda p: L.gen_walk_sum(self.seed, offset + p[0], offset + p[1]),
+                               parts))
+            bases, acc = [], walk_base
+            for v in sums:
+                bases.append(acc)
+                acc = (acc + v) & M
+
+            def wjob(ip):
+                (s, e), b = ip
+                L.gen_fill_walk_from(self.seed, offset + s, e - s, b, self.x0, self.c, self.lo,
+                                     self.hi, out[s:].ctypes.data)
+            list(ex.map(wjob, zip(parts, bases)))
+            return out, acc
 
     def host_sample(self, idx: np.ndarray, table: np.ndarray | None = None) -> np.ndarray:
         """Targets at the given global indices (walk: idx must be sorted)."""

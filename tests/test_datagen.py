@@ -40,6 +40,23 @@ def test_walk_fill_sample_and_offset():
     assert abs(np.median(step) / 0.6745 - 0.01) < 0.001
 
 
+def test_parallel_fill_same_bits_as_serial():
+    """host_fill_parallel (threads; walk chunks chained by their step sums) reproduces the
+    serial generator bit for bit, at any thread count and chunk boundary."""
+    for name in ("cfg1", "cfg3", "cfg5"):
+        w = datagen.workload(name, count=120_007)
+        full = w.targets.host_fill(0, w.count, w.table).view(np.uint64)
+        for threads in (1, 3, 8):
+            got, _ = w.targets.host_fill_parallel(5, w.count - 5, w.table, threads=threads)
+            assert np.array_equal(got.view(np.uint64), full[5:])
+        a, base = w.targets.host_fill_parallel(0, 50_001, w.table, threads=4)
+        b, _ = w.targets.host_fill_parallel(50_001, w.count - 50_001, w.table, threads=5,
+                                            walk_base=base)
+        assert np.array_equal(np.concatenate([a, b]).view(np.uint64), full)
+        if name == "cfg3":   # the chained base is the walk's step sum through the chunk
+            assert base == datagen.host_lib().gen_walk_sum(w.targets.seed, 0, 50_001)
+
+
 def test_cfg1_recipe_out_of_range_and_copies():
     """BASELINE.json configs[0]: '~5% out of range' plus '1% exact copies'."""
     w = datagen.workload("cfg1")

@@ -33,17 +33,19 @@ THREADS = len(os.sched_getaffinity(0))
 REL_TOL = 1e-12
 
 
-def _host_fill(spec, table, offset, count):
-    """Host targets [offset, offset + count) of a counter-based stream, over host threads."""
-    out = np.empty(count, dtype=np.float64)
-    step = (count + THREADS - 1) // THREADS
+def _host_fill(spec, table, offset, count, walk_base=None):
+    """Host targets [offset, offset + count) over host threads (datagen's parallel host
+    fill: the same bits as the serial generator; for the walk, walk_base chains chunks)."""
+    return spec.host_fill_parallel(offset, count, table, threads=THREADS, walk_base=walk_base)
 
-    def job(s):
-        e = min(count, s + step)
-        out[s:e] = spec.host_fill(offset + s, e - s, table)
+
+def _counters(X, Y, idx, off):
+    """oracle.counters over host threads (sub-range sums add modulo 2^64)."""
+    step = (Y.size + THREADS - 1) // THREADS
     with ThreadPoolExecutor(THREADS) as ex:
-        list(ex.map(job, range(0, count, step)))
-    return out
+        parts = list(ex.map(lambda s: oracle.counters(X, Y[s:s + step], idx[s:s + step], off + s),
+                            range(0, Y.size, step)))
+    return np.sum(parts, axis=0, dtype=np.uint64)
 
 
 def _check_chunk_targets(dev_vals, host_vals, rng):
@@ -71,12 +73,20 @@ def test_cfg5_every_lookup_bit_exact():
     t.search(Yd, out=out)
     torch.cuda.synchronize()
     rng = np.random.default_rng(5)
+    cref = np.zeros(8, dtype=np.uint64)
     for off in range(0, w.count, CHUNK):
         n = min(CHUNK, w.count - off)
-        Y = _host_fill(w.targets, w.table, off, n)
+        Y, _ = _host_fill(w.targets, w.table, off, n)
         _check_chunk_targets(Yd[off:off + n], Y, rng)
         ref = oracle.search(w.table, Y, threads=THREADS)
         _compare_indices(out[off:off + n].cpu().numpy(), ref, Y, f"cfg5 chunk at {off}")
+        # validation counters (a11) of the whole stream: chunk sums add modulo 2^64
+        cref += _counters(w.table, Y, ref, off)
+    c = torch.zeros(8, dtype=torch.int64, device=DEV)
+    t.search(Yd, out=out, counters=c)
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy().view(np.uint64), cref)
+    assert int(cref[0]) == w.count
     t.close()
 
 
@@ -89,11 +99,11 @@ def test_cfg3_every_lookup_bit_exact():
     t = eos.Table(w.table)
     t.search(Yd, out=out)
     torch.cuda.synchronize()
-    Yall = w.targets.host_fill(0, w.count)  # the walk is generated sequentially on the host
     rng = np.random.default_rng(3)
+    base = 0   # walk position before the chunk (the step sum through off - 1)
     for off in range(0, w.count, CHUNK):
         n = min(CHUNK, w.count - off)
-        Y = Yall[off:off + n]
+        Y, base = _host_fill(w.targets, None, off, n, walk_base=base)
         _check_chunk_targets(Yd[off:off + n], Y, rng)
         ref = oracle.search(w.table, Y, threads=THREADS)
         _compare_indices(out[off:off + n].cpu().numpy(), ref, Y, f"cfg3 chunk at {off}")
@@ -115,8 +125,8 @@ def test_cfg4_every_pair():
     worst = 0.0
     for off in range(0, w.count, CHUNK):
         n = min(CHUNK, w.count - off)
-        rho = _host_fill(w.rho_targets, None, off, n)
-        T = _host_fill(w.T_targets, None, off, n)
+        rho, _ = _host_fill(w.rho_targets, None, off, n)
+        T, _ = _host_fill(w.T_targets, None, off, n)
         _check_chunk_targets(rd[off:off + n], rho, rng)
         _check_chunk_targets(td[off:off + n], T, rng)
         Pr, iRr, iTr = oracle.interp2d(w.rho, w.T, w.P, rho, T, threads=THREADS)
@@ -137,8 +147,8 @@ def test_cfg4_exact_layout_every_pair_bit_identical():
     cfg4 plus the grid nodes, the points just inside / outside the range, and NaN."""
     w = datagen.workload("cfg4")
     m = 1 << 26
-    rho = _host_fill(w.rho_targets, None, 0, m)
-    T = _host_fill(w.T_targets, None, 0, m)
+    rho, _ = _host_fill(w.rho_targets, None, 0, m)
+    T, _ = _host_fill(w.T_targets, None, 0, m)
     nodes = np.repeat(w.rho, w.T.size)
     rho[:nodes.size] = nodes
     T[:nodes.size] = np.tile(w.T, w.rho.size)
