@@ -375,6 +375,16 @@ def run_ours(a, d: Dist):
             "ceiling_gunits_s": round(im["units_per_s"] / 1e9, 2),
             "frac": round(count / (kern_ms * 1e-3) / im["units_per_s"], 4), "peak_source": "measured",
             "probe": im}
+    elif is2d and not a.derivatives and not a.loglog:
+        # grid in device memory: one 32-B cell-quad gather per pair from
+        # L2 beside the 2-D stream; the same mix as a trivial kernel, measured now
+        im = measure.interp_gg_mix_ceiling(rho, T, P, iR, iT, len(w.rho), len(w.T))
+        res["roofline"]["l2"] = {
+            "bound": "l2 sector gathers + hbm stream (one cell quad per pair)",
+            "achieved_gunits_s": round(count / (kern_ms * 1e-3) / 1e9, 2),
+            "ceiling_gunits_s": round(im["units_per_s"] / 1e9, 2),
+            "frac": round(count / (kern_ms * 1e-3) / im["units_per_s"], 4), "peak_source": "measured",
+            "probe": im}
     if not is2d and obj.info.levels > 0:
         # tiered table: each level reads one 32-B sector from L2 (packed
         # tables: one level of nodes); random sector gathers, not HBM, bound it.  Ceiling

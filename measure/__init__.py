@@ -53,9 +53,10 @@ def lib():
         L.probe_gather_line.argtypes = [_P, _U64, _I, _I, _P, _P]
         L.probe_stream_gather.argtypes = [_P, _P, _I64, _P, _U64, _I, _P]
         L.probe_interp_mix.argtypes = [_P, _P, _P, _P, _P, _I64, _I, _I, _P]
+        L.probe_interp_gg_mix.argtypes = [_P, _P, _P, _P, _P, _I64, _P, _I, _I, _I, _P]
         for f in (L.probe_stream, L.probe_stream2d, L.probe_fill, L.probe_gather, L.probe_gather_line,
                   L.probe_stream_variants, L.probe_sms, L.probe_stream_gather,
-                  L.probe_stream_gather_variants, L.probe_interp_mix):
+                  L.probe_stream_gather_variants, L.probe_interp_mix, L.probe_interp_gg_mix):
             f.restype = _I
         _lib = L
     return _lib
@@ -206,3 +207,30 @@ def interp_mix_ceiling(rho, T, P, iR, iT, nR: int, nT: int, reps: int = 5) -> di
             "what": "2-D stream + per pair 2 bank-pinned 16-B record reads and 4 random 8-B corner "
                     "reads from an nR x nT fp64 grid in shared memory, no search and no "
                     f"interpolation arithmetic; interp2d_kernel's launch shape; {reps} launches"}
+
+
+def interp_gg_mix_ceiling(rho, T, P, iR, iT, nR: int, nT: int, reps: int = 5) -> dict:
+    """Pairs/s of the device-memory-grid interpolation mix (measure/probes.cu
+    k_interp_gg_mix) on the bench's own buffers: the 2-D stream plus one 32-B cell-quad
+    gather per pair from (nR-1) x (nT-1) quads in device memory (L2-resident) and the
+    bank-pinned record reads (as many copies, up to 8, as fit in shared memory): the
+    same-mix ceiling of interp2d_kernel with a grid in device memory."""
+    import torch
+    L = lib()
+    m = rho.numel() - rho.numel() % 2048
+    st = torch.cuda.current_stream()
+    quads = torch.ones(4 * (nR - 1) * (nT - 1), dtype=torch.float64, device=rho.device)
+    csh = 3
+    while csh > 0 and 16 * ((nR + nT) << csh) > 200 * 1024:
+        csh -= 1
+    ms = _time(lambda: _check(L.probe_interp_gg_mix(rho.data_ptr(), T.data_ptr(), P.data_ptr(),
+                                                    iR.data_ptr(), iT.data_ptr(), m, quads.data_ptr(),
+                                                    nR, nT, csh, st.cuda_stream),
+                              "probe_interp_gg_mix"), reps, st)
+    del quads
+    return {"units_per_s": m / (ms * 1e-3), "grid": [nR, nT], "record_copies": 1 << csh,
+            "quad_bytes": 32 * (nR - 1) * (nT - 1),
+            "what": "2-D stream + per pair one random 32-B cell-quad gather from device memory "
+                    "(L2-resident) and 2 bank-pinned 16-B record reads from shared memory, no "
+                    f"search and no interpolation arithmetic; interp2d_kernel's launch shape; "
+                    f"{reps} launches"}

@@ -508,6 +508,61 @@ __global__ void __launch_bounds__(1024, 1) k_interp_mix(const double2* __restric
   }
 }
 
+// The device-memory grid interpolation mix (big2d) with no search and
+// no interpolation arithmetic: the 2-D stream plus, per pair, one bank-pinned 16-B
+// record read per axis from shared memory (C copies, lane l reads copy l mod C) and one
+// 32-B cell quad (the 4 corners) gathered from nR x nT quads in device memory
+// (L2-resident) at a cell hashed from the coordinates' bits -- interp2d_kernel's GG
+// traffic, in its launch shape (1 CTA x 1024 threads per SM, static tiles, next tile's
+// loads after this tile's pairs).
+__global__ void __launch_bounds__(1024, 1) k_interp_gg_mix(const double2* __restrict__ rho,
+                                                          const double2* __restrict__ T,
+                                                          double2* __restrict__ P, int2* __restrict__ iR,
+                                                          int2* __restrict__ iT, int64_t pairs2,
+                                                          const double* __restrict__ quads, int nR,
+                                                          int nT, int csh) {
+  extern __shared__ __align__(16) double sm[];
+  double2* recR = reinterpret_cast<double2*>(sm);   // nR << csh
+  double2* recT = recR + ((int64_t)nR << csh);      // nT << csh
+  for (int q = threadIdx.x; q < ((nR + nT) << csh); q += blockDim.x) recR[q] = make_double2(q, 1.0 / (q + 1));
+  __syncthreads();
+  const int c = threadIdx.x & ((1 << csh) - 1);
+  const int64_t tiles = pairs2 / 1024;
+  auto one = [&](double x, double y, int32_t& i, int32_t& j) {
+    const uint32_t hx = (uint32_t)__double2loint(x) ^ (uint32_t)__double2hiint(x);
+    const uint32_t hy = (uint32_t)__double2loint(y) ^ (uint32_t)__double2hiint(y);
+    i = (int32_t)__umulhi(hx * 0x9E3779B1u, (uint32_t)(nR - 1));
+    j = (int32_t)__umulhi(hy * 0x85EBCA77u, (uint32_t)(nT - 1));
+    const double2 rr = recR[(i << csh) + c], rt = recT[(j << csh) + c];
+    double g0, g1, g2, g3;
+    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(g0), "=d"(g1), "=d"(g2), "=d"(g3)
+        : "l"(quads + 4 * ((int64_t)i * (nT - 1) + j)));
+    return ((g0 + g1) * rr.y + (g2 + g3) * rt.y) + rr.x * rt.x;
+  };
+  int64_t t = blockIdx.x;
+  double2 vr = make_double2(0, 0), vt = vr;
+  if (t < tiles) {
+    vr = ldcs2(rho + t * 1024 + threadIdx.x);
+    vt = ldcs2(T + t * 1024 + threadIdx.x);
+  }
+  for (; t < tiles; t += gridDim.x) {
+    int2 a, b;
+    double2 p;
+    p.x = one(vr.x, vt.x, a.x, b.x);
+    p.y = one(vr.y, vt.y, a.y, b.y);
+    const int64_t tn = t + gridDim.x;
+    if (tn < tiles) {
+      vr = ldcs2(rho + tn * 1024 + threadIdx.x);
+      vt = ldcs2(T + tn * 1024 + threadIdx.x);
+    }
+    const int64_t i = t * 1024 + threadIdx.x;
+    __stcs(P + i, p);
+    __stcs(iR + i, a);
+    __stcs(iT + i, b);
+  }
+}
+
 __global__ void k_fill(uint32_t* buf, uint64_t words) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride)
@@ -680,6 +735,22 @@ int probe_interp_mix(const double* rho, const double* T, double* P, int32_t* iR,
       reinterpret_cast<const double2*>(rho), reinterpret_cast<const double2*>(T),
       reinterpret_cast<double2*>(P), reinterpret_cast<int2*>(iR), reinterpret_cast<int2*>(iT), m / 2,
       nR, nT);
+  return (int)cudaGetLastError();
+}
+
+// One launch of the device-memory-grid interpolation mix over m pairs (m a multiple of
+// 2048, aligned): quads = (nR-1) x (nT-1) cells of 4 fp64 in device memory, 2^csh
+// record copies per axis node in shared memory (k_interp_gg_mix).
+int probe_interp_gg_mix(const double* rho, const double* T, double* P, int32_t* iR, int32_t* iT,
+                        int64_t m, const double* quads, int nR, int nT, int csh, void* stream) {
+  const size_t smem = (size_t)16 * (((int64_t)nR + nT) << csh);
+  if (nR < 2 || nT < 2 || csh < 0 || csh > 3 || smem > 227 * 1024 || m % 2048)
+    return (int)cudaErrorInvalidValue;
+  cudaFuncSetAttribute((const void*)k_interp_gg_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_interp_gg_mix<<<sms(), 1024, smem, (cudaStream_t)stream>>>(
+      reinterpret_cast<const double2*>(rho), reinterpret_cast<const double2*>(T),
+      reinterpret_cast<double2*>(P), reinterpret_cast<int2*>(iR), reinterpret_cast<int2*>(iT), m / 2,
+      quads, nR, nT, csh);
   return (int)cudaGetLastError();
 }
 
