@@ -106,8 +106,9 @@ def load_library():
     # EOS_LIBRARY=checked selects the bounds-checked debug build (tests only);
     # EOS_LIBRARY=exp an A/B tuning build (_build.py --exp -D...)
     which = os.environ.get("EOS_LIBRARY")
-    path = {"checked": _CHECKED_LIB_PATH,
-            "exp": os.path.join(os.path.dirname(_LIB_PATH), "libeossearch_exp.so")}.get(which, _LIB_PATH)
+    path = _CHECKED_LIB_PATH if which == "checked" else (
+        os.path.join(os.path.dirname(_LIB_PATH), f"libeossearch_{which}.so")  # exp, exp2, ...
+        if which and which.startswith("exp") and which.isalnum() else _LIB_PATH)
     if not os.path.exists(path):
         raise ImportError(f"{path} is missing: run __graft_entry__.build() "
                           "(python -m paper_2112_03229_b200._build); there is no CPU fallback")

@@ -105,7 +105,15 @@ using Shape2DDeep = dv::Shape<512, 1, 1, false>;
 struct InterpKernel {
   const void* fn;
   int threads;
+  int unroll = 1;
 };
+// log-log grids in shared memory (issue-bound): the default 2-D shape; the experiment
+// build takes -DEOS_EXP_LL_T=<threads> -DEOS_EXP_LL_U=<pairs of pairs per thread>
+#if defined(EOS_EXPERIMENTS) && defined(EOS_EXP_LL_T)
+using Shape2DLL = dv::Shape<EOS_EXP_LL_T, EOS_EXP_LL_U, 1, false>;
+#else
+using Shape2DLL = dv::Shape2D;
+#endif
 
 template <int S, bool LOGLOG, int REP, bool GG, int NK = 0>
 InterpKernel interp_fn(bool deriv) {
@@ -119,7 +127,10 @@ InterpKernel interp_fn(bool deriv) {
     return {(const void*)dv::interp2d_kernel<S, dv::Shape2DDeriv, true, LOGLOG, REP, GG>,
             dv::Shape2DDeriv::kThreads};
   }
-  if constexpr ((S == 1 || S == dv::kMapped) && !(LOGLOG && REP == 0))  // (plain log-log axes: 2 log1p per axis)
+  if constexpr (LOGLOG && !GG && REP == 2 && NK > 0)
+    return {(const void*)dv::interp2d_kernel<S, Shape2DLL, false, LOGLOG, REP, GG, NK>,
+            Shape2DLL::kThreads, Shape2DLL::kUnroll};
+  else if constexpr ((S == 1 || S == dv::kMapped) && !(LOGLOG && REP == 0))  // (plain log-log axes: 2 log1p per axis)
     return {(const void*)dv::interp2d_kernel<S, dv::Shape2D, false, LOGLOG, REP, GG, NK>,
             dv::Shape2D::kThreads};
   else
@@ -451,6 +462,7 @@ eos_status eos_grid2d_create_ex(const double* rho_host, int64_t n_rho, const dou
   const InterpKernel k1 = pick_interp(steps_max, loglog, g->rep, g->gg, true, g->narrow);
   g->fn = k0.fn;
   g->threads = k0.threads;
+  g->unroll = k0.unroll;
   g->fn_deriv = k1.fn;
   g->threads_deriv = k1.threads;
   st = configure(g->fn, g->threads, g->image_bytes, g->num_sms, &g->grid, nullptr);
