@@ -247,53 +247,6 @@ __device__ __forceinline__ int32_t lookup_b(double y, const double* __restrict__
   return (y >= a.x0) ? idx : 0;
 }
 
-#if defined(EOS_EXPERIMENTS) && defined(EOS_EXP_HIPROBE)
-// Experiment (-DEOS_EXP_HIPROBE): mode-0 lifting on the upper words of the
-// entries (LDS.32 probes: ~half the shared-memory wavefronts of LDS.64).  For keys
-// hi(X[j]) != hi(y) the words order as the doubles do; a probe with equal words is
-// accepted and sets `tie`, and the caller redoes the thread's batch with the fp64 steps.
-#define EOS_HI_STEP(S_, FIRST_, LAST_)                                              \
-  "setp.ge.s32 pi, %1, " #S_ ";\n\t"                                                \
-  "@pi ld.shared.u32 h, [%0+(8*" #S_ "-4)];\n\t"                                    \
-  "setp.le.and.u32 pt, h, %3, pi;\n\t" FIRST_ "@pt add.u32 %0, %0, 8*" #S_ ";\n\t" LAST_
-#define EOS_HI_TIE0 "setp.eq.u32 pe, h, %3;\n\t"
-#define EOS_HI_TIE "setp.eq.or.u32 pe, h, %3, pe;\n\t"
-#define EOS_HI_SUB(S_) "@pt sub.s32 %1, %1, " #S_ ";\n\t"
-template <int S>
-__device__ __forceinline__ void lift_fixed_hi(uint32_t ky, uint32_t& pa, int32_t& r, uint32_t& tie) {
-  static_assert(S >= 1 && S <= 3, "hi-word lifting: S = 1..3");
-  if (S == 3) {
-    asm("{\n\t.reg .pred pi, pt, pe;\n\t.reg .u32 h;\n\tmov.u32 h, 0xFFFFFFFF;\n\t"
-        EOS_HI_STEP(4, EOS_HI_TIE0, EOS_HI_SUB(4)) EOS_HI_STEP(2, EOS_HI_TIE, EOS_HI_SUB(2))
-        EOS_HI_STEP(1, EOS_HI_TIE, "") "@pe mov.u32 %2, 1;\n\t}"
-        : "+r"(pa), "+r"(r), "+r"(tie) : "r"(ky));
-  } else if (S == 2) {
-    asm("{\n\t.reg .pred pi, pt, pe;\n\t.reg .u32 h;\n\tmov.u32 h, 0xFFFFFFFF;\n\t"
-        EOS_HI_STEP(2, EOS_HI_TIE0, EOS_HI_SUB(2)) EOS_HI_STEP(1, EOS_HI_TIE, "")
-        "@pe mov.u32 %2, 1;\n\t}"
-        : "+r"(pa), "+r"(r), "+r"(tie) : "r"(ky));
-  } else {
-    asm("{\n\t.reg .pred pi, pt, pe;\n\t.reg .u32 h;\n\tmov.u32 h, 0xFFFFFFFF;\n\t"
-        EOS_HI_STEP(1, EOS_HI_TIE0, "") "@pe mov.u32 %2, 1;\n\t}"
-        : "+r"(pa), "+r"(r), "+r"(tie) : "r"(ky));
-  }
-}
-template <int SF, bool D16>
-__device__ __forceinline__ int32_t lookup_hi(double y, const double* __restrict__ sX,
-                                             const void* __restrict__ sD, const AxisParams& a,
-                                             uint32_t& tie) {
-  const uint32_t key = key_hi<0>(y);
-  const uint32_t b = bin_of_m0(key, a);
-  const uint32_t xa = smem_u32(sX);
-  uint32_t pa;
-  int32_t r;
-  dir_entry<D16>(sD, b, xa, pa, r);
-  lift_fixed_hi<SF>(key, pa, r, tie);
-  const int32_t idx = (int32_t)(pa - xa - 8u) >> 3;
-  return (y >= a.x0) ? idx : 0;
-}
-#endif
-
 // S fixed steps (S = 0: runtime), 32-bit directory (grid axes, tiered sample
 // tables, counters launches)
 template <int S, int MODE>
@@ -343,14 +296,6 @@ struct SmemLookup {
   AxisParams a;
   template <int N>
   __device__ __forceinline__ void many(const double (&y)[N], int32_t (&r)[N]) const {
-#if defined(EOS_EXPERIMENTS) && defined(EOS_EXP_HIPROBE)
-    if constexpr (MODE == 0 && !BIG && SF >= 1 && SF <= 3) {
-      uint32_t tie = 0;
-#pragma unroll
-      for (int i = 0; i < N; ++i) r[i] = lookup_hi<SF, D16>(y[i], sX, sD, a, tie);
-      if (tie == 0) return;  // (rare: a probe whose upper word equals the target's)
-    }
-#endif
 #pragma unroll
     for (int i = 0; i < N; ++i) r[i] = lookup_b<SF, BIG, MODE, D16>(y[i], sX, sD, a);
   }

@@ -12,8 +12,6 @@
 // and compile-time A/B flags of that build (-D...):
 //   EOS_EXP_NO_L2_PREFETCH                  2-D kernels without the L2 prefetch of the
 //                                           tile after next
-//   EOS_EXP_HIPROBE                         mode-0 shared-memory tables (S <= 3): lifting on the
-//                                           entries' upper words (LDS.32), fp64 redo on ties
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
